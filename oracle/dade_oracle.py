@@ -1,0 +1,429 @@
+"""CPU ORACLE for the DADE hot path — TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, float64 NumPy restatement of what arxiv 2404.16322
+computes on the path BASELINE.json's `north_star` names: PCA rotation,
+IVF build/probe, the §V data-driven linear correction calibrated per Δd step,
+and the epoch-frozen-τ progressive search. It shares no code with the CUDA
+library (paper_2404_16322_b200/) and neither imports the other. Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import it; the product path never does.
+
+Citations: `P:L<n>` = /root/reference/PAPER.md line n; `R<n>` = the reading
+numbered n in DESIGN.md §3 (copied from SURVEY.md §8(c)).
+
+Parity pins: every public function is pinned by a `-m "not gpu"` test in
+tests/test_oracle_*.py against a closed form, a hand-worked example, brute
+force on tiny inputs or a property the paper states (DESIGN.md §4 lists which).
+No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import math
+import numpy as np
+
+F64 = np.float64
+U64 = np.uint64
+MASK64 = (1 << 64) - 1
+
+
+# ----------------------------------------------------------------------------- helpers
+def strided_ids(n: int, m: int) -> np.ndarray:
+    """Portable sample ⌊k·n/m⌋, k = 0..m-1 (R17/R19: integer rule both sides can compute)."""
+    return (np.arange(m, dtype=np.int64) * n) // m
+
+
+def sqdist_seq(rows: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """dis(p, q) = ||p - q||^2, evaluated in float64 as the SEQUENTIAL sum over
+    j = 0..D-1 of (p_j - q_j)^2 (R20: the exact rule assignment/probe/brute force share).
+    `rows` n x D, `v` D; the difference of two fp32 numbers is formed in fp64."""
+    rows = np.asarray(rows)
+    v = np.asarray(v, dtype=F64)
+    acc = np.zeros(rows.shape[0], dtype=F64)
+    for j in range(rows.shape[1]):
+        t = rows[:, j].astype(F64) - v[j]
+        acc += t * t
+    return acc
+
+
+def order_by_dist_id(dist: np.ndarray, ids: np.ndarray) -> np.ndarray:
+    """Permutation sorting by (dist, id) ascending (R12 tie rule: lower id first)."""
+    return np.lexsort((ids, dist))
+
+
+# ----------------------------------------------------------------------------- O1 fit_rotation
+def fit_rotation(X: np.ndarray, sample_size: int = 0):
+    """PCA rotation (Theorem 1; proof P:L4067-4096: principal directions are the
+    eigenvectors of the covariance Σ, ordered by eigenvalue). Data are centred (P:L305
+    footnote). Sample: strided ids, n_s = min(N, 1,000,000) when sample_size == 0 (P:L3105,
+    R17). Σ = (X_s-μ)^T(X_s-μ)/n_s (divisor as P:L4074). Eigenvectors sorted by λ
+    descending; sign: largest-|component| positive, lowest index on ties (R18).
+    Returns (mean[D], R[D,D] rows = directions, lam[D])."""
+    X = np.asarray(X)
+    n = X.shape[0]
+    ns = min(n, 1_000_000) if sample_size <= 0 else min(n, sample_size)
+    Xs = X[strided_ids(n, ns)].astype(F64)
+    mean = Xs.mean(axis=0)
+    Y = Xs - mean
+    cov = (Y.T @ Y) / ns
+    lam, V = np.linalg.eigh(cov)
+    order = np.argsort(-lam, kind="stable")
+    lam, V = lam[order], V[:, order]
+    for i in range(V.shape[1]):
+        j = int(np.argmax(np.abs(V[:, i])))          # argmax returns the lowest index on ties
+        if V[j, i] < 0:
+            V[:, i] = -V[:, i]
+    return mean, np.ascontiguousarray(V.T), lam
+
+
+def rotate(X: np.ndarray, mean: np.ndarray, R: np.ndarray) -> np.ndarray:
+    """x̃ = R(x - μ) in float64 (x_D = R x, after centring P:L305)."""
+    return (np.asarray(X, dtype=F64) - mean) @ np.asarray(R, dtype=F64).T
+
+
+def err_variance(q_rot: np.ndarray, sigma2: np.ndarray, d: int) -> float:
+    """Eq. 3: Var(−2⟨q_r, x_r⟩) = 4·Σ_{i>d} (q_i σ_i)^2 over the residual dims
+    (0-based: dims d..D-1). Context for the PCA choice; used by the NEXT-1 BSA-res test."""
+    q = np.asarray(q_rot, F64)
+    return float(4.0 * np.sum(q[d:] ** 2 * np.asarray(sigma2, F64)[d:]))
+
+
+# ----------------------------------------------------------------------------- O3 IVF
+def assign(X: np.ndarray, centroids: np.ndarray) -> np.ndarray:
+    """IVF bucket of each point = its nearest centroid, raw space, exact
+    sequential fp64 sum (R20), ties to the lower centroid id (R12)."""
+    X = np.asarray(X)
+    best = np.full(X.shape[0], np.inf)
+    arg = np.zeros(X.shape[0], dtype=np.int64)
+    for c in range(centroids.shape[0]):
+        d = sqdist_seq(X, centroids[c])
+        upd = d < best                                  # strict: lower c wins ties
+        best[upd] = d[upd]
+        arg[upd] = c
+    return arg
+
+
+def kmeans(X: np.ndarray, nlist: int, iters: int = 10) -> np.ndarray:
+    """k-means clustering for the IVF buckets ("uses the k-means algorithm";
+    details are R19): strided sample of min(N, 64·C) rows, init = first C sampled rows,
+    `iters` Lloyd iterations with exact assignment, centroid = fp64 mean rounded to fp32,
+    empty cluster keeps its centroid. Returns float32 centroids."""
+    X = np.asarray(X, dtype=np.float32)
+    n = X.shape[0]
+    sample = X[strided_ids(n, min(n, 64 * nlist))]
+    cent = sample[:nlist].copy()
+    for _ in range(iters):
+        a = assign(sample, cent)
+        sums = np.zeros((nlist, X.shape[1]), dtype=F64)
+        np.add.at(sums, a, sample.astype(F64))
+        cnt = np.bincount(a, minlength=nlist)
+        nz = cnt > 0
+        cent[nz] = (sums[nz] / cnt[nz, None]).astype(np.float32)
+    return cent
+
+
+def build_ivf(X: np.ndarray, centroids: np.ndarray, id_base: int = 0):
+    """Buckets: every id in exactly one list; lists hold ids ascending.
+    Returns (assign[n], off[nlist+1], row_id[n]) with row_id = global ids, list-major."""
+    a = assign(X, centroids)
+    nlist = centroids.shape[0]
+    cnt = np.bincount(a, minlength=nlist)
+    off = np.zeros(nlist + 1, dtype=np.int64)
+    off[1:] = np.cumsum(cnt)
+    row_id = np.argsort(a, kind="stable").astype(np.int64) + id_base
+    return a, off, row_id
+
+
+def probe(q: np.ndarray, centroids: np.ndarray, nprobe: int) -> np.ndarray:
+    """The N^probe nearest centroids of q, raw space, exact fp64 sequential sums,
+    ordered by (dist, centroid id) (R12, R20)."""
+    d = sqdist_seq(centroids, q)
+    return order_by_dist_id(d, np.arange(len(d)))[:nprobe]
+
+
+# ----------------------------------------------------------------------------- O6 brute force
+def brute_force_knn(X: np.ndarray, Q: np.ndarray, K: int, id_base: int = 0):
+    """Exact KNN under squared L2, fp64 sequential sums, (dist, id) order
+    (R12). Returns ids (nq x K int64) and dists (nq x K float64)."""
+    Q = np.atleast_2d(Q)
+    ids = np.empty((Q.shape[0], K), dtype=np.int64)
+    dists = np.empty((Q.shape[0], K), dtype=F64)
+    gid = np.arange(X.shape[0], dtype=np.int64) + id_base
+    for i, q in enumerate(Q):
+        d = sqdist_seq(X, q)
+        o = order_by_dist_id(d, gid)[:K]
+        ids[i], dists[i] = gid[o], d[o]
+    return ids, dists
+
+
+# ----------------------------------------------------------------------------- O4 calibrate
+def splitmix64(x) -> np.ndarray:
+    """SplitMix64 output for state `x` (one step: x += golden gamma, then the finaliser).
+    Counter-based: both the oracle and the library evaluate it on (seed ⊕ (q<<32 | id))."""
+    z = (np.asarray(x, dtype=U64) + U64(0x9E3779B97F4A7C15))
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> U64(30))) * U64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> U64(27))) * U64(0x94D049BB133111EB)
+    return z ^ (z >> U64(31))
+
+
+def neg_hash(seed: int, qi: int, ids: np.ndarray) -> np.ndarray:
+    key = (U64(qi) << U64(32)) | np.asarray(ids, dtype=U64)
+    return splitmix64(U64(seed) ^ key)
+
+
+def logistic_irls(P: np.ndarray, tau: np.ndarray, y: np.ndarray, ridge: float = 1e-8,
+                  max_iter: int = 100, tol: float = 1e-12):
+    """Logistic regression with cross-entropy loss on features (dis', τ)
+    (P:L529), label y = 1 ⇔ dis > τ. R3: the BCE minimiser, computed by damped
+    Newton/IRLS on standardised features, ridge on the non-intercept weights.
+    Returns (m1, beta, ok): the model in the form sign(m1·dis' + β > τ)."""
+    P = np.asarray(P, F64); tau = np.asarray(tau, F64); y = np.asarray(y, F64)
+    mP, sP = P.mean(), P.std()
+    mt, st = tau.mean(), tau.std()
+    sP = sP if sP > 0 else 1.0
+    st = st if st > 0 else 1.0
+    A = np.stack([np.ones_like(P), (P - mP) / sP, (tau - mt) / st], axis=1)
+    reg = np.array([0.0, ridge, ridge])
+
+    def loss(w):
+        z = A @ w
+        return float(np.sum(np.logaddexp(0.0, z) - y * z) + 0.5 * np.sum(reg * w * w))
+
+    w = np.zeros(3)
+    cur = loss(w)
+    for _ in range(max_iter):
+        z = A @ w
+        p = 0.5 * (1.0 + np.tanh(0.5 * z))           # logistic σ(z), overflow-free
+        g = A.T @ (y - p) - reg * w
+        H = (A * (p * (1 - p))[:, None]).T @ A + np.diag(reg)
+        step = np.linalg.solve(H, g)
+        t = 1.0
+        for _h in range(30):                            # damping: halve until the loss does not grow
+            nw = w + t * step
+            nl = loss(nw)
+            if nl <= cur:
+                break
+            t *= 0.5
+        w, cur = nw, nl
+        if np.max(np.abs(t * step)) < tol:
+            break
+    wP, wt = w[1] / sP, w[2] / st
+    b = w[0] - w[1] * mP / sP - w[2] * mt / st
+    # w_P·P + w_τ·τ + b > 0  ⇔  (−w_P/w_τ)·P + (−b/w_τ) > τ  when w_τ < 0
+    if not (wt < 0) or not np.isfinite(wP) or not np.isfinite(wt):
+        return 1.0, 0.0, False
+    m1 = -wP / wt
+    if not (m1 > 0) or not np.isfinite(m1):
+        return 1.0, 0.0, False
+    return float(m1), float(-b / wt), True
+
+
+def calibration_pairs(X, index, Qc, K, n_neg, nprobe_neg, seed):
+    """Training samples (R14-R16): per calibration query the exact K NN over
+    the whole base are Label 0 and τ_q is the K-th NN distance; Label 1 =
+    the n_neg non-KNN candidates of q's nprobe_neg probed lists (whole base if 0 or flat)
+    with the smallest SplitMix64(seed ⊕ (q<<32 | id)).
+    Returns (qi[], id[], label[], tau_of_pair[])."""
+    off, row_id, cent = index["off"], index["row_id"], index["centroids"]
+    nlist = len(off) - 1
+    knn_ids, knn_d = brute_force_knn(X, Qc, K)
+    qi_l, id_l, lab_l, tau_l = [], [], [], []
+    for qi in range(Qc.shape[0]):
+        tau = knn_d[qi, K - 1]
+        if nprobe_neg <= 0 or nlist == 1:
+            cand = np.arange(X.shape[0], dtype=np.int64)
+        else:
+            pr = probe(Qc[qi], cent, nprobe_neg)
+            cand = np.concatenate([row_id[off[l]:off[l + 1]] for l in pr])
+        cand = np.setdiff1d(cand, knn_ids[qi])
+        h = neg_hash(seed, qi, cand)
+        negs = cand[np.lexsort((cand, h))[:n_neg]]
+        for i in knn_ids[qi]:
+            qi_l.append(qi); id_l.append(i); lab_l.append(0); tau_l.append(tau)
+        for i in negs:
+            qi_l.append(qi); id_l.append(i); lab_l.append(1); tau_l.append(tau)
+    return (np.array(qi_l), np.array(id_l, dtype=np.int64), np.array(lab_l), np.array(tau_l))
+
+
+def calibrate(X, index, Qc, K, n_neg=50, nprobe_neg=0, seed=0, block=16):
+    """§V-A data-driven correction in its incremental form: one
+    linear classifier per projected dimension d ∈ {16, 32, …, D-16}. For each d: the slope
+    m1_d from the logistic fit on (P_d, τ) (R3), then the sorted array
+    v_d = sort_desc(τ − m1_d·P_d) over Label-0 pairs, from which search derives β'_d (R4).
+    P_d = Σ_{i<d}(x̃_i − q̃_i)^2 is BSA-p's plain PCA projected distance (R2).
+    Returns dict(m1[ns], v[ns, n0], ok[ns], n0, K)."""
+    D = X.shape[1]
+    qi, ids, lab, tau = calibration_pairs(X, index, Qc, K, n_neg, nprobe_neg, seed)
+    Xr = rotate(X[ids], index["mean"], index["R"])
+    Qr = rotate(Qc, index["mean"], index["R"])[qi]
+    Pcum = np.cumsum((Xr - Qr) ** 2, axis=1)            # sequential prefix sums over dims
+    ns = D // block - 1
+    n0 = int(np.sum(lab == 0))
+    m1 = np.ones(ns); ok = np.zeros(ns, dtype=bool); v = np.empty((ns, n0))
+    for s in range(ns):
+        d = (s + 1) * block
+        P = Pcum[:, d - 1]
+        m1[s], _, ok[s] = logistic_irls(P, tau, lab)
+        v[s] = np.sort(tau[lab == 0] - m1[s] * P[lab == 0])[::-1]
+    return {"m1": m1, "v": v, "ok": ok, "n0": n0, "K": K, "block": block}
+
+
+def step_recall(r: float, D: int, delta_d: int) -> float:
+    """Per-classifier target recall r_i = 1 − (1 − r)/(D/Δd) (R5)."""
+    return 1.0 - (1.0 - r) / (D / delta_d)
+
+
+def beta_from_v(v_d: np.ndarray, alpha_s: float) -> float:
+    """β'_d: the LARGEST intercept whose Label-0 recall on the calibration set is ≥ 1−α_s
+    (R4). With v = sort_desc(τ − m1·P), recall(β') = #{v ≥ β'}/n0, so the answer
+    is v[k−1], k = clamp(⌈(1−α_s)·n0⌉, 1, n0)."""
+    n0 = len(v_d)
+    k = min(max(int(math.ceil((1.0 - alpha_s) * n0)), 1), n0)
+    return float(v_d[k - 1])
+
+
+def step_table(cal: dict, D: int, delta_d: int, alpha: float):
+    """Per-step (m1, β') used by search at d = Δd, 2Δd, …, D−Δd. α_s = (α·Δd)/D (R5);
+    α = 0 disables pruning (β' = −∞, R26)."""
+    block = cal["block"]
+    ns = D // delta_d
+    alpha_s = (alpha * delta_d) / D
+    m = np.empty(ns - 1); b = np.empty(ns - 1)
+    for s in range(1, ns):
+        idx = (s * delta_d) // block - 1
+        m[s - 1] = cal["m1"][idx]
+        b[s - 1] = -np.inf if alpha == 0 else beta_from_v(cal["v"][idx], alpha_s)
+    return m, b
+
+
+# ----------------------------------------------------------------------------- O5 search
+def epoch_bounds(total: int, K: int, c0: int | None = None):
+    """R13 epoch schedule: positions 0, c0, 2c0, 4c0, … (c0 = 4K); τ frozen per epoch."""
+    c0 = 4 * K if c0 is None else c0
+    b = [0]
+    nxt = c0
+    while b[-1] < total:
+        b.append(min(nxt, total))
+        nxt *= 2
+    return b
+
+
+def build_index(X, centroids, mean=None, R=None, cal=None, id_base=0):
+    """Bundle the artefacts search needs (fp64 rotated base, lists, rotation, calibration)."""
+    a, off, row_id = build_ivf(X, centroids, id_base)
+    return {"centroids": np.asarray(centroids, np.float32), "assign": a, "off": off,
+            "row_id": row_id, "mean": mean, "R": R, "cal": cal, "id_base": id_base,
+            "Xr": None if mean is None else rotate(X, mean, R)}
+
+
+def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False):
+    """IVF search with the per-step data-driven correction (O5).
+    Refinement: result queue of size K, τ = its K-th distance (R11: +∞ until full).
+    Candidates = the probed lists in probe order. For each candidate, the partial
+    squared distance P_d over the first d rotated dims is accumulated in Δd steps
+    (Alg. 2 loop, R9) and the cascade classifier for d prunes iff
+    m1_d·P_d + β'_d > τ. Survivors reach d = D, where P_D is the exact distance
+    (R10), and enter the queue. mode="epoch": τ frozen per epoch (R13, the parity
+    target); mode="sequential": τ refreshed after every survivor (P:L42-43 literal)."""
+    Q = np.atleast_2d(Q)
+    D = Q.shape[1]
+    ns = D // delta_d
+    m, b = step_table(index["cal"], D, delta_d, alpha) if alpha > 0 else (np.ones(ns - 1), np.full(ns - 1, -np.inf))
+    off, row_id, Xr = index["off"], index["row_id"], index["Xr"]
+    base = index["id_base"]                          # Xr rows are in id order: row = id - id_base
+    out_ids = np.full((Q.shape[0], K), -1, dtype=np.int64)
+    out_d = np.full((Q.shape[0], K), np.inf)
+    st = {"tested": 0, "dims_scanned": 0, "survivors": 0, "pruned_at_step": np.zeros(ns, np.int64),
+          "n_epochs": 0, "decisions": []}
+    Qr = rotate(Q, index["mean"], index["R"])
+    steps = np.arange(1, ns) * delta_d
+    for qn in range(Q.shape[0]):
+        pr = probe(Q[qn], index["centroids"], nprobe)
+        cand = np.concatenate([row_id[off[l]:off[l + 1]] for l in pr]) if len(pr) else np.zeros(0, np.int64)
+        top_d = np.zeros(0); top_i = np.zeros(0, dtype=np.int64)
+        st["tested"] += len(cand)
+        if mode == "epoch":
+            bounds = epoch_bounds(len(cand), K, c0)
+            st["n_epochs"] = max(st["n_epochs"], len(bounds) - 1)
+            for e in range(len(bounds) - 1):
+                tau = top_d[K - 1] if len(top_d) >= K else np.inf
+                ids = cand[bounds[e]:bounds[e + 1]]
+                P = np.cumsum((Xr[ids - base] - Qr[qn]) ** 2, axis=1)
+                keep = np.ones(len(ids), dtype=bool)
+                dims = np.full(len(ids), D)
+                if np.isfinite(tau) and ns > 1:
+                    test = m[None, :] * P[:, steps - 1] + b[None, :] > tau
+                    anyp = test.any(axis=1)
+                    first = np.argmax(test, axis=1)
+                    keep = ~anyp
+                    dims[anyp] = steps[first[anyp]]
+                    np.add.at(st["pruned_at_step"], first[anyp] + 1, 1)
+                    if log:
+                        for i in np.nonzero(anyp)[0]:
+                            s = first[i]
+                            st["decisions"].append((qn, int(ids[i]), int(steps[s]),
+                                                    float(m[s] * P[i, steps[s] - 1] + b[s]), float(tau)))
+                st["dims_scanned"] += int(dims.sum())
+                st["survivors"] += int(keep.sum())
+                cd = np.concatenate([top_d, P[keep, D - 1]])
+                ci = np.concatenate([top_i, ids[keep]])
+                o = order_by_dist_id(cd, ci)[:K]
+                top_d, top_i = cd[o], ci[o]
+        else:
+            for idn in cand:
+                tau = top_d[K - 1] if len(top_d) >= K else np.inf
+                P = np.cumsum((Xr[idn - base] - Qr[qn]) ** 2)
+                pruned_at = 0
+                if np.isfinite(tau):
+                    for si, d in enumerate(steps):
+                        if m[si] * P[d - 1] + b[si] > tau:
+                            pruned_at = d
+                            st["pruned_at_step"][si + 1] += 1
+                            break
+                st["dims_scanned"] += pruned_at if pruned_at else D
+                if pruned_at:
+                    continue
+                st["survivors"] += 1
+                cd = np.append(top_d, P[D - 1]); ci = np.append(top_i, idn)
+                o = order_by_dist_id(cd, ci)[:K]
+                top_d, top_i = cd[o], ci[o]
+        out_ids[qn, :len(top_i)] = top_i
+        out_d[qn, :len(top_d)] = top_d
+    return out_ids, out_d, st
+
+
+def exact_ivf(index, X, Q, K, nprobe):
+    """IVF without any DCO: exact raw-space distances of every candidate of the probed lists
+    (P:L174-175), (dist, id) order. Used to pin search(α=0)."""
+    Q = np.atleast_2d(Q)
+    off, row_id = index["off"], index["row_id"]
+    ids = np.full((Q.shape[0], K), -1, dtype=np.int64); ds = np.full((Q.shape[0], K), np.inf)
+    for qn, q in enumerate(Q):
+        pr = probe(q, index["centroids"], nprobe)
+        cand = np.concatenate([row_id[off[l]:off[l + 1]] for l in pr])
+        d = sqdist_seq(X[cand - index["id_base"]], q)
+        o = order_by_dist_id(d, cand)[:K]
+        ids[qn, :len(o)], ds[qn, :len(o)] = cand[o], d[o]
+    return ids, ds
+
+
+def merge_shards(parts, K):
+    """Combine per-shard top-K lists by (dist, id) (local top-K → all-gather →
+    merge). parts: list of (ids[nq,K], dists[nq,K])."""
+    nq = parts[0][0].shape[0]
+    ids = np.full((nq, K), -1, dtype=np.int64); ds = np.full((nq, K), np.inf)
+    for q in range(nq):
+        ci = np.concatenate([p[0][q] for p in parts]); cd = np.concatenate([p[1][q] for p in parts])
+        valid = ci >= 0
+        ci, cd = ci[valid], cd[valid]
+        o = order_by_dist_id(cd, ci)[:K]
+        ids[q, :len(o)], ds[q, :len(o)] = ci[o], cd[o]
+    return ids, ds
+
+
+def recall_at_k(found: np.ndarray, truth: np.ndarray, K: int) -> float:
+    """recall@K = |T ∩ G| / K averaged over queries."""
+    tot = 0
+    for f, g in zip(found, truth):
+        tot += len(set(f[:K].tolist()) & set(g[:K].tolist()))
+    return tot / (K * len(found))
