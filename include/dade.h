@@ -1,0 +1,180 @@
+/*
+ * dade.h — C ABI of the B200-native DADE hot path (arxiv 2404.16322, "Effective and General
+ * Distance Computation for Approximate Nearest Neighbor Search"; PAPER.md = /root/reference/PAPER.md).
+ *
+ * What the library computes (citations are PAPER.md lines, "R<n>" = DESIGN.md §3 readings):
+ *   - KNN under squared Euclidean distance dis(p,q) = ||p-q||^2
+ *   - IVF: k-means buckets, query probes the N^probe nearest centroids
+ *   - PCA rotation x~ = R(x - mu) (Theorem 1)
+ *   - refinement with result queue Q of size K, tau = its max
+ *   - BSA-p estimator dis'_d = partial PCA distance over the first d dims
+ *   - data-driven correction: prune iff m1_d * dis'_d + beta'_d > tau
+ *     one classifier per projected dimension d (cascade)
+ *     beta'_d calibrated to Label-0 recall r_i = 1 - (1-r)/(D/Delta_d)
+ *   - tau frozen within geometric epochs of the candidate stream (R13)
+ *
+ * Conventions for every entry point
+ *   - Return: dade_status; DADE_OK (0) on success. On error the index state is unchanged and
+ *     dade_last_error() returns a thread-local message. No C++ exception crosses the ABI.
+ *   - Pointers are plain: "device" = CUDA device memory of the index's device, "host" = host memory.
+ *     Arrays are dense, row-major, 0-based. Inputs are borrowed for the duration of the call;
+ *     the library copies everything it keeps. Outputs are caller-allocated.
+ *   - All device work is ordered on the stream given to dade_create. Build calls (fit/build/
+ *     calibrate) and calls returning host data synchronise before returning; dade_search is
+ *     asynchronous unless `stats` is non-NULL.
+ *   - One host thread per dade_index at a time.
+ *   - Global ids are int64 in the ABI and must be < 2^31 (kernels carry 32-bit ids).
+ *   - D must be a multiple of 16 (the layout block width B_L = 16 dims = 64 B rows); else
+ *     DADE_ERR_UNSUPPORTED.
+ */
+#ifndef DADE_H
+#define DADE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dade_index dade_index; /* opaque; owns the device memory of ONE GPU (one shard) */
+
+typedef enum {
+  DADE_OK = 0,
+  DADE_ERR_ARG = 1,        /* bad scalar argument (K, nprobe, delta_d, significance, NULL ptr) */
+  DADE_ERR_SHAPE = 2,      /* dimension mismatch */
+  DADE_ERR_STATE = 3,      /* call order violated (e.g. search before build, alpha>0 without calibration) */
+  DADE_ERR_NONFINITE = 4,  /* NaN/Inf in an input array */
+  DADE_ERR_OOM = 5,        /* device allocation failed */
+  DADE_ERR_CUDA = 6,       /* CUDA runtime error */
+  DADE_ERR_UNSUPPORTED = 8 /* valid but outside what the kernels implement (D%16, K>256, ...) */
+} dade_status;
+
+#define DADE_MAX_STEPS 64
+#define DADE_MAX_K 256
+
+/* Per-search counters (P:L3964-3974 pruning rate; Exp-6 "dimensions scanned"). */
+typedef struct {
+  int64_t tested;                         /* candidates entering the DCO (sum of probed list sizes) */
+  int64_t survivors;                      /* candidates that reached d = D (exact distance computed) */
+  int64_t dims_scanned;                   /* sum over tested candidates of dims read (d at prune, else D) */
+  int64_t pruned_at_step[DADE_MAX_STEPS]; /* [s] = pruned by the classifier at d = s*delta_d, s>=1 */
+  int32_t n_steps;                        /* D / delta_d */
+  int32_t n_epochs;                       /* epochs of the longest candidate stream */
+  float ms_rotate, ms_probe, ms_scan, ms_total; /* CUDA-event times of the stages */
+} dade_stats;
+
+/* Thread-local message describing the last failing call ("" if none). */
+const char* dade_last_error(void);
+
+/* Create an index for dimension D on CUDA `device`; `cuda_stream` is a cudaStream_t (NULL =
+ * the legacy default stream). Errors: ARG (D<=0), UNSUPPORTED (D%16 != 0 or D > 4096), CUDA. */
+dade_status dade_create(int device, void* cuda_stream, int D, dade_index** out);
+dade_status dade_destroy(dade_index* idx);
+
+/* ---------------------------------------------------------------- a0 fit_rotation
+ * PCA of the rows of X (device, n x D fp32): strided sample ids floor(k*n/ns), k < ns,
+ * ns = min(n, sample_size>0 ? sample_size : 1,000,000) (R17); mu = sample mean,
+ * Sigma = (Xs-mu)^T(Xs-mu)/ns (fp64 on the GPU), eigendecomposition in fp64 on the host;
+ * R rows = eigenvectors by descending eigenvalue, sign: largest-|component| positive (R18).
+ * Errors: ARG, NONFINITE, CUDA. */
+dade_status dade_fit_rotation(dade_index* idx, const float* X, int64_t n, int64_t sample_size);
+
+/* Multi-rank form of fit_rotation (each rank owns global ids [id_base, id_base+n) of a base of
+ * n_total rows; the caller all-reduces the fp64 partials between the calls):
+ *   1. dade_pca_mean_partial  -> sum[D] (host), count (host) of the sampled rows this rank owns
+ *   2. dade_pca_cov_partial   -> cov_sum[D*D] (host) = sum over owned sampled rows of (x-mean)(x-mean)^T
+ *   3. dade_set_rotation_from_cov(mean, cov_sum, count) -> eigendecomposition as above. */
+dade_status dade_pca_mean_partial(dade_index* idx, const float* X, int64_t n, int64_t id_base,
+                                  int64_t n_total, int64_t sample_size, double* sum, int64_t* count);
+dade_status dade_pca_cov_partial(dade_index* idx, const float* X, int64_t n, int64_t id_base,
+                                 int64_t n_total, int64_t sample_size, const double* mean,
+                                 double* cov_sum);
+dade_status dade_set_rotation_from_cov(dade_index* idx, const double* mean, const double* cov_sum,
+                                       int64_t count);
+
+/* Host copies of the rotation: mean[D], R[D*D] (row-major, rows = directions), eigvals[D]. */
+dade_status dade_get_rotation(const dade_index* idx, double* mean, double* R, double* eigvals);
+dade_status dade_set_rotation(dade_index* idx, const double* mean, const double* R,
+                              const double* eigvals);
+
+/* ---------------------------------------------------------------- a1+a2 build_ivf
+ * X: device n x D fp32 raw rows with global ids [id_base, id_base+n). Requires a rotation.
+ * centroids: device nlist x D fp32 raw-space centroids, or NULL -> k-means (R19: strided sample
+ * of min(n, 64*nlist) rows, init = first nlist sampled rows, `kmeans_iters` Lloyd iterations).
+ * assign(i) = argmin_c sum_j (x_ij - c_cj)^2 evaluated EXACTLY as an fp64 sequential sum, ties to
+ * the lower c (R20; fp32 tile filter + fp64 certification). Lists hold ids ascending. The rotated
+ * rows x~ = R(x - mu) (fp64 accumulation, stored fp32) are written dimension-blocked and
+ * list-major: block b (dims 16b..16b+15) is an n x 16 matrix whose row p is list-major position p.
+ * Errors: ARG (nlist<1 or nlist>n), STATE (no rotation), NONFINITE, OOM, CUDA. */
+dade_status dade_build_ivf(dade_index* idx, const float* X, int64_t n, int64_t id_base, int nlist,
+                           const float* centroids_or_null, int kmeans_iters);
+
+/* Host copies of the IVF: off[nlist+1] list offsets, row_id[n] global id of list-major position p,
+ * assign[n] (by local row i = id - id_base), centroids[nlist*D]. Any pointer may be NULL. */
+dade_status dade_get_ivf(const dade_index* idx, int64_t* off, int64_t* row_id, int32_t* assign,
+                         float* centroids);
+/* Sizes: *n rows, *nlist lists (either may be NULL). */
+dade_status dade_get_sizes(const dade_index* idx, int64_t* n, int* nlist);
+/* Host copy of the blocked layout as list-major rows: Xrot[n*D] (row p = x~ of row_id[p]). */
+dade_status dade_get_layout(const dade_index* idx, float* Xrot);
+
+/* ---------------------------------------------------------------- a3 calibrate
+ * X: device n x D, the raw rows given to dade_build_ivf (the index keeps only the rotated layout).
+ * Qc: device nq x D raw calibration queries. For each: exact K NN over this index's base
+ * (Label 0; tau_q = K-th NN distance, R14); Label 1 = the n_neg non-KNN candidates of
+ * its nprobe_neg probed lists (whole base if 0 or nlist==1) with the smallest
+ * SplitMix64(seed ^ (q<<32 | id)) (R16). For d = 16, 32, ..., D-16: m1_d from the logistic
+ * (BCE) fit on (P_d, tau) (R3) and v_d = sort_desc(tau - m1_d*P_d) over Label-0 pairs.
+ * Errors: ARG (K<1, K>n, K>DADE_MAX_K, n_neg<0), STATE (no IVF), NONFINITE, CUDA. */
+dade_status dade_calibrate(dade_index* idx, const float* X, const float* Qc, int nq, int K,
+                           int n_neg, int nprobe_neg, uint64_t seed);
+/* Host copy of the calibration table: m1[n_cls], v[n_cls*n0] (row s = d = 16(s+1)), n_cls = D/16-1.
+ * Pass NULL arrays to query K, n0, n_cls only. */
+dade_status dade_get_calibration(const dade_index* idx, int* K, int* n0, int* n_cls, double* m1,
+                                 double* v);
+dade_status dade_set_calibration(dade_index* idx, int K, int n0, int n_cls, const double* m1,
+                                 const double* v);
+
+/* ---------------------------------------------------------------- a4..a8 search
+ * Q: device nq x D raw queries; ids (int64) / dists (fp32 squared L2) device nq x K, ascending by
+ * (dist, id); missing slots -> id -1, dist +inf. delta_d: positive multiple of 16 dividing D.
+ * significance alpha in [0,1): alpha = 0 disables pruning (exact IVF); alpha > 0 uses
+ * beta'_d = v_d[k-1], k = clamp(ceil((1 - alpha*delta_d/D) * n0), 1, n0) (R4, R5).
+ * Per query: q~ = R(q-mu) (fp64 accumulation), exact probes (fp64-certified, ties to lower id),
+ * candidate stream = probed lists in probe order, epochs [0,4K),[4K,8K),[8K,16K),... with tau
+ * frozen per epoch, prune iff m1_d*P_d + beta'_d > tau, survivors' exact P_D enter the top-K.
+ * stats may be NULL (then the call is asynchronous on the stream).
+ * Errors: ARG, STATE (no IVF; alpha>0 without calibration; K != calibrated K), UNSUPPORTED
+ * (K > DADE_MAX_K, D/delta_d > DADE_MAX_STEPS), CUDA. */
+dade_status dade_search(dade_index* idx, const float* Q, int nq, int K, int nprobe, int delta_d,
+                        double significance, int64_t* ids, float* dists, dade_stats* stats);
+
+/* Same as dade_search with HOST Q/ids/dists: the H2D copy of Q and the D2H copy of the results
+ * are part of the call (synchronous). Used for the end-to-end (e2e) measurement. */
+dade_status dade_search_host(dade_index* idx, const float* Q_host, int nq, int K, int nprobe,
+                             int delta_d, double significance, int64_t* ids_host, float* dists_host,
+                             dade_stats* stats);
+
+/* Exact probes (a5 alone): probes[nq*nprobe] int32 device, ordered by (exact fp64 dist, id). */
+dade_status dade_probe(dade_index* idx, const float* Q, int nq, int nprobe, int32_t* probes);
+
+/* ---------------------------------------------------------------- tools
+ * Exact KNN (K12): X device n x D (global ids id_base+i), Q device nq x D -> ids/dists device
+ * nq x K ascending by (exact fp64 dist rounded to fp32, id). fp32 tile filter + fp64 re-rank. */
+dade_status dade_bruteforce_knn(dade_index* idx, const float* X, int64_t n, int64_t id_base,
+                                const float* Q, int nq, int K, int64_t* ids, float* dists);
+
+/* a9 shard merge: ids_in/dists_in device S x nq x K (rank-major, as an all-gather lays them
+ * out) -> ids_out/dists_out device nq x K, first K by (dist, id) over the S lists; id -1 slots
+ * are ignored. */
+dade_status dade_merge_topk(dade_index* idx, const int64_t* ids_in, const float* dists_in, int S,
+                            int nq, int K, int64_t* ids_out, float* dists_out);
+
+/* Persistence of {rotation, IVF, layout, calibration} (little-endian binary). */
+dade_status dade_save(const dade_index* idx, const char* path);
+dade_status dade_load(dade_index* idx, const char* path);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DADE_H */

@@ -1,0 +1,854 @@
+// C-ABI of the DADE library: index state, orchestration of the kernels, error mapping.
+// Every entry point follows include/dade.h; citations there.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "dade_internal.h"
+
+using namespace dade;
+
+struct dade_index {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int D = 0;
+  // rotation (a0)
+  bool has_rot = false;
+  std::vector<double> mean, R, lam;
+  DBuf<double> R_d, mean_d;
+  // IVF + layout (a1, a2)
+  bool has_ivf = false;
+  int nlist = 0;
+  int64_t n = 0, id_base = 0;
+  DBuf<float> cent, layout;
+  DBuf<int32_t> off_d, row_id_d;
+  std::vector<int64_t> off_h, row_id_h;
+  std::vector<int32_t> assign_h, pos_of_h;  // pos_of_h[local id] = list-major position
+  // calibration (a3)
+  bool has_cal = false;
+  int calK = 0, n0 = 0, ncls = 0;
+  std::vector<double> m1, v;
+  // scratch
+  DBuf<float> qrot, dmat, qbuf;
+  DBuf<int32_t> probes, cand, idx32;
+  DBuf<double> d64;
+  DBuf<int> flag;
+  DBuf<unsigned long long> counters;
+  DBuf<int64_t> ids_tmp;
+  DBuf<float> dists_tmp;
+  cudaEvent_t ev[5] = {};
+};
+
+// ------------------------------------------------------------------ error plumbing
+static thread_local std::string g_err;
+#define API_BEGIN try {
+#define API_END                                  \
+  g_err.clear();                                 \
+  return DADE_OK;                                \
+  }                                              \
+  catch (const Error& e) {                       \
+    g_err = e.what();                            \
+    return e.st;                                 \
+  }                                              \
+  catch (const std::bad_alloc&) {                \
+    g_err = "host allocation failed";            \
+    return DADE_ERR_OOM;                         \
+  }                                              \
+  catch (const std::exception& e) {              \
+    g_err = e.what();                            \
+    return DADE_ERR_CUDA;                        \
+  }
+
+extern "C" const char* dade_last_error(void) { return g_err.c_str(); }
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) DADE_CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void need(const void* p, const char* what) {
+  DADE_REQUIRE(p != nullptr, DADE_ERR_ARG, std::string("NULL pointer: ") + what);
+}
+
+void check_finite(dade_index* x, const float* X, int64_t count, const char* what) {
+  x->flag.reserve(1);
+  DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+  launch_check_finite(X, count, x->flag.p, x->stream);
+  int h = 0;
+  DADE_CK(cudaMemcpyAsync(&h, x->flag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  DADE_REQUIRE(h == 0, DADE_ERR_NONFINITE, std::string("non-finite value in ") + what);
+}
+
+// Exact k nearest rows of B for every row of A (fp32 tile filter + fp64-certified re-rank).
+// out_idx: device m x k int32 (column index into B); out_d64: device m x k fp64 or null.
+void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t n, int k,
+               int32_t* out_idx, double* out_d64) {
+  const int D = x->D;
+  DADE_REQUIRE(k >= 1 && k <= n, DADE_ERR_ARG, "exact_knn: k out of range");
+  DADE_REQUIRE(k <= 4096, DADE_ERR_UNSUPPORTED, "exact_knn: k > 4096");
+  const int64_t budget = (int64_t)1 << 29;  // floats of d_hat per chunk (2 GiB)
+  int64_t chunk = std::max<int64_t>(1, budget / std::max<int64_t>(n, 1));
+  chunk = std::min<int64_t>(chunk, m);
+  const int cand_cap = 4096;
+  if (k > 1 || out_d64) {
+    chunk = std::min<int64_t>(chunk, 16384);
+    x->cand.reserve((size_t)chunk * cand_cap);
+  }
+  x->dmat.reserve((size_t)chunk * n);
+  x->flag.reserve(1);
+  DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+  for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+    const int64_t mm = std::min(chunk, m - r0);
+    launch_l2_tile(A + r0 * D, mm, B, n, D, x->dmat.p, x->stream);
+    if (k == 1 && !out_d64)
+      launch_argmin_exact(x->dmat.p, mm, n, A + r0 * D, B, D, out_idx + r0, x->flag.p, x->stream);
+    else
+      launch_select_exact(x->dmat.p, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
+                          out_d64 ? out_d64 + r0 * k : nullptr, x->cand.p, cand_cap, x->flag.p,
+                          x->stream);
+  }
+  int h = 0;
+  DADE_CK(cudaMemcpyAsync(&h, x->flag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  DADE_REQUIRE(h == 0, DADE_ERR_UNSUPPORTED,
+               "exact_knn: more than 4096 near-tied candidates for one row (duplicate points?)");
+}
+
+void upload_rotation(dade_index* x) {
+  const int D = x->D;
+  x->R_d.reserve((size_t)D * D);
+  x->mean_d.reserve(D);
+  DADE_CK(cudaMemcpyAsync(x->R_d.p, x->R.data(), sizeof(double) * D * D, cudaMemcpyHostToDevice, x->stream));
+  DADE_CK(cudaMemcpyAsync(x->mean_d.p, x->mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  x->has_rot = true;
+}
+
+int64_t sample_count(int64_t n_total, int64_t sample_size) {
+  return std::min<int64_t>(n_total, sample_size > 0 ? sample_size : 1000000);
+}
+
+__global__ void k_ids_from_idx(const int32_t* idx, const double* d64, int64_t cnt, int64_t id_base,
+                               int64_t* ids, float* dists) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = idx[i];
+    ids[i] = c < 0 ? -1 : id_base + c;
+    dists[i] = c < 0 ? INFINITY : (float)d64[i];
+  }
+}
+
+void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d, double alpha,
+               int64_t* ids, float* dists, dade_stats* stats) {
+  const int D = x->D;
+  DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
+  need(Q, "Q"); need(ids, "ids"); need(dists, "dists");
+  DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
+  DADE_REQUIRE(K >= 1, DADE_ERR_ARG, "K < 1");
+  DADE_REQUIRE(K <= DADE_MAX_K, DADE_ERR_UNSUPPORTED, "K > DADE_MAX_K");
+  DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
+  DADE_REQUIRE(delta_d >= 16 && delta_d % 16 == 0 && D % delta_d == 0, DADE_ERR_ARG,
+               "delta_d must be a positive multiple of 16 dividing D");
+  DADE_REQUIRE(alpha >= 0.0 && alpha < 1.0, DADE_ERR_ARG, "significance not in [0,1)");
+  const int nsteps = D / delta_d;
+  DADE_REQUIRE(nsteps <= DADE_MAX_STEPS, DADE_ERR_UNSUPPORTED, "D/delta_d > DADE_MAX_STEPS");
+  const int dd = delta_d / 16;
+  DADE_REQUIRE(dd == 1 || dd == 2 || dd == 4, DADE_ERR_UNSUPPORTED, "delta_d must be 16, 32 or 64");
+  const bool prune = alpha > 0.0 && nsteps > 1;
+  if (prune) {
+    DADE_REQUIRE(x->has_cal, DADE_ERR_STATE, "significance > 0 requires calibration");
+    DADE_REQUIRE(x->calK == K, DADE_ERR_STATE, "K differs from the calibrated K");
+  }
+  if (nq == 0) return;
+  cudaStream_t st = x->stream;
+  if (stats) {
+    for (auto& e : x->ev)
+      if (!e) DADE_CK(cudaEventCreate(&e));
+    DADE_CK(cudaEventRecord(x->ev[0], st));
+  }
+  // a4 rotate queries (fp64 accumulation)
+  x->qrot.reserve((size_t)nq * D);
+  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
+  if (stats) DADE_CK(cudaEventRecord(x->ev[1], st));
+  // a5 exact probes
+  x->probes.reserve((size_t)nq * nprobe);
+  if (x->nlist == 1) {
+    DADE_CK(cudaMemsetAsync(x->probes.p, 0, sizeof(int32_t) * nq, st));
+  } else {
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr);
+  }
+  if (stats) DADE_CK(cudaEventRecord(x->ev[2], st));
+  // step table (R4, R5): alpha_s = alpha*delta_d/D, k = clamp(ceil((1-alpha_s)*n0), 1, n0)
+  ScanParams p{};
+  p.qrot = x->qrot.p; p.probes = x->probes.p; p.off = x->off_d.p; p.row_id = x->row_id_d.p;
+  p.layout = x->layout.p; p.n = x->n; p.D = D; p.nq = nq; p.nprobe = nprobe; p.K = K;
+  p.dd = dd; p.nsteps = nsteps; p.c0 = 4 * K; p.prune = prune ? 1 : 0;
+  for (int s = 1; s < nsteps; ++s) {
+    if (prune) {
+      const int idx = (s * delta_d) / 16 - 1;
+      const double alpha_s = (alpha * delta_d) / D;
+      long k = (long)std::ceil((1.0 - alpha_s) * (double)x->n0);
+      k = std::min<long>(std::max<long>(k, 1), x->n0);
+      p.m1[s - 1] = (float)x->m1[idx];
+      p.beta[s - 1] = (float)x->v[(size_t)idx * x->n0 + (k - 1)];
+    } else {
+      p.m1[s - 1] = 1.f;
+      p.beta[s - 1] = -INFINITY;
+    }
+  }
+  p.out_ids = ids; p.out_d = dists;
+  if (stats) {
+    x->counters.reserve(4 + DADE_MAX_STEPS);
+    DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS), st));
+    p.counters = x->counters.p;
+  }
+  launch_scan(p, st);
+  if (stats) {
+    DADE_CK(cudaEventRecord(x->ev[3], st));
+    unsigned long long c[4 + DADE_MAX_STEPS];
+    DADE_CK(cudaMemcpyAsync(c, x->counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    memset(stats, 0, sizeof(*stats));
+    stats->tested = (int64_t)c[0];
+    stats->survivors = (int64_t)c[1];
+    stats->dims_scanned = (int64_t)c[2];
+    stats->n_epochs = (int32_t)c[3];
+    for (int s = 0; s < DADE_MAX_STEPS; ++s) stats->pruned_at_step[s] = (int64_t)c[4 + s];
+    stats->n_steps = nsteps;
+    cudaEventElapsedTime(&stats->ms_rotate, x->ev[0], x->ev[1]);
+    cudaEventElapsedTime(&stats->ms_probe, x->ev[1], x->ev[2]);
+    cudaEventElapsedTime(&stats->ms_scan, x->ev[2], x->ev[3]);
+    cudaEventElapsedTime(&stats->ms_total, x->ev[0], x->ev[3]);
+  }
+}
+
+}  // namespace
+
+// ================================================================== lifecycle
+extern "C" dade_status dade_create(int device, void* cuda_stream, int D, dade_index** out) {
+  API_BEGIN
+  need(out, "out");
+  DADE_REQUIRE(D > 0, DADE_ERR_ARG, "D must be positive");
+  DADE_REQUIRE(D % 16 == 0 && D <= 4096, DADE_ERR_UNSUPPORTED, "D must be a multiple of 16, <= 4096");
+  int ndev = 0;
+  DADE_CK(cudaGetDeviceCount(&ndev));
+  DADE_REQUIRE(device >= 0 && device < ndev, DADE_ERR_ARG, "bad device ordinal");
+  DeviceGuard g(device);
+  auto* x = new dade_index();
+  x->device = device;
+  x->stream = (cudaStream_t)cuda_stream;
+  x->D = D;
+  *out = x;
+  API_END
+}
+
+extern "C" dade_status dade_destroy(dade_index* x) {
+  API_BEGIN
+  if (!x) { g_err.clear(); return DADE_OK; }
+  DeviceGuard g(x->device);
+  cudaStreamSynchronize(x->stream);
+  x->R_d.release(); x->mean_d.release(); x->cent.release(); x->layout.release();
+  x->off_d.release(); x->row_id_d.release(); x->qrot.release(); x->dmat.release();
+  x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
+  x->d64.release(); x->flag.release(); x->counters.release(); x->ids_tmp.release();
+  x->dists_tmp.release();
+  for (auto& e : x->ev)
+    if (e) cudaEventDestroy(e);
+  delete x;
+  API_END
+}
+
+// ================================================================== a0 rotation
+extern "C" dade_status dade_pca_mean_partial(dade_index* x, const float* X, int64_t n,
+                                             int64_t id_base, int64_t n_total, int64_t sample_size,
+                                             double* sum, int64_t* count) {
+  API_BEGIN
+  need(x, "index"); need(sum, "sum"); need(count, "count");
+  DADE_REQUIRE(n >= 0 && id_base >= 0 && id_base + n <= n_total && n_total > 0, DADE_ERR_ARG,
+               "bad row range");
+  if (n > 0) need(X, "X");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  if (n > 0) check_finite(x, X, n * D, "X");
+  DBuf<double> s;
+  s.reserve(D);
+  int64_t cnt = 0;
+  if (n > 0) {
+    launch_pca_sum(X, n, id_base, n_total, sample_count(n_total, sample_size), D, s.p, &cnt, x->stream);
+  } else {
+    DADE_CK(cudaMemsetAsync(s.p, 0, sizeof(double) * D, x->stream));
+  }
+  DADE_CK(cudaMemcpyAsync(sum, s.p, sizeof(double) * D, cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  s.release();
+  *count = cnt;
+  API_END
+}
+
+extern "C" dade_status dade_pca_cov_partial(dade_index* x, const float* X, int64_t n,
+                                            int64_t id_base, int64_t n_total, int64_t sample_size,
+                                            const double* mean, double* cov_sum) {
+  API_BEGIN
+  need(x, "index"); need(mean, "mean"); need(cov_sum, "cov_sum");
+  DADE_REQUIRE(n >= 0 && id_base >= 0 && id_base + n <= n_total && n_total > 0, DADE_ERR_ARG,
+               "bad row range");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  DBuf<double> mu, cov, scratch;
+  mu.reserve(D);
+  cov.reserve((size_t)D * D);
+  DADE_CK(cudaMemcpyAsync(mu.p, mean, sizeof(double) * D, cudaMemcpyHostToDevice, x->stream));
+  if (n > 0) {
+    need(X, "X");
+    const int64_t ns = sample_count(n_total, sample_size);
+    const int64_t sc = pca_cov_scratch_elems(std::min(ns, n) + 1, D);
+    scratch.reserve((size_t)sc);
+    launch_pca_cov(X, n, id_base, n_total, ns, D, mu.p, cov.p, scratch.p, sc, x->stream);
+  } else {
+    DADE_CK(cudaMemsetAsync(cov.p, 0, sizeof(double) * D * D, x->stream));
+  }
+  DADE_CK(cudaMemcpyAsync(cov_sum, cov.p, sizeof(double) * D * D, cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  API_END
+}
+
+extern "C" dade_status dade_set_rotation_from_cov(dade_index* x, const double* mean,
+                                                  const double* cov_sum, int64_t count) {
+  API_BEGIN
+  need(x, "index"); need(mean, "mean"); need(cov_sum, "cov_sum");
+  DADE_REQUIRE(count > 0, DADE_ERR_ARG, "count must be positive");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  std::vector<double> cov(cov_sum, cov_sum + (size_t)D * D), ev(D), V((size_t)D * D);
+  for (auto& c : cov) c /= (double)count;                       // divisor n_s
+  for (int a = 0; a < D; ++a)                                   // exact symmetry
+    for (int b = a + 1; b < D; ++b) cov[(size_t)b * D + a] = cov[(size_t)a * D + b];
+  sym_eig(D, cov.data(), ev.data(), V.data());                  // V column-major
+  std::vector<int> order(D);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ev[a] > ev[b]; });
+  std::vector<double> R((size_t)D * D), lam(D);
+  for (int i = 0; i < D; ++i) {
+    const double* col = &V[(size_t)order[i] * D];
+    int jm = 0;
+    for (int j = 1; j < D; ++j)
+      if (std::fabs(col[j]) > std::fabs(col[jm])) jm = j;      // lowest index on ties (R18)
+    const double sg = col[jm] < 0 ? -1.0 : 1.0;
+    for (int j = 0; j < D; ++j) R[(size_t)i * D + j] = sg * col[j];
+    lam[i] = ev[order[i]];
+  }
+  x->mean.assign(mean, mean + D);
+  x->R = std::move(R);
+  x->lam = std::move(lam);
+  upload_rotation(x);
+  API_END
+}
+
+extern "C" dade_status dade_fit_rotation(dade_index* x, const float* X, int64_t n,
+                                         int64_t sample_size) {
+  API_BEGIN
+  need(x, "index"); need(X, "X");
+  DADE_REQUIRE(n >= 1, DADE_ERR_ARG, "n must be >= 1");
+  const int D = x->D;
+  std::vector<double> sum(D), cov((size_t)D * D);
+  int64_t cnt = 0;
+  dade_status s = dade_pca_mean_partial(x, X, n, 0, n, sample_size, sum.data(), &cnt);
+  if (s != DADE_OK) throw Error(s, g_err);
+  std::vector<double> mean(D);
+  for (int j = 0; j < D; ++j) mean[j] = sum[j] / (double)cnt;
+  s = dade_pca_cov_partial(x, X, n, 0, n, sample_size, mean.data(), cov.data());
+  if (s != DADE_OK) throw Error(s, g_err);
+  s = dade_set_rotation_from_cov(x, mean.data(), cov.data(), cnt);
+  if (s != DADE_OK) throw Error(s, g_err);
+  API_END
+}
+
+extern "C" dade_status dade_get_rotation(const dade_index* x, double* mean, double* R, double* ev) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_rot, DADE_ERR_STATE, "no rotation");
+  const int D = x->D;
+  if (mean) memcpy(mean, x->mean.data(), sizeof(double) * D);
+  if (R) memcpy(R, x->R.data(), sizeof(double) * D * D);
+  if (ev) memcpy(ev, x->lam.data(), sizeof(double) * D);
+  API_END
+}
+
+extern "C" dade_status dade_set_rotation(dade_index* x, const double* mean, const double* R,
+                                         const double* ev) {
+  API_BEGIN
+  need(x, "index"); need(mean, "mean"); need(R, "R");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  for (int64_t i = 0; i < (int64_t)D * D; ++i)
+    DADE_REQUIRE(std::isfinite(R[i]), DADE_ERR_NONFINITE, "non-finite R");
+  x->mean.assign(mean, mean + D);
+  x->R.assign(R, R + (size_t)D * D);
+  if (ev) x->lam.assign(ev, ev + D); else x->lam.assign(D, 0.0);
+  upload_rotation(x);
+  API_END
+}
+
+// ================================================================== a1 + a2 IVF
+extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, int64_t id_base,
+                                      int nlist, const float* centroids, int kmeans_iters) {
+  API_BEGIN
+  need(x, "index"); need(X, "X");
+  DADE_REQUIRE(x->has_rot, DADE_ERR_STATE, "build_ivf needs a rotation (fit or set it first)");
+  DADE_REQUIRE(n >= 1 && id_base >= 0 && id_base + n < ((int64_t)1 << 31), DADE_ERR_ARG,
+               "bad row range (ids must be < 2^31)");
+  DADE_REQUIRE(nlist >= 1 && nlist <= n, DADE_ERR_ARG, "nlist not in [1, n]");
+  DADE_REQUIRE(kmeans_iters >= 0, DADE_ERR_ARG, "kmeans_iters < 0");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  check_finite(x, X, n * D, "X");
+  DBuf<float> cent;
+  cent.reserve((size_t)nlist * D);
+  if (centroids) {
+    check_finite(x, centroids, (int64_t)nlist * D, "centroids");
+    DADE_CK(cudaMemcpyAsync(cent.p, centroids, sizeof(float) * nlist * D, cudaMemcpyDeviceToDevice, st));
+  } else {
+    // k-means (R19): strided sample, init = first nlist sampled rows, exact assignment,
+    // centroid = fp64 mean (sample order) rounded to fp32, empty cluster keeps its centroid.
+    const int64_t nkm = std::min<int64_t>(n, (int64_t)64 * nlist);
+    std::vector<int32_t> sid(nkm);
+    for (int64_t k = 0; k < nkm; ++k) sid[k] = (int32_t)(((__int128)k * n) / nkm);
+    DBuf<int32_t> sid_d;
+    sid_d.reserve(nkm);
+    DBuf<float> S;
+    S.reserve((size_t)nkm * D);
+    DADE_CK(cudaMemcpyAsync(sid_d.p, sid.data(), sizeof(int32_t) * nkm, cudaMemcpyHostToDevice, st));
+    launch_gather_rows(X, sid_d.p, nkm, D, S.p, st);
+    std::vector<float> Sh((size_t)nkm * D);
+    DADE_CK(cudaMemcpyAsync(Sh.data(), S.p, sizeof(float) * nkm * D, cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaMemcpyAsync(cent.p, S.p, sizeof(float) * nlist * D, cudaMemcpyDeviceToDevice, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    std::vector<float> ch(Sh.begin(), Sh.begin() + (size_t)nlist * D);
+    DBuf<int32_t> a_d;
+    a_d.reserve(nkm);
+    std::vector<int32_t> a(nkm);
+    std::vector<double> sums((size_t)nlist * D);
+    std::vector<int64_t> cnt(nlist);
+    for (int it = 0; it < kmeans_iters; ++it) {
+      exact_knn(x, S.p, nkm, cent.p, nlist, 1, a_d.p, nullptr);
+      DADE_CK(cudaMemcpyAsync(a.data(), a_d.p, sizeof(int32_t) * nkm, cudaMemcpyDeviceToHost, st));
+      DADE_CK(cudaStreamSynchronize(st));
+      std::fill(sums.begin(), sums.end(), 0.0);
+      std::fill(cnt.begin(), cnt.end(), 0);
+      for (int64_t k = 0; k < nkm; ++k) {
+        double* sr = &sums[(size_t)a[k] * D];
+        const float* xr = &Sh[(size_t)k * D];
+        for (int j = 0; j < D; ++j) sr[j] += (double)xr[j];
+        ++cnt[a[k]];
+      }
+      for (int c = 0; c < nlist; ++c)
+        if (cnt[c] > 0)
+          for (int j = 0; j < D; ++j) ch[(size_t)c * D + j] = (float)(sums[(size_t)c * D + j] / (double)cnt[c]);
+      DADE_CK(cudaMemcpyAsync(cent.p, ch.data(), sizeof(float) * nlist * D, cudaMemcpyHostToDevice, st));
+    }
+    DADE_CK(cudaStreamSynchronize(st));
+    S.release(); sid_d.release(); a_d.release();
+  }
+  // exact assignment of every row (R20)
+  std::vector<int32_t> assign(n);
+  {
+    DBuf<int32_t> a_d;
+    a_d.reserve(n);
+    if (nlist == 1) DADE_CK(cudaMemsetAsync(a_d.p, 0, sizeof(int32_t) * n, st));
+    else exact_knn(x, X, n, cent.p, nlist, 1, a_d.p, nullptr);
+    DADE_CK(cudaMemcpyAsync(assign.data(), a_d.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+  }
+  // counting sort by (list, id): lists hold ids ascending
+  std::vector<int64_t> off(nlist + 1, 0);
+  for (int64_t i = 0; i < n; ++i) ++off[assign[i] + 1];
+  for (int c = 0; c < nlist; ++c) off[c + 1] += off[c];
+  std::vector<int64_t> fill(off.begin(), off.end() - 1), row_id(n);
+  std::vector<int32_t> pos_of(n), src(n), off32(nlist + 1), rid32(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t p = fill[assign[i]]++;
+    row_id[p] = id_base + i;
+    pos_of[i] = (int32_t)p;
+    src[p] = (int32_t)i;
+  }
+  for (int c = 0; c <= nlist; ++c) off32[c] = (int32_t)off[c];
+  for (int64_t p = 0; p < n; ++p) rid32[p] = (int32_t)row_id[p];
+  // rotated, dimension-blocked, list-major layout (a1)
+  DBuf<float> layout;
+  layout.reserve((size_t)n * D);
+  DBuf<int32_t> off_d, rid_d, src_d;
+  off_d.reserve(nlist + 1); rid_d.reserve(n); src_d.reserve(n);
+  DADE_CK(cudaMemcpyAsync(off_d.p, off32.data(), sizeof(int32_t) * (nlist + 1), cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(rid_d.p, rid32.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(src_d.p, src.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+  launch_rotate(X, src_d.p, n, D, x->R_d.p, x->mean_d.p, nullptr, layout.p, st);
+  DADE_CK(cudaStreamSynchronize(st));
+  src_d.release();
+  // commit (state unchanged on any earlier error)
+  std::swap(x->cent, cent); cent.release();
+  std::swap(x->layout, layout); layout.release();
+  std::swap(x->off_d, off_d); off_d.release();
+  std::swap(x->row_id_d, rid_d); rid_d.release();
+  x->off_h = std::move(off);
+  x->row_id_h = std::move(row_id);
+  x->assign_h = std::move(assign);
+  x->pos_of_h = std::move(pos_of);
+  x->nlist = nlist;
+  x->n = n;
+  x->id_base = id_base;
+  x->has_ivf = true;
+  x->has_cal = false;
+  API_END
+}
+
+extern "C" dade_status dade_get_ivf(const dade_index* x, int64_t* off, int64_t* row_id,
+                                    int32_t* assign, float* centroids) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "no IVF");
+  if (off) memcpy(off, x->off_h.data(), sizeof(int64_t) * (x->nlist + 1));
+  if (row_id) memcpy(row_id, x->row_id_h.data(), sizeof(int64_t) * x->n);
+  if (assign) memcpy(assign, x->assign_h.data(), sizeof(int32_t) * x->n);
+  if (centroids) {
+    DeviceGuard g(x->device);
+    DADE_CK(cudaMemcpyAsync(centroids, x->cent.p, sizeof(float) * x->nlist * x->D, cudaMemcpyDeviceToHost, x->stream));
+    DADE_CK(cudaStreamSynchronize(x->stream));
+  }
+  API_END
+}
+
+extern "C" dade_status dade_get_sizes(const dade_index* x, int64_t* n, int* nlist) {
+  API_BEGIN
+  need(x, "index");
+  if (n) *n = x->has_ivf ? x->n : 0;
+  if (nlist) *nlist = x->has_ivf ? x->nlist : 0;
+  API_END
+}
+
+extern "C" dade_status dade_get_layout(const dade_index* x, float* Xrot) {
+  API_BEGIN
+  need(x, "index"); need(Xrot, "Xrot");
+  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "no IVF");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  const int64_t n = x->n;
+  std::vector<float> blk((size_t)n * D);
+  DADE_CK(cudaMemcpyAsync(blk.data(), x->layout.p, sizeof(float) * n * D, cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  for (int b = 0; b < D / 16; ++b)
+    for (int64_t p = 0; p < n; ++p)
+      memcpy(Xrot + p * D + b * 16, &blk[((size_t)b * n + p) * 16], 64);
+  API_END
+}
+
+// ================================================================== a3 calibration
+extern "C" dade_status dade_calibrate(dade_index* x, const float* X, const float* Qc, int nq, int K,
+                                      int n_neg, int nprobe_neg, uint64_t seed) {
+  API_BEGIN
+  need(x, "index"); need(X, "X"); need(Qc, "Qc");
+  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "calibrate needs build_ivf first");
+  DADE_REQUIRE(nq >= 1, DADE_ERR_ARG, "nq < 1");
+  DADE_REQUIRE(K >= 1 && K <= x->n, DADE_ERR_ARG, "K not in [1, n]");
+  DADE_REQUIRE(K <= DADE_MAX_K, DADE_ERR_UNSUPPORTED, "K > DADE_MAX_K");
+  DADE_REQUIRE(n_neg >= 0, DADE_ERR_ARG, "n_neg < 0");
+  DADE_REQUIRE(nprobe_neg >= 0 && nprobe_neg <= x->nlist, DADE_ERR_ARG, "nprobe_neg not in [0, nlist]");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  const int64_t n = x->n;
+  cudaStream_t st = x->stream;
+  check_finite(x, Qc, (int64_t)nq * D, "Qc");
+  // exact KNN over the whole base (Label 0, tau_q) — P:L3930, R14
+  DBuf<int32_t> knn_i;
+  DBuf<double> knn_d;
+  knn_i.reserve((size_t)nq * K);
+  knn_d.reserve((size_t)nq * K);
+  exact_knn(x, Qc, nq, X, n, K, knn_i.p, knn_d.p);
+  std::vector<int32_t> ki((size_t)nq * K);
+  std::vector<double> kd((size_t)nq * K);
+  DADE_CK(cudaMemcpyAsync(ki.data(), knn_i.p, sizeof(int32_t) * ki.size(), cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaMemcpyAsync(kd.data(), knn_d.p, sizeof(double) * kd.size(), cudaMemcpyDeviceToHost, st));
+  // probes for the negatives (R16)
+  const bool whole = nprobe_neg == 0 || x->nlist == 1;
+  std::vector<int32_t> pr;
+  if (!whole) {
+    DBuf<int32_t> pd;
+    pd.reserve((size_t)nq * nprobe_neg);
+    exact_knn(x, Qc, nq, x->cent.p, x->nlist, nprobe_neg, pd.p, nullptr);
+    pr.resize((size_t)nq * nprobe_neg);
+    DADE_CK(cudaMemcpyAsync(pr.data(), pd.p, sizeof(int32_t) * pr.size(), cudaMemcpyDeviceToHost, st));
+  }
+  DADE_CK(cudaStreamSynchronize(st));
+  // pairs: Label 0 = the K NN, Label 1 = n_neg non-KNN candidates with the smallest hash
+  std::vector<int32_t> pq, prow;
+  std::vector<double> ptau, py;
+  std::vector<std::pair<uint64_t, int64_t>> cand;
+  for (int qi = 0; qi < nq; ++qi) {
+    const double tau = kd[(size_t)qi * K + K - 1];
+    std::vector<int64_t> knn_ids(K);
+    for (int j = 0; j < K; ++j) {
+      const int32_t loc = ki[(size_t)qi * K + j];
+      knn_ids[j] = x->id_base + loc;
+      pq.push_back(qi); prow.push_back(x->pos_of_h[loc]); ptau.push_back(tau); py.push_back(0.0);
+    }
+    std::sort(knn_ids.begin(), knn_ids.end());
+    cand.clear();
+    auto consider = [&](int64_t id) {
+      if (std::binary_search(knn_ids.begin(), knn_ids.end(), id)) return;
+      const uint64_t key = ((uint64_t)(uint32_t)qi << 32) | (uint64_t)id;
+      cand.emplace_back(splitmix64(seed ^ key), id);
+    };
+    if (whole) {
+      for (int64_t i = 0; i < n; ++i) consider(x->id_base + i);
+    } else {
+      for (int j = 0; j < nprobe_neg; ++j) {
+        const int l = pr[(size_t)qi * nprobe_neg + j];
+        for (int64_t p = x->off_h[l]; p < x->off_h[l + 1]; ++p) consider(x->row_id_h[p]);
+      }
+    }
+    const size_t take = std::min<size_t>((size_t)n_neg, cand.size());
+    std::partial_sort(cand.begin(), cand.begin() + take, cand.end());
+    for (size_t j = 0; j < take; ++j) {
+      pq.push_back(qi); prow.push_back(x->pos_of_h[cand[j].second - x->id_base]);
+      ptau.push_back(tau); py.push_back(1.0);
+    }
+  }
+  const int npairs = (int)pq.size();
+  const int nblk = D / 16;
+  // features P_d at every 16-dim prefix, from the rotated layout (fp64 accumulation)
+  DBuf<float> qr;
+  qr.reserve((size_t)nq * D);
+  launch_rotate(Qc, nullptr, nq, D, x->R_d.p, x->mean_d.p, qr.p, nullptr, st);
+  DBuf<int32_t> pq_d, pr_d;
+  DBuf<double> feat;
+  pq_d.reserve(npairs); pr_d.reserve(npairs); feat.reserve((size_t)npairs * nblk);
+  DADE_CK(cudaMemcpyAsync(pq_d.p, pq.data(), sizeof(int32_t) * npairs, cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(pr_d.p, prow.data(), sizeof(int32_t) * npairs, cudaMemcpyHostToDevice, st));
+  launch_pair_prefix(x->layout.p, n, D, qr.p, pq_d.p, pr_d.p, npairs, feat.p, st);
+  std::vector<double> F((size_t)npairs * nblk);
+  DADE_CK(cudaMemcpyAsync(F.data(), feat.p, sizeof(double) * F.size(), cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaStreamSynchronize(st));
+  // per-step logistic slope (R3) and sorted thresholds (R4)
+  const int ncls = nblk - 1;
+  int n0 = 0;
+  for (double y : py) n0 += y == 0.0;
+  std::vector<double> m1(ncls, 1.0), v((size_t)ncls * n0);
+  std::vector<double> P(npairs);
+  for (int s = 0; s < ncls; ++s) {
+    for (int i = 0; i < npairs; ++i) P[i] = F[(size_t)i * nblk + s];
+    double m, b;
+    logistic_irls(P, ptau, py, 1e-8, 100, 1e-12, &m, &b);
+    m1[s] = m;
+    std::vector<double> vv;
+    vv.reserve(n0);
+    for (int i = 0; i < npairs; ++i)
+      if (py[i] == 0.0) vv.push_back(ptau[i] - m * P[i]);
+    std::sort(vv.begin(), vv.end(), std::greater<double>());
+    std::copy(vv.begin(), vv.end(), v.begin() + (size_t)s * n0);
+  }
+  x->m1 = std::move(m1);
+  x->v = std::move(v);
+  x->calK = K;
+  x->n0 = n0;
+  x->ncls = ncls;
+  x->has_cal = true;
+  API_END
+}
+
+extern "C" dade_status dade_get_calibration(const dade_index* x, int* K, int* n0, int* ncls,
+                                            double* m1, double* v) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_cal, DADE_ERR_STATE, "no calibration");
+  if (K) *K = x->calK;
+  if (n0) *n0 = x->n0;
+  if (ncls) *ncls = x->ncls;
+  if (m1) memcpy(m1, x->m1.data(), sizeof(double) * x->ncls);
+  if (v) memcpy(v, x->v.data(), sizeof(double) * x->v.size());
+  API_END
+}
+
+extern "C" dade_status dade_set_calibration(dade_index* x, int K, int n0, int ncls,
+                                            const double* m1, const double* v) {
+  API_BEGIN
+  need(x, "index"); need(m1, "m1"); need(v, "v");
+  DADE_REQUIRE(K >= 1 && K <= DADE_MAX_K && n0 >= 1, DADE_ERR_ARG, "bad K / n0");
+  DADE_REQUIRE(ncls == x->D / 16 - 1, DADE_ERR_SHAPE, "n_cls must be D/16 - 1");
+  x->m1.assign(m1, m1 + ncls);
+  x->v.assign(v, v + (size_t)ncls * n0);
+  x->calK = K;
+  x->n0 = n0;
+  x->ncls = ncls;
+  x->has_cal = true;
+  API_END
+}
+
+// ================================================================== a4..a8 search
+extern "C" dade_status dade_search(dade_index* x, const float* Q, int nq, int K, int nprobe,
+                                   int delta_d, double significance, int64_t* ids, float* dists,
+                                   dade_stats* stats) {
+  API_BEGIN
+  need(x, "index");
+  DeviceGuard g(x->device);
+  do_search(x, Q, nq, K, nprobe, delta_d, significance, ids, dists, stats);
+  API_END
+}
+
+extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, int K, int nprobe,
+                                        int delta_d, double significance, int64_t* ids_h,
+                                        float* dists_h, dade_stats* stats) {
+  API_BEGIN
+  need(x, "index"); need(Qh, "Q"); need(ids_h, "ids"); need(dists_h, "dists");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  x->qbuf.reserve((size_t)std::max(nq, 1) * D);
+  x->ids_tmp.reserve((size_t)std::max(nq, 1) * K);
+  x->dists_tmp.reserve((size_t)std::max(nq, 1) * K);
+  DADE_CK(cudaMemcpyAsync(x->qbuf.p, Qh, sizeof(float) * nq * D, cudaMemcpyHostToDevice, st));
+  do_search(x, x->qbuf.p, nq, K, nprobe, delta_d, significance, x->ids_tmp.p, x->dists_tmp.p, stats);
+  DADE_CK(cudaMemcpyAsync(ids_h, x->ids_tmp.p, sizeof(int64_t) * nq * K, cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaMemcpyAsync(dists_h, x->dists_tmp.p, sizeof(float) * nq * K, cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaStreamSynchronize(st));
+  API_END
+}
+
+extern "C" dade_status dade_probe(dade_index* x, const float* Q, int nq, int nprobe, int32_t* probes) {
+  API_BEGIN
+  need(x, "index"); need(Q, "Q"); need(probes, "probes");
+  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "no IVF");
+  DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
+  DeviceGuard g(x->device);
+  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr);
+  API_END
+}
+
+// ================================================================== tools
+extern "C" dade_status dade_bruteforce_knn(dade_index* x, const float* X, int64_t n, int64_t id_base,
+                                           const float* Q, int nq, int K, int64_t* ids, float* dists) {
+  API_BEGIN
+  need(x, "index"); need(X, "X"); need(Q, "Q"); need(ids, "ids"); need(dists, "dists");
+  DADE_REQUIRE(K >= 1 && K <= n, DADE_ERR_ARG, "K not in [1, n]");
+  DADE_REQUIRE(n < ((int64_t)1 << 31), DADE_ERR_UNSUPPORTED, "n >= 2^31");
+  DeviceGuard g(x->device);
+  if (nq <= 0) { g_err.clear(); return DADE_OK; }
+  x->idx32.reserve((size_t)nq * K);
+  x->d64.reserve((size_t)nq * K);
+  exact_knn(x, Q, nq, X, n, K, x->idx32.p, x->d64.p);
+  k_ids_from_idx<<<256, 256, 0, x->stream>>>(x->idx32.p, x->d64.p, (int64_t)nq * K, id_base, ids, dists);
+  DADE_CK(cudaGetLastError());
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  API_END
+}
+
+extern "C" dade_status dade_merge_topk(dade_index* x, const int64_t* ids_in, const float* dists_in,
+                                       int S, int nq, int K, int64_t* ids_out, float* dists_out) {
+  API_BEGIN
+  need(x, "index"); need(ids_in, "ids_in"); need(dists_in, "dists_in");
+  need(ids_out, "ids_out"); need(dists_out, "dists_out");
+  DADE_REQUIRE(S >= 1 && K >= 1 && nq >= 0, DADE_ERR_ARG, "bad S / K / nq");
+  DeviceGuard g(x->device);
+  launch_merge_topk(ids_in, dists_in, S, nq, K, ids_out, dists_out, x->stream);
+  API_END
+}
+
+// ================================================================== persistence
+namespace {
+const uint64_t kMagic = 0x3130454441444144ull;  // "DADADE01"
+void wr(FILE* f, const void* p, size_t b) {
+  DADE_REQUIRE(fwrite(p, 1, b, f) == b, DADE_ERR_ARG, "write failed");
+}
+void rd(FILE* f, void* p, size_t b) {
+  DADE_REQUIRE(fread(p, 1, b, f) == b, DADE_ERR_ARG, "read failed / truncated file");
+}
+}  // namespace
+
+extern "C" dade_status dade_save(const dade_index* x, const char* path) {
+  API_BEGIN
+  need(x, "index"); need(path, "path");
+  DADE_REQUIRE(x->has_rot && x->has_ivf, DADE_ERR_STATE, "save needs rotation + IVF");
+  DeviceGuard g(x->device);
+  FILE* f = fopen(path, "wb");
+  DADE_REQUIRE(f, DADE_ERR_ARG, std::string("cannot open ") + path);
+  struct Closer { FILE* f; ~Closer() { fclose(f); } } cl{f};
+  const int D = x->D;
+  const int64_t hdr[6] = {(int64_t)kMagic, D, x->nlist, x->n, x->id_base, x->has_cal ? 1 : 0};
+  wr(f, hdr, sizeof(hdr));
+  wr(f, x->mean.data(), 8 * D); wr(f, x->R.data(), 8 * (size_t)D * D); wr(f, x->lam.data(), 8 * D);
+  std::vector<float> cent((size_t)x->nlist * D), lay((size_t)x->n * D);
+  DADE_CK(cudaMemcpy(cent.data(), x->cent.p, 4 * cent.size(), cudaMemcpyDeviceToHost));
+  DADE_CK(cudaMemcpy(lay.data(), x->layout.p, 4 * lay.size(), cudaMemcpyDeviceToHost));
+  wr(f, cent.data(), 4 * cent.size());
+  wr(f, x->off_h.data(), 8 * x->off_h.size());
+  wr(f, x->row_id_h.data(), 8 * x->row_id_h.size());
+  wr(f, x->assign_h.data(), 4 * x->assign_h.size());
+  wr(f, lay.data(), 4 * lay.size());
+  if (x->has_cal) {
+    const int64_t c[3] = {x->calK, x->n0, x->ncls};
+    wr(f, c, sizeof(c));
+    wr(f, x->m1.data(), 8 * x->m1.size());
+    wr(f, x->v.data(), 8 * x->v.size());
+  }
+  API_END
+}
+
+extern "C" dade_status dade_load(dade_index* x, const char* path) {
+  API_BEGIN
+  need(x, "index"); need(path, "path");
+  DeviceGuard g(x->device);
+  FILE* f = fopen(path, "rb");
+  DADE_REQUIRE(f, DADE_ERR_ARG, std::string("cannot open ") + path);
+  struct Closer { FILE* f; ~Closer() { fclose(f); } } cl{f};
+  int64_t hdr[6];
+  rd(f, hdr, sizeof(hdr));
+  DADE_REQUIRE(hdr[0] == (int64_t)kMagic, DADE_ERR_ARG, "not a DADE index file");
+  DADE_REQUIRE(hdr[1] == x->D, DADE_ERR_SHAPE, "file D differs from the index D");
+  const int D = x->D;
+  const int nlist = (int)hdr[2];
+  const int64_t n = hdr[3];
+  std::vector<double> mean(D), R((size_t)D * D), lam(D);
+  rd(f, mean.data(), 8 * D); rd(f, R.data(), 8 * R.size()); rd(f, lam.data(), 8 * D);
+  std::vector<float> cent((size_t)nlist * D), lay((size_t)n * D);
+  std::vector<int64_t> off(nlist + 1), rid(n);
+  std::vector<int32_t> asg(n);
+  rd(f, cent.data(), 4 * cent.size()); rd(f, off.data(), 8 * off.size());
+  rd(f, rid.data(), 8 * rid.size()); rd(f, asg.data(), 4 * asg.size());
+  rd(f, lay.data(), 4 * lay.size());
+  std::vector<double> m1, v;
+  int64_t c[3] = {0, 0, 0};
+  if (hdr[5]) {
+    rd(f, c, sizeof(c));
+    m1.resize(c[2]); v.resize((size_t)c[2] * c[1]);
+    rd(f, m1.data(), 8 * m1.size()); rd(f, v.data(), 8 * v.size());
+  }
+  x->mean = mean; x->R = R; x->lam = lam;
+  upload_rotation(x);
+  x->cent.reserve(cent.size()); x->layout.reserve(lay.size());
+  x->off_d.reserve(nlist + 1); x->row_id_d.reserve(n);
+  std::vector<int32_t> off32(off.begin(), off.end()), rid32(rid.begin(), rid.end());
+  DADE_CK(cudaMemcpy(x->cent.p, cent.data(), 4 * cent.size(), cudaMemcpyHostToDevice));
+  DADE_CK(cudaMemcpy(x->layout.p, lay.data(), 4 * lay.size(), cudaMemcpyHostToDevice));
+  DADE_CK(cudaMemcpy(x->off_d.p, off32.data(), 4 * off32.size(), cudaMemcpyHostToDevice));
+  DADE_CK(cudaMemcpy(x->row_id_d.p, rid32.data(), 4 * rid32.size(), cudaMemcpyHostToDevice));
+  x->off_h = off; x->row_id_h = rid; x->assign_h = asg;
+  x->pos_of_h.assign(n, 0);
+  for (int64_t p = 0; p < n; ++p) x->pos_of_h[rid[p] - hdr[4]] = (int32_t)p;
+  x->nlist = nlist; x->n = n; x->id_base = hdr[4]; x->has_ivf = true;
+  x->has_cal = hdr[5] != 0;
+  if (x->has_cal) { x->calK = (int)c[0]; x->n0 = (int)c[1]; x->ncls = (int)c[2]; x->m1 = m1; x->v = v; }
+  API_END
+}

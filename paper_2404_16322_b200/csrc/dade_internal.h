@@ -1,0 +1,121 @@
+// Internal declarations shared by the C-ABI layer (dade_api.cu) and the kernel TUs.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dade.h"
+
+namespace dade {
+
+// A dade_status-carrying exception used inside the library only; converted at the ABI edge.
+struct Error : std::runtime_error {
+  dade_status st;
+  Error(dade_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define DADE_CK(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::dade::Error(e_ == cudaErrorMemoryAllocation ? DADE_ERR_OOM : DADE_ERR_CUDA, \
+                          std::string(#call) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+#define DADE_REQUIRE(cond, st, msg) \
+  do {                              \
+    if (!(cond)) throw ::dade::Error(st, msg); \
+  } while (0)
+
+// Owning device buffer (grows, never shrinks).
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void reserve(size_t n) {
+    if (n <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (n == 0) return;
+    DADE_CK(cudaMalloc(&p, n * sizeof(T)));
+    cap = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+constexpr int kBlk = 16;  // layout block width B_L (dims per 64-B row)
+
+// --------------------------------------------------------------------- kernel launchers
+// exact.cu : fp32 tile distances + fp64-certified selection (assign / probe / KNN)
+// d_hat[i*n + j] = fp32 sum_k fma((a_ik - b_jk)^2) for a block of rows of A against all rows of B.
+void launch_l2_tile(const float* A, int64_t m, const float* B, int64_t n, int D, float* out,
+                    cudaStream_t st);
+// For each row i of the m x n matrix d_hat: the k nearest columns under the EXACT fp64
+// sequential-sum distance between A[i] and B[col], ordered by (dist, col). Writes
+// out_idx[i*k..] (column indices), out_d64[i*k..] (fp64 distances, may be null). Returns via
+// *d_flag a nonzero value if a candidate buffer overflowed (caller reports an error).
+void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const float* A,
+                         const float* B, int D, int32_t* out_idx, double* out_d64,
+                         int32_t* cand_buf, int cand_cap, int* d_flag, cudaStream_t st);
+// Argmin (k = 1) specialisation for assignment: out[i] = argmin_c exact(A[i], B[c]).
+void launch_argmin_exact(const float* d_hat, int64_t m, int64_t n, const float* A, const float* B,
+                         int D, int32_t* out, int* d_flag, cudaStream_t st);
+
+// rotate.cu : x~ = R (x - mu) with fp64 accumulation, stored fp32.
+//  rowmajor_out != null: out[p*D + i]; else blocked layout out[(b*n_out + p)*16 + i%16].
+//  src_rows != null: input row of output p is X[src_rows[p]] (gather) else X[p].
+void launch_rotate(const float* X, const int32_t* src_rows, int64_t n_out, int D, const double* R,
+                   const double* mu, float* rowmajor_out, float* blocked_out, cudaStream_t st);
+
+// pca.cu : strided-sample moments in fp64
+void launch_pca_sum(const float* X, int64_t n, int64_t id_base, int64_t n_total, int64_t ns,
+                    int D, double* sum_dev, int64_t* cnt_host, cudaStream_t st);
+void launch_pca_cov(const float* X, int64_t n, int64_t id_base, int64_t n_total, int64_t ns, int D,
+                    const double* mean_dev, double* cov_dev, double* scratch, int64_t scratch_elems,
+                    cudaStream_t st);
+int64_t pca_cov_scratch_elems(int64_t n_owned, int D);
+
+// calib.cu : per-pair prefix partial distances in fp64 from the fp32 layout
+void launch_pair_prefix(const float* layout, int64_t n_rows, int D, const float* qrot,
+                        const int32_t* pair_q, const int32_t* pair_row, int npairs, double* out,
+                        cudaStream_t st);
+// scan.cu
+struct ScanParams {
+  const float* qrot;      // nq x D
+  const int32_t* probes;  // nq x nprobe
+  const int32_t* off;     // nlist + 1
+  const int32_t* row_id;  // n global ids (list-major)
+  const float* layout;    // D/16 blocks of n x 16
+  int64_t n;
+  int D, nq, nprobe, K, dd, nsteps, c0;
+  int prune;              // 0: no classifier can prune (alpha = 0 or one step)
+  float m1[DADE_MAX_STEPS];
+  float beta[DADE_MAX_STEPS];
+  int64_t* out_ids;
+  float* out_d;
+  unsigned long long* counters;  // [0]=tested [1]=survivors [2]=dims [3]=max epochs [4..4+64) pruned_at_step
+};
+void launch_scan(const ScanParams& p, cudaStream_t st);
+// merge.cu
+void launch_merge_topk(const int64_t* ids_in, const float* d_in, int S, int nq, int K,
+                       int64_t* ids_out, float* d_out, cudaStream_t st);
+void launch_check_finite(const float* X, int64_t n, int* flag, cudaStream_t st);
+void launch_gather_rows(const float* X, const int32_t* rows, int64_t m, int D, float* out,
+                        cudaStream_t st);
+
+// host_eig.cpp : symmetric eigendecomposition (Householder tridiagonalisation + implicit QL)
+void sym_eig(int n, const double* A, double* eigval, double* eigvec_colmajor);
+// host_calib.cpp
+bool logistic_irls(const std::vector<double>& P, const std::vector<double>& tau,
+                   const std::vector<double>& y, double ridge, int max_iter, double tol,
+                   double* m1, double* beta);
+uint64_t splitmix64(uint64_t x);
+
+}  // namespace dade

@@ -1,0 +1,282 @@
+// Exact nearest-centroid / nearest-neighbour selection (IVF assignment P:L172-173, probe P:L174,
+// brute-force KNN P:L132-137) that is BIT-EXACT with the fp64 sequential-sum definition (R20):
+//   1. d_hat = fp32 direct-difference distances for a tile of rows (FMA accumulation),
+//   2. relative error bound rho = gamma_{D+2}: d_hat in [d(1-rho), d(1+rho)],
+//   3. candidates = columns with d_hat <= d_hat_(k) * (1+rho)/(1-rho)  (contains every column whose
+//      exact distance is <= the exact k-th distance, ties included),
+//   4. exact fp64 sequential sums (no FMA contraction) for the candidates, sort by (dist, column).
+#include <cfloat>
+#include <cstdio>
+
+#include "dade_internal.h"
+
+namespace dade {
+
+// ------------------------------------------------------------------ fp32 tile distances
+// 64 x 64 output tile per CTA, 256 threads, 4 x 4 outputs per thread, D consumed 16 dims at a time.
+__global__ void __launch_bounds__(256) k_l2_tile(const float* __restrict__ A, int64_t m,
+                                                 const float* __restrict__ B, int64_t n, int D,
+                                                 float* __restrict__ out) {
+  __shared__ __align__(16) float As[16][64];
+  __shared__ __align__(16) float Bs[16][64];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t r0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 64;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // loader mapping: 256 threads load 64 rows x 16 dims = 1024 floats each for A and B (4 per thread)
+  const int lr = threadIdx.x >> 2, lc = (threadIdx.x & 3) * 4;
+  for (int k0 = 0; k0 < D; k0 += 16) {
+    float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+    if (r0 + lr < m) va = *reinterpret_cast<const float4*>(A + (r0 + lr) * D + k0 + lc);
+    if (c0 + lr < n) vb = *reinterpret_cast<const float4*>(B + (c0 + lr) * D + k0 + lc);
+    As[lc + 0][lr] = va.x; As[lc + 1][lr] = va.y; As[lc + 2][lr] = va.z; As[lc + 3][lr] = va.w;
+    Bs[lc + 0][lr] = vb.x; Bs[lc + 1][lr] = vb.y; Bs[lc + 2][lr] = vb.z; Bs[lc + 3][lr] = vb.w;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float t = av[i] - bv[j];
+          acc[i][j] = fmaf(t, t, acc[i][j]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + ty * 4 + i;
+    if (r >= m) continue;
+    const int64_t c = c0 + tx * 4;
+    float* o = out + r * n + c;
+    if (c + 3 < n && (n & 3) == 0) {
+      *reinterpret_cast<float4*>(o) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c + j < n) o[j] = acc[i][j];
+    }
+  }
+}
+
+void launch_l2_tile(const float* A, int64_t m, const float* B, int64_t n, int D, float* out,
+                    cudaStream_t st) {
+  dim3 grid((unsigned)((n + 63) / 64), (unsigned)((m + 63) / 64));
+  k_l2_tile<<<grid, 256, 0, st>>>(A, m, B, n, D, out);
+  DADE_CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ exact fp64 distance
+// The definition (R20): sum_{j=0}^{D-1} (a_j - b_j)^2 in IEEE fp64, sequential, each operation
+// rounded separately (explicit _rn intrinsics forbid FMA contraction).
+__device__ __forceinline__ double exact_sqdist(const float* __restrict__ a,
+                                               const float* __restrict__ b, int D) {
+  double acc = 0.0;
+  for (int j = 0; j < D; ++j) {
+    const double t = __dsub_rn((double)a[j], (double)b[j]);
+    acc = __dadd_rn(acc, __dmul_rn(t, t));
+  }
+  return acc;
+}
+
+// threshold on d_hat bits: T = v * (1+rho)/(1-rho) rounded up, rho = 2 * gamma_{D+2}
+__device__ __forceinline__ unsigned thr_bits(float v, int D) {
+  const double u = 5.9604644775390625e-08;  // 2^-24
+  const double g = (D + 2) * u / (1.0 - (D + 2) * u);
+  const double rho = 2.0 * g;
+  const double T = (double)v * (1.0 + rho) / (1.0 - rho);
+  float tf = (float)T;
+  unsigned b = __float_as_uint(tf);
+  if (!(tf >= 0.f)) return 0xffffffffu;
+  return b == 0x7f800000u ? b : b + 2u;  // two ulps of slack on top of the rounding of T
+}
+
+struct Cand {
+  double d;
+  int32_t c;
+};
+__device__ __forceinline__ bool cand_less(const Cand& x, const Cand& y) {
+  return x.d < y.d || (x.d == y.d && x.c < y.c);
+}
+
+constexpr int kSelThreads = 512;
+constexpr int kSortCap = 4096;
+
+// One CTA per row: radix-select the k-th smallest d_hat, collect candidates, exact re-rank, sort.
+__global__ void __launch_bounds__(kSelThreads) k_select_exact(
+    const float* __restrict__ dh, int64_t n, int k, const float* __restrict__ A,
+    const float* __restrict__ B, int D, int32_t* __restrict__ out_idx, double* __restrict__ out_d,
+    int32_t* __restrict__ cand_buf, int cand_cap, int* flag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cand* cs = reinterpret_cast<Cand*>(smem_raw);  // kSortCap entries
+  __shared__ unsigned hist[256];
+  __shared__ unsigned s_prefix, s_krem, s_count;
+  const int64_t row = blockIdx.x;
+  const float* d = dh + row * n;
+  const unsigned* du = reinterpret_cast<const unsigned*>(d);
+  const int tid = threadIdx.x;
+  if (tid == 0) { s_prefix = 0; s_krem = (unsigned)k; s_count = 0; }
+  unsigned mask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    for (int64_t i = tid; i < n; i += blockDim.x) {
+      const unsigned b = du[i];
+      if ((b & mask) == prefix) atomicAdd(&hist[(b >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned kr = s_krem, cum = 0;
+      int dig = 0;
+      for (; dig < 256; ++dig) {
+        if (cum + hist[dig] >= kr) break;
+        cum += hist[dig];
+      }
+      s_krem = kr - cum;
+      s_prefix = prefix | ((unsigned)dig << shift);
+    }
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  const unsigned tb = thr_bits(__uint_as_float(s_prefix), D);
+  int32_t* cb = cand_buf + row * (int64_t)cand_cap;
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    if (du[i] <= tb) {
+      const unsigned pos = atomicAdd(&s_count, 1u);
+      if (pos < (unsigned)cand_cap) cb[pos] = (int32_t)i;
+    }
+  }
+  __syncthreads();
+  unsigned cnt = s_count;
+  if (cnt > (unsigned)cand_cap || cnt > (unsigned)kSortCap) {
+    if (tid == 0) atomicExch(flag, 1);
+    cnt = min(cnt, (unsigned)min(cand_cap, kSortCap));
+  }
+  unsigned P = 1;
+  while (P < cnt) P <<= 1;
+  const float* a = A + row * (int64_t)D;
+  for (unsigned i = tid; i < P; i += blockDim.x) {
+    if (i < cnt) {
+      const int32_t c = cb[i];
+      cs[i].d = exact_sqdist(a, B + (int64_t)c * D, D);
+      cs[i].c = c;
+    } else {
+      cs[i].d = DBL_MAX;
+      cs[i].c = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  // bitonic sort of P entries by (d, c)
+  for (unsigned size = 2; size <= P; size <<= 1) {
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      for (unsigned i = tid; i < P / 2; i += blockDim.x) {
+        const unsigned lo = 2 * i - (i & (stride - 1));
+        const unsigned hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        Cand x = cs[lo], y = cs[hi];
+        if (cand_less(y, x) == up) { cs[lo] = y; cs[hi] = x; }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < k; i += blockDim.x) {
+    const bool ok = (unsigned)i < cnt;
+    out_idx[row * k + i] = ok ? cs[i].c : -1;
+    if (out_d) out_d[row * k + i] = ok ? cs[i].d : DBL_MAX;
+  }
+}
+
+void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const float* A,
+                         const float* B, int D, int32_t* out_idx, double* out_d64,
+                         int32_t* cand_buf, int cand_cap, int* d_flag, cudaStream_t st) {
+  if (m <= 0) return;
+  static bool attr = false;
+  const size_t smem = kSortCap * sizeof(Cand);
+  if (!attr) {
+    DADE_CK(cudaFuncSetAttribute(k_select_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  k_select_exact<<<(unsigned)m, kSelThreads, smem, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64,
+                                                         cand_buf, cand_cap, d_flag);
+  DADE_CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ argmin (k = 1), warp per row
+__global__ void __launch_bounds__(256) k_argmin_exact(const float* __restrict__ dh, int64_t m,
+                                                      int64_t n, const float* __restrict__ A,
+                                                      const float* __restrict__ B, int D,
+                                                      int32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= m) return;
+  const float* d = dh + row * n;
+  float mn = FLT_MAX;
+  for (int64_t i = lane; i < n; i += 32) mn = fminf(mn, d[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  const unsigned tb = thr_bits(mn, D);
+  const float* a = A + row * (int64_t)D;
+  double best = DBL_MAX;
+  int32_t bc = 0x7fffffff;
+  for (int64_t i0 = 0; i0 < n; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const bool c = i < n && __float_as_uint(d[i]) <= tb;
+    if (c) {
+      const double e = exact_sqdist(a, B + i * D, D);
+      if (e < best || (e == best && (int32_t)i < bc)) { best = e; bc = (int32_t)i; }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+    if (ob < best || (ob == best && oc < bc)) { best = ob; bc = oc; }
+  }
+  if (lane == 0) out[row] = bc;
+}
+
+void launch_argmin_exact(const float* d_hat, int64_t m, int64_t n, const float* A, const float* B,
+                         int D, int32_t* out, int* d_flag, cudaStream_t st) {
+  (void)d_flag;
+  if (m <= 0) return;
+  k_argmin_exact<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(d_hat, m, n, A, B, D, out);
+  DADE_CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ misc small kernels
+__global__ void k_check_finite(const float* __restrict__ X, int64_t n, int* flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(X[i])) { atomicExch(flag, 1); return; }
+}
+void launch_check_finite(const float* X, int64_t n, int* flag, cudaStream_t st) {
+  if (n <= 0) return;
+  k_check_finite<<<1184, 256, 0, st>>>(X, n, flag);
+  DADE_CK(cudaGetLastError());
+}
+
+__global__ void k_gather_rows(const float* __restrict__ X, const int32_t* __restrict__ rows,
+                              int64_t m, int D, float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m * D;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / D;
+    out[i] = X[(int64_t)rows[r] * D + (i - r * D)];
+  }
+}
+void launch_gather_rows(const float* X, const int32_t* rows, int64_t m, int D, float* out,
+                        cudaStream_t st) {
+  if (m <= 0) return;
+  k_gather_rows<<<1184, 256, 0, st>>>(X, rows, m, D, out);
+  DADE_CK(cudaGetLastError());
+}
+
+}  // namespace dade

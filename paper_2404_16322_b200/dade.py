@@ -1,0 +1,269 @@
+"""Thin ctypes binding over the C ABI in include/dade.h (argument marshalling only).
+
+Every computation runs in libdade.so (hand-written sm_100a CUDA kernels + host C++). PyTorch
+is used for device memory and streams only. There is no CPU fallback: if the library is not
+built, or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdade.so")
+MAX_STEPS = 64
+MAX_K = 256
+
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_STATE", 4: "ERR_NONFINITE", 5: "ERR_OOM",
+          6: "ERR_CUDA", 8: "ERR_UNSUPPORTED"}
+
+
+class DadeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Stats(C.Structure):
+    _fields_ = [("tested", C.c_int64), ("survivors", C.c_int64), ("dims_scanned", C.c_int64),
+                ("pruned_at_step", C.c_int64 * MAX_STEPS), ("n_steps", C.c_int32),
+                ("n_epochs", C.c_int32), ("ms_rotate", C.c_float), ("ms_probe", C.c_float),
+                ("ms_scan", C.c_float), ("ms_total", C.c_float)]
+
+    def as_dict(self) -> dict:
+        return {"tested": self.tested, "survivors": self.survivors, "dims_scanned": self.dims_scanned,
+                "pruned_at_step": list(self.pruned_at_step[: self.n_steps]), "n_steps": self.n_steps,
+                "n_epochs": self.n_epochs, "ms_rotate": self.ms_rotate, "ms_probe": self.ms_probe,
+                "ms_scan": self.ms_scan, "ms_total": self.ms_total}
+
+
+_lib = None
+P = C.c_void_p
+I64, I32, DBL = C.c_int64, C.c_int, C.c_double
+_SIGS = {
+    "dade_create": [I32, P, I32, C.POINTER(P)],
+    "dade_destroy": [P],
+    "dade_fit_rotation": [P, P, I64, I64],
+    "dade_pca_mean_partial": [P, P, I64, I64, I64, I64, P, P],
+    "dade_pca_cov_partial": [P, P, I64, I64, I64, I64, P, P],
+    "dade_set_rotation_from_cov": [P, P, P, I64],
+    "dade_get_rotation": [P, P, P, P],
+    "dade_set_rotation": [P, P, P, P],
+    "dade_build_ivf": [P, P, I64, I64, I32, P, I32],
+    "dade_get_ivf": [P, P, P, P, P],
+    "dade_get_sizes": [P, P, P],
+    "dade_get_layout": [P, P],
+    "dade_calibrate": [P, P, P, I32, I32, I32, I32, C.c_uint64],
+    "dade_get_calibration": [P, P, P, P, P, P],
+    "dade_set_calibration": [P, I32, I32, I32, P, P],
+    "dade_search": [P, P, I32, I32, I32, I32, DBL, P, P, P],
+    "dade_search_host": [P, P, I32, I32, I32, I32, DBL, P, P, P],
+    "dade_probe": [P, P, I32, I32, P],
+    "dade_bruteforce_knn": [P, P, I64, I64, P, I32, I32, P, P],
+    "dade_merge_topk": [P, P, P, I32, I32, I32, P, P],
+    "dade_save": [P, C.c_char_p],
+    "dade_load": [P, C.c_char_p],
+}
+
+
+def lib():
+    """Load libdade.so (built in-tree by paper_2404_16322_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2404_16322_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.dade_last_error.restype = C.c_char_p
+        L.dade_last_error.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _ck(st: int):
+    if st != 0:
+        raise DadeError(st, lib().dade_last_error().decode())
+
+
+def _ptr(t) -> int:
+    """Device (torch CUDA tensor) or host (numpy / torch CPU) pointer of a contiguous array."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    assert t.is_contiguous(), "tensor must be contiguous"
+    return t.data_ptr()
+
+
+def _dev(t, dtype):
+    import torch
+    assert isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.is_contiguous(), \
+        f"expected a contiguous CUDA {dtype} tensor"
+    return t
+
+
+class Index:
+    """One shard of a DADE index on one GPU (wraps `dade_index*`)."""
+
+    def __init__(self, D: int, device: int = 0, stream=None):
+        import torch
+        self.D = D
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = P()
+        _ck(lib().dade_create(device, P(self.stream.cuda_stream), D, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().dade_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------- a0
+    def fit_rotation(self, X, sample_size: int = 0):
+        import torch
+        X = _dev(X, torch.float32)
+        _ck(lib().dade_fit_rotation(self.h, _ptr(X), X.shape[0], sample_size))
+
+    def pca_mean_partial(self, X, id_base: int, n_total: int, sample_size: int = 0):
+        s = np.zeros(self.D); cnt = np.zeros(1, np.int64)
+        n = 0 if X is None else X.shape[0]
+        _ck(lib().dade_pca_mean_partial(self.h, _ptr(X), n, id_base, n_total, sample_size, _ptr(s), _ptr(cnt)))
+        return s, int(cnt[0])
+
+    def pca_cov_partial(self, X, id_base: int, n_total: int, mean, sample_size: int = 0):
+        mean = np.ascontiguousarray(mean, np.float64)
+        cov = np.zeros((self.D, self.D))
+        n = 0 if X is None else X.shape[0]
+        _ck(lib().dade_pca_cov_partial(self.h, _ptr(X), n, id_base, n_total, sample_size, _ptr(mean), _ptr(cov)))
+        return cov
+
+    def set_rotation_from_cov(self, mean, cov_sum, count: int):
+        mean = np.ascontiguousarray(mean, np.float64); cov_sum = np.ascontiguousarray(cov_sum, np.float64)
+        _ck(lib().dade_set_rotation_from_cov(self.h, _ptr(mean), _ptr(cov_sum), count))
+
+    def get_rotation(self):
+        D = self.D
+        m, R, l = np.zeros(D), np.zeros((D, D)), np.zeros(D)
+        _ck(lib().dade_get_rotation(self.h, _ptr(m), _ptr(R), _ptr(l)))
+        return m, R, l
+
+    def set_rotation(self, mean, R, eigvals=None):
+        mean = np.ascontiguousarray(mean, np.float64); R = np.ascontiguousarray(R, np.float64)
+        ev = None if eigvals is None else np.ascontiguousarray(eigvals, np.float64)
+        _ck(lib().dade_set_rotation(self.h, _ptr(mean), _ptr(R), _ptr(ev)))
+
+    # -------------------------------------------------- a1 + a2
+    def build_ivf(self, X, nlist: int, centroids=None, kmeans_iters: int = 10, id_base: int = 0):
+        import torch
+        X = _dev(X, torch.float32)
+        if centroids is not None:
+            centroids = _dev(centroids, torch.float32)
+        _ck(lib().dade_build_ivf(self.h, _ptr(X), X.shape[0], id_base, nlist, _ptr(centroids), kmeans_iters))
+
+    def sizes(self):
+        n = np.zeros(1, np.int64); nl = np.zeros(1, np.int32)
+        _ck(lib().dade_get_sizes(self.h, _ptr(n), _ptr(nl)))
+        return int(n[0]), int(nl[0])
+
+    def get_ivf(self):
+        n, nlist = self.sizes()
+        off = np.zeros(nlist + 1, np.int64); row_id = np.zeros(n, np.int64)
+        assign = np.zeros(n, np.int32); cent = np.zeros((nlist, self.D), np.float32)
+        _ck(lib().dade_get_ivf(self.h, _ptr(off), _ptr(row_id), _ptr(assign), _ptr(cent)))
+        return off, row_id, assign, cent
+
+    def get_layout(self):
+        n, _ = self.sizes()
+        out = np.zeros((n, self.D), np.float32)
+        _ck(lib().dade_get_layout(self.h, _ptr(out)))
+        return out
+
+    # -------------------------------------------------- a3
+    def calibrate(self, X, Qc, K: int, n_neg: int = 50, nprobe_neg: int = 0, seed: int = 0):
+        import torch
+        X = _dev(X, torch.float32); Qc = _dev(Qc, torch.float32)
+        _ck(lib().dade_calibrate(self.h, _ptr(X), _ptr(Qc), Qc.shape[0], K, n_neg, nprobe_neg, seed))
+
+    def get_calibration(self):
+        K, n0, nc = (np.zeros(1, np.int32) for _ in range(3))
+        _ck(lib().dade_get_calibration(self.h, _ptr(K), _ptr(n0), _ptr(nc), None, None))
+        m1 = np.zeros(int(nc[0])); v = np.zeros((int(nc[0]), int(n0[0])))
+        _ck(lib().dade_get_calibration(self.h, None, None, None, _ptr(m1), _ptr(v)))
+        return {"K": int(K[0]), "n0": int(n0[0]), "m1": m1, "v": v, "block": 16}
+
+    def set_calibration(self, K: int, m1, v):
+        m1 = np.ascontiguousarray(m1, np.float64); v = np.ascontiguousarray(v, np.float64)
+        _ck(lib().dade_set_calibration(self.h, K, v.shape[1], v.shape[0], _ptr(m1), _ptr(v)))
+
+    # -------------------------------------------------- a4..a8
+    def search(self, Q, K: int, nprobe: int, delta_d: int, significance: float, ids=None, dists=None,
+               stats: bool = False):
+        import torch
+        Q = _dev(Q, torch.float32)
+        nq = Q.shape[0]
+        if ids is None:
+            ids = torch.empty((nq, K), dtype=torch.int64, device=Q.device)
+        if dists is None:
+            dists = torch.empty((nq, K), dtype=torch.float32, device=Q.device)
+        st = Stats() if stats else None
+        _ck(lib().dade_search(self.h, _ptr(Q), nq, K, nprobe, delta_d, float(significance), _ptr(ids),
+                              _ptr(dists), C.byref(st) if st is not None else None))
+        return (ids, dists, st.as_dict()) if stats else (ids, dists)
+
+    def search_host(self, Q, K: int, nprobe: int, delta_d: int, significance: float, ids=None, dists=None,
+                    stats: bool = False):
+        """Q, ids, dists in HOST memory (numpy or pinned torch CPU tensors); H2D/D2H inside."""
+        nq = Q.shape[0]
+        if ids is None:
+            ids = np.empty((nq, K), np.int64)
+        if dists is None:
+            dists = np.empty((nq, K), np.float32)
+        st = Stats() if stats else None
+        _ck(lib().dade_search_host(self.h, _ptr(Q), nq, K, nprobe, delta_d, float(significance), _ptr(ids),
+                                   _ptr(dists), C.byref(st) if st is not None else None))
+        return (ids, dists, st.as_dict()) if stats else (ids, dists)
+
+    def probe(self, Q, nprobe: int):
+        import torch
+        Q = _dev(Q, torch.float32)
+        out = torch.empty((Q.shape[0], nprobe), dtype=torch.int32, device=Q.device)
+        _ck(lib().dade_probe(self.h, _ptr(Q), Q.shape[0], nprobe, _ptr(out)))
+        return out
+
+    # -------------------------------------------------- tools
+    def bruteforce_knn(self, X, Q, K: int, id_base: int = 0):
+        import torch
+        X = _dev(X, torch.float32); Q = _dev(Q, torch.float32)
+        ids = torch.empty((Q.shape[0], K), dtype=torch.int64, device=Q.device)
+        d = torch.empty((Q.shape[0], K), dtype=torch.float32, device=Q.device)
+        _ck(lib().dade_bruteforce_knn(self.h, _ptr(X), X.shape[0], id_base, _ptr(Q), Q.shape[0], K, _ptr(ids), _ptr(d)))
+        return ids, d
+
+    def merge_topk(self, ids_in, dists_in):
+        """ids_in/dists_in: CUDA tensors S x nq x K (as all_gather_into_tensor lays them out)."""
+        import torch
+        ids_in = _dev(ids_in, torch.int64); dists_in = _dev(dists_in, torch.float32)
+        S, nq, K = ids_in.shape
+        ids = torch.empty((nq, K), dtype=torch.int64, device=ids_in.device)
+        d = torch.empty((nq, K), dtype=torch.float32, device=ids_in.device)
+        _ck(lib().dade_merge_topk(self.h, _ptr(ids_in), _ptr(dists_in), S, nq, K, _ptr(ids), _ptr(d)))
+        return ids, d
+
+    def save(self, path: str):
+        _ck(lib().dade_save(self.h, path.encode()))
+
+    def load(self, path: str):
+        _ck(lib().dade_load(self.h, path.encode()))

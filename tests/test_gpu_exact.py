@@ -1,0 +1,67 @@
+"""GPU parity: exact KNN / probe / assignment (bit-exact ids vs the oracle's fp64 definition)."""
+import numpy as np
+import pytest
+
+from oracle import dade_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU test run without a GPU"
+    from paper_2404_16322_b200 import build
+    build.build()
+    return torch
+
+
+def _idx(torch, D):
+    from paper_2404_16322_b200 import Index
+    return Index(D)
+
+
+@pytest.mark.parametrize("n,D,K", [(1000, 16, 1), (3001, 48, 10), (777, 128, 100), (5000, 64, 257)])
+def test_bruteforce_knn_bit_exact(torch_cuda, n, D, K):
+    torch = torch_cuda
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, D)).astype(np.float32)
+    Q = rng.standard_normal((37, D)).astype(np.float32)
+    ix = _idx(torch, D)
+    gi, gd = ix.bruteforce_knn(torch.from_numpy(X).cuda(), torch.from_numpy(Q).cuda(), K, id_base=5)
+    oi, od = O.brute_force_knn(X, Q, K, id_base=5)
+    assert np.array_equal(gi.cpu().numpy(), oi)
+    assert np.array_equal(gd.cpu().numpy(), od.astype(np.float32))  # fp32 rounding of the exact fp64 value
+
+
+def test_bruteforce_knn_integer_ties(torch_cuda):
+    torch = torch_cuda
+    rng = np.random.default_rng(1)
+    X = rng.integers(0, 4, size=(4000, 32)).astype(np.float32)   # massive exact ties
+    Q = rng.integers(0, 4, size=(20, 32)).astype(np.float32)
+    ix = _idx(torch, 32)
+    gi, gd = ix.bruteforce_knn(torch.from_numpy(X).cuda(), torch.from_numpy(Q).cuda(), 50)
+    oi, od = O.brute_force_knn(X, Q, 50)
+    assert np.array_equal(gi.cpu().numpy(), oi)
+
+
+def test_probe_and_assign_bit_exact(torch_cuda):
+    torch = torch_cuda
+    rng = np.random.default_rng(2)
+    D, n, C = 64, 6000, 200
+    X = rng.integers(0, 6, size=(n, D)).astype(np.float32)
+    cent = X[rng.choice(n, C, replace=False)].copy()
+    cent[17] = cent[3]                                           # duplicated centroid -> tie to 3
+    cent[:50] += rng.standard_normal((50, D)).astype(np.float32) * 0.5
+    ix = _idx(torch, D)
+    mean, R, lam = O.fit_rotation(X)
+    ix.set_rotation(mean, R, lam)
+    ix.build_ivf(torch.from_numpy(X).cuda(), C, centroids=torch.from_numpy(cent).cuda())
+    off, row_id, assign, c2 = ix.get_ivf()
+    oa, ooff, orow = O.build_ivf(X, cent)
+    assert np.array_equal(assign, oa)
+    assert np.array_equal(off, ooff) and np.array_equal(row_id, orow)
+    Q = rng.integers(0, 6, size=(25, D)).astype(np.float32)
+    pr = ix.probe(torch.from_numpy(Q).cuda(), 31).cpu().numpy()
+    for q in range(25):
+        assert pr[q].tolist() == O.probe(Q[q], cent, 31).tolist()
