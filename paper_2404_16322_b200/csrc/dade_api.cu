@@ -156,8 +156,8 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
                int64_t* ids, float* dists, dade_stats* stats) {
   const int D = x->D;
   DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
-  need(Q, "Q"); need(ids, "ids"); need(dists, "dists");
   DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
+  if (nq > 0) { need(Q, "Q"); need(ids, "ids"); need(dists, "dists"); }
   DADE_REQUIRE(K >= 1, DADE_ERR_ARG, "K < 1");
   DADE_REQUIRE(K <= DADE_MAX_K, DADE_ERR_UNSUPPORTED, "K > DADE_MAX_K");
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
@@ -167,8 +167,9 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   const int nsteps = D / delta_d;
   DADE_REQUIRE(nsteps <= DADE_MAX_STEPS, DADE_ERR_UNSUPPORTED, "D/delta_d > DADE_MAX_STEPS");
   const int dd = delta_d / 16;
-  DADE_REQUIRE(dd == 1 || dd == 2 || dd == 4, DADE_ERR_UNSUPPORTED, "delta_d must be 16, 32 or 64");
   const bool prune = alpha > 0.0 && nsteps > 1;
+  DADE_REQUIRE(!prune || dd == 1 || dd == 2 || dd == 4, DADE_ERR_UNSUPPORTED,
+               "with pruning, delta_d must be 16, 32 or 64");
   if (prune) {
     DADE_REQUIRE(x->has_cal, DADE_ERR_STATE, "significance > 0 requires calibration");
     DADE_REQUIRE(x->calK == K, DADE_ERR_STATE, "K differs from the calibrated K");
@@ -196,8 +197,10 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   ScanParams p{};
   p.qrot = x->qrot.p; p.probes = x->probes.p; p.off = x->off_d.p; p.row_id = x->row_id_d.p;
   p.layout = x->layout.p; p.n = x->n; p.D = D; p.nq = nq; p.nprobe = nprobe; p.K = K;
-  p.dd = dd; p.nsteps = nsteps; p.c0 = 4 * K; p.prune = prune ? 1 : 0;
-  for (int s = 1; s < nsteps; ++s) {
+  // alpha = 0 (or a single step): nothing can be pruned; the kernel then runs with 16-dim
+  // steps (no classifier fires: m1 = 1, beta' = -inf), which serves every delta_d | D.
+  p.dd = prune ? dd : 1; p.nsteps = prune ? nsteps : D / 16; p.c0 = 4 * K; p.prune = prune ? 1 : 0;
+  for (int s = 1; s < p.nsteps; ++s) {
     if (prune) {
       const int idx = (s * delta_d) / 16 - 1;
       const double alpha_s = (alpha * delta_d) / D;

@@ -27,7 +27,8 @@ namespace dade {
 namespace {
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int kQCap = 64;  // per-warp survivor queue capacity
+constexpr int kQCap = 128;  // per-warp survivor ring capacity (power of two)
+constexpr int kMinBlocks = 4;
 constexpr unsigned long long kKeyInf = ~0ull;
 
 struct __align__(16) QEntry {
@@ -142,22 +143,25 @@ __device__ void topk_insert(unsigned long long key, Shared& sh, unsigned long lo
 }  // namespace
 
 template <int DD>
-__global__ void __launch_bounds__(kThreads, 4) k_scan(const __grid_constant__ ScanParams p) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Shared sh;
   const int D = p.D, K = p.K;
   float* qs = reinterpret_cast<float*>(smem);                                  // D floats
   unsigned long long* topk = reinterpret_cast<unsigned long long*>(qs + D);    // 2 x MAX_K
-  QEntry* queues = reinterpret_cast<QEntry*>(topk + 2 * DADE_MAX_K);          // kWarps x kQCap
+  QEntry* queues = reinterpret_cast<QEntry*>(topk + 2 * DADE_MAX_K);          // kWarps x kQCap ring
   unsigned long long* sBall = reinterpret_cast<unsigned long long*>(queues + kWarps * kQCap);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
-  QEntry* queue = queues + warp * kQCap;
+  QEntry* ring = queues + warp * kQCap;
   unsigned long long* sB = sBall + warp * 32;
   const int64_t q = blockIdx.x;
-  constexpr int TR = 64 / DD;  // rows per tile
+  constexpr int TR = 64 / DD;  // rows per stage-1 tile (8 x 128-bit loads per lane)
   constexpr int NI = TR / 8;   // 8 rows per warp instruction
+  constexpr int LA = 4;        // queue lookahead slots (blocks) per entry per round
+  constexpr int NB = 2;        // queue batches (8 entries each) per round
   const int nsteps = p.nsteps;
+  const int nblk = D >> 4;
   const int64_t n = p.n;
   const float* lay = p.layout;
 
@@ -177,8 +181,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scan(const __grid_constant__ Sc
   __syncthreads();
 
   unsigned long long c_tested = 0, c_surv = 0, c_dims = 0;
-  int qcnt = 0;
-  // stream cursor (warp-uniform, identical in all warps)
+  int head = 0, tail = 0;  // ring indices (monotonic), warp-uniform
   int cj = 0;
   int64_t cpos = 0, cstart = 0, clen = 0;
   auto load_list = [&](int j) {
@@ -193,56 +196,115 @@ __global__ void __launch_bounds__(kThreads, 4) k_scan(const __grid_constant__ Sc
   };
   load_list(0);
 
-  // one queue round: advance every queued survivor by one step
-  auto queue_round = [&](float tau) {
-    const int nq_ = qcnt;
-    int newc = 0;
-    constexpr int NB = 4;  // 8-entry batches per sub-round
-    for (int base = 0; base < nq_; base += 8 * NB) {
-      QEntry e[NB];
-      bool val[NB];
-      float4 v[NB][DD];
+  // finished candidate -> CTA top-K
+  auto finish = [&](bool fin, float P, int32_t row) {
+    unsigned long long key = kKeyInf;
+    if (fin && c == 0) {
+      key = make_key(P, (uint32_t)p.row_id[row]);
+      c_dims += D;
+      ++c_surv;
+    }
+    topk_insert(key, sh, topk, K, sB, lane);
+  };
+
+  // One memory round trip: stage 1 of an optional tile (rows row0..row0+nr) and up to
+  // NB*8 queued survivors advanced by up to LA blocks (1 step for fresh survivors, LA blocks
+  // for older ones or when draining), all loads issued before any arithmetic.
+  auto round = [&](float tau, bool has_tile, int64_t row0, int nr, bool drain) {
+    // ---- issue loads
+    float4 tv[NI][DD];
+    if (has_tile) {
 #pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const int idx = base + i * 8 + g;
-        val[i] = idx < nq_;
-        e[i] = val[i] ? queue[idx] : QEntry{0, 0.f, 0.f, 0};
+      for (int i = 0; i < NI; ++i)
 #pragma unroll
         for (int bb = 0; bb < DD; ++bb)
-          v[i][bb] = val[i] ? ldg4(lay + (((int64_t)(e[i].step * DD + bb) * n + e[i].row) << 4) + c * 4)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const int st = e[i].step;  // 0-based index of the step being added
-        const float s = step_sum<DD>(v[i], qs + st * 16 * DD, c);
-        float phi, plo, err;
-        two_sum(e[i].phi, s, phi, err);
-        plo = e[i].plo + err;
-        const int ns = st + 1;
-        const bool fin = val[i] && ns == nsteps;
-        const float P = phi + plo;
-        bool prune = false;
-        if (val[i] && !fin) prune = fmaf(p.m1[ns - 1], P, p.beta[ns - 1]) > tau;
-        const bool keep = val[i] && !fin && !prune;
-        const unsigned km = __ballot_sync(0xffffffffu, keep && c == 0);
-        if (keep && c == 0) {
-          const int pos = newc + __popc(km & ((1u << lane) - 1));
-          queue[pos] = QEntry{e[i].row, phi, plo, ns};
-        }
-        newc += __popc(km);
-        if (c == 0) {
-          if (prune) { c_dims += (unsigned long long)ns * DD * 16; atomicAdd(&sh.pruned[ns], 1u); }
-          if (fin) { c_dims += D; ++c_surv; }
-        }
-        unsigned long long key = kKeyInf;
-        if (fin && c == 0) key = make_key(P, (uint32_t)p.row_id[e[i].row]);
-        topk_insert(key, sh, topk, K, sB, lane);
-      }
-      __syncwarp();
+          tv[i][bb] = (i * 8 + g < nr) ? ldg4(lay + (((int64_t)bb * n + row0 + i * 8 + g) << 4) + c * 4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    qcnt = newc;
+    const int qn = min(tail - head, NB * 8);
+    QEntry e[NB];
+    int want[NB];
+    float4 qv[NB][LA];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int idx = i * 8 + g;
+      const bool val = idx < qn;
+      e[i] = val ? ring[(head + idx) & (kQCap - 1)] : QEntry{0, 0.f, 0.f, nblk};
+      const int rem = nblk - e[i].step;  // .step = blocks done
+      want[i] = (drain || e[i].step > DD) ? LA : DD;
+      want[i] = min(want[i], rem);
+#pragma unroll
+      for (int s = 0; s < LA; ++s)
+        qv[i][s] = (s < want[i]) ? ldg4(lay + (((int64_t)(e[i].step + s) * n + e[i].row) << 4) + c * 4)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    head += qn;
+    __syncwarp();
+    // ---- stage 1 of the tile
+    if (has_tile) {
+      if (lane == 0) c_tested += nr;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const bool val = i * 8 + g < nr;
+        const float s = step_sum<DD>(tv[i], qs, c);
+        const int32_t row = (int32_t)(row0 + i * 8 + g);
+        if (nsteps == 1) {
+          finish(val, s, row);
+          continue;
+        }
+        const bool prune = val && fmaf(p.m1[0], s, p.beta[0]) > tau;
+        const bool keep = val && !prune;
+        const unsigned km = __ballot_sync(0xffffffffu, keep && c == 0);
+        if (keep && c == 0) ring[(tail + __popc(km & ((1u << lane) - 1))) & (kQCap - 1)] = QEntry{row, s, 0.f, DD};
+        tail += __popc(km);
+        if (prune && c == 0) { c_dims += DD * 16; atomicAdd(&sh.pruned[1], 1u); }
+      }
+    }
+    // ---- queued survivors
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const bool val = i * 8 + g < qn;
+      float phi = e[i].phi, plo = e[i].plo, acc = 0.f;
+      int blk = e[i].step;
+      bool alive = val, fin = false;
+#pragma unroll
+      for (int s = 0; s < LA; ++s) {
+        const bool act = alive && s < want[i];
+        // block sum (all lanes take part in the shuffles)
+        const float4 qq = *reinterpret_cast<const float4*>(qs + min(blk, nblk - 1) * 16 + c * 4);
+        float t = qv[i][s].x - qq.x, bs = t * t;
+        t = qv[i][s].y - qq.y; bs = fmaf(t, t, bs);
+        t = qv[i][s].z - qq.z; bs = fmaf(t, t, bs);
+        t = qv[i][s].w - qq.w; bs = fmaf(t, t, bs);
+        bs += __shfl_xor_sync(0xffffffffu, bs, 1);
+        bs += __shfl_xor_sync(0xffffffffu, bs, 2);
+        if (act) {
+          acc += bs;
+          ++blk;
+          if (blk % DD == 0) {  // step boundary: compensated add, then the classifier
+            float err;
+            two_sum(phi, acc, phi, err);
+            plo += err;
+            acc = 0.f;
+            const int ns = blk / DD;
+            if (ns == nsteps) {
+              fin = true;
+              alive = false;
+            } else if (fmaf(p.m1[ns - 1], phi + plo, p.beta[ns - 1]) > tau) {
+              alive = false;
+              if (c == 0) { c_dims += (unsigned long long)blk * 16; atomicAdd(&sh.pruned[ns], 1u); }
+            }
+          }
+        }
+      }
+      // keep (step boundary reached with lookahead < remaining) -> back to the ring tail
+      const unsigned km = __ballot_sync(0xffffffffu, alive && c == 0);
+      if (alive && c == 0)
+        ring[(tail + __popc(km & ((1u << lane) - 1))) & (kQCap - 1)] = QEntry{e[i].row, phi, plo, blk};
+      tail += __popc(km);
+      finish(fin, phi + plo, e[i].row);
+    }
+    __syncwarp();
   };
 
   int64_t e_lo = 0, e_hi_raw = p.c0;
@@ -251,7 +313,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_scan(const __grid_constant__ Sc
     const int64_t e_hi = e_hi_raw < L ? e_hi_raw : L;
     ++n_epochs;
     const float tau = sh.tau;
-    const bool full = !p.prune || !(tau < INFINITY);
     int t = 0;
     while (cj < p.nprobe) {
       const int64_t seg_lo = e_lo > cpos ? e_lo : cpos;
@@ -259,68 +320,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_scan(const __grid_constant__ Sc
       for (int64_t r = seg_lo; r < seg_hi; r += TR, ++t) {
         if ((t % kWarps) != warp) continue;
         const int nr = (int)(seg_hi - r < TR ? seg_hi - r : TR);
-        const int64_t row0 = cstart + (r - cpos);
-        if (lane == 0) c_tested += nr;
-        if (full) {
-          float phi[NI], plo[NI];
-#pragma unroll
-          for (int i = 0; i < NI; ++i) { phi[i] = 0.f; plo[i] = 0.f; }
-          for (int st = 0; st < nsteps; ++st) {
-            float4 v[NI][DD];
-#pragma unroll
-            for (int i = 0; i < NI; ++i)
-#pragma unroll
-              for (int bb = 0; bb < DD; ++bb)
-                v[i][bb] = (i * 8 + g < nr)
-                               ? ldg4(lay + (((int64_t)(st * DD + bb) * n + row0 + i * 8 + g) << 4) + c * 4)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-              const float s = step_sum<DD>(v[i], qs + st * 16 * DD, c);
-              float err;
-              if (st == 0) { phi[i] = s; plo[i] = 0.f; }
-              else { two_sum(phi[i], s, phi[i], err); plo[i] += err; }
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < NI; ++i) {
-            const bool val = i * 8 + g < nr;
-            unsigned long long key = kKeyInf;
-            if (val && c == 0) {
-              key = make_key(phi[i] + plo[i], (uint32_t)p.row_id[row0 + i * 8 + g]);
-              c_dims += D;
-              ++c_surv;
-            }
-            topk_insert(key, sh, topk, K, sB, lane);
-          }
-        } else {
-          while (qcnt + TR > kQCap) queue_round(tau);
-          float4 v[NI][DD];
-#pragma unroll
-          for (int i = 0; i < NI; ++i)
-#pragma unroll
-            for (int bb = 0; bb < DD; ++bb)
-              v[i][bb] = (i * 8 + g < nr)
-                             ? ldg4(lay + (((int64_t)bb * n + row0 + i * 8 + g) << 4) + c * 4)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int i = 0; i < NI; ++i) {
-            const bool val = i * 8 + g < nr;
-            const float s = step_sum<DD>(v[i], qs, c);
-            // nsteps >= 2 here (nsteps == 1 implies !prune, i.e. the full path)
-            const bool prune = val && fmaf(p.m1[0], s, p.beta[0]) > tau;
-            const bool keep = val && !prune;
-            const unsigned km = __ballot_sync(0xffffffffu, keep && c == 0);
-            if (keep && c == 0) {
-              const int pos = qcnt + __popc(km & ((1u << lane) - 1));
-              queue[pos] = QEntry{(int32_t)(row0 + i * 8 + g), s, 0.f, 1};
-            }
-            qcnt += __popc(km);
-            if (prune && c == 0) { c_dims += DD * 16; atomicAdd(&sh.pruned[1], 1u); }
-          }
-          __syncwarp();
-          if (qcnt > 0) queue_round(tau);
-        }
+        while (tail - head > kQCap - TR - NB * 8) round(tau, false, 0, 0, false);
+        round(tau, true, cstart + (r - cpos), nr, false);
       }
       if (cpos + clen <= e_hi) {
         cpos += clen;
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scan(const __grid_constant__ Sc
         break;
       }
     }
-    while (qcnt > 0) queue_round(tau);
+    while (tail > head) round(tau, false, 0, 0, true);
     __syncthreads();
     if (tid == 0) sh.tau = (sh.n == K) ? __uint_as_float((unsigned)(sh.kth >> 32)) : INFINITY;
     __syncthreads();
