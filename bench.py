@@ -110,7 +110,7 @@ def run_dade(args):
     if world > 1:
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
-    from paper_2404_16322_b200 import Index, build
+    from paper_2404_16322_b200 import Index, build, sharded
     if rank == 0:
         build.build()
     if world > 1:
@@ -133,19 +133,13 @@ def run_dade(args):
     Qd = torch.from_numpy(Q).to(dev)
     Qcd = torch.from_numpy(Qc).to(dev)
     K, dd = cfg.k, cfg.delta_d
-    lo, hi = rank * cfg.n // world, (rank + 1) * cfg.n // world
+    lo, hi = rank * cfg.n // world, (rank + 1) * cfg.n // world  # == sharded.shard_range
 
     # ---- build (replicated artefacts are deterministic: identical on every rank)
     t0 = time.time()
     full = Index(cfg.d, local, stream)
     if world > 1:  # a0 over the sharded base: fp64 partial moments + NCCL all-reduce
-        s, c = full.pca_mean_partial(Xd[lo:hi].contiguous(), lo, cfg.n)
-        t = torch.tensor(np.r_[s, c], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        mean = (t[:-1] / t[-1]).cpu().numpy(); cnt = int(t[-1].item())
-        cov = torch.from_numpy(full.pca_cov_partial(Xd[lo:hi].contiguous(), lo, cfg.n, mean)).to(dev)
-        dist.all_reduce(cov)
-        full.set_rotation_from_cov(mean, cov.cpu().numpy(), cnt)
+        sharded.fit_rotation_sharded(full, Xd[lo:hi].contiguous(), lo, cfg.n)
     else:
         full.fit_rotation(Xd)
     torch.cuda.synchronize()
@@ -175,15 +169,12 @@ def run_dade(args):
 
     ids = torch.empty((cfg.nq, K), dtype=torch.int64, device=dev)
     dists = torch.empty((cfg.nq, K), dtype=torch.float32, device=dev)
-    g_ids = torch.empty((world, cfg.nq, K), dtype=torch.int64, device=dev) if world > 1 else None
-    g_d = torch.empty((world, cfg.nq, K), dtype=torch.float32, device=dev) if world > 1 else None
+
 
     def step(nprobe, stats=False):
         r = ix.search(Qd, K, nprobe, dd, ALPHA, ids=ids, dists=dists, stats=stats)
         if world > 1:  # a9: NCCL all-gather of the local top-K + merge kernel
-            dist.all_gather_into_tensor(g_ids.view(-1), ids.view(-1))
-            dist.all_gather_into_tensor(g_d.view(-1), dists.view(-1))
-            out = ix.merge_topk(g_ids, g_d)
+            out = ix.merge_topk(sharded._all_gather(ids), sharded._all_gather(dists))
             return out, (r[2] if stats else None)
         return (ids, dists), (r[2] if stats else None)
 

@@ -36,7 +36,7 @@ struct dade_index {
   DBuf<float> qrot, dmat, qbuf;
   DBuf<int32_t> probes, cand, idx32;
   DBuf<double> d64;
-  DBuf<int> flag;
+  DBuf<int> flag, work;
   DBuf<unsigned long long> counters;
   DBuf<int64_t> ids_tmp;
   DBuf<float> dists_tmp;
@@ -219,6 +219,9 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS), st));
     p.counters = x->counters.p;
   }
+  x->work.reserve(1);
+  DADE_CK(cudaMemsetAsync(x->work.p, 0, sizeof(int), st));
+  p.work_counter = x->work.p;
   launch_scan(p, st);
   if (stats) {
     DADE_CK(cudaEventRecord(x->ev[3], st));
@@ -267,7 +270,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->R_d.release(); x->mean_d.release(); x->cent.release(); x->layout.release();
   x->off_d.release(); x->row_id_d.release(); x->qrot.release(); x->dmat.release();
   x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
-  x->d64.release(); x->flag.release(); x->counters.release(); x->ids_tmp.release();
+  x->d64.release(); x->flag.release(); x->work.release(); x->counters.release(); x->ids_tmp.release();
   x->dists_tmp.release();
   for (auto& e : x->ev)
     if (e) cudaEventDestroy(e);

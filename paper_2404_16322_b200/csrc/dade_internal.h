@@ -101,6 +101,7 @@ struct ScanParams {
   int64_t* out_ids;
   float* out_d;
   unsigned long long* counters;  // [0]=tested [1]=survivors [2]=dims [3]=max epochs [4..4+64) pruned_at_step
+  int* work_counter;             // zeroed before the launch; persistent warps take queries from it
 };
 void launch_scan(const ScanParams& p, cudaStream_t st);
 // merge.cu

@@ -1,0 +1,63 @@
+"""Multi-GPU plumbing for the DADE path.
+
+The database is sharded by contiguous global-id ranges, one shard per rank (one process per GPU).
+Replicated state (μ, R, centroids, calibration) is computed from fp64 partials all-reduced over
+the process group; a search runs on every shard and the local top-K lists are combined by an
+all-gather followed by the library's merge kernel (`dade_merge_topk`). The collective is NCCL
+(`torch.distributed`, backend "nccl") on GPUs; the same code runs over gloo in the CPU tests.
+
+`engine` is the per-shard object: `paper_2404_16322_b200.Index` in production. It must provide
+search(Q, K, nprobe, delta_d, alpha) -> (ids, dists), merge_topk(ids[S,nq,K], dists[S,nq,K]),
+pca_mean_partial / pca_cov_partial / set_rotation_from_cov.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Rows [lo, hi) owned by `rank`: contiguous id ranges, sizes differing by at most 1."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+def _all_gather(t, group=None):
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out.view(-1), t.contiguous().view(-1), group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), t.contiguous(), group=group)
+    return out
+
+
+def fit_rotation_sharded(engine, X_shard, id_base: int, n_total: int, sample_size: int = 0, group=None):
+    """a0 over a sharded base: fp64 sum and count of the owned strided-sample rows, all-reduce,
+    mean; fp64 centred cross products, all-reduce; every rank then runs the same eigensolve."""
+    import torch
+    import torch.distributed as dist
+    dev = X_shard.device if X_shard is not None and hasattr(X_shard, "device") else torch.device("cpu")
+    s, c = engine.pca_mean_partial(X_shard, id_base, n_total, sample_size)
+    t = torch.tensor(np.r_[s, c], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, group=group)
+    t = t.cpu().numpy()
+    cnt = int(round(t[-1]))
+    mean = t[:-1] / cnt
+    cov = torch.from_numpy(engine.pca_cov_partial(X_shard, id_base, n_total, mean, sample_size)).to(dev)
+    dist.all_reduce(cov, group=group)
+    engine.set_rotation_from_cov(mean, cov.cpu().numpy(), cnt)
+    return mean, cnt
+
+
+class ShardedSearch:
+    """search() on this rank's shard, then all-gather of the local top-K and the merge (a9)."""
+
+    def __init__(self, engine, group=None):
+        self.engine, self.group = engine, group
+
+    def search(self, Q, K: int, nprobe: int, delta_d: int, significance: float):
+        ids, dists = self.engine.search(Q, K, nprobe, delta_d, significance)[:2]
+        g_ids = _all_gather(ids, self.group)
+        g_d = _all_gather(dists, self.group)
+        return self.engine.merge_topk(g_ids, g_d)

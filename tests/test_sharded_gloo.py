@@ -1,0 +1,107 @@
+"""World-size-2 gloo tests of the multi-rank path on CPU (no GPU): shard ranges, the PCA
+all-reduce, and the all-gather + merge of local top-K lists. The per-shard engine here is the
+oracle (test infrastructure); in production it is the C-ABI library on each GPU."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from datagen import synth
+from oracle import dade_oracle as O
+from paper_2404_16322_b200 import sharded
+
+
+class OracleEngine:
+    """Per-shard engine over the oracle (CPU tensors), same interface as dade.Index."""
+
+    def __init__(self, X, id_base, centroids=None, mean=None, R=None):
+        self.X, self.id_base = X, id_base
+        self.idx = None if centroids is None else O.build_index(X, centroids, mean, R, id_base=id_base)
+
+    def pca_mean_partial(self, X, id_base, n_total, sample_size=0):
+        ns = min(n_total, 1_000_000) if sample_size <= 0 else min(n_total, sample_size)
+        g = O.strided_ids(n_total, ns)
+        mine = g[(g >= id_base) & (g < id_base + len(self.X))] - id_base
+        return self.X[mine].astype(np.float64).sum(axis=0), len(mine)
+
+    def pca_cov_partial(self, X, id_base, n_total, mean, sample_size=0):
+        ns = min(n_total, 1_000_000) if sample_size <= 0 else min(n_total, sample_size)
+        g = O.strided_ids(n_total, ns)
+        Y = self.X[g[(g >= id_base) & (g < id_base + len(self.X))] - id_base].astype(np.float64) - mean
+        return Y.T @ Y
+
+    def set_rotation_from_cov(self, mean, cov, cnt):
+        lam, V = np.linalg.eigh(cov / cnt)
+        self.rot = (mean, lam[::-1])
+
+    def search(self, Q, K, nprobe, dd, alpha):
+        i, d, _ = O.search(self.idx, Q.numpy(), K, nprobe, dd, alpha)
+        return torch.from_numpy(i), torch.from_numpy(d)
+
+    def merge_topk(self, g_ids, g_d):
+        i, d = O.merge_shards([(g_ids[s].numpy(), g_d[s].numpy()) for s in range(g_ids.shape[0])],
+                              g_ids.shape[2])
+        return torch.from_numpy(i), torch.from_numpy(d)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config("c2", n=6000, nlist=24, nq=12)
+        X = synth.base(cfg)
+        Q = synth.queries(cfg)
+        lo, hi = sharded.shard_range(cfg.n, rank, world)
+        # a0 over the sharded base
+        eng = OracleEngine(X[lo:hi], lo)
+        mean, cnt = sharded.fit_rotation_sharded(eng, None, lo, cfg.n, sample_size=3000)
+        om, _, olam = O.fit_rotation(X, sample_size=3000)
+        assert cnt == 3000 and np.allclose(mean, om, rtol=1e-12)
+        assert np.allclose(eng.rot[1], olam, rtol=1e-9)
+        # search on the shard + all-gather + merge == unsharded exact IVF (alpha = 0)
+        mean, R, lam = O.fit_rotation(X)
+        cent = O.kmeans(X, cfg.nlist, iters=2)
+        eng = OracleEngine(X[lo:hi], lo, cent, mean, R)
+        ids, d = sharded.ShardedSearch(eng).search(torch.from_numpy(Q), 10, 5, 16, 0.0)
+        full = O.build_index(X, cent, mean, R)
+        ei, ed = O.exact_ivf(full, X, Q, 10, 5)
+        assert np.array_equal(ids.numpy(), ei), "sharded merge differs from unsharded exact IVF"
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(60)
+    assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_shard_ranges_partition():
+    for n in (1, 7, 100, 1_000_003):
+        for w in (1, 2, 3, 8):
+            rs = [sharded.shard_range(n, r, w) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+            assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
