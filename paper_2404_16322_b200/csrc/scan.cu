@@ -76,9 +76,13 @@ struct TopK {
   int K, n, sel;
   unsigned long long kth;   // K-th key when n == K
 
-  __device__ void insert(unsigned long long key, int lane) {
+  __device__ __forceinline__ void insert(unsigned long long key, int lane) {
     if (n == K && key >= kth) key = kKeyInf;
     if (__ballot_sync(0xffffffffu, key != kKeyInf) == 0) return;
+    merge(key, lane);
+  }
+
+  __device__ __noinline__ void merge(unsigned long long key, int lane) {
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
@@ -281,31 +285,45 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
       __syncwarp();
     };
 
-    int64_t e_lo = 0, e_hi_raw = p.c0;
+    int64_t e_lo = 0, e_hi_raw = p.c0, e_hi = p.c0 < L ? p.c0 : L, r = 0;
     float tau = INFINITY;
+    if (L > 0) ++c_epochs;
     while (e_lo < L) {
-      const int64_t e_hi = e_hi_raw < L ? e_hi_raw : L;
-      ++c_epochs;
-      while (cj < p.nprobe) {
-        const int64_t seg_lo = e_lo > cpos ? e_lo : cpos;
-        const int64_t seg_hi = e_hi < cpos + clen ? e_hi : cpos + clen;
-        for (int64_t r = seg_lo; r < seg_hi; r += TR) {
-          const int nr = (int)(seg_hi - r < TR ? seg_hi - r : TR);
-          while (tail - head > kQCap - TR - NB * 8) round(tau, false, 0, 0, false);
-          round(tau, true, cstart + (r - cpos), nr, false);
-        }
-        if (cpos + clen <= e_hi) {
-          cpos += clen;
-          ++cj;
-          load_list(cj);
-        } else {
-          break;
+      // next action (warp-uniform): a stage-1 tile of the current epoch, a make-room round,
+      // a drain round, or the epoch boundary
+      bool has_tile = false;
+      int64_t row0 = 0;
+      int nr = 0;
+      if (tail - head <= kQCap - TR - NB * 8) {
+        while (cj < p.nprobe) {
+          const int64_t lo = r > cpos ? r : cpos;
+          const int64_t hi = e_hi < cpos + clen ? e_hi : cpos + clen;
+          if (lo < hi) {
+            nr = (int)(hi - lo < TR ? hi - lo : TR);
+            row0 = cstart + (lo - cpos);
+            r = lo + nr;
+            has_tile = true;
+            break;
+          }
+          if (cpos + clen <= e_hi) {
+            cpos += clen;
+            ++cj;
+            load_list(cj);
+          } else {
+            break;
+          }
         }
       }
-      while (tail > head) round(tau, false, 0, 0, true);
-      tau = (tk.n == K) ? __uint_as_float((unsigned)(tk.kth >> 32)) : INFINITY;
-      e_lo = e_hi;
-      e_hi_raw *= 2;
+      const bool epoch_done = !has_tile && (r >= e_hi || cj >= p.nprobe);
+      if (!has_tile && epoch_done && tail == head) {  // epoch boundary: refresh tau (R13)
+        tau = (tk.n == K) ? __uint_as_float((unsigned)(tk.kth >> 32)) : INFINITY;
+        e_lo = e_hi;
+        e_hi_raw *= 2;
+        e_hi = e_hi_raw < L ? e_hi_raw : L;
+        if (e_lo < L) ++c_epochs;
+        continue;
+      }
+      round(tau, has_tile, row0, nr, epoch_done);
     }
     const unsigned long long* fin = tk.buf + tk.sel * K;
     for (int i = lane; i < K; i += 32) {
