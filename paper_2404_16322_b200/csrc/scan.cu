@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
       for (int i = 0; i < NB; ++i) {
         const int idx = i * 8 + g;
         e[i] = idx < qn ? ring[(head + idx) & (kQCap - 1)] : QEntry{0, 0.f, 0.f, nblk};
-        want[i] = min((drain || e[i].blk > DD) ? LA : DD, nblk - e[i].blk);
+        want[i] = min((drain || e[i].blk > DD) ? LA : (DD < LA ? DD : LA), nblk - e[i].blk);
 #pragma unroll
         for (int s = 0; s < LA; ++s)
           qv[i][s] = (s < want[i]) ? ldg4(lay + (((int64_t)(e[i].blk + s) * n + e[i].row) << 4) + c * 4)
@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
         if (lane == 0) c_tested += nr;
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
+          if (i * 8 >= nr) break;  // warp-uniform: ragged tail of a list segment
           const bool val = i * 8 + g < nr;
           const float s = step_sum<DD>(tv[i], qs, c);
           const int32_t row = (int32_t)(row0 + i * 8 + g);
@@ -244,11 +245,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
       }
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        float phi = e[i].phi, plo = e[i].plo, acc = 0.f;
+        if (i * 8 >= qn) break;  // warp-uniform: no queued entries left
+        float phi = e[i].phi, plo = e[i].plo;
         int blk = e[i].blk;
         bool alive = i * 8 + g < qn, fin = false;
+        const int wmax = __reduce_max_sync(0xffffffffu, alive ? want[i] : 0);
 #pragma unroll
         for (int s = 0; s < LA; ++s) {
+          if (s >= wmax) break;  // warp-uniform
           const bool act = alive && s < want[i];
           const float4 qq = *reinterpret_cast<const float4*>(qs + min(blk, nblk - 1) * 16 + c * 4);
           float t = qv[i][s].x - qq.x, bs = t * t;
@@ -258,13 +262,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
           bs += __shfl_xor_sync(0xffffffffu, bs, 1);
           bs += __shfl_xor_sync(0xffffffffu, bs, 2);
           if (act) {
-            acc += bs;
+            float err;  // compensated running sum over blocks (R21)
+            two_sum(phi, bs, phi, err);
+            plo += err;
             ++blk;
-            if (blk % DD == 0) {  // step boundary: compensated add, then the classifier
-              float err;
-              two_sum(phi, acc, phi, err);
-              plo += err;
-              acc = 0.f;
+            if (blk % DD == 0) {  // step boundary: the classifier for d = blk*16
               const int ns = blk / DD;
               if (ns == nsteps) {
                 fin = true;
