@@ -9,15 +9,17 @@
 // candidate stream (R13: [0,4K), [4K,8K), [8K,16K), ...) so the result does not depend on
 // the parallel schedule.
 //
-// B200 mapping: persistent warps, ONE WARP PER QUERY (queries fetched from an
-// atomic counter), so an epoch boundary only waits for the warp's own survivors and never for a
-// CTA barrier. The rotated query, the sorted top-K and a survivor ring live in the warp's slice
-// of shared memory. The database layout is dimension-blocked and list-major (16 dims = one 64-B
-// row per block): the first step of a tile is one contiguous stream, 4 lanes per row, 8 rows per
-// 128-bit load (fully coalesced). Survivors are ballot-compacted into the ring; each round issues
-// the tile's loads AND the next-block gathers of up to 16 queued survivors (with lookahead) before
-// any arithmetic, so one memory round trip serves both. Finished candidates are merged into the
-// warp's sorted top-K (order-independent result).
+// B200 mapping:
+//  * persistent warps, ONE WARP PER QUERY (queries taken from an atomic counter): an epoch
+//    boundary waits only for the warp's own survivors, never for a CTA barrier;
+//  * the first step of every candidate is STREAMED with TMA bulk copies (cp.async.bulk, one
+//    elected lane, mbarrier completion) into a per-warp shared-memory ring of tiles, issued
+//    kStages tiles ahead of consumption (across list and epoch boundaries: the data does not
+//    depend on tau). The dimension-blocked, list-major layout makes every tile one contiguous
+//    block-row range (64 B per row per 16 dims);
+//  * survivors of a step are ballot-compacted into a per-warp ring; their next blocks are
+//    gathered with 128-bit loads, 4 lanes per 64-B row, several blocks of lookahead per round;
+//  * finished candidates are merged into the warp's sorted top-K (order-independent result).
 #include <cfloat>
 #include <cstdint>
 
@@ -28,8 +30,9 @@ namespace dade {
 namespace {
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int kMinBlocks = 4;
-constexpr int kQCap = 128;  // per-warp survivor ring capacity (power of two)
+constexpr int kMinBlocks = 3;
+constexpr int kQCap = 128;        // per-warp survivor ring capacity (power of two)
+constexpr int kStages = 4;        // TMA tile ring depth per warp
 constexpr unsigned long long kKeyInf = ~0ull;
 
 struct __align__(16) QEntry {
@@ -37,6 +40,37 @@ struct __align__(16) QEntry {
   float phi, plo;
   int32_t blk;  // 16-dim blocks already accumulated
 };
+
+struct TileMeta {
+  int32_t row0, nr, ep, pad;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
 
 __device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
   s = a + b;
@@ -50,23 +84,6 @@ __device__ __forceinline__ unsigned long long make_key(float d, uint32_t id) {
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
-}
-
-// sum over the 4*DD dims this lane holds, reduced over the 4 lanes of the row
-template <int DD>
-__device__ __forceinline__ float step_sum(const float4 (&v)[DD], const float* qs_step, int c) {
-  float s = 0.f;
-#pragma unroll
-  for (int bb = 0; bb < DD; ++bb) {
-    const float4 q = *reinterpret_cast<const float4*>(qs_step + bb * 16 + c * 4);
-    float t = v[bb].x - q.x; s = fmaf(t, t, s);
-    t = v[bb].y - q.y; s = fmaf(t, t, s);
-    t = v[bb].z - q.z; s = fmaf(t, t, s);
-    t = v[bb].w - q.w; s = fmaf(t, t, s);
-  }
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  return s;
 }
 
 // Warp-local top-K (owned by one warp): merge up to 32 keys (one per lane, kKeyInf = none).
@@ -122,33 +139,91 @@ struct TopK {
   }
 };
 
+// Candidate-stream tile iterator (warp-uniform): tiles never cross a list or an epoch boundary.
+struct TileIter {
+  const int32_t* probes;
+  const int32_t* off;
+  int nprobe, cj;
+  int64_t cpos, cstart, clen, r, L, e_hi_raw, e_hi;
+  int ep;
+
+  __device__ void load_list() {
+    if (cj < nprobe) {
+      const int l = probes[cj];
+      cstart = off[l];
+      clen = off[l + 1] - cstart;
+    } else {
+      cstart = 0;
+      clen = 0;
+    }
+  }
+  __device__ void init(const int32_t* pr, const int32_t* of, int np, int64_t L_, int64_t c0) {
+    probes = pr; off = of; nprobe = np; cj = 0; cpos = 0; r = 0; L = L_;
+    e_hi_raw = c0; e_hi = c0 < L ? c0 : L; ep = 0;
+    load_list();
+  }
+  // next tile of at most TR rows; returns false at the end of the stream
+  __device__ bool next(int TR, int32_t& row0, int& nr, int& epoch) {
+    if (r >= L) return false;
+    if (r >= e_hi) {  // epoch boundary (R13): [0,c0), [c0,2c0), [2c0,4c0), ...
+      ++ep;
+      e_hi_raw *= 2;
+      e_hi = e_hi_raw < L ? e_hi_raw : L;
+    }
+    while (cj < nprobe && cpos + clen <= r) {  // skip exhausted (and empty) lists
+      cpos += clen;
+      ++cj;
+      load_list();
+    }
+    if (cj >= nprobe) return false;
+    const int64_t hi = e_hi < cpos + clen ? e_hi : cpos + clen;
+    const int64_t n_ = hi - r < TR ? hi - r : TR;
+    row0 = (int32_t)(cstart + (r - cpos));
+    nr = (int)n_;
+    epoch = ep;
+    r += n_;
+    return true;
+  }
+};
+
 }  // namespace
 
 template <int DD>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_constant__ ScanParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int D = p.D, K = p.K;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, c = lane & 3;
-  // per-warp smem slice: qs[D] | topk[2K] | sB[32] | ring[kQCap] | pruned[64]
-  const size_t slice = (size_t)D * 4 + (size_t)2 * K * 8 + 32 * 8 + kQCap * sizeof(QEntry) + DADE_MAX_STEPS * 4;
-  unsigned char* base = smem + warp * ((slice + 15) & ~(size_t)15);
-  float* qs = reinterpret_cast<float*>(base);
-  unsigned long long* tkbuf = reinterpret_cast<unsigned long long*>(base + (size_t)D * 4);
+  constexpr int TR = 32;                 // rows per tile: one row per lane
+  constexpr int TB = TR * 64 * DD;       // tile bytes (DD blocks of 32 rows)
+  constexpr int LA = 4;                  // lookahead blocks per queued survivor per round
+  // per-warp smem slice: tiles | mbar | meta | ring | topk[2K] | sB | pruned | qs[D]
+  const size_t slice = (size_t)kStages * TB + kStages * 8 + kStages * sizeof(TileMeta) +
+                       kQCap * sizeof(QEntry) + (size_t)2 * K * 8 + 32 * 8 + DADE_MAX_STEPS * 4 + (size_t)D * 4;
+  unsigned char* base = smem + warp * ((slice + 127) & ~(size_t)127);
+  unsigned char* tiles = base;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
+  TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + kStages);
+  QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
+  unsigned long long* tkbuf = reinterpret_cast<unsigned long long*>(ring + kQCap);
   unsigned long long* sB = tkbuf + 2 * K;
-  QEntry* ring = reinterpret_cast<QEntry*>(sB + 32);
-  unsigned* pruned = reinterpret_cast<unsigned*>(ring + kQCap);
-  for (int j = lane; j < DADE_MAX_STEPS; j += 32) pruned[j] = 0;
+  unsigned* pruned = reinterpret_cast<unsigned*>(sB + 32);
+  float* qs = reinterpret_cast<float*>(pruned + DADE_MAX_STEPS);
 
-  constexpr int TR = 64 / DD;  // rows per stage-1 tile (8 x 128-bit loads per lane)
-  constexpr int NI = TR / 8;   // 8 rows per warp instruction
-  constexpr int LA = 4;        // lookahead slots (blocks) per queued survivor per round
-  constexpr int NB = 2;        // queued-survivor batches (8 each) per round
+  for (int j = lane; j < DADE_MAX_STEPS; j += 32) pruned[j] = 0;
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&mbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
   const int nsteps = p.nsteps;
   const int nblk = D >> 4;
   const int64_t n = p.n;
   const float* lay = p.layout;
-  unsigned long long c_tested = 0, c_surv = 0, c_dims = 0, c_epochs = 0;
+  const bool stats = p.counters != nullptr;
+  unsigned long long c_tested = 0, c_surv = 0, c_dims = 0;  // warp-uniform (lane 0 authoritative)
+  uint32_t phase_bits = 0;
+  const unsigned lt_mask = (1u << lane) - 1;
 
   for (;;) {
     int qi = 0;
@@ -156,7 +231,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
     qi = __shfl_sync(0xffffffffu, qi, 0);
     if (qi >= p.nq) break;
     const int64_t q = qi;
-    __syncwarp();
     for (int j = lane; j < D; j += 32) qs[j] = p.qrot[q * D + j];
     TopK tk{tkbuf, sB, K, 0, 0, kKeyInf};
     const int32_t* probes = p.probes + q * p.nprobe;
@@ -169,181 +243,169 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
     __syncwarp();
 
-    int head = 0, tail = 0;  // ring indices (monotonic), warp-uniform
-    int cj = 0;
-    int64_t cpos = 0, cstart = 0, clen = 0;
-    auto load_list = [&](int j) {
-      if (j < p.nprobe) {
-        const int l = probes[j];
-        cstart = p.off[l];
-        clen = p.off[l + 1] - cstart;
-      } else {
-        cstart = 0;
-        clen = 0;
+    // ------------------------------------------------------------ producer (TMA bulk copies)
+    TileIter prod;
+    prod.init(probes, p.off, p.nprobe, L, p.c0);
+    int issued = 0;
+    auto issue = [&](int slot) {  // warp-uniform call; lane 0 issues
+      int32_t row0;
+      int nr, ep;
+      if (!prod.next(TR, row0, nr, ep)) return false;
+      if (lane == 0) {
+        meta[slot] = TileMeta{row0, nr, ep, 0};
+        const uint32_t bytes = (uint32_t)nr * 64u;
+        mbar_expect_tx(&mbar[slot], bytes * DD);
+#pragma unroll
+        for (int bb = 0; bb < DD; ++bb)
+          bulk_g2s(tiles + slot * TB + bb * TR * 64, lay + (((int64_t)bb * n + row0) << 4), bytes, &mbar[slot]);
       }
+      ++issued;
+      return true;
     };
-    load_list(0);
+    for (int s = 0; s < kStages; ++s)
+      if (!issue(s)) break;
 
+    int head = 0, tail = 0;  // survivor ring (monotonic indices), warp-uniform
+    float tau = INFINITY;
+    int cur_ep = 0, consumed = 0;
+
+    auto push = [&](bool keep, const QEntry& e) {
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (keep) ring[(tail + __popc(km & lt_mask)) & (kQCap - 1)] = e;
+      tail += __popc(km);
+    };
     auto finish = [&](bool fin, float P, int32_t row) {
       unsigned long long key = kKeyInf;
-      if (fin && c == 0) {
-        key = make_key(P, (uint32_t)p.row_id[row]);
-        c_dims += D;
-        ++c_surv;
+      if (fin) key = make_key(P, (uint32_t)p.row_id[row]);
+      if (stats) {
+        const int nf = __popc(__ballot_sync(0xffffffffu, fin));
+        c_surv += nf;
+        c_dims += (unsigned long long)nf * D;
       }
       tk.insert(key, lane);
     };
 
-    // One memory round trip: stage 1 of an optional tile and up to NB*8 queued survivors
-    // advanced by up to LA blocks (one step for fresh survivors; LA blocks for older ones or
-    // when draining), all loads issued before any arithmetic.
-    auto round = [&](float tau, bool has_tile, int64_t row0, int nr, bool drain) {
-      float4 tv[NI][DD];
-      if (has_tile) {
+    // one gather round: up to 32 queued survivors (one per lane) advanced by up to LA blocks
+    auto queue_round = [&](bool drain) {
+      const int qn = min(tail - head, 32);
+      const bool val = lane < qn;
+      QEntry e = val ? ring[(head + lane) & (kQCap - 1)] : QEntry{0, 0.f, 0.f, nblk};
+      const int want = min((drain || e.blk > DD) ? LA : (DD < LA ? DD : LA), nblk - e.blk);
+      float4 v[LA][4];
 #pragma unroll
-        for (int i = 0; i < NI; ++i)
+      for (int s = 0; s < LA; ++s)
 #pragma unroll
-          for (int bb = 0; bb < DD; ++bb)
-            tv[i][bb] = (i * 8 + g < nr) ? ldg4(lay + (((int64_t)bb * n + row0 + i * 8 + g) << 4) + c * 4)
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      const int qn = min(tail - head, NB * 8);
-      QEntry e[NB];
-      int want[NB];
-      float4 qv[NB][LA];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const int idx = i * 8 + g;
-        e[i] = idx < qn ? ring[(head + idx) & (kQCap - 1)] : QEntry{0, 0.f, 0.f, nblk};
-        want[i] = min((drain || e[i].blk > DD) ? LA : (DD < LA ? DD : LA), nblk - e[i].blk);
-#pragma unroll
-        for (int s = 0; s < LA; ++s)
-          qv[i][s] = (s < want[i]) ? ldg4(lay + (((int64_t)(e[i].blk + s) * n + e[i].row) << 4) + c * 4)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+        for (int k = 0; k < 4; ++k)
+          v[s][k] = (s < want) ? ldg4(lay + (((int64_t)(e.blk + s) * n + e.row) << 4) + k * 4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
       head += qn;
       __syncwarp();
-      if (has_tile) {
-        if (lane == 0) c_tested += nr;
+      float phi = e.phi, plo = e.plo;
+      int blk = e.blk;
+      bool alive = val, fin = false;
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
-          if (i * 8 >= nr) break;  // warp-uniform: ragged tail of a list segment
-          const bool val = i * 8 + g < nr;
-          const float s = step_sum<DD>(tv[i], qs, c);
-          const int32_t row = (int32_t)(row0 + i * 8 + g);
-          if (nsteps == 1) {
-            finish(val, s, row);
-            continue;
+      for (int s = 0; s < LA; ++s) {
+        if (alive && s < want) {
+          const float* qb = qs + blk * 16;
+          float bs = 0.f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 qq = *reinterpret_cast<const float4*>(qb + k * 4);
+            float t = v[s][k].x - qq.x; bs = fmaf(t, t, bs);
+            t = v[s][k].y - qq.y; bs = fmaf(t, t, bs);
+            t = v[s][k].z - qq.z; bs = fmaf(t, t, bs);
+            t = v[s][k].w - qq.w; bs = fmaf(t, t, bs);
           }
-          const bool prune = val && fmaf(p.m1[0], s, p.beta[0]) > tau;
-          const bool keep = val && !prune;
-          const unsigned km = __ballot_sync(0xffffffffu, keep && c == 0);
-          if (keep && c == 0) ring[(tail + __popc(km & ((1u << lane) - 1))) & (kQCap - 1)] = QEntry{row, s, 0.f, DD};
-          tail += __popc(km);
-          if (prune && c == 0) { c_dims += DD * 16; atomicAdd(&pruned[1], 1u); }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        if (i * 8 >= qn) break;  // warp-uniform: no queued entries left
-        float phi = e[i].phi, plo = e[i].plo;
-        int blk = e[i].blk;
-        bool alive = i * 8 + g < qn, fin = false;
-        const int wmax = __reduce_max_sync(0xffffffffu, alive ? want[i] : 0);
-#pragma unroll
-        for (int s = 0; s < LA; ++s) {
-          if (s >= wmax) break;  // warp-uniform
-          const bool act = alive && s < want[i];
-          const float4 qq = *reinterpret_cast<const float4*>(qs + min(blk, nblk - 1) * 16 + c * 4);
-          float t = qv[i][s].x - qq.x, bs = t * t;
-          t = qv[i][s].y - qq.y; bs = fmaf(t, t, bs);
-          t = qv[i][s].z - qq.z; bs = fmaf(t, t, bs);
-          t = qv[i][s].w - qq.w; bs = fmaf(t, t, bs);
-          bs += __shfl_xor_sync(0xffffffffu, bs, 1);
-          bs += __shfl_xor_sync(0xffffffffu, bs, 2);
-          if (act) {
-            float err;  // compensated running sum over blocks (R21)
-            two_sum(phi, bs, phi, err);
-            plo += err;
-            ++blk;
-            if (blk % DD == 0) {  // step boundary: the classifier for d = blk*16
-              const int ns = blk / DD;
-              if (ns == nsteps) {
-                fin = true;
-                alive = false;
-              } else if (fmaf(p.m1[ns - 1], phi + plo, p.beta[ns - 1]) > tau) {
-                alive = false;
-                if (c == 0) { c_dims += (unsigned long long)blk * 16; atomicAdd(&pruned[ns], 1u); }
-              }
+          float err;  // compensated running sum over blocks (R21)
+          two_sum(phi, bs, phi, err);
+          plo += err;
+          ++blk;
+          if (blk % DD == 0) {  // step boundary: the classifier for d = blk*16
+            const int ns = blk / DD;
+            if (ns == nsteps) {
+              fin = true;
+              alive = false;
+            } else if (fmaf(p.m1[ns - 1], phi + plo, p.beta[ns - 1]) > tau) {
+              alive = false;
+              if (stats) atomicAdd(&pruned[ns], 1u);
             }
           }
         }
-        const unsigned km = __ballot_sync(0xffffffffu, alive && c == 0);
-        if (alive && c == 0)
-          ring[(tail + __popc(km & ((1u << lane) - 1))) & (kQCap - 1)] = QEntry{e[i].row, phi, plo, blk};
-        tail += __popc(km);
-        finish(fin, phi + plo, e[i].row);
       }
+      if (stats) {
+        // dims of candidates pruned in this round: blk*16 each (warp sum)
+        unsigned long long dp = (val && !alive && !fin) ? (unsigned long long)blk * 16 : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
+        c_dims += dp;
+      }
+      push(alive, QEntry{e.row, phi, plo, blk});
+      finish(fin, phi + plo, e.row);
       __syncwarp();
     };
 
-    int64_t e_lo = 0, e_hi_raw = p.c0, e_hi = p.c0 < L ? p.c0 : L, r = 0;
-    float tau = INFINITY;
-    if (L > 0) ++c_epochs;
-    while (e_lo < L) {
-      // next action (warp-uniform): a stage-1 tile of the current epoch, a make-room round,
-      // a drain round, or the epoch boundary
-      bool has_tile = false;
-      int64_t row0 = 0;
-      int nr = 0;
-      if (tail - head <= kQCap - TR - NB * 8) {
-        while (cj < p.nprobe) {
-          const int64_t lo = r > cpos ? r : cpos;
-          const int64_t hi = e_hi < cpos + clen ? e_hi : cpos + clen;
-          if (lo < hi) {
-            nr = (int)(hi - lo < TR ? hi - lo : TR);
-            row0 = cstart + (lo - cpos);
-            r = lo + nr;
-            has_tile = true;
-            break;
-          }
-          if (cpos + clen <= e_hi) {
-            cpos += clen;
-            ++cj;
-            load_list(cj);
-          } else {
-            break;
-          }
+    // ------------------------------------------------------------ consumer
+    while (consumed < issued) {
+      const int slot = consumed % kStages;
+      mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
+      phase_bits ^= 1u << slot;
+      const TileMeta tm = meta[slot];
+      if (tm.ep != cur_ep) {  // epoch boundary: finish every survivor, then refresh tau (R13)
+        while (tail > head) queue_round(true);
+        tau = (tk.n == K) ? __uint_as_float((unsigned)(tk.kth >> 32)) : INFINITY;
+        cur_ep = tm.ep;
+      }
+      while (tail - head > kQCap - TR) queue_round(false);  // room for this tile's survivors
+      const int nr = tm.nr;
+      const bool val = lane < nr;
+      // stage 1: one row per lane; the 16-B chunk order is rotated per lane so the 8 lanes of
+      // each shared-memory phase hit distinct banks
+      const unsigned char* trow = tiles + slot * TB + lane * 64;
+      float s = 0.f;
+#pragma unroll
+      for (int bb = 0; bb < DD; ++bb) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int ch = (k + lane) & 3;
+          const float4 x = *reinterpret_cast<const float4*>(trow + bb * TR * 64 + ch * 16);
+          const float4 qq = *reinterpret_cast<const float4*>(qs + bb * 16 + ch * 4);
+          float t = x.x - qq.x; s = fmaf(t, t, s);
+          t = x.y - qq.y; s = fmaf(t, t, s);
+          t = x.z - qq.z; s = fmaf(t, t, s);
+          t = x.w - qq.w; s = fmaf(t, t, s);
         }
       }
-      const bool epoch_done = !has_tile && (r >= e_hi || cj >= p.nprobe);
-      if (!has_tile && epoch_done && tail == head) {  // epoch boundary: refresh tau (R13)
-        tau = (tk.n == K) ? __uint_as_float((unsigned)(tk.kth >> 32)) : INFINITY;
-        e_lo = e_hi;
-        e_hi_raw *= 2;
-        e_hi = e_hi_raw < L ? e_hi_raw : L;
-        if (e_lo < L) ++c_epochs;
-        continue;
+      __syncwarp();  // every lane is done reading this slot
+      ++consumed;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(slot);
+      const int32_t row = tm.row0 + lane;
+      if (stats) c_tested += nr;
+      if (nsteps == 1) {
+        finish(val, s, row);
+      } else {
+        const bool prune = val && fmaf(p.m1[0], s, p.beta[0]) > tau;
+        push(val && !prune, QEntry{row, s, 0.f, DD});
+        if (stats) {
+          const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
+          if (lane == 0 && np_) pruned[1] += np_;
+          c_dims += (unsigned long long)np_ * DD * 16;
+        }
       }
-      round(tau, has_tile, row0, nr, epoch_done);
+      if (tail - head >= 16) queue_round(false);
     }
+    while (tail > head) queue_round(true);
+
     const unsigned long long* fin = tk.buf + tk.sel * K;
     for (int i = lane; i < K; i += 32) {
       const unsigned long long key = i < tk.n ? fin[i] : kKeyInf;
       p.out_ids[q * K + i] = key == kKeyInf ? -1 : (int64_t)(uint32_t)(key & 0xffffffffu);
       p.out_d[q * K + i] = key == kKeyInf ? INFINITY : __uint_as_float((unsigned)(key >> 32));
     }
-    if (lane == 0 && p.counters) atomicMax(p.counters + 3, c_epochs);
-    c_epochs = 0;
+    if (lane == 0 && stats) atomicMax(p.counters + 3, (unsigned long long)(L > 0 ? cur_ep + 1 : 0));
     __syncwarp();
   }
-  if (p.counters) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c_tested += __shfl_xor_sync(0xffffffffu, c_tested, o);
-      c_surv += __shfl_xor_sync(0xffffffffu, c_surv, o);
-      c_dims += __shfl_xor_sync(0xffffffffu, c_dims, o);
-    }
+  if (stats) {
     if (lane == 0) {
       atomicAdd(p.counters + 0, c_tested);
       atomicAdd(p.counters + 1, c_surv);
@@ -355,22 +417,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_cons
   }
 }
 
-static size_t scan_smem(int D, int K) {
-  const size_t slice = (size_t)D * 4 + (size_t)2 * K * 8 + 32 * 8 + kQCap * sizeof(QEntry) + DADE_MAX_STEPS * 4;
-  return kWarps * ((slice + 15) & ~(size_t)15);
+static size_t scan_smem(int D, int K, int DD) {
+  const size_t slice = (size_t)kStages * 32 * 64 * DD + kStages * 8 + kStages * sizeof(TileMeta) +
+                       kQCap * sizeof(QEntry) + (size_t)2 * K * 8 + 32 * 8 + DADE_MAX_STEPS * 4 + (size_t)D * 4;
+  return kWarps * ((slice + 127) & ~(size_t)127);
 }
 
 template <int DD>
 static void launch_dd(const ScanParams& p, cudaStream_t st) {
-  const size_t smem = scan_smem(p.D, p.K);
+  const size_t smem = scan_smem(p.D, p.K, DD);
   static int sms = 0;
   if (!sms) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int dev;
     DADE_CK(cudaGetDevice(&dev));
     DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  DADE_REQUIRE(smem <= 96 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory slice too large (D, K)");
+  DADE_REQUIRE(smem <= 200 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory slice too large (D, K)");
   int occ = 0;
   DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD>, kThreads, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;

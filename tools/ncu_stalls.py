@@ -57,3 +57,18 @@ for c, v in tot.most_common(10):
 print("top source lines by samples:")
 for l, v in by_line.most_common(25):
     print(f"   {v:8.0f}  {l}")
+
+# instruction counts per source line
+ie = hdr.index("Instructions Executed") if "Instructions Executed" in hdr else None
+if ie is not None:
+    cnt = collections.Counter()
+    for r in src[i0 + 1:]:
+        if len(r) == len(hdr):
+            try:
+                cnt[r[hdr.index("Source")][:110]] += float(r[ie] or 0)
+            except ValueError:
+                pass
+    tot = sum(cnt.values()) or 1
+    print(f"warp instructions executed by source line (total {tot:.3e}):")
+    for l, v in cnt.most_common(30):
+        print(f"   {100 * v / tot:5.1f}%  {l.strip()}")
