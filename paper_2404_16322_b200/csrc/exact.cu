@@ -194,10 +194,149 @@ __global__ void __launch_bounds__(kSelThreads) k_select_exact(
   }
 }
 
+// Fast path for short rows (probe: n = nlist <= 8192): the row lives in registers; a linear
+// histogram over [min, max] (refined on the boundary bin until few candidates remain) yields a
+// value E >= the k-th smallest d_hat with few elements below it. Every column with
+// d_hat <= E * (1+rho)/(1-rho) is re-ranked exactly (a superset of the certified set).
+constexpr int kSmallThreads = 256;
+constexpr int kBins = 1024;
+constexpr int kSmallCap = 1024;
+
+__device__ __forceinline__ float block_reduce(float v, bool is_max, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, x) : fminf(v, x);
+  }
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  v = red[0];
+  for (int i = 1; i < kSmallThreads / 32; ++i) v = is_max ? fmaxf(v, red[i]) : fminf(v, red[i]);
+  return v;
+}
+
+template <int EPT>
+__global__ void __launch_bounds__(kSmallThreads) k_select_small(
+    const float* __restrict__ dh, int64_t n, int k, const float* __restrict__ A,
+    const float* __restrict__ B, int D, int32_t* __restrict__ out_idx, double* __restrict__ out_d,
+    int* flag) {
+  __shared__ unsigned hist[kBins];
+  __shared__ float red[kSmallThreads / 32];
+  __shared__ Cand cs[kSmallCap];
+  __shared__ unsigned s_cnt, s_bin, s_cum;
+  const int tid = threadIdx.x;
+  const int64_t row = blockIdx.x;
+  float v[EPT];
+  uint32_t inplay = 0;
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int64_t idx = (int64_t)j * kSmallThreads + tid;
+    v[j] = idx < n ? dh[row * n + idx] : INFINITY;
+    if (idx < n) inplay |= 1u << j;
+  }
+  unsigned below = 0;  // elements known to be below the in-play range
+  float E = 0.f;
+  for (int level = 0; level < 4; ++level) {
+    float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+      if (inplay >> j & 1u) { lo = fminf(lo, v[j]); hi = fmaxf(hi, v[j]); }
+    lo = block_reduce(lo, false, red);
+    hi = block_reduce(hi, true, red);
+    if (!(hi > lo)) { E = hi; break; }  // all in-play values equal
+    const float scale = (float)kBins / (hi - lo);
+    for (int i = tid; i < kBins; i += kSmallThreads) hist[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+      if (inplay >> j & 1u) atomicAdd(&hist[min(kBins - 1, (int)((v[j] - lo) * scale))], 1u);
+    __syncthreads();
+    if (tid == 0) {
+      unsigned cum = below;
+      int b = 0;
+      for (; b < kBins; ++b) {
+        if (cum + hist[b] >= (unsigned)k) break;
+        cum += hist[b];
+      }
+      s_bin = (unsigned)b;
+      s_cum = cum;  // elements strictly below bin b
+    }
+    __syncthreads();
+    const int b = (int)s_bin;
+    const unsigned cum = s_cum;
+    const unsigned in_b = hist[b];
+    if (cum + in_b <= kSmallCap / 2 || level == 3) {
+      float e = -INFINITY;  // E = largest in-play value with bin <= b (>= the k-th smallest)
+#pragma unroll
+      for (int j = 0; j < EPT; ++j)
+        if ((inplay >> j & 1u) && min(kBins - 1, (int)((v[j] - lo) * scale)) <= b) e = fmaxf(e, v[j]);
+      E = block_reduce(e, true, red);
+      break;
+    }
+    below = cum;  // refine inside bin b
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+      if ((inplay >> j & 1u) && min(kBins - 1, (int)((v[j] - lo) * scale)) != b) inplay &= ~(1u << j);
+    __syncthreads();
+  }
+  const unsigned tb = thr_bits(E, D);
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  const float* a = A + row * (int64_t)D;
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int64_t idx = (int64_t)j * kSmallThreads + tid;
+    if (idx < n && __float_as_uint(v[j]) <= tb) {
+      const unsigned pos = atomicAdd(&s_cnt, 1u);
+      if (pos < (unsigned)kSmallCap) { cs[pos].c = (int32_t)idx; cs[pos].d = 0.0; }
+    }
+  }
+  __syncthreads();
+  unsigned cnt = s_cnt;
+  if (cnt > (unsigned)kSmallCap) {
+    if (tid == 0) atomicExch(flag, 1);
+    cnt = kSmallCap;
+  }
+  unsigned P = 1;
+  while (P < cnt) P <<= 1;
+  for (unsigned i = tid; i < P; i += kSmallThreads) {
+    if (i < cnt) cs[i].d = exact_sqdist(a, B + (int64_t)cs[i].c * D, D);
+    else { cs[i].d = DBL_MAX; cs[i].c = 0x7fffffff; }
+  }
+  __syncthreads();
+  for (unsigned size = 2; size <= P; size <<= 1)
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      for (unsigned i = tid; i < P / 2; i += kSmallThreads) {
+        const unsigned lo2 = 2 * i - (i & (stride - 1)), hi2 = lo2 + stride;
+        const bool up = (lo2 & size) == 0;
+        const Cand x = cs[lo2], y = cs[hi2];
+        if (cand_less(y, x) == up) { cs[lo2] = y; cs[hi2] = x; }
+      }
+      __syncthreads();
+    }
+  for (int i = tid; i < k; i += kSmallThreads) {
+    const bool ok = (unsigned)i < cnt;
+    out_idx[row * k + i] = ok ? cs[i].c : -1;
+    if (out_d) out_d[row * k + i] = ok ? cs[i].d : DBL_MAX;
+  }
+}
+
 void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const float* A,
                          const float* B, int D, int32_t* out_idx, double* out_d64,
                          int32_t* cand_buf, int cand_cap, int* d_flag, cudaStream_t st) {
   if (m <= 0) return;
+  if (n <= 16 * kSmallThreads && k <= kSmallCap / 2) {
+    k_select_small<16><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag);
+    DADE_CK(cudaGetLastError());
+    return;
+  }
+  if (n <= 32 * kSmallThreads && k <= kSmallCap / 2) {
+    k_select_small<32><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag);
+    DADE_CK(cudaGetLastError());
+    return;
+  }
   static bool attr = false;
   const size_t smem = kSortCap * sizeof(Cand);
   if (!attr) {

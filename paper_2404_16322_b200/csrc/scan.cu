@@ -22,6 +22,7 @@
 //  * finished candidates are merged into the warp's sorted top-K (order-independent result).
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "dade_internal.h"
 
@@ -30,7 +31,6 @@ namespace dade {
 namespace {
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int kMinBlocks = 3;
 constexpr int kQCap = 128;        // per-warp survivor ring capacity (power of two)
 constexpr int kStages = 4;        // TMA tile ring depth per warp
 constexpr unsigned long long kKeyInf = ~0ull;
@@ -188,14 +188,13 @@ struct TileIter {
 
 }  // namespace
 
-template <int DD>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_scan(const __grid_constant__ ScanParams p) {
+template <int DD, int LA, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int D = p.D, K = p.K;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int TR = 32;                 // rows per tile: one row per lane
   constexpr int TB = TR * 64 * DD;       // tile bytes (DD blocks of 32 rows)
-  constexpr int LA = 4;                  // lookahead blocks per queued survivor per round
   // per-warp smem slice: tiles | mbar | meta | ring | topk[2K] | sB | pruned | qs[D]
   const size_t slice = (size_t)kStages * TB + kStages * 8 + kStages * sizeof(TileMeta) +
                        kQCap * sizeof(QEntry) + (size_t)2 * K * 8 + 32 * 8 + DADE_MAX_STEPS * 4 + (size_t)D * 4;
@@ -423,22 +422,42 @@ static size_t scan_smem(int D, int K, int DD) {
   return kWarps * ((slice + 127) & ~(size_t)127);
 }
 
-template <int DD>
-static void launch_dd(const ScanParams& p, cudaStream_t st) {
+template <int DD, int LA, int MINB>
+static void launch_v(const ScanParams& p, cudaStream_t st) {
   const size_t smem = scan_smem(p.D, p.K, DD);
   static int sms = 0;
   if (!sms) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD, LA, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int dev;
     DADE_CK(cudaGetDevice(&dev));
     DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   DADE_REQUIRE(smem <= 200 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory slice too large (D, K)");
   int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD>, kThreads, smem));
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, LA, MINB>, kThreads, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;
   const int need = (p.nq + kWarps - 1) / kWarps;
-  k_scan<DD><<<need < max_blocks ? need : max_blocks, kThreads, smem, st>>>(p);
+  k_scan<DD, LA, MINB><<<need < max_blocks ? need : max_blocks, kThreads, smem, st>>>(p);
+}
+
+// variant (lookahead blocks, min CTAs/SM) selectable for tuning via DADE_SCAN_VARIANT
+static int scan_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DADE_SCAN_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int DD>
+static void launch_dd(const ScanParams& p, cudaStream_t st) {
+  switch (scan_variant()) {
+    case 1: launch_v<DD, 2, 4>(p, st); break;
+    case 2: launch_v<DD, 2, 5>(p, st); break;
+    case 3: launch_v<DD, 4, 3>(p, st); break;
+    default: launch_v<DD, 2, 4>(p, st); break;
+  }
 }
 
 void launch_scan(const ScanParams& p, cudaStream_t st) {
