@@ -12,6 +12,15 @@
 
 using namespace dade;
 
+// A matrix pre-split for the tensor-core distance filter (gemm_tf32.cu): tf32 hi/lo parts in the
+// UMMA tiled layout, fp32 squared norms, and the largest norm (for the error bound).
+struct TcOp {
+  DBuf<float> hi, lo, norm, maxn;
+  int64_t rows = 0;
+  float maxnorm = 0.f;
+  void release() { hi.release(); lo.release(); norm.release(); maxn.release(); rows = 0; }
+};
+
 struct dade_index {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -25,6 +34,7 @@ struct dade_index {
   int nlist = 0;
   int64_t n = 0, id_base = 0;
   DBuf<float> cent, layout;
+  TcOp cent_tc;  // centroids, pre-split for the tensor-core probe filter
   DBuf<int32_t> off_d, row_id_d;
   std::vector<int64_t> off_h, row_id_h;
   std::vector<int32_t> assign_h, pos_of_h;  // pos_of_h[local id] = list-major position
@@ -33,7 +43,8 @@ struct dade_index {
   int calK = 0, n0 = 0, ncls = 0;
   std::vector<double> m1, v;
   // scratch
-  DBuf<float> qrot, dmat, qbuf;
+  DBuf<float> qrot, dmat, qbuf, slack, gmin;
+  TcOp a_tc;  // scratch: query-side operand of the filter GEMM
   DBuf<int32_t> probes, cand, idx32;
   DBuf<double> d64;
   DBuf<int> flag, work;
@@ -93,39 +104,83 @@ void check_finite(dade_index* x, const float* X, int64_t count, const char* what
   DADE_REQUIRE(h == 0, DADE_ERR_NONFINITE, std::string("non-finite value in ") + what);
 }
 
-// Exact k nearest rows of B for every row of A (fp32 tile filter + fp64-certified re-rank).
-// out_idx: device m x k int32 (column index into B); out_d64: device m x k fp64 or null.
+void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_max) {
+  const int D = x->D;
+  const int64_t rp = tc_rows_pad(n);
+  const size_t elems = (size_t)rp * tc_nkc(D) * 32;
+  op.hi.reserve(elems);
+  op.lo.reserve(elems);
+  op.norm.reserve(rp);
+  launch_split_tf32(B, n, D, op.hi.p, op.lo.p, op.norm.p, x->stream);
+  op.rows = n;
+  if (need_max) {
+    op.maxn.reserve(1);
+    launch_max_nonneg(op.norm.p, n, op.maxn.p, x->stream);
+    DADE_CK(cudaMemcpyAsync(&op.maxnorm, op.maxn.p, sizeof(float), cudaMemcpyDeviceToHost, x->stream));
+    DADE_CK(cudaStreamSynchronize(x->stream));
+  }
+}
+
+// Exact k nearest rows of B for every row of A: tensor-core distance filter (tcgen05 kind::tf32,
+// 3-pass split; bop = B pre-split by tc_prepare) with a rigorous absolute error bound, then fp64
+// re-rank of every column inside the certified window (exact.cu). Bit-exact with the fp64
+// sequential-sum definition (R20). out_idx: device m x k int32; out_d64: device m x k or null.
 void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t n, int k,
-               int32_t* out_idx, double* out_d64) {
+               int32_t* out_idx, double* out_d64, const TcOp& bop) {
   const int D = x->D;
   DADE_REQUIRE(k >= 1 && k <= n, DADE_ERR_ARG, "exact_knn: k out of range");
   DADE_REQUIRE(k <= 4096, DADE_ERR_UNSUPPORTED, "exact_knn: k > 4096");
+  DADE_REQUIRE(bop.rows == n, DADE_ERR_STATE, "exact_knn: operand not prepared");
   const int64_t budget = (int64_t)1 << 29;  // floats of d_hat per chunk (2 GiB)
-  int64_t chunk = std::max<int64_t>(1, budget / std::max<int64_t>(n, 1));
-  chunk = std::min<int64_t>(chunk, m);
+  int64_t chunk = std::max<int64_t>(128, budget / std::max<int64_t>(n, 1) / 128 * 128);
   const int cand_cap = 4096;
   if (k > 1 || out_d64) {
     chunk = std::min<int64_t>(chunk, 16384);
-    x->cand.reserve((size_t)chunk * cand_cap);
+    x->cand.reserve((size_t)std::min(chunk, tc_rows_pad(m)) * cand_cap);
   }
+  chunk = std::min<int64_t>(chunk, tc_rows_pad(m));
   x->dmat.reserve((size_t)chunk * n);
+  x->slack.reserve((size_t)chunk);
+  x->gmin.reserve((size_t)chunk * ((n + 31) / 32));
   x->flag.reserve(1);
   DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t mm = std::min(chunk, m - r0);
-    launch_l2_tile(A + r0 * D, mm, B, n, D, x->dmat.p, x->stream);
+    tc_prepare(x, A + r0 * D, mm, x->a_tc, false);
+    const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 256;
+    launch_l2_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
+                 x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr);
+    launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream);
+    if (use_gmin) {
+      launch_select_gmin(x->dmat.p, x->gmin.p, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
+                         out_d64 ? out_d64 + r0 * k : nullptr, x->flag.p, x->slack.p, x->stream);
+      int h = 0;  // rows with > 256 near-tied candidates: redo the chunk with the histogram select
+      DADE_CK(cudaMemcpyAsync(&h, x->flag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
+      DADE_CK(cudaStreamSynchronize(x->stream));
+      if (h != 2) continue;
+      DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+    }
     if (k == 1 && !out_d64)
-      launch_argmin_exact(x->dmat.p, mm, n, A + r0 * D, B, D, out_idx + r0, x->flag.p, x->stream);
+      launch_argmin_exact(x->dmat.p, mm, n, A + r0 * D, B, D, out_idx + r0, x->flag.p, x->stream,
+                          x->slack.p);
     else
       launch_select_exact(x->dmat.p, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
                           out_d64 ? out_d64 + r0 * k : nullptr, x->cand.p, cand_cap, x->flag.p,
-                          x->stream);
+                          x->stream, x->slack.p);
   }
   int h = 0;
   DADE_CK(cudaMemcpyAsync(&h, x->flag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
   DADE_CK(cudaStreamSynchronize(x->stream));
   DADE_REQUIRE(h == 0, DADE_ERR_UNSUPPORTED,
                "exact_knn: more than 4096 near-tied candidates for one row (duplicate points?)");
+}
+
+void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t n, int k,
+               int32_t* out_idx, double* out_d64) {
+  TcOp bop;
+  tc_prepare(x, B, n, bop, true);
+  exact_knn(x, A, m, B, n, k, out_idx, out_d64, bop);
+  bop.release();
 }
 
 void upload_rotation(dade_index* x) {
@@ -190,7 +245,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   if (x->nlist == 1) {
     DADE_CK(cudaMemsetAsync(x->probes.p, 0, sizeof(int32_t) * nq, st));
   } else {
-    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr);
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr, x->cent_tc);
   }
   if (stats) DADE_CK(cudaEventRecord(x->ev[2], st));
   // step table (R4, R5): alpha_s = alpha*delta_d/D, k = clamp(ceil((1-alpha_s)*n0), 1, n0)
@@ -272,6 +327,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
   x->d64.release(); x->flag.release(); x->work.release(); x->counters.release(); x->ids_tmp.release();
   x->dists_tmp.release();
+  x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release();
   for (auto& e : x->ev)
     if (e) cudaEventDestroy(e);
   delete x;
@@ -507,6 +563,7 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
   src_d.release();
   // commit (state unchanged on any earlier error)
   std::swap(x->cent, cent); cent.release();
+  tc_prepare(x, x->cent.p, nlist, x->cent_tc, true);
   std::swap(x->layout, layout); layout.release();
   std::swap(x->off_d, off_d); off_d.release();
   std::swap(x->row_id_d, rid_d); rid_d.release();
@@ -594,7 +651,7 @@ extern "C" dade_status dade_calibrate(dade_index* x, const float* X, const float
   if (!whole) {
     DBuf<int32_t> pd;
     pd.reserve((size_t)nq * nprobe_neg);
-    exact_knn(x, Qc, nq, x->cent.p, x->nlist, nprobe_neg, pd.p, nullptr);
+    exact_knn(x, Qc, nq, x->cent.p, x->nlist, nprobe_neg, pd.p, nullptr, x->cent_tc);
     pr.resize((size_t)nq * nprobe_neg);
     DADE_CK(cudaMemcpyAsync(pr.data(), pd.p, sizeof(int32_t) * pr.size(), cudaMemcpyDeviceToHost, st));
   }
@@ -739,7 +796,7 @@ extern "C" dade_status dade_probe(dade_index* x, const float* Q, int nq, int npr
   DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "no IVF");
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
   DeviceGuard g(x->device);
-  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr);
+  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc);
   API_END
 }
 
@@ -854,6 +911,7 @@ extern "C" dade_status dade_load(dade_index* x, const char* path) {
   x->pos_of_h.assign(n, 0);
   for (int64_t p = 0; p < n; ++p) x->pos_of_h[rid[p] - hdr[4]] = (int32_t)p;
   x->nlist = nlist; x->n = n; x->id_base = hdr[4]; x->has_ivf = true;
+  tc_prepare(x, x->cent.p, nlist, x->cent_tc, true);
   x->has_cal = hdr[5] != 0;
   if (x->has_cal) { x->calK = (int)c[0]; x->n0 = (int)c[1]; x->ncls = (int)c[2]; x->m1 = m1; x->v = v; }
   API_END

@@ -63,10 +63,27 @@ void launch_l2_tile(const float* A, int64_t m, const float* B, int64_t n, int D,
 // *d_flag a nonzero value if a candidate buffer overflowed (caller reports an error).
 void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const float* A,
                          const float* B, int D, int32_t* out_idx, double* out_d64,
-                         int32_t* cand_buf, int cand_cap, int* d_flag, cudaStream_t st);
+                         int32_t* cand_buf, int cand_cap, int* d_flag, cudaStream_t st,
+                         const float* slack = nullptr);
 // Argmin (k = 1) specialisation for assignment: out[i] = argmin_c exact(A[i], B[c]).
 void launch_argmin_exact(const float* d_hat, int64_t m, int64_t n, const float* A, const float* B,
-                         int D, int32_t* out, int* d_flag, cudaStream_t st);
+                         int D, int32_t* out, int* d_flag, cudaStream_t st,
+                         const float* slack = nullptr);
+// gemm_tf32.cu : tensor-core (tcgen05 kind::tf32, 3-pass split) distance filter tiles
+int64_t tc_rows_pad(int64_t rows);
+int tc_nkc(int D);
+float tc_gamma(int D);
+void launch_split_tf32(const float* X, int64_t rows, int D, float* hi, float* lo, float* norm,
+                       cudaStream_t st);
+void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, cudaStream_t st);
+void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
+                  const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
+                  cudaStream_t st, float* gmin = nullptr);
+// warp-per-row exact select using the GEMM's 32-column group minima (k <= ceil(n/32) <= 256)
+void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_t n, int k,
+                        const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
+                        int* d_flag, const float* slack, cudaStream_t st);
+void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st);
 
 // rotate.cu : x~ = R (x - mu) with fp64 accumulation, stored fp32.
 //  rowmajor_out != null: out[p*D + i]; else blocked layout out[(b*n_out + p)*16 + i%16].

@@ -98,6 +98,15 @@ __device__ __forceinline__ unsigned thr_bits(float v, int D) {
   return b == 0x7f800000u ? b : b + 2u;  // two ulps of slack on top of the rounding of T
 }
 
+// absolute window for the tensor-core filter: bits of (v + 2*slack) rounded up
+__device__ __forceinline__ unsigned abs_thr_bits(float v, float slack) {
+  const double T = (double)v + 2.0 * (double)slack;
+  const float tf = (float)T;
+  if (!(tf >= 0.f)) return 0xffffffffu;
+  const unsigned b = __float_as_uint(tf);
+  return b == 0x7f800000u ? b : b + 2u;
+}
+
 struct Cand {
   double d;
   int32_t c;
@@ -113,7 +122,7 @@ constexpr int kSortCap = 4096;
 __global__ void __launch_bounds__(kSelThreads) k_select_exact(
     const float* __restrict__ dh, int64_t n, int k, const float* __restrict__ A,
     const float* __restrict__ B, int D, int32_t* __restrict__ out_idx, double* __restrict__ out_d,
-    int32_t* __restrict__ cand_buf, int cand_cap, int* flag) {
+    int32_t* __restrict__ cand_buf, int cand_cap, int* flag, const float* __restrict__ slack) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cand* cs = reinterpret_cast<Cand*>(smem_raw);  // kSortCap entries
   __shared__ unsigned hist[256];
@@ -146,7 +155,8 @@ __global__ void __launch_bounds__(kSelThreads) k_select_exact(
     mask |= 255u << shift;
     __syncthreads();
   }
-  const unsigned tb = thr_bits(__uint_as_float(s_prefix), D);
+  const unsigned tb = slack ? abs_thr_bits(__uint_as_float(s_prefix), slack[row])
+                           : thr_bits(__uint_as_float(s_prefix), D);
   int32_t* cb = cand_buf + row * (int64_t)cand_cap;
   for (int64_t i = tid; i < n; i += blockDim.x) {
     if (du[i] <= tb) {
@@ -221,7 +231,7 @@ template <int EPT>
 __global__ void __launch_bounds__(kSmallThreads) k_select_small(
     const float* __restrict__ dh, int64_t n, int k, const float* __restrict__ A,
     const float* __restrict__ B, int D, int32_t* __restrict__ out_idx, double* __restrict__ out_d,
-    int* flag) {
+    int* flag, const float* __restrict__ slack) {
   __shared__ unsigned hist[kBins];
   __shared__ float red[kSmallThreads / 32];
   __shared__ Cand cs[kSmallCap];
@@ -253,15 +263,30 @@ __global__ void __launch_bounds__(kSmallThreads) k_select_small(
     for (int j = 0; j < EPT; ++j)
       if (inplay >> j & 1u) atomicAdd(&hist[min(kBins - 1, (int)((v[j] - lo) * scale))], 1u);
     __syncthreads();
-    if (tid == 0) {
-      unsigned cum = below;
-      int b = 0;
-      for (; b < kBins; ++b) {
-        if (cum + hist[b] >= (unsigned)k) break;
-        cum += hist[b];
+    if (tid < 32) {  // warp prefix over 1024 bins: 32 bins per lane
+      constexpr int BPL = kBins / 32;
+      unsigned own = 0;
+#pragma unroll 8
+      for (int i = 0; i < BPL; ++i) own += hist[tid * BPL + i];
+      unsigned inc = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (tid >= o) inc += t;
       }
-      s_bin = (unsigned)b;
-      s_cum = cum;  // elements strictly below bin b
+      const unsigned excl = below + inc - own;
+      const unsigned hit = __ballot_sync(0xffffffffu, excl + own >= (unsigned)k);
+      const int L0 = hit ? __ffs(hit) - 1 : 31;
+      if (tid == L0) {
+        unsigned cum = excl;
+        int b = tid * BPL;
+        for (; b < tid * BPL + BPL - 1; ++b) {
+          if (cum + hist[b] >= (unsigned)k) break;
+          cum += hist[b];
+        }
+        s_bin = (unsigned)b;
+        s_cum = cum;  // elements strictly below bin b
+      }
     }
     __syncthreads();
     const int b = (int)s_bin;
@@ -281,7 +306,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_select_small(
       if ((inplay >> j & 1u) && min(kBins - 1, (int)((v[j] - lo) * scale)) != b) inplay &= ~(1u << j);
     __syncthreads();
   }
-  const unsigned tb = thr_bits(E, D);
+  const unsigned tb = slack ? abs_thr_bits(E, slack[row]) : thr_bits(E, D);
   if (tid == 0) s_cnt = 0;
   __syncthreads();
   const float* a = A + row * (int64_t)D;
@@ -323,17 +348,120 @@ __global__ void __launch_bounds__(kSmallThreads) k_select_small(
   }
 }
 
+// Warp-per-row exact select for the tensor-core filter. E = the k-th smallest of the row's
+// 32-column group minima is >= the k-th smallest d_hat (k groups each hold an element <= E), so
+// every column with d_hat <= E + 2 slack is re-ranked exactly; the certified set is contained.
+constexpr int kGmWarps = 8;
+constexpr int kGmCap = 256;
+
+__device__ __forceinline__ bool cand_less2(double d0, int32_t c0, double d1, int32_t c1) {
+  return d0 < d1 || (d0 == d1 && c0 < c1);
+}
+
+__global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
+    const float* __restrict__ dh, const float* __restrict__ gm, int64_t m, int64_t n, int k,
+    const float* __restrict__ A, const float* __restrict__ B, int D, int32_t* __restrict__ out_idx,
+    double* __restrict__ out_d, int* flag, const float* __restrict__ slack) {
+  __shared__ float sg[kGmWarps][256];
+  __shared__ double cd[kGmWarps][kGmCap];
+  __shared__ int32_t cc[kGmWarps][kGmCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * kGmWarps + w;
+  if (row >= m) return;
+  const int ng = (int)((n + 31) / 32);
+  float* g = sg[w];
+  for (int i = lane; i < 256; i += 32) g[i] = i < ng ? gm[row * ng + i] : INFINITY;
+  __syncwarp();
+  // bitonic sort of the 256 group minima (8 per lane)
+  for (int size = 2; size <= 256; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < 128; i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const float x = g[lo], y = g[hi];
+        if ((y < x) == up) { g[lo] = y; g[hi] = x; }
+      }
+      __syncwarp();
+    }
+  const float E = g[k - 1];
+  const unsigned tb = abs_thr_bits(E, slack[row]);
+  // collect every column inside the window (one coalesced pass over the row)
+  const float* d = dh + row * n;
+  int cnt = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += 128) {
+    const int64_t i = i0 + lane * 4;
+    float4 v = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+    if (i + 3 < n && (n & 3) == 0) v = *reinterpret_cast<const float4*>(d + i);
+    else {
+      if (i + 3 < n) v.w = d[i + 3];
+      if (i < n) v.x = d[i];
+      if (i + 1 < n) v.y = d[i + 1];
+      if (i + 2 < n) v.z = d[i + 2];
+    }
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool in = __float_as_uint(vv[t]) <= tb;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+        if (pos < kGmCap) cc[w][pos] = (int32_t)(i + t);
+      }
+      cnt += __popc(bal);
+    }
+  }
+  if (cnt > kGmCap) {
+    if (lane == 0) atomicExch(flag, 2);  // too many near-ties: caller re-runs the histogram select
+    return;
+  }
+  __syncwarp();
+  const float* a = A + row * (int64_t)D;
+  int P = 1;
+  while (P < cnt) P <<= 1;
+  for (int i = lane; i < P; i += 32) {
+    if (i < cnt) cd[w][i] = exact_sqdist(a, B + (int64_t)cc[w][i] * D, D);
+    else { cd[w][i] = DBL_MAX; cc[w][i] = 0x7fffffff; }
+  }
+  __syncwarp();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < P / 2; i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const double x = cd[w][lo], y = cd[w][hi];
+        const int32_t xc = cc[w][lo], yc = cc[w][hi];
+        if (cand_less2(y, yc, x, xc) == up) { cd[w][lo] = y; cd[w][hi] = x; cc[w][lo] = yc; cc[w][hi] = xc; }
+      }
+      __syncwarp();
+    }
+  for (int i = lane; i < k; i += 32) {
+    const bool ok = i < cnt;
+    out_idx[row * k + i] = ok ? cc[w][i] : -1;
+    if (out_d) out_d[row * k + i] = ok ? cd[w][i] : DBL_MAX;
+  }
+}
+
+void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_t n, int k,
+                        const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
+                        int* d_flag, const float* slack, cudaStream_t st) {
+  if (m <= 0) return;
+  k_select_gmin<<<(unsigned)((m + kGmWarps - 1) / kGmWarps), kGmWarps * 32, 0, st>>>(
+      d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, d_flag, slack);
+  DADE_CK(cudaGetLastError());
+}
+
 void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const float* A,
                          const float* B, int D, int32_t* out_idx, double* out_d64,
-                         int32_t* cand_buf, int cand_cap, int* d_flag, cudaStream_t st) {
+                         int32_t* cand_buf, int cand_cap, int* d_flag, cudaStream_t st,
+                         const float* slack) {
   if (m <= 0) return;
   if (n <= 16 * kSmallThreads && k <= kSmallCap / 2) {
-    k_select_small<16><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag);
+    k_select_small<16><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag, slack);
     DADE_CK(cudaGetLastError());
     return;
   }
   if (n <= 32 * kSmallThreads && k <= kSmallCap / 2) {
-    k_select_small<32><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag);
+    k_select_small<32><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag, slack);
     DADE_CK(cudaGetLastError());
     return;
   }
@@ -345,7 +473,7 @@ void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const 
     attr = true;
   }
   k_select_exact<<<(unsigned)m, kSelThreads, smem, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64,
-                                                         cand_buf, cand_cap, d_flag);
+                                                         cand_buf, cand_cap, d_flag, slack);
   DADE_CK(cudaGetLastError());
 }
 
@@ -353,7 +481,8 @@ void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const 
 __global__ void __launch_bounds__(256) k_argmin_exact(const float* __restrict__ dh, int64_t m,
                                                       int64_t n, const float* __restrict__ A,
                                                       const float* __restrict__ B, int D,
-                                                      int32_t* __restrict__ out) {
+                                                      int32_t* __restrict__ out,
+                                                      const float* __restrict__ slack) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= m) return;
@@ -362,7 +491,7 @@ __global__ void __launch_bounds__(256) k_argmin_exact(const float* __restrict__ 
   for (int64_t i = lane; i < n; i += 32) mn = fminf(mn, d[i]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  const unsigned tb = thr_bits(mn, D);
+  const unsigned tb = slack ? abs_thr_bits(mn, slack[row]) : thr_bits(mn, D);
   const float* a = A + row * (int64_t)D;
   double best = DBL_MAX;
   int32_t bc = 0x7fffffff;
@@ -384,10 +513,10 @@ __global__ void __launch_bounds__(256) k_argmin_exact(const float* __restrict__ 
 }
 
 void launch_argmin_exact(const float* d_hat, int64_t m, int64_t n, const float* A, const float* B,
-                         int D, int32_t* out, int* d_flag, cudaStream_t st) {
+                         int D, int32_t* out, int* d_flag, cudaStream_t st, const float* slack) {
   (void)d_flag;
   if (m <= 0) return;
-  k_argmin_exact<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(d_hat, m, n, A, B, D, out);
+  k_argmin_exact<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(d_hat, m, n, A, B, D, out, slack);
   DADE_CK(cudaGetLastError());
 }
 

@@ -1,0 +1,296 @@
+// Tensor-core distance tiles for the exact IVF probe / assignment / KNN filter (a2, a5, K12).
+//
+//   d_hat(q, c) = max(0, ||q||^2 + ||c||^2 - 2 <q, c>)
+//
+// <q, c> runs on the 5th-generation tensor cores (tcgen05.mma kind::tf32, accumulators in TMEM)
+// in 3-pass split precision: x = x_hi + x_lo with x_hi = tf32(x), x_lo = tf32(x - x_hi), and
+// <q,c> ~ q_hi.c_hi + q_hi.c_lo + q_lo.c_hi (FP32-accurate to ~2^-21). Operand tiles are
+// pre-split into the UMMA canonical K-major no-swizzle layout in global memory, so each
+// (128-row tile, 32-wide K chunk) is one contiguous 16 KB block fetched by a TMA bulk copy
+// (cp.async.bulk + mbarrier). One elected thread issues TMA and MMA; tcgen05.commit releases
+// stages; 4 warps drain TMEM with tcgen05.ld in the epilogue.
+//
+// The result is only a FILTER: |d_hat - d| <= slack(q) = gamma * (||q||^2 + max_c ||c||^2),
+// gamma = 2 (3 Dp + 16) 2^-23 (split error 3 2^-22 |q_j c_j| per term, fp32 accumulation of 3 Dp
+// terms, norm and final roundings, x2 margin). The exact answer is then decided in fp64 over
+// every column with d_hat <= d_hat_(k) + 2 slack (exact.cu), so tensor-core rounding never
+// reaches the output (R20).
+#include <cstdint>
+
+#include "dade_internal.h"
+
+namespace dade {
+
+namespace {
+constexpr int kTM = 128;               // rows per operand tile (M and N tiles)
+constexpr int kKC = 16;                // K elements per chunk (64 B per row)
+constexpr int kSub = kTM * kKC;        // floats per (tile, chunk) block = 8 KB
+constexpr int kSBO = (kKC / 4) * 128;  // bytes between 8-row core-matrix groups
+constexpr int kStageBytes = 4 * kSub * 4;  // A_hi, A_lo, B_hi, B_lo
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// canonical K-major, no swizzle: core matrix = 8 rows x 16 B; LBO (K direction) = 128 B,
+// SBO (8-row groups) = kSBO bytes inside a 128 x kKC block
+__device__ __forceinline__ int64_t tiled_index(int64_t r, int k, int nkc) {
+  const int64_t tile = r / kTM;
+  const int rr = (int)(r % kTM), kc = k / kKC, kk = k % kKC;
+  return (tile * nkc + kc) * kSub + (rr >> 3) * (kSBO / 4) + (kk >> 2) * 32 + (rr & 7) * 4 + (kk & 3);
+}
+
+__global__ void k_split_tf32(const float* __restrict__ X, int64_t rows, int D, int nkc,
+                             float* __restrict__ hi, float* __restrict__ lo, float* __restrict__ norm,
+                             int64_t rows_pad) {
+  // one warp per row: split into (hi, lo) in the tiled layout, fp64 squared norm -> fp32
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows_pad) return;
+  const int Dp = nkc * kKC;
+  double s = 0.0;
+  for (int k = lane; k < Dp; k += 32) {
+    const float x = (r < rows && k < D) ? X[r * D + k] : 0.f;
+    const float h = tf32_rna(x);
+    const float l = tf32_rna(x - h);
+    const int64_t t = tiled_index(r, k, nkc);
+    hi[t] = h;
+    lo[t] = l;
+    s += (double)x * (double)x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) norm[r] = (float)s;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, int c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(const void* smem, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(smem) >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  // base_offset = 0, lbo_mode = 0, layout_type = 0 (SWIZZLE_NONE)
+  return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                          \
+  asm volatile(                                                                                      \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                      \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), \
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), \
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                         \
+      : "r"(taddr))
+
+// One CTA = one 128 x 128 output tile; K = nkc chunks of 32, 2-stage TMA -> MMA pipeline.
+__global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi, const float* __restrict__ Alo,
+                                                  const float* __restrict__ an, const float* __restrict__ Bhi,
+                                                  const float* __restrict__ Blo, const float* __restrict__ bn,
+                                                  int nkc, float* __restrict__ out, int64_t m, int64_t n,
+                                                  int64_t ldo, float* __restrict__ gmin, int64_t ldg) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * kStageBytes);
+  uint64_t* empty = full + 2;
+  uint64_t* accf = full + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(full + 5);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tm = blockIdx.y, tn = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
+    mbar_init(&empty[0], 1); mbar_init(&empty[1], 1);
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (tid == 0) {
+    // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+    auto load = [&](int kc) {
+      const int s = kc & 1;
+      unsigned char* st = sm + s * kStageBytes;
+      mbar_expect_tx(&full[s], kStageBytes);
+      const int64_t ao = (tm * nkc + kc) * kSub, bo = (tn * nkc + kc) * kSub;
+      bulk_g2s(st, Ahi + ao, kSub * 4, &full[s]);
+      bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
+      bulk_g2s(st + 2 * kSub * 4, Bhi + bo, kSub * 4, &full[s]);
+      bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
+    };
+    load(0);
+    if (nkc > 1) load(1);
+    for (int kc = 0; kc < nkc; ++kc) {
+      const int s = kc & 1;
+      mbar_wait(&full[s], (kc >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      unsigned char* st = sm + s * kStageBytes;
+#pragma unroll
+      for (int j = 0; j < kKC / 8; ++j) {  // UMMA_K = 8 for tf32 (32 B of K)
+        const uint64_t ah = umma_desc(st + j * 256, 128, kSBO);
+        const uint64_t al = umma_desc(st + kSub * 4 + j * 256, 128, kSBO);
+        const uint64_t bh = umma_desc(st + 2 * kSub * 4 + j * 256, 128, kSBO);
+        const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
+        mma_tf32(tmem, ah, bh, idesc, (kc | j) != 0);
+        mma_tf32(tmem, ah, bl, idesc, 1);
+        mma_tf32(tmem, al, bh, idesc, 1);
+      }
+      mma_commit(&empty[s]);
+      if (kc + 2 < nkc) {
+        mbar_wait(&empty[s], (kc >> 1) & 1);  // MMAs reading this stage are done
+        load(kc + 2);
+      }
+    }
+    mma_commit(accf);
+  }
+  __syncwarp();
+  mbar_wait(accf, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int64_t row = tm * kTM + warp * 32 + lane;
+  const float a2 = row < m ? an[row] : 0.f;
+#pragma unroll 1
+  for (int cb = 0; cb < kTM / 32; ++cb) {
+    uint32_t r[32];
+    TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + cb * 32, r);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int64_t c0 = tn * kTM + cb * 32;
+    if (gmin && row < m) {  // per-row minimum of this 32-column group (select hint)
+      float mn = INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c0 + j < n) mn = fminf(mn, fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j])));
+      if (c0 < n) gmin[row * ldg + (c0 >> 5)] = mn;
+    }
+    if (row < m) {
+      float* o = out + row * ldo + c0;
+      if (c0 + 32 <= n && (ldo & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bn + c0 + j);
+          float4 v;
+          v.x = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 0]), a2 + b4.x));
+          v.y = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 1]), a2 + b4.y));
+          v.z = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 2]), a2 + b4.z));
+          v.w = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 3]), a2 + b4.w));
+          *reinterpret_cast<float4*>(o + j) = v;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < n) o[j] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j]));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+}
+
+__global__ void k_slack(const float* __restrict__ an, int64_t m, float bmax, float gamma, float* __restrict__ slack) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) slack[i] = gamma * (an[i] + bmax);
+}
+}  // namespace
+
+int64_t tc_rows_pad(int64_t rows) { return (rows + kTM - 1) / kTM * kTM; }
+int tc_nkc(int D) { return (D + kKC - 1) / kKC; }
+
+void launch_split_tf32(const float* X, int64_t rows, int D, float* hi, float* lo, float* norm,
+                       cudaStream_t st) {
+  const int64_t rp = tc_rows_pad(rows);
+  if (rp == 0) return;
+  k_split_tf32<<<(unsigned)((rp + 7) / 8), 256, 0, st>>>(X, rows, D, tc_nkc(D), hi, lo, norm, rp);
+  DADE_CK(cudaGetLastError());
+}
+
+float tc_gamma(int D) {
+  const double u23 = 1.1920928955078125e-07;  // 2^-23
+  return (float)(2.0 * (3.0 * tc_nkc(D) * kKC + 16.0) * u23);
+}
+
+void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, cudaStream_t st) {
+  if (m <= 0) return;
+  k_slack<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(an, m, bmax, tc_gamma(D), slack);
+  DADE_CK(cudaGetLastError());
+}
+
+void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
+                  const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
+                  cudaStream_t st, float* gmin) {
+  if (m <= 0 || n <= 0) return;
+  static bool attr = false;
+  const size_t smem = 2 * kStageBytes + 64;
+  if (!attr) {
+    DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
+  k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), out, m, n, ldo, gmin,
+                                   (n + 31) / 32);
+  DADE_CK(cudaGetLastError());
+}
+
+}  // namespace dade
+
+namespace dade {
+namespace {
+__global__ void k_max_nonneg(const float* __restrict__ v, int64_t n, unsigned* out) {
+  unsigned m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(v[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+}  // namespace
+void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st) {
+  DADE_CK(cudaMemsetAsync(out_dev, 0, sizeof(float), st));
+  if (n <= 0) return;
+  k_max_nonneg<<<592, 256, 0, st>>>(v, n, reinterpret_cast<unsigned*>(out_dev));
+  DADE_CK(cudaGetLastError());
+}
+}  // namespace dade
