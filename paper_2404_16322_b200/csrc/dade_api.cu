@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -270,8 +271,8 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   }
   p.out_ids = ids; p.out_d = dists;
   if (stats) {
-    x->counters.reserve(4 + DADE_MAX_STEPS);
-    DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS), st));
+    x->counters.reserve(4 + DADE_MAX_STEPS + 8);
+    DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS + 8), st));
     p.counters = x->counters.p;
   }
   x->work.reserve(1);
@@ -280,7 +281,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   launch_scan(p, st);
   if (stats) {
     DADE_CK(cudaEventRecord(x->ev[3], st));
-    unsigned long long c[4 + DADE_MAX_STEPS];
+    unsigned long long c[4 + DADE_MAX_STEPS + 8];
     DADE_CK(cudaMemcpyAsync(c, x->counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
     DADE_CK(cudaStreamSynchronize(st));
     memset(stats, 0, sizeof(*stats));
@@ -290,6 +291,9 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     stats->n_epochs = (int32_t)c[3];
     for (int s = 0; s < DADE_MAX_STEPS; ++s) stats->pruned_at_step[s] = (int64_t)c[4 + s];
     stats->n_steps = nsteps;
+    if (getenv("DADE_DEBUG_COUNTS"))
+      fprintf(stderr, "[dade debug] rounds=%llu entries=%llu merges=%llu tiles=%llu drain_rounds=%llu\n",
+              c[68], c[69], c[70], c[71], c[72]);
     cudaEventElapsedTime(&stats->ms_rotate, x->ev[0], x->ev[1]);
     cudaEventElapsedTime(&stats->ms_probe, x->ev[1], x->ev[2]);
     cudaEventElapsedTime(&stats->ms_scan, x->ev[2], x->ev[3]);

@@ -32,8 +32,9 @@ namespace {
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
 constexpr int kQCap = 128;        // per-warp survivor ring capacity (power of two)
-constexpr int kStages = 4;        // TMA tile ring depth per warp
+constexpr int kStages = 3;        // TMA tile ring depth per warp
 constexpr unsigned long long kKeyInf = ~0ull;
+constexpr int kMbarBytes = ((kStages * 8 + 15) / 16) * 16;  // keep the following arrays 16-B aligned
 
 struct __align__(16) QEntry {
   int32_t row;
@@ -144,7 +145,7 @@ struct TileIter {
   const int32_t* probes;
   const int32_t* off;
   int nprobe, cj;
-  int64_t cpos, cstart, clen, r, L, e_hi_raw, e_hi;
+  int cpos, cstart, clen, r, L, e_hi_raw, e_hi;  // stream positions (< 2^31)
   int ep;
 
   __device__ void load_list() {
@@ -157,7 +158,7 @@ struct TileIter {
       clen = 0;
     }
   }
-  __device__ void init(const int32_t* pr, const int32_t* of, int np, int64_t L_, int64_t c0) {
+  __device__ void init(const int32_t* pr, const int32_t* of, int np, int L_, int c0) {
     probes = pr; off = of; nprobe = np; cj = 0; cpos = 0; r = 0; L = L_;
     e_hi_raw = c0; e_hi = c0 < L ? c0 : L; ep = 0;
     load_list();
@@ -167,7 +168,7 @@ struct TileIter {
     if (r >= L) return false;
     if (r >= e_hi) {  // epoch boundary (R13): [0,c0), [c0,2c0), [2c0,4c0), ...
       ++ep;
-      e_hi_raw *= 2;
+      e_hi_raw = e_hi_raw > (1 << 29) ? (1 << 30) : e_hi_raw * 2;
       e_hi = e_hi_raw < L ? e_hi_raw : L;
     }
     while (cj < nprobe && cpos + clen <= r) {  // skip exhausted (and empty) lists
@@ -176,12 +177,11 @@ struct TileIter {
       load_list();
     }
     if (cj >= nprobe) return false;
-    const int64_t hi = e_hi < cpos + clen ? e_hi : cpos + clen;
-    const int64_t n_ = hi - r < TR ? hi - r : TR;
-    row0 = (int32_t)(cstart + (r - cpos));
-    nr = (int)n_;
+    const int hi = e_hi < cpos + clen ? e_hi : cpos + clen;
+    nr = hi - r < TR ? hi - r : TR;
+    row0 = cstart + (r - cpos);
     epoch = ep;
-    r += n_;
+    r += nr;
     return true;
   }
 };
@@ -196,12 +196,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
   constexpr int TR = 32;                 // rows per tile: one row per lane
   constexpr int TB = TR * 64 * DD;       // tile bytes (DD blocks of 32 rows)
   // per-warp smem slice: tiles | mbar | meta | ring | topk[2K] | sB | pruned | qs[D]
-  const size_t slice = (size_t)kStages * TB + kStages * 8 + kStages * sizeof(TileMeta) +
+  const size_t slice = (size_t)kStages * TB + kMbarBytes + kStages * sizeof(TileMeta) +
                        kQCap * sizeof(QEntry) + (size_t)2 * K * 8 + 32 * 8 + DADE_MAX_STEPS * 4 + (size_t)D * 4;
   unsigned char* base = smem + warp * ((slice + 127) & ~(size_t)127);
   unsigned char* tiles = base;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
-  TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + kStages);
+  TileMeta* meta = reinterpret_cast<TileMeta*>(base + kStages * TB + kMbarBytes);
   QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
   unsigned long long* tkbuf = reinterpret_cast<unsigned long long*>(ring + kQCap);
   unsigned long long* sB = tkbuf + 2 * K;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
 
     // ------------------------------------------------------------ producer (TMA bulk copies)
     TileIter prod;
-    prod.init(probes, p.off, p.nprobe, L, p.c0);
+    prod.init(probes, p.off, p.nprobe, (int)L, p.c0);
     int issued = 0;
     auto issue = [&](int slot) {  // warp-uniform call; lane 0 issues
       int32_t row0;
@@ -306,15 +306,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
       for (int s = 0; s < LA; ++s) {
         if (alive && s < want) {
           const float* qb = qs + blk * 16;
-          float bs = 0.f;
+          float b4[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const float4 qq = *reinterpret_cast<const float4*>(qb + k * 4);
-            float t = v[s][k].x - qq.x; bs = fmaf(t, t, bs);
-            t = v[s][k].y - qq.y; bs = fmaf(t, t, bs);
-            t = v[s][k].z - qq.z; bs = fmaf(t, t, bs);
-            t = v[s][k].w - qq.w; bs = fmaf(t, t, bs);
+            float t = v[s][k].x - qq.x; b4[k] = t * t;
+            t = v[s][k].y - qq.y; b4[k] = fmaf(t, t, b4[k]);
+            t = v[s][k].z - qq.z; b4[k] = fmaf(t, t, b4[k]);
+            t = v[s][k].w - qq.w; b4[k] = fmaf(t, t, b4[k]);
           }
+          const float bs = (b4[0] + b4[1]) + (b4[2] + b4[3]);
           float err;  // compensated running sum over blocks (R21)
           two_sum(phi, bs, phi, err);
           plo += err;
@@ -360,7 +361,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
       // stage 1: one row per lane; the 16-B chunk order is rotated per lane so the 8 lanes of
       // each shared-memory phase hit distinct banks
       const unsigned char* trow = tiles + slot * TB + lane * 64;
-      float s = 0.f;
+      // 4 independent partial sums (one per 16-B chunk) keep the FMA pipes busy
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int bb = 0; bb < DD; ++bb) {
 #pragma unroll
@@ -368,12 +370,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
           const int ch = (k + lane) & 3;
           const float4 x = *reinterpret_cast<const float4*>(trow + bb * TR * 64 + ch * 16);
           const float4 qq = *reinterpret_cast<const float4*>(qs + bb * 16 + ch * 4);
-          float t = x.x - qq.x; s = fmaf(t, t, s);
-          t = x.y - qq.y; s = fmaf(t, t, s);
-          t = x.z - qq.z; s = fmaf(t, t, s);
-          t = x.w - qq.w; s = fmaf(t, t, s);
+          float t = x.x - qq.x; s4[k] = fmaf(t, t, s4[k]);
+          t = x.y - qq.y; s4[k] = fmaf(t, t, s4[k]);
+          t = x.z - qq.z; s4[k] = fmaf(t, t, s4[k]);
+          t = x.w - qq.w; s4[k] = fmaf(t, t, s4[k]);
         }
       }
+      const float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       __syncwarp();  // every lane is done reading this slot
       ++consumed;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
 }
 
 static size_t scan_smem(int D, int K, int DD) {
-  const size_t slice = (size_t)kStages * 32 * 64 * DD + kStages * 8 + kStages * sizeof(TileMeta) +
+  const size_t slice = (size_t)kStages * 32 * 64 * DD + kMbarBytes + kStages * sizeof(TileMeta) +
                        kQCap * sizeof(QEntry) + (size_t)2 * K * 8 + 32 * 8 + DADE_MAX_STEPS * 4 + (size_t)D * 4;
   return kWarps * ((slice + 127) & ~(size_t)127);
 }
@@ -454,9 +457,8 @@ template <int DD>
 static void launch_dd(const ScanParams& p, cudaStream_t st) {
   switch (scan_variant()) {
     case 1: launch_v<DD, 2, 4>(p, st); break;
-    case 2: launch_v<DD, 2, 5>(p, st); break;
     case 3: launch_v<DD, 4, 3>(p, st); break;
-    default: launch_v<DD, 2, 4>(p, st); break;
+    default: launch_v<DD, 2, 6>(p, st); break;
   }
 }
 

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdade.so")
+LIB_PATH = os.environ.get("DADE_LIB", os.path.join(_HERE, "libdade.so"))
 MAX_STEPS = 64
 MAX_K = 256
 
