@@ -308,10 +308,13 @@ def run_dade(args):
 
 
 def launches_per_search(cfg, world):
-    # k_rotate + (k_l2_tile + k_select_exact per probe chunk) + k_scan (+ k_merge_topk if sharded)
-    chunk = max(1, (1 << 29) // cfg.nlist)
-    chunks = (cfg.nq + min(chunk, 16384) - 1) // min(chunk, 16384) if cfg.nlist > 1 else 0
-    return 2 + 2 * chunks + (1 if world > 1 else 0)
+    """Kernels of ours per dade_search: k_check_finite, k_rotate, per probe chunk (k_split_tf32,
+    k_l2_tc, k_slack, k_select_gmin, k_select_small fallback over the overflow list), k_scan,
+    (+ k_merge_topk when sharded)."""
+    chunk = max(128, (1 << 29) // cfg.nlist // 128 * 128)
+    chunk = min(chunk, 16384)
+    chunks = (cfg.nq + chunk - 1) // chunk if cfg.nlist > 1 else 0
+    return 2 + 5 * chunks + 1 + (1 if world > 1 else 0)
 
 
 # ============================================================================ CPU oracle legs

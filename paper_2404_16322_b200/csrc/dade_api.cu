@@ -48,7 +48,7 @@ struct dade_index {
   TcOp a_tc;  // scratch: query-side operand of the filter GEMM
   DBuf<int32_t> probes, cand, idx32;
   DBuf<double> d64;
-  DBuf<int> flag, work;
+  DBuf<int> flag, fflag, work, ovf;
   DBuf<unsigned long long> counters;
   DBuf<int64_t> ids_tmp;
   DBuf<float> dists_tmp;
@@ -96,13 +96,27 @@ void need(const void* p, const char* what) {
 }
 
 void check_finite(dade_index* x, const float* X, int64_t count, const char* what) {
-  x->flag.reserve(1);
-  DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
-  launch_check_finite(X, count, x->flag.p, x->stream);
+  x->fflag.reserve(1);
+  DADE_CK(cudaMemsetAsync(x->fflag.p, 0, sizeof(int), x->stream));
+  launch_check_finite(X, count, x->fflag.p, x->stream);
+  int h = 0;
+  DADE_CK(cudaMemcpyAsync(&h, x->fflag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  DADE_REQUIRE(h == 0, DADE_ERR_NONFINITE, std::string("non-finite value in ") + what);
+}
+
+// Errors of the exact selection (candidate buffers overflowed) latch in x->flag and are reported
+// at the next synchronising call.
+void check_knn_flag(dade_index* x) {
+  if (!x->flag.p) return;
   int h = 0;
   DADE_CK(cudaMemcpyAsync(&h, x->flag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
   DADE_CK(cudaStreamSynchronize(x->stream));
-  DADE_REQUIRE(h == 0, DADE_ERR_NONFINITE, std::string("non-finite value in ") + what);
+  if (h != 0) {
+    DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+    if (h == 3) throw Error(DADE_ERR_NONFINITE, "non-finite value in the queries of a previous search");
+    throw Error(DADE_ERR_UNSUPPORTED, "exact selection: more than 4096 near-tied candidates for one row");
+  }
 }
 
 void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_max) {
@@ -127,7 +141,7 @@ void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_ma
 // re-rank of every column inside the certified window (exact.cu). Bit-exact with the fp64
 // sequential-sum definition (R20). out_idx: device m x k int32; out_d64: device m x k or null.
 void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t n, int k,
-               int32_t* out_idx, double* out_d64, const TcOp& bop) {
+               int32_t* out_idx, double* out_d64, const TcOp& bop, bool sync = true) {
   const int D = x->D;
   DADE_REQUIRE(k >= 1 && k <= n, DADE_ERR_ARG, "exact_knn: k out of range");
   DADE_REQUIRE(k <= 4096, DADE_ERR_UNSUPPORTED, "exact_knn: k > 4096");
@@ -143,23 +157,23 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   x->dmat.reserve((size_t)chunk * n);
   x->slack.reserve((size_t)chunk);
   x->gmin.reserve((size_t)chunk * ((n + 31) / 32));
-  x->flag.reserve(1);
-  DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+  if (!x->flag.p) {
+    x->flag.reserve(1);
+    DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+  }
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t mm = std::min(chunk, m - r0);
     tc_prepare(x, A + r0 * D, mm, x->a_tc, false);
-    const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 256;
+    const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 256 && n <= 32 * 256;
     launch_l2_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
                  x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr);
     launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream);
     if (use_gmin) {
+      x->ovf.reserve((size_t)chunk + 1);
       launch_select_gmin(x->dmat.p, x->gmin.p, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
-                         out_d64 ? out_d64 + r0 * k : nullptr, x->flag.p, x->slack.p, x->stream);
-      int h = 0;  // rows with > 256 near-tied candidates: redo the chunk with the histogram select
-      DADE_CK(cudaMemcpyAsync(&h, x->flag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
-      DADE_CK(cudaStreamSynchronize(x->stream));
-      if (h != 2) continue;
-      DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+                         out_d64 ? out_d64 + r0 * k : nullptr, x->flag.p, x->slack.p, x->ovf.p,
+                         x->ovf.p + 1, x->stream);
+      continue;
     }
     if (k == 1 && !out_d64)
       launch_argmin_exact(x->dmat.p, mm, n, A + r0 * D, B, D, out_idx + r0, x->flag.p, x->stream,
@@ -169,11 +183,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
                           out_d64 ? out_d64 + r0 * k : nullptr, x->cand.p, cand_cap, x->flag.p,
                           x->stream, x->slack.p);
   }
-  int h = 0;
-  DADE_CK(cudaMemcpyAsync(&h, x->flag.p, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
-  DADE_CK(cudaStreamSynchronize(x->stream));
-  DADE_REQUIRE(h == 0, DADE_ERR_UNSUPPORTED,
-               "exact_knn: more than 4096 near-tied candidates for one row (duplicate points?)");
+  if (sync) check_knn_flag(x);
 }
 
 void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t n, int k,
@@ -237,6 +247,12 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
       if (!e) DADE_CK(cudaEventCreate(&e));
     DADE_CK(cudaEventRecord(x->ev[0], st));
   }
+  // non-finite queries latch error 3 in the flag (reported at the next synchronising call)
+  if (!x->flag.p) {
+    x->flag.reserve(1);
+    DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), st));
+  }
+  launch_check_finite(Q, (int64_t)nq * D, x->flag.p, st, 3);
   // a4 rotate queries (fp64 accumulation)
   x->qrot.reserve((size_t)nq * D);
   launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
@@ -246,7 +262,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   if (x->nlist == 1) {
     DADE_CK(cudaMemsetAsync(x->probes.p, 0, sizeof(int32_t) * nq, st));
   } else {
-    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr, x->cent_tc);
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr, x->cent_tc, false);
   }
   if (stats) DADE_CK(cudaEventRecord(x->ev[2], st));
   // step table (R4, R5): alpha_s = alpha*delta_d/D, k = clamp(ceil((1-alpha_s)*n0), 1, n0)
@@ -284,6 +300,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     unsigned long long c[4 + DADE_MAX_STEPS + 8];
     DADE_CK(cudaMemcpyAsync(c, x->counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
     DADE_CK(cudaStreamSynchronize(st));
+    check_knn_flag(x);
     memset(stats, 0, sizeof(*stats));
     stats->tested = (int64_t)c[0];
     stats->survivors = (int64_t)c[1];
@@ -329,7 +346,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->R_d.release(); x->mean_d.release(); x->cent.release(); x->layout.release();
   x->off_d.release(); x->row_id_d.release(); x->qrot.release(); x->dmat.release();
   x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
-  x->d64.release(); x->flag.release(); x->work.release(); x->counters.release(); x->ids_tmp.release();
+  x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->ids_tmp.release();
   x->dists_tmp.release();
   x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release();
   for (auto& e : x->ev)
@@ -791,6 +808,7 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   DADE_CK(cudaMemcpyAsync(ids_h, x->ids_tmp.p, sizeof(int64_t) * nq * K, cudaMemcpyDeviceToHost, st));
   DADE_CK(cudaMemcpyAsync(dists_h, x->dists_tmp.p, sizeof(float) * nq * K, cudaMemcpyDeviceToHost, st));
   DADE_CK(cudaStreamSynchronize(st));
+  check_knn_flag(x);
   API_END
 }
 

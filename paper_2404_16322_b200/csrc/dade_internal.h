@@ -82,7 +82,8 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
 // warp-per-row exact select using the GEMM's 32-column group minima (k <= ceil(n/32) <= 256)
 void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_t n, int k,
                         const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
-                        int* d_flag, const float* slack, cudaStream_t st);
+                        int* d_flag, const float* slack, int* ovf_n, int32_t* ovf_rows,
+                        cudaStream_t st);
 void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st);
 
 // rotate.cu : x~ = R (x - mu) with fp64 accumulation, stored fp32.
@@ -124,7 +125,7 @@ void launch_scan(const ScanParams& p, cudaStream_t st);
 // merge.cu
 void launch_merge_topk(const int64_t* ids_in, const float* d_in, int S, int nq, int K,
                        int64_t* ids_out, float* d_out, cudaStream_t st);
-void launch_check_finite(const float* X, int64_t n, int* flag, cudaStream_t st);
+void launch_check_finite(const float* X, int64_t n, int* flag, cudaStream_t st, int code = 1);
 void launch_gather_rows(const float* X, const int32_t* rows, int64_t m, int D, float* out,
                         cudaStream_t st);
 

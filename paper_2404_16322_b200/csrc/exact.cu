@@ -231,13 +231,15 @@ template <int EPT>
 __global__ void __launch_bounds__(kSmallThreads) k_select_small(
     const float* __restrict__ dh, int64_t n, int k, const float* __restrict__ A,
     const float* __restrict__ B, int D, int32_t* __restrict__ out_idx, double* __restrict__ out_d,
-    int* flag, const float* __restrict__ slack) {
+    int* flag, const float* __restrict__ slack, const int32_t* __restrict__ rows,
+    const int* __restrict__ nrows) {
   __shared__ unsigned hist[kBins];
   __shared__ float red[kSmallThreads / 32];
   __shared__ Cand cs[kSmallCap];
   __shared__ unsigned s_cnt, s_bin, s_cum;
   const int tid = threadIdx.x;
-  const int64_t row = blockIdx.x;
+  if (rows && (int)blockIdx.x >= *nrows) return;  // fallback mode: only the listed rows
+  const int64_t row = rows ? rows[blockIdx.x] : blockIdx.x;
   float v[EPT];
   uint32_t inplay = 0;
 #pragma unroll
@@ -361,7 +363,7 @@ __device__ __forceinline__ bool cand_less2(double d0, int32_t c0, double d1, int
 __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
     const float* __restrict__ dh, const float* __restrict__ gm, int64_t m, int64_t n, int k,
     const float* __restrict__ A, const float* __restrict__ B, int D, int32_t* __restrict__ out_idx,
-    double* __restrict__ out_d, int* flag, const float* __restrict__ slack) {
+    double* __restrict__ out_d, int* ovf_n, int32_t* __restrict__ ovf_rows, const float* __restrict__ slack) {
   __shared__ float sg[kGmWarps][256];
   __shared__ double cd[kGmWarps][kGmCap];
   __shared__ int32_t cc[kGmWarps][kGmCap];
@@ -410,8 +412,8 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
       cnt += __popc(bal);
     }
   }
-  if (cnt > kGmCap) {
-    if (lane == 0) atomicExch(flag, 2);  // too many near-ties: caller re-runs the histogram select
+  if (cnt > kGmCap) {  // too many near-ties: the histogram select redoes this row
+    if (lane == 0) ovf_rows[atomicAdd(ovf_n, 1)] = (int32_t)row;
     return;
   }
   __syncwarp();
@@ -443,10 +445,20 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
 
 void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_t n, int k,
                         const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
-                        int* d_flag, const float* slack, cudaStream_t st) {
+                        int* d_flag, const float* slack, int* ovf_n, int32_t* ovf_rows,
+                        cudaStream_t st) {
   if (m <= 0) return;
+  DADE_CK(cudaMemsetAsync(ovf_n, 0, sizeof(int), st));
   k_select_gmin<<<(unsigned)((m + kGmWarps - 1) / kGmWarps), kGmWarps * 32, 0, st>>>(
-      d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, d_flag, slack);
+      d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+  DADE_CK(cudaGetLastError());
+  // device-side fallback (no host round trip): the listed rows only
+  if (n <= 16 * kSmallThreads)
+    k_select_small<16><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag,
+                                                               slack, ovf_rows, ovf_n);
+  else
+    k_select_small<32><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag,
+                                                               slack, ovf_rows, ovf_n);
   DADE_CK(cudaGetLastError());
 }
 
@@ -456,12 +468,14 @@ void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const 
                          const float* slack) {
   if (m <= 0) return;
   if (n <= 16 * kSmallThreads && k <= kSmallCap / 2) {
-    k_select_small<16><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag, slack);
+    k_select_small<16><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag, slack,
+                                                               nullptr, nullptr);
     DADE_CK(cudaGetLastError());
     return;
   }
   if (n <= 32 * kSmallThreads && k <= kSmallCap / 2) {
-    k_select_small<32><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag, slack);
+    k_select_small<32><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag, slack,
+                                                               nullptr, nullptr);
     DADE_CK(cudaGetLastError());
     return;
   }
@@ -521,14 +535,14 @@ void launch_argmin_exact(const float* d_hat, int64_t m, int64_t n, const float* 
 }
 
 // ------------------------------------------------------------------ misc small kernels
-__global__ void k_check_finite(const float* __restrict__ X, int64_t n, int* flag) {
+__global__ void k_check_finite(const float* __restrict__ X, int64_t n, int* flag, int code) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(X[i])) { atomicExch(flag, 1); return; }
+    if (!isfinite(X[i])) { atomicExch(flag, code); return; }
 }
-void launch_check_finite(const float* X, int64_t n, int* flag, cudaStream_t st) {
+void launch_check_finite(const float* X, int64_t n, int* flag, cudaStream_t st, int code) {
   if (n <= 0) return;
-  k_check_finite<<<1184, 256, 0, st>>>(X, n, flag);
+  k_check_finite<<<1184, 256, 0, st>>>(X, n, flag, code);
   DADE_CK(cudaGetLastError());
 }
 

@@ -182,3 +182,13 @@ def test_save_load_roundtrip(sift_small, tmp_path):
     a, b = ix.search(Q, 10, 8, 16, 0.005)
     c, d = iy.search(Q, 10, 8, 16, 0.005)
     assert torch.equal(a, c) and torch.equal(b, d)
+
+
+def test_nonfinite_query_reported(sift_small):
+    cfg, (torch, ix, oidx, X, Xd) = sift_small
+    from paper_2404_16322_b200 import DadeError
+    Q = torch.from_numpy(synth.queries(cfg)[:4]).cuda()
+    Q[1, 3] = float("inf")
+    with pytest.raises(DadeError):
+        ix.search(Q, 10, 4, 16, 0.005, stats=True)   # a synchronising call reports it
+    ix.search(Q[:1].contiguous(), 10, 4, 16, 0.005, stats=True)  # the latch is cleared
