@@ -304,7 +304,10 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     memset(stats, 0, sizeof(*stats));
     stats->tested = (int64_t)c[0];
     stats->survivors = (int64_t)c[1];
-    stats->dims_scanned = (int64_t)c[2];
+    // dims read: a candidate pruned at step s read s*delta_d dims; a survivor read all D
+    int64_t dims = (int64_t)c[1] * D;
+    for (int s = 1; s < DADE_MAX_STEPS; ++s) dims += (int64_t)c[4 + s] * s * (p.dd * 16);
+    stats->dims_scanned = dims;
     stats->n_epochs = (int32_t)c[3];
     for (int s = 0; s < DADE_MAX_STEPS; ++s) stats->pruned_at_step[s] = (int64_t)c[4 + s];
     stats->n_steps = nsteps;

@@ -10,16 +10,22 @@
 // the parallel schedule.
 //
 // B200 mapping:
-//  * persistent warps, ONE WARP PER QUERY (queries taken from an atomic counter): an epoch
-//    boundary waits only for the warp's own survivors, never for a CTA barrier;
-//  * the first step of every candidate is STREAMED with TMA bulk copies (cp.async.bulk, one
-//    elected lane, mbarrier completion) into a per-warp shared-memory ring of tiles, issued
-//    kStages tiles ahead of consumption (across list and epoch boundaries: the data does not
-//    depend on tau). The dimension-blocked, list-major layout makes every tile one contiguous
-//    block-row range (64 B per row per 16 dims);
-//  * survivors of a step are ballot-compacted into a per-warp ring; their next blocks are
-//    gathered with 128-bit loads, 4 lanes per 64-B row, several blocks of lookahead per round;
-//  * finished candidates are merged into the warp's sorted top-K (order-independent result).
+//  * persistent CTAs of ONE WARP, one query at a time (queries taken from an atomic counter):
+//    an epoch boundary waits only for the warp's own survivors, never for other warps;
+//  * the probed lists' (start, length) table and q~ sit in shared memory; the first step of
+//    every candidate is STREAMED with TMA bulk copies (cp.async.bulk, one elected lane,
+//    mbarrier completion) into a ring of tiles, issued kStages tiles ahead of consumption
+//    (across list and epoch boundaries: the data does not depend on tau). The
+//    dimension-blocked, list-major layout makes every tile one contiguous block-row range
+//    (64 B per row per 16 dims);
+//  * survivors of a step are ballot-compacted into a shared-memory ring; their next blocks are
+//    gathered with 128-bit loads (one 64-B row per lane, up to LA blocks per round trip); the
+//    global id of a candidate is fetched in the same round trip as its last block;
+//  * arithmetic is packed FP32x2 (FADD2/FFMA2): a 16-dim block costs 16 packed instructions;
+//    the distance is the fp32 sum of per-block sums, added in block order (R21) — identical
+//    whichever round a block is processed in, so results never depend on the schedule;
+//  * the top-K is REGISTER-RESIDENT: KPL sorted keys (dist_bits << 32 | id) per lane, position
+//    lane*KPL + i; an accepted key is inserted by a warp-wide shift (no shared memory).
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
@@ -29,17 +35,15 @@
 namespace dade {
 
 namespace {
-constexpr int kWarps = 4;
-constexpr int kThreads = kWarps * 32;
-constexpr int kQCap = 128;        // per-warp survivor ring capacity (power of two)
-constexpr int kStages = 3;        // TMA tile ring depth per warp
+constexpr int kQCap = 128;        // survivor ring capacity (power of two)
+constexpr int TR = 32;            // rows per tile: one row per lane
 constexpr unsigned long long kKeyInf = ~0ull;
-constexpr int kMbarBytes = ((kStages * 8 + 15) / 16) * 16;  // keep the following arrays 16-B aligned
 
 struct __align__(16) QEntry {
-  int32_t row;
-  float phi, plo;
-  int32_t blk;  // 16-dim blocks already accumulated
+  int32_t row;   // list-major position
+  float phi;     // partial distance over blocks [0, blk)
+  int32_t blk;   // 16-dim blocks accumulated
+  int32_t pad;
 };
 
 struct TileMeta {
@@ -73,142 +77,140 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-__device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
-  s = a + b;
-  const float bb = s - a;
-  e = (a - (s - bb)) + (b - bb);
+// ---- packed FP32x2 arithmetic (sm_100a FADD2 / FFMA2)
+__device__ __forceinline__ unsigned long long pk(float2 a) {
+  return *reinterpret_cast<unsigned long long*>(&a);
+}
+__device__ __forceinline__ float2 upk(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b,
+                                                   unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Sum over one 16-dim block of (x_i - q_i)^2: 4 packed accumulators, fixed association
+// ((a0 + a1) + (a2 + a3)), then lo + hi. x: 8 packed pairs (registers); q: 16 floats (smem).
+__device__ __forceinline__ float block_sum(const unsigned long long (&x)[8], const float* q) {
+  const ulonglong2* qq = reinterpret_cast<const ulonglong2*>(q);
+  unsigned long long a[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const ulonglong2 qc = qq[c];
+    const unsigned long long t0 = sub2(x[2 * c], qc.x);
+    const unsigned long long t1 = sub2(x[2 * c + 1], qc.y);
+    a[c] = fma2(t1, t1, 0ull);
+    a[c] = fma2(t0, t0, a[c]);
+  }
+  const float2 s = upk(add2(add2(a[0], a[1]), add2(a[2], a[3])));
+  return s.x + s.y;
+}
+
+// Same with the 16-B chunks in a per-lane rotated order (stage 1 reads the tile rotated so the
+// 8 lanes of a shared-memory phase hit distinct banks); q chunk c pairs with x chunk c.
+__device__ __forceinline__ float block_sum_rot(const unsigned long long (&x)[8], const float* const (&q)[4]) {
+  unsigned long long a[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const ulonglong2 qc = *reinterpret_cast<const ulonglong2*>(q[c]);
+    const unsigned long long t0 = sub2(x[2 * c], qc.x);
+    const unsigned long long t1 = sub2(x[2 * c + 1], qc.y);
+    a[c] = fma2(t1, t1, 0ull);
+    a[c] = fma2(t0, t0, a[c]);
+  }
+  const float2 s = upk(add2(add2(a[0], a[1]), add2(a[2], a[3])));
+  return s.x + s.y;
+}
+
+__device__ __forceinline__ void ld_block(unsigned long long (&x)[8], const float* src) {
+  const ulonglong2* s = reinterpret_cast<const ulonglong2*>(src);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const ulonglong2 v = __ldg(s + c);
+    x[2 * c] = v.x;
+    x[2 * c + 1] = v.y;
+  }
 }
 
 __device__ __forceinline__ unsigned long long make_key(float d, uint32_t id) {
   return ((unsigned long long)__float_as_uint(d) << 32) | id;
 }
 
-__device__ __forceinline__ float4 ldg4(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
+// Register-resident sorted top-K: position g = lane*KPL + i holds key k[i] (kKeyInf = empty).
+template <int KPL>
+struct RegTopK {
+  unsigned long long k[KPL];
+  unsigned long long kth;  // key at position K-1 (kKeyInf while fewer than K keys)
+  int kl, ki;              // lane / slot of position K-1
 
-// Warp-local top-K (owned by one warp): merge up to 32 keys (one per lane, kKeyInf = none).
-struct TopK {
-  unsigned long long* buf;  // 2 x K keys (double buffer)
-  unsigned long long* sB;   // 32 keys scratch
-  int K, n, sel;
-  unsigned long long kth;   // K-th key when n == K
-
-  __device__ __forceinline__ void insert(unsigned long long key, int lane) {
-    if (n == K && key >= kth) key = kKeyInf;
-    if (__ballot_sync(0xffffffffu, key != kKeyInf) == 0) return;
-    merge(key, lane);
-  }
-
-  __device__ __noinline__ void merge(unsigned long long key, int lane) {
+  __device__ __forceinline__ void init(int K) {
 #pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
+    for (int i = 0; i < KPL; ++i) k[i] = kKeyInf;
+    kth = kKeyInf;
+    kl = (K - 1) / KPL;
+    ki = (K - 1) % KPL;
+  }
+  __device__ __forceinline__ void refresh_kth() {
+    unsigned long long t = k[0];
 #pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const unsigned long long o = __shfl_xor_sync(0xffffffffu, key, j);
-        const bool lower = (lane & j) == 0, up = (lane & k) == 0;
-        const unsigned long long mn = key < o ? key : o, mx = key < o ? o : key;
-        key = (lower == up) ? mn : mx;
-      }
-    }
-    const int m = __popc(__ballot_sync(0xffffffffu, key != kKeyInf));
-    const unsigned long long* A = buf + sel * K;
-    unsigned long long* Bn = buf + (sel ^ 1) * K;
-    sB[lane] = key;
-    __syncwarp();
-    if (lane < m) {
-      int lo = 0, hi = n;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (A[mid] < key) lo = mid + 1; else hi = mid;
-      }
-      if (lane + lo < K) Bn[lane + lo] = key;
-    }
-    for (int j = lane; j < n; j += 32) {
-      const unsigned long long a = A[j];
-      int lo = 0, hi = m;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sB[mid] < a) lo = mid + 1; else hi = mid;
-      }
-      if (j + lo < K) Bn[j + lo] = a;
-    }
-    __syncwarp();
-    n = min(K, n + m);
-    sel ^= 1;
-    if (n == K) kth = Bn[K - 1];
+    for (int i = 1; i < KPL; ++i)
+      if (i == ki) t = k[i];
+    kth = __shfl_sync(0xffffffffu, t, kl);
   }
-};
-
-// Candidate-stream tile iterator (warp-uniform): tiles never cross a list or an epoch boundary.
-struct TileIter {
-  const int32_t* probes;
-  const int32_t* off;
-  int nprobe, cj;
-  int cpos, cstart, clen, r, L, e_hi_raw, e_hi;  // stream positions (< 2^31)
-  int ep;
-
-  __device__ void load_list() {
-    if (cj < nprobe) {
-      const int l = probes[cj];
-      cstart = off[l];
-      clen = off[l + 1] - cstart;
-    } else {
-      cstart = 0;
-      clen = 0;
+  // insert x (warp-uniform, x < kth): shift every key >= x one position up
+  __device__ __forceinline__ void insert_one(unsigned long long x, int lane) {
+    unsigned long long left = __shfl_up_sync(0xffffffffu, k[KPL - 1], 1);
+    if (lane == 0) left = 0ull;  // "smaller than x"
+#pragma unroll
+    for (int i = KPL - 1; i >= 0; --i) {
+      const unsigned long long l = i > 0 ? k[i - 1] : left;
+      if (k[i] >= x) k[i] = l < x ? x : l;
     }
+    refresh_kth();
   }
-  __device__ void init(const int32_t* pr, const int32_t* of, int np, int L_, int c0) {
-    probes = pr; off = of; nprobe = np; cj = 0; cpos = 0; r = 0; L = L_;
-    e_hi_raw = c0; e_hi = c0 < L ? c0 : L; ep = 0;
-    load_list();
-  }
-  // next tile of at most TR rows; returns false at the end of the stream
-  __device__ bool next(int TR, int32_t& row0, int& nr, int& epoch) {
-    if (r >= L) return false;
-    if (r >= e_hi) {  // epoch boundary (R13): [0,c0), [c0,2c0), [2c0,4c0), ...
-      ++ep;
-      e_hi_raw = e_hi_raw > (1 << 29) ? (1 << 30) : e_hi_raw * 2;
-      e_hi = e_hi_raw < L ? e_hi_raw : L;
+  // offer one key per lane (kKeyInf = none)
+  __device__ __forceinline__ void offer(unsigned long long key, int lane) {
+    unsigned m = __ballot_sync(0xffffffffu, key < kth);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const unsigned long long x = __shfl_sync(0xffffffffu, key, src);
+      if (x < kth) insert_one(x, lane);
     }
-    while (cj < nprobe && cpos + clen <= r) {  // skip exhausted (and empty) lists
-      cpos += clen;
-      ++cj;
-      load_list();
-    }
-    if (cj >= nprobe) return false;
-    const int hi = e_hi < cpos + clen ? e_hi : cpos + clen;
-    nr = hi - r < TR ? hi - r : TR;
-    row0 = cstart + (r - cpos);
-    epoch = ep;
-    r += nr;
-    return true;
   }
 };
 
 }  // namespace
 
-template <int DD, int LA, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__ ScanParams p) {
+// One warp per CTA. Shared memory: tiles | mbar | meta | ring | pruned | lists | qs.
+template <int DD, int KPL, int LA>
+__global__ void __launch_bounds__(32, 20) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kStages = DD == 1 ? 3 : 2;
+  constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
   const int D = p.D, K = p.K;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int TR = 32;                 // rows per tile: one row per lane
-  constexpr int TB = TR * 64 * DD;       // tile bytes (DD blocks of 32 rows)
-  // per-warp smem slice: tiles | mbar | meta | ring | topk[2K] | sB | pruned | qs[D]
-  const size_t slice = (size_t)kStages * TB + kMbarBytes + kStages * sizeof(TileMeta) +
-                       kQCap * sizeof(QEntry) + (size_t)2 * K * 8 + 32 * 8 + DADE_MAX_STEPS * 4 + (size_t)D * 4;
-  unsigned char* base = smem + warp * ((slice + 127) & ~(size_t)127);
-  unsigned char* tiles = base;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
-  TileMeta* meta = reinterpret_cast<TileMeta*>(base + kStages * TB + kMbarBytes);
+  const int lane = threadIdx.x;
+  unsigned char* tiles = smem;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + kStages * TB);
+  TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + 4);
   QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
-  unsigned long long* tkbuf = reinterpret_cast<unsigned long long*>(ring + kQCap);
-  unsigned long long* sB = tkbuf + 2 * K;
-  unsigned* pruned = reinterpret_cast<unsigned*>(sB + 32);
-  float* qs = reinterpret_cast<float*>(pruned + DADE_MAX_STEPS);
+  unsigned* pruned = reinterpret_cast<unsigned*>(ring + kQCap);
+  int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
+  float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
 
-  for (int j = lane; j < DADE_MAX_STEPS; j += 32) pruned[j] = 0;
+  const bool stats = p.counters != nullptr;
+  if (stats)
+    for (int j = lane; j < DADE_MAX_STEPS; j += 32) pruned[j] = 0;
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -217,10 +219,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
 
   const int nsteps = p.nsteps;
   const int nblk = D >> 4;
-  const int64_t n = p.n;
   const float* lay = p.layout;
-  const bool stats = p.counters != nullptr;
-  unsigned long long c_tested = 0, c_surv = 0, c_dims = 0;  // warp-uniform (lane 0 authoritative)
+  const int64_t n = p.n;
+  unsigned long long c_tested = 0, c_surv = 0;  // warp-uniform
   uint32_t phase_bits = 0;
   const unsigned lt_mask = (1u << lane) - 1;
 
@@ -231,27 +232,41 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
     if (qi >= p.nq) break;
     const int64_t q = qi;
     for (int j = lane; j < D; j += 32) qs[j] = p.qrot[q * D + j];
-    TopK tk{tkbuf, sB, K, 0, 0, kKeyInf};
-    const int32_t* probes = p.probes + q * p.nprobe;
-    int64_t L = 0;
+    int L = 0;
     for (int j = lane; j < p.nprobe; j += 32) {
-      const int l = probes[j];
-      L += p.off[l + 1] - p.off[l];
+      const int l = p.probes[q * p.nprobe + j];
+      const int s0 = p.off[l], s1 = p.off[l + 1];
+      lists[j] = make_int2(s0, s1 - s0);
+      L += s1 - s0;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
     __syncwarp();
 
-    // ------------------------------------------------------------ producer (TMA bulk copies)
-    TileIter prod;
-    prod.init(probes, p.off, p.nprobe, (int)L, p.c0);
+    RegTopK<KPL> tk;
+    tk.init(K);
+
+    // ---------------------------------------------------- producer state (warp-uniform)
+    // tiles never cross a list or an epoch boundary (R13: [0,c0), [c0,2c0), [2c0,4c0), ...)
+    int pj = 0, ppos = 0, pr = 0, pep = 0, pe_hi = p.c0;
+    int2 pl = p.nprobe > 0 ? lists[0] : make_int2(0, 0);
     int issued = 0;
-    auto issue = [&](int slot) {  // warp-uniform call; lane 0 issues
-      int32_t row0;
-      int nr, ep;
-      if (!prod.next(TR, row0, nr, ep)) return false;
+    auto issue = [&](int slot) -> bool {
+      if (pr >= L) return false;
+      if (pr >= pe_hi) {
+        ++pep;
+        pe_hi = pe_hi > (1 << 29) ? (1 << 30) : pe_hi * 2;
+      }
+      while (ppos + pl.y <= pr) {  // skip exhausted (and empty) lists; pr < L keeps pj < nprobe
+        ppos += pl.y;
+        pl = lists[++pj];
+      }
+      const int hi = min(pe_hi, ppos + pl.y);
+      const int nr = min(hi - pr, TR);
+      const int row0 = pl.x + (pr - ppos);
+      pr += nr;
       if (lane == 0) {
-        meta[slot] = TileMeta{row0, nr, ep, 0};
+        meta[slot] = TileMeta{row0, nr, pep, 0};
         const uint32_t bytes = (uint32_t)nr * 64u;
         mbar_expect_tx(&mbar[slot], bytes * DD);
 #pragma unroll
@@ -261,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
       ++issued;
       return true;
     };
+#pragma unroll 1
     for (int s = 0; s < kStages; ++s)
       if (!issue(s)) break;
 
@@ -273,136 +289,119 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
       if (keep) ring[(tail + __popc(km & lt_mask)) & (kQCap - 1)] = e;
       tail += __popc(km);
     };
-    auto finish = [&](bool fin, float P, int32_t row) {
-      unsigned long long key = kKeyInf;
-      if (fin) key = make_key(P, (uint32_t)p.row_id[row]);
-      if (stats) {
-        const int nf = __popc(__ballot_sync(0xffffffffu, fin));
-        c_surv += nf;
-        c_dims += (unsigned long long)nf * D;
-      }
-      tk.insert(key, lane);
-    };
 
     // one gather round: up to 32 queued survivors (one per lane) advanced by up to LA blocks
     auto queue_round = [&](bool drain) {
       const int qn = min(tail - head, 32);
       const bool val = lane < qn;
-      QEntry e = val ? ring[(head + lane) & (kQCap - 1)] : QEntry{0, 0.f, 0.f, nblk};
-      const int want = min((drain || e.blk > DD) ? LA : (DD < LA ? DD : LA), nblk - e.blk);
-      float4 v[LA][4];
+      QEntry e = val ? ring[(head + lane) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0};
+      int want = (drain || e.blk > DD) ? LA : (DD < LA ? DD : LA);
+      want = min(want, nblk - e.blk);
+      unsigned long long v[LA][8];
 #pragma unroll
       for (int s = 0; s < LA; ++s)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          v[s][k] = (s < want) ? ldg4(lay + (((int64_t)(e.blk + s) * n + e.row) << 4) + k * 4)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s < want) ld_block(v[s], lay + (((int64_t)(e.blk + s) * n + e.row) << 4));
+      uint32_t gid = 0;
+      if (e.blk + want == nblk && val) gid = (uint32_t)__ldg(p.row_id + e.row);
       head += qn;
       __syncwarp();
-      float phi = e.phi, plo = e.plo;
+      float phi = e.phi;
       int blk = e.blk;
-      bool alive = val, fin = false;
+      bool alive = val;
 #pragma unroll
       for (int s = 0; s < LA; ++s) {
         if (alive && s < want) {
-          const float* qb = qs + blk * 16;
-          float b4[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float4 qq = *reinterpret_cast<const float4*>(qb + k * 4);
-            float t = v[s][k].x - qq.x; b4[k] = t * t;
-            t = v[s][k].y - qq.y; b4[k] = fmaf(t, t, b4[k]);
-            t = v[s][k].z - qq.z; b4[k] = fmaf(t, t, b4[k]);
-            t = v[s][k].w - qq.w; b4[k] = fmaf(t, t, b4[k]);
-          }
-          const float bs = (b4[0] + b4[1]) + (b4[2] + b4[3]);
-          float err;  // compensated running sum over blocks (R21)
-          two_sum(phi, bs, phi, err);
-          plo += err;
+          phi += block_sum(v[s], qs + blk * 16);
           ++blk;
-          if (blk % DD == 0) {  // step boundary: the classifier for d = blk*16
+          if (blk % DD == 0 && blk < nblk) {  // step boundary d = blk*16 < D: classifier
             const int ns = blk / DD;
-            if (ns == nsteps) {
-              fin = true;
-              alive = false;
-            } else if (fmaf(p.m1[ns - 1], phi + plo, p.beta[ns - 1]) > tau) {
+            if (fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau) {
               alive = false;
               if (stats) atomicAdd(&pruned[ns], 1u);
             }
           }
         }
       }
-      if (stats) {
-        // dims of candidates pruned in this round: blk*16 each (warp sum)
-        unsigned long long dp = (val && !alive && !fin) ? (unsigned long long)blk * 16 : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
-        c_dims += dp;
-      }
-      push(alive, QEntry{e.row, phi, plo, blk});
-      finish(fin, phi + plo, e.row);
-      __syncwarp();
+      const bool fin = alive && blk == nblk;  // d = D: exact distance (no test, R10)
+      push(alive && !fin, QEntry{e.row, phi, blk, 0});
+      if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
+      tk.offer(fin ? make_key(phi, gid) : kKeyInf, lane);
     };
 
-    // ------------------------------------------------------------ consumer
-    while (consumed < issued) {
-      const int slot = consumed % kStages;
-      mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
-      phase_bits ^= 1u << slot;
-      const TileMeta tm = meta[slot];
-      if (tm.ep != cur_ep) {  // epoch boundary: finish every survivor, then refresh tau (R13)
-        while (tail > head) queue_round(true);
-        tau = (tk.n == K) ? __uint_as_float((unsigned)(tk.kth >> 32)) : INFINITY;
-        cur_ep = tm.ep;
+    // ---------------------------------------------------- consumer (one call site per action)
+    bool ready = false;  // the tile in `slot` has landed and its meta is read
+    TileMeta tm{0, 0, 0, 0};
+    for (;;) {
+      const int qlen = tail - head;
+      bool round = qlen >= 16, drain = false;
+      if (!round) {
+        if (!ready) {
+          if (consumed < issued) {
+            const int slot = consumed % kStages;
+            mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
+            phase_bits ^= 1u << slot;
+            tm = meta[slot];
+            ready = true;
+          } else if (qlen == 0) {
+            break;
+          } else {
+            round = drain = true;  // end of the stream: finish every survivor
+          }
+        }
+        if (ready && tm.ep != cur_ep) {  // epoch boundary: finish every survivor, then refresh tau
+          if (qlen > 0) {
+            round = drain = true;
+          } else {
+            tau = tk.kth == kKeyInf ? INFINITY : __uint_as_float((unsigned)(tk.kth >> 32));
+            cur_ep = tm.ep;
+          }
+        }
       }
-      while (tail - head > kQCap - TR) queue_round(false);  // room for this tile's survivors
-      const int nr = tm.nr;
-      const bool val = lane < nr;
-      // stage 1: one row per lane; the 16-B chunk order is rotated per lane so the 8 lanes of
-      // each shared-memory phase hit distinct banks
+      if (round) {
+        queue_round(drain);
+        continue;
+      }
+      // stage 1 (qlen < 16: the ring has room for 32 more): one row per lane, DD blocks
+      const int slot = consumed % kStages;
+      const bool val = lane < tm.nr;
       const unsigned char* trow = tiles + slot * TB + lane * 64;
-      // 4 independent partial sums (one per 16-B chunk) keep the FMA pipes busy
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      float s = 0.f;
 #pragma unroll
       for (int bb = 0; bb < DD; ++bb) {
+        unsigned long long x[8];
+        const float* qc[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int ch = (k + lane) & 3;
-          const float4 x = *reinterpret_cast<const float4*>(trow + bb * TR * 64 + ch * 16);
-          const float4 qq = *reinterpret_cast<const float4*>(qs + bb * 16 + ch * 4);
-          float t = x.x - qq.x; s4[k] = fmaf(t, t, s4[k]);
-          t = x.y - qq.y; s4[k] = fmaf(t, t, s4[k]);
-          t = x.z - qq.z; s4[k] = fmaf(t, t, s4[k]);
-          t = x.w - qq.w; s4[k] = fmaf(t, t, s4[k]);
+        for (int c = 0; c < 4; ++c) {  // 16-B chunks rotated per lane: distinct banks per phase
+          const int ch = (c + lane) & 3;
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(trow + bb * TR * 64 + ch * 16);
+          x[2 * c] = v.x;
+          x[2 * c + 1] = v.y;
+          qc[c] = qs + bb * 16 + ch * 4;
         }
+        s += block_sum_rot(x, qc);
       }
-      const float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       __syncwarp();  // every lane is done reading this slot
       ++consumed;
+      ready = false;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(slot);
-      const int32_t row = tm.row0 + lane;
-      if (stats) c_tested += nr;
-      if (nsteps == 1) {
-        finish(val, s, row);
-      } else {
-        const bool prune = val && fmaf(p.m1[0], s, p.beta[0]) > tau;
-        push(val && !prune, QEntry{row, s, 0.f, DD});
-        if (stats) {
-          const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
-          if (lane == 0 && np_) pruned[1] += np_;
-          c_dims += (unsigned long long)np_ * DD * 16;
-        }
+      if (stats) c_tested += tm.nr;
+      const bool prune = val && nsteps > 1 && fmaf(p.m1[0], s, p.beta[0]) > tau;
+      push(val && !prune, QEntry{tm.row0 + lane, s, DD, 0});
+      if (stats) {
+        const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
+        if (lane == 0 && np_) pruned[1] += np_;
       }
-      if (tail - head >= 16) queue_round(false);
     }
-    while (tail > head) queue_round(true);
 
-    const unsigned long long* fin = tk.buf + tk.sel * K;
-    for (int i = lane; i < K; i += 32) {
-      const unsigned long long key = i < tk.n ? fin[i] : kKeyInf;
-      p.out_ids[q * K + i] = key == kKeyInf ? -1 : (int64_t)(uint32_t)(key & 0xffffffffu);
-      p.out_d[q * K + i] = key == kKeyInf ? INFINITY : __uint_as_float((unsigned)(key >> 32));
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int pos = lane * KPL + i;
+      if (pos < K) {
+        const unsigned long long key = tk.k[i];
+        p.out_ids[q * K + pos] = key == kKeyInf ? -1 : (int64_t)(uint32_t)(key & 0xffffffffu);
+        p.out_d[q * K + pos] = key == kKeyInf ? INFINITY : __uint_as_float((unsigned)(key >> 32));
+      }
     }
     if (lane == 0 && stats) atomicMax(p.counters + 3, (unsigned long long)(L > 0 ? cur_ep + 1 : 0));
     __syncwarp();
@@ -411,7 +410,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
     if (lane == 0) {
       atomicAdd(p.counters + 0, c_tested);
       atomicAdd(p.counters + 1, c_surv);
-      atomicAdd(p.counters + 2, c_dims);
     }
     __syncwarp();
     for (int j = lane; j < DADE_MAX_STEPS; j += 32)
@@ -419,51 +417,50 @@ __global__ void __launch_bounds__(kThreads, MINB) k_scan(const __grid_constant__
   }
 }
 
-static size_t scan_smem(int D, int K, int DD) {
-  const size_t slice = (size_t)kStages * 32 * 64 * DD + kMbarBytes + kStages * sizeof(TileMeta) +
-                       kQCap * sizeof(QEntry) + (size_t)2 * K * 8 + 32 * 8 + DADE_MAX_STEPS * 4 + (size_t)D * 4;
-  return kWarps * ((slice + 127) & ~(size_t)127);
+template <int DD>
+static size_t scan_smem(int D, int nprobe) {
+  constexpr int kStages = DD == 1 ? 3 : 2;
+  return (size_t)kStages * TR * 64 * DD + 4 * 8 + kStages * sizeof(TileMeta) + kQCap * sizeof(QEntry) +
+         DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 + (size_t)D * 4;
 }
 
-template <int DD, int LA, int MINB>
+template <int DD, int KPL, int LA>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
-  const size_t smem = scan_smem(p.D, p.K, DD);
+  const size_t smem = scan_smem<DD>(p.D, p.nprobe);
   static int sms = 0;
+  static size_t attr = 0;
   if (!sms) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD, LA, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int dev;
     DADE_CK(cudaGetDevice(&dev));
     DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  DADE_REQUIRE(smem <= 200 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory slice too large (D, K)");
+  DADE_REQUIRE(smem <= 200 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, nprobe)");
+  if (smem > attr) {
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
   int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, LA, MINB>, kThreads, smem));
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA>, 32, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;
-  const int need = (p.nq + kWarps - 1) / kWarps;
-  k_scan<DD, LA, MINB><<<need < max_blocks ? need : max_blocks, kThreads, smem, st>>>(p);
+  k_scan<DD, KPL, LA><<<p.nq < max_blocks ? p.nq : max_blocks, 32, smem, st>>>(p);
 }
 
-// variant (lookahead blocks, min CTAs/SM) selectable for tuning via DADE_SCAN_VARIANT
-static int scan_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DADE_SCAN_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
+template <int DD, int KPL>
+static void launch_k(const ScanParams& p, cudaStream_t st) {
+  launch_v<DD, KPL, 2>(p, st);
 }
 
 template <int DD>
 static void launch_dd(const ScanParams& p, cudaStream_t st) {
-  switch (scan_variant()) {
-    case 1: launch_v<DD, 2, 4>(p, st); break;
-    case 3: launch_v<DD, 4, 3>(p, st); break;
-    default: launch_v<DD, 2, 6>(p, st); break;
-  }
+  if (p.K <= 32) launch_k<DD, 1>(p, st);
+  else if (p.K <= 64) launch_k<DD, 2>(p, st);
+  else if (p.K <= 128) launch_k<DD, 4>(p, st);
+  else launch_k<DD, 8>(p, st);
 }
 
 void launch_scan(const ScanParams& p, cudaStream_t st) {
   if (p.nq <= 0) return;
+  DADE_REQUIRE(p.K <= 256, DADE_ERR_UNSUPPORTED, "scan: K > 256");
   switch (p.dd) {
     case 1: launch_dd<1>(p, st); break;
     case 2: launch_dd<2>(p, st); break;
