@@ -193,8 +193,8 @@ struct RegTopK {
 }  // namespace
 
 // One warp per CTA. Shared memory: tiles | mbar | meta | ring | pruned | lists | qs.
-template <int DD, int KPL, int LA>
-__global__ void __launch_bounds__(32, 20) k_scan(const __grid_constant__ ScanParams p) {
+template <int DD, int KPL, int LA, int MINB>
+__global__ void __launch_bounds__(32, MINB) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int kStages = DD == 1 ? 3 : 2;
   constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
@@ -290,40 +290,59 @@ __global__ void __launch_bounds__(32, 20) k_scan(const __grid_constant__ ScanPar
       tail += __popc(km);
     };
 
-    // one gather round: up to 32 queued survivors (one per lane) advanced by up to LA blocks
+    // One gather round over up to 32 queued survivors. Normally one lane per survivor, up to LA
+    // blocks per round trip. When draining a short queue (epoch boundary, end of stream) G = 2
+    // or 4 lanes share a survivor and each loads LA consecutive blocks, so one round trip
+    // advances it by up to G*LA blocks; the group's block sums are then accumulated in block
+    // order by every lane of the group (shuffles), so phi is bit-identical to the G = 1 path.
     auto queue_round = [&](bool drain) {
       const int qn = min(tail - head, 32);
-      const bool val = lane < qn;
-      QEntry e = val ? ring[(head + lane) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0};
-      int want = (drain || e.blk > DD) ? LA : (DD < LA ? DD : LA);
-      want = min(want, nblk - e.blk);
+      const int lg = !drain ? 0 : qn <= 8 ? 2 : qn <= 16 ? 1 : 0;  // log2 lanes per survivor
+      const int ei = lane >> lg, sub = lane & ((1 << lg) - 1);
+      const bool val = ei < qn;
+      QEntry e = val ? ring[(head + ei) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0};
+      int wtot = (drain || e.blk > DD) ? (LA << lg) : (DD < LA ? DD : LA);
+      wtot = min(wtot, nblk - e.blk);
+      const int b0 = e.blk + sub * LA;  // this lane's first block
+      const int want = max(0, min(LA, e.blk + wtot - b0));
       unsigned long long v[LA][8];
 #pragma unroll
       for (int s = 0; s < LA; ++s)
-        if (s < want) ld_block(v[s], lay + (((int64_t)(e.blk + s) * n + e.row) << 4));
+        if (s < want) ld_block(v[s], lay + (((int64_t)(b0 + s) * n + e.row) << 4));
       uint32_t gid = 0;
-      if (e.blk + want == nblk && val) gid = (uint32_t)__ldg(p.row_id + e.row);
+      if (e.blk + wtot == nblk && val && sub == 0) gid = (uint32_t)__ldg(p.row_id + e.row);
       head += qn;
       __syncwarp();
+      float bs[LA];
+#pragma unroll
+      for (int s = 0; s < LA; ++s) bs[s] = s < want ? block_sum(v[s], qs + (b0 + s) * 16) : 0.f;
       float phi = e.phi;
       int blk = e.blk;
       bool alive = val;
-#pragma unroll
-      for (int s = 0; s < LA; ++s) {
-        if (alive && s < want) {
-          phi += block_sum(v[s], qs + blk * 16);
+      const int bend = e.blk + wtot;
+      auto step = [&](float b) {  // add the next block; classifier at step boundaries d < D
+        if (alive && blk < bend) {
+          phi += b;
           ++blk;
-          if (blk % DD == 0 && blk < nblk) {  // step boundary d = blk*16 < D: classifier
+          if (blk % DD == 0 && blk < nblk) {
             const int ns = blk / DD;
             if (fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau) {
               alive = false;
-              if (stats) atomicAdd(&pruned[ns], 1u);
+              if (stats && sub == 0) atomicAdd(&pruned[ns], 1u);
             }
           }
         }
+      };
+      if (lg == 0) {
+#pragma unroll
+        for (int s = 0; s < LA; ++s) step(bs[s]);
+      } else {
+        for (int j = 0; j < (1 << lg); ++j)
+#pragma unroll
+          for (int s = 0; s < LA; ++s) step(__shfl_sync(0xffffffffu, bs[s], (ei << lg) + j));
       }
-      const bool fin = alive && blk == nblk;  // d = D: exact distance (no test, R10)
-      push(alive && !fin, QEntry{e.row, phi, blk, 0});
+      const bool fin = alive && blk == nblk && sub == 0;  // d = D: exact distance (no test, R10)
+      push(alive && blk < nblk && sub == 0, QEntry{e.row, phi, blk, 0});
       if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
       tk.offer(fin ? make_key(phi, gid) : kKeyInf, lane);
     };
@@ -333,7 +352,7 @@ __global__ void __launch_bounds__(32, 20) k_scan(const __grid_constant__ ScanPar
     TileMeta tm{0, 0, 0, 0};
     for (;;) {
       const int qlen = tail - head;
-      bool round = qlen >= 16, drain = false;
+      bool round = qlen >= 32, drain = false;
       if (!round) {
         if (!ready) {
           if (consumed < issued) {
@@ -361,7 +380,7 @@ __global__ void __launch_bounds__(32, 20) k_scan(const __grid_constant__ ScanPar
         queue_round(drain);
         continue;
       }
-      // stage 1 (qlen < 16: the ring has room for 32 more): one row per lane, DD blocks
+      // stage 1 (qlen < 32: the ring has room for 32 more): one row per lane, DD blocks
       const int slot = consumed % kStages;
       const bool val = lane < tm.nr;
       const unsigned char* trow = tiles + slot * TB + lane * 64;
@@ -424,7 +443,7 @@ static size_t scan_smem(int D, int nprobe) {
          DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 + (size_t)D * 4;
 }
 
-template <int DD, int KPL, int LA>
+template <int DD, int KPL, int LA, int MINB>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
   const size_t smem = scan_smem<DD>(p.D, p.nprobe);
   static int sms = 0;
@@ -436,18 +455,32 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
   }
   DADE_REQUIRE(smem <= 200 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, nprobe)");
   if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
   int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA>, 32, smem));
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MINB>, 32, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;
-  k_scan<DD, KPL, LA><<<p.nq < max_blocks ? p.nq : max_blocks, 32, smem, st>>>(p);
+  k_scan<DD, KPL, LA, MINB><<<p.nq < max_blocks ? p.nq : max_blocks, 32, smem, st>>>(p);
+}
+
+// tuning variants (DADE_SCAN_VARIANT, read per launch) for the Delta_d = 16, K <= 32 kernel
+static int scan_variant() {
+  const char* e = getenv("DADE_SCAN_VARIANT");
+  return e ? atoi(e) : 0;
 }
 
 template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
-  launch_v<DD, KPL, 2>(p, st);
+  if constexpr (DD == 1 && KPL == 1) {
+    switch (scan_variant()) {
+      case 1: launch_v<DD, KPL, 2, 20>(p, st); return;
+      case 2: launch_v<DD, KPL, 1, 20>(p, st); return;
+      case 3: launch_v<DD, KPL, 1, 28>(p, st); return;
+      default: break;
+    }
+  }
+  launch_v<DD, KPL, 1, 24>(p, st);
 }
 
 template <int DD>
