@@ -16,10 +16,11 @@ using namespace dade;
 // A matrix pre-split for the tensor-core distance filter (gemm_tf32.cu): tf32 hi/lo parts in the
 // UMMA tiled layout, fp32 squared norms, and the largest norm (for the error bound).
 struct TcOp {
-  DBuf<float> hi, lo, norm, maxn;
+  DBuf<float> hi, lo, norm, maxn, center;
+  DBuf<double> csum;
   int64_t rows = 0;
   float maxnorm = 0.f;
-  void release() { hi.release(); lo.release(); norm.release(); maxn.release(); rows = 0; }
+  void release() { hi.release(); lo.release(); norm.release(); maxn.release(); center.release(); csum.release(); rows = 0; }
 };
 
 struct dade_index {
@@ -119,14 +120,22 @@ void check_knn_flag(dade_index* x) {
   }
 }
 
-void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_max) {
+// need_max: B operand (computes its column mean = the centre both operands use, and the largest
+// centred norm); else A operand, centred on `center` (the B operand's).
+void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_max, const float* center = nullptr) {
   const int D = x->D;
   const int64_t rp = tc_rows_pad(n);
   const size_t elems = (size_t)rp * tc_nkc(D) * 32;
   op.hi.reserve(elems);
   op.lo.reserve(elems);
   op.norm.reserve(rp);
-  launch_split_tf32(B, n, D, op.hi.p, op.lo.p, op.norm.p, x->stream);
+  if (need_max) {
+    op.center.reserve(D);
+    op.csum.reserve(D);
+    launch_col_mean(B, n, D, op.csum.p, op.center.p, x->stream);
+    center = op.center.p;
+  }
+  launch_split_tf32(B, n, D, center, op.hi.p, op.lo.p, op.norm.p, x->stream);
   op.rows = n;
   if (need_max) {
     op.maxn.reserve(1);
@@ -163,7 +172,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   }
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t mm = std::min(chunk, m - r0);
-    tc_prepare(x, A + r0 * D, mm, x->a_tc, false);
+    tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
     const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 256 && n <= 32 * 256;
     launch_l2_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
                  x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr);

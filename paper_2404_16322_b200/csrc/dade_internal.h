@@ -73,8 +73,11 @@ void launch_argmin_exact(const float* d_hat, int64_t m, int64_t n, const float* 
 int64_t tc_rows_pad(int64_t rows);
 int tc_nkc(int D);
 float tc_gamma(int D);
-void launch_split_tf32(const float* X, int64_t rows, int D, float* hi, float* lo, float* norm,
-                       cudaStream_t st);
+// center (nullable, fp32 D): operands are split from fl(x - center)
+void launch_split_tf32(const float* X, int64_t rows, int D, const float* center, float* hi, float* lo,
+                       float* norm, cudaStream_t st);
+// out[j] = fp32(mean_r X[r, j]) (fp64 sums in scratch[D])
+void launch_col_mean(const float* X, int64_t n, int D, double* scratch, float* out, cudaStream_t st);
 void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, cudaStream_t st);
 void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,

@@ -98,9 +98,12 @@ __device__ __forceinline__ unsigned thr_bits(float v, int D) {
   return b == 0x7f800000u ? b : b + 2u;  // two ulps of slack on top of the rounding of T
 }
 
-// absolute window for the tensor-core filter: bits of (v + 2*slack) rounded up
+// window for the tensor-core filter (gemm_tf32.cu): |d_hat - d| <= slack + delta d, so every true
+// k-nearest column has d_hat <= (v + slack)(1 + delta)/(1 - delta) + slack, v = k-th smallest
+// d_hat; bits rounded up
 __device__ __forceinline__ unsigned abs_thr_bits(float v, float slack) {
-  const double T = (double)v + 2.0 * (double)slack;
+  const double delta = 9.5367431640625e-07;  // 2^-20
+  const double T = ((double)v + (double)slack) * (1.0 + delta) / (1.0 - delta) + (double)slack;
   const float tf = (float)T;
   if (!(tf >= 0.f)) return 0xffffffffu;
   const unsigned b = __float_as_uint(tf);

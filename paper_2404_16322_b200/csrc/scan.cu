@@ -10,8 +10,9 @@
 // the parallel schedule.
 //
 // B200 mapping:
-//  * persistent CTAs of ONE WARP, one query at a time (queries taken from an atomic counter):
-//    an epoch boundary waits only for the warp's own survivors, never for other warps;
+//  * persistent CTAs of G warps (G = 1 when there are enough queries to fill the machine), one
+//    query at a time (queries taken from an atomic counter); with G = 1 an epoch boundary
+//    waits only for the warp's own survivors, never for other warps;
 //  * the probed lists' (start, length) table and q~ sit in shared memory; the first step of
 //    every candidate is STREAMED with TMA bulk copies (cp.async.bulk, one elected lane,
 //    mbarrier completion) into a ring of tiles, issued kStages tiles ahead of consumption
@@ -192,30 +193,49 @@ struct RegTopK {
 
 }  // namespace
 
-// One warp per CTA. Shared memory: tiles | mbar | meta | ring | pruned | lists | qs.
-template <int DD, int KPL, int LA, int MINB>
-__global__ void __launch_bounds__(32, MINB) k_scan(const __grid_constant__ ScanParams p) {
+// Per-warp shared-memory slice: tiles | mbar | meta | ring.
+template <int DD>
+struct Slice {
+  static constexpr int kStages = DD == 1 ? 3 : 2;
+  static constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
+  static constexpr size_t bytes = (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + kQCap * sizeof(QEntry);
+};
+
+// CTA = G warps (blockDim.x = 32 G), one query at a time. G = 1: the warp owns the query and its
+// register top-K is the query's top-K. G > 1: the query's candidate tiles are dealt round-robin
+// to the G warps (tile t -> warp t mod G); within an epoch every warp tests against the same
+// frozen tau (R13), so the split cannot change a decision; at each epoch end the warps' local
+// top-K lists are merged exactly (rank by binary search, smem) into the query's top-K.
+// CTA shared memory: G slices | pruned[64] | lists[nprobe] | qs[D] | (G > 1) W[G][K] + Gk[2][K] | qi.
+template <int DD, int KPL, int LA, int MAXREG>
+__global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int kStages = DD == 1 ? 3 : 2;
-  constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
+  using SL = Slice<DD>;
+  constexpr int kStages = SL::kStages;
+  constexpr int TB = SL::TB;
   const int D = p.D, K = p.K;
-  const int lane = threadIdx.x;
-  unsigned char* tiles = smem;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + kStages * TB);
+  const int G = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* base = smem + warp * SL::bytes;
+  unsigned char* tiles = base;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
   TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + 4);
   QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
-  unsigned* pruned = reinterpret_cast<unsigned*>(ring + kQCap);
+  unsigned* pruned = reinterpret_cast<unsigned*>(smem + G * SL::bytes);
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
+  unsigned long long* W = reinterpret_cast<unsigned long long*>(qs + ((D + 3) & ~3));  // G x K
+  unsigned long long* Gk = W + (size_t)G * K;                                         // 2 x K
+  int* qslot = reinterpret_cast<int*>(Gk + 2 * K);
 
   const bool stats = p.counters != nullptr;
   if (stats)
-    for (int j = lane; j < DADE_MAX_STEPS; j += 32) pruned[j] = 0;
+    for (int j = threadIdx.x; j < DADE_MAX_STEPS; j += blockDim.x) pruned[j] = 0;
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncwarp();
+  __syncthreads();
 
   const int nsteps = p.nsteps;
   const int nblk = D >> 4;
@@ -226,45 +246,53 @@ __global__ void __launch_bounds__(32, MINB) k_scan(const __grid_constant__ ScanP
   const unsigned lt_mask = (1u << lane) - 1;
 
   for (;;) {
-    int qi = 0;
-    if (lane == 0) qi = atomicAdd(p.work_counter, 1);
-    qi = __shfl_sync(0xffffffffu, qi, 0);
+    if (threadIdx.x == 0) *qslot = atomicAdd(p.work_counter, 1);
+    __syncthreads();
+    const int qi = *qslot;
     if (qi >= p.nq) break;
     const int64_t q = qi;
-    for (int j = lane; j < D; j += 32) qs[j] = p.qrot[q * D + j];
-    int L = 0;
-    for (int j = lane; j < p.nprobe; j += 32) {
+    for (int j = threadIdx.x; j < D; j += blockDim.x) qs[j] = p.qrot[q * D + j];
+    for (int j = threadIdx.x; j < p.nprobe; j += blockDim.x) {
       const int l = p.probes[q * p.nprobe + j];
-      const int s0 = p.off[l], s1 = p.off[l + 1];
-      lists[j] = make_int2(s0, s1 - s0);
-      L += s1 - s0;
+      const int s0 = p.off[l];
+      lists[j] = make_int2(s0, p.off[l + 1] - s0);
     }
+    if (G > 1)
+      for (int j = threadIdx.x; j < K; j += blockDim.x) Gk[j] = kKeyInf;
+    __syncthreads();
+    int L = 0;
+    for (int j = lane; j < p.nprobe; j += 32) L += lists[j].y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    __syncwarp();
+    int n_ep = 0;  // epochs the stream touches: [0,c0), [c0,2c0), [2c0,4c0), ...
+    for (int64_t e_lo = 0, e_hi = p.c0; e_lo < L; e_lo = e_hi, e_hi *= 2) ++n_ep;
 
     RegTopK<KPL> tk;
     tk.init(K);
+    unsigned long long cap = kKeyInf;  // G > 1: the query's K-th key at the start of the epoch
 
     // ---------------------------------------------------- producer state (warp-uniform)
-    // tiles never cross a list or an epoch boundary (R13: [0,c0), [c0,2c0), [2c0,4c0), ...)
-    int pj = 0, ppos = 0, pr = 0, pep = 0, pe_hi = p.c0;
+    // tiles never cross a list or an epoch boundary (R13); tile t belongs to warp t mod G
+    int pj = 0, ppos = 0, pr = 0, pep = 0, pe_hi = p.c0, tix = 0;
     int2 pl = p.nprobe > 0 ? lists[0] : make_int2(0, 0);
     int issued = 0;
     auto issue = [&](int slot) -> bool {
-      if (pr >= L) return false;
-      if (pr >= pe_hi) {
-        ++pep;
-        pe_hi = pe_hi > (1 << 29) ? (1 << 30) : pe_hi * 2;
+      int row0, nr;
+      for (;;) {
+        if (pr >= L) return false;
+        if (pr >= pe_hi) {
+          ++pep;
+          pe_hi = pe_hi > (1 << 29) ? (1 << 30) : pe_hi * 2;
+        }
+        while (ppos + pl.y <= pr) {  // skip exhausted (and empty) lists; pr < L keeps pj < nprobe
+          ppos += pl.y;
+          pl = lists[++pj];
+        }
+        nr = min(min(pe_hi, ppos + pl.y) - pr, TR);
+        row0 = pl.x + (pr - ppos);
+        pr += nr;
+        if (tix++ % G == warp) break;
       }
-      while (ppos + pl.y <= pr) {  // skip exhausted (and empty) lists; pr < L keeps pj < nprobe
-        ppos += pl.y;
-        pl = lists[++pj];
-      }
-      const int hi = min(pe_hi, ppos + pl.y);
-      const int nr = min(hi - pr, TR);
-      const int row0 = pl.x + (pr - ppos);
-      pr += nr;
       if (lane == 0) {
         meta[slot] = TileMeta{row0, nr, pep, 0};
         const uint32_t bytes = (uint32_t)nr * 64u;
@@ -291,10 +319,10 @@ __global__ void __launch_bounds__(32, MINB) k_scan(const __grid_constant__ ScanP
     };
 
     // One gather round over up to 32 queued survivors. Normally one lane per survivor, up to LA
-    // blocks per round trip. When draining a short queue (epoch boundary, end of stream) G = 2
-    // or 4 lanes share a survivor and each loads LA consecutive blocks, so one round trip
-    // advances it by up to G*LA blocks; the group's block sums are then accumulated in block
-    // order by every lane of the group (shuffles), so phi is bit-identical to the G = 1 path.
+    // blocks per round trip. When draining a short queue (epoch boundary, end of stream) 2 or 4
+    // lanes share a survivor and each loads LA consecutive blocks, so one round trip advances it
+    // by up to 4*LA blocks; the group's block sums are then accumulated in block order by every
+    // lane of the group (shuffles), so phi is bit-identical to the one-lane path.
     auto queue_round = [&](bool drain) {
       const int qn = min(tail - head, 32);
       const int lg = !drain ? 0 : qn <= 8 ? 2 : qn <= 16 ? 1 : 0;  // log2 lanes per survivor
@@ -344,7 +372,47 @@ __global__ void __launch_bounds__(32, MINB) k_scan(const __grid_constant__ ScanP
       const bool fin = alive && blk == nblk && sub == 0;  // d = D: exact distance (no test, R10)
       push(alive && blk < nblk && sub == 0, QEntry{e.row, phi, blk, 0});
       if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
-      tk.offer(fin ? make_key(phi, gid) : kKeyInf, lane);
+      const unsigned long long key = fin ? make_key(phi, gid) : kKeyInf;
+      tk.offer(key < cap ? key : kKeyInf, lane);
+    };
+
+    // End of epoch cur_ep (every survivor of this warp finished): refresh tau (R13). G > 1: merge
+    // the warps' local lists with the query list: the rank of a key in the union is its own
+    // index plus its lower bounds in the other sorted lists (keys are unique).
+    auto epoch_end = [&]() {
+      if (G == 1) {
+        tau = tk.kth == kKeyInf ? INFINITY : __uint_as_float((unsigned)(tk.kth >> 32));
+        return;
+      }
+      unsigned long long* Gcur = Gk + (cur_ep & 1) * K;
+      unsigned long long* Gnew = Gk + ((cur_ep + 1) & 1) * K;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i)
+        if (lane * KPL + i < K) W[warp * K + lane * KPL + i] = tk.k[i];
+      for (int j = threadIdx.x; j < K; j += blockDim.x) Gnew[j] = kKeyInf;
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < (G + 1) * K; idx += blockDim.x) {
+        const int li = idx / K, own = idx - li * K;
+        const unsigned long long* Lst = li < G ? W + li * K : Gcur;
+        const unsigned long long x = Lst[own];
+        if (x == kKeyInf) continue;
+        int rank = own;
+        for (int w = 0; w <= G && rank < K; ++w) {
+          if (w == li) continue;
+          const unsigned long long* M = w < G ? W + w * K : Gcur;
+          int lo = 0, hi = K;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (M[mid] < x) lo = mid + 1; else hi = mid;
+          }
+          rank += lo;
+        }
+        if (rank < K) Gnew[rank] = x;
+      }
+      __syncthreads();
+      cap = Gnew[K - 1];
+      tau = cap == kKeyInf ? INFINITY : __uint_as_float((unsigned)(cap >> 32));
+      tk.init(K);
     };
 
     // ---------------------------------------------------- consumer (one call site per action)
@@ -352,32 +420,32 @@ __global__ void __launch_bounds__(32, MINB) k_scan(const __grid_constant__ ScanP
     TileMeta tm{0, 0, 0, 0};
     for (;;) {
       const int qlen = tail - head;
-      bool round = qlen >= 32, drain = false;
+      bool round = qlen >= 32, drain = false, ep_end = false;
       if (!round) {
-        if (!ready) {
-          if (consumed < issued) {
-            const int slot = consumed % kStages;
-            mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
-            phase_bits ^= 1u << slot;
-            tm = meta[slot];
-            ready = true;
-          } else if (qlen == 0) {
-            break;
-          } else {
-            round = drain = true;  // end of the stream: finish every survivor
-          }
+        if (!ready && consumed < issued) {
+          const int slot = consumed % kStages;
+          mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
+          phase_bits ^= 1u << slot;
+          tm = meta[slot];
+          ready = true;
         }
-        if (ready && tm.ep != cur_ep) {  // epoch boundary: finish every survivor, then refresh tau
-          if (qlen > 0) {
-            round = drain = true;
-          } else {
-            tau = tk.kth == kKeyInf ? INFINITY : __uint_as_float((unsigned)(tk.kth >> 32));
-            cur_ep = tm.ep;
-          }
+        // the current epoch ends when the next own tile is from a later epoch, or at the end
+        // of the stream (then every epoch up to n_ep - 1 is closed)
+        if (ready ? tm.ep != cur_ep : cur_ep < n_ep) {
+          if (qlen > 0) round = drain = true;
+          else ep_end = true;
+        } else if (!ready) {
+          if (qlen == 0) break;
+          round = drain = true;
         }
       }
       if (round) {
         queue_round(drain);
+        continue;
+      }
+      if (ep_end) {
+        epoch_end();
+        ++cur_ep;
         continue;
       }
       // stage 1 (qlen < 32: the ring has room for 32 more): one row per lane, DD blocks
@@ -409,43 +477,60 @@ __global__ void __launch_bounds__(32, MINB) k_scan(const __grid_constant__ ScanP
       push(val && !prune, QEntry{tm.row0 + lane, s, DD, 0});
       if (stats) {
         const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
-        if (lane == 0 && np_) pruned[1] += np_;
+        if (lane == 0 && np_) atomicAdd(&pruned[1], (unsigned)np_);
       }
     }
 
+    // results: the register top-K (G = 1) or the merged list (G > 1)
+    if (G == 1) {
 #pragma unroll
-    for (int i = 0; i < KPL; ++i) {
-      const int pos = lane * KPL + i;
-      if (pos < K) {
-        const unsigned long long key = tk.k[i];
+      for (int i = 0; i < KPL; ++i) {
+        const int pos = lane * KPL + i;
+        if (pos < K) {
+          const unsigned long long key = tk.k[i];
+          p.out_ids[q * K + pos] = key == kKeyInf ? -1 : (int64_t)(uint32_t)(key & 0xffffffffu);
+          p.out_d[q * K + pos] = key == kKeyInf ? INFINITY : __uint_as_float((unsigned)(key >> 32));
+        }
+      }
+    } else {
+      const unsigned long long* Gfin = Gk + (cur_ep & 1) * K;
+      for (int pos = threadIdx.x; pos < K; pos += blockDim.x) {
+        const unsigned long long key = Gfin[pos];
         p.out_ids[q * K + pos] = key == kKeyInf ? -1 : (int64_t)(uint32_t)(key & 0xffffffffu);
         p.out_d[q * K + pos] = key == kKeyInf ? INFINITY : __uint_as_float((unsigned)(key >> 32));
       }
     }
-    if (lane == 0 && stats) atomicMax(p.counters + 3, (unsigned long long)(L > 0 ? cur_ep + 1 : 0));
-    __syncwarp();
+    if (threadIdx.x == 0 && stats) atomicMax(p.counters + 3, (unsigned long long)n_ep);
+    __syncthreads();  // qslot / lists / qs / Gk are rewritten for the next query
   }
   if (stats) {
     if (lane == 0) {
       atomicAdd(p.counters + 0, c_tested);
       atomicAdd(p.counters + 1, c_surv);
     }
-    __syncwarp();
-    for (int j = lane; j < DADE_MAX_STEPS; j += 32)
+    __syncthreads();
+    for (int j = threadIdx.x; j < DADE_MAX_STEPS; j += blockDim.x)
       if (pruned[j]) atomicAdd(p.counters + 4 + j, (unsigned long long)pruned[j]);
   }
 }
 
 template <int DD>
-static size_t scan_smem(int D, int nprobe) {
-  constexpr int kStages = DD == 1 ? 3 : 2;
-  return (size_t)kStages * TR * 64 * DD + 4 * 8 + kStages * sizeof(TileMeta) + kQCap * sizeof(QEntry) +
-         DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 + (size_t)D * 4;
+static size_t scan_smem(int D, int K, int nprobe, int G) {
+  return (size_t)G * Slice<DD>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
+         (size_t)((D + 3) & ~3) * 4 + (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
 
-template <int DD, int KPL, int LA, int MINB>
+// warps per query: enough CTAs x warps to fill the machine (2 resident waves of ~24 warps/SM)
+static int scan_group(int nq, int sms) {
+  const char* e = getenv("DADE_SCAN_G");
+  if (e) return atoi(e);
+  int G = 1;
+  while (G < 8 && (int64_t)nq * G < (int64_t)sms * 48) G *= 2;
+  return G;
+}
+
+template <int DD, int KPL, int LA, int MAXREG>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
-  const size_t smem = scan_smem<DD>(p.D, p.nprobe);
   static int sms = 0;
   static size_t attr = 0;
   if (!sms) {
@@ -453,15 +538,18 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
     DADE_CK(cudaGetDevice(&dev));
     DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  DADE_REQUIRE(smem <= 200 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, nprobe)");
+  const int G = scan_group(p.nq, sms);
+  DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
+  const size_t smem = scan_smem<DD>(p.D, p.K, p.nprobe, G);
+  DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
   if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
   int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MINB>, 32, smem));
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG>, 32 * G, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;
-  k_scan<DD, KPL, LA, MINB><<<p.nq < max_blocks ? p.nq : max_blocks, 32, smem, st>>>(p);
+  k_scan<DD, KPL, LA, MAXREG><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
 }
 
 // tuning variants (DADE_SCAN_VARIANT, read per launch) for the Delta_d = 16, K <= 32 kernel
@@ -474,13 +562,13 @@ template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
   if constexpr (DD == 1 && KPL == 1) {
     switch (scan_variant()) {
-      case 1: launch_v<DD, KPL, 2, 20>(p, st); return;
-      case 2: launch_v<DD, KPL, 1, 20>(p, st); return;
-      case 3: launch_v<DD, KPL, 1, 28>(p, st); return;
+      case 1: launch_v<DD, KPL, 2, 96>(p, st); return;
+      case 2: launch_v<DD, KPL, 1, 96>(p, st); return;
+      case 3: launch_v<DD, KPL, 1, 72>(p, st); return;
       default: break;
     }
   }
-  launch_v<DD, KPL, 1, 24>(p, st);
+  launch_v<DD, KPL, 1, (KPL >= 4 || DD >= 4) ? 96 : 80>(p, st);
 }
 
 template <int DD>

@@ -79,3 +79,29 @@ def test_c5_shape_logical_shards_alpha():
     mi, md = ix.merge_topk(torch.stack(gids), torch.stack(gds))
     oi, od = O.merge_shards(parts, cfg.k)
     assert tie_adjusted_overlap(mi.cpu().numpy(), md.cpu().numpy(), oi, od) >= 0.999
+
+
+_G_CFGS = {"c4": dict(n=20_000, nlist=64, nq=24, n_cal=100), "c5": dict(n=16_000, nlist=40, nq=10, n_cal=30)}
+
+
+@pytest.fixture(scope="module", params=["c4", "c5"])
+def g_setup(request):
+    cfg = synth.config(request.param, **_G_CFGS[request.param])
+    return cfg, _setup(cfg, nprobe_neg=6)
+
+
+@pytest.mark.parametrize("G", ["1", "2", "4", "8"])
+def test_warps_per_query_do_not_change_results(g_setup, G, monkeypatch):
+    # the scan deals a query's tiles to G warps with tau frozen per epoch (R13) and merges the
+    # warps' top-K lists exactly at each epoch end: decisions and results must not depend on G
+    # (K = 10: one key per lane; K = 100: four keys per lane)
+    cfg, (torch, ix, oidx, X, Xd) = g_setup
+    Q = torch.from_numpy(synth.queries(cfg)).cuda()
+    monkeypatch.setenv("DADE_SCAN_G", "1")
+    ri, rd, rs = ix.search(Q, cfg.k, 10, cfg.delta_d, 0.005, stats=True)
+    monkeypatch.setenv("DADE_SCAN_G", G)
+    gi, gd, gs = ix.search(Q, cfg.k, 10, cfg.delta_d, 0.005, stats=True)
+    assert torch.equal(ri, gi) and torch.equal(rd, gd)
+    assert rs["tested"] == gs["tested"] and rs["dims_scanned"] == gs["dims_scanned"]
+    assert rs["pruned_at_step"] == gs["pruned_at_step"]
+    _compare(torch, ix, oidx, synth.queries(cfg), cfg.k, 10, cfg.delta_d, 0.005)
