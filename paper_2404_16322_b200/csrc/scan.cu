@@ -206,16 +206,16 @@ struct Slice {
 // to the G warps (tile t -> warp t mod G); within an epoch every warp tests against the same
 // frozen tau (R13), so the split cannot change a decision; at each epoch end the warps' local
 // top-K lists are merged exactly (rank by binary search, smem) into the query's top-K.
-// CTA shared memory: G slices | pruned[64] | lists[nprobe] | qs[D] | (G > 1) W[G][K] + Gk[2][K] | qi.
-template <int DD, int KPL, int LA, int MAXREG>
+// CTA shared memory: G slices | pruned[64] | lists[nprobe] | qs[D] | qi | (G > 1) W[G][K] + Gk[2][K].
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI>
 __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   using SL = Slice<DD>;
   constexpr int kStages = SL::kStages;
   constexpr int TB = SL::TB;
   const int D = p.D, K = p.K;
-  const int G = blockDim.x >> 5;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = MULTI ? (blockDim.x >> 5) : 1;  // warps per query (power of two)
+  const int lane = threadIdx.x & 31, warp = MULTI ? threadIdx.x >> 5 : 0;
   unsigned char* base = smem + warp * SL::bytes;
   unsigned char* tiles = base;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
@@ -224,9 +224,9 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   unsigned* pruned = reinterpret_cast<unsigned*>(smem + G * SL::bytes);
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
-  unsigned long long* W = reinterpret_cast<unsigned long long*>(qs + ((D + 3) & ~3));  // G x K
-  unsigned long long* Gk = W + (size_t)G * K;                                         // 2 x K
-  int* qslot = reinterpret_cast<int*>(Gk + 2 * K);
+  int* qslot = reinterpret_cast<int*>(qs + ((D + 3) & ~3));
+  unsigned long long* W = reinterpret_cast<unsigned long long*>(qslot + 4);  // G x K (G > 1)
+  unsigned long long* Gk = W + (size_t)G * K;                               // 2 x K (G > 1)
 
   const bool stats = p.counters != nullptr;
   if (stats)
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const int s0 = p.off[l];
       lists[j] = make_int2(s0, p.off[l + 1] - s0);
     }
-    if (G > 1)
+    if (MULTI)
       for (int j = threadIdx.x; j < K; j += blockDim.x) Gk[j] = kKeyInf;
     __syncthreads();
     int L = 0;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         nr = min(min(pe_hi, ppos + pl.y) - pr, TR);
         row0 = pl.x + (pr - ppos);
         pr += nr;
-        if (tix++ % G == warp) break;
+        if (!MULTI || (tix++ & (G - 1)) == warp) break;
       }
       if (lane == 0) {
         meta[slot] = TileMeta{row0, nr, pep, 0};
@@ -373,14 +373,14 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       push(alive && blk < nblk && sub == 0, QEntry{e.row, phi, blk, 0});
       if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
       const unsigned long long key = fin ? make_key(phi, gid) : kKeyInf;
-      tk.offer(key < cap ? key : kKeyInf, lane);
+      tk.offer(!MULTI || key < cap ? key : kKeyInf, lane);
     };
 
     // End of epoch cur_ep (every survivor of this warp finished): refresh tau (R13). G > 1: merge
     // the warps' local lists with the query list: the rank of a key in the union is its own
     // index plus its lower bounds in the other sorted lists (keys are unique).
     auto epoch_end = [&]() {
-      if (G == 1) {
+      if (!MULTI) {
         tau = tk.kth == kKeyInf ? INFINITY : __uint_as_float((unsigned)(tk.kth >> 32));
         return;
       }
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     }
 
     // results: the register top-K (G = 1) or the merged list (G > 1)
-    if (G == 1) {
+    if (!MULTI) {
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const int pos = lane * KPL + i;
@@ -529,10 +529,24 @@ static int scan_group(int nq, int sms) {
   return G;
 }
 
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI>
+static void launch_g(const ScanParams& p, cudaStream_t st, int G, int sms) {
+  const size_t smem = scan_smem<DD>(p.D, p.K, p.nprobe, G);
+  DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
+  static size_t attr = 0;
+  if (smem > attr) {
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  int occ = 0;
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG, MULTI>, 32 * G, smem));
+  const int max_blocks = (occ > 0 ? occ : 1) * sms;
+  k_scan<DD, KPL, LA, MAXREG, MULTI><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
+}
+
 template <int DD, int KPL, int LA, int MAXREG>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
   static int sms = 0;
-  static size_t attr = 0;
   if (!sms) {
     int dev;
     DADE_CK(cudaGetDevice(&dev));
@@ -540,16 +554,8 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
   }
   const int G = scan_group(p.nq, sms);
   DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
-  const size_t smem = scan_smem<DD>(p.D, p.K, p.nprobe, G);
-  DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
-  if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG>, 32 * G, smem));
-  const int max_blocks = (occ > 0 ? occ : 1) * sms;
-  k_scan<DD, KPL, LA, MAXREG><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
+  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false>(p, st, 1, sms);
+  else launch_g<DD, KPL, LA, MAXREG, true>(p, st, G, sms);
 }
 
 // tuning variants (DADE_SCAN_VARIANT, read per launch) for the Delta_d = 16, K <= 32 kernel
