@@ -155,6 +155,32 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   DADE_REQUIRE(k >= 1 && k <= n, DADE_ERR_ARG, "exact_knn: k out of range");
   DADE_REQUIRE(k <= 4096, DADE_ERR_UNSUPPORTED, "exact_knn: k > 4096");
   DADE_REQUIRE(bop.rows == n, DADE_ERR_STATE, "exact_knn: operand not prepared");
+  if (!x->flag.p) {
+    x->flag.reserve(1);
+    DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+  }
+  const int64_t ng = (n + 31) / 32;
+  // group-minima-only path (no d_hat matrix): measured slower than the d_hat path at k <= 32
+  // (32 exact fp64 columns per candidate group, uncoalesced); kept for very wide rows
+  if (k <= 512 && (int64_t)k * 4 <= ng && n > (int64_t)1 << 20) {
+    // the GEMM writes only 32-column group minima; exact fp64 distances for the columns of the
+    // groups inside the certified window (no m x n d_hat matrix)
+    int64_t chunk = std::max<int64_t>(128, ((int64_t)1 << 27) / ng / 128 * 128);
+    chunk = std::min<int64_t>(chunk, tc_rows_pad(m));
+    x->slack.reserve((size_t)chunk);
+    x->gmin.reserve((size_t)chunk * ng);
+    for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+      const int64_t mm = std::min(chunk, m - r0);
+      tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
+      launch_l2_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
+                   nullptr, 0, x->stream, x->gmin.p);
+      launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream);
+      launch_select_groups(x->gmin.p, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
+                           out_d64 ? out_d64 + r0 * k : nullptr, x->slack.p, x->stream);
+    }
+    if (sync) check_knn_flag(x);
+    return;
+  }
   const int64_t budget = (int64_t)1 << 29;  // floats of d_hat per chunk (2 GiB)
   int64_t chunk = std::max<int64_t>(128, budget / std::max<int64_t>(n, 1) / 128 * 128);
   const int cand_cap = 4096;

@@ -87,6 +87,10 @@ void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_
                         const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
                         int* d_flag, const float* slack, int* ovf_n, int32_t* ovf_rows,
                         cudaStream_t st);
+// k nearest columns from the filter GEMM's 32-column group minima only (no d_hat matrix):
+// exact fp64 distances for every column of the groups inside the certified window (k <= 512)
+void launch_select_groups(const float* gmin, int64_t m, int64_t n, int k, const float* A, const float* B,
+                          int D, int32_t* out_idx, double* out_d64, const float* slack, cudaStream_t st);
 void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st);
 
 // rotate.cu : x~ = R (x - mu) with fp64 accumulation, stored fp32.

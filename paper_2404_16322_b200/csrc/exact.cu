@@ -446,6 +446,137 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   }
 }
 
+// ------------------------------------------------------------------ group select (no d_hat)
+// The filter GEMM wrote only the per-row minima of d_hat over 32-column groups (gm[row][g]). Every
+// group minimum is some column's d_hat, so the k-th smallest group minimum E bounds the k-th
+// smallest d_hat from above; every true k-nearest column therefore has d_hat <= thr(E) (window of
+// abs_thr_bits) and lies in a group with gm <= thr(E). All columns of those groups get their
+// exact fp64 distance (one lane per column) and the k smallest by (dist, column) are kept: a
+// running top-k in shared memory (chunks of kGsCap - k new candidates, bitonic sort, truncate).
+constexpr int kGsWarps = 4;
+constexpr int kGsCap = 1024;
+
+__global__ void __launch_bounds__(kGsWarps * 32) k_select_groups(
+    const float* __restrict__ gm, int64_t m, int64_t n, int k, const float* __restrict__ A,
+    const float* __restrict__ B, int D, int32_t* __restrict__ out_idx, double* __restrict__ out_d,
+    const float* __restrict__ slack) {
+  extern __shared__ __align__(16) unsigned char gs_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* cd = reinterpret_cast<double*>(gs_smem) + (size_t)w * kGsCap;
+  int32_t* cc = reinterpret_cast<int32_t*>(reinterpret_cast<double*>(gs_smem) + (size_t)kGsWarps * kGsCap) +
+                (size_t)w * kGsCap;
+  unsigned* hist = reinterpret_cast<unsigned*>(reinterpret_cast<int32_t*>(
+                       reinterpret_cast<double*>(gs_smem) + (size_t)kGsWarps * kGsCap) + (size_t)kGsWarps * kGsCap) +
+                   w * 256;
+  const int64_t row = (int64_t)blockIdx.x * kGsWarps + w;
+  if (row >= m) return;
+  const int ng = (int)((n + 31) / 32);
+  const float* g = gm + row * ng;
+  // 1. E = k-th smallest group minimum: radix select on the float bits (non-negative)
+  unsigned prefix = 0;
+  int krem = k;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
+    for (int i = lane; i < ng; i += 32) {
+      const unsigned v = __float_as_uint(g[i]);
+      if (shift == 24 || ((v ^ prefix) >> (shift + 8)) == 0) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    unsigned h[8], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { h[j] = hist[lane * 8 + j]; tot += h[j]; }
+    unsigned inc = tot;  // inclusive scan over lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    unsigned before = inc - tot;
+    const bool mine = before < (unsigned)krem && (unsigned)krem <= inc;
+    int bin = 0;
+    unsigned below = 0;
+    if (mine) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (before + h[j] >= (unsigned)krem) { bin = lane * 8 + j; below = before; break; }
+        before += h[j];
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, mine);
+    const int src = __ffs(bal) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    below = __shfl_sync(0xffffffffu, below, src);
+    prefix |= (unsigned)bin << shift;
+    krem -= (int)below;
+    __syncwarp();
+  }
+  const unsigned tb = abs_thr_bits(__uint_as_float(prefix), slack[row]);
+  // 2. exact distances of every column of every group inside the window; running top-k
+  const float* a = A + row * (int64_t)D;
+  for (int i = lane; i < k; i += 32) { cd[i] = DBL_MAX; cc[i] = 0x7fffffff; }
+  int cnt = k;  // slots [0, k) hold the running top-k
+  auto compact = [&]() {  // sort slots [0, cnt) (padded to a power of two) and keep the first k
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    for (int i = cnt + lane; i < P; i += 32) { cd[i] = DBL_MAX; cc[i] = 0x7fffffff; }
+    __syncwarp();
+    for (int size = 2; size <= P; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = lane; i < P / 2; i += 32) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const double x = cd[lo], y = cd[hi];
+          const int32_t xc = cc[lo], yc = cc[hi];
+          if (cand_less2(y, yc, x, xc) == up) { cd[lo] = y; cd[hi] = x; cc[lo] = yc; cc[hi] = xc; }
+        }
+        __syncwarp();
+      }
+    cnt = k;
+  };
+  for (int g0 = 0; g0 < ng; g0 += 32) {
+    const int gi = g0 + lane;
+    const bool in = gi < ng && __float_as_uint(g[gi]) <= tb;
+    unsigned bal = __ballot_sync(0xffffffffu, in);
+    while (bal) {
+      const int grp = g0 + __ffs(bal) - 1;
+      bal &= bal - 1;
+      if (cnt + 32 > kGsCap) compact();
+      const int64_t c = (int64_t)grp * 32 + lane;
+      if (c < n) {
+        cd[cnt + lane] = exact_sqdist(a, B + c * D, D);
+        cc[cnt + lane] = (int32_t)c;
+      } else {
+        cd[cnt + lane] = DBL_MAX;
+        cc[cnt + lane] = 0x7fffffff;
+      }
+      cnt += 32;
+      __syncwarp();
+    }
+  }
+  compact();
+  for (int i = lane; i < k; i += 32) {
+    const bool ok = cd[i] != DBL_MAX;
+    out_idx[row * k + i] = ok ? cc[i] : -1;
+    if (out_d) out_d[row * k + i] = ok ? cd[i] : DBL_MAX;
+  }
+}
+
+void launch_select_groups(const float* gmin, int64_t m, int64_t n, int k, const float* A, const float* B,
+                          int D, int32_t* out_idx, double* out_d64, const float* slack, cudaStream_t st) {
+  if (m <= 0) return;
+  DADE_REQUIRE(k >= 1 && k <= 512, DADE_ERR_UNSUPPORTED, "group select: k > 512");
+  const size_t smem = (size_t)kGsWarps * kGsCap * 12 + (size_t)kGsWarps * 256 * 4;
+  static bool attr = false;
+  if (!attr) {
+    DADE_CK(cudaFuncSetAttribute(k_select_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k_select_groups<<<(unsigned)((m + kGsWarps - 1) / kGsWarps), kGsWarps * 32, smem, st>>>(
+      gmin, m, n, k, A, B, D, out_idx, out_d64, slack);
+  DADE_CK(cudaGetLastError());
+}
+
 void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_t n, int k,
                         const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
                         int* d_flag, const float* slack, int* ovf_n, int32_t* ovf_rows,

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
         if (c0 + j < n) mn = fminf(mn, fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j])));
       if (c0 < n) gmin[row * ldg + (c0 >> 5)] = mn;
     }
-    if (row < m) {
+    if (out && row < m) {  // out == nullptr: group minima only (k_select_groups)
       float* o = out + row * ldo + c0;
       if (c0 + 32 <= n && (ldo & 3) == 0) {
 #pragma unroll
