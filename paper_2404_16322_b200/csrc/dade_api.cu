@@ -159,6 +159,30 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     x->flag.reserve(1);
     DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
   }
+  // fused path for wide rows (measured: faster than the d_hat path from nlist ~8k on; slower at
+  // 4096); DADE_FUSED_PROBE=0/1 forces either path (tests cover both)
+  const char* fz = getenv("DADE_FUSED_PROBE");
+  const bool fused = k <= 64 && n >= 256 && (fz ? atoi(fz) != 0 : n >= 8192);
+  if (fused) {
+    // fused filter GEMM + candidate tracking (probe_tc.cu): no m x n d_hat matrix
+    static int sms = 0;
+    if (!sms) DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device));
+    const int64_t chunk = std::min<int64_t>(tc_rows_pad(m), 65536);
+    const int nsplit = probe_tc_splits(chunk, n, sms);
+    const int C = probe_tc_cap(k);
+    x->slack.reserve((size_t)chunk);
+    x->cand.reserve((size_t)chunk * nsplit * C * 2 + (size_t)chunk * nsplit);
+    for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+      const int64_t mm = std::min(chunk, m - r0);
+      tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
+      launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream);
+      launch_probe_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D, k,
+                      x->slack.p, A + r0 * D, B, x->cand.p, x->cand.p + (size_t)chunk * nsplit * C * 2, nsplit,
+                      out_idx + r0 * k, out_d64 ? out_d64 + r0 * k : nullptr, x->stream);
+    }
+    if (sync) check_knn_flag(x);
+    return;
+  }
   const int64_t ng = (n + 31) / 32;
   // group-minima-only path (no d_hat matrix): measured slower than the d_hat path at k <= 32
   // (32 exact fp64 columns per candidate group, uncoalesced); kept for very wide rows

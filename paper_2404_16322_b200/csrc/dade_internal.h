@@ -91,6 +91,14 @@ void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_
 // exact fp64 distances for every column of the groups inside the certified window (k <= 512)
 void launch_select_groups(const float* gmin, int64_t m, int64_t n, int k, const float* A, const float* B,
                           int D, int32_t* out_idx, double* out_d64, const float* slack, cudaStream_t st);
+// probe_tc.cu: fused filter GEMM + candidate tracking (no d_hat matrix) + exact finish, k <= 64.
+// cand: m * nsplit * probe_tc_cap(k) * 2 int32 scratch, ccount: m * nsplit int32 scratch.
+int probe_tc_cap(int k);
+int probe_tc_splits(int64_t m, int64_t n, int sms);
+void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
+                     const float* Blo, const float* bn, int64_t n, int D, int k, const float* slack,
+                     const float* A, const float* B, int32_t* cand, int32_t* ccount, int nsplit,
+                     int32_t* out_idx, double* out_d64, cudaStream_t st);
 void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st);
 
 // rotate.cu : x~ = R (x - mu) with fp64 accumulation, stored fp32.

@@ -1,0 +1,527 @@
+// a5 probe (and every exact k-nearest search with small k): the tensor-core distance filter FUSED
+// with the candidate selection, so the m x n matrix of filter distances is never written.
+//
+// Definition (R20): the k nearest columns of every row under the EXACT fp64 sequential
+// sum of squared differences, ordered by (dist, column). The filter d_hat and its rigorous error
+// window are those of gemm_tf32.cu (centred 3-pass tf32 tcgen05 GEMM): every column whose exact
+// distance can be among the k smallest satisfies d_hat <= thr(t), t = the k-th smallest d_hat,
+// thr(v) = (v + slack)(1 + delta)/(1 - delta) + slack.
+//
+// k_probe_tc: CTA = 128 rows x a contiguous range of column tiles (grid.y splits the columns).
+// Warp specialisation: warp 0 = TMA producer (bulk copies of pre-split operand chunks into a
+// 2-stage ring), warp 1 = MMA issuer (one thread, tcgen05.mma kind::tf32 x3 per k-step into one
+// of two 128-column TMEM accumulators), warps 2-5 = epilogue (tcgen05.ld, one thread per row).
+// The epilogue keeps, per row, the k smallest d_hat seen so far (sorted, shared memory) and the
+// list of every column with d_hat <= thr(current k-th); a column above the threshold costs one
+// compare. Since t_split >= t (the split sees a subset), thr(t_split) >= thr(t): the union of
+// the splits' lists contains every exact k-nearest column.
+// k_probe_finish: warp per row, exact fp64 distances of the union (candidate rows staged in
+// shared memory so global loads stay coalesced), bitonic sort by (dist, column), first k out.
+// A row whose list overflowed is finished by an exact scan of all n columns (correct, slow).
+#include <cfloat>
+#include <cstdint>
+#include <cstdlib>
+
+#include "dade_internal.h"
+
+namespace dade {
+
+namespace {
+constexpr int kTM = 128;
+constexpr int kKC = 16;
+constexpr int kSub = kTM * kKC;            // floats per (tile, chunk) block
+constexpr int kSBO = (kKC / 4) * 128;
+constexpr int kStageBytes = 4 * kSub * 4;  // A_hi, A_lo, B_hi, B_lo = 32 KB
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(const void* smem, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(smem) >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                          \
+  asm volatile(                                                                                      \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                      \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), \
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), \
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                         \
+      : "r"(taddr))
+
+constexpr unsigned kAll = 0x7fffffffu;  // window that accepts every value (signed compare)
+
+// certified window of the filter (gemm_tf32.cu): bits of thr(v), rounded up
+__device__ __forceinline__ unsigned win_bits(float v, float slack) {
+  const double delta = 9.5367431640625e-07;  // 2^-20
+  const double T = ((double)v + (double)slack) * (1.0 + delta) / (1.0 - delta) + (double)slack;
+  const float tf = (float)T;
+  if (!(tf >= 0.f)) return kAll;
+  const unsigned b = __float_as_uint(tf);
+  return b >= 0x7f800000u ? kAll : b + 2u;
+}
+
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// smem: stages | bars | per-row S[k][128] (floats) | Lv[C][128] | Lc[C][128]
+__global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
+    const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ an,
+    const float* __restrict__ Bhi, const float* __restrict__ Blo, const float* __restrict__ bn, int nkc,
+    int64_t m, int64_t n, int tiles_per_split, int k, int C, const float* __restrict__ slack,
+    int32_t* __restrict__ cand, int32_t* __restrict__ ccount, int dbg) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* S = reinterpret_cast<float*>(sm + kStages * kStageBytes + 128);
+  float* Lv = S + (size_t)k * kTM;
+  int32_t* Lc = reinterpret_cast<int32_t*>(Lv + (size_t)C * kTM);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tm = blockIdx.x;
+  const int64_t ntiles = (n + kTM - 1) / kTM;
+  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
+  const int64_t rem = ntiles - t0;
+  const int nt = rem <= 0 ? 0 : (int)(rem < tiles_per_split ? rem : tiles_per_split);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int it = 0;
+      for (int t = 0; t < nt; ++t) {
+        const int64_t tn = t0 + t;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % kStages;
+          if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          unsigned char* st = sm + s * kStageBytes;
+          mbar_expect_tx(&full[s], kStageBytes);
+          const int64_t ao = (tm * nkc + kc) * kSub, bo = (tn * nkc + kc) * kSub;
+          bulk_g2s(st, Ahi + ao, kSub * 4, &full[s]);
+          bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
+          bulk_g2s(st + 2 * kSub * 4, Bhi + bo, kSub * 4, &full[s]);
+          bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+      int it = 0;
+      for (int t = 0; t < nt; ++t) {
+        const int b = t & 1;
+        if (t >= 2) mbar_wait(&tempty[b], ((t >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + b * kTM;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          unsigned char* st = sm + s * kStageBytes;
+#pragma unroll
+          for (int j = 0; j < kKC / 8; ++j) {
+            const uint64_t ah = umma_desc(st + j * 256, 128, kSBO);
+            const uint64_t al = umma_desc(st + kSub * 4 + j * 256, 128, kSBO);
+            const uint64_t bh = umma_desc(st + 2 * kSub * 4 + j * 256, 128, kSBO);
+            const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
+            mma_tf32(acc, ah, bh, idesc, (kc | j) != 0);
+            mma_tf32(acc, ah, bl, idesc, 1);
+            mma_tf32(acc, al, bh, idesc, 1);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[b]);
+      }
+    }
+  } else {  // ---------------- epilogue: one thread per row
+    // Per row: the list L of every column whose d_hat was <= the window bits thr at the time it
+    // was seen. L always contains the k smallest d_hat seen (thr >= thr(k-th) >= k-th), so
+    // reduce() can recompute the exact k-th smallest from L alone, tighten thr and drop the
+    // entries above it. Appends are branch-free (predicated, unrolled); reduce() runs only when
+    // L fills up or thr is still open.
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r = q * 32 + lane;
+    const int64_t row = tm * kTM + r;
+    const bool live = row < m;
+    const float a2 = live ? an[row] : 0.f;
+    const float sl = live ? slack[row] : 0.f;
+    unsigned thr = kAll;
+    int nl = 0;
+    bool ovf = false;
+    auto reduce = [&]() {
+      int ns = 0;
+      for (int i = 0; i < nl; ++i) {  // k smallest of L, ascending, into S
+        const float v = Lv[i * kTM + r];
+        if (ns < k || v < S[(k - 1) * kTM + r]) {
+          int pos = ns < k ? ns++ : k - 1;
+          while (pos > 0 && S[(pos - 1) * kTM + r] > v) {
+            S[pos * kTM + r] = S[(pos - 1) * kTM + r];
+            --pos;
+          }
+          S[pos * kTM + r] = v;
+        }
+      }
+      if (ns < k) return;
+      thr = win_bits(S[(k - 1) * kTM + r], sl);
+      int j = 0;
+      for (int i = 0; i < nl; ++i) {
+        const float v = Lv[i * kTM + r];
+        if (__float_as_uint(v) <= thr) {
+          Lv[j * kTM + r] = v;
+          Lc[j * kTM + r] = Lc[i * kTM + r];
+          ++j;
+        }
+      }
+      nl = j;
+    };
+    for (int t = 0; t < nt; ++t) {
+      const int b = t & 1;
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t cb0 = (t0 + t) * kTM;
+#pragma unroll 1
+      for (int cb = 0; cb < kTM / 32; ++cb) {
+        uint32_t v[32];
+        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + b * kTM + cb * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (cb == kTM / 32 - 1) {  // the accumulator may be overwritten from here on
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        const int64_t c0 = cb0 + cb * 32;
+        if (dbg) continue;  // dbg: timing of the GEMM pipeline alone
+        // d_hat = max(0, fma(-2, acc, a2 + bn)) in packed FP32x2 (same roundings as the scalar
+        // form); the max(0, .) is applied on append only: as signed ints, negative d compare
+        // below any window, like 0 does
+        float d[32];
+        unsigned mask = 0;
+        const float2* bn2 = reinterpret_cast<const float2*>(bn + c0);  // bn is padded to 128
+        const unsigned long long a2p = pk2(a2, a2), m2 = pk2(-2.f, -2.f);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float2 bb = __ldg(bn2 + jj);
+          const unsigned long long x = fma2(m2, pk2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1])),
+                                            add2(a2p, pk2(bb.x, bb.y)));
+          const float2 xf = *reinterpret_cast<const float2*>(&x);
+          d[2 * jj] = xf.x;
+          d[2 * jj + 1] = xf.y;
+          mask |= (unsigned)((int)__float_as_uint(xf.x) <= (int)thr) << (2 * jj);
+          mask |= (unsigned)((int)__float_as_uint(xf.y) <= (int)thr) << (2 * jj + 1);
+        }
+        {
+          const int64_t valid = live ? n - c0 : 0;
+          mask &= valid >= 32 ? 0xffffffffu : valid <= 0 ? 0u : ((1u << valid) - 1u);
+        }
+        // list maintenance is warp-synchronous (every lane reduces when any lane must), so the
+        // warp never serialises per-lane slow paths
+        if (__any_sync(0xffffffffu, nl + __popc(mask) > C)) {
+          reduce();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if ((int)__float_as_uint(d[j]) > (int)thr) mask &= ~(1u << j);
+          if (nl + __popc(mask) > C) { ovf = true; mask = 0; }  // k_probe_finish rescans the row
+        }
+        if (__any_sync(0xffffffffu, mask != 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const bool on = (mask >> j) & 1u;
+            if (on) {
+              Lv[nl * kTM + r] = fmaxf(0.f, d[j]);
+              Lc[nl * kTM + r] = (int32_t)(c0 + j);
+            }
+            nl += on;
+          }
+          if (__any_sync(0xffffffffu, nl >= k && (thr == kAll || 2 * nl > C))) reduce();
+        }
+      }
+    }
+    if (live && dbg) ccount[row * gridDim.y + blockIdx.y] = 0;
+    if (live && !dbg) {
+      if (nl >= k) reduce();
+      const int64_t slot = row * gridDim.y + blockIdx.y;
+      for (int i = 0; i < nl; ++i) {  // (column, d_hat bits) pairs
+        cand[(slot * C + i) * 2] = Lc[i * kTM + r];
+        cand[(slot * C + i) * 2 + 1] = (int32_t)__float_as_uint(Lv[i * kTM + r]);
+      }
+      ccount[slot] = ovf ? -1 : nl;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+__device__ __forceinline__ bool cless(double d0, int32_t c0, double d1, int32_t c1) {
+  return d0 < d1 || (d0 == d1 && c0 < c1);
+}
+
+constexpr int kFinWarps = 4;
+constexpr int kFinCap = 512;   // candidates per row held at once (running top-k beyond that)
+constexpr int kFinDim = 64;    // dims staged per pass
+
+// exact distances of up to 32 candidate columns (one per lane; c < 0 = none), accumulated
+// sequentially over j = 0..D-1 in fp64 (R20); rows staged through shared memory in 64-dim slices
+__device__ __forceinline__ double exact_batch(const float* __restrict__ a, const float* __restrict__ B, int D,
+                                              int32_t c, float* stage, int lane) {
+  double acc = 0.0;
+  for (int j0 = 0; j0 < D; j0 += kFinDim) {
+    const int w = min(kFinDim, D - j0);
+    for (int i = 0; i < 32; ++i) {  // candidate i's slice, coalesced
+      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
+      if (ci >= 0)
+        for (int jj = lane; jj < w; jj += 32) stage[i * (kFinDim + 1) + jj] = __ldg(B + (int64_t)ci * D + j0 + jj);
+    }
+    __syncwarp();
+    if (c >= 0) {
+      const float* sr = stage + lane * (kFinDim + 1);
+      for (int jj = 0; jj < w; ++jj) {
+        const double t = __dsub_rn((double)a[j0 + jj], (double)sr[jj]);
+        acc = __dadd_rn(acc, __dmul_rn(t, t));
+      }
+    }
+    __syncwarp();
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
+    const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount, int nsplit, int C, int64_t m,
+    int64_t n, int k, const float* __restrict__ A, const float* __restrict__ B, int D,
+    const float* __restrict__ slack, int32_t* __restrict__ out_idx, double* __restrict__ out_d) {
+  extern __shared__ __align__(16) unsigned char fs[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* cd = reinterpret_cast<double*>(fs) + (size_t)w * kFinCap;
+  int32_t* cc = reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) + (size_t)kFinWarps * kFinCap) + (size_t)w * kFinCap;
+  float* stage = reinterpret_cast<float*>(reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) + (size_t)kFinWarps * kFinCap) +
+                                          (size_t)kFinWarps * kFinCap) + (size_t)w * 32 * (kFinDim + 1);
+  int32_t* sel = reinterpret_cast<int32_t*>(reinterpret_cast<float*>(reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) +
+                   (size_t)kFinWarps * kFinCap) + (size_t)kFinWarps * kFinCap) + (size_t)kFinWarps * 32 * (kFinDim + 1)) +
+                 (size_t)kFinWarps * 256 + (size_t)w * kFinCap;
+  unsigned* hist = reinterpret_cast<unsigned*>(reinterpret_cast<float*>(reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) +
+                                     (size_t)kFinWarps * kFinCap) + (size_t)kFinWarps * kFinCap) +
+                                     (size_t)kFinWarps * 32 * (kFinDim + 1)) + w * 256;
+  const int64_t row = (int64_t)blockIdx.x * kFinWarps + w;
+  if (row >= m) return;
+  const float* a = A + row * (int64_t)D;
+  bool full_scan = false;
+  int total = 0;
+  for (int s = 0; s < nsplit; ++s) {
+    const int c = ccount[row * nsplit + s];
+    full_scan |= c < 0;
+    total += c < 0 ? 0 : c;
+  }
+  for (int i = lane; i < k; i += 32) { cd[i] = DBL_MAX; cc[i] = 0x7fffffff; }
+  int cnt = k;
+  auto compact = [&]() {
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    for (int i = cnt + lane; i < P; i += 32) { cd[i] = DBL_MAX; cc[i] = 0x7fffffff; }
+    __syncwarp();
+    for (int size = 2; size <= P; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = lane; i < P / 2; i += 32) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const double x = cd[lo], y = cd[hi];
+          const int32_t xc = cc[lo], yc = cc[hi];
+          if (cless(y, yc, x, xc) == up) { cd[lo] = y; cd[hi] = x; cc[lo] = yc; cc[hi] = xc; }
+        }
+        __syncwarp();
+      }
+    cnt = k;
+  };
+  auto add32 = [&](int32_t c) {  // one candidate per lane (c < 0: none)
+    if (cnt + 32 > kFinCap) compact();
+    const double d = exact_batch(a, B, D, c, stage, lane);
+    cd[cnt + lane] = c >= 0 ? d : DBL_MAX;
+    cc[cnt + lane] = c >= 0 ? c : 0x7fffffff;
+    cnt += 32;
+    __syncwarp();
+  };
+  if (full_scan || total < k) {
+    for (int64_t c0 = 0; c0 < n; c0 += 32) add32(c0 + lane < n ? (int32_t)(c0 + lane) : -1);
+  } else {
+    // E = k-th smallest d_hat of the union (it holds every split's k smallest): radix select
+    unsigned prefix = 0;
+    int krem = k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = lane; i < 256; i += 32) hist[i] = 0;
+      __syncwarp();
+      for (int s = 0; s < nsplit; ++s) {
+        const int nc = ccount[row * nsplit + s];
+        const int32_t* cl = cand + (row * nsplit + s) * (int64_t)C * 2;
+        for (int i = lane; i < nc; i += 32) {
+          const unsigned v = (unsigned)cl[2 * i + 1];
+          if (shift == 24 || ((v ^ prefix) >> (shift + 8)) == 0) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+        }
+      }
+      __syncwarp();
+      unsigned h[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { h[j] = hist[lane * 8 + j]; tot += h[j]; }
+      unsigned inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      unsigned before = inc - tot;
+      const bool mine = before < (unsigned)krem && (unsigned)krem <= inc;
+      int bin = 0;
+      unsigned below = 0;
+      if (mine) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (before + h[j] >= (unsigned)krem) { bin = lane * 8 + j; below = before; break; }
+          before += h[j];
+        }
+      }
+      const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+      bin = __shfl_sync(0xffffffffu, bin, src);
+      below = __shfl_sync(0xffffffffu, below, src);
+      prefix |= (unsigned)bin << shift;
+      krem -= (int)below;
+      __syncwarp();
+    }
+    const unsigned tb = win_bits(__uint_as_float(prefix), slack[row]);
+    // the union's columns inside the global window, ballot-compacted into a list, then exact
+    // distances 32 at a time
+    int np = 0;
+    for (int s = 0; s < nsplit; ++s) {
+      const int nc = ccount[row * nsplit + s];
+      const int32_t* cl = cand + (row * nsplit + s) * (int64_t)C * 2;
+      for (int i0 = 0; i0 < nc; i0 += 32) {
+        const int i = i0 + lane;
+        const bool in = i < nc && (unsigned)cl[2 * i + 1] <= tb;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        const int pos = np + __popc(bal & ((1u << lane) - 1));
+        if (in && pos < kFinCap) sel[pos] = cl[2 * i];
+        np += __popc(bal);
+      }
+    }
+    __syncwarp();
+    if (np > kFinCap) {  // cannot happen for nsplit * C <= kFinCap; stay exact anyway
+      for (int64_t c0 = 0; c0 < n; c0 += 32) add32(c0 + lane < n ? (int32_t)(c0 + lane) : -1);
+    } else {
+      for (int i0 = 0; i0 < np; i0 += 32) add32(i0 + lane < np ? sel[i0 + lane] : -1);
+    }
+  }
+  compact();
+  for (int i = lane; i < k; i += 32) {
+    const bool ok = cd[i] != DBL_MAX;
+    out_idx[row * k + i] = ok ? cc[i] : -1;
+    if (out_d) out_d[row * k + i] = ok ? cd[i] : DBL_MAX;
+  }
+}
+}  // namespace
+
+int probe_tc_cap(int k) { return k + 32; }
+
+int probe_tc_splits(int64_t m, int64_t n, int sms) {
+  const int64_t mt = (m + kTM - 1) / kTM, nt = (n + kTM - 1) / kTM;
+  int64_t s = 1;
+  while (mt * s < 2 * sms && s * 2 <= nt / 2) s *= 2;  // >= 2 tiles per split
+  return (int)s;
+}
+
+void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
+                     const float* Blo, const float* bn, int64_t n, int D, int k, const float* slack,
+                     const float* A, const float* B, int32_t* cand, int32_t* ccount, int nsplit,
+                     int32_t* out_idx, double* out_d64, cudaStream_t st) {
+  if (m <= 0) return;
+  const int C = probe_tc_cap(k);
+  const size_t smem = kStages * kStageBytes + 128 + (size_t)kTM * (k * 4 + C * 8);
+  DADE_REQUIRE(smem <= 227 * 1024, DADE_ERR_UNSUPPORTED, "probe: k too large for the fused filter");
+  static size_t attr = 0;
+  if (smem > attr) {
+    DADE_CK(cudaFuncSetAttribute(k_probe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const int64_t ntiles = (n + kTM - 1) / kTM;
+  const int tps = (int)((ntiles + nsplit - 1) / nsplit);
+  dim3 grid((unsigned)((m + kTM - 1) / kTM), (unsigned)nsplit);
+  const int dbg = getenv("DADE_PROBE_DBG") ? atoi(getenv("DADE_PROBE_DBG")) : 0;
+  k_probe_tc<<<grid, kThreads, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), m, n, tps, k, C, slack, cand,
+                                          ccount, dbg);
+  DADE_CK(cudaGetLastError());
+  const size_t fsm = (size_t)kFinWarps * kFinCap * 12 + (size_t)kFinWarps * 32 * (kFinDim + 1) * 4 +
+                     (size_t)kFinWarps * 256 * 4 + (size_t)kFinWarps * kFinCap * 4;
+  static bool fattr = false;
+  if (!fattr) {
+    DADE_CK(cudaFuncSetAttribute(k_probe_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    fattr = true;
+  }
+  k_probe_finish<<<(unsigned)((m + kFinWarps - 1) / kFinWarps), kFinWarps * 32, fsm, st>>>(
+      cand, ccount, nsplit, C, m, n, k, A, B, D, slack, out_idx, out_d64);
+  DADE_CK(cudaGetLastError());
+}
+
+}  // namespace dade

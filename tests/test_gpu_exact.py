@@ -7,6 +7,14 @@ from oracle import dade_oracle as O
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["0", "1"], ids=["dhat-matrix", "fused-filter"])
+def knn_path(request, monkeypatch):
+    # both selection paths: the d_hat-matrix select (exact.cu) and the fused filter GEMM with
+    # in-epilogue candidate tracking (probe_tc.cu); each must be bit-exact
+    monkeypatch.setenv("DADE_FUSED_PROBE", request.param)
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def torch_cuda():
     import torch
@@ -65,3 +73,23 @@ def test_probe_and_assign_bit_exact(torch_cuda):
     pr = ix.probe(torch.from_numpy(Q).cuda(), 31).cpu().numpy()
     for q in range(25):
         assert pr[q].tolist() == O.probe(Q[q], cent, 31).tolist()
+
+
+@pytest.mark.parametrize("nprobe", [1, 7, 64])
+def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe):
+    # several column tiles per split and a ragged last tile (3000 = 23 x 128 + 56), integer data
+    # with exact distance ties; both selection paths must return the oracle's probes exactly
+    torch = torch_cuda
+    rng = np.random.default_rng(7)
+    D, n, C = 96, 9000, 3000
+    X = rng.integers(0, 5, size=(n, D)).astype(np.float32)
+    cent = X[rng.choice(n, C, replace=False)].copy()
+    cent[1000] = cent[10]
+    ix = _idx(torch, D)
+    mean, R, lam = O.fit_rotation(X)
+    ix.set_rotation(mean, R, lam)
+    ix.build_ivf(torch.from_numpy(X).cuda(), C, centroids=torch.from_numpy(cent).cuda())
+    Q = rng.integers(0, 5, size=(300, D)).astype(np.float32)
+    pr = ix.probe(torch.from_numpy(Q).cuda(), nprobe).cpu().numpy()
+    for q in range(0, 300, 7):
+        assert pr[q].tolist() == O.probe(Q[q], cent, nprobe).tolist()

@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--nprobe", type=int, default=8)
 ap.add_argument("--alpha", type=float, default=0.005)
+ap.add_argument("--env", default="", help="NAME=VALUE set just before the profiled search")
 a = ap.parse_args()
 build.build()
 cfg = synth.config(a.config)
@@ -31,6 +32,9 @@ ix.build_ivf(X, cfg.nlist, kmeans_iters=10)
 ix.calibrate(X, Qc, cfg.k, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
 for _ in range(3):
     ix.search(Q, cfg.k, a.nprobe, cfg.delta_d, a.alpha)
+if a.env:
+    k_, v_ = a.env.split("=", 1)
+    os.environ[k_] = v_
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
 ix.search(Q, cfg.k, a.nprobe, cfg.delta_d, a.alpha)
