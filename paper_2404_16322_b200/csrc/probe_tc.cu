@@ -325,7 +325,8 @@ __device__ __forceinline__ bool cless(double d0, int32_t c0, double d1, int32_t 
 
 constexpr int kFinWarps = 4;
 constexpr int kFinCap = 512;   // candidates per row held at once (running top-k beyond that)
-constexpr int kFinDim = 64;    // dims staged per pass
+constexpr int kFinDim = 32;    // dims staged per pass
+constexpr size_t kFinWarpBytes = (size_t)kFinCap * (8 + 4 * 4) + 256 * 4 + 32 * (kFinDim + 1) * 4;
 
 // exact distances of up to 32 candidate columns (one per lane; c < 0 = none), accumulated
 // sequentially over j = 0..D-1 in fp64 (R20); rows staged through shared memory in 64-dim slices
@@ -358,16 +359,15 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
     const float* __restrict__ slack, int32_t* __restrict__ out_idx, double* __restrict__ out_d) {
   extern __shared__ __align__(16) unsigned char fs[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double* cd = reinterpret_cast<double*>(fs) + (size_t)w * kFinCap;
-  int32_t* cc = reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) + (size_t)kFinWarps * kFinCap) + (size_t)w * kFinCap;
-  float* stage = reinterpret_cast<float*>(reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) + (size_t)kFinWarps * kFinCap) +
-                                          (size_t)kFinWarps * kFinCap) + (size_t)w * 32 * (kFinDim + 1);
-  int32_t* sel = reinterpret_cast<int32_t*>(reinterpret_cast<float*>(reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) +
-                   (size_t)kFinWarps * kFinCap) + (size_t)kFinWarps * kFinCap) + (size_t)kFinWarps * 32 * (kFinDim + 1)) +
-                 (size_t)kFinWarps * 256 + (size_t)w * kFinCap;
-  unsigned* hist = reinterpret_cast<unsigned*>(reinterpret_cast<float*>(reinterpret_cast<int32_t*>(reinterpret_cast<double*>(fs) +
-                                     (size_t)kFinWarps * kFinCap) + (size_t)kFinWarps * kFinCap) +
-                                     (size_t)kFinWarps * 32 * (kFinDim + 1)) + w * 256;
+  // per-warp region: cd | cc | sel | ucol | udh | hist[256] | stage[32][kFinDim + 1]
+  unsigned char* base = fs + (size_t)w * kFinWarpBytes;
+  double* cd = reinterpret_cast<double*>(base);
+  int32_t* cc = reinterpret_cast<int32_t*>(cd + kFinCap);
+  int32_t* sel = cc + kFinCap;
+  int32_t* ucol = sel + kFinCap;
+  unsigned* udh = reinterpret_cast<unsigned*>(ucol + kFinCap);
+  unsigned* hist = udh + kFinCap;
+  float* stage = reinterpret_cast<float*>(hist + 256);
   const int64_t row = (int64_t)blockIdx.x * kFinWarps + w;
   if (row >= m) return;
   const float* a = A + row * (int64_t)D;
@@ -406,22 +406,36 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
     cnt += 32;
     __syncwarp();
   };
+  if (!full_scan && total >= k) {
+    // stage the union (column, d_hat bits) in shared memory once
+    int nu = 0;
+    for (int s = 0; s < nsplit; ++s) {
+      const int nc = ccount[row * nsplit + s];
+      const int32_t* cl = cand + (row * nsplit + s) * (int64_t)C * 2;
+      for (int i = lane; i < nc; i += 32) {
+        if (nu + i < kFinCap) {
+          ucol[nu + i] = cl[2 * i];
+          udh[nu + i] = (unsigned)cl[2 * i + 1];
+        }
+      }
+      nu += nc;
+    }
+    __syncwarp();
+    if (nu > kFinCap) full_scan = true;
+  }
   if (full_scan || total < k) {
     for (int64_t c0 = 0; c0 < n; c0 += 32) add32(c0 + lane < n ? (int32_t)(c0 + lane) : -1);
   } else {
+    const int nu = total;
     // E = k-th smallest d_hat of the union (it holds every split's k smallest): radix select
     unsigned prefix = 0;
     int krem = k;
     for (int shift = 24; shift >= 0; shift -= 8) {
       for (int i = lane; i < 256; i += 32) hist[i] = 0;
       __syncwarp();
-      for (int s = 0; s < nsplit; ++s) {
-        const int nc = ccount[row * nsplit + s];
-        const int32_t* cl = cand + (row * nsplit + s) * (int64_t)C * 2;
-        for (int i = lane; i < nc; i += 32) {
-          const unsigned v = (unsigned)cl[2 * i + 1];
-          if (shift == 24 || ((v ^ prefix) >> (shift + 8)) == 0) atomicAdd(&hist[(v >> shift) & 255u], 1u);
-        }
+      for (int i = lane; i < nu; i += 32) {
+        const unsigned v = udh[i];
+        if (shift == 24 || ((v ^ prefix) >> (shift + 8)) == 0) atomicAdd(&hist[(v >> shift) & 255u], 1u);
       }
       __syncwarp();
       unsigned h[8], tot = 0;
@@ -455,17 +469,13 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
     // the union's columns inside the global window, ballot-compacted into a list, then exact
     // distances 32 at a time
     int np = 0;
-    for (int s = 0; s < nsplit; ++s) {
-      const int nc = ccount[row * nsplit + s];
-      const int32_t* cl = cand + (row * nsplit + s) * (int64_t)C * 2;
-      for (int i0 = 0; i0 < nc; i0 += 32) {
-        const int i = i0 + lane;
-        const bool in = i < nc && (unsigned)cl[2 * i + 1] <= tb;
-        const unsigned bal = __ballot_sync(0xffffffffu, in);
-        const int pos = np + __popc(bal & ((1u << lane) - 1));
-        if (in && pos < kFinCap) sel[pos] = cl[2 * i];
-        np += __popc(bal);
-      }
+    for (int i0 = 0; i0 < nu; i0 += 32) {
+      const int i = i0 + lane;
+      const bool in = i < nu && udh[i] <= tb;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      const int pos = np + __popc(bal & ((1u << lane) - 1));
+      if (in) sel[pos] = ucol[i];
+      np += __popc(bal);
     }
     __syncwarp();
     if (np > kFinCap) {  // cannot happen for nsplit * C <= kFinCap; stay exact anyway
@@ -512,8 +522,7 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
   k_probe_tc<<<grid, kThreads, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), m, n, tps, k, C, slack, cand,
                                           ccount, dbg);
   DADE_CK(cudaGetLastError());
-  const size_t fsm = (size_t)kFinWarps * kFinCap * 12 + (size_t)kFinWarps * 32 * (kFinDim + 1) * 4 +
-                     (size_t)kFinWarps * 256 * 4 + (size_t)kFinWarps * kFinCap * 4;
+  const size_t fsm = (size_t)kFinWarps * kFinWarpBytes;
   static bool fattr = false;
   if (!fattr) {
     DADE_CK(cudaFuncSetAttribute(k_probe_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
