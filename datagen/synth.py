@@ -124,28 +124,51 @@ def _post(cfg: Config, x: np.ndarray, minmax=None) -> np.ndarray:
     return np.ascontiguousarray(x, dtype=np.float32)
 
 
+_MINMAX: dict = {}
+
+
 def _gist_minmax(cfg: Config, m: Model):
-    lo, hi = np.inf, -np.inf
-    for c in range((cfg.n + CHUNK - 1) // CHUNK):
-        n = min(CHUNK, cfg.n - c * CHUNK)
-        x = _draw(cfg, m, _rng(cfg, 1, c), n)
-        lo, hi = min(lo, x.min()), max(hi, x.max())
-    return lo, hi
+    """Global scalar min / max of the raw base (one pass; cached per config: the model is a
+    deterministic function of the config)."""
+    if cfg not in _MINMAX:
+        lo, hi = np.inf, -np.inf
+        for c in range((cfg.n + CHUNK - 1) // CHUNK):
+            n = min(CHUNK, cfg.n - c * CHUNK)
+            x = _draw(cfg, m, _rng(cfg, 1, c), n)
+            lo, hi = min(lo, x.min()), max(hi, x.max())
+        _MINMAX[cfg] = (lo, hi)
+    return _MINMAX[cfg]
 
 
-def base(cfg: Config, m: Model | None = None, rows: slice | None = None) -> np.ndarray:
+def _chunk(args):
+    cfg, m, c, minmax = args
+    n = min(CHUNK, cfg.n - c * CHUNK)
+    return _post(cfg, _draw(cfg, m, _rng(cfg, 1, c), n), minmax)
+
+
+def base(cfg: Config, m: Model | None = None, rows: slice | None = None, workers: int = 0) -> np.ndarray:
     """Base vectors S (n x D float32, row-major). `rows` selects a contiguous id range
-    (e.g. one shard) without generating the rest (chunk c is seeded [seed, 1, c])."""
+    (e.g. one shard) without generating the rest (chunk c is seeded [seed, 1, c]).
+    `workers` > 1 draws chunks in parallel processes (identical result: chunks are independent)."""
     m = m or model(cfg)
     lo_id, hi_id = (0, cfg.n) if rows is None else (rows.start or 0, rows.stop)
     minmax = _gist_minmax(cfg, m) if cfg.kind == "gist" else None
     out = np.empty((hi_id - lo_id, cfg.d), dtype=np.float32)
-    for c in range(lo_id // CHUNK, (hi_id + CHUNK - 1) // CHUNK):
+    chunks = list(range(lo_id // CHUNK, (hi_id + CHUNK - 1) // CHUNK))
+
+    def put(c, x):
         c0 = c * CHUNK
-        n = min(CHUNK, cfg.n - c0)
-        x = _post(cfg, _draw(cfg, m, _rng(cfg, 1, c), n), minmax)
-        a, b = max(lo_id, c0), min(hi_id, c0 + n)
+        a, b = max(lo_id, c0), min(hi_id, c0 + x.shape[0])
         out[a - lo_id:b - lo_id] = x[a - c0:b - c0]
+
+    if workers > 1 and len(chunks) > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(workers) as pool:
+            for c, x in zip(chunks, pool.imap(_chunk, [(cfg, m, c, minmax) for c in chunks])):
+                put(c, x)
+    else:
+        for c in chunks:
+            put(c, _chunk((cfg, m, c, minmax)))
     return out
 
 
