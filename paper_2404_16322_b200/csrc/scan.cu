@@ -36,7 +36,6 @@
 namespace dade {
 
 namespace {
-constexpr int kQCap = 128;        // survivor ring capacity (power of two)
 constexpr int TR = 32;            // rows per tile: one row per lane
 constexpr unsigned long long kKeyInf = ~0ull;
 
@@ -193,12 +192,17 @@ struct RegTopK {
 
 }  // namespace
 
-// Per-warp shared-memory slice: tiles | mbar | meta | ring.
-template <int DD>
+// Per-warp shared-memory slice: tiles | mbar | meta | ring | (ASY) staging.
+// Ring capacity: synchronous rounds start at 32 queued and stage 1 runs below 32, so at most 63
+// entries are queued; with an async round in flight stage 1 may run up to 64 queued (+32 + 32).
+template <int DD, bool ASY>
 struct Slice {
   static constexpr int kStages = DD == 1 ? 3 : 2;
   static constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
-  static constexpr size_t bytes = (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + kQCap * sizeof(QEntry);
+  static constexpr int QCAP = ASY ? 128 : 64;
+  static constexpr size_t stage_bytes = ASY ? 32 * 64 + 32 * 4 : 0;  // async gather round: rows + ids
+  static constexpr size_t bytes = (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + QCAP * sizeof(QEntry) +
+                                  stage_bytes;
 };
 
 // CTA = G warps (blockDim.x = 32 G), one query at a time. G = 1: the warp owns the query and its
@@ -207,10 +211,11 @@ struct Slice {
 // frozen tau (R13), so the split cannot change a decision; at each epoch end the warps' local
 // top-K lists are merged exactly (rank by binary search, smem) into the query's top-K.
 // CTA shared memory: G slices | pruned[64] | lists[nprobe] | qs[D] | qi | (G > 1) W[G][K] + Gk[2][K].
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI>
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY>
 __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  using SL = Slice<DD>;
+  using SL = Slice<DD, ASY>;
+  constexpr int kQCap = SL::QCAP;
   constexpr int kStages = SL::kStages;
   constexpr int TB = SL::TB;
   const int D = p.D, K = p.K;
@@ -221,6 +226,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
   TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + 4);
   QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
+  unsigned char* stg = reinterpret_cast<unsigned char*>(ring + kQCap);  // async round: 32 x 64 B rows
+  uint32_t* stg_id = reinterpret_cast<uint32_t*>(stg + 32 * 64);
   unsigned* pruned = reinterpret_cast<unsigned*>(smem + G * SL::bytes);
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
@@ -415,13 +422,82 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       tk.init(K);
     };
 
+    // ASY: a full round (32 queued survivors, one block each) is issued as cp.async copies into
+    // the warp's staging buffer and completed later, so its memory latency overlaps with stage-1
+    // work on the next tiles (the TMA ring has them in shared memory already)
+    QEntry pe{0, 0.f, nblk, 0};
+    bool pend = false;
+    int since = 0;
+    auto issue_round = [&]() {
+      pe = ring[(head + lane) & (kQCap - 1)];
+      head += 32;
+      const float* src = lay + (((int64_t)pe.blk * n + pe.row) << 4);
+      const uint32_t dst = smem_u32(stg + lane * 64);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(src + c * 4) : "memory");
+      if (pe.blk + 1 == nblk)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stg_id + lane)), "l"(p.row_id + pe.row)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      pend = true;
+      since = 0;
+    };
+    auto complete_round = [&]() {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      const ulonglong2* sr = reinterpret_cast<const ulonglong2*>(stg + lane * 64);
+      unsigned long long x[8];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const ulonglong2 v = sr[c];
+        x[2 * c] = v.x;
+        x[2 * c + 1] = v.y;
+      }
+      const float phi = pe.phi + block_sum(x, qs + pe.blk * 16);
+      const int blk = pe.blk + 1;
+      bool alive = true;
+      if (blk % DD == 0 && blk < nblk) {
+        const int ns = blk / DD;
+        if (fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau) {
+          alive = false;
+          if (stats) atomicAdd(&pruned[ns], 1u);
+        }
+      }
+      const bool fin = alive && blk == nblk;
+      push(alive && !fin, QEntry{pe.row, phi, blk, 0});
+      if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
+      const unsigned long long key = fin ? make_key(phi, stg_id[lane]) : kKeyInf;
+      __syncwarp();
+      tk.offer(!MULTI || key < cap ? key : kKeyInf, lane);
+      pend = false;
+    };
+
     // ---------------------------------------------------- consumer (one call site per action)
     bool ready = false;  // the tile in `slot` has landed and its meta is read
     TileMeta tm{0, 0, 0, 0};
     for (;;) {
       const int qlen = tail - head;
-      bool round = qlen >= 32, drain = false, ep_end = false;
-      if (!round) {
+      if (ASY) {
+        if (!pend && qlen >= 32) {
+          issue_round();
+          continue;
+        }
+        if (pend) {
+          if (!ready && consumed < issued) {
+            const int slot = consumed % kStages;
+            mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
+            phase_bits ^= 1u << slot;
+            tm = meta[slot];
+            ready = true;
+          }
+          if (!(ready && tm.ep == cur_ep && since < 2 && qlen <= kQCap - 64)) {
+            complete_round();
+            continue;
+          }
+        }
+      }
+      bool round = !ASY && qlen >= 32, drain = false, ep_end = false;
+      if (!round && !(ASY && pend)) {
         if (!ready && consumed < issued) {
           const int slot = consumed % kStages;
           mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
@@ -469,6 +545,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       }
       __syncwarp();  // every lane is done reading this slot
       ++consumed;
+      ++since;
       ready = false;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(slot);
@@ -514,9 +591,9 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   }
 }
 
-template <int DD>
+template <int DD, bool ASY>
 static size_t scan_smem(int D, int K, int nprobe, int G) {
-  return (size_t)G * Slice<DD>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
+  return (size_t)G * Slice<DD, ASY>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
          (size_t)((D + 3) & ~3) * 4 + (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
 
@@ -529,22 +606,22 @@ static int scan_group(int nq, int sms) {
   return G;
 }
 
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI>
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY>
 static void launch_g(const ScanParams& p, cudaStream_t st, int G, int sms) {
-  const size_t smem = scan_smem<DD>(p.D, p.K, p.nprobe, G);
+  const size_t smem = scan_smem<DD, ASY>(p.D, p.K, p.nprobe, G);
   DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
   static size_t attr = 0;
   if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG, MULTI, ASY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
   int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG, MULTI>, 32 * G, smem));
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG, MULTI, ASY>, 32 * G, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;
-  k_scan<DD, KPL, LA, MAXREG, MULTI><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
+  k_scan<DD, KPL, LA, MAXREG, MULTI, ASY><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
 }
 
-template <int DD, int KPL, int LA, int MAXREG>
+template <int DD, int KPL, int LA, int MAXREG, bool ASY = false>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
   static int sms = 0;
   if (!sms) {
@@ -554,8 +631,8 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
   }
   const int G = scan_group(p.nq, sms);
   DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
-  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false>(p, st, 1, sms);
-  else launch_g<DD, KPL, LA, MAXREG, true>(p, st, G, sms);
+  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, ASY>(p, st, 1, sms);
+  else launch_g<DD, KPL, LA, MAXREG, true, ASY>(p, st, G, sms);
 }
 
 // tuning variants (DADE_SCAN_VARIANT, read per launch) for the Delta_d = 16, K <= 32 kernel
@@ -568,9 +645,10 @@ template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
   if constexpr (DD == 1 && KPL == 1) {
     switch (scan_variant()) {
-      case 1: launch_v<DD, KPL, 2, 96>(p, st); return;
-      case 2: launch_v<DD, KPL, 1, 96>(p, st); return;
+      case 1: launch_v<DD, KPL, 1, 80, true>(p, st); return;
+      case 2: launch_v<DD, KPL, 1, 72, true>(p, st); return;
       case 3: launch_v<DD, KPL, 1, 72>(p, st); return;
+      case 4: launch_v<DD, KPL, 1, 64>(p, st); return;
       default: break;
     }
   }
