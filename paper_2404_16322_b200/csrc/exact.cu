@@ -9,6 +9,7 @@
 #include <cstdio>
 
 #include "dade_internal.h"
+#include "exact_batch.cuh"
 
 namespace dade {
 
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_select_small(
 // Warp-per-row exact select for the tensor-core filter. E = the k-th smallest of the row's
 // 32-column group minima is >= the k-th smallest d_hat (k groups each hold an element <= E), so
 // every column with d_hat <= E + 2 slack is re-ranked exactly; the certified set is contained.
-constexpr int kGmWarps = 8;
+constexpr int kGmWarps = 4;
 constexpr int kGmCap = 256;
 
 __device__ __forceinline__ bool cand_less2(double d0, int32_t c0, double d1, int32_t c1) {
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   __shared__ float sg[kGmWarps][256];
   __shared__ double cd[kGmWarps][kGmCap];
   __shared__ int32_t cc[kGmWarps][kGmCap];
+  __shared__ float xstage[kGmWarps][32 * (kXbDim + 1)];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * kGmWarps + w;
   if (row >= m) return;
@@ -423,9 +425,14 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   const float* a = A + row * (int64_t)D;
   int P = 1;
   while (P < cnt) P <<= 1;
-  for (int i = lane; i < P; i += 32) {
-    if (i < cnt) cd[w][i] = exact_sqdist(a, B + (int64_t)cc[w][i] * D, D);
-    else { cd[w][i] = DBL_MAX; cc[w][i] = 0x7fffffff; }
+  for (int i0 = 0; i0 < P; i0 += 32) {  // exact fp64 distances, 32 candidates per staged batch
+    const int i = i0 + lane;
+    const int32_t c = (i < cnt) ? cc[w][i] : -1;
+    const double d = i0 < cnt ? exact_batch32(a, B, D, c, xstage[w], lane) : 0.0;
+    if (i < P) {
+      if (i < cnt) cd[w][i] = d;
+      else { cd[w][i] = DBL_MAX; cc[w][i] = 0x7fffffff; }
+    }
   }
   __syncwarp();
   for (int size = 2; size <= P; size <<= 1)

@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "dade_internal.h"
+#include "exact_batch.cuh"
 
 namespace dade {
 

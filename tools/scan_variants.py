@@ -18,11 +18,12 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--nprobe", type=int, default=8)
 ap.add_argument("--variants", default="0,1,2,3,4,5")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--var", default="DADE_SCAN_VARIANT", help="environment variable the values are assigned to")
 a = ap.parse_args()
 build.build()
 cfg = synth.config(a.config)
 m = synth.model(cfg)
-X = torch.from_numpy(synth.base(cfg, m)).cuda()
+X = torch.from_numpy(synth.base(cfg, m, workers=min(16, os.cpu_count() or 1))).cuda()
 Q = torch.from_numpy(synth.queries(cfg, m=m)).cuda()
 Qc = torch.from_numpy(synth.cal_queries(cfg, m=m)).cuda()
 ix = Index(cfg.d)
@@ -31,7 +32,7 @@ ix.build_ivf(X, cfg.nlist, kmeans_iters=10)
 ix.calibrate(X, Qc, cfg.k, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 for v in a.variants.split(","):
-    os.environ["DADE_SCAN_VARIANT"] = v
+    os.environ[a.var] = v
     for _ in range(3):
         ix.search(Q, cfg.k, a.nprobe, cfg.delta_d, 0.005)
     sc, tot = [], []
@@ -40,4 +41,4 @@ for v in a.variants.split(","):
         _, _, st = ix.search(Q, cfg.k, a.nprobe, cfg.delta_d, 0.005, stats=True)
         sc.append(st["ms_scan"]); tot.append(st["ms_total"])
     sc.sort(); tot.sort()
-    print(f"variant {v}: scan median {sc[len(sc)//2]:.4f} ms min {sc[0]:.4f}  total median {tot[len(tot)//2]:.4f} ms", flush=True)
+    print(f"{a.var}={v}: scan median {sc[len(sc)//2]:.4f} ms min {sc[0]:.4f}  total median {tot[len(tot)//2]:.4f} ms", flush=True)
