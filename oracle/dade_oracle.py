@@ -308,15 +308,45 @@ def epoch_bounds(total: int, K: int, c0: int | None = None):
     return b
 
 
-def build_index(X, centroids, mean=None, R=None, cal=None, id_base=0):
-    """Bundle the artefacts search needs (fp64 rotated base, lists, rotation, calibration)."""
+def build_index(X, centroids, mean=None, R=None, cal=None, id_base=0, lam=None):
+    """Bundle the artefacts search needs (fp64 rotated base, lists, rotation, calibration;
+    lam = per-dimension variances σ_i² of the rotated data, for BSA-res)."""
     a, off, row_id = build_ivf(X, centroids, id_base)
     return {"centroids": np.asarray(centroids, np.float32), "assign": a, "off": off,
-            "row_id": row_id, "mean": mean, "R": R, "cal": cal, "id_base": id_base,
+            "row_id": row_id, "mean": mean, "R": R, "cal": cal, "id_base": id_base, "lam": lam,
             "Xr": None if mean is None else rotate(X, mean, R)}
 
 
-def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False):
+# ----------------------------------------------------------------------------- NEXT-1 corrections
+def adsampling_table(D: int, delta_d: int, eps0: float):
+    """ADSampling's hypothesis test as a linear classifier: after d
+    randomly projected dims the estimate (D/d)·P_d (JL scaling, Lemma 1) prunes iff
+    it exceeds (1 + ε)²·τ with ε = ε₀/√d (R8: squared distances). Returned as the per-step
+    (m1, β') of the BSA-p form: m1_d = (D/d)/(1 + ε₀/√d)², β' = 0."""
+    ns = D // delta_d
+    d = np.arange(1, ns) * delta_d
+    return (D / d) / (1.0 + eps0 / np.sqrt(d)) ** 2, np.zeros(ns - 1)
+
+
+def bsa_res_consts(q_rot: np.ndarray, lam: np.ndarray, delta_d: int, m: float) -> np.ndarray:
+    """Per-step query constants of the BSA-res test (Alg. 2; incremental form
+    P:L455-470; R6): with P_d the partial distance and N_d = ‖x_{:d}‖², the estimate is
+    dis'_d = C1 − C2 = P_d + ‖x_r‖² + ‖q_r‖² (Eq. 2: the dropped term is the error
+    −2⟨q_r, x_r⟩), σ_d² = 4·Σ_{i≥d} q_i² σ_i² (Eq. 3, σ_i² = λ_i for the PCA
+    basis), and the test prunes iff dis'_d − m·σ_d > τ. Returns c_d = ‖q_r‖² −
+    m·σ_d for d = Δd, 2Δd, …, D − Δd; the test is P_d + (‖x‖² − N_d) + c_d > τ."""
+    q = np.asarray(q_rot, F64)
+    D = q.shape[0]
+    ns = D // delta_d
+    out = np.empty(ns - 1)
+    for s in range(1, ns):
+        d = s * delta_d
+        out[s - 1] = float(np.sum(q[d:] ** 2)) - m * math.sqrt(err_variance(q, lam, d))
+    return out
+
+
+def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False, method="bsa_p",
+           eps0=2.1, m_res=8.0):
     """IVF search with the per-step data-driven correction (O5).
     Refinement: result queue of size K, τ = its K-th distance (R11: +∞ until full).
     Candidates = the probed lists in probe order. For each candidate, the partial
@@ -324,11 +354,24 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
     (Alg. 2 loop, R9) and the cascade classifier for d prunes iff
     m1_d·P_d + β'_d > τ. Survivors reach d = D, where P_D is the exact distance
     (R10), and enter the queue. mode="epoch": τ frozen per epoch (R13, the parity
-    target); mode="sequential": τ refreshed after every survivor (P:L42-43 literal)."""
+    target); mode="sequential": τ refreshed after every survivor (P:L42-43 literal).
+    method (NEXT-1, the paper's other corrections on the same loop): "bsa_p" (above, α =
+    significance), "adsampling" (adsampling_table(ε₀); use a random orthogonal R), "bsa_res"
+    (bsa_res_consts(m_res); needs index["lam"]). α = 0 disables pruning for every method."""
     Q = np.atleast_2d(Q)
     D = Q.shape[1]
     ns = D // delta_d
-    m, b = step_table(index["cal"], D, delta_d, alpha) if alpha > 0 else (np.ones(ns - 1), np.full(ns - 1, -np.inf))
+    if alpha == 0:
+        m, b = np.ones(ns - 1), np.full(ns - 1, -np.inf)
+    elif method == "bsa_p":
+        m, b = step_table(index["cal"], D, delta_d, alpha)
+    elif method == "adsampling":
+        m, b = adsampling_table(D, delta_d, eps0)
+    elif method == "bsa_res":
+        m, b = np.ones(ns - 1), np.zeros(ns - 1)
+    else:
+        raise ValueError(method)
+    res = method == "bsa_res" and alpha > 0
     off, row_id, Xr = index["off"], index["row_id"], index["Xr"]
     base = index["id_base"]                          # Xr rows are in id order: row = id - id_base
     out_ids = np.full((Q.shape[0], K), -1, dtype=np.int64)
@@ -339,6 +382,7 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
     steps = np.arange(1, ns) * delta_d
     for qn in range(Q.shape[0]):
         pr = probe(Q[qn], index["centroids"], nprobe)
+        qc = bsa_res_consts(Qr[qn], index["lam"], delta_d, m_res) if res else None
         cand = np.concatenate([row_id[off[l]:off[l + 1]] for l in pr]) if len(pr) else np.zeros(0, np.int64)
         top_d = np.zeros(0); top_i = np.zeros(0, dtype=np.int64)
         st["tested"] += len(cand)
@@ -352,7 +396,11 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
                 keep = np.ones(len(ids), dtype=bool)
                 dims = np.full(len(ids), D)
                 if np.isfinite(tau) and ns > 1:
-                    test = m[None, :] * P[:, steps - 1] + b[None, :] > tau
+                    score = m[None, :] * P[:, steps - 1] + b[None, :]
+                    if res:  # P_d + ‖x_r‖² + c_d, ‖x_r‖² = ‖x‖² − N_d
+                        N = np.cumsum(Xr[ids - base] ** 2, axis=1)
+                        score = score + (N[:, D - 1:D] - N[:, steps - 1]) + qc[None, :]
+                    test = score > tau
                     anyp = test.any(axis=1)
                     first = np.argmax(test, axis=1)
                     keep = ~anyp
@@ -362,7 +410,7 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
                         for i in np.nonzero(anyp)[0]:
                             s = first[i]
                             st["decisions"].append((qn, int(ids[i]), int(steps[s]),
-                                                    float(m[s] * P[i, steps[s] - 1] + b[s]), float(tau)))
+                                                    float(score[i, s]), float(tau)))
                 st["dims_scanned"] += int(dims.sum())
                 st["survivors"] += int(keep.sum())
                 cd = np.concatenate([top_d, P[keep, D - 1]])
@@ -373,10 +421,14 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
             for idn in cand:
                 tau = top_d[K - 1] if len(top_d) >= K else np.inf
                 P = np.cumsum((Xr[idn - base] - Qr[qn]) ** 2)
+                N = np.cumsum(Xr[idn - base] ** 2)
                 pruned_at = 0
                 if np.isfinite(tau):
                     for si, d in enumerate(steps):
-                        if m[si] * P[d - 1] + b[si] > tau:
+                        sc = m[si] * P[d - 1] + b[si]
+                        if res:
+                            sc += (N[D - 1] - N[d - 1]) + qc[si]
+                        if sc > tau:
                             pruned_at = d
                             st["pruned_at_step"][si + 1] += 1
                             break
