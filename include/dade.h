@@ -149,6 +149,22 @@ dade_status dade_set_calibration(dade_index* idx, int K, int n0, int n_cls, cons
 dade_status dade_search(dade_index* idx, const float* Q, int nq, int K, int nprobe, int delta_d,
                         double significance, int64_t* ids, float* dists, dade_stats* stats);
 
+/* ---------------------------------------------------------------- NEXT-1: the paper's other DCOs
+ * Same scan, different per-step test:
+ *   DADE_METHOD_BSA_P      param = significance alpha (== dade_search).
+ *   DADE_METHOD_ADSAMPLING param = eps0 > 0: prune iff (D/d) P_d > (1 + eps0/sqrt(d))^2 tau — the
+ *       ADSampling hypothesis test (linear form P:L3937; R8). Meaningful on a RANDOM
+ *       orthogonal rotation (install it with dade_set_rotation); eps0 = 2.1 in the paper.
+ *   DADE_METHOD_BSA_RES    param = multiplier m > 0: prune iff P_d + ||x_r||^2 + ||q_r||^2 - m sigma_d
+ *       > tau, sigma_d^2 = 4 sum_{i>=d} q~_i^2 lambda_i (Alg. 2, Eq. 3, R6);
+ *       lambda = the rotation's eigenvalues; m = 8 in the paper.
+ * Errors: as dade_search; ARG if param <= 0 for ADSAMPLING / BSA_RES or method unknown. */
+#define DADE_METHOD_BSA_P 0
+#define DADE_METHOD_ADSAMPLING 1
+#define DADE_METHOD_BSA_RES 2
+dade_status dade_search_method(dade_index* idx, const float* Q, int nq, int K, int nprobe, int delta_d,
+                               int method, double param, int64_t* ids, float* dists, dade_stats* stats);
+
 /* Same as dade_search with HOST Q/ids/dists: the H2D copy of Q and the D2H copy of the results
  * are part of the call (synchronous). Used for the end-to-end (e2e) measurement. */
 dade_status dade_search_host(dade_index* idx, const float* Q_host, int nq, int K, int nprobe,

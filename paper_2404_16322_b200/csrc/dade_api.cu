@@ -53,6 +53,10 @@ struct dade_index {
   DBuf<unsigned long long> counters;
   DBuf<int64_t> ids_tmp;
   DBuf<float> dists_tmp;
+  // NEXT-1 BSA-res: per-row ‖x~‖² (list-major, computed on first use), eigenvalues, query constants
+  DBuf<float> xnorm, qconst;
+  DBuf<double> lam_d;
+  bool xnorm_ok = false;
   cudaEvent_t ev[5] = {};
 };
 
@@ -278,7 +282,7 @@ __global__ void k_ids_from_idx(const int32_t* idx, const double* d64, int64_t cn
 }
 
 void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d, double alpha,
-               int64_t* ids, float* dists, dade_stats* stats) {
+               int64_t* ids, float* dists, dade_stats* stats, int method = DADE_METHOD_BSA_P) {
   const int D = x->D;
   DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
   DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
@@ -288,14 +292,21 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
   DADE_REQUIRE(delta_d >= 16 && delta_d % 16 == 0 && D % delta_d == 0, DADE_ERR_ARG,
                "delta_d must be a positive multiple of 16 dividing D");
-  DADE_REQUIRE(alpha >= 0.0 && alpha < 1.0, DADE_ERR_ARG, "significance not in [0,1)");
+  DADE_REQUIRE(method == DADE_METHOD_BSA_P || method == DADE_METHOD_ADSAMPLING || method == DADE_METHOD_BSA_RES,
+               DADE_ERR_ARG, "unknown method");
+  if (method == DADE_METHOD_BSA_P)
+    DADE_REQUIRE(alpha >= 0.0 && alpha < 1.0, DADE_ERR_ARG, "significance not in [0,1)");
+  else
+    DADE_REQUIRE(alpha > 0.0 && std::isfinite(alpha), DADE_ERR_ARG, "eps0 / m must be positive");
+  if (method == DADE_METHOD_BSA_RES)
+    DADE_REQUIRE(!x->lam.empty(), DADE_ERR_STATE, "BSA-res needs the rotation's eigenvalues");
   const int nsteps = D / delta_d;
   DADE_REQUIRE(nsteps <= DADE_MAX_STEPS, DADE_ERR_UNSUPPORTED, "D/delta_d > DADE_MAX_STEPS");
   const int dd = delta_d / 16;
   const bool prune = alpha > 0.0 && nsteps > 1;
   DADE_REQUIRE(!prune || dd == 1 || dd == 2 || dd == 4, DADE_ERR_UNSUPPORTED,
                "with pruning, delta_d must be 16, 32 or 64");
-  if (prune) {
+  if (prune && method == DADE_METHOD_BSA_P) {
     DADE_REQUIRE(x->has_cal, DADE_ERR_STATE, "significance > 0 requires calibration");
     DADE_REQUIRE(x->calK == K, DADE_ERR_STATE, "K differs from the calibrated K");
   }
@@ -332,7 +343,14 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   // steps (no classifier fires: m1 = 1, beta' = -inf), which serves every delta_d | D.
   p.dd = prune ? dd : 1; p.nsteps = prune ? nsteps : D / 16; p.c0 = 4 * K; p.prune = prune ? 1 : 0;
   for (int s = 1; s < p.nsteps; ++s) {
-    if (prune) {
+    if (prune && method == DADE_METHOD_ADSAMPLING) {  // m1_d = (D/d)/(1 + eps0/sqrt(d))^2, beta = 0
+      const double d = (double)s * delta_d;
+      p.m1[s - 1] = (float)((D / d) / ((1.0 + alpha / std::sqrt(d)) * (1.0 + alpha / std::sqrt(d))));
+      p.beta[s - 1] = 0.f;
+    } else if (prune && method == DADE_METHOD_BSA_RES) {  // the residual test uses qconst instead
+      p.m1[s - 1] = 1.f;
+      p.beta[s - 1] = 0.f;
+    } else if (prune) {
       const int idx = (s * delta_d) / 16 - 1;
       const double alpha_s = (alpha * delta_d) / D;
       long k = (long)std::ceil((1.0 - alpha_s) * (double)x->n0);
@@ -349,6 +367,20 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     x->counters.reserve(4 + DADE_MAX_STEPS + 8);
     DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS + 8), st));
     p.counters = x->counters.p;
+  }
+  if (prune && method == DADE_METHOD_BSA_RES) {
+    if (!x->xnorm_ok) {
+      x->xnorm.reserve((size_t)std::max<int64_t>(x->n, 1));
+      launch_row_norms(x->layout.p, x->n, D, x->xnorm.p, st);
+      x->xnorm_ok = true;
+    }
+    x->lam_d.reserve(D);
+    DADE_CK(cudaMemcpyAsync(x->lam_d.p, x->lam.data(), sizeof(double) * D, cudaMemcpyHostToDevice, st));
+    x->qconst.reserve((size_t)nq * (nsteps - 1) + 1);
+    launch_res_consts(x->qrot.p, nq, D, delta_d, x->lam_d.p, alpha, x->qconst.p, st);
+    p.residual = 1;
+    p.xnorm = x->xnorm.p;
+    p.qconst = x->qconst.p;
   }
   x->work.reserve(1);
   DADE_CK(cudaMemsetAsync(x->work.p, 0, sizeof(int), st));
@@ -408,7 +440,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->R_d.release(); x->mean_d.release(); x->cent.release(); x->layout.release();
   x->off_d.release(); x->row_id_d.release(); x->qrot.release(); x->dmat.release();
   x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
-  x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->ids_tmp.release();
+  x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->ids_tmp.release(); x->xnorm.release(); x->qconst.release(); x->lam_d.release();
   x->dists_tmp.release();
   x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release();
   for (auto& e : x->ev)
@@ -658,6 +690,7 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
   x->n = n;
   x->id_base = id_base;
   x->has_ivf = true;
+  x->xnorm_ok = false;
   x->has_cal = false;
   API_END
 }
@@ -854,6 +887,16 @@ extern "C" dade_status dade_search(dade_index* x, const float* Q, int nq, int K,
   API_END
 }
 
+extern "C" dade_status dade_search_method(dade_index* x, const float* Q, int nq, int K, int nprobe,
+                                          int delta_d, int method, double param, int64_t* ids,
+                                          float* dists, dade_stats* stats) {
+  API_BEGIN
+  need(x, "index");
+  DeviceGuard g(x->device);
+  do_search(x, Q, nq, K, nprobe, delta_d, param, ids, dists, stats, method);
+  API_END
+}
+
 extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, int K, int nprobe,
                                         int delta_d, double significance, int64_t* ids_h,
                                         float* dists_h, dade_stats* stats) {
@@ -994,7 +1037,7 @@ extern "C" dade_status dade_load(dade_index* x, const char* path) {
   x->off_h = off; x->row_id_h = rid; x->assign_h = asg;
   x->pos_of_h.assign(n, 0);
   for (int64_t p = 0; p < n; ++p) x->pos_of_h[rid[p] - hdr[4]] = (int32_t)p;
-  x->nlist = nlist; x->n = n; x->id_base = hdr[4]; x->has_ivf = true;
+  x->nlist = nlist; x->n = n; x->id_base = hdr[4]; x->has_ivf = true; x->xnorm_ok = false;
   tc_prepare(x, x->cent.p, nlist, x->cent_tc, true);
   x->has_cal = hdr[5] != 0;
   if (x->has_cal) { x->calK = (int)c[0]; x->n0 = (int)c[1]; x->ncls = (int)c[2]; x->m1 = m1; x->v = v; }

@@ -135,8 +135,17 @@ struct ScanParams {
   float* out_d;
   unsigned long long* counters;  // [0]=tested [1]=survivors [2]=dims [3]=max epochs [4..4+64) pruned_at_step
   int* work_counter;             // zeroed before the launch; persistent warps take queries from it
+  // residual test (BSA-res, NEXT-1): prune iff P_d + (‖x‖² − N_d) + qconst[q][s-1] > tau
+  int residual;
+  const float* xnorm;   // n: ‖x~‖² per list-major row (residual only)
+  const float* qconst;  // nq x (nsteps - 1): ‖q_r‖² − m·σ_d per step (residual only)
 };
 void launch_scan(const ScanParams& p, cudaStream_t st);
+// ‖x~‖² of every list-major row of the blocked layout (fp64 sums, stored fp32)
+void launch_row_norms(const float* layout, int64_t n, int D, float* out, cudaStream_t st);
+// BSA-res per-step query constants c_s = sum_{i>=d} q_i^2 - m sqrt(4 sum_{i>=d} q_i^2 lam_i), d = s*delta_d
+void launch_res_consts(const float* qrot, int nq, int D, int delta_d, const double* lam, double m,
+                       float* out, cudaStream_t st);
 // merge.cu
 void launch_merge_topk(const int64_t* ids_in, const float* d_in, int S, int nq, int K,
                        int64_t* ids_out, float* d_out, cudaStream_t st);

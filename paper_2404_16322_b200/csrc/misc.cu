@@ -1,4 +1,5 @@
 // a9 shard merge and calibration feature kernels.
+#include <algorithm>
 #include <cfloat>
 
 #include "dade_internal.h"
@@ -84,6 +85,56 @@ void launch_pair_prefix(const float* layout, int64_t n_rows, int D, const float*
   if (npairs <= 0) return;
   k_pair_prefix<<<(npairs + 127) / 128, 128, 0, st>>>(layout, n_rows, D, qrot, pair_q, pair_row,
                                                       npairs, out);
+  DADE_CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ NEXT-1 BSA-res helpers
+// ‖x~‖² per list-major row of the blocked layout (block b of row r at (b*n + r)*16): fp64 sum in
+// block order, stored fp32 (the kernel subtracts fp32 block sums from it)
+__global__ void k_row_norms(const float* __restrict__ lay, int64_t n, int nblk, float* __restrict__ out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) {
+      const float4* v = reinterpret_cast<const float4*>(lay + (((int64_t)b * n + r) << 4));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 x = __ldg(v + c);
+        s += (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z + (double)x.w * x.w;
+      }
+    }
+    out[r] = (float)s;
+  }
+}
+
+void launch_row_norms(const float* layout, int64_t n, int D, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_row_norms<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(layout, n, D / 16, out);
+  DADE_CK(cudaGetLastError());
+}
+
+// c_s = sum_{i>=d} q_i^2 - m sqrt(4 sum_{i>=d} q_i^2 lam_i), d = s*delta_d, s = 1..D/delta_d-1
+// (Alg. 2 / Eq. 3), one thread per (query, step), fp64
+__global__ void k_res_consts(const float* __restrict__ qrot, int nq, int D, int delta_d, const double* __restrict__ lam,
+                             double m, float* __restrict__ out) {
+  const int ns = D / delta_d - 1;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nq * ns) return;
+  const int64_t q = t / ns;
+  const int s = (int)(t % ns) + 1;
+  double qr = 0.0, var = 0.0;
+  for (int i = s * delta_d; i < D; ++i) {
+    const double v = qrot[q * D + i];
+    qr += v * v;
+    var += v * v * lam[i];
+  }
+  out[t] = (float)(qr - m * sqrt(4.0 * var));
+}
+
+void launch_res_consts(const float* qrot, int nq, int D, int delta_d, const double* lam, double m, float* out,
+                       cudaStream_t st) {
+  const int64_t tot = (int64_t)nq * (D / delta_d - 1);
+  if (tot <= 0) return;
+  k_res_consts<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(qrot, nq, D, delta_d, lam, m, out);
   DADE_CK(cudaGetLastError());
 }
 

@@ -43,7 +43,7 @@ struct __align__(16) QEntry {
   int32_t row;   // list-major position
   float phi;     // partial distance over blocks [0, blk)
   int32_t blk;   // 16-dim blocks accumulated
-  int32_t pad;
+  float res;     // residual test only: ‖x‖² − (x² summed over blocks [0, blk))
 };
 
 struct TileMeta {
@@ -132,6 +132,18 @@ __device__ __forceinline__ float block_sum_rot(const unsigned long long (&x)[8],
   return s.x + s.y;
 }
 
+// Σ x_i² over one 16-dim block (residual test), fixed association
+__device__ __forceinline__ float block_sq(const unsigned long long (&x)[8]) {
+  unsigned long long a[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    a[c] = fma2(x[2 * c + 1], x[2 * c + 1], 0ull);
+    a[c] = fma2(x[2 * c], x[2 * c], a[c]);
+  }
+  const float2 s = upk(add2(add2(a[0], a[1]), add2(a[2], a[3])));
+  return s.x + s.y;
+}
+
 __device__ __forceinline__ void ld_block(unsigned long long (&x)[8], const float* src) {
   const ulonglong2* s = reinterpret_cast<const ulonglong2*>(src);
 #pragma unroll
@@ -211,7 +223,7 @@ struct Slice {
 // frozen tau (R13), so the split cannot change a decision; at each epoch end the warps' local
 // top-K lists are merged exactly (rank by binary search, smem) into the query's top-K.
 // CTA shared memory: G slices | pruned[64] | lists[nprobe] | qs[D] | qi | (G > 1) W[G][K] + Gk[2][K].
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY>
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY, bool RES>
 __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   using SL = Slice<DD, ASY>;
@@ -231,7 +243,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   unsigned* pruned = reinterpret_cast<unsigned*>(smem + G * SL::bytes);
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
-  int* qslot = reinterpret_cast<int*>(qs + ((D + 3) & ~3));
+  float* qcs = qs + ((D + 3) & ~3);                       // residual: per-step query constants
+  int* qslot = reinterpret_cast<int*>(qcs + (RES ? DADE_MAX_STEPS : 0));
   unsigned long long* W = reinterpret_cast<unsigned long long*>(qslot + 4);  // G x K (G > 1)
   unsigned long long* Gk = W + (size_t)G * K;                               // 2 x K (G > 1)
 
@@ -259,6 +272,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     if (qi >= p.nq) break;
     const int64_t q = qi;
     for (int j = threadIdx.x; j < D; j += blockDim.x) qs[j] = p.qrot[q * D + j];
+    if (RES)
+      for (int j = threadIdx.x; j < nsteps - 1; j += blockDim.x) qcs[j] = p.qconst[q * (nsteps - 1) + j];
     for (int j = threadIdx.x; j < p.nprobe; j += blockDim.x) {
       const int l = p.probes[q * p.nprobe + j];
       const int s0 = p.off[l];
@@ -335,7 +350,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const int lg = !drain ? 0 : qn <= 8 ? 2 : qn <= 16 ? 1 : 0;  // log2 lanes per survivor
       const int ei = lane >> lg, sub = lane & ((1 << lg) - 1);
       const bool val = ei < qn;
-      QEntry e = val ? ring[(head + ei) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0};
+      QEntry e = val ? ring[(head + ei) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0.f};
       int wtot = (drain || e.blk > DD) ? (LA << lg) : (DD < LA ? DD : LA);
       wtot = min(wtot, nblk - e.blk);
       const int b0 = e.blk + sub * LA;  // this lane's first block
@@ -348,20 +363,25 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       if (e.blk + wtot == nblk && val && sub == 0) gid = (uint32_t)__ldg(p.row_id + e.row);
       head += qn;
       __syncwarp();
-      float bs[LA];
+      float bs[LA], bq[LA];
 #pragma unroll
-      for (int s = 0; s < LA; ++s) bs[s] = s < want ? block_sum(v[s], qs + (b0 + s) * 16) : 0.f;
-      float phi = e.phi;
+      for (int s = 0; s < LA; ++s) {
+        bs[s] = s < want ? block_sum(v[s], qs + (b0 + s) * 16) : 0.f;
+        bq[s] = RES && s < want ? block_sq(v[s]) : 0.f;
+      }
+      float phi = e.phi, res = e.res;
       int blk = e.blk;
       bool alive = val;
       const int bend = e.blk + wtot;
-      auto step = [&](float b) {  // add the next block; classifier at step boundaries d < D
+      auto step = [&](float b, float nq) {  // add the next block; classifier at step boundaries d < D
         if (alive && blk < bend) {
           phi += b;
+          if (RES) res -= nq;
           ++blk;
           if (blk % DD == 0 && blk < nblk) {
             const int ns = blk / DD;
-            if (fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau) {
+            const bool pr = RES ? phi + res + qcs[ns - 1] > tau : fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau;
+            if (pr) {
               alive = false;
               if (stats && sub == 0) atomicAdd(&pruned[ns], 1u);
             }
@@ -370,14 +390,16 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       };
       if (lg == 0) {
 #pragma unroll
-        for (int s = 0; s < LA; ++s) step(bs[s]);
+        for (int s = 0; s < LA; ++s) step(bs[s], bq[s]);
       } else {
         for (int j = 0; j < (1 << lg); ++j)
 #pragma unroll
-          for (int s = 0; s < LA; ++s) step(__shfl_sync(0xffffffffu, bs[s], (ei << lg) + j));
+          for (int s = 0; s < LA; ++s)
+            step(__shfl_sync(0xffffffffu, bs[s], (ei << lg) + j),
+                 RES ? __shfl_sync(0xffffffffu, bq[s], (ei << lg) + j) : 0.f);
       }
       const bool fin = alive && blk == nblk && sub == 0;  // d = D: exact distance (no test, R10)
-      push(alive && blk < nblk && sub == 0, QEntry{e.row, phi, blk, 0});
+      push(alive && blk < nblk && sub == 0, QEntry{e.row, phi, blk, res});
       if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
       const unsigned long long key = fin ? make_key(phi, gid) : kKeyInf;
       tk.offer(!MULTI || key < cap ? key : kKeyInf, lane);
@@ -425,7 +447,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     // ASY: a full round (32 queued survivors, one block each) is issued as cp.async copies into
     // the warp's staging buffer and completed later, so its memory latency overlaps with stage-1
     // work on the next tiles (the TMA ring has them in shared memory already)
-    QEntry pe{0, 0.f, nblk, 0};
+    QEntry pe{0, 0.f, nblk, 0.f};
     bool pend = false;
     int since = 0;
     auto issue_round = [&]() {
@@ -454,17 +476,18 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         x[2 * c + 1] = v.y;
       }
       const float phi = pe.phi + block_sum(x, qs + pe.blk * 16);
+      const float res = RES ? pe.res - block_sq(x) : 0.f;
       const int blk = pe.blk + 1;
       bool alive = true;
       if (blk % DD == 0 && blk < nblk) {
         const int ns = blk / DD;
-        if (fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau) {
+        if (RES ? phi + res + qcs[ns - 1] > tau : fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau) {
           alive = false;
           if (stats) atomicAdd(&pruned[ns], 1u);
         }
       }
       const bool fin = alive && blk == nblk;
-      push(alive && !fin, QEntry{pe.row, phi, blk, 0});
+      push(alive && !fin, QEntry{pe.row, phi, blk, res});
       if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
       const unsigned long long key = fin ? make_key(phi, stg_id[lane]) : kKeyInf;
       __syncwarp();
@@ -528,7 +551,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const int slot = consumed % kStages;
       const bool val = lane < tm.nr;
       const unsigned char* trow = tiles + slot * TB + lane * 64;
-      float s = 0.f;
+      float s = 0.f, sq = 0.f;
+      const float xn = RES && val ? __ldg(p.xnorm + tm.row0 + lane) : 0.f;
 #pragma unroll
       for (int bb = 0; bb < DD; ++bb) {
         unsigned long long x[8];
@@ -542,6 +566,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
           qc[c] = qs + bb * 16 + ch * 4;
         }
         s += block_sum_rot(x, qc);
+        if (RES) sq += block_sq(x);  // chunk order differs per lane: only feeds the prune test
       }
       __syncwarp();  // every lane is done reading this slot
       ++consumed;
@@ -550,8 +575,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(slot);
       if (stats) c_tested += tm.nr;
-      const bool prune = val && nsteps > 1 && fmaf(p.m1[0], s, p.beta[0]) > tau;
-      push(val && !prune, QEntry{tm.row0 + lane, s, DD, 0});
+      const float res = xn - sq;
+      const bool prune = val && nsteps > 1 &&
+                         (RES ? s + res + qcs[0] > tau : fmaf(p.m1[0], s, p.beta[0]) > tau);
+      push(val && !prune, QEntry{tm.row0 + lane, s, DD, res});
       if (stats) {
         const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
         if (lane == 0 && np_) atomicAdd(&pruned[1], (unsigned)np_);
@@ -591,10 +618,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   }
 }
 
-template <int DD, bool ASY>
+template <int DD, bool ASY, bool RES>
 static size_t scan_smem(int D, int K, int nprobe, int G) {
   return (size_t)G * Slice<DD, ASY>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
-         (size_t)((D + 3) & ~3) * 4 + (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
+         (size_t)((D + 3) & ~3) * 4 + (RES ? DADE_MAX_STEPS * 4 : 0) + (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
 
 // warps per query: the smallest G giving >= 12 query-warps per SM (measured on C3, 1,000
@@ -607,22 +634,22 @@ static int scan_group(int nq, int sms) {
   return G;
 }
 
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY>
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY, bool RES>
 static void launch_g(const ScanParams& p, cudaStream_t st, int G, int sms) {
-  const size_t smem = scan_smem<DD, ASY>(p.D, p.K, p.nprobe, G);
+  const size_t smem = scan_smem<DD, ASY, RES>(p.D, p.K, p.nprobe, G);
   DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
   static size_t attr = 0;
   if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG, MULTI, ASY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG, MULTI, ASY, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
   int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG, MULTI, ASY>, 32 * G, smem));
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG, MULTI, ASY, RES>, 32 * G, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;
-  k_scan<DD, KPL, LA, MAXREG, MULTI, ASY><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
+  k_scan<DD, KPL, LA, MAXREG, MULTI, ASY, RES><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
 }
 
-template <int DD, int KPL, int LA, int MAXREG, bool ASY = false>
+template <int DD, int KPL, int LA, int MAXREG, bool ASY = false, bool RES = false>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
   static int sms = 0;
   if (!sms) {
@@ -632,8 +659,8 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
   }
   const int G = scan_group(p.nq, sms);
   DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
-  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, ASY>(p, st, 1, sms);
-  else launch_g<DD, KPL, LA, MAXREG, true, ASY>(p, st, G, sms);
+  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, ASY, RES>(p, st, 1, sms);
+  else launch_g<DD, KPL, LA, MAXREG, true, ASY, RES>(p, st, G, sms);
 }
 
 // tuning variants (DADE_SCAN_VARIANT, read per launch) for the Delta_d = 16, K <= 32 kernel
@@ -644,6 +671,11 @@ static int scan_variant() {
 
 template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
+  constexpr int kReg = (KPL >= 4 || DD >= 4) ? 96 : 80;
+  if (p.residual) {  // BSA-res (NEXT-1): residual-norm test
+    launch_v<DD, KPL, 1, 96, false, true>(p, st);
+    return;
+  }
   if constexpr (DD == 1 && KPL == 1) {
     switch (scan_variant()) {
       case 1: launch_v<DD, KPL, 1, 80, true>(p, st); return;
@@ -653,7 +685,7 @@ static void launch_k(const ScanParams& p, cudaStream_t st) {
       default: break;
     }
   }
-  launch_v<DD, KPL, 1, (KPL >= 4 || DD >= 4) ? 96 : 80>(p, st);
+  launch_v<DD, KPL, 1, kReg>(p, st);
 }
 
 template <int DD>

@@ -60,6 +60,7 @@ _SIGS = {
     "dade_set_calibration": [P, I32, I32, I32, P, P],
     "dade_search": [P, P, I32, I32, I32, I32, DBL, P, P, P],
     "dade_search_host": [P, P, I32, I32, I32, I32, DBL, P, P, P],
+    "dade_search_method": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
     "dade_probe": [P, P, I32, I32, P],
     "dade_bruteforce_knn": [P, P, I64, I64, P, I32, I32, P, P],
     "dade_merge_topk": [P, P, P, I32, I32, I32, P, P],
@@ -221,6 +222,25 @@ class Index:
         st = Stats() if stats else None
         _ck(lib().dade_search(self.h, _ptr(Q), nq, K, nprobe, delta_d, float(significance), _ptr(ids),
                               _ptr(dists), C.byref(st) if st is not None else None))
+        return (ids, dists, st.as_dict()) if stats else (ids, dists)
+
+    METHODS = {"bsa_p": 0, "adsampling": 1, "bsa_res": 2}
+
+    def search_method(self, Q, K: int, nprobe: int, delta_d: int, method: str, param: float, ids=None,
+                      dists=None, stats: bool = False):
+        """NEXT-1: the same scan with another per-step test. method "bsa_p" (param = significance),
+        "adsampling" (param = eps0; install a random orthogonal rotation first), "bsa_res"
+        (param = multiplier m)."""
+        import torch
+        Q = _dev(Q, torch.float32)
+        nq = Q.shape[0]
+        if ids is None:
+            ids = torch.empty((nq, K), dtype=torch.int64, device=Q.device)
+        if dists is None:
+            dists = torch.empty((nq, K), dtype=torch.float32, device=Q.device)
+        st = Stats() if stats else None
+        _ck(lib().dade_search_method(self.h, _ptr(Q), nq, K, nprobe, delta_d, self.METHODS[method], float(param),
+                                     _ptr(ids), _ptr(dists), C.byref(st) if st is not None else None))
         return (ids, dists, st.as_dict()) if stats else (ids, dists)
 
     def search_host(self, Q, K: int, nprobe: int, delta_d: int, significance: float, ids=None, dists=None,
