@@ -38,7 +38,9 @@ SHAPE = {"c1": "flat, 20-component Gaussian mixture", "c2": "SIFT-shaped", "c3":
          "c4": "Deep-shaped (unit norm)", "c5": "100M-config-shaped mixture"}
 # nprobe at which the GPU arm first reaches recall@10 >= 0.95 (bench sweeps, profiles/): the
 # reference arm (the CPU oracle) is timed on the same operating point
-REF_NPROBE = {"c1": 1, "c2": 8, "c3": 96, "c4": 8, "c5": 32}
+REF_NPROBE = {"c1": 1, "c2": 8, "c3": 64, "c4": 8, "c5": 8}
+# NEXT-1 comparison (--method): the paper's defaults ε₀ = 2.1 (ADSampling), m = 8 (BSA-res)
+METHOD_PARAM = {"bsa_p": ALPHA, "adsampling": 2.1, "bsa_res": 8.0}
 
 
 def log(*a):
@@ -147,12 +149,16 @@ def run_dade(args):
         sharded.fit_rotation_sharded(full, Xd[lo:hi].contiguous(), lo, cfg.n)
     else:
         full.fit_rotation(Xd)
+    if args.method == "adsampling":  # ADSampling's projection: a Haar-random orthogonal matrix
+        mean, _, lam = full.get_rotation()
+        full.set_rotation(mean, synth.haar_basis(cfg.d, np.random.default_rng(12345)).T.copy(), lam)
     torch.cuda.synchronize()
     t_rot = time.time() - t0
     full.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
     torch.cuda.synchronize()
     t_ivf = time.time() - t0 - t_rot
-    full.calibrate(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
+    if args.method == "bsa_p":
+        full.calibrate(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
     torch.cuda.synchronize()
     t_cal = time.time() - t0 - t_rot - t_ivf
     log(f"[rank {rank}] build: rotation {t_rot:.2f}s ivf {t_ivf:.2f}s calibration {t_cal:.2f}s")
@@ -161,12 +167,13 @@ def run_dade(args):
     if world > 1:
         mean, R, lam = full.get_rotation()
         _, _, _, cent = full.get_ivf()
-        cal = full.get_calibration()
+        cal = full.get_calibration() if args.method == "bsa_p" else None
         full.close()
         ix = Index(cfg.d, local, stream)
         ix.set_rotation(mean, R, lam)
         ix.build_ivf(Xd[lo:hi].contiguous(), cfg.nlist, centroids=torch.from_numpy(cent).to(dev), id_base=lo)
-        ix.set_calibration(K, cal["m1"], cal["v"])
+        if args.method == "bsa_p":
+            ix.set_calibration(K, cal["m1"], cal["v"])
     else:
         ix = full
     del Xd
@@ -177,7 +184,11 @@ def run_dade(args):
 
 
     def step(nprobe, stats=False):
-        r = ix.search(Qd, K, nprobe, dd, ALPHA, ids=ids, dists=dists, stats=stats)
+        if args.method == "bsa_p":
+            r = ix.search(Qd, K, nprobe, dd, ALPHA, ids=ids, dists=dists, stats=stats)
+        else:
+            r = ix.search_method(Qd, K, nprobe, dd, args.method, METHOD_PARAM[args.method], ids=ids, dists=dists,
+                                 stats=stats)
         if world > 1:  # a9: NCCL all-gather of the local top-K + merge kernel
             out = ix.merge_topk(sharded._all_gather(ids), sharded._all_gather(dists))
             return out, (r[2] if stats else None)
@@ -247,12 +258,19 @@ def run_dade(args):
     ih = torch.empty((cfg.nq, K), dtype=torch.int64).pin_memory()
     dh = torch.empty((cfg.nq, K), dtype=torch.float32).pin_memory()
     e2e_ms = []
+    Qtmp = torch.empty_like(Qd)
     for it in range(args.warmup + args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ix.search_host(Qh, K, chosen, dd, ALPHA, ids=ih, dists=dh)
+        if args.method == "bsa_p":
+            ix.search_host(Qh, K, chosen, dd, ALPHA, ids=ih, dists=dh)
+        else:  # H2D of the queries, search, D2H of the results, all on the library's stream
+            Qtmp.copy_(Qh, non_blocking=True)
+            ix.search_method(Qtmp, K, chosen, dd, args.method, METHOD_PARAM[args.method], ids=ids, dists=dists)
+            ih.copy_(ids, non_blocking=True)
+            dh.copy_(dists, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         if it >= args.warmup:
@@ -280,7 +298,8 @@ def run_dade(args):
 
     out = None
     if rank == 0:
-        cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(cfg, chosen, budget_s=args.cpu_budget)
+        cpu = None if (args.no_cpu_baseline or world > 1 or args.method != "bsa_p") else \
+            cpu_baseline(cfg, chosen, budget_s=args.cpu_budget)
         out = {
             "metric": "QPS at recall@10=0.95 (dade_search, all stages)",
             "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -289,6 +308,7 @@ def run_dade(args):
             "data": f"synthetic (datagen/synth.py, seed 0; {SHAPE[cfg.name]} stand-in for the paper's datasets)",
             "config": {"workload": f"{cfg.name}: IVF-DADE {SHAPE[cfg.name]} n={cfg.n} D={cfg.d} nq={cfg.nq} "
                                    f"nlist={cfg.nlist} K={K} delta_d={dd} significance={ALPHA}",
+                       "method": args.method, "method_param": METHOD_PARAM[args.method],
                        "nprobe": chosen, "recall@10": next(s["recall"] for s in sweep if s["nprobe"] == chosen),
                        "qps_interp_at_0.95": None if interp is None else round(interp, 1),
                        "sweep": sweep, "parallelism": f"db-shard{world}" if world > 1 else "single",
@@ -422,6 +442,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dade", choices=["dade", "reference"])
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--method", default="bsa_p", choices=["bsa_p", "adsampling", "bsa_res"],
+                    help="per-step correction: the paper's data-driven BSA-p (default, the headline), or the "
+                         "NEXT-1 comparisons ADSampling (eps0 = 2.1, random rotation) / BSA-res (m = 8)")
     ap.add_argument("--nprobe", type=int, default=0, help="fix nprobe instead of sweeping to recall 0.95")
     ap.add_argument("--n", type=int, default=0, help="override base size (testing only)")
     ap.add_argument("--nlist", type=int, default=0)
