@@ -58,6 +58,9 @@ struct dade_index {
   DBuf<double> lam_d;
   bool xnorm_ok = false;
   cudaEvent_t ev[5] = {};
+  // a4 (rotation) runs on a side stream concurrently with a5 (probe): fork/join events
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 // ------------------------------------------------------------------ error plumbing
@@ -322,11 +325,20 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     x->flag.reserve(1);
     DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), st));
   }
-  launch_check_finite(Q, (int64_t)nq * D, x->flag.p, st, 3);
-  // a4 rotate queries (fp64 accumulation)
+  // a4 rotate queries (fp64 accumulation) on the side stream, concurrently with the a5 probe
+  // (the probe reads the raw queries); both join before the scan
+  if (!x->side) {
+    DADE_CK(cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking));
+    DADE_CK(cudaEventCreateWithFlags(&x->fork, cudaEventDisableTiming));
+    DADE_CK(cudaEventCreateWithFlags(&x->join, cudaEventDisableTiming));
+  }
+  DADE_CK(cudaEventRecord(x->fork, st));
+  DADE_CK(cudaStreamWaitEvent(x->side, x->fork, 0));
+  launch_check_finite(Q, (int64_t)nq * D, x->flag.p, x->side, 3);
   x->qrot.reserve((size_t)nq * D);
-  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
-  if (stats) DADE_CK(cudaEventRecord(x->ev[1], st));
+  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, x->side);
+  if (stats) DADE_CK(cudaEventRecord(x->ev[1], x->side));
+  DADE_CK(cudaEventRecord(x->join, x->side));
   // a5 exact probes
   x->probes.reserve((size_t)nq * nprobe);
   if (x->nlist == 1) {
@@ -334,6 +346,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   } else {
     exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr, x->cent_tc, false);
   }
+  DADE_CK(cudaStreamWaitEvent(st, x->join, 0));
   if (stats) DADE_CK(cudaEventRecord(x->ev[2], st));
   // step table (R4, R5): alpha_s = alpha*delta_d/D, k = clamp(ceil((1-alpha_s)*n0), 1, n0)
   ScanParams p{};
@@ -405,8 +418,8 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     if (getenv("DADE_DEBUG_COUNTS"))
       fprintf(stderr, "[dade debug] rounds=%llu entries=%llu merges=%llu tiles=%llu drain_rounds=%llu\n",
               c[68], c[69], c[70], c[71], c[72]);
-    cudaEventElapsedTime(&stats->ms_rotate, x->ev[0], x->ev[1]);
-    cudaEventElapsedTime(&stats->ms_probe, x->ev[1], x->ev[2]);
+    cudaEventElapsedTime(&stats->ms_rotate, x->ev[0], x->ev[1]);  // concurrent with the probe
+    cudaEventElapsedTime(&stats->ms_probe, x->ev[0], x->ev[2]);
     cudaEventElapsedTime(&stats->ms_scan, x->ev[2], x->ev[3]);
     cudaEventElapsedTime(&stats->ms_total, x->ev[0], x->ev[3]);
   }
@@ -445,6 +458,12 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release();
   for (auto& e : x->ev)
     if (e) cudaEventDestroy(e);
+  if (x->side) {
+    cudaStreamSynchronize(x->side);
+    cudaStreamDestroy(x->side);
+    cudaEventDestroy(x->fork);
+    cudaEventDestroy(x->join);
+  }
   delete x;
   API_END
 }
