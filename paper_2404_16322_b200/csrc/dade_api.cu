@@ -157,7 +157,7 @@ void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_ma
 // re-rank of every column inside the certified window (exact.cu). Bit-exact with the fp64
 // sequential-sum definition (R20). out_idx: device m x k int32; out_d64: device m x k or null.
 void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t n, int k,
-               int32_t* out_idx, double* out_d64, const TcOp& bop, bool sync = true) {
+               int32_t* out_idx, double* out_d64, const TcOp& bop, bool sync = true, int passes = 3) {
   const int D = x->D;
   DADE_REQUIRE(k >= 1 && k <= n, DADE_ERR_ARG, "exact_knn: k out of range");
   DADE_REQUIRE(k <= 4096, DADE_ERR_UNSUPPORTED, "exact_knn: k > 4096");
@@ -182,10 +182,10 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     for (int64_t r0 = 0; r0 < m; r0 += chunk) {
       const int64_t mm = std::min(chunk, m - r0);
       tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
-      launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream);
+      launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream, passes);
       launch_probe_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D, k,
                       x->slack.p, A + r0 * D, B, x->cand.p, x->cand.p + (size_t)chunk * nsplit * C * 2, nsplit,
-                      out_idx + r0 * k, out_d64 ? out_d64 + r0 * k : nullptr, x->stream);
+                      out_idx + r0 * k, out_d64 ? out_d64 + r0 * k : nullptr, x->stream, passes);
     }
     if (sync) check_knn_flag(x);
     return;
@@ -232,8 +232,8 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
     const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 256 && n <= 32 * 256;
     launch_l2_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
-                 x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr);
-    launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream);
+                 x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr, passes);
+    launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream, passes);
     if (use_gmin) {
       x->ovf.reserve((size_t)chunk + 1);
       launch_select_gmin(x->dmat.p, x->gmin.p, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
@@ -258,6 +258,14 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   tc_prepare(x, B, n, bop, true);
   exact_knn(x, A, m, B, n, k, out_idx, out_d64, bop);
   bop.release();
+}
+
+// passes of the probe's tensor-core filter: 1 (tf32 hi parts only: 1/3 of the MMAs and 1/2 of the
+// operand bytes, a ~40x wider but still rigorous certified window; the fp64 re-rank keeps the
+// result exact) unless DADE_PROBE_PASSES=3
+int probe_passes() {
+  const char* e = getenv("DADE_PROBE_PASSES");
+  return e ? atoi(e) : 1;
 }
 
 void upload_rotation(dade_index* x) {
@@ -344,7 +352,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   if (x->nlist == 1) {
     DADE_CK(cudaMemsetAsync(x->probes.p, 0, sizeof(int32_t) * nq, st));
   } else {
-    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr, x->cent_tc, false);
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr, x->cent_tc, false, probe_passes());
   }
   DADE_CK(cudaStreamWaitEvent(st, x->join, 0));
   if (stats) DADE_CK(cudaEventRecord(x->ev[2], st));
@@ -942,7 +950,7 @@ extern "C" dade_status dade_probe(dade_index* x, const float* Q, int nq, int npr
   DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "no IVF");
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
   DeviceGuard g(x->device);
-  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc);
+  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, true, probe_passes());
   API_END
 }
 

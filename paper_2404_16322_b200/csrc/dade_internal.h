@@ -72,16 +72,17 @@ void launch_argmin_exact(const float* d_hat, int64_t m, int64_t n, const float* 
 // gemm_tf32.cu : tensor-core (tcgen05 kind::tf32, 3-pass split) distance filter tiles
 int64_t tc_rows_pad(int64_t rows);
 int tc_nkc(int D);
-float tc_gamma(int D);
+float tc_gamma(int D, int passes = 3);
 // center (nullable, fp32 D): operands are split from fl(x - center)
 void launch_split_tf32(const float* X, int64_t rows, int D, const float* center, float* hi, float* lo,
                        float* norm, cudaStream_t st);
 // out[j] = fp32(mean_r X[r, j]) (fp64 sums in scratch[D])
 void launch_col_mean(const float* X, int64_t n, int D, double* scratch, float* out, cudaStream_t st);
-void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, cudaStream_t st);
+void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, cudaStream_t st,
+                  int passes = 3);
 void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
-                  cudaStream_t st, float* gmin = nullptr);
+                  cudaStream_t st, float* gmin = nullptr, int passes = 3);
 // warp-per-row exact select using the GEMM's 32-column group minima (k <= ceil(n/32) <= 256)
 void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_t n, int k,
                         const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
@@ -98,7 +99,7 @@ int probe_tc_splits(int64_t m, int64_t n, int sms);
 void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                      const float* Blo, const float* bn, int64_t n, int D, int k, const float* slack,
                      const float* A, const float* B, int32_t* cand, int32_t* ccount, int nsplit,
-                     int32_t* out_idx, double* out_d64, cudaStream_t st);
+                     int32_t* out_idx, double* out_d64, cudaStream_t st, int passes = 3);
 void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st);
 
 // rotate.cu : x~ = R (x - mu) with fp64 accumulation, stored fp32.

@@ -5,6 +5,7 @@
 //   3. candidates = columns with d_hat <= d_hat_(k) * (1+rho)/(1-rho)  (contains every column whose
 //      exact distance is <= the exact k-th distance, ties included),
 //   4. exact fp64 sequential sums (no FMA contraction) for the candidates, sort by (dist, column).
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 
@@ -242,8 +243,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_select_small(
   __shared__ Cand cs[kSmallCap];
   __shared__ unsigned s_cnt, s_bin, s_cum;
   const int tid = threadIdx.x;
-  if (rows && (int)blockIdx.x >= *nrows) return;  // fallback mode: only the listed rows
-  const int64_t row = rows ? rows[blockIdx.x] : blockIdx.x;
+  // fallback mode (rows != null): a small grid walks the listed rows
+  const int64_t nr = rows ? (int64_t)*nrows : (int64_t)gridDim.x;
+  for (int64_t ri = blockIdx.x; ri < nr; ri += rows ? gridDim.x : nr) {
+  const int64_t row = rows ? rows[ri] : ri;
   float v[EPT];
   uint32_t inplay = 0;
 #pragma unroll
@@ -352,6 +355,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_select_small(
     out_idx[row * k + i] = ok ? cs[i].c : -1;
     if (out_d) out_d[row * k + i] = ok ? cs[i].d : DBL_MAX;
   }
+  __syncthreads();  // shared state is reused by the next listed row
+  }
 }
 
 // Warp-per-row exact select for the tensor-core filter. E = the k-th smallest of the row's
@@ -376,43 +381,69 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   const int64_t row = (int64_t)blockIdx.x * kGmWarps + w;
   if (row >= m) return;
   const int ng = (int)((n + 31) / 32);
-  float* g = sg[w];
-  for (int i = lane; i < 256; i += 32) g[i] = i < ng ? gm[row * ng + i] : INFINITY;
-  __syncwarp();
-  // bitonic sort of the 256 group minima (8 per lane)
-  for (int size = 2; size <= 256; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = lane; i < 128; i += 32) {
-        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const float x = g[lo], y = g[hi];
-        if ((y < x) == up) { g[lo] = y; g[hi] = x; }
+  // the k-th smallest group minimum E bounds the k-th smallest d_hat from above
+  float gv[8];  // group lane + 32 j
+#pragma unroll
+  for (int j = 0; j < 8; ++j) gv[j] = lane + 32 * j < ng ? gm[row * ng + lane + 32 * j] : INFINITY;
+  float E;
+  if (k <= 16) {  // k rounds of a warp-wide minimum (keys (value bits, group) are unique)
+    float rem[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) rem[j] = gv[j];
+    unsigned long long key = 0;
+    for (int r = 0; r < k; ++r) {
+      unsigned long long mine = ~0ull;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const unsigned long long kk = ((unsigned long long)__float_as_uint(rem[j]) << 32) | (unsigned)(lane + 32 * j);
+        mine = kk < mine ? kk : mine;
       }
-      __syncwarp();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, mine, o);
+        mine = t < mine ? t : mine;
+      }
+      key = mine;
+      const int gsel = (int)(key & 0xffffffffu);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j == gsel) rem[j] = __uint_as_float(0x7f800001u);  // removed (NaN: sorts last as bits)
     }
-  const float E = g[k - 1];
+    E = __uint_as_float((unsigned)(key >> 32));
+  } else {  // bitonic sort of the 256 group minima (8 per lane)
+    float* g = sg[w];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[lane + 32 * j] = gv[j];
+    __syncwarp();
+    for (int size = 2; size <= 256; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = lane; i < 128; i += 32) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const float x = g[lo], y = g[hi];
+          if ((y < x) == up) { g[lo] = y; g[hi] = x; }
+        }
+        __syncwarp();
+      }
+    E = g[k - 1];
+  }
   const unsigned tb = abs_thr_bits(E, slack[row]);
-  // collect every column inside the window (one coalesced pass over the row)
+  // every column inside the window lies in a group whose minimum is inside it: read only those
+  // groups' d_hat (one coalesced 128-B row segment per group)
   const float* d = dh + row * n;
   int cnt = 0;
-  for (int64_t i0 = 0; i0 < n; i0 += 128) {
-    const int64_t i = i0 + lane * 4;
-    float4 v = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-    if (i + 3 < n && (n & 3) == 0) v = *reinterpret_cast<const float4*>(d + i);
-    else {
-      if (i + 3 < n) v.w = d[i + 3];
-      if (i < n) v.x = d[i];
-      if (i + 1 < n) v.y = d[i + 1];
-      if (i + 2 < n) v.z = d[i + 2];
-    }
-    const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const bool in = __float_as_uint(vv[t]) <= tb;
+#pragma unroll 1
+  for (int j = 0; j < 8; ++j) {
+    unsigned gb = __ballot_sync(0xffffffffu, __float_as_uint(gv[j]) <= tb);
+    while (gb) {
+      const int grp = 32 * j + __ffs(gb) - 1;
+      gb &= gb - 1;
+      const int64_t c = (int64_t)grp * 32 + lane;
+      const bool in = c < n && __float_as_uint(d[c]) <= tb;
       const unsigned bal = __ballot_sync(0xffffffffu, in);
       if (in) {
         const int pos = cnt + __popc(bal & ((1u << lane) - 1));
-        if (pos < kGmCap) cc[w][pos] = (int32_t)(i + t);
+        if (pos < kGmCap) cc[w][pos] = (int32_t)c;
       }
       cnt += __popc(bal);
     }
@@ -593,13 +624,14 @@ void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_
   k_select_gmin<<<(unsigned)((m + kGmWarps - 1) / kGmWarps), kGmWarps * 32, 0, st>>>(
       d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
   DADE_CK(cudaGetLastError());
-  // device-side fallback (no host round trip): the listed rows only
+  // device-side fallback (no host round trip): a small grid walks the listed rows
+  const unsigned fg = (unsigned)std::min<int64_t>(m, 296);
   if (n <= 16 * kSmallThreads)
-    k_select_small<16><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag,
-                                                               slack, ovf_rows, ovf_n);
+    k_select_small<16><<<fg, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag,
+                                                      slack, ovf_rows, ovf_n);
   else
-    k_select_small<32><<<(unsigned)m, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag,
-                                                               slack, ovf_rows, ovf_n);
+    k_select_small<32><<<fg, kSmallThreads, 0, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64, d_flag,
+                                                      slack, ovf_rows, ovf_n);
   DADE_CK(cudaGetLastError());
 }
 

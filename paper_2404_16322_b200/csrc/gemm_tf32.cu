@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
                                                   const float* __restrict__ an, const float* __restrict__ Bhi,
                                                   const float* __restrict__ Blo, const float* __restrict__ bn,
                                                   int nkc, float* __restrict__ out, int64_t m, int64_t n,
-                                                  int64_t ldo, float* __restrict__ gmin, int64_t ldg) {
+                                                  int64_t ldo, float* __restrict__ gmin, int64_t ldg, int passes) {
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * kStageBytes);
   uint64_t* empty = full + 2;
@@ -161,15 +161,17 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   if (tid == 0) {
     // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
-    auto load = [&](int kc) {
+    auto load = [&](int kc) {  // passes == 1: the hi parts only
       const int s = kc & 1;
       unsigned char* st = sm + s * kStageBytes;
-      mbar_expect_tx(&full[s], kStageBytes);
+      mbar_expect_tx(&full[s], passes == 1 ? kStageBytes / 2 : kStageBytes);
       const int64_t ao = (tm * nkc + kc) * kSub, bo = (tn * nkc + kc) * kSub;
       bulk_g2s(st, Ahi + ao, kSub * 4, &full[s]);
-      bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
       bulk_g2s(st + 2 * kSub * 4, Bhi + bo, kSub * 4, &full[s]);
-      bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
+      if (passes != 1) {
+        bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
+        bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
+      }
     };
     load(0);
     if (nkc > 1) load(1);
@@ -185,8 +187,10 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
         const uint64_t bh = umma_desc(st + 2 * kSub * 4 + j * 256, 128, kSBO);
         const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
         mma_tf32(tmem, ah, bh, idesc, (kc | j) != 0);
-        mma_tf32(tmem, ah, bl, idesc, 1);
-        mma_tf32(tmem, al, bh, idesc, 1);
+        if (passes != 1) {
+          mma_tf32(tmem, ah, bl, idesc, 1);
+          mma_tf32(tmem, al, bh, idesc, 1);
+        }
       }
       mma_commit(&empty[s]);
       if (kc + 2 < nkc) {
@@ -262,20 +266,25 @@ void launch_split_tf32(const float* X, int64_t rows, int D, const float* center,
   DADE_CK(cudaGetLastError());
 }
 
-float tc_gamma(int D) {
+// relative error coefficient of d_hat (x2 margin): 3-pass split: split error 3 2^-22 per term,
+// fp32 accumulation of 3 Dp terms, norm and final roundings; 1-pass (hi parts only): tf32
+// rounding of both operands (2 2^-11 + 2^-22 per term) and Dp accumulated terms
+float tc_gamma(int D, int passes) {
   const double u23 = 1.1920928955078125e-07;  // 2^-23
-  return (float)(2.0 * (3.0 * tc_nkc(D) * kKC + 16.0) * u23);
+  const int Dp = tc_nkc(D) * kKC;
+  if (passes == 1) return (float)(2.0 * (9.765625e-04 + (Dp + 16.0) * u23));  // 2^-10
+  return (float)(2.0 * (3.0 * Dp + 16.0) * u23);
 }
 
-void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, cudaStream_t st) {
+void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, cudaStream_t st, int passes) {
   if (m <= 0) return;
-  k_slack<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(an, m, bmax, tc_gamma(D), slack);
+  k_slack<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(an, m, bmax, tc_gamma(D, passes), slack);
   DADE_CK(cudaGetLastError());
 }
 
 void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
-                  cudaStream_t st, float* gmin) {
+                  cudaStream_t st, float* gmin, int passes) {
   if (m <= 0 || n <= 0) return;
   static bool attr = false;
   const size_t smem = 2 * kStageBytes + 64;
@@ -285,7 +294,7 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
   }
   dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
   k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), out, m, n, ldo, gmin,
-                                   (n + 31) / 32);
+                                   (n + 31) / 32, passes);
   DADE_CK(cudaGetLastError());
 }
 

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
     const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ an,
     const float* __restrict__ Bhi, const float* __restrict__ Blo, const float* __restrict__ bn, int nkc,
     int64_t m, int64_t n, int tiles_per_split, int k, int C, const float* __restrict__ slack,
-    int32_t* __restrict__ cand, int32_t* __restrict__ ccount, int dbg) {
+    int32_t* __restrict__ cand, int32_t* __restrict__ ccount, int dbg, int passes) {
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
@@ -163,12 +163,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
           const int s = it % kStages;
           if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
           unsigned char* st = sm + s * kStageBytes;
-          mbar_expect_tx(&full[s], kStageBytes);
+          mbar_expect_tx(&full[s], passes == 1 ? kStageBytes / 2 : kStageBytes);
           const int64_t ao = (tm * nkc + kc) * kSub, bo = (tn * nkc + kc) * kSub;
           bulk_g2s(st, Ahi + ao, kSub * 4, &full[s]);
-          bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
           bulk_g2s(st + 2 * kSub * 4, Bhi + bo, kSub * 4, &full[s]);
-          bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
+          if (passes != 1) {  // 3-pass split: the lo parts too
+            bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
+            bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
+          }
         }
       }
     }
@@ -193,8 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
             const uint64_t bh = umma_desc(st + 2 * kSub * 4 + j * 256, 128, kSBO);
             const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
             mma_tf32(acc, ah, bh, idesc, (kc | j) != 0);
-            mma_tf32(acc, ah, bl, idesc, 1);
-            mma_tf32(acc, al, bh, idesc, 1);
+            if (passes != 1) {
+              mma_tf32(acc, ah, bl, idesc, 1);
+              mma_tf32(acc, al, bh, idesc, 1);
+            }
           }
           mma_commit(&empty[s]);
         }
@@ -506,7 +510,7 @@ int probe_tc_splits(int64_t m, int64_t n, int sms) {
 void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                      const float* Blo, const float* bn, int64_t n, int D, int k, const float* slack,
                      const float* A, const float* B, int32_t* cand, int32_t* ccount, int nsplit,
-                     int32_t* out_idx, double* out_d64, cudaStream_t st) {
+                     int32_t* out_idx, double* out_d64, cudaStream_t st, int passes) {
   if (m <= 0) return;
   const int C = probe_tc_cap(k);
   const size_t smem = kStages * kStageBytes + 128 + (size_t)kTM * (k * 4 + C * 8);
@@ -521,7 +525,7 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
   dim3 grid((unsigned)((m + kTM - 1) / kTM), (unsigned)nsplit);
   const int dbg = getenv("DADE_PROBE_DBG") ? atoi(getenv("DADE_PROBE_DBG")) : 0;
   k_probe_tc<<<grid, kThreads, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), m, n, tps, k, C, slack, cand,
-                                          ccount, dbg);
+                                          ccount, dbg, passes);
   DADE_CK(cudaGetLastError());
   const size_t fsm = (size_t)kFinWarps * kFinWarpBytes;
   static bool fattr = false;

@@ -53,7 +53,15 @@ def test_bruteforce_knn_integer_ties(torch_cuda):
     assert np.array_equal(gi.cpu().numpy(), oi)
 
 
-def test_probe_and_assign_bit_exact(torch_cuda):
+@pytest.fixture(params=["1", "3"], ids=["1-pass", "3-pass"])
+def probe_passes(request, monkeypatch):
+    # the probe's tensor-core filter runs 1-pass (hi parts, wide window) or 3-pass (split); both
+    # must certify the same exact answer
+    monkeypatch.setenv("DADE_PROBE_PASSES", request.param)
+    return request.param
+
+
+def test_probe_and_assign_bit_exact(torch_cuda, probe_passes):
     torch = torch_cuda
     rng = np.random.default_rng(2)
     D, n, C = 64, 6000, 200
@@ -76,7 +84,7 @@ def test_probe_and_assign_bit_exact(torch_cuda):
 
 
 @pytest.mark.parametrize("nprobe", [1, 7, 64])
-def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe):
+def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe, probe_passes):
     # several column tiles per split and a ragged last tile (3000 = 23 x 128 + 56), integer data
     # with exact distance ties; both selection paths must return the oracle's probes exactly
     torch = torch_cuda
