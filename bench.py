@@ -343,7 +343,7 @@ def launches_per_search(cfg, world, nprobe):
     k_scan; + k_merge_topk when sharded."""
     if cfg.nlist <= 1:
         probe = 0
-    elif nprobe <= 64 and cfg.nlist >= 8192:
+    elif nprobe <= 64 and (cfg.nlist + 31) // 32 > 1024:
         probe = 4 * ((cfg.nq + 65535) // 65536)
     else:
         chunk = min(max(128, (1 << 29) // cfg.nlist // 128 * 128), 16384)

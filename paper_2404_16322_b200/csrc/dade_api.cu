@@ -166,10 +166,11 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     x->flag.reserve(1);
     DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
   }
-  // fused path for wide rows (measured: faster than the d_hat path from nlist ~8k on; slower at
-  // 4096); DADE_FUSED_PROBE=0/1 forces either path (tests cover both)
+  // fused path only for very wide rows, where the d_hat matrix would not fit the group-minima
+  // select (> 1024 groups; measured at 16,384 columns: d_hat path 0.31 ms, fused 0.61 ms);
+  // DADE_FUSED_PROBE=0/1 forces either path (tests cover both)
   const char* fz = getenv("DADE_FUSED_PROBE");
-  const bool fused = k <= 64 && n >= 256 && (fz ? atoi(fz) != 0 : n >= 8192);
+  const bool fused = k <= 64 && n >= 256 && (fz ? atoi(fz) != 0 : (n + 31) / 32 > 1024);
   if (fused) {
     // fused filter GEMM + candidate tracking (probe_tc.cu): no m x n d_hat matrix
     static int sms = 0;
@@ -230,7 +231,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t mm = std::min(chunk, m - r0);
     tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
-    const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 256 && n <= 32 * 256;
+    const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 1024;
     launch_l2_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
                  x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr, passes);
     launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream, passes);

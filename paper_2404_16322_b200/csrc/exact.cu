@@ -369,11 +369,12 @@ __device__ __forceinline__ bool cand_less2(double d0, int32_t c0, double d1, int
   return d0 < d1 || (d0 == d1 && c0 < c1);
 }
 
+template <int GPL>  // group minima per lane: rows of up to 32 * GPL groups (32 * 32 * GPL columns)
 __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
     const float* __restrict__ dh, const float* __restrict__ gm, int64_t m, int64_t n, int k,
     const float* __restrict__ A, const float* __restrict__ B, int D, int32_t* __restrict__ out_idx,
     double* __restrict__ out_d, int* ovf_n, int32_t* __restrict__ ovf_rows, const float* __restrict__ slack) {
-  __shared__ float sg[kGmWarps][256];
+  __shared__ float sg[kGmWarps][32 * GPL];
   __shared__ double cd[kGmWarps][kGmCap];
   __shared__ int32_t cc[kGmWarps][kGmCap];
   __shared__ float xstage[kGmWarps][32 * (kXbDim + 1)];
@@ -382,19 +383,19 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   if (row >= m) return;
   const int ng = (int)((n + 31) / 32);
   // the k-th smallest group minimum E bounds the k-th smallest d_hat from above
-  float gv[8];  // group lane + 32 j
+  float gv[GPL];  // group lane + 32 j
 #pragma unroll
-  for (int j = 0; j < 8; ++j) gv[j] = lane + 32 * j < ng ? gm[row * ng + lane + 32 * j] : INFINITY;
+  for (int j = 0; j < GPL; ++j) gv[j] = lane + 32 * j < ng ? gm[row * ng + lane + 32 * j] : INFINITY;
   float E;
   if (k <= 16) {  // k rounds of a warp-wide minimum (keys (value bits, group) are unique)
-    float rem[8];
+    float rem[GPL];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) rem[j] = gv[j];
+    for (int j = 0; j < GPL; ++j) rem[j] = gv[j];
     unsigned long long key = 0;
     for (int r = 0; r < k; ++r) {
       unsigned long long mine = ~0ull;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < GPL; ++j) {
         const unsigned long long kk = ((unsigned long long)__float_as_uint(rem[j]) << 32) | (unsigned)(lane + 32 * j);
         mine = kk < mine ? kk : mine;
       }
@@ -406,18 +407,18 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
       key = mine;
       const int gsel = (int)(key & 0xffffffffu);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < GPL; ++j)
         if (lane + 32 * j == gsel) rem[j] = __uint_as_float(0x7f800001u);  // removed (NaN: sorts last as bits)
     }
     E = __uint_as_float((unsigned)(key >> 32));
-  } else {  // bitonic sort of the 256 group minima (8 per lane)
+  } else {  // bitonic sort of the group minima (GPL per lane)
     float* g = sg[w];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) g[lane + 32 * j] = gv[j];
+    for (int j = 0; j < GPL; ++j) g[lane + 32 * j] = gv[j];
     __syncwarp();
-    for (int size = 2; size <= 256; size <<= 1)
+    for (int size = 2; size <= 32 * GPL; size <<= 1)
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = lane; i < 128; i += 32) {
+        for (int i = lane; i < 16 * GPL; i += 32) {
           const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
           const bool up = (lo & size) == 0;
           const float x = g[lo], y = g[hi];
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   const float* d = dh + row * n;
   int cnt = 0;
 #pragma unroll 1
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < GPL; ++j) {
     unsigned gb = __ballot_sync(0xffffffffu, __float_as_uint(gv[j]) <= tb);
     while (gb) {
       const int grp = 32 * j + __ffs(gb) - 1;
@@ -621,8 +622,14 @@ void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_
                         cudaStream_t st) {
   if (m <= 0) return;
   DADE_CK(cudaMemsetAsync(ovf_n, 0, sizeof(int), st));
-  k_select_gmin<<<(unsigned)((m + kGmWarps - 1) / kGmWarps), kGmWarps * 32, 0, st>>>(
-      d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+  const int64_t ngr = (n + 31) / 32;
+  const unsigned gsz = (unsigned)((m + kGmWarps - 1) / kGmWarps);
+  if (ngr <= 256)
+    k_select_gmin<8><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+  else if (ngr <= 512)
+    k_select_gmin<16><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+  else
+    k_select_gmin<32><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
   DADE_CK(cudaGetLastError());
   // device-side fallback (no host round trip): a small grid walks the listed rows
   const unsigned fg = (unsigned)std::min<int64_t>(m, 296);

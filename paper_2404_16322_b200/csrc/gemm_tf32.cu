@@ -205,37 +205,57 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int64_t row = tm * kTM + warp * 32 + lane;
   const float a2 = row < m ? an[row] : 0.f;
+  // the operand stages are free once every MMA completed: each warp transposes its 32 x 32
+  // d_hat chunk through shared memory so the global stores are row-contiguous (128 B per row)
+  float* stg = reinterpret_cast<float*>(sm) + warp * 32 * 33;
 #pragma unroll 1
   for (int cb = 0; cb < kTM / 32; ++cb) {
     uint32_t r[32];
     TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + cb * 32, r);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     const int64_t c0 = tn * kTM + cb * 32;
-    if (gmin && row < m) {  // per-row minimum of this 32-column group (select hint)
-      float mn = INFINITY;
+    const bool full = c0 + 32 <= n;
+    float d[32];
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(bn + c0 + j);
+        d[j + 0] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 0]), a2 + b4.x));
+        d[j + 1] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 1]), a2 + b4.y));
+        d[j + 2] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 2]), a2 + b4.z));
+        d[j + 3] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 3]), a2 + b4.w));
+      }
+    } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        if (c0 + j < n) mn = fminf(mn, fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j])));
-      if (c0 < n) gmin[row * ldg + (c0 >> 5)] = mn;
+        d[j] = c0 + j < n ? fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j])) : INFINITY;
     }
-    if (out && row < m) {  // out == nullptr: group minima only (k_select_groups)
-      float* o = out + row * ldo + c0;
-      if (c0 + 32 <= n && (ldo & 3) == 0) {
+    if (gmin && row < m && c0 < n) {  // per-row minimum of this 32-column group (select hint)
+      float mn = d[0];
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const float4 b4 = *reinterpret_cast<const float4*>(bn + c0 + j);
-          float4 v;
-          v.x = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 0]), a2 + b4.x));
-          v.y = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 1]), a2 + b4.y));
-          v.z = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 2]), a2 + b4.z));
-          v.w = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 3]), a2 + b4.w));
-          *reinterpret_cast<float4*>(o + j) = v;
+      for (int j = 1; j < 32; ++j) mn = fminf(mn, d[j]);
+      gmin[row * ldg + (c0 >> 5)] = mn;
+    }
+    if (!out) continue;  // group minima only (k_select_groups)
+    if (full && (ldo & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = d[j];
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {  // 4 rows x 32 columns per instruction, 128 B per row
+        const int ri = it * 4 + (lane >> 3), cc = (lane & 7) * 4;
+        const int64_t grow = tm * kTM + warp * 32 + ri;
+        if (grow < m) {
+          const float* sp = stg + ri * 33 + cc;
+          *reinterpret_cast<float4*>(out + grow * ldo + c0 + cc) = make_float4(sp[0], sp[1], sp[2], sp[3]);
         }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c0 + j < n) o[j] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j]));
       }
+      __syncwarp();
+    } else if (row < m) {
+      float* o = out + row * ldo + c0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c0 + j < n) o[j] = d[j];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -84,12 +84,14 @@ def test_probe_and_assign_bit_exact(torch_cuda, probe_passes):
 
 
 @pytest.mark.parametrize("nprobe", [1, 7, 64])
-def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe, probe_passes):
-    # several column tiles per split and a ragged last tile (3000 = 23 x 128 + 56), integer data
-    # with exact distance ties; both selection paths must return the oracle's probes exactly
+@pytest.mark.parametrize("C", [3000, 20000])
+def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe, C, probe_passes):
+    # several column tiles per split and a ragged last tile (3000 = 23 x 128 + 56; 20000 = 625
+    # 32-column groups), integer data with exact distance ties; both selection paths must return
+    # the oracle's probes exactly
     torch = torch_cuda
     rng = np.random.default_rng(7)
-    D, n, C = 96, 9000, 3000
+    D, n = 96, 3 * C
     X = rng.integers(0, 5, size=(n, D)).astype(np.float32)
     cent = X[rng.choice(n, C, replace=False)].copy()
     cent[1000] = cent[10]
