@@ -685,6 +685,12 @@ static void launch_k(const ScanParams& p, cudaStream_t st) {
       default: break;
     }
   }
+  if constexpr (DD >= 2) {  // a step spans DD blocks: gather a whole step per round trip
+    if (scan_variant() != 7) {
+      launch_v<DD, KPL, 2, 96>(p, st);
+      return;
+    }
+  }
   launch_v<DD, KPL, 1, kReg>(p, st);
 }
 
