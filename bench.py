@@ -115,7 +115,10 @@ def run_dade(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl")
+        # NCCL over NVLink in production; DADE_DIST_BACKEND=gloo runs the same multi-rank code path
+        # on a single visible GPU as a functional check (its timings are not a measurement)
+        dist.init_process_group(os.environ.get("DADE_DIST_BACKEND", "nccl"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     from paper_2404_16322_b200 import Index, build, sharded
     if rank == 0:
@@ -183,15 +186,25 @@ def run_dade(args):
     dists = torch.empty((cfg.nq, K), dtype=torch.float32, device=dev)
 
 
+    qpart = sharded.QueryPartitionedSearch(ix) if world > 1 else None
+
+    def shard_stats(nprobe):
+        """N > 1: counters and stage times of this rank's scan of all queries (a separate prepared
+        search; never inside a timed region)."""
+        qr, pr = ix.prepare(Qd, nprobe)
+        return ix.search_prepared(qr, pr, K, dd, args.method, METHOD_PARAM[args.method], stats=True)[2]
+
     def step(nprobe, stats=False):
+        if world > 1:
+            # N > 1: each rank rotates + probes nq/N queries, NCCL all-gather of q~ and probes,
+            # every rank scans all queries on its shard, NCCL all-gather of the local top-K + merge
+            out = qpart.search(Qd, K, nprobe, dd, args.method, METHOD_PARAM[args.method])
+            return out, (shard_stats(nprobe) if stats else None)
         if args.method == "bsa_p":
             r = ix.search(Qd, K, nprobe, dd, ALPHA, ids=ids, dists=dists, stats=stats)
         else:
             r = ix.search_method(Qd, K, nprobe, dd, args.method, METHOD_PARAM[args.method], ids=ids, dists=dists,
                                  stats=stats)
-        if world > 1:  # a9: NCCL all-gather of the local top-K + merge kernel
-            out = ix.merge_topk(sharded._all_gather(ids), sharded._all_gather(dists))
-            return out, (r[2] if stats else None)
         return (ids, dists), (r[2] if stats else None)
 
     # ---- nprobe sweep: the metric is QPS at recall@10 = 0.95
@@ -239,10 +252,12 @@ def run_dade(args):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _, st = step(chosen, stats=True)
+            _, st = step(chosen, stats=(world == 1))
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+            if world > 1:
+                st = shard_stats(chosen)  # untimed
             scan_ms.append(st["ms_scan"])
             stats_acc = st
     total_ms = sum(times)
@@ -264,8 +279,13 @@ def run_dade(args):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if args.method == "bsa_p":
+        if args.method == "bsa_p" and world == 1:
             ix.search_host(Qh, K, chosen, dd, ALPHA, ids=ih, dists=dh)
+        elif world > 1:  # H2D, the query-partitioned multi-GPU search (NCCL inside), D2H
+            Qtmp.copy_(Qh, non_blocking=True)
+            oi, od = qpart.search(Qtmp, K, chosen, dd, args.method, METHOD_PARAM[args.method])
+            ih.copy_(oi, non_blocking=True)
+            dh.copy_(od, non_blocking=True)
         else:  # H2D of the queries, search, D2H of the results, all on the library's stream
             Qtmp.copy_(Qh, non_blocking=True)
             ix.search_method(Qtmp, K, chosen, dd, args.method, METHOD_PARAM[args.method], ids=ids, dists=dists)

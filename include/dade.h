@@ -165,6 +165,17 @@ dade_status dade_search(dade_index* idx, const float* Q, int nq, int K, int npro
 dade_status dade_search_method(dade_index* idx, const float* Q, int nq, int K, int nprobe, int delta_d,
                                int method, double param, int64_t* ids, float* dists, dade_stats* stats);
 
+/* Split search (multi-GPU query partitioning): dade_prepare runs a4 + a5 for a block
+ * of queries — qrot (device nq x D fp32, q~ = R(q - mu)) and probes (device nq x nprobe int32,
+ * exact, ordered by (dist, id)); dade_search_prepared runs a6-a8 on this index's shard for
+ * queries prepared anywhere (e.g. on another rank with the same replicated mu, R, centroids,
+ * then all-gathered). Results are identical to dade_search / dade_search_method on the same
+ * queries. Errors: as dade_search. */
+dade_status dade_prepare(dade_index* idx, const float* Q, int nq, int nprobe, float* qrot, int32_t* probes);
+dade_status dade_search_prepared(dade_index* idx, const float* qrot, const int32_t* probes, int nq, int K,
+                                 int nprobe, int delta_d, int method, double param, int64_t* ids,
+                                 float* dists, dade_stats* stats);
+
 /* Same as dade_search with HOST Q/ids/dists: the H2D copy of Q and the D2H copy of the results
  * are part of the call (synchronous). Used for the end-to-end (e2e) measurement. */
 dade_status dade_search_host(dade_index* idx, const float* Q_host, int nq, int K, int nprobe,

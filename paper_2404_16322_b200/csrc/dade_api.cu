@@ -293,12 +293,48 @@ __global__ void k_ids_from_idx(const int32_t* idx, const double* d64, int64_t cn
   }
 }
 
+// a4 + a5: q~ = R(q - mu) (side stream) and the exact probes (main stream), joined on the main
+// stream. qrot: device nq x D, probes: device nq x nprobe.
+void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int32_t* probes, bool stats) {
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  // non-finite queries latch error 3 in the flag (reported at the next synchronising call)
+  if (!x->flag.p) {
+    x->flag.reserve(1);
+    DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), st));
+  }
+  if (!x->side) {
+    DADE_CK(cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking));
+    DADE_CK(cudaEventCreateWithFlags(&x->fork, cudaEventDisableTiming));
+    DADE_CK(cudaEventCreateWithFlags(&x->join, cudaEventDisableTiming));
+  }
+  DADE_CK(cudaEventRecord(x->fork, st));
+  DADE_CK(cudaStreamWaitEvent(x->side, x->fork, 0));
+  launch_check_finite(Q, (int64_t)nq * D, x->flag.p, x->side, 3);
+  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, qrot, nullptr, x->side);
+  if (stats) DADE_CK(cudaEventRecord(x->ev[1], x->side));
+  DADE_CK(cudaEventRecord(x->join, x->side));
+  if (x->nlist == 1) {
+    DADE_CK(cudaMemsetAsync(probes, 0, sizeof(int32_t) * nq, st));
+  } else {
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, false, probe_passes());
+  }
+  DADE_CK(cudaStreamWaitEvent(st, x->join, 0));
+}
+
+// qrot_in / probes_in (device, optional): queries already rotated and probed (dade_prepare, e.g.
+// on another rank) — only the scan runs.
 void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d, double alpha,
-               int64_t* ids, float* dists, dade_stats* stats, int method = DADE_METHOD_BSA_P) {
+               int64_t* ids, float* dists, dade_stats* stats, int method = DADE_METHOD_BSA_P,
+               const float* qrot_in = nullptr, const int32_t* probes_in = nullptr) {
   const int D = x->D;
   DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
   DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
-  if (nq > 0) { need(Q, "Q"); need(ids, "ids"); need(dists, "dists"); }
+  if (nq > 0) {
+    if (!qrot_in) need(Q, "Q");
+    else need(probes_in, "probes");
+    need(ids, "ids"); need(dists, "dists");
+  }
   DADE_REQUIRE(K >= 1, DADE_ERR_ARG, "K < 1");
   DADE_REQUIRE(K <= DADE_MAX_K, DADE_ERR_UNSUPPORTED, "K > DADE_MAX_K");
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
@@ -329,37 +365,21 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
       if (!e) DADE_CK(cudaEventCreate(&e));
     DADE_CK(cudaEventRecord(x->ev[0], st));
   }
-  // non-finite queries latch error 3 in the flag (reported at the next synchronising call)
-  if (!x->flag.p) {
-    x->flag.reserve(1);
-    DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), st));
+  const float* qrot = qrot_in;
+  const int32_t* probes = probes_in;
+  if (!qrot_in) {
+    x->qrot.reserve((size_t)nq * D);
+    x->probes.reserve((size_t)nq * nprobe);
+    prepare(x, Q, nq, nprobe, x->qrot.p, x->probes.p, stats != nullptr);
+    qrot = x->qrot.p;
+    probes = x->probes.p;
+  } else if (stats) {
+    DADE_CK(cudaEventRecord(x->ev[1], st));
   }
-  // a4 rotate queries (fp64 accumulation) on the side stream, concurrently with the a5 probe
-  // (the probe reads the raw queries); both join before the scan
-  if (!x->side) {
-    DADE_CK(cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking));
-    DADE_CK(cudaEventCreateWithFlags(&x->fork, cudaEventDisableTiming));
-    DADE_CK(cudaEventCreateWithFlags(&x->join, cudaEventDisableTiming));
-  }
-  DADE_CK(cudaEventRecord(x->fork, st));
-  DADE_CK(cudaStreamWaitEvent(x->side, x->fork, 0));
-  launch_check_finite(Q, (int64_t)nq * D, x->flag.p, x->side, 3);
-  x->qrot.reserve((size_t)nq * D);
-  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, x->side);
-  if (stats) DADE_CK(cudaEventRecord(x->ev[1], x->side));
-  DADE_CK(cudaEventRecord(x->join, x->side));
-  // a5 exact probes
-  x->probes.reserve((size_t)nq * nprobe);
-  if (x->nlist == 1) {
-    DADE_CK(cudaMemsetAsync(x->probes.p, 0, sizeof(int32_t) * nq, st));
-  } else {
-    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, x->probes.p, nullptr, x->cent_tc, false, probe_passes());
-  }
-  DADE_CK(cudaStreamWaitEvent(st, x->join, 0));
   if (stats) DADE_CK(cudaEventRecord(x->ev[2], st));
   // step table (R4, R5): alpha_s = alpha*delta_d/D, k = clamp(ceil((1-alpha_s)*n0), 1, n0)
   ScanParams p{};
-  p.qrot = x->qrot.p; p.probes = x->probes.p; p.off = x->off_d.p; p.row_id = x->row_id_d.p;
+  p.qrot = qrot; p.probes = probes; p.off = x->off_d.p; p.row_id = x->row_id_d.p;
   p.layout = x->layout.p; p.n = x->n; p.D = D; p.nq = nq; p.nprobe = nprobe; p.K = K;
   // alpha = 0 (or a single step): nothing can be pruned; the kernel then runs with 16-dim
   // steps (no classifier fires: m1 = 1, beta' = -inf), which serves every delta_d | D.
@@ -399,7 +419,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     x->lam_d.reserve(D);
     DADE_CK(cudaMemcpyAsync(x->lam_d.p, x->lam.data(), sizeof(double) * D, cudaMemcpyHostToDevice, st));
     x->qconst.reserve((size_t)nq * (nsteps - 1) + 1);
-    launch_res_consts(x->qrot.p, nq, D, delta_d, x->lam_d.p, alpha, x->qconst.p, st);
+    launch_res_consts(qrot, nq, D, delta_d, x->lam_d.p, alpha, x->qconst.p, st);
     p.residual = 1;
     p.xnorm = x->xnorm.p;
     p.qconst = x->qconst.p;
@@ -922,6 +942,31 @@ extern "C" dade_status dade_search_method(dade_index* x, const float* Q, int nq,
   need(x, "index");
   DeviceGuard g(x->device);
   do_search(x, Q, nq, K, nprobe, delta_d, param, ids, dists, stats, method);
+  API_END
+}
+
+extern "C" dade_status dade_prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot,
+                                    int32_t* probes) {
+  API_BEGIN
+  need(x, "index");
+  DeviceGuard g(x->device);
+  DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "prepare before build_ivf");
+  DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
+  DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
+  if (nq == 0) { g_err.clear(); return DADE_OK; }
+  need(Q, "Q"); need(qrot, "qrot"); need(probes, "probes");
+  prepare(x, Q, nq, nprobe, qrot, probes, false);
+  API_END
+}
+
+extern "C" dade_status dade_search_prepared(dade_index* x, const float* qrot, const int32_t* probes, int nq,
+                                            int K, int nprobe, int delta_d, int method, double param,
+                                            int64_t* ids, float* dists, dade_stats* stats) {
+  API_BEGIN
+  need(x, "index");
+  DeviceGuard g(x->device);
+  if (nq > 0) need(qrot, "qrot");
+  do_search(x, nullptr, nq, K, nprobe, delta_d, param, ids, dists, stats, method, qrot, probes);
   API_END
 }
 

@@ -61,6 +61,8 @@ _SIGS = {
     "dade_search": [P, P, I32, I32, I32, I32, DBL, P, P, P],
     "dade_search_host": [P, P, I32, I32, I32, I32, DBL, P, P, P],
     "dade_search_method": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
+    "dade_prepare": [P, P, I32, I32, P, P],
+    "dade_search_prepared": [P, P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
     "dade_probe": [P, P, I32, I32, P],
     "dade_bruteforce_knn": [P, P, I64, I64, P, I32, I32, P, P],
     "dade_merge_topk": [P, P, P, I32, I32, I32, P, P],
@@ -241,6 +243,33 @@ class Index:
         st = Stats() if stats else None
         _ck(lib().dade_search_method(self.h, _ptr(Q), nq, K, nprobe, delta_d, self.METHODS[method], float(param),
                                      _ptr(ids), _ptr(dists), C.byref(st) if st is not None else None))
+        return (ids, dists, st.as_dict()) if stats else (ids, dists)
+
+    def prepare(self, Q, nprobe: int):
+        """a4 + a5 only: (q~ = R(q - mu) [nq, D] fp32, probes [nq, nprobe] int32) on the device."""
+        import torch
+        Q = _dev(Q, torch.float32)
+        nq = Q.shape[0]
+        qrot = torch.empty((nq, self.D), dtype=torch.float32, device=Q.device)
+        probes = torch.empty((nq, nprobe), dtype=torch.int32, device=Q.device)
+        _ck(lib().dade_prepare(self.h, _ptr(Q), nq, nprobe, _ptr(qrot), _ptr(probes)))
+        return qrot, probes
+
+    def search_prepared(self, qrot, probes, K: int, delta_d: int, method: str, param: float, ids=None,
+                        dists=None, stats: bool = False):
+        """a6-a8 on this shard for prepared queries (see prepare)."""
+        import torch
+        qrot = _dev(qrot, torch.float32)
+        probes = _dev(probes, torch.int32)
+        nq, nprobe = probes.shape
+        if ids is None:
+            ids = torch.empty((nq, K), dtype=torch.int64, device=qrot.device)
+        if dists is None:
+            dists = torch.empty((nq, K), dtype=torch.float32, device=qrot.device)
+        st = Stats() if stats else None
+        _ck(lib().dade_search_prepared(self.h, _ptr(qrot), _ptr(probes), nq, K, nprobe, delta_d,
+                                       self.METHODS[method], float(param), _ptr(ids), _ptr(dists),
+                                       C.byref(st) if st is not None else None))
         return (ids, dists, st.as_dict()) if stats else (ids, dists)
 
     def search_host(self, Q, K: int, nprobe: int, delta_d: int, significance: float, ids=None, dists=None,

@@ -61,3 +61,38 @@ class ShardedSearch:
         g_ids = _all_gather(ids, self.group)
         g_d = _all_gather(dists, self.group)
         return self.engine.merge_topk(g_ids, g_d)
+
+
+def _gather_rows(t, rows_per_rank: int, nq: int, group=None):
+    """All-gather equal-size row blocks (padded to rows_per_rank) and return the first nq rows in
+    rank order (rank r prepared queries [r*rows_per_rank, (r+1)*rows_per_rank))."""
+    import torch
+    pad = rows_per_rank - t.shape[0]
+    if pad:
+        t = torch.cat([t, torch.zeros((pad,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)])
+    g = _all_gather(t, group)
+    return g.reshape((-1,) + tuple(t.shape[1:]))[:nq].contiguous()
+
+
+class QueryPartitionedSearch:
+    """Multi-GPU search that also splits the per-query fixed costs: rank r rotates
+    and probes only its block of queries (a4 + a5, `engine.prepare`), the blocks are all-gathered
+    (q~ and probe lists, ~D*4 + nprobe*4 bytes per query), every rank scans ALL queries on its own
+    shard (a6-a8, `engine.search_prepared`), and the local top-K lists are all-gathered and merged
+    (a9). μ, R and the centroids are replicated, so any rank's prepared queries are valid on every
+    shard and the result equals ShardedSearch's."""
+
+    def __init__(self, engine, group=None):
+        self.engine, self.group = engine, group
+
+    def search(self, Q, K: int, nprobe: int, delta_d: int, method: str = "bsa_p", param: float = 0.005):
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        nq = Q.shape[0]
+        per = (nq + world - 1) // world
+        lo, hi = min(rank * per, nq), min((rank + 1) * per, nq)
+        qrot, probes = self.engine.prepare(Q[lo:hi].contiguous(), nprobe)
+        qrot = _gather_rows(qrot, per, nq, self.group)
+        probes = _gather_rows(probes, per, nq, self.group)
+        ids, dists = self.engine.search_prepared(qrot, probes, K, delta_d, method, param)[:2]
+        return self.engine.merge_topk(_all_gather(ids, self.group), _all_gather(dists, self.group))

@@ -192,3 +192,23 @@ def test_nonfinite_query_reported(sift_small):
     with pytest.raises(DadeError):
         ix.search(Q, 10, 4, 16, 0.005, stats=True)   # a synchronising call reports it
     ix.search(Q[:1].contiguous(), 10, 4, 16, 0.005, stats=True)  # the latch is cleared
+
+
+def test_prepare_then_search_prepared_equals_search(sift_small):
+    # the split used by the query-partitioned multi-GPU path: a4 + a5 (prepare) and a6-a8
+    # (search_prepared) give bit-identical results to one dade_search, for every method; queries
+    # prepared in blocks (as ranks would) and concatenated give the same too
+    cfg, (torch, ix, oidx, X, Xd) = sift_small
+    Q = torch.from_numpy(synth.queries(cfg)[:30]).cuda()
+    qrot, probes = ix.prepare(Q, 8)
+    a, b = ix.search(Q, 10, 8, 16, 0.005)
+    c, d = ix.search_prepared(qrot, probes, 10, 16, "bsa_p", 0.005)
+    assert torch.equal(a, c) and torch.equal(b, d)
+    parts = [ix.prepare(Q[i:i + 7].contiguous(), 8) for i in range(0, 30, 7)]
+    qr2 = torch.cat([p[0] for p in parts]); pr2 = torch.cat([p[1] for p in parts])
+    assert torch.equal(qr2, qrot) and torch.equal(pr2, probes)
+    e, f = ix.search_method(Q, 10, 8, 16, "bsa_res", 8.0)
+    g, h = ix.search_prepared(qrot, probes, 10, 16, "bsa_res", 8.0)
+    assert torch.equal(e, g) and torch.equal(f, h)
+    z = ix.prepare(Q[:0].contiguous(), 8)                      # an empty block (more ranks than queries)
+    assert z[0].shape == (0, cfg.d) and z[1].shape == (0, 8)

@@ -42,6 +42,21 @@ class OracleEngine:
         i, d, _ = O.search(self.idx, Q.numpy(), K, nprobe, dd, alpha)
         return torch.from_numpy(i), torch.from_numpy(d)
 
+    # split search: "q~" here is the raw query (the oracle rotates inside search); the probes the
+    # ranks computed must be the ones this shard's own search would use
+    def prepare(self, Q, nprobe):
+        Qn = Q.numpy()
+        pr = np.stack([O.probe(q, self.idx["centroids"], nprobe) for q in Qn]) if len(Qn) else \
+            np.zeros((0, nprobe), np.int64)
+        return torch.from_numpy(Qn.copy()), torch.from_numpy(pr.astype(np.int32))
+
+    def search_prepared(self, qrot, probes, K, dd, method, param):
+        Qn = qrot.numpy()
+        for q in range(len(Qn)):
+            assert probes[q].tolist() == O.probe(Qn[q], self.idx["centroids"], probes.shape[1]).tolist()
+        i, d, _ = O.search(self.idx, Qn, K, probes.shape[1], dd, param if method == "bsa_p" else 0.0)
+        return torch.from_numpy(i), torch.from_numpy(d)
+
     def merge_topk(self, g_ids, g_d):
         i, d = O.merge_shards([(g_ids[s].numpy(), g_d[s].numpy()) for s in range(g_ids.shape[0])],
                               g_ids.shape[2])
@@ -78,6 +93,11 @@ def _worker(rank, world, port, q):
         full = O.build_index(X, cent, mean, R)
         ei, ed = O.exact_ivf(full, X, Q, 10, 5)
         assert np.array_equal(ids.numpy(), ei), "sharded merge differs from unsharded exact IVF"
+        # query-partitioned split search (each rank prepares a block of queries; 12 queries over
+        # 2 ranks, and 11 so that the last block is ragged) == the same exact IVF
+        for nq in (12, 11):
+            ids, d = sharded.QueryPartitionedSearch(eng).search(torch.from_numpy(Q[:nq]), 10, 5, 16, "bsa_p", 0.0)
+            assert np.array_equal(ids.numpy(), ei[:nq]), "query-partitioned search differs"
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e)))
