@@ -170,7 +170,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   // select (> 1024 groups; measured at 16,384 columns: d_hat path 0.31 ms, fused 0.61 ms);
   // DADE_FUSED_PROBE=0/1 forces either path (tests cover both)
   const char* fz = getenv("DADE_FUSED_PROBE");
-  const bool fused = k <= 64 && n >= 256 && (fz ? atoi(fz) != 0 : (n + 31) / 32 > 1024);
+  const bool fused = k <= 64 && n >= 256 && (fz ? atoi(fz) != 0 : (n + 63) / 64 > 1024);
   if (fused) {
     // fused filter GEMM + candidate tracking (probe_tc.cu): no m x n d_hat matrix
     static int sms = 0;
@@ -223,7 +223,10 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   chunk = std::min<int64_t>(chunk, tc_rows_pad(m));
   x->dmat.reserve((size_t)chunk * n);
   x->slack.reserve((size_t)chunk);
-  x->gmin.reserve((size_t)chunk * ((n + 31) / 32));
+  // group minima over 32 columns (64 beyond 32,768 columns, so a row has <= 1024 groups)
+  const int gshift = (n + 31) / 32 > 1024 ? 6 : 5;
+  const int64_t ngrp = (n + (1 << gshift) - 1) >> gshift;
+  x->gmin.reserve((size_t)chunk * ngrp);
   if (!x->flag.p) {
     x->flag.reserve(1);
     DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
@@ -231,13 +234,13 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t mm = std::min(chunk, m - r0);
     tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
-    const bool use_gmin = k > 1 && k <= (n + 31) / 32 && (n + 31) / 32 <= 1024;
+    const bool use_gmin = k > 1 && k <= ngrp && ngrp <= 1024;
     launch_l2_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
-                 x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr, passes);
+                 x->dmat.p, n, x->stream, use_gmin ? x->gmin.p : nullptr, passes, gshift);
     launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream, passes);
     if (use_gmin) {
       x->ovf.reserve((size_t)chunk + 1);
-      launch_select_gmin(x->dmat.p, x->gmin.p, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
+      launch_select_gmin(x->dmat.p, x->gmin.p, gshift, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
                          out_d64 ? out_d64 + r0 * k : nullptr, x->flag.p, x->slack.p, x->ovf.p,
                          x->ovf.p + 1, x->stream);
       continue;

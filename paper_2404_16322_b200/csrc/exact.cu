@@ -369,9 +369,9 @@ __device__ __forceinline__ bool cand_less2(double d0, int32_t c0, double d1, int
   return d0 < d1 || (d0 == d1 && c0 < c1);
 }
 
-template <int GPL>  // group minima per lane: rows of up to 32 * GPL groups (32 * 32 * GPL columns)
+template <int GPL>  // group minima per lane: rows of up to 32 * GPL groups of 2^gshift columns
 __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
-    const float* __restrict__ dh, const float* __restrict__ gm, int64_t m, int64_t n, int k,
+    const float* __restrict__ dh, const float* __restrict__ gm, int gshift, int64_t m, int64_t n, int k,
     const float* __restrict__ A, const float* __restrict__ B, int D, int32_t* __restrict__ out_idx,
     double* __restrict__ out_d, int* ovf_n, int32_t* __restrict__ ovf_rows, const float* __restrict__ slack) {
   __shared__ float sg[kGmWarps][32 * GPL];
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * kGmWarps + w;
   if (row >= m) return;
-  const int ng = (int)((n + 31) / 32);
+  const int ng = (int)((n + (1 << gshift) - 1) >> gshift);
   // the k-th smallest group minimum E bounds the k-th smallest d_hat from above
   float gv[GPL];  // group lane + 32 j
 #pragma unroll
@@ -439,14 +439,16 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
     while (gb) {
       const int grp = 32 * j + __ffs(gb) - 1;
       gb &= gb - 1;
-      const int64_t c = (int64_t)grp * 32 + lane;
-      const bool in = c < n && __float_as_uint(d[c]) <= tb;
-      const unsigned bal = __ballot_sync(0xffffffffu, in);
-      if (in) {
-        const int pos = cnt + __popc(bal & ((1u << lane) - 1));
-        if (pos < kGmCap) cc[w][pos] = (int32_t)c;
+      for (int h = 0; h < (1 << gshift); h += 32) {
+        const int64_t c = ((int64_t)grp << gshift) + h + lane;
+        const bool in = c < n && __float_as_uint(d[c]) <= tb;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+          if (pos < kGmCap) cc[w][pos] = (int32_t)c;
+        }
+        cnt += __popc(bal);
       }
-      cnt += __popc(bal);
     }
   }
   if (cnt > kGmCap) {  // too many near-ties: the histogram select redoes this row
@@ -616,20 +618,20 @@ void launch_select_groups(const float* gmin, int64_t m, int64_t n, int k, const 
   DADE_CK(cudaGetLastError());
 }
 
-void launch_select_gmin(const float* d_hat, const float* gmin, int64_t m, int64_t n, int k,
+void launch_select_gmin(const float* d_hat, const float* gmin, int gshift, int64_t m, int64_t n, int k,
                         const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,
                         int* d_flag, const float* slack, int* ovf_n, int32_t* ovf_rows,
                         cudaStream_t st) {
   if (m <= 0) return;
   DADE_CK(cudaMemsetAsync(ovf_n, 0, sizeof(int), st));
-  const int64_t ngr = (n + 31) / 32;
+  const int64_t ngr = (n + (1 << gshift) - 1) >> gshift;
   const unsigned gsz = (unsigned)((m + kGmWarps - 1) / kGmWarps);
   if (ngr <= 256)
-    k_select_gmin<8><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+    k_select_gmin<8><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
   else if (ngr <= 512)
-    k_select_gmin<16><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+    k_select_gmin<16><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
   else
-    k_select_gmin<32><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+    k_select_gmin<32><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
   DADE_CK(cudaGetLastError());
   // device-side fallback (no host round trip): a small grid walks the listed rows
   const unsigned fg = (unsigned)std::min<int64_t>(m, 296);

@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
                                                   const float* __restrict__ an, const float* __restrict__ Bhi,
                                                   const float* __restrict__ Blo, const float* __restrict__ bn,
                                                   int nkc, float* __restrict__ out, int64_t m, int64_t n,
-                                                  int64_t ldo, float* __restrict__ gmin, int64_t ldg, int passes) {
+                                                  int64_t ldo, float* __restrict__ gmin, int64_t ldg, int passes,
+                                                  int gshift) {
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * kStageBytes);
   uint64_t* empty = full + 2;
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   // the operand stages are free once every MMA completed: each warp transposes its 32 x 32
   // d_hat chunk through shared memory so the global stores are row-contiguous (128 B per row)
   float* stg = reinterpret_cast<float*>(sm) + warp * 32 * 33;
+  float gmn = INFINITY;  // 64-column groups: minimum of the group's first chunk
 #pragma unroll 1
   for (int cb = 0; cb < kTM / 32; ++cb) {
     uint32_t r[32];
@@ -230,11 +232,15 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
       for (int j = 0; j < 32; ++j)
         d[j] = c0 + j < n ? fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j])) : INFINITY;
     }
-    if (gmin && row < m && c0 < n) {  // per-row minimum of this 32-column group (select hint)
+    if (gmin && row < m && c0 < n) {  // per-row minimum of this 2^gshift-column group (select hint)
       float mn = d[0];
 #pragma unroll
       for (int j = 1; j < 32; ++j) mn = fminf(mn, d[j]);
-      gmin[row * ldg + (c0 >> 5)] = mn;
+      if (gshift == 6) {  // 64-column groups: two chunks per group
+        if ((cb & 1) == 0) gmn = mn;
+        mn = fminf(mn, gmn);
+      }
+      if (gshift == 5 || (cb & 1) == 1 || c0 + 32 >= n) gmin[row * ldg + (c0 >> gshift)] = mn;
     }
     if (!out) continue;  // group minima only (k_select_groups)
     if (full && (ldo & 3) == 0) {
@@ -304,7 +310,7 @@ void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, c
 
 void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
-                  cudaStream_t st, float* gmin, int passes) {
+                  cudaStream_t st, float* gmin, int passes, int gshift) {
   if (m <= 0 || n <= 0) return;
   static bool attr = false;
   const size_t smem = 2 * kStageBytes + 64;
@@ -314,7 +320,7 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
   }
   dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
   k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), out, m, n, ldo, gmin,
-                                   (n + 31) / 32, passes);
+                                   (n + (1 << gshift) - 1) >> gshift, passes, gshift);
   DADE_CK(cudaGetLastError());
 }
 

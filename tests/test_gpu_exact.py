@@ -84,7 +84,7 @@ def test_probe_and_assign_bit_exact(torch_cuda, probe_passes):
 
 
 @pytest.mark.parametrize("nprobe", [1, 7, 64])
-@pytest.mark.parametrize("C", [3000, 20000])
+@pytest.mark.parametrize("C", [3000, 20000, 40000])
 def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe, C, probe_passes):
     # several column tiles per split and a ragged last tile (3000 = 23 x 128 + 56; 20000 = 625
     # 32-column groups), integer data with exact distance ties; both selection paths must return

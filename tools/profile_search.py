@@ -18,12 +18,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--nprobe", type=int, default=8)
 ap.add_argument("--alpha", type=float, default=0.005)
+ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--nlist", type=int, default=0)
 ap.add_argument("--env", default="", help="NAME=VALUE set just before the profiled search")
 a = ap.parse_args()
 build.build()
 cfg = synth.config(a.config)
+if a.n:
+    cfg = cfg.scaled(n=a.n, nlist=a.nlist or max(1, a.n // 244))
 m = synth.model(cfg)
-X = torch.from_numpy(synth.base(cfg, m)).cuda()
+X = torch.from_numpy(synth.base(cfg, m, workers=min(16, os.cpu_count() or 1))).cuda()
 Q = torch.from_numpy(synth.queries(cfg, m=m)).cuda()
 Qc = torch.from_numpy(synth.cal_queries(cfg, m=m)).cuda()
 ix = Index(cfg.d)
