@@ -138,15 +138,18 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
                                                   int64_t ldo, float* __restrict__ gmin, int64_t ldg, int passes,
                                                   int gshift) {
   extern __shared__ __align__(1024) unsigned char sm[];
+  // 64 KB of operand stages: 2 x 32 KB (3-pass: A_hi, A_lo, B_hi, B_lo) or 4 x 16 KB (1-pass:
+  // A_hi, B_hi) — the 1-pass filter keeps four chunks in flight
+  const int S = passes == 1 ? 4 : 2;
+  const int SB = passes == 1 ? kStageBytes / 2 : kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * kStageBytes);
-  uint64_t* empty = full + 2;
-  uint64_t* accf = full + 4;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(full + 5);
+  uint64_t* empty = full + 4;
+  uint64_t* accf = full + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(full + 9);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t tm = blockIdx.y, tn = blockIdx.x;
   if (tid == 0) {
-    mbar_init(&full[0], 1); mbar_init(&full[1], 1);
-    mbar_init(&empty[0], 1); mbar_init(&empty[1], 1);
+    for (int i = 0; i < 4; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -162,41 +165,42 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   if (tid == 0) {
     // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
-    auto load = [&](int kc) {  // passes == 1: the hi parts only
-      const int s = kc & 1;
-      unsigned char* st = sm + s * kStageBytes;
-      mbar_expect_tx(&full[s], passes == 1 ? kStageBytes / 2 : kStageBytes);
+    // stage layout: A_hi | B_hi (1-pass) or A_hi | A_lo | B_hi | B_lo (3-pass)
+    const int offB = passes == 1 ? kSub * 4 : 2 * kSub * 4;
+    auto load = [&](int kc) {
+      const int s = kc % S;
+      unsigned char* st = sm + s * SB;
+      mbar_expect_tx(&full[s], SB);
       const int64_t ao = (tm * nkc + kc) * kSub, bo = (tn * nkc + kc) * kSub;
       bulk_g2s(st, Ahi + ao, kSub * 4, &full[s]);
-      bulk_g2s(st + 2 * kSub * 4, Bhi + bo, kSub * 4, &full[s]);
+      bulk_g2s(st + offB, Bhi + bo, kSub * 4, &full[s]);
       if (passes != 1) {
         bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
         bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
       }
     };
-    load(0);
-    if (nkc > 1) load(1);
+    for (int kc = 0; kc < S && kc < nkc; ++kc) load(kc);
     for (int kc = 0; kc < nkc; ++kc) {
-      const int s = kc & 1;
-      mbar_wait(&full[s], (kc >> 1) & 1);
+      const int s = kc % S;
+      mbar_wait(&full[s], (kc / S) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      unsigned char* st = sm + s * kStageBytes;
+      unsigned char* st = sm + s * SB;
 #pragma unroll
       for (int j = 0; j < kKC / 8; ++j) {  // UMMA_K = 8 for tf32 (32 B of K)
         const uint64_t ah = umma_desc(st + j * 256, 128, kSBO);
-        const uint64_t al = umma_desc(st + kSub * 4 + j * 256, 128, kSBO);
-        const uint64_t bh = umma_desc(st + 2 * kSub * 4 + j * 256, 128, kSBO);
-        const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
+        const uint64_t bh = umma_desc(st + offB + j * 256, 128, kSBO);
         mma_tf32(tmem, ah, bh, idesc, (kc | j) != 0);
         if (passes != 1) {
+          const uint64_t al = umma_desc(st + kSub * 4 + j * 256, 128, kSBO);
+          const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
           mma_tf32(tmem, ah, bl, idesc, 1);
           mma_tf32(tmem, al, bh, idesc, 1);
         }
       }
       mma_commit(&empty[s]);
-      if (kc + 2 < nkc) {
-        mbar_wait(&empty[s], (kc >> 1) & 1);  // MMAs reading this stage are done
-        load(kc + 2);
+      if (kc + S < nkc) {
+        mbar_wait(&empty[s], (kc / S) & 1);  // MMAs reading this stage are done
+        load(kc + S);
       }
     }
     mma_commit(accf);
@@ -313,7 +317,7 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
                   cudaStream_t st, float* gmin, int passes, int gshift) {
   if (m <= 0 || n <= 0) return;
   static bool attr = false;
-  const size_t smem = 2 * kStageBytes + 64;
+  const size_t smem = 2 * kStageBytes + 128;
   if (!attr) {
     DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
