@@ -209,7 +209,7 @@ struct RegTopK {
 // entries are queued; with an async round in flight stage 1 may run up to 64 queued (+32 + 32).
 template <int DD, bool ASY>
 struct Slice {
-  static constexpr int kStages = DD == 1 ? 3 : 2;
+  static constexpr int kStages = (DD == 1 && !ASY) ? 3 : 2;  // ASY: the staging buffer replaces a stage
   static constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
   static constexpr int QCAP = ASY ? 128 : 64;
   static constexpr size_t stage_bytes = ASY ? 32 * 64 + 32 * 4 : 0;  // async gather round: rows + ids
