@@ -244,6 +244,12 @@ def run_dade(args):
         step(chosen)
     torch.cuda.synchronize()
     times, scan_ms, stats_acc = [], [], None
+    # the timed steps are plain asynchronous searches (as a user calls them); the library records
+    # stage events inside them (dade_set_timing, no synchronisation) and the k_scan duration for
+    # the roofline is read from those events after each step; the counters (deterministic) come
+    # from one untimed stats call
+    ix.set_timing(True)
+    stats_acc = step(chosen, stats=True)[1] if world == 1 else shard_stats(chosen)
     with Clocks(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)
@@ -252,14 +258,14 @@ def run_dade(args):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _, st = step(chosen, stats=(world == 1))
+            step(chosen)
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-            if world > 1:
-                st = shard_stats(chosen)  # untimed
-            scan_ms.append(st["ms_scan"])
-            stats_acc = st
+            tm = ix.get_timing()
+            scan_ms.append(tm["scan"])
+            stage_last = tm
+    ix.set_timing(False)
     total_ms = sum(times)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -335,8 +341,8 @@ def run_dade(args):
                        "l2": "flushed between timed steps (256 MB write, untimed)",
                        "scan_rate": round(st["dims_scanned"] / (st["tested"] * cfg.d), 4),
                        "tested_per_query": st["tested"] / cfg.nq, "n_epochs": st["n_epochs"],
-                       "stage_ms": {"rotate": round(st["ms_rotate"], 4), "probe": round(st["ms_probe"], 4),
-                                    "scan": round(st["ms_scan"], 4)}},
+                       "stage_ms": {"rotate": round(stage_last["rotate"], 4), "probe": round(stage_last["probe"], 4),
+                                    "scan": round(stage_last["scan"], 4)}},
             "e2e": {"value": round(e2e_value, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": cfg.nq * cfg.d * 4, "d2h_bytes_per_step": cfg.nq * K * 12},
             "gpu_launches": args.steps * launches_per_search(cfg, world, chosen),

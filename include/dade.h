@@ -165,6 +165,13 @@ dade_status dade_search(dade_index* idx, const float* Q, int nq, int K, int npro
 dade_status dade_search_method(dade_index* idx, const float* Q, int nq, int K, int nprobe, int delta_d,
                                int method, double param, int64_t* ids, float* dists, dade_stats* stats);
 
+/* Stage timing without synchronisation: with timing on, every search records CUDA events around
+ * a4 (rotation), a5 (probe) and a6-a8 (scan) on the index's stream(s); dade_get_timing waits for
+ * the last search's events and returns ms3 = {rotate, probe (both from the search start, they
+ * run concurrently), scan} in milliseconds. Errors: STATE (no search recorded), CUDA. */
+dade_status dade_set_timing(dade_index* idx, int on);
+dade_status dade_get_timing(dade_index* idx, float* ms3);
+
 /* Split search (multi-GPU query partitioning): dade_prepare runs a4 + a5 for a block
  * of queries — qrot (device nq x D fp32, q~ = R(q - mu)) and probes (device nq x nprobe int32,
  * exact, ordered by (dist, id)); dade_search_prepared runs a6-a8 on this index's shard for

@@ -58,6 +58,7 @@ struct dade_index {
   DBuf<double> lam_d;
   bool xnorm_ok = false;
   cudaEvent_t ev[5] = {};
+  bool timing = false;  // record the stage events on every search (dade_set_timing)
   // a4 (rotation) runs on a side stream concurrently with a5 (probe): fork/join events
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -363,7 +364,8 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   }
   if (nq == 0) return;
   cudaStream_t st = x->stream;
-  if (stats) {
+  const bool evs = stats || x->timing;  // stage events (no synchronisation unless stats)
+  if (evs) {
     for (auto& e : x->ev)
       if (!e) DADE_CK(cudaEventCreate(&e));
     DADE_CK(cudaEventRecord(x->ev[0], st));
@@ -373,13 +375,13 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   if (!qrot_in) {
     x->qrot.reserve((size_t)nq * D);
     x->probes.reserve((size_t)nq * nprobe);
-    prepare(x, Q, nq, nprobe, x->qrot.p, x->probes.p, stats != nullptr);
+    prepare(x, Q, nq, nprobe, x->qrot.p, x->probes.p, evs);
     qrot = x->qrot.p;
     probes = x->probes.p;
-  } else if (stats) {
+  } else if (evs) {
     DADE_CK(cudaEventRecord(x->ev[1], st));
   }
-  if (stats) DADE_CK(cudaEventRecord(x->ev[2], st));
+  if (evs) DADE_CK(cudaEventRecord(x->ev[2], st));
   // step table (R4, R5): alpha_s = alpha*delta_d/D, k = clamp(ceil((1-alpha_s)*n0), 1, n0)
   ScanParams p{};
   p.qrot = qrot; p.probes = probes; p.off = x->off_d.p; p.row_id = x->row_id_d.p;
@@ -431,6 +433,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   DADE_CK(cudaMemsetAsync(x->work.p, 0, sizeof(int), st));
   p.work_counter = x->work.p;
   launch_scan(p, st);
+  if (evs && !stats) DADE_CK(cudaEventRecord(x->ev[3], st));
   if (stats) {
     DADE_CK(cudaEventRecord(x->ev[3], st));
     unsigned long long c[4 + DADE_MAX_STEPS + 8];
@@ -945,6 +948,25 @@ extern "C" dade_status dade_search_method(dade_index* x, const float* Q, int nq,
   need(x, "index");
   DeviceGuard g(x->device);
   do_search(x, Q, nq, K, nprobe, delta_d, param, ids, dists, stats, method);
+  API_END
+}
+
+extern "C" dade_status dade_set_timing(dade_index* x, int on) {
+  API_BEGIN
+  need(x, "index");
+  x->timing = on != 0;
+  API_END
+}
+
+extern "C" dade_status dade_get_timing(dade_index* x, float* ms3) {
+  API_BEGIN
+  need(x, "index"); need(ms3, "ms3");
+  DeviceGuard g(x->device);
+  DADE_REQUIRE(x->ev[3] != nullptr, DADE_ERR_STATE, "no timed search yet");
+  DADE_CK(cudaEventSynchronize(x->ev[3]));
+  DADE_CK(cudaEventElapsedTime(&ms3[0], x->ev[0], x->ev[1]));
+  DADE_CK(cudaEventElapsedTime(&ms3[1], x->ev[0], x->ev[2]));
+  DADE_CK(cudaEventElapsedTime(&ms3[2], x->ev[2], x->ev[3]));
   API_END
 }
 

@@ -62,6 +62,8 @@ _SIGS = {
     "dade_search_host": [P, P, I32, I32, I32, I32, DBL, P, P, P],
     "dade_search_method": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
     "dade_prepare": [P, P, I32, I32, P, P],
+    "dade_set_timing": [P, I32],
+    "dade_get_timing": [P, P],
     "dade_search_prepared": [P, P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
     "dade_probe": [P, P, I32, I32, P],
     "dade_bruteforce_knn": [P, P, I64, I64, P, I32, I32, P, P],
@@ -244,6 +246,16 @@ class Index:
         _ck(lib().dade_search_method(self.h, _ptr(Q), nq, K, nprobe, delta_d, self.METHODS[method], float(param),
                                      _ptr(ids), _ptr(dists), C.byref(st) if st is not None else None))
         return (ids, dists, st.as_dict()) if stats else (ids, dists)
+
+    def set_timing(self, on: bool):
+        """Record stage events on every search (no synchronisation); read them with get_timing."""
+        _ck(lib().dade_set_timing(self.h, int(bool(on))))
+
+    def get_timing(self):
+        """{'rotate', 'probe', 'scan'} ms of the last search (waits for its events)."""
+        ms = np.zeros(3, np.float32)
+        _ck(lib().dade_get_timing(self.h, _ptr(ms)))
+        return {"rotate": float(ms[0]), "probe": float(ms[1]), "scan": float(ms[2])}
 
     def prepare(self, Q, nprobe: int):
         """a4 + a5 only: (q~ = R(q - mu) [nq, D] fp32, probes [nq, nprobe] int32) on the device."""
