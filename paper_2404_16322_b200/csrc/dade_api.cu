@@ -679,6 +679,9 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
       exact_knn(x, S.p, nkm, cent.p, nlist, 1, a_d.p, nullptr);
       DADE_CK(cudaMemcpyAsync(a.data(), a_d.p, sizeof(int32_t) * nkm, cudaMemcpyDeviceToHost, st));
       DADE_CK(cudaStreamSynchronize(st));
+      check_knn_flag(x);
+      for (int64_t k = 0; k < nkm; ++k)
+        DADE_REQUIRE(a[k] >= 0 && a[k] < nlist, DADE_ERR_CUDA, "k-means: invalid list id from the assignment");
       std::fill(sums.begin(), sums.end(), 0.0);
       std::fill(cnt.begin(), cnt.end(), 0);
       for (int64_t k = 0; k < nkm; ++k) {
@@ -704,6 +707,9 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
     else exact_knn(x, X, n, cent.p, nlist, 1, a_d.p, nullptr);
     DADE_CK(cudaMemcpyAsync(assign.data(), a_d.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     DADE_CK(cudaStreamSynchronize(st));
+    check_knn_flag(x);
+    for (int64_t i = 0; i < n; ++i)
+      DADE_REQUIRE(assign[i] >= 0 && assign[i] < nlist, DADE_ERR_CUDA, "build_ivf: invalid list id from the assignment");
   }
   // counting sort by (list, id): lists hold ids ascending
   std::vector<int64_t> off(nlist + 1, 0);

@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   for (int i0 = 0; i0 < P; i0 += 32) {  // exact fp64 distances, 32 candidates per staged batch
     const int i = i0 + lane;
     const int32_t c = (i < cnt) ? cc[w][i] : -1;
-    const double d = i0 < cnt ? exact_batch32(a, B, D, c, xstage[w], lane) : 0.0;
+    const double d = i0 < cnt ? exact_batch32(a, B, D, c, xstage[w], lane, min(32, cnt - i0)) : 0.0;
     if (i < P) {
       if (i < cnt) cd[w][i] = d;
       else { cd[w][i] = DBL_MAX; cc[w][i] = 0x7fffffff; }

@@ -10,25 +10,35 @@ namespace dade {
 
 constexpr int kXbDim = 32;  // dims staged per pass; stage = 32 x (kXbDim + 1) floats per warp
 
-// c: this lane's candidate row index (< 0: none); a: the query row (global, broadcast reads)
+// c: this lane's candidate row index (< 0: none); a: the query row (global, broadcast reads);
+// nc (warp-uniform, <= 32): candidates are in lanes [0, nc) — only those rows are staged
 __device__ __forceinline__ double exact_batch32(const float* __restrict__ a, const float* __restrict__ B, int D,
-                                                int32_t c, float* stage, int lane) {
+                                                int32_t c, float* stage, int lane, int nc = 32) {
   double acc = 0.0;
   // the next slice's 32 loads are issued before the current slice is accumulated
   float v[32];
   auto load = [&](int j0) {
     const int w = min(kXbDim, D - j0);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
-      v[i] = (ci >= 0 && lane < w) ? __ldg(B + (int64_t)ci * D + j0 + lane) : 0.f;
+    for (int i0 = 0; i0 < 32; i0 += 8) {  // only the groups of 8 that hold candidates
+      if (i0 < nc) {
+#pragma unroll
+        for (int i = i0; i < i0 + 8; ++i) {
+          const int32_t ci = __shfl_sync(0xffffffffu, c, i);
+          v[i] = (ci >= 0 && lane < w) ? __ldg(B + (int64_t)ci * D + j0 + lane) : 0.f;
+        }
+      }
     }
   };
   load(0);
   for (int j0 = 0; j0 < D; j0 += kXbDim) {
     const int w = min(kXbDim, D - j0);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) stage[i * (kXbDim + 1) + lane] = v[i];
+    for (int i0 = 0; i0 < 32; i0 += 8)
+      if (i0 < nc) {
+#pragma unroll
+        for (int i = i0; i < i0 + 8; ++i) stage[i * (kXbDim + 1) + lane] = v[i];
+      }
     __syncwarp();
     if (j0 + kXbDim < D) load(j0 + kXbDim);
     if (c >= 0) {
