@@ -209,10 +209,10 @@ struct RegTopK {
 // entries are queued; with an async round in flight stage 1 may run up to 64 queued (+32 + 32).
 template <int DD, bool ASY>
 struct Slice {
-  static constexpr int kStages = (DD == 1 && !ASY) ? 3 : 2;  // ASY: the staging buffer replaces a stage
+  static constexpr int kStages = (DD == 1 && !ASY) ? 3 : 2;  // ASY: the staging buffers replace a stage
   static constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
   static constexpr int QCAP = ASY ? 128 : 64;
-  static constexpr size_t stage_bytes = ASY ? 32 * 64 + 32 * 4 : 0;  // async gather round: rows + ids
+  static constexpr size_t stage_bytes = ASY ? 2 * (32 * 64 + 32 * 4) : 0;  // 2 async rounds: rows + ids
   static constexpr size_t bytes = (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + QCAP * sizeof(QEntry) +
                                   stage_bytes;
 };
@@ -238,8 +238,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
   TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + 4);
   QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
-  unsigned char* stg = reinterpret_cast<unsigned char*>(ring + kQCap);  // async round: 32 x 64 B rows
-  uint32_t* stg_id = reinterpret_cast<uint32_t*>(stg + 32 * 64);
+  unsigned char* stg = reinterpret_cast<unsigned char*>(ring + kQCap);  // async rounds: 2 x (32 x 64 B rows, ids)
   unsigned* pruned = reinterpret_cast<unsigned*>(smem + G * SL::bytes);
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
@@ -444,30 +443,37 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       tk.init(K);
     };
 
-    // ASY: a full round (32 queued survivors, one block each) is issued as cp.async copies into
-    // the warp's staging buffer and completed later, so its memory latency overlaps with stage-1
-    // work on the next tiles (the TMA ring has them in shared memory already)
-    QEntry pe{0, 0.f, nblk, 0.f};
-    bool pend = false;
-    int since = 0;
+    // ASY: full rounds (32 queued survivors, one block each) are issued as cp.async copies into
+    // one of two staging buffers and completed later (oldest first), so up to two gather round
+    // trips are in flight per warp while stage 1 works on the tiles the TMA ring already holds
+    QEntry pe0{0, 0.f, nblk, 0.f}, pe1{0, 0.f, nblk, 0.f};
+    int npend = 0, pfirst = 0, since = 0;
     auto issue_round = [&]() {
-      pe = ring[(head + lane) & (kQCap - 1)];
+      const int slot = (pfirst + npend) & 1;
+      const QEntry e = ring[(head + lane) & (kQCap - 1)];
+      if (slot) pe1 = e; else pe0 = e;
       head += 32;
-      const float* src = lay + (((int64_t)pe.blk * n + pe.row) << 4);
-      const uint32_t dst = smem_u32(stg + lane * 64);
+      unsigned char* sb = stg + slot * (32 * 64 + 32 * 4);
+      const float* src = lay + (((int64_t)e.blk * n + e.row) << 4);
+      const uint32_t dst = smem_u32(sb + lane * 64);
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(src + c * 4) : "memory");
-      if (pe.blk + 1 == nblk)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stg_id + lane)), "l"(p.row_id + pe.row)
+      if (e.blk + 1 == nblk)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sb + 32 * 64 + lane * 4)),
+                     "l"(p.row_id + e.row)
                      : "memory");
       asm volatile("cp.async.commit_group;" ::: "memory");
-      pend = true;
-      since = 0;
+      if (npend == 0) since = 0;
+      ++npend;
     };
-    auto complete_round = [&]() {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      const ulonglong2* sr = reinterpret_cast<const ulonglong2*>(stg + lane * 64);
+    auto complete_round = [&]() {  // the oldest pending round
+      if (npend == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      const int slot = pfirst;
+      const QEntry pe = slot ? pe1 : pe0;
+      const unsigned char* sb = stg + slot * (32 * 64 + 32 * 4);
+      const ulonglong2* sr = reinterpret_cast<const ulonglong2*>(sb + lane * 64);
       unsigned long long x[8];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -489,10 +495,12 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const bool fin = alive && blk == nblk;
       push(alive && !fin, QEntry{pe.row, phi, blk, res});
       if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
-      const unsigned long long key = fin ? make_key(phi, stg_id[lane]) : kKeyInf;
+      const unsigned long long key = fin ? make_key(phi, reinterpret_cast<const uint32_t*>(sb + 32 * 64)[lane]) : kKeyInf;
       __syncwarp();
       tk.offer(!MULTI || key < cap ? key : kKeyInf, lane);
-      pend = false;
+      pfirst ^= 1;
+      --npend;
+      since = 0;
     };
 
     // ---------------------------------------------------- consumer (one call site per action)
@@ -501,11 +509,11 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     for (;;) {
       const int qlen = tail - head;
       if (ASY) {
-        if (!pend && qlen >= 32) {
+        if (npend < 2 && qlen >= 32) {
           issue_round();
           continue;
         }
-        if (pend) {
+        if (npend > 0) {
           if (!ready && consumed < issued) {
             const int slot = consumed % kStages;
             mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
@@ -513,14 +521,15 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
             tm = meta[slot];
             ready = true;
           }
-          if (!(ready && tm.ep == cur_ep && since < 2 && qlen <= kQCap - 64)) {
+          // room: this tile's survivors (32) and every pending round's results (32 each)
+          if (!(ready && tm.ep == cur_ep && since < 4 && qlen + 32 * (npend + 1) <= kQCap)) {
             complete_round();
             continue;
           }
         }
       }
       bool round = !ASY && qlen >= 32, drain = false, ep_end = false;
-      if (!round && !(ASY && pend)) {
+      if (!round && !(ASY && npend > 0)) {
         if (!ready && consumed < issued) {
           const int slot = consumed % kStages;
           mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
