@@ -486,6 +486,130 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
     if (out_d) out_d[row * k + i] = ok ? cd[w][i] : DBL_MAX;
   }
 }
+// Same selection with ONE row per CTA (large k, e.g. nprobe 64 at D = 960): warp 0 finds the
+// candidates, the four warps share the row's fp64 batches (each a long sequential chain), warp 0
+// sorts. Used when k > 16.
+template <int GPL>
+__global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin_wide(
+    const float* __restrict__ dh, const float* __restrict__ gm, int gshift, int64_t m, int64_t n, int k,
+    const float* __restrict__ A, const float* __restrict__ B, int D, int32_t* __restrict__ out_idx,
+    double* __restrict__ out_d, int* ovf_n, int32_t* __restrict__ ovf_rows, const float* __restrict__ slack) {
+  __shared__ float sg[1][32 * GPL];
+  __shared__ double cd[1][kGmCap];
+  __shared__ int32_t cc[1][kGmCap];
+  __shared__ float xstage[kGmWarps][32 * (kXbDim + 1)];
+  __shared__ int s_cnt;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, w = 0;
+  const int64_t row = blockIdx.x;
+  int cnt = 0;
+  if (wid == 0) {
+  const int ng = (int)((n + (1 << gshift) - 1) >> gshift);
+  // the k-th smallest group minimum E bounds the k-th smallest d_hat from above
+  float gv[GPL];  // group lane + 32 j
+#pragma unroll
+  for (int j = 0; j < GPL; ++j) gv[j] = lane + 32 * j < ng ? gm[row * ng + lane + 32 * j] : INFINITY;
+  float E;
+  if (k <= 16) {  // k rounds of a warp-wide minimum (keys (value bits, group) are unique)
+    float rem[GPL];
+#pragma unroll
+    for (int j = 0; j < GPL; ++j) rem[j] = gv[j];
+    unsigned long long key = 0;
+    for (int r = 0; r < k; ++r) {
+      unsigned long long mine = ~0ull;
+#pragma unroll
+      for (int j = 0; j < GPL; ++j) {
+        const unsigned long long kk = ((unsigned long long)__float_as_uint(rem[j]) << 32) | (unsigned)(lane + 32 * j);
+        mine = kk < mine ? kk : mine;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, mine, o);
+        mine = t < mine ? t : mine;
+      }
+      key = mine;
+      const int gsel = (int)(key & 0xffffffffu);
+#pragma unroll
+      for (int j = 0; j < GPL; ++j)
+        if (lane + 32 * j == gsel) rem[j] = __uint_as_float(0x7f800001u);  // removed (NaN: sorts last as bits)
+    }
+    E = __uint_as_float((unsigned)(key >> 32));
+  } else {  // bitonic sort of the group minima (GPL per lane)
+    float* g = sg[w];
+#pragma unroll
+    for (int j = 0; j < GPL; ++j) g[lane + 32 * j] = gv[j];
+    __syncwarp();
+    for (int size = 2; size <= 32 * GPL; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = lane; i < 16 * GPL; i += 32) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const float x = g[lo], y = g[hi];
+          if ((y < x) == up) { g[lo] = y; g[hi] = x; }
+        }
+        __syncwarp();
+      }
+    E = g[k - 1];
+  }
+  const unsigned tb = abs_thr_bits(E, slack[row]);
+  // every column inside the window lies in a group whose minimum is inside it: read only those
+  // groups' d_hat (one coalesced 128-B row segment per group)
+  const float* d = dh + row * n;
+  int cnt = 0;
+#pragma unroll 1
+  for (int j = 0; j < GPL; ++j) {
+    unsigned gb = __ballot_sync(0xffffffffu, __float_as_uint(gv[j]) <= tb);
+    while (gb) {
+      const int grp = 32 * j + __ffs(gb) - 1;
+      gb &= gb - 1;
+      for (int h = 0; h < (1 << gshift); h += 32) {
+        const int64_t c = ((int64_t)grp << gshift) + h + lane;
+        const bool in = c < n && __float_as_uint(d[c]) <= tb;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+          if (pos < kGmCap) cc[w][pos] = (int32_t)c;
+        }
+        cnt += __popc(bal);
+      }
+    }
+  }
+  if (cnt > kGmCap && lane == 0) ovf_rows[atomicAdd(ovf_n, 1)] = (int32_t)row;  // histogram select redoes it
+  if (lane == 0) s_cnt = cnt;
+  }
+  __syncthreads();
+  cnt = s_cnt;
+  if (cnt > kGmCap) return;
+  for (int i0 = wid * 32; i0 < cnt; i0 += kGmWarps * 32) {  // batches shared by the four warps
+    const int i = i0 + lane;
+    const int32_t c = i < cnt ? cc[0][i] : -1;
+    const double d = exact_batch32(A + row * (int64_t)D, B, D, c, xstage[wid], lane, min(32, cnt - i0));
+    if (i < cnt) cd[0][i] = d;
+  }
+  __syncthreads();
+  if (wid != 0) return;
+  const float* a = A + row * (int64_t)D;
+  (void)a;
+  int P = 1;
+  while (P < cnt) P <<= 1;
+  for (int i = cnt + lane; i < P; i += 32) { cd[0][i] = DBL_MAX; cc[0][i] = 0x7fffffff; }
+  __syncwarp();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < P / 2; i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const double x = cd[w][lo], y = cd[w][hi];
+        const int32_t xc = cc[w][lo], yc = cc[w][hi];
+        if (cand_less2(y, yc, x, xc) == up) { cd[w][lo] = y; cd[w][hi] = x; cc[w][lo] = yc; cc[w][hi] = xc; }
+      }
+      __syncwarp();
+    }
+  for (int i = lane; i < k; i += 32) {
+    const bool ok = i < cnt;
+    out_idx[row * k + i] = ok ? cc[w][i] : -1;
+    if (out_d) out_d[row * k + i] = ok ? cd[w][i] : DBL_MAX;
+  }
+}
 
 // ------------------------------------------------------------------ group select (no d_hat)
 // The filter GEMM wrote only the per-row minima of d_hat over 32-column groups (gm[row][g]). Every
@@ -626,7 +750,13 @@ void launch_select_gmin(const float* d_hat, const float* gmin, int gshift, int64
   DADE_CK(cudaMemsetAsync(ovf_n, 0, sizeof(int), st));
   const int64_t ngr = (n + (1 << gshift) - 1) >> gshift;
   const unsigned gsz = (unsigned)((m + kGmWarps - 1) / kGmWarps);
-  if (ngr <= 256)
+  if (k > 16 && ngr <= 256)
+    k_select_gmin_wide<8><<<(unsigned)m, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+  else if (k > 16 && ngr <= 512)
+    k_select_gmin_wide<16><<<(unsigned)m, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+  else if (k > 16)
+    k_select_gmin_wide<32><<<(unsigned)m, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
+  else if (ngr <= 256)
     k_select_gmin<8><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
   else if (ngr <= 512)
     k_select_gmin<16><<<gsz, kGmWarps * 32, 0, st>>>(d_hat, gmin, gshift, m, n, k, A, B, D, out_idx, out_d64, ovf_n, ovf_rows, slack);
