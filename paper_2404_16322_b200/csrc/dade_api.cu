@@ -450,9 +450,6 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     stats->n_epochs = (int32_t)c[3];
     for (int s = 0; s < DADE_MAX_STEPS; ++s) stats->pruned_at_step[s] = (int64_t)c[4 + s];
     stats->n_steps = nsteps;
-    if (getenv("DADE_DEBUG_COUNTS"))
-      fprintf(stderr, "[dade debug] rounds=%llu entries=%llu merges=%llu tiles=%llu drain_rounds=%llu\n",
-              c[68], c[69], c[70], c[71], c[72]);
     cudaEventElapsedTime(&stats->ms_rotate, x->ev[0], x->ev[1]);  // concurrent with the probe
     cudaEventElapsedTime(&stats->ms_probe, x->ev[0], x->ev[2]);
     cudaEventElapsedTime(&stats->ms_scan, x->ev[2], x->ev[3]);

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
     const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ an,
     const float* __restrict__ Bhi, const float* __restrict__ Blo, const float* __restrict__ bn, int nkc,
     int64_t m, int64_t n, int tiles_per_split, int k, int C, const float* __restrict__ slack,
-    int32_t* __restrict__ cand, int32_t* __restrict__ ccount, int dbg, int passes) {
+    int32_t* __restrict__ cand, int32_t* __restrict__ ccount, int passes) {
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
@@ -262,7 +262,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
           if (lane == 0) mbar_arrive(&tempty[b]);
         }
         const int64_t c0 = cb0 + cb * 32;
-        if (dbg) continue;  // dbg: timing of the GEMM pipeline alone
         // d_hat = max(0, fma(-2, acc, a2 + bn)) in packed FP32x2 (same roundings as the scalar
         // form); the max(0, .) is applied on append only: as signed ints, negative d compare
         // below any window, like 0 does
@@ -308,8 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
         }
       }
     }
-    if (live && dbg) ccount[row * gridDim.y + blockIdx.y] = 0;
-    if (live && !dbg) {
+    if (live) {
       if (nl >= k) reduce();
       const int64_t slot = row * gridDim.y + blockIdx.y;
       for (int i = 0; i < nl; ++i) {  // (column, d_hat bits) pairs
@@ -523,9 +521,8 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
   const int64_t ntiles = (n + kTM - 1) / kTM;
   const int tps = (int)((ntiles + nsplit - 1) / nsplit);
   dim3 grid((unsigned)((m + kTM - 1) / kTM), (unsigned)nsplit);
-  const int dbg = getenv("DADE_PROBE_DBG") ? atoi(getenv("DADE_PROBE_DBG")) : 0;
   k_probe_tc<<<grid, kThreads, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), m, n, tps, k, C, slack, cand,
-                                          ccount, dbg, passes);
+                                          ccount, passes);
   DADE_CK(cudaGetLastError());
   const size_t fsm = (size_t)kFinWarps * kFinWarpBytes;
   static bool fattr = false;
