@@ -449,8 +449,11 @@ def run_reference(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(ts), 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (datagen/synth.py, seed 0)",
-           "config": {"workload": f"{cfg.name} sample: oracle index on {sub.n} rows, nlist={nlist}, "
-                                  f"nprobe={nprobe}, {per_step} queries per step", "nprobe": nprobe},
+           "config": {"workload": f"{cfg.name}: IVF-DADE {SHAPE[cfg.name]} n={cfg.n} D={cfg.d} nq={cfg.nq} "
+                                  f"nlist={cfg.nlist} K={cfg.k} delta_d={cfg.delta_d} significance={ALPHA}",
+                      "nprobe": nprobe, "method": "bsa_p",
+                      "sample": f"each step: {per_step} queries on an oracle index over a {sub.n}-row prefix of the "
+                                f"same base (nlist={nlist}, same ~{cfg.n // cfg.nlist} rows per list)"},
            "cpu_baseline": {"value": round(val, 3), "unit": "queries/s", "kind": "oracle", "cores": 1,
                             "sample": f"{per_step} queries per step on a {sub.n}-row prefix index"},
            "e2e": {"value": round(val, 3), "unit": "queries/s", "h2d_bytes_per_step": 0,
