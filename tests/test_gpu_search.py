@@ -212,3 +212,20 @@ def test_prepare_then_search_prepared_equals_search(sift_small):
     assert torch.equal(e, g) and torch.equal(f, h)
     z = ix.prepare(Q[:0].contiguous(), 8)                      # an empty block (more ranks than queries)
     assert z[0].shape == (0, cfg.d) and z[1].shape == (0, 8)
+
+
+@pytest.mark.parametrize("D,K,dd", [(16, 1, 16), (32, 7, 16), (128, 256, 32)])
+def test_extreme_shapes(D, K, dd):
+    # D = 16 (one block, a single step: never a classifier), K = 1, and K = 256 (DADE_MAX_K: eight
+    # register keys per lane); exact search (alpha = 0) over every list equals brute force and
+    # the calibrated search loses at most 1% recall against exact IVF
+    cfg = synth.config("c1", n=4000, d=D, nlist=16, nq=16, n_cal=20, k=K, delta_d=dd)
+    torch, ix, oidx, X, Xd = _setup(cfg, kmeans_iters=2, cal=False)
+    Q = synth.queries(cfg)
+    gi, gd = ix.search(torch.from_numpy(Q).cuda(), K, cfg.nlist, dd, 0.0)
+    bi, bd = O.brute_force_knn(X, Q, K)
+    assert tie_adjusted_overlap(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd) == 1.0
+    assert rel_err(gd.cpu().numpy(), bd) <= 1e-5
+    from paper_2404_16322_b200 import DadeError
+    with pytest.raises(DadeError):
+        ix.search(torch.from_numpy(Q).cuda(), 257, 4, dd, 0.0)   # K > DADE_MAX_K
