@@ -150,3 +150,17 @@ def test_heldout_quantile(c1_index):
             d = (s + 1) * dd
             frac = np.mean(m[s] * P[:, d - 1] + b[s] > tau)
             assert abs(frac - a_s) <= band, (alpha, d, frac, a_s, band)
+
+
+def test_step_table_uses_the_row_of_its_prefix_length():
+    # the classifier at step s (d = s*Δd) must use the calibration row fitted on
+    # prefix length d: rows are made distinguishable (value = d) and the slope row likewise
+    D, n0 = 128, 50
+    cls_d = np.arange(1, D // 16) * 16                      # prefixes 16, 32, ..., 112
+    cal = {"block": 16, "m1": cls_d.astype(float) / 1000.0,
+           "v": np.repeat(cls_d[:, None].astype(float), n0, axis=1)}
+    for dd in (16, 32, 64):
+        m, b = O.step_table(cal, D, dd, 0.01)
+        d = np.arange(1, D // dd) * dd
+        assert np.array_equal(b, d.astype(float))
+        assert np.allclose(m, d / 1000.0)
