@@ -95,6 +95,11 @@ void launch_select_groups(const float* gmin, int64_t m, int64_t n, int k, const 
 // probe_tc.cu: fused filter GEMM + candidate tracking (no d_hat matrix) + exact finish, k <= 64.
 // cand: m * nsplit * probe_tc_cap(k) * 2 int32 scratch, ccount: m * nsplit int32 scratch.
 int probe_tc_cap(int k);
+// d_hat matrix + group minima with the warp-specialised pipeline of probe_tc.cu (same contract as
+// launch_l2_tc with out != nullptr)
+void launch_dhat_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
+                    const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo, float* gmin,
+                    int gshift, int passes, cudaStream_t st);
 int probe_tc_splits(int64_t m, int64_t n, int sms);
 void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                      const float* Blo, const float* bn, int64_t n, int D, int k, const float* slack,

@@ -322,6 +322,172 @@ __global__ void __launch_bounds__(kThreads, 1) k_probe_tc(
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
+// d_hat writer (the filter of the group-minima select, exact.cu): the same warp-specialised
+// pipeline as k_probe_tc — TMA warp, MMA warp, two TMEM accumulators, 4 epilogue warps, each CTA
+// looping over a range of column tiles so MMA of tile t+1 overlaps the epilogue of tile t — with
+// an epilogue that writes d_hat (each warp transposes its 32 x 32 chunk through shared memory
+// for row-contiguous stores) and the per-row minima of 2^gshift-column groups. 1-pass: four
+// 16 KB stages (hi parts), 3-pass: two 32 KB stages.
+__global__ void __launch_bounds__(kThreads, 2) k_dhat_tc(
+    const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ an,
+    const float* __restrict__ Bhi, const float* __restrict__ Blo, const float* __restrict__ bn, int nkc,
+    int64_t m, int64_t n, int tiles_per_split, float* __restrict__ out, int64_t ldo, float* __restrict__ gmin,
+    int64_t ldg, int gshift, int passes) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int S = passes == 1 ? 4 : 2;
+  const int SB = (kStages * kStageBytes) / S;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
+  uint64_t* empty = full + 4;
+  uint64_t* tfull = empty + 4;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stg_all = reinterpret_cast<float*>(sm + kStages * kStageBytes + 128);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tm = blockIdx.x;
+  const int64_t ntiles = (n + kTM - 1) / kTM;
+  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
+  const int64_t rem = ntiles - t0;
+  const int nt = rem <= 0 ? 0 : (int)(rem < tiles_per_split ? rem : tiles_per_split);
+  const int offB = passes == 1 ? kSub * 4 : 2 * kSub * 4;
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int it = 0;
+      for (int t = 0; t < nt; ++t) {
+        const int64_t tn = t0 + t;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % S;
+          if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+          unsigned char* st = sm + s * SB;
+          mbar_expect_tx(&full[s], SB);
+          const int64_t ao = (tm * nkc + kc) * kSub, bo = (tn * nkc + kc) * kSub;
+          bulk_g2s(st, Ahi + ao, kSub * 4, &full[s]);
+          bulk_g2s(st + offB, Bhi + bo, kSub * 4, &full[s]);
+          if (passes != 1) {
+            bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
+            bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+      int it = 0;
+      for (int t = 0; t < nt; ++t) {
+        const int b = t & 1;
+        if (t >= 2) mbar_wait(&tempty[b], ((t >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + b * kTM;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          unsigned char* st = sm + s * SB;
+#pragma unroll
+          for (int j = 0; j < kKC / 8; ++j) {
+            const uint64_t ah = umma_desc(st + j * 256, 128, kSBO);
+            const uint64_t bh = umma_desc(st + offB + j * 256, 128, kSBO);
+            mma_tf32(acc, ah, bh, idesc, (kc | j) != 0);
+            if (passes != 1) {
+              const uint64_t al = umma_desc(st + kSub * 4 + j * 256, 128, kSBO);
+              const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
+              mma_tf32(acc, ah, bl, idesc, 1);
+              mma_tf32(acc, al, bh, idesc, 1);
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[b]);
+      }
+    }
+  } else {  // ---------------- epilogue: one thread per row, warp-transposed stores
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int64_t row = tm * kTM + r;
+    const float a2 = row < m ? an[row] : 0.f;
+    float* stg = stg_all + (warp - 2) * 32 * 33;
+    float gmn = INFINITY;
+    for (int t = 0; t < nt; ++t) {
+      const int b = t & 1;
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t cb0 = (t0 + t) * kTM;
+#pragma unroll 1
+      for (int cb = 0; cb < kTM / 32; ++cb) {
+        uint32_t v[32];
+        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + b * kTM + cb * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (cb == kTM / 32 - 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        const int64_t c0 = cb0 + cb * 32;
+        const bool fullc = c0 + 32 <= n;
+        float d[32];
+        const float2* bn2 = reinterpret_cast<const float2*>(bn + c0);  // bn is padded to 128
+        const unsigned long long a2p = pk2(a2, a2), m2 = pk2(-2.f, -2.f);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float2 bb = __ldg(bn2 + jj);
+          const unsigned long long x = fma2(m2, pk2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1])),
+                                            add2(a2p, pk2(bb.x, bb.y)));
+          const float2 xf = *reinterpret_cast<const float2*>(&x);
+          d[2 * jj] = c0 + 2 * jj < n ? fmaxf(0.f, xf.x) : INFINITY;
+          d[2 * jj + 1] = c0 + 2 * jj + 1 < n ? fmaxf(0.f, xf.y) : INFINITY;
+        }
+        if (gmin && row < m && c0 < n) {
+          float mn = d[0];
+#pragma unroll
+          for (int j = 1; j < 32; ++j) mn = fminf(mn, d[j]);
+          if (gshift == 6) {
+            if ((cb & 1) == 0) gmn = mn;
+            mn = fminf(mn, gmn);
+          }
+          if (gshift == 5 || (cb & 1) == 1 || c0 + 32 >= n) gmin[row * ldg + (c0 >> gshift)] = mn;
+        }
+        if (fullc && (ldo & 3) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = d[j];
+          __syncwarp();
+#pragma unroll
+          for (int itr = 0; itr < 8; ++itr) {
+            const int ri = itr * 4 + (lane >> 3), cc = (lane & 7) * 4;
+            const int64_t grow = tm * kTM + q * 32 + ri;
+            if (grow < m) {
+              const float* sp = stg + ri * 33 + cc;
+              *reinterpret_cast<float4*>(out + grow * ldo + c0 + cc) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+            }
+          }
+          __syncwarp();
+        } else if (row < m) {
+          float* o = out + row * ldo + c0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) o[j] = d[j];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
 __device__ __forceinline__ bool cless(double d0, int32_t c0, double d1, int32_t c1) {
   return d0 < d1 || (d0 == d1 && c0 < c1);
 }
@@ -497,6 +663,32 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
 }  // namespace
 
 int probe_tc_cap(int k) { return k + 32; }
+
+void launch_dhat_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
+                    const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo, float* gmin,
+                    int gshift, int passes, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return;
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    DADE_CK(cudaGetDevice(&dev));
+    DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const size_t smem = kStages * kStageBytes + 128 + 4 * 32 * 33 * 4;
+  static bool attr = false;
+  if (!attr) {
+    DADE_CK(cudaFuncSetAttribute(k_dhat_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM;
+  int64_t nsplit = 1;
+  while (mt * nsplit < 2 * sms && nsplit * 4 <= ntiles) nsplit *= 2;  // >= 4 tiles per CTA
+  const int tps = (int)((ntiles + nsplit - 1) / nsplit);
+  dim3 grid((unsigned)mt, (unsigned)((ntiles + tps - 1) / tps));
+  k_dhat_tc<<<grid, kThreads, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), m, n, tps, out, ldo, gmin,
+                                         (n + (1 << gshift) - 1) >> gshift, gshift, passes);
+  DADE_CK(cudaGetLastError());
+}
 
 int probe_tc_splits(int64_t m, int64_t n, int sms) {
   const int64_t mt = (m + kTM - 1) / kTM, nt = (n + kTM - 1) / kTM;
