@@ -396,6 +396,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   // alpha = 0 (or a single step): nothing can be pruned; the kernel then runs with 16-dim
   // steps (no classifier fires: m1 = 1, beta' = -inf), which serves every delta_d | D.
   p.dd = prune ? dd : 1; p.nsteps = prune ? nsteps : D / 16; p.c0 = 4 * K; p.prune = prune ? 1 : 0;
+  p.avg_stream = (int64_t)nprobe * x->n / std::max(1, x->nlist);
   for (int s = 1; s < p.nsteps; ++s) {
     if (prune && method == DADE_METHOD_ADSAMPLING) {  // m1_d = (D/d)/(1 + eps0/sqrt(d))^2, beta = 0
       const double d = (double)s * delta_d;

@@ -145,6 +145,7 @@ struct ScanParams {
   int residual;
   const float* xnorm;   // n: ‖x~‖² per list-major row (residual only)
   const float* qconst;  // nq x (nsteps - 1): ‖q_r‖² − m·σ_d per step (residual only)
+  int64_t avg_stream;   // expected candidates per query (nprobe * n / nlist): picks warps per query
 };
 void launch_scan(const ScanParams& p, cudaStream_t st);
 // ‖x~‖² of every list-major row of the blocked layout (fp64 sums, stored fp32)

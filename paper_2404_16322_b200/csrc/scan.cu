@@ -633,13 +633,15 @@ static size_t scan_smem(int D, int K, int nprobe, int G) {
          (size_t)((D + 3) & ~3) * 4 + (RES ? DADE_MAX_STEPS * 4 : 0) + (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
 
-// warps per query: the smallest G giving >= 12 query-warps per SM (measured on C3, 1,000
-// queries: G = 2 1.84 ms, 4 1.91 ms, 8 2.34 ms, 1 2.92 ms — larger groups pay epoch barriers)
-static int scan_group(int nq, int sms) {
+// warps per query: the smallest G giving >= 16 query-warps per SM, and G >= 2 for long candidate
+// streams (>= 4,000 per query) — measured: C3 (1,000 queries) G = 4 1.35 ms, 2 1.41, 1 1.87;
+// C4 (10k queries, ~4,900 candidates each) G = 2 1.19 ms vs 1 1.26; C2 (~2,000) G = 1 0.57 vs
+// 2 0.67; C5 shard (~1,500) G = 1 1.66 vs 2 1.90 — larger groups pay epoch barriers
+static int scan_group(int nq, int sms, int64_t avg_stream) {
   const char* e = getenv("DADE_SCAN_G");
   if (e) return atoi(e);
-  int G = 1;
-  while (G < 8 && (int64_t)nq * G < (int64_t)sms * 12) G *= 2;
+  int G = avg_stream >= 4000 ? 2 : 1;
+  while (G < 8 && (int64_t)nq * G < (int64_t)sms * 16) G *= 2;
   return G;
 }
 
@@ -666,7 +668,7 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
     DADE_CK(cudaGetDevice(&dev));
     DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int G = scan_group(p.nq, sms);
+  const int G = scan_group(p.nq, sms, p.avg_stream);
   DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
   if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, ASY, RES>(p, st, 1, sms);
   else launch_g<DD, KPL, LA, MAXREG, true, ASY, RES>(p, st, G, sms);
@@ -695,8 +697,12 @@ static void launch_k(const ScanParams& p, cudaStream_t st) {
     }
   }
   if constexpr (DD >= 2) {  // a step spans DD blocks: gather a whole step per round trip
-    if (scan_variant() != 7) {
-      launch_v<DD, KPL, 2, 96>(p, st);
+    // register cap 128 (16 warps/SM, no spills): measured C5 shard 1.99 -> 1.66 ms, C3 1.50 -> 1.40
+    const int v = scan_variant();
+    if (v == 8) { launch_v<DD, KPL, 2, 96>(p, st); return; }
+    if (v == 9) { launch_v<DD, KPL, 2, 112>(p, st); return; }
+    if (v != 7) {
+      launch_v<DD, KPL, 2, 128>(p, st);
       return;
     }
   }

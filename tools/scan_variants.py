@@ -19,9 +19,13 @@ ap.add_argument("--nprobe", type=int, default=8)
 ap.add_argument("--variants", default="0,1,2,3,4,5")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--var", default="DADE_SCAN_VARIANT", help="environment variable the values are assigned to")
+ap.add_argument("--n", type=int, default=0)
+ap.add_argument("--nlist", type=int, default=0)
 a = ap.parse_args()
 build.build()
 cfg = synth.config(a.config)
+if a.n:
+    cfg = cfg.scaled(n=a.n, nlist=a.nlist or max(1, a.n // 244))
 m = synth.model(cfg)
 X = torch.from_numpy(synth.base(cfg, m, workers=min(16, os.cpu_count() or 1))).cuda()
 Q = torch.from_numpy(synth.queries(cfg, m=m)).cuda()
