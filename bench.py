@@ -157,7 +157,11 @@ def run_dade(args):
         full.set_rotation(mean, synth.haar_basis(cfg.d, np.random.default_rng(12345)).T.copy(), lam)
     torch.cuda.synchronize()
     t_rot = time.time() - t0
-    full.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
+    if world > 1:  # k-means over the sharded base: fp64 sums / counts all-reduced
+        cent = sharded.kmeans_sharded(full, Xd[lo:hi].contiguous(), lo, cfg.n, cfg.nlist, iters=10)
+        full.build_ivf(Xd, cfg.nlist, centroids=torch.from_numpy(cent).to(dev))
+    else:
+        full.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
     torch.cuda.synchronize()
     t_ivf = time.time() - t0 - t_rot
     if args.method == "bsa_p":

@@ -172,6 +172,17 @@ dade_status dade_search_method(dade_index* idx, const float* Q, int nq, int K, i
 dade_status dade_set_timing(dade_index* idx, int on);
 dade_status dade_get_timing(dade_index* idx, float* ms3);
 
+/* Sharded k-means (R19): this rank's part of one Lloyd step over the GLOBAL strided
+ * sample floor(k*n_total/n_km), n_km = min(n_total, 64*nlist). X: device rows [id_base, id_base+n)
+ * of the base. centroids: HOST nlist x D fp32 — the sampled rows this rank owns are assigned
+ * exactly (R20, lower id on ties) and their fp64 sums / counts are written to sums (host
+ * nlist x D) and counts (host nlist); the caller all-reduces them and sets centroid = sum / count
+ * rounded to fp32 (empty: keep). centroids == NULL: the init step — sampled rows with sample index
+ * < nlist are written to sums[k] (counts[k] = 1), so an all-reduce yields the first nlist sampled
+ * rows. Errors: ARG (bad range, nlist), CUDA. */
+dade_status dade_kmeans_partial(dade_index* idx, const float* X, int64_t n, int64_t id_base, int64_t n_total,
+                                int nlist, const float* centroids, double* sums, int64_t* counts);
+
 /* Split search (multi-GPU query partitioning): dade_prepare runs a4 + a5 for a block
  * of queries — qrot (device nq x D fp32, q~ = R(q - mu)) and probes (device nq x nprobe int32,
  * exact, ordered by (dist, id)); dade_search_prepared runs a6-a8 on this index's shard for

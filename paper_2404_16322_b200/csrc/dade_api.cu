@@ -760,6 +760,78 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
   API_END
 }
 
+// Sharded k-means: this rank's contribution to one Lloyd step over the GLOBAL
+// strided sample ⌊k·n_total/n_km⌋, n_km = min(n_total, 64·nlist) (R19). Rows of the sample in
+// [id_base, id_base + n) are assigned exactly to `centroids` (host nlist x D fp32; R20) and their
+// fp64 sums / counts added to sums (host nlist x D) / counts (host nlist). centroids == NULL:
+// the init step — the sampled rows with sample index < nlist are written into sums (row = sample
+// index) and counts[k] = 1 for them.
+extern "C" dade_status dade_kmeans_partial(dade_index* x, const float* X, int64_t n, int64_t id_base,
+                                           int64_t n_total, int nlist, const float* centroids, double* sums,
+                                           int64_t* counts) {
+  API_BEGIN
+  need(x, "index"); need(sums, "sums"); need(counts, "counts");
+  DADE_REQUIRE(nlist >= 1 && nlist <= n_total, DADE_ERR_ARG, "nlist not in [1, n_total]");
+  DADE_REQUIRE(n >= 0 && id_base >= 0 && id_base + n <= n_total, DADE_ERR_ARG, "bad row range");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  std::fill(sums, sums + (size_t)nlist * D, 0.0);
+  std::fill(counts, counts + nlist, (int64_t)0);
+  const int64_t nkm = std::min<int64_t>(n_total, (int64_t)64 * nlist);
+  std::vector<int32_t> sid;     // local row of each owned sample
+  std::vector<int64_t> sidx;    // its sample index k
+  for (int64_t k = 0; k < nkm; ++k) {
+    const int64_t gid = (int64_t)(((__int128)k * n_total) / nkm);
+    if (gid >= id_base && gid < id_base + n) { sid.push_back((int32_t)(gid - id_base)); sidx.push_back(k); }
+  }
+  if (centroids == nullptr) {  // init: the first nlist sampled rows
+    std::vector<int32_t> rows; std::vector<int64_t> ks;
+    for (size_t i = 0; i < sid.size(); ++i)
+      if (sidx[i] < nlist) { rows.push_back(sid[i]); ks.push_back(sidx[i]); }
+    if (!rows.empty()) {
+      need(X, "X");
+      DBuf<int32_t> r_d; DBuf<float> S;
+      r_d.reserve(rows.size()); S.reserve(rows.size() * D);
+      DADE_CK(cudaMemcpyAsync(r_d.p, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice, st));
+      launch_gather_rows(X, r_d.p, (int64_t)rows.size(), D, S.p, st);
+      std::vector<float> Sh(rows.size() * D);
+      DADE_CK(cudaMemcpyAsync(Sh.data(), S.p, 4 * Sh.size(), cudaMemcpyDeviceToHost, st));
+      DADE_CK(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < rows.size(); ++i) {
+        for (int j = 0; j < D; ++j) sums[(size_t)ks[i] * D + j] = (double)Sh[i * D + j];
+        counts[ks[i]] = 1;
+      }
+      r_d.release(); S.release();
+    }
+    g_err.clear();
+    return DADE_OK;
+  }
+  if (sid.empty()) { g_err.clear(); return DADE_OK; }
+  need(X, "X");
+  const int64_t m = (int64_t)sid.size();
+  DBuf<int32_t> sid_d, a_d; DBuf<float> S, C;
+  sid_d.reserve(m); a_d.reserve(m); S.reserve((size_t)m * D); C.reserve((size_t)nlist * D);
+  DADE_CK(cudaMemcpyAsync(sid_d.p, sid.data(), 4 * m, cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(C.p, centroids, sizeof(float) * nlist * D, cudaMemcpyHostToDevice, st));
+  launch_gather_rows(X, sid_d.p, m, D, S.p, st);
+  exact_knn(x, S.p, m, C.p, nlist, 1, a_d.p, nullptr);
+  std::vector<int32_t> a(m);
+  std::vector<float> Sh((size_t)m * D);
+  DADE_CK(cudaMemcpyAsync(a.data(), a_d.p, 4 * m, cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaMemcpyAsync(Sh.data(), S.p, 4 * Sh.size(), cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < m; ++i) {  // sample order within the shard (R19: fp64 sums)
+    DADE_REQUIRE(a[i] >= 0 && a[i] < nlist, DADE_ERR_CUDA, "k-means: invalid list id from the assignment");
+    double* sr = &sums[(size_t)a[i] * D];
+    const float* xr = &Sh[(size_t)i * D];
+    for (int j = 0; j < D; ++j) sr[j] += (double)xr[j];
+    ++counts[a[i]];
+  }
+  sid_d.release(); a_d.release(); S.release(); C.release();
+  API_END
+}
+
 extern "C" dade_status dade_get_ivf(const dade_index* x, int64_t* off, int64_t* row_id,
                                     int32_t* assign, float* centroids) {
   API_BEGIN

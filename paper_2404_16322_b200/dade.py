@@ -62,6 +62,7 @@ _SIGS = {
     "dade_search_host": [P, P, I32, I32, I32, I32, DBL, P, P, P],
     "dade_search_method": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
     "dade_prepare": [P, P, I32, I32, P, P],
+    "dade_kmeans_partial": [P, P, I64, I64, I64, I32, P, P, P],
     "dade_set_timing": [P, I32],
     "dade_get_timing": [P, P],
     "dade_search_prepared": [P, P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
@@ -246,6 +247,17 @@ class Index:
         _ck(lib().dade_search_method(self.h, _ptr(Q), nq, K, nprobe, delta_d, self.METHODS[method], float(param),
                                      _ptr(ids), _ptr(dists), C.byref(st) if st is not None else None))
         return (ids, dists, st.as_dict()) if stats else (ids, dists)
+
+    def kmeans_partial(self, X, id_base: int, n_total: int, nlist: int, centroids=None):
+        """This shard's fp64 sums / counts of one Lloyd step over the global strided sample
+        (centroids: host nlist x D fp32, None = the init step). Returns (sums, counts)."""
+        import torch
+        X = _dev(X, torch.float32)
+        sums = np.zeros((nlist, self.D)); counts = np.zeros(nlist, np.int64)
+        c = None if centroids is None else np.ascontiguousarray(centroids, np.float32)
+        _ck(lib().dade_kmeans_partial(self.h, _ptr(X), X.shape[0], id_base, n_total, nlist,
+                                      None if c is None else _ptr(c), _ptr(sums), _ptr(counts)))
+        return sums, counts
 
     def set_timing(self, on: bool):
         """Record stage events on every search (no synchronisation); read them with get_timing."""

@@ -50,6 +50,33 @@ def fit_rotation_sharded(engine, X_shard, id_base: int, n_total: int, sample_siz
     return mean, cnt
 
 
+def kmeans_sharded(engine, X_shard, id_base: int, n_total: int, nlist: int, iters: int = 10, group=None):
+    """k-means over a sharded base: the global strided sample, init = its first
+    nlist rows, `iters` Lloyd steps whose per-cluster fp64 sums and counts are all-reduced across
+    ranks; centroid = sum / count rounded to fp32, an empty cluster keeps its centroid. Every rank
+    ends with the same centroids (nlist x D fp32, host)."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(a, dtype):
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(dtype)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t, group=group)
+        return t.cpu().numpy()
+
+    sums, counts = engine.kmeans_partial(X_shard, id_base, n_total, nlist, None)
+    cent = allreduce(sums, torch.float64).astype(np.float32)
+    for _ in range(iters):
+        sums, counts = engine.kmeans_partial(X_shard, id_base, n_total, nlist, cent)
+        sums = allreduce(sums, torch.float64)
+        counts = allreduce(counts, torch.int64)
+        nz = counts > 0
+        cent = cent.copy()
+        cent[nz] = (sums[nz] / counts[nz, None]).astype(np.float32)
+    return cent
+
+
 class ShardedSearch:
     """search() on this rank's shard, then all-gather of the local top-K and the merge (a9)."""
 

@@ -72,3 +72,38 @@ def test_sharded_pca_partials_equal_single(env):
     om, oR, olam = O.fit_rotation(X, sample_size=7000)
     assert cnt == 7000
     np.testing.assert_allclose(lam, olam, rtol=1e-9, atol=1e-9 * olam[0])
+
+
+def test_kmeans_partial_logical_shards_equal_single():
+    # sharded k-means through the C-ABI (dade_kmeans_partial): S logical shards of one base on one
+    # GPU, their fp64 partial sums / counts added (what the all-reduce does) == the single-index
+    # k-means on the whole base (centroids up to the fp64 summation order) and the oracle's
+    import torch
+    from paper_2404_16322_b200 import Index, build
+    build.build()
+    cfg = synth.config("c4", n=20000, nlist=48)
+    X = synth.base(cfg)
+    Xd = torch.from_numpy(X).cuda()
+    mean, R, lam = O.fit_rotation(X)
+    full = Index(cfg.d)
+    full.set_rotation(mean, R, lam)
+    full.build_ivf(Xd, cfg.nlist, kmeans_iters=3)
+    cent_single = full.get_ivf()[3]
+    S = 3
+    shards = []
+    for s in range(S):
+        lo, hi = s * cfg.n // S, (s + 1) * cfg.n // S
+        ix = Index(cfg.d)
+        ix.set_rotation(mean, R, lam)
+        shards.append((ix, Xd[lo:hi].contiguous(), lo))
+    parts = [ix.kmeans_partial(Xs, lo, cfg.n, cfg.nlist) for ix, Xs, lo in shards]
+    cent = sum(p[0] for p in parts).astype(np.float32)
+    assert np.array_equal(sum(p[1] for p in parts), np.ones(cfg.nlist, np.int64))
+    for _ in range(3):
+        parts = [ix.kmeans_partial(Xs, lo, cfg.n, cfg.nlist, cent) for ix, Xs, lo in shards]
+        sums, counts = sum(p[0] for p in parts), sum(p[1] for p in parts)
+        nz = counts > 0
+        cent = cent.copy()
+        cent[nz] = (sums[nz] / counts[nz, None]).astype(np.float32)
+    assert np.allclose(cent, cent_single, rtol=1e-6, atol=1e-6)
+    assert np.allclose(cent, O.kmeans(X, cfg.nlist, iters=3), rtol=1e-6, atol=1e-6)

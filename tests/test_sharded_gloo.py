@@ -34,6 +34,23 @@ class OracleEngine:
         Y = self.X[g[(g >= id_base) & (g < id_base + len(self.X))] - id_base].astype(np.float64) - mean
         return Y.T @ Y
 
+    def kmeans_partial(self, X, id_base, n_total, nlist, centroids=None):
+        nkm = min(n_total, 64 * nlist)
+        g = O.strided_ids(n_total, nkm)
+        own = (g >= id_base) & (g < id_base + len(self.X))
+        ks, rows = np.nonzero(own)[0], g[own] - id_base
+        D = self.X.shape[1]
+        sums, counts = np.zeros((nlist, D)), np.zeros(nlist, np.int64)
+        if centroids is None:
+            sel = ks < nlist
+            sums[ks[sel]] = self.X[rows[sel]].astype(np.float64)
+            counts[ks[sel]] = 1
+            return sums, counts
+        a = O.assign(self.X[rows], centroids)
+        np.add.at(sums, a, self.X[rows].astype(np.float64))
+        counts += np.bincount(a, minlength=nlist)
+        return sums, counts
+
     def set_rotation_from_cov(self, mean, cov, cnt):
         lam, V = np.linalg.eigh(cov / cnt)
         self.rot = (mean, lam[::-1])
@@ -85,6 +102,11 @@ def _worker(rank, world, port, q):
         om, _, olam = O.fit_rotation(X, sample_size=3000)
         assert cnt == 3000 and np.allclose(mean, om, rtol=1e-12)
         assert np.allclose(eng.rot[1], olam, rtol=1e-9)
+        # k-means over the sharded base (fp64 sums all-reduced) == the oracle's k-means on the whole
+        # base (up to the summation order of the fp64 sums)
+        cent_s = sharded.kmeans_sharded(eng, None, lo, cfg.n, cfg.nlist, iters=3)
+        cent_o = O.kmeans(X, cfg.nlist, iters=3)
+        assert np.allclose(cent_s, cent_o, rtol=1e-6, atol=1e-6), "sharded k-means differs"
         # search on the shard + all-gather + merge == unsharded exact IVF (alpha = 0)
         mean, R, lam = O.fit_rotation(X)
         cent = O.kmeans(X, cfg.nlist, iters=2)
