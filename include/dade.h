@@ -183,6 +183,32 @@ dade_status dade_get_timing(dade_index* idx, float* ms3);
 dade_status dade_kmeans_partial(dade_index* idx, const float* X, int64_t n, int64_t id_base, int64_t n_total,
                                 int nlist, const float* centroids, double* sums, int64_t* counts);
 
+/* Sharded calibration: dade_calibrate's steps, each over this rank's shard, for a
+ * driver that combines them across ranks (paper_2404_16322_b200/sharded.py):
+ *   dade_calib_knn        exact K nearest rows of THIS shard for each calibration query (X: device
+ *                         raw rows of the shard), ids global (host nq x K int64), fp64 distances
+ *                         (host nq x K) — the caller merges the shards' lists by (dist, id) (R14);
+ *   dade_calib_negatives  Label-1 candidates of this shard (R15/R16: rows of the query's nprobe_neg
+ *                         probed lists, or the whole shard if 0, not among the GLOBAL knn_ids) with
+ *                         the n_neg smallest (SplitMix64(seed ^ (q << 32 | id)), id): keys / ids host
+ *                         nq x n_neg, counts host nq — the caller keeps the n_neg smallest overall;
+ *   dade_pair_features    P_d at every 16-dim prefix (fp64, from the stored rotated rows) for the
+ *                         pairs (pair_q, global pair_id) whose id lies in this shard, zero rows for
+ *                         the others: F host npairs x D/16 — the caller sums F over ranks;
+ *   dade_fit_calibration  the per-step logistic slope (R3) and sorted thresholds (R4) from the
+ *                         pairs' features, tau and labels y (0 = a K-NN, 1 = a negative); installs
+ *                         the calibration exactly as dade_calibrate does.
+ * dade_calibrate is these four steps on one shard. Errors: ARG, STATE, NONFINITE, CUDA. */
+dade_status dade_calib_knn(dade_index* idx, const float* X, const float* Qc, int nq, int K, int64_t* ids,
+                           double* dists);
+dade_status dade_calib_negatives(dade_index* idx, const float* Qc, int nq, int K, const int64_t* knn_ids,
+                                 int n_neg, int nprobe_neg, uint64_t seed, uint64_t* keys, int64_t* ids,
+                                 int32_t* counts);
+dade_status dade_pair_features(dade_index* idx, const float* Qc, int nq, int npairs, const int32_t* pair_q,
+                               const int64_t* pair_id, double* F);
+dade_status dade_fit_calibration(dade_index* idx, int K, int npairs, const double* F, const double* tau,
+                                 const double* y);
+
 /* Split search (multi-GPU query partitioning): dade_prepare runs a4 + a5 for a block
  * of queries — qrot (device nq x D fp32, q~ = R(q - mu)) and probes (device nq x nprobe int32,
  * exact, ordered by (dist, id)); dade_search_prepared runs a6-a8 on this index's shard for

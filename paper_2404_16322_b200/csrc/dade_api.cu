@@ -873,32 +873,30 @@ extern "C" dade_status dade_get_layout(const dade_index* x, float* Xrot) {
 }
 
 // ================================================================== a3 calibration
-extern "C" dade_status dade_calibrate(dade_index* x, const float* X, const float* Qc, int nq, int K,
-                                      int n_neg, int nprobe_neg, uint64_t seed) {
-  API_BEGIN
-  need(x, "index"); need(X, "X"); need(Qc, "Qc");
-  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "calibrate needs build_ivf first");
-  DADE_REQUIRE(nq >= 1, DADE_ERR_ARG, "nq < 1");
-  DADE_REQUIRE(K >= 1 && K <= x->n, DADE_ERR_ARG, "K not in [1, n]");
-  DADE_REQUIRE(K <= DADE_MAX_K, DADE_ERR_UNSUPPORTED, "K > DADE_MAX_K");
-  DADE_REQUIRE(n_neg >= 0, DADE_ERR_ARG, "n_neg < 0");
-  DADE_REQUIRE(nprobe_neg >= 0 && nprobe_neg <= x->nlist, DADE_ERR_ARG, "nprobe_neg not in [0, nlist]");
-  DeviceGuard g(x->device);
-  const int D = x->D;
-  const int64_t n = x->n;
-  cudaStream_t st = x->stream;
-  check_finite(x, Qc, (int64_t)nq * D, "Qc");
-  // exact KNN over the whole base (Label 0, tau_q) — P:L3930, R14
+// ---- calibration building blocks (single-GPU dade_calibrate and the sharded protocol share them)
+namespace {
+// exact K nearest rows of this index's base X (raw, id order) for every query, fp64 distances
+void calib_knn(dade_index* x, const float* X, const float* Qc, int nq, int K, std::vector<int64_t>& ids,
+               std::vector<double>& d) {
   DBuf<int32_t> knn_i;
   DBuf<double> knn_d;
   knn_i.reserve((size_t)nq * K);
   knn_d.reserve((size_t)nq * K);
-  exact_knn(x, Qc, nq, X, n, K, knn_i.p, knn_d.p);
+  exact_knn(x, Qc, nq, X, x->n, K, knn_i.p, knn_d.p);
   std::vector<int32_t> ki((size_t)nq * K);
-  std::vector<double> kd((size_t)nq * K);
-  DADE_CK(cudaMemcpyAsync(ki.data(), knn_i.p, sizeof(int32_t) * ki.size(), cudaMemcpyDeviceToHost, st));
-  DADE_CK(cudaMemcpyAsync(kd.data(), knn_d.p, sizeof(double) * kd.size(), cudaMemcpyDeviceToHost, st));
-  // probes for the negatives (R16)
+  d.resize((size_t)nq * K);
+  DADE_CK(cudaMemcpyAsync(ki.data(), knn_i.p, sizeof(int32_t) * ki.size(), cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaMemcpyAsync(d.data(), knn_d.p, sizeof(double) * d.size(), cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  ids.resize(ki.size());
+  for (size_t i = 0; i < ki.size(); ++i) ids[i] = x->id_base + ki[i];
+}
+
+// Label-1 candidates of this shard (R15/R16): the rows of the query's nprobe_neg probed lists (the
+// whole shard if 0 or flat) that are not among its K nearest (knn_ids: global ids, nq x K), the
+// n_neg smallest by (SplitMix64(seed ^ (q << 32 | id)), id). Outputs per query, ascending.
+void calib_negatives(dade_index* x, const float* Qc, int nq, int K, const int64_t* knn_ids, int n_neg,
+                     int nprobe_neg, uint64_t seed, std::vector<std::vector<std::pair<uint64_t, int64_t>>>& out) {
   const bool whole = nprobe_neg == 0 || x->nlist == 1;
   std::vector<int32_t> pr;
   if (!whole) {
@@ -906,30 +904,22 @@ extern "C" dade_status dade_calibrate(dade_index* x, const float* X, const float
     pd.reserve((size_t)nq * nprobe_neg);
     exact_knn(x, Qc, nq, x->cent.p, x->nlist, nprobe_neg, pd.p, nullptr, x->cent_tc);
     pr.resize((size_t)nq * nprobe_neg);
-    DADE_CK(cudaMemcpyAsync(pr.data(), pd.p, sizeof(int32_t) * pr.size(), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaMemcpyAsync(pr.data(), pd.p, sizeof(int32_t) * pr.size(), cudaMemcpyDeviceToHost, x->stream));
+    DADE_CK(cudaStreamSynchronize(x->stream));
   }
-  DADE_CK(cudaStreamSynchronize(st));
-  // pairs: Label 0 = the K NN, Label 1 = n_neg non-KNN candidates with the smallest hash
-  std::vector<int32_t> pq, prow;
-  std::vector<double> ptau, py;
+  out.assign(nq, {});
   std::vector<std::pair<uint64_t, int64_t>> cand;
   for (int qi = 0; qi < nq; ++qi) {
-    const double tau = kd[(size_t)qi * K + K - 1];
-    std::vector<int64_t> knn_ids(K);
-    for (int j = 0; j < K; ++j) {
-      const int32_t loc = ki[(size_t)qi * K + j];
-      knn_ids[j] = x->id_base + loc;
-      pq.push_back(qi); prow.push_back(x->pos_of_h[loc]); ptau.push_back(tau); py.push_back(0.0);
-    }
-    std::sort(knn_ids.begin(), knn_ids.end());
+    std::vector<int64_t> kn(knn_ids + (size_t)qi * K, knn_ids + (size_t)qi * K + K);
+    std::sort(kn.begin(), kn.end());
     cand.clear();
     auto consider = [&](int64_t id) {
-      if (std::binary_search(knn_ids.begin(), knn_ids.end(), id)) return;
+      if (std::binary_search(kn.begin(), kn.end(), id)) return;
       const uint64_t key = ((uint64_t)(uint32_t)qi << 32) | (uint64_t)id;
       cand.emplace_back(splitmix64(seed ^ key), id);
     };
     if (whole) {
-      for (int64_t i = 0; i < n; ++i) consider(x->id_base + i);
+      for (int64_t i = 0; i < x->n; ++i) consider(x->id_base + i);
     } else {
       for (int j = 0; j < nprobe_neg; ++j) {
         const int l = pr[(size_t)qi * nprobe_neg + j];
@@ -938,32 +928,49 @@ extern "C" dade_status dade_calibrate(dade_index* x, const float* X, const float
     }
     const size_t take = std::min<size_t>((size_t)n_neg, cand.size());
     std::partial_sort(cand.begin(), cand.begin() + take, cand.end());
-    for (size_t j = 0; j < take; ++j) {
-      pq.push_back(qi); prow.push_back(x->pos_of_h[cand[j].second - x->id_base]);
-      ptau.push_back(tau); py.push_back(1.0);
-    }
+    out[qi].assign(cand.begin(), cand.begin() + take);
   }
-  const int npairs = (int)pq.size();
-  const int nblk = D / 16;
-  // features P_d at every 16-dim prefix, from the rotated layout (fp64 accumulation)
+}
+
+// P_d at every 16-dim prefix for the pairs whose id lies in this shard (fp64 from the stored fp32
+// rotated rows); rows of other shards' pairs are zero. F: npairs x (D/16).
+void pair_features(dade_index* x, const float* Qc, int nq, int npairs, const int32_t* pq, const int64_t* pid,
+                   std::vector<double>& F) {
+  const int D = x->D, nblk = D / 16;
+  F.assign((size_t)npairs * nblk, 0.0);
+  std::vector<int32_t> q_own, row_own, which;
+  for (int i = 0; i < npairs; ++i) {
+    const int64_t loc = pid[i] - x->id_base;
+    if (loc < 0 || loc >= x->n) continue;
+    q_own.push_back(pq[i]); row_own.push_back(x->pos_of_h[loc]); which.push_back(i);
+  }
+  const int m = (int)which.size();
+  if (m == 0) return;
+  cudaStream_t st = x->stream;
   DBuf<float> qr;
   qr.reserve((size_t)nq * D);
   launch_rotate(Qc, nullptr, nq, D, x->R_d.p, x->mean_d.p, qr.p, nullptr, st);
   DBuf<int32_t> pq_d, pr_d;
   DBuf<double> feat;
-  pq_d.reserve(npairs); pr_d.reserve(npairs); feat.reserve((size_t)npairs * nblk);
-  DADE_CK(cudaMemcpyAsync(pq_d.p, pq.data(), sizeof(int32_t) * npairs, cudaMemcpyHostToDevice, st));
-  DADE_CK(cudaMemcpyAsync(pr_d.p, prow.data(), sizeof(int32_t) * npairs, cudaMemcpyHostToDevice, st));
-  launch_pair_prefix(x->layout.p, n, D, qr.p, pq_d.p, pr_d.p, npairs, feat.p, st);
-  std::vector<double> F((size_t)npairs * nblk);
-  DADE_CK(cudaMemcpyAsync(F.data(), feat.p, sizeof(double) * F.size(), cudaMemcpyDeviceToHost, st));
+  pq_d.reserve(m); pr_d.reserve(m); feat.reserve((size_t)m * nblk);
+  DADE_CK(cudaMemcpyAsync(pq_d.p, q_own.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(pr_d.p, row_own.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+  launch_pair_prefix(x->layout.p, x->n, D, qr.p, pq_d.p, pr_d.p, m, feat.p, st);
+  std::vector<double> Fm((size_t)m * nblk);
+  DADE_CK(cudaMemcpyAsync(Fm.data(), feat.p, sizeof(double) * Fm.size(), cudaMemcpyDeviceToHost, st));
   DADE_CK(cudaStreamSynchronize(st));
-  // per-step logistic slope (R3) and sorted thresholds (R4)
-  const int ncls = nblk - 1;
+  for (int i = 0; i < m; ++i)
+    std::copy(Fm.begin() + (size_t)i * nblk, Fm.begin() + (size_t)(i + 1) * nblk, F.begin() + (size_t)which[i] * nblk);
+}
+
+// per-step logistic slope (R3) and sorted thresholds v_d = sort_desc(tau - m1 P_d) over Label 0 (R4)
+void fit_calibration(dade_index* x, int K, int npairs, const double* F, const double* ptau_, const double* py_) {
+  const int nblk = x->D / 16, ncls = nblk - 1;
+  std::vector<double> ptau(ptau_, ptau_ + npairs), py(py_, py_ + npairs);
   int n0 = 0;
   for (double y : py) n0 += y == 0.0;
-  std::vector<double> m1(ncls, 1.0), v((size_t)ncls * n0);
-  std::vector<double> P(npairs);
+  DADE_REQUIRE(n0 >= 1, DADE_ERR_ARG, "calibration needs Label-0 pairs");
+  std::vector<double> m1(ncls, 1.0), v((size_t)ncls * n0), P(npairs);
   for (int s = 0; s < ncls; ++s) {
     for (int i = 0; i < npairs; ++i) P[i] = F[(size_t)i * nblk + s];
     double m, b;
@@ -982,6 +989,101 @@ extern "C" dade_status dade_calibrate(dade_index* x, const float* X, const float
   x->n0 = n0;
   x->ncls = ncls;
   x->has_cal = true;
+}
+
+void calib_checks(dade_index* x, const float* Qc, int nq, int K, int n_neg, int nprobe_neg) {
+  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "calibrate needs build_ivf first");
+  DADE_REQUIRE(nq >= 1, DADE_ERR_ARG, "nq < 1");
+  DADE_REQUIRE(K >= 1 && K <= DADE_MAX_K, DADE_ERR_ARG, "K not in [1, DADE_MAX_K]");
+  DADE_REQUIRE(n_neg >= 0, DADE_ERR_ARG, "n_neg < 0");
+  DADE_REQUIRE(nprobe_neg >= 0 && nprobe_neg <= x->nlist, DADE_ERR_ARG, "nprobe_neg not in [0, nlist]");
+  check_finite(x, Qc, (int64_t)nq * x->D, "Qc");
+}
+}  // namespace
+
+extern "C" dade_status dade_calibrate(dade_index* x, const float* X, const float* Qc, int nq, int K,
+                                      int n_neg, int nprobe_neg, uint64_t seed) {
+  API_BEGIN
+  need(x, "index"); need(X, "X"); need(Qc, "Qc");
+  DeviceGuard g(x->device);
+  calib_checks(x, Qc, nq, K, n_neg, nprobe_neg);
+  DADE_REQUIRE(K <= x->n, DADE_ERR_ARG, "K not in [1, n]");
+  // exact KNN over the whole base (Label 0, tau_q) — P:L3930, R14
+  std::vector<int64_t> ki;
+  std::vector<double> kd;
+  calib_knn(x, X, Qc, nq, K, ki, kd);
+  // Label 1 = n_neg non-KNN candidates with the smallest hash (R15, R16)
+  std::vector<std::vector<std::pair<uint64_t, int64_t>>> neg;
+  calib_negatives(x, Qc, nq, K, ki.data(), n_neg, nprobe_neg, seed, neg);
+  std::vector<int32_t> pq;
+  std::vector<int64_t> pid;
+  std::vector<double> ptau, py;
+  for (int qi = 0; qi < nq; ++qi) {
+    const double tau = kd[(size_t)qi * K + K - 1];
+    for (int j = 0; j < K; ++j) { pq.push_back(qi); pid.push_back(ki[(size_t)qi * K + j]); ptau.push_back(tau); py.push_back(0.0); }
+    for (const auto& c : neg[qi]) { pq.push_back(qi); pid.push_back(c.second); ptau.push_back(tau); py.push_back(1.0); }
+  }
+  std::vector<double> F;
+  pair_features(x, Qc, nq, (int)pq.size(), pq.data(), pid.data(), F);
+  fit_calibration(x, K, (int)pq.size(), F.data(), ptau.data(), py.data());
+  API_END
+}
+
+// ---- sharded calibration: the same steps split across ranks (sharded.py)
+extern "C" dade_status dade_calib_knn(dade_index* x, const float* X, const float* Qc, int nq, int K,
+                                      int64_t* ids, double* dists) {
+  API_BEGIN
+  need(x, "index"); need(X, "X"); need(Qc, "Qc"); need(ids, "ids"); need(dists, "dists");
+  DeviceGuard g(x->device);
+  calib_checks(x, Qc, nq, K, 0, 0);
+  DADE_REQUIRE(K <= x->n, DADE_ERR_ARG, "K > shard size");
+  std::vector<int64_t> ki;
+  std::vector<double> kd;
+  calib_knn(x, X, Qc, nq, K, ki, kd);
+  std::copy(ki.begin(), ki.end(), ids);
+  std::copy(kd.begin(), kd.end(), dists);
+  API_END
+}
+
+extern "C" dade_status dade_calib_negatives(dade_index* x, const float* Qc, int nq, int K, const int64_t* knn_ids,
+                                            int n_neg, int nprobe_neg, uint64_t seed, uint64_t* keys, int64_t* ids,
+                                            int32_t* counts) {
+  API_BEGIN
+  need(x, "index"); need(Qc, "Qc"); need(knn_ids, "knn_ids"); need(counts, "counts");
+  if (n_neg > 0) { need(keys, "keys"); need(ids, "ids"); }
+  DeviceGuard g(x->device);
+  calib_checks(x, Qc, nq, K, n_neg, nprobe_neg);
+  std::vector<std::vector<std::pair<uint64_t, int64_t>>> neg;
+  calib_negatives(x, Qc, nq, K, knn_ids, n_neg, nprobe_neg, seed, neg);
+  for (int qi = 0; qi < nq; ++qi) {
+    counts[qi] = (int32_t)neg[qi].size();
+    for (size_t j = 0; j < neg[qi].size(); ++j) {
+      keys[(size_t)qi * n_neg + j] = neg[qi][j].first;
+      ids[(size_t)qi * n_neg + j] = neg[qi][j].second;
+    }
+  }
+  API_END
+}
+
+extern "C" dade_status dade_pair_features(dade_index* x, const float* Qc, int nq, int npairs, const int32_t* pair_q,
+                                          const int64_t* pair_id, double* F) {
+  API_BEGIN
+  need(x, "index"); need(Qc, "Qc"); need(F, "F");
+  if (npairs > 0) { need(pair_q, "pair_q"); need(pair_id, "pair_id"); }
+  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "pair features need build_ivf first");
+  DeviceGuard g(x->device);
+  std::vector<double> Fv;
+  pair_features(x, Qc, nq, npairs, pair_q, pair_id, Fv);
+  std::copy(Fv.begin(), Fv.end(), F);
+  API_END
+}
+
+extern "C" dade_status dade_fit_calibration(dade_index* x, int K, int npairs, const double* F, const double* tau,
+                                            const double* y) {
+  API_BEGIN
+  need(x, "index"); need(F, "F"); need(tau, "tau"); need(y, "y");
+  DADE_REQUIRE(K >= 1 && K <= DADE_MAX_K && npairs >= 1, DADE_ERR_ARG, "bad K / npairs");
+  fit_calibration(x, K, npairs, F, tau, y);
   API_END
 }
 

@@ -693,6 +693,8 @@ static void launch_k(const ScanParams& p, cudaStream_t st) {
       case 2: launch_v<DD, KPL, 1, 72, true>(p, st); return;
       case 3: launch_v<DD, KPL, 1, 72>(p, st); return;
       case 4: launch_v<DD, KPL, 1, 64>(p, st); return;
+      case 5: launch_v<DD, KPL, 1, 96>(p, st); return;
+      case 6: launch_v<DD, KPL, 1, 88>(p, st); return;
       default: break;
     }
   }

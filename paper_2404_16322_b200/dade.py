@@ -63,6 +63,10 @@ _SIGS = {
     "dade_search_method": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
     "dade_prepare": [P, P, I32, I32, P, P],
     "dade_kmeans_partial": [P, P, I64, I64, I64, I32, P, P, P],
+    "dade_calib_knn": [P, P, P, I32, I32, P, P],
+    "dade_calib_negatives": [P, P, I32, I32, P, I32, I32, C.c_uint64, P, P, P],
+    "dade_pair_features": [P, P, I32, I32, P, P, P],
+    "dade_fit_calibration": [P, I32, I32, P, P, P],
     "dade_set_timing": [P, I32],
     "dade_get_timing": [P, P],
     "dade_search_prepared": [P, P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
@@ -258,6 +262,39 @@ class Index:
         _ck(lib().dade_kmeans_partial(self.h, _ptr(X), X.shape[0], id_base, n_total, nlist,
                                       None if c is None else _ptr(c), _ptr(sums), _ptr(counts)))
         return sums, counts
+
+    # ---- sharded calibration steps (sharded.calibrate_sharded combines them across ranks)
+    def calib_knn(self, X, Qc, K: int):
+        import torch
+        X = _dev(X, torch.float32); Qc = _dev(Qc, torch.float32)
+        nq = Qc.shape[0]
+        ids = np.zeros((nq, K), np.int64); d = np.zeros((nq, K))
+        _ck(lib().dade_calib_knn(self.h, _ptr(X), _ptr(Qc), nq, K, _ptr(ids), _ptr(d)))
+        return ids, d
+
+    def calib_negatives(self, Qc, K: int, knn_ids, n_neg: int, nprobe_neg: int, seed: int):
+        import torch
+        Qc = _dev(Qc, torch.float32)
+        nq = Qc.shape[0]
+        knn = np.ascontiguousarray(knn_ids, np.int64)
+        keys = np.zeros((nq, max(n_neg, 1)), np.uint64); ids = np.zeros((nq, max(n_neg, 1)), np.int64)
+        cnt = np.zeros(nq, np.int32)
+        _ck(lib().dade_calib_negatives(self.h, _ptr(Qc), nq, K, _ptr(knn), n_neg, nprobe_neg, seed, _ptr(keys),
+                                       _ptr(ids), _ptr(cnt)))
+        return keys, ids, cnt
+
+    def pair_features(self, Qc, pair_q, pair_id):
+        import torch
+        Qc = _dev(Qc, torch.float32)
+        pq = np.ascontiguousarray(pair_q, np.int32); pid = np.ascontiguousarray(pair_id, np.int64)
+        F = np.zeros((len(pq), self.D // 16))
+        _ck(lib().dade_pair_features(self.h, _ptr(Qc), Qc.shape[0], len(pq), _ptr(pq), _ptr(pid), _ptr(F)))
+        return F
+
+    def fit_calibration(self, K: int, F, tau, y):
+        F = np.ascontiguousarray(F, np.float64); tau = np.ascontiguousarray(tau, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        _ck(lib().dade_fit_calibration(self.h, K, len(tau), _ptr(F), _ptr(tau), _ptr(y)))
 
     def set_timing(self, on: bool):
         """Record stage events on every search (no synchronisation); read them with get_timing."""

@@ -77,6 +77,66 @@ def kmeans_sharded(engine, X_shard, id_base: int, n_total: int, nlist: int, iter
     return cent
 
 
+def _gather_np(a, group=None):
+    """All-gather a host numpy array (same shape on every rank) -> [world, ...] numpy."""
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    return _all_gather(t, group).cpu().numpy()
+
+
+def merge_knn_lists(ids_g, d_g, K: int):
+    """[S, nq, K] per-shard K-NN lists (global ids, fp64 dists) -> the global K-NN by (dist, id)."""
+    S, nq, _ = ids_g.shape
+    knn_ids, knn_d = np.zeros((nq, K), np.int64), np.zeros((nq, K))
+    for q in range(nq):
+        ci, cd = ids_g[:, q, :].ravel(), d_g[:, q, :].ravel()
+        o = np.lexsort((ci, cd))[:K]
+        knn_ids[q], knn_d[q] = ci[o], cd[o]
+    return knn_ids, knn_d
+
+
+def calibration_pairs(knn_ids, knn_d, keys_g, nids_g, cnt_g, n_neg: int):
+    """The calibration pairs in dade_calibrate's order: per query its K nearest (Label 0, in (dist,
+    id) order) then the n_neg smallest (hash, id) negatives over all shards (Label 1); tau = the
+    query's K-th distance. keys_g / nids_g: [S, nq, n_neg], cnt_g: [S, nq]."""
+    nq, K = knn_ids.shape
+    pq, pid, tau, y = [], [], [], []
+    for q in range(nq):
+        t = knn_d[q, K - 1]
+        pq += [q] * K; pid += knn_ids[q].tolist(); tau += [t] * K; y += [0.0] * K
+        kk = np.concatenate([keys_g[s, q, :cnt_g[s, q]] for s in range(keys_g.shape[0])]).astype(np.uint64)
+        ii = np.concatenate([nids_g[s, q, :cnt_g[s, q]] for s in range(keys_g.shape[0])])
+        o = np.lexsort((ii, kk))[:n_neg]
+        pq += [q] * len(o); pid += ii[o].tolist(); tau += [t] * len(o); y += [1.0] * len(o)
+    return np.array(pq, np.int32), np.array(pid, np.int64), np.array(tau), np.array(y)
+
+
+def calibrate_sharded(engine, X_shard, Qc, K: int, n_neg: int = 50, nprobe_neg: int = 0, seed: int = 0,
+                      group=None):
+    """dade_calibrate over a sharded base: every rank runs each step on its shard
+    and the steps are combined exactly as the single-GPU calibration defines them — the K nearest
+    neighbours are the shards' lists merged by (fp64 dist, id) (R14), the negatives the n_neg
+    smallest (hash, id) over the shards' candidates (R15/R16), the pair features P_d (held by the
+    rank owning the row) summed over ranks — so the installed table equals an unsharded
+    dade_calibrate on the same base, centroids and rotation."""
+    import torch
+    import torch.distributed as dist
+    ids_l, d_l = engine.calib_knn(X_shard, Qc, K)
+    knn_ids, knn_d = merge_knn_lists(_gather_np(ids_l, group), _gather_np(d_l, group), K)
+    keys_l, nids_l, cnt_l = engine.calib_negatives(Qc, K, knn_ids, n_neg, nprobe_neg, seed)
+    keys_g = _gather_np(keys_l.view(np.int64), group).view(np.uint64)
+    pq, pid, tau, y = calibration_pairs(knn_ids, knn_d, keys_g, _gather_np(nids_l, group),
+                                        _gather_np(cnt_l, group), n_neg)
+    t = torch.from_numpy(engine.pair_features(Qc, pq, pid))
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, group=group)
+    engine.fit_calibration(K, t.cpu().numpy(), tau, y)
+
+
 class ShardedSearch:
     """search() on this rank's shard, then all-gather of the local top-K and the merge (a9)."""
 
