@@ -132,57 +132,55 @@ def run_dade(args):
     if args.nq:
         cfg = cfg.scaled(nq=args.nq)
     t0 = time.time()
+    lo, hi = rank * cfg.n // world, (rank + 1) * cfg.n // world  # == sharded.shard_range
     m = synth.model(cfg)
-    X = synth.base(cfg, m)
+    # every rank generates and holds only its own shard of the base (rows [lo, hi))
+    X = synth.base(cfg, m, rows=slice(lo, hi), workers=min(16, max(1, (os.cpu_count() or 1) // world)))
     Q = synth.queries(cfg, m=m)
     Qc = synth.cal_queries(cfg, m=m)
-    log(f"[rank {rank}] data {cfg.name} n={cfg.n} D={cfg.d} nq={cfg.nq} in {time.time() - t0:.1f}s")
+    log(f"[rank {rank}] data {cfg.name} n={cfg.n} (rows {lo}:{hi}) D={cfg.d} nq={cfg.nq} in {time.time() - t0:.1f}s")
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     Xd = torch.from_numpy(X).to(dev)
+    del X
     Qd = torch.from_numpy(Q).to(dev)
     Qcd = torch.from_numpy(Qc).to(dev)
     K, dd = cfg.k, cfg.delta_d
-    lo, hi = rank * cfg.n // world, (rank + 1) * cfg.n // world  # == sharded.shard_range
 
-    # ---- build (replicated artefacts are deterministic: identical on every rank)
+    # ---- build. N > 1: every step runs over the sharded base and combines partial results exactly
+    # (SURVEY §8(e)); the replicated artefacts (mu, R, centroids, calibration table) come out
+    # identical on every rank and equal to the single-GPU build's.
     t0 = time.time()
-    full = Index(cfg.d, local, stream)
-    if world > 1:  # a0 over the sharded base: fp64 partial moments + NCCL all-reduce
-        sharded.fit_rotation_sharded(full, Xd[lo:hi].contiguous(), lo, cfg.n)
+    ix = Index(cfg.d, local, stream)
+    if world > 1:  # a0: fp64 partial moments + all-reduce
+        sharded.fit_rotation_sharded(ix, Xd, lo, cfg.n)
     else:
-        full.fit_rotation(Xd)
+        ix.fit_rotation(Xd)
     if args.method == "adsampling":  # ADSampling's projection: a Haar-random orthogonal matrix
-        mean, _, lam = full.get_rotation()
-        full.set_rotation(mean, synth.haar_basis(cfg.d, np.random.default_rng(12345)).T.copy(), lam)
+        mean, _, lam = ix.get_rotation()
+        ix.set_rotation(mean, synth.haar_basis(cfg.d, np.random.default_rng(12345)).T.copy(), lam)
     torch.cuda.synchronize()
     t_rot = time.time() - t0
-    if world > 1:  # k-means over the sharded base: fp64 sums / counts all-reduced
-        cent = sharded.kmeans_sharded(full, Xd[lo:hi].contiguous(), lo, cfg.n, cfg.nlist, iters=10)
-        full.build_ivf(Xd, cfg.nlist, centroids=torch.from_numpy(cent).to(dev))
+    if world > 1:  # k-means: fp64 per-centroid sums / counts all-reduced; then the local IVF
+        cent = sharded.kmeans_sharded(ix, Xd, lo, cfg.n, cfg.nlist, iters=10)
+        ix.build_ivf(Xd, cfg.nlist, centroids=torch.from_numpy(cent).to(dev), id_base=lo)
     else:
-        full.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
+        ix.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
     torch.cuda.synchronize()
     t_ivf = time.time() - t0 - t_rot
     if args.method == "bsa_p":
-        full.calibrate(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
+        if world > 1:  # R14-R16 over the shards: merged K-NN, merged negatives, summed P_d
+            sharded.calibrate_sharded(ix, Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
+        else:
+            ix.calibrate(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
     torch.cuda.synchronize()
     t_cal = time.time() - t0 - t_rot - t_ivf
     log(f"[rank {rank}] build: rotation {t_rot:.2f}s ivf {t_ivf:.2f}s calibration {t_cal:.2f}s")
-    gt_i, _ = full.bruteforce_knn(Xd, Qd, K)
-    gt = gt_i.cpu().numpy()
+    # ground truth for recall: exact K-NN on each shard, all-gathered and merged (untimed)
+    gt_i, gt_d = ix.bruteforce_knn(Xd, Qd, K, id_base=lo)
     if world > 1:
-        mean, R, lam = full.get_rotation()
-        _, _, _, cent = full.get_ivf()
-        cal = full.get_calibration() if args.method == "bsa_p" else None
-        full.close()
-        ix = Index(cfg.d, local, stream)
-        ix.set_rotation(mean, R, lam)
-        ix.build_ivf(Xd[lo:hi].contiguous(), cfg.nlist, centroids=torch.from_numpy(cent).to(dev), id_base=lo)
-        if args.method == "bsa_p":
-            ix.set_calibration(K, cal["m1"], cal["v"])
-    else:
-        ix = full
+        gt_i, _ = ix.merge_topk(sharded._all_gather(gt_i), sharded._all_gather(gt_d))
+    gt = gt_i.cpu().numpy()
     del Xd
     torch.cuda.empty_cache()
 
@@ -479,7 +477,8 @@ def main():
                     help="per-step correction: the paper's data-driven BSA-p (default, the headline), or the "
                          "NEXT-1 comparisons ADSampling (eps0 = 2.1, random rotation) / BSA-res (m = 8)")
     ap.add_argument("--nprobe", type=int, default=0, help="fix nprobe instead of sweeping to recall 0.95")
-    ap.add_argument("--n", type=int, default=0, help="override base size (testing only)")
+    ap.add_argument("--n", "--base-n", dest="n", type=int, default=0,
+                    help="override base size (testing only; use --base-n under torchrun)")
     ap.add_argument("--nlist", type=int, default=0)
     ap.add_argument("--nq", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -221,7 +221,13 @@ dade_status dade_search_prepared(dade_index* idx, const float* qrot, const int32
                                  float* dists, dade_stats* stats);
 
 /* Same as dade_search with HOST Q/ids/dists: the H2D copy of Q and the D2H copy of the results
- * are part of the call (synchronous). Used for the end-to-end (e2e) measurement. */
+ * are part of the call (synchronous; returns when ids/dists are written). The copies run on two
+ * copy streams; with DADE_HOST_CHUNKS=c (default 1) the batch is cut into c chunks pipelined so
+ * that chunk c's H2D overlaps the search of chunk c-1 and its D2H the search of chunk c+1 (not
+ * the default: measured slower on C2). Each query's result is independent of
+ * the chunking. Pinned host memory gives asynchronous copies;
+ * pageable memory works but serialises them. With stats != NULL the batch runs unchunked.
+ * Used for the end-to-end (e2e) measurement. Errors: as dade_search. */
 dade_status dade_search_host(dade_index* idx, const float* Q_host, int nq, int K, int nprobe,
                              int delta_d, double significance, int64_t* ids_host, float* dists_host,
                              dade_stats* stats);

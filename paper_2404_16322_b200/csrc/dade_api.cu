@@ -62,6 +62,9 @@ struct dade_index {
   // a4 (rotation) runs on a side stream concurrently with a5 (probe): fork/join events
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // dade_search_host: copy streams and per-chunk events of the H2D / search / D2H pipeline
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> hev;
 };
 
 // ------------------------------------------------------------------ error plumbing
@@ -335,6 +338,15 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
 
 // qrot_in / probes_in (device, optional): queries already rotated and probed (dade_prepare, e.g.
 // on another rank) — only the scan runs.
+// dade_search_host's pipeline depth. Default 1: on C2 (tools/e2e_breakdown.py) a search cut in
+// two costs 0.19 ms more on the device (the scan's per-launch tail: 0.36 ms at 5,000 queries vs
+// 0.55 ms at 10,000) while the H2D it could hide is 0.20 ms, so chunking does not pay at these
+// batch sizes. DADE_HOST_CHUNKS=c sets c chunks.
+int host_chunks(int nq) {
+  if (const char* e = getenv("DADE_HOST_CHUNKS")) return std::max(1, std::min(atoi(e), std::max(nq, 1)));
+  return 1;
+}
+
 void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d, double alpha,
                int64_t* ids, float* dists, dade_stats* stats, int method = DADE_METHOD_BSA_P,
                const float* qrot_in = nullptr, const int32_t* probes_in = nullptr) {
@@ -504,6 +516,12 @@ extern "C" dade_status dade_destroy(dade_index* x) {
     cudaEventDestroy(x->fork);
     cudaEventDestroy(x->join);
   }
+  for (cudaStream_t s2 : {x->h2d, x->d2h})
+    if (s2) {
+      cudaStreamSynchronize(s2);
+      cudaStreamDestroy(s2);
+    }
+  for (auto e : x->hev) cudaEventDestroy(e);
   delete x;
   API_END
 }
@@ -1191,10 +1209,43 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   x->qbuf.reserve((size_t)std::max(nq, 1) * D);
   x->ids_tmp.reserve((size_t)std::max(nq, 1) * K);
   x->dists_tmp.reserve((size_t)std::max(nq, 1) * K);
-  DADE_CK(cudaMemcpyAsync(x->qbuf.p, Qh, sizeof(float) * nq * D, cudaMemcpyHostToDevice, st));
-  do_search(x, x->qbuf.p, nq, K, nprobe, delta_d, significance, x->ids_tmp.p, x->dists_tmp.p, stats);
-  DADE_CK(cudaMemcpyAsync(ids_h, x->ids_tmp.p, sizeof(int64_t) * nq * K, cudaMemcpyDeviceToHost, st));
-  DADE_CK(cudaMemcpyAsync(dists_h, x->dists_tmp.p, sizeof(float) * nq * K, cudaMemcpyDeviceToHost, st));
+  // Pipeline: the batch is cut into chunks; chunk c's H2D (copy stream) overlaps the search of
+  // chunk c-1 (library stream), whose results' D2H (second copy stream) overlaps chunk c's search.
+  // Stats need one search over the whole batch, so they run unchunked.
+  int nch = host_chunks(nq);
+  if (stats || nq <= 0) nch = 1;
+  if (!x->h2d) {
+    DADE_CK(cudaStreamCreateWithFlags(&x->h2d, cudaStreamNonBlocking));
+    DADE_CK(cudaStreamCreateWithFlags(&x->d2h, cudaStreamNonBlocking));
+  }
+  while ((int)x->hev.size() < 2 * nch + 1) {
+    cudaEvent_t e;
+    DADE_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    x->hev.push_back(e);
+  }
+  DADE_CK(cudaEventRecord(x->hev[0], st));  // the copies start after earlier work on the stream
+  DADE_CK(cudaStreamWaitEvent(x->h2d, x->hev[0], 0));
+  DADE_CK(cudaStreamWaitEvent(x->d2h, x->hev[0], 0));
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = (int)((int64_t)nq * c / nch), q1 = (int)((int64_t)nq * (c + 1) / nch);
+    DADE_CK(cudaMemcpyAsync(x->qbuf.p + (size_t)q0 * D, Qh + (size_t)q0 * D, sizeof(float) * (q1 - q0) * D,
+                            cudaMemcpyHostToDevice, x->h2d));
+    DADE_CK(cudaEventRecord(x->hev[1 + 2 * c], x->h2d));
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = (int)((int64_t)nq * c / nch), q1 = (int)((int64_t)nq * (c + 1) / nch);
+    DADE_CK(cudaStreamWaitEvent(st, x->hev[1 + 2 * c], 0));
+    do_search(x, x->qbuf.p + (size_t)q0 * D, q1 - q0, K, nprobe, delta_d, significance,
+              x->ids_tmp.p + (size_t)q0 * K, x->dists_tmp.p + (size_t)q0 * K, stats);
+    DADE_CK(cudaEventRecord(x->hev[2 + 2 * c], st));
+    DADE_CK(cudaStreamWaitEvent(x->d2h, x->hev[2 + 2 * c], 0));
+    DADE_CK(cudaMemcpyAsync(ids_h + (size_t)q0 * K, x->ids_tmp.p + (size_t)q0 * K, sizeof(int64_t) * (q1 - q0) * K,
+                            cudaMemcpyDeviceToHost, x->d2h));
+    DADE_CK(cudaMemcpyAsync(dists_h + (size_t)q0 * K, x->dists_tmp.p + (size_t)q0 * K,
+                            sizeof(float) * (q1 - q0) * K, cudaMemcpyDeviceToHost, x->d2h));
+  }
+  DADE_CK(cudaEventRecord(x->hev[0], x->d2h));  // the library stream resumes after the last D2H
+  DADE_CK(cudaStreamWaitEvent(st, x->hev[0], 0));
   DADE_CK(cudaStreamSynchronize(st));
   check_knn_flag(x);
   API_END
