@@ -232,6 +232,22 @@ dade_status dade_search_host(dade_index* idx, const float* Q_host, int nq, int K
                              int delta_d, double significance, int64_t* ids_host, float* dists_host,
                              dade_stats* stats);
 
+/* NEXT-2, Exp-7 / Table III: standalone approximation accuracy. A flat scan of the
+ * whole index in which each row's distance is ESTIMATED from its first d rotated dimensions
+ * (R27): DADE_EST_PARTIAL  est = P_d = ||x~_{:d} - q~_{:d}||^2 (the table's "PCA" column in the
+ * PCA basis; its "Rand" column after dade_set_rotation with a random orthogonal R before
+ * dade_build_ivf); DADE_EST_RESIDUAL  est = P_d + ||x~_r||^2 + ||q~_r||^2, the BSA-res estimate
+ * of Eq. 2 without the per-query m*sigma margin, which does not change the
+ * ranking. Returns, per query, the K rows with the smallest estimate, ordered by (fp32 est, id):
+ * ids[nq*K] int64 (global ids), est[nq*K] fp32, device. Q: device nq x D fp32 (raw).
+ * fp32 arithmetic with the scan's block association (R21); the residual estimate is clamped
+ * at 0. Errors: STATE (no IVF / rotation), ARG (d not a multiple of 16 in [16, D], K not in
+ * [1, min(n, DADE_MAX_K)], unknown estimator, NULL), NONFINITE, UNSUPPORTED (n >= 2^31). */
+#define DADE_EST_PARTIAL 0
+#define DADE_EST_RESIDUAL 1
+dade_status dade_estimate_knn(dade_index* idx, const float* Q, int nq, int d, int method, int K, int64_t* ids,
+                              float* est);
+
 /* Exact probes (a5 alone): probes[nq*nprobe] int32 device, ordered by (exact fp64 dist, id). */
 dade_status dade_probe(dade_index* idx, const float* Q, int nq, int nprobe, int32_t* probes);
 

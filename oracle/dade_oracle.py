@@ -479,3 +479,37 @@ def recall_at_k(found: np.ndarray, truth: np.ndarray, K: int) -> float:
     for f, g in zip(found, truth):
         tot += len(set(f[:K].tolist()) & set(g[:K].tolist()))
     return tot / (K * len(found))
+
+
+# ----------------------------------------------------------------------------- NEXT-2 Exp-7
+def estimate_dists(Xr: np.ndarray, q_rot: np.ndarray, d: int, estimator: str = "partial") -> np.ndarray:
+    """Exp-7 / Table III's estimates of every row's squared distance from its first d rotated
+    dims (R27). "partial": P_d = Σ_{i<d} (x_i − q_i)² — the "PCA" column in the
+    PCA basis, the "Rand" column in a random orthogonal basis (its (D/d) JL scale, is
+    a constant factor and does not change the ranking). "residual": the BSA-res estimate of Eq. 2
+    (P:L289-297), dis'_d = P_d + ‖x_r‖² + ‖q_r‖² with x_r, q_r the dims i ≥ d — the exact distance
+    minus the dropped cross term −2⟨q_r, x_r⟩ (Eq. 3's m·σ margin is per query: no effect on a
+    ranking). fp64."""
+    Xr = np.asarray(Xr, F64)
+    q = np.asarray(q_rot, F64)
+    e = np.sum((Xr[:, :d] - q[:d]) ** 2, axis=1)
+    if estimator == "residual":
+        e = e + np.sum(Xr[:, d:] ** 2, axis=1) + float(np.sum(q[d:] ** 2))
+    elif estimator != "partial":
+        raise ValueError(estimator)
+    return e
+
+
+def estimate_knn(index, Q: np.ndarray, d: int, K: int, estimator: str = "partial"):
+    """Flat scan by the d-dim estimate (Exp-7): per query the K rows with the smallest estimate,
+    (estimate, id) order (R12). Uses the index's rotation and fp64 rotated base."""
+    Q = np.atleast_2d(Q)
+    Qr = rotate(Q, index["mean"], index["R"])
+    gid = np.arange(index["Xr"].shape[0], dtype=np.int64) + index["id_base"]
+    ids = np.empty((Q.shape[0], K), dtype=np.int64)
+    est = np.empty((Q.shape[0], K), dtype=F64)
+    for i, q in enumerate(Qr):
+        e = estimate_dists(index["Xr"], q, d, estimator)
+        o = order_by_dist_id(e, gid)[:K]
+        ids[i], est[i] = gid[o], e[o]
+    return ids, est

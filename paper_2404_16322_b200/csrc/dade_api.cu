@@ -1251,6 +1251,35 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   API_END
 }
 
+// NEXT-2: Exp-7 / Table III standalone approximation accuracy (flat scan by a d-dim estimate)
+extern "C" dade_status dade_estimate_knn(dade_index* x, const float* Q, int nq, int d, int method, int K,
+                                         int64_t* ids, float* est) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "estimate before build_ivf");
+  DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
+  DADE_REQUIRE(d >= 16 && d % 16 == 0 && d <= x->D, DADE_ERR_ARG, "d must be a positive multiple of 16, <= D");
+  DADE_REQUIRE(K >= 1 && K <= DADE_MAX_K && K <= x->n, DADE_ERR_ARG, "K not in [1, min(n, DADE_MAX_K)]");
+  DADE_REQUIRE(method == DADE_EST_PARTIAL || method == DADE_EST_RESIDUAL, DADE_ERR_ARG, "unknown estimator");
+  DADE_REQUIRE(x->n < ((int64_t)1 << 31), DADE_ERR_UNSUPPORTED, "n >= 2^31");
+  if (nq == 0) { g_err.clear(); return DADE_OK; }
+  need(Q, "Q"); need(ids, "ids"); need(est, "est");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  check_finite(x, Q, (int64_t)nq * D, "Q");
+  x->qrot.reserve((size_t)nq * D);
+  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
+  if (method == DADE_EST_RESIDUAL && !x->xnorm_ok) {
+    x->xnorm.reserve((size_t)std::max<int64_t>(x->n, 1));
+    launch_row_norms(x->layout.p, x->n, D, x->xnorm.p, st);
+    x->xnorm_ok = true;
+  }
+  launch_estimate_topk(x->layout.p, x->row_id_d.p, method == DADE_EST_RESIDUAL ? x->xnorm.p : nullptr, x->n, D, d,
+                       x->qrot.p, nq, K, est, ids, st);
+  API_END
+}
+
 extern "C" dade_status dade_probe(dade_index* x, const float* Q, int nq, int nprobe, int32_t* probes) {
   API_BEGIN
   need(x, "index"); need(Q, "Q"); need(probes, "probes");

@@ -150,6 +150,11 @@ struct ScanParams {
 void launch_scan(const ScanParams& p, cudaStream_t st);
 // ‖x~‖² of every list-major row of the blocked layout (fp64 sums, stored fp32)
 void launch_row_norms(const float* layout, int64_t n, int D, float* out, cudaStream_t st);
+// estimate.cu (NEXT-2, Exp-7): top-K by the d-dim estimate over the whole layout; xnorm != null
+// adds the residual terms ||x_r||^2 + ||q_r||^2 (Eq. 2)
+#define DADE_EST_MAX_D 4096
+void launch_estimate_topk(const float* layout, const int32_t* row_id, const float* xnorm, int64_t n, int D, int d,
+                          const float* qrot, int nq, int K, float* est, int64_t* ids, cudaStream_t st);
 // BSA-res per-step query constants c_s = sum_{i>=d} q_i^2 - m sqrt(4 sum_{i>=d} q_i^2 lam_i), d = s*delta_d
 void launch_res_consts(const float* qrot, int nq, int D, int delta_d, const double* lam, double m,
                        float* out, cudaStream_t st);

@@ -154,6 +154,16 @@ __device__ __forceinline__ void ld_block(unsigned long long (&x)[8], const float
   }
 }
 
+// lanes per survivor in a draining gather round (log2): 32 / qn rounded down to a power of two,
+// at most DADE_DRAIN_LG (the profile build's knob; 5 = up to 32 lanes)
+#ifndef DADE_DRAIN_LG
+#define DADE_DRAIN_LG 5
+#endif
+__device__ __forceinline__ int drain_lanes_log2(int qn) {
+  const int lg = qn <= 1 ? 5 : qn <= 2 ? 4 : qn <= 4 ? 3 : qn <= 8 ? 2 : qn <= 16 ? 1 : 0;
+  return lg < DADE_DRAIN_LG ? lg : DADE_DRAIN_LG;
+}
+
 __device__ __forceinline__ unsigned long long make_key(float d, uint32_t id) {
   return ((unsigned long long)__float_as_uint(d) << 32) | id;
 }
@@ -204,6 +214,25 @@ struct RegTopK {
 
 }  // namespace
 
+// DADE_SCAN_PROF builds only (tools/scan_prof.py, a separate library): per-phase clock64 cycles
+// summed over warps, to see where a query's latency chain goes. Not in the product library.
+#ifdef DADE_SCAN_PROF
+__device__ unsigned long long g_scan_prof[16];
+#define PROF_MARK(cat)                                        \
+  do {                                                        \
+    const long long _t = clock64();                           \
+    if (lane == 0) {                                          \
+      sprof[cat] += (unsigned long long)(_t - prof_last);     \
+      sprof[8 + (cat)] += 1;                                  \
+    }                                                         \
+    prof_last = _t;                                           \
+  } while (0)
+#else
+#define PROF_MARK(cat) \
+  do {                 \
+  } while (0)
+#endif
+
 // Per-warp shared-memory slice: tiles | mbar | meta | ring | (ASY) staging.
 // Ring capacity: synchronous rounds start at 32 queued and stage 1 runs below 32, so at most 63
 // entries are queued; with an async round in flight stage 1 may run up to 64 queued (+32 + 32).
@@ -250,6 +279,12 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   const bool stats = p.counters != nullptr;
   if (stats)
     for (int j = threadIdx.x; j < DADE_MAX_STEPS; j += blockDim.x) pruned[j] = 0;
+#ifdef DADE_SCAN_PROF
+  __shared__ unsigned long long sprof_all[8][16];
+  unsigned long long* sprof = sprof_all[warp];
+  if (lane < 16) sprof[lane] = 0;
+  long long prof_last = clock64();
+#endif
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -328,6 +363,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
 #pragma unroll 1
     for (int s = 0; s < kStages; ++s)
       if (!issue(s)) break;
+    PROF_MARK(0);  // query start: work item, q~, list table, first tile issues
 
     int head = 0, tail = 0;  // survivor ring (monotonic indices), warp-uniform
     float tau = INFINITY;
@@ -340,17 +376,19 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     };
 
     // One gather round over up to 32 queued survivors. Normally one lane per survivor, up to LA
-    // blocks per round trip. When draining a short queue (epoch boundary, end of stream) 2 or 4
-    // lanes share a survivor and each loads LA consecutive blocks, so one round trip advances it
-    // by up to 4*LA blocks; the group's block sums are then accumulated in block order by every
+    // blocks per round trip. When draining a short queue (epoch boundary, end of stream) 2 to 32
+    // lanes share a survivor (32/qn rounded down to a power of two) and each loads LA consecutive
+    // blocks, so one round trip advances it by up to 32/qn*LA blocks; the group's block sums are then accumulated in block order by every
     // lane of the group (shuffles), so phi is bit-identical to the one-lane path.
     auto queue_round = [&](bool drain) {
       const int qn = min(tail - head, 32);
-      const int lg = !drain ? 0 : qn <= 8 ? 2 : qn <= 16 ? 1 : 0;  // log2 lanes per survivor
+      // log2 lanes per survivor: a draining round spreads its survivors over all 32 lanes
+      const int lg = !drain ? 0 : drain_lanes_log2(qn);
       const int ei = lane >> lg, sub = lane & ((1 << lg) - 1);
       const bool val = ei < qn;
       QEntry e = val ? ring[(head + ei) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0.f};
-      int wtot = (drain || e.blk > DD) ? (LA << lg) : (DD < LA ? DD : LA);
+      // full rounds: one step (DD blocks, LA >= DD) or LA blocks; draining rounds: LA per lane
+      int wtot = drain ? (LA << lg) : (DD < LA ? DD : LA);
       wtot = min(wtot, nblk - e.blk);
       const int b0 = e.blk + sub * LA;  // this lane's first block
       const int want = max(0, min(LA, e.blk + wtot - b0));
@@ -536,6 +574,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
           phase_bits ^= 1u << slot;
           tm = meta[slot];
           ready = true;
+          PROF_MARK(1);  // waiting for a TMA tile
         }
         // the current epoch ends when the next own tile is from a later epoch, or at the end
         // of the stream (then every epoch up to n_ep - 1 is closed)
@@ -549,11 +588,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       }
       if (round) {
         queue_round(drain);
+        if (drain) PROF_MARK(3); else PROF_MARK(2);  // gather round: full / draining
         continue;
       }
       if (ep_end) {
         epoch_end();
         ++cur_ep;
+        PROF_MARK(4);
         continue;
       }
       // stage 1 (qlen < 32: the ring has room for 32 more): one row per lane, DD blocks
@@ -592,6 +633,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
         if (lane == 0 && np_) atomicAdd(&pruned[1], (unsigned)np_);
       }
+      PROF_MARK(5);  // stage 1 of one tile
     }
 
     // results: the register top-K (G = 1) or the merged list (G > 1)
@@ -615,7 +657,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     }
     if (threadIdx.x == 0 && stats) atomicMax(p.counters + 3, (unsigned long long)n_ep);
     __syncthreads();  // qslot / lists / qs / Gk are rewritten for the next query
+    PROF_MARK(6);  // results
   }
+#ifdef DADE_SCAN_PROF
+  PROF_MARK(7);  // exit (last work-counter poll)
+  __syncwarp();
+  if (lane < 16) atomicAdd(&g_scan_prof[lane], sprof[lane]);
+#endif
   if (stats) {
     if (lane == 0) {
       atomicAdd(p.counters + 0, c_tested);
@@ -695,6 +743,9 @@ static void launch_k(const ScanParams& p, cudaStream_t st) {
       case 4: launch_v<DD, KPL, 1, 64>(p, st); return;
       case 5: launch_v<DD, KPL, 1, 96>(p, st); return;
       case 6: launch_v<DD, KPL, 1, 88>(p, st); return;
+      case 10: launch_v<DD, KPL, 2, 80>(p, st); return;   // 2 blocks per lane in draining rounds
+      case 11: launch_v<DD, KPL, 2, 88>(p, st); return;
+      case 12: launch_v<DD, KPL, 2, 96>(p, st); return;
       default: break;
     }
   }
@@ -718,6 +769,17 @@ static void launch_dd(const ScanParams& p, cudaStream_t st) {
   else if (p.K <= 128) launch_k<DD, 4>(p, st);
   else launch_k<DD, 8>(p, st);
 }
+
+#ifdef DADE_SCAN_PROF
+extern "C" int dade_scan_prof_read(unsigned long long* out16, int reset) {
+  if (cudaMemcpyFromSymbol(out16, g_scan_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(g_scan_prof, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+#endif
 
 void launch_scan(const ScanParams& p, cudaStream_t st) {
   if (p.nq <= 0) return;

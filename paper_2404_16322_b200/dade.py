@@ -71,6 +71,7 @@ _SIGS = {
     "dade_get_timing": [P, P],
     "dade_search_prepared": [P, P, P, I32, I32, I32, I32, I32, DBL, P, P, P],
     "dade_probe": [P, P, I32, I32, P],
+    "dade_estimate_knn": [P, P, I32, I32, I32, I32, P, P],
     "dade_bruteforce_knn": [P, P, I64, I64, P, I32, I32, P, P],
     "dade_merge_topk": [P, P, P, I32, I32, I32, P, P],
     "dade_save": [P, C.c_char_p],
@@ -354,6 +355,19 @@ class Index:
         return out
 
     # -------------------------------------------------- tools
+    ESTIMATORS = {"partial": 0, "residual": 1}
+
+    def estimate_knn(self, Q, d: int, K: int, estimator: str = "partial"):
+        """NEXT-2 (Exp-7 / Table III): per query the K rows with the smallest d-dim distance
+        estimate over the whole index ("partial" = P_d, "residual" = P_d + ||x_r||^2 + ||q_r||^2)."""
+        import torch
+        Q = _dev(Q, torch.float32)
+        nq = Q.shape[0]
+        ids = torch.empty((nq, K), dtype=torch.int64, device=Q.device)
+        est = torch.empty((nq, K), dtype=torch.float32, device=Q.device)
+        _ck(lib().dade_estimate_knn(self.h, _ptr(Q), nq, d, self.ESTIMATORS[estimator], K, _ptr(ids), _ptr(est)))
+        return ids, est
+
     def bruteforce_knn(self, X, Q, K: int, id_base: int = 0):
         import torch
         X = _dev(X, torch.float32); Q = _dev(Q, torch.float32)
