@@ -369,6 +369,52 @@ __device__ __forceinline__ bool cand_less2(double d0, int32_t c0, double d1, int
   return d0 < d1 || (d0 == d1 && c0 < c1);
 }
 
+
+// The columns inside the window: every such column lies in a group whose minimum is inside it,
+// so only those groups' d_hat are read, as 32-column (128-B, coalesced) segments. The selected
+// groups are listed first (glist, per-warp smem) and their segments are then loaded kSegBatch at
+// a time, so a row with many candidate groups pays ~1/kSegBatch of the dependent round trips.
+// Returns the candidate count (may exceed kGmCap: only the first kGmCap are stored in cc).
+constexpr int kSegBatch = 4;
+template <int GPL>
+__device__ __forceinline__ int window_cands(const float (&gv)[GPL], unsigned tb, const float* __restrict__ d, int64_t n,
+                                            int gshift, int lane, int* glist, int32_t* cc) {
+  int ns = 0;
+#pragma unroll
+  for (int j = 0; j < GPL; ++j) {
+    const bool in = __float_as_uint(gv[j]) <= tb;
+    const unsigned b = __ballot_sync(0xffffffffu, in);
+    if (in) glist[ns + __popc(b & ((1u << lane) - 1))] = lane + 32 * j;
+    ns += __popc(b);
+  }
+  __syncwarp();
+  const int sh = gshift - 5;  // log2 segments per group
+  const int nseg = ns << sh;
+  int cnt = 0;
+#pragma unroll 1
+  for (int s0 = 0; s0 < nseg; s0 += kSegBatch) {
+    float v[kSegBatch];
+    int64_t col[kSegBatch];
+#pragma unroll
+    for (int u = 0; u < kSegBatch; ++u) {
+      const int s = s0 + u;
+      col[u] = s < nseg ? ((int64_t)glist[s >> sh] << gshift) + ((s & ((1 << sh) - 1)) << 5) + lane : n;
+      v[u] = col[u] < n ? __ldg(d + col[u]) : INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < kSegBatch; ++u) {
+      const bool in = col[u] < n && __float_as_uint(v[u]) <= tb;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+        if (pos < kGmCap) cc[pos] = (int32_t)col[u];
+      }
+      cnt += __popc(bal);
+    }
+  }
+  return cnt;
+}
+
 template <int GPL>  // group minima per lane: rows of up to 32 * GPL groups of 2^gshift columns
 __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
     const float* __restrict__ dh, const float* __restrict__ gm, int gshift, int64_t m, int64_t n, int k,
@@ -429,28 +475,8 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
     E = g[k - 1];
   }
   const unsigned tb = abs_thr_bits(E, slack[row]);
-  // every column inside the window lies in a group whose minimum is inside it: read only those
-  // groups' d_hat (one coalesced 128-B row segment per group)
-  const float* d = dh + row * n;
-  int cnt = 0;
-#pragma unroll 1
-  for (int j = 0; j < GPL; ++j) {
-    unsigned gb = __ballot_sync(0xffffffffu, __float_as_uint(gv[j]) <= tb);
-    while (gb) {
-      const int grp = 32 * j + __ffs(gb) - 1;
-      gb &= gb - 1;
-      for (int h = 0; h < (1 << gshift); h += 32) {
-        const int64_t c = ((int64_t)grp << gshift) + h + lane;
-        const bool in = c < n && __float_as_uint(d[c]) <= tb;
-        const unsigned bal = __ballot_sync(0xffffffffu, in);
-        if (in) {
-          const int pos = cnt + __popc(bal & ((1u << lane) - 1));
-          if (pos < kGmCap) cc[w][pos] = (int32_t)c;
-        }
-        cnt += __popc(bal);
-      }
-    }
-  }
+  __syncwarp();  // sg[w] (the k > 16 sort's buffer) now holds the selected group list
+  const int cnt = window_cands<GPL>(gv, tb, dh + row * n, n, gshift, lane, reinterpret_cast<int*>(sg[w]), cc[w]);
   if (cnt > kGmCap) {  // too many near-ties: the histogram select redoes this row
     if (lane == 0) ovf_rows[atomicAdd(ovf_n, 1)] = (int32_t)row;
     return;
@@ -551,28 +577,8 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin_wide(
     E = g[k - 1];
   }
   const unsigned tb = abs_thr_bits(E, slack[row]);
-  // every column inside the window lies in a group whose minimum is inside it: read only those
-  // groups' d_hat (one coalesced 128-B row segment per group)
-  const float* d = dh + row * n;
-  int cnt = 0;
-#pragma unroll 1
-  for (int j = 0; j < GPL; ++j) {
-    unsigned gb = __ballot_sync(0xffffffffu, __float_as_uint(gv[j]) <= tb);
-    while (gb) {
-      const int grp = 32 * j + __ffs(gb) - 1;
-      gb &= gb - 1;
-      for (int h = 0; h < (1 << gshift); h += 32) {
-        const int64_t c = ((int64_t)grp << gshift) + h + lane;
-        const bool in = c < n && __float_as_uint(d[c]) <= tb;
-        const unsigned bal = __ballot_sync(0xffffffffu, in);
-        if (in) {
-          const int pos = cnt + __popc(bal & ((1u << lane) - 1));
-          if (pos < kGmCap) cc[w][pos] = (int32_t)c;
-        }
-        cnt += __popc(bal);
-      }
-    }
-  }
+  __syncwarp();  // sg[w] (the k > 16 sort's buffer) now holds the selected group list
+  cnt = window_cands<GPL>(gv, tb, dh + row * n, n, gshift, lane, reinterpret_cast<int*>(sg[w]), cc[w]);
   if (cnt > kGmCap && lane == 0) ovf_rows[atomicAdd(ovf_n, 1)] = (int32_t)row;  // histogram select redoes it
   if (lane == 0) s_cnt = cnt;
   }

@@ -205,11 +205,15 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
     }
     mma_commit(accf);
   }
-  __syncwarp();
-  mbar_wait(accf, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // the epilogue's norms are fetched while the MMAs run: ||a||^2 of this thread's row and the
+  // tile's 128 column norms (smem), so their latency is not exposed after the accumulator wait
+  __shared__ float sbn[kTM];
   const int64_t row = tm * kTM + warp * 32 + lane;
   const float a2 = row < m ? an[row] : 0.f;
+  sbn[tid] = tn * kTM + tid < n ? bn[tn * kTM + tid] : 0.f;
+  __syncthreads();
+  mbar_wait(accf, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // the operand stages are free once every MMA completed: each warp transposes its 32 x 32
   // d_hat chunk through shared memory so the global stores are row-contiguous (128 B per row)
   float* stg = reinterpret_cast<float*>(sm) + warp * 32 * 33;
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
     if (full) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
-        const float4 b4 = *reinterpret_cast<const float4*>(bn + c0 + j);
+        const float4 b4 = *reinterpret_cast<const float4*>(sbn + cb * 32 + j);
         d[j + 0] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 0]), a2 + b4.x));
         d[j + 1] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 1]), a2 + b4.y));
         d[j + 2] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 2]), a2 + b4.z));
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        d[j] = c0 + j < n ? fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + bn[c0 + j])) : INFINITY;
+        d[j] = c0 + j < n ? fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + sbn[cb * 32 + j])) : INFINITY;
     }
     if (gmin && row < m && c0 < n) {  // per-row minimum of this 2^gshift-column group (select hint)
       float mn = d[0];
