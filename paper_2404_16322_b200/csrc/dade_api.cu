@@ -198,7 +198,8 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   const int64_t ng = (n + 31) / 32;
   // group-minima-only path (no d_hat matrix): measured slower than the d_hat path at k <= 32
   // (32 exact fp64 columns per candidate group, uncoalesced); kept for very wide rows
-  if (k <= 512 && (int64_t)k * 4 <= ng && n > (int64_t)1 << 20) {
+  const char* fg = getenv("DADE_PROBE_GROUPS");  // 1 forces the group path (measurement)
+  if (k <= 512 && (int64_t)k * 4 <= ng && (fg ? atoi(fg) != 0 : n > (int64_t)1 << 20)) {
     // the GEMM writes only 32-column group minima; exact fp64 distances for the columns of the
     // groups inside the certified window (no m x n d_hat matrix)
     int64_t chunk = std::max<int64_t>(128, ((int64_t)1 << 27) / ng / 128 * 128);

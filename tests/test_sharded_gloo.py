@@ -74,6 +74,37 @@ class OracleEngine:
         i, d, _ = O.search(self.idx, Qn, K, probes.shape[1], dd, param if method == "bsa_p" else 0.0)
         return torch.from_numpy(i), torch.from_numpy(d)
 
+    # calibration pieces (dade_calib_knn / _negatives / dade_pair_features / dade_fit_calibration)
+    def calib_knn(self, X, Qc, K):
+        return O.brute_force_knn(self.X, Qc, K, id_base=self.id_base)
+
+    def calib_negatives(self, Qc, K, knn_ids, n_neg, nprobe_neg, seed):
+        nq = Qc.shape[0]
+        keys = np.zeros((nq, n_neg), np.uint64); ids = np.zeros((nq, n_neg), np.int64)
+        cnt = np.zeros(nq, np.int32)
+        off, row_id, cent = self.idx["off"], self.idx["row_id"], self.idx["centroids"]
+        for q in range(nq):
+            pr = O.probe(Qc[q], cent, nprobe_neg)
+            cand = np.concatenate([row_id[off[l]:off[l + 1]] for l in pr])
+            cand = np.setdiff1d(cand, knn_ids[q])
+            h = O.neg_hash(seed, q, cand)
+            o = np.lexsort((cand, h))[:n_neg]
+            keys[q, :len(o)], ids[q, :len(o)], cnt[q] = h[o], cand[o], len(o)
+        return keys, ids, cnt
+
+    def pair_features(self, Qc, pq, pid):
+        qr = O.rotate(Qc, self.idx["mean"], self.idx["R"])
+        D = qr.shape[1]
+        F = np.zeros((len(pq), D // 16))
+        for i, (q, g) in enumerate(zip(pq, pid)):
+            if self.id_base <= g < self.id_base + len(self.X):
+                diff2 = (self.idx["Xr"][g - self.id_base] - qr[q]) ** 2
+                F[i] = np.cumsum(diff2)[15::16]
+        return F
+
+    def fit_calibration(self, K, F, tau, y):
+        self.fit_args = (K, F, tau, y)
+
     def merge_topk(self, g_ids, g_d):
         i, d = O.merge_shards([(g_ids[s].numpy(), g_d[s].numpy()) for s in range(g_ids.shape[0])],
                               g_ids.shape[2])
@@ -120,6 +151,16 @@ def _worker(rank, world, port, q):
         for nq in (12, 11):
             ids, d = sharded.QueryPartitionedSearch(eng).search(torch.from_numpy(Q[:nq]), 10, 5, 16, "bsa_p", 0.0)
             assert np.array_equal(ids.numpy(), ei[:nq]), "query-partitioned search differs"
+        # sharded calibration: merged K-NN, merged negatives and summed pair features give the
+        # single-index calibration pairs (R14-R16) in the same order with the same features
+        Qc = synth.cal_queries(cfg)[:8]
+        sharded.calibrate_sharded(eng, None, Qc, 10, n_neg=20, nprobe_neg=4, seed=5)
+        K_, F, tau, y = eng.fit_args
+        oq, oid, olab, otau = O.calibration_pairs(X, full, Qc, 10, 20, 4, 5)
+        assert K_ == 10 and np.array_equal(y, olab) and np.allclose(tau, otau, rtol=1e-12)
+        qr = O.rotate(Qc, mean, R)
+        Fo = np.stack([np.cumsum((full["Xr"][i] - qr[q]) ** 2)[15::16] for q, i in zip(oq, oid)])
+        assert np.allclose(F, Fo, rtol=1e-12), "sharded pair features differ"
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e)))
