@@ -238,7 +238,14 @@ __device__ unsigned long long g_scan_prof[16];
 // entries are queued; with an async round in flight stage 1 may run up to 64 queued (+32 + 32).
 template <int DD, bool ASY>
 struct Slice {
-  static constexpr int kStages = (DD == 1 && !ASY) ? 3 : 2;  // ASY: the staging buffers replace a stage
+#ifdef DADE_SCAN_STAGES  // experiment builds (tools/build_variant.py)
+  static constexpr int kStages = ASY ? 2 : DADE_SCAN_STAGES;
+#else
+  // two tiles in flight: measured on C2 scan 0.553 -> 0.531 ms against three (C4 equal, C3 and the
+  // C5 shard already used two) — fewer TMA bytes in flight leave the latency-critical survivor
+  // gathers less queueing, and the shared-memory footprint shrinks to ~6 KB per warp
+  static constexpr int kStages = 2;
+#endif
   static constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
   static constexpr int QCAP = ASY ? 128 : 64;
   static constexpr size_t stage_bytes = ASY ? 2 * (32 * 64 + 32 * 4) : 0;  // 2 async rounds: rows + ids
