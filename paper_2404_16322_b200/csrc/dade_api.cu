@@ -339,6 +339,10 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
 
 // qrot_in / probes_in (device, optional): queries already rotated and probed (dade_prepare, e.g.
 // on another rank) — only the scan runs.
+#ifndef DADE_C0_MULT  // R13: c0 = 4K (experiment builds may change it)
+#define DADE_C0_MULT 4
+#endif
+
 // dade_search_host's pipeline depth. Default 1: on C2 (tools/e2e_breakdown.py) a search cut in
 // two costs 0.19 ms more on the device (the scan's per-launch tail: 0.36 ms at 5,000 queries vs
 // 0.55 ms at 10,000) while the H2D it could hide is 0.20 ms, so chunking does not pay at these
@@ -408,7 +412,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   p.layout = x->layout.p; p.n = x->n; p.D = D; p.nq = nq; p.nprobe = nprobe; p.K = K;
   // alpha = 0 (or a single step): nothing can be pruned; the kernel then runs with 16-dim
   // steps (no classifier fires: m1 = 1, beta' = -inf), which serves every delta_d | D.
-  p.dd = prune ? dd : 1; p.nsteps = prune ? nsteps : D / 16; p.c0 = 4 * K; p.prune = prune ? 1 : 0;
+  p.dd = prune ? dd : 1; p.nsteps = prune ? nsteps : D / 16; p.c0 = DADE_C0_MULT * K; p.prune = prune ? 1 : 0;
   p.avg_stream = (int64_t)nprobe * x->n / std::max(1, x->nlist);
   for (int s = 1; s < p.nsteps; ++s) {
     if (prune && method == DADE_METHOD_ADSAMPLING) {  // m1_d = (D/d)/(1 + eps0/sqrt(d))^2, beta = 0

@@ -37,6 +37,9 @@ namespace dade {
 
 namespace {
 constexpr int TR = 32;            // rows per tile: one row per lane
+#ifndef DADE_EPOCH_GROWTH  // R13: epoch boundaries c0, 2 c0, 4 c0, ... (experiment builds may change it)
+#define DADE_EPOCH_GROWTH 2
+#endif
 constexpr unsigned long long kKeyInf = ~0ull;
 
 struct __align__(16) QEntry {
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
     int n_ep = 0;  // epochs the stream touches: [0,c0), [c0,2c0), [2c0,4c0), ...
-    for (int64_t e_lo = 0, e_hi = p.c0; e_lo < L; e_lo = e_hi, e_hi *= 2) ++n_ep;
+    for (int64_t e_lo = 0, e_hi = p.c0; e_lo < L; e_lo = e_hi, e_hi *= DADE_EPOCH_GROWTH) ++n_ep;
 
     RegTopK<KPL> tk;
     tk.init(K);
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         if (pr >= L) return false;
         if (pr >= pe_hi) {
           ++pep;
-          pe_hi = pe_hi > (1 << 29) ? (1 << 30) : pe_hi * 2;
+          pe_hi = pe_hi > (1 << 29) / DADE_EPOCH_GROWTH ? (1 << 30) : pe_hi * DADE_EPOCH_GROWTH;
         }
         while (ppos + pl.y <= pr) {  // skip exhausted (and empty) lists; pr < L keeps pj < nprobe
           ppos += pl.y;
