@@ -225,7 +225,9 @@ dade_status dade_search_prepared(dade_index* idx, const float* qrot, const int32
  * copy streams; with DADE_HOST_CHUNKS=c (default 1) the batch is cut into c chunks pipelined so
  * that chunk c's H2D overlaps the search of chunk c-1 and its D2H the search of chunk c+1 (not
  * the default: measured slower on C2). Each query's result is independent of
- * the chunking. Pinned host memory gives asynchronous copies;
+ * the chunking. Unchunked batches of >= 4,096 queries copy Q in two halves and rotate + probe
+ * each half as it lands (DADE_HOST_PREP_CHUNKS overrides), then scan once. Pinned host memory
+ * gives asynchronous copies;
  * pageable memory works but serialises them. With stats != NULL the batch runs unchunked.
  * Used for the end-to-end (e2e) measurement. Errors: as dade_search. */
 dade_status dade_search_host(dade_index* idx, const float* Q_host, int nq, int K, int nprobe,

@@ -347,6 +347,13 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
 // two costs 0.19 ms more on the device (the scan's per-launch tail: 0.36 ms at 5,000 queries vs
 // 0.55 ms at 10,000) while the H2D it could hide is 0.20 ms, so chunking does not pay at these
 // batch sizes. DADE_HOST_CHUNKS=c sets c chunks.
+// dade_search_host's rotation + probe chunks when the search itself is not chunked
+// (DADE_HOST_PREP_CHUNKS overrides; default 2 for batches of >= 4,096 queries)
+int host_prep_chunks(int nq) {
+  if (const char* e = getenv("DADE_HOST_PREP_CHUNKS")) return std::max(1, std::min(atoi(e), std::max(nq, 1)));
+  return nq >= 4096 ? 2 : 1;
+}
+
 int host_chunks(int nq) {
   if (const char* e = getenv("DADE_HOST_CHUNKS")) return std::max(1, std::min(atoi(e), std::max(nq, 1)));
   return 1;
@@ -1231,11 +1238,53 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   DADE_CK(cudaEventRecord(x->hev[0], st));  // the copies start after earlier work on the stream
   DADE_CK(cudaStreamWaitEvent(x->h2d, x->hev[0], 0));
   DADE_CK(cudaStreamWaitEvent(x->d2h, x->hev[0], 0));
-  for (int c = 0; c < nch; ++c) {
-    const int q0 = (int)((int64_t)nq * c / nch), q1 = (int)((int64_t)nq * (c + 1) / nch);
-    DADE_CK(cudaMemcpyAsync(x->qbuf.p + (size_t)q0 * D, Qh + (size_t)q0 * D, sizeof(float) * (q1 - q0) * D,
-                            cudaMemcpyHostToDevice, x->h2d));
-    DADE_CK(cudaEventRecord(x->hev[1 + 2 * c], x->h2d));
+  const int npc_copy = nch == 1 && !stats && nq > 0 ? host_prep_chunks(nq) : 1;
+  while ((int)x->hev.size() < npc_copy + 3) {
+    cudaEvent_t e;
+    DADE_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    x->hev.push_back(e);
+  }
+  if (npc_copy > 1) {
+    for (int c = 0; c < npc_copy; ++c) {
+      const int q0 = (int)((int64_t)nq * c / npc_copy), q1 = (int)((int64_t)nq * (c + 1) / npc_copy);
+      DADE_CK(cudaMemcpyAsync(x->qbuf.p + (size_t)q0 * D, Qh + (size_t)q0 * D, sizeof(float) * (q1 - q0) * D,
+                              cudaMemcpyHostToDevice, x->h2d));
+      DADE_CK(cudaEventRecord(x->hev[3 + c], x->h2d));
+    }
+  } else {
+    for (int c = 0; c < nch; ++c) {
+      const int q0 = (int)((int64_t)nq * c / nch), q1 = (int)((int64_t)nq * (c + 1) / nch);
+      DADE_CK(cudaMemcpyAsync(x->qbuf.p + (size_t)q0 * D, Qh + (size_t)q0 * D, sizeof(float) * (q1 - q0) * D,
+                              cudaMemcpyHostToDevice, x->h2d));
+      DADE_CK(cudaEventRecord(x->hev[1 + 2 * c], x->h2d));
+    }
+  }
+  // one search: its rotation + probe (a4, a5) run per H2D chunk, so the copy of chunk c+1
+  // overlaps the probe of chunk c; the scan (a6-a8) then runs once over the whole batch
+  const int npc = nch == 1 && !stats && nq > 0 ? host_prep_chunks(nq) : 1;
+  if (npc > 1) {
+    DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
+    DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
+    while ((int)x->hev.size() < npc + 3) {
+      cudaEvent_t e;
+      DADE_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      x->hev.push_back(e);
+    }
+    x->qrot.reserve((size_t)nq * D);
+    x->probes.reserve((size_t)nq * nprobe);
+    for (int c = 0; c < npc; ++c) {
+      const int q0 = (int)((int64_t)nq * c / npc), q1 = (int)((int64_t)nq * (c + 1) / npc);
+      DADE_CK(cudaStreamWaitEvent(st, x->hev[3 + c], 0));
+      prepare(x, x->qbuf.p + (size_t)q0 * D, q1 - q0, nprobe, x->qrot.p + (size_t)q0 * D,
+              x->probes.p + (size_t)q0 * nprobe, false);
+    }
+    do_search(x, nullptr, nq, K, nprobe, delta_d, significance, x->ids_tmp.p, x->dists_tmp.p, nullptr,
+              DADE_METHOD_BSA_P, x->qrot.p, x->probes.p);
+    DADE_CK(cudaEventRecord(x->hev[2], st));
+    DADE_CK(cudaStreamWaitEvent(x->d2h, x->hev[2], 0));
+    DADE_CK(cudaMemcpyAsync(ids_h, x->ids_tmp.p, sizeof(int64_t) * nq * K, cudaMemcpyDeviceToHost, x->d2h));
+    DADE_CK(cudaMemcpyAsync(dists_h, x->dists_tmp.p, sizeof(float) * nq * K, cudaMemcpyDeviceToHost, x->d2h));
+    nch = 0;  // done: skip the per-chunk searches below
   }
   for (int c = 0; c < nch; ++c) {
     const int q0 = (int)((int64_t)nq * c / nch), q1 = (int)((int64_t)nq * (c + 1) / nch);

@@ -171,14 +171,16 @@ def test_search_host_matches_device(sift_small):
     assert np.array_equal(a.cpu().numpy(), c) and np.array_equal(b.cpu().numpy(), d)
 
 
-@pytest.mark.parametrize("chunks", ["1", "3", "7"])
-def test_search_host_pipeline_chunks(sift_small, chunks, monkeypatch):
-    """The H2D / search / D2H pipeline of dade_search_host (pinned buffers, ragged chunks)
-    returns exactly the device-buffer search's results."""
+@pytest.mark.parametrize("chunks,prep", [("1", "1"), ("3", "1"), ("7", "1"), ("1", "2"), ("1", "3")])
+def test_search_host_pipeline_chunks(sift_small, chunks, prep, monkeypatch):
+    """The H2D / search / D2H pipeline of dade_search_host (pinned buffers, ragged chunks; search
+    chunks or rotation + probe chunks ahead of one scan) returns exactly the device-buffer
+    search's results."""
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     Q = synth.queries(cfg, n=1001)
     a, b = ix.search(torch.from_numpy(Q).cuda(), 10, 8, 16, 0.005)
     monkeypatch.setenv("DADE_HOST_CHUNKS", chunks)
+    monkeypatch.setenv("DADE_HOST_PREP_CHUNKS", prep)
     Qh = torch.from_numpy(Q).pin_memory()
     ih = torch.empty((1001, 10), dtype=torch.int64).pin_memory()
     dh = torch.empty((1001, 10), dtype=torch.float32).pin_memory()

@@ -67,9 +67,10 @@ def dev_chunks(c):
     return f
 
 
-def host_chunks(c):
+def host_chunks(c, prep=1):
     def f():
         os.environ["DADE_HOST_CHUNKS"] = str(c)
+        os.environ["DADE_HOST_PREP_CHUNKS"] = str(prep)
         ix.search_host(Qh, K, a.nprobe, dd, 0.005, ids=ih, dists=dh)
     return f
 
@@ -82,6 +83,8 @@ for c in (2, 4):
     out[f"search_{c}dev_chunks_ms"] = timeit(dev_chunks(c))
 for c in (1, 2, 4):
     out[f"search_host_{c}_ms"] = timeit(host_chunks(c))
+for pc in (2, 3, 4):
+    out[f"search_host_prep{pc}_ms"] = timeit(host_chunks(1, pc))
 out["h2d_GBps"] = round(Qh.numel() * 4 / out["h2d_ms"] / 1e6, 1)
 print(json.dumps(out), flush=True)
 
