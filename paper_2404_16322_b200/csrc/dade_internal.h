@@ -146,8 +146,14 @@ struct ScanParams {
   const float* xnorm;   // n: ‖x~‖² per list-major row (residual only)
   const float* qconst;  // nq x (nsteps - 1): ‖q_r‖² − m·σ_d per step (residual only)
   int64_t avg_stream;   // expected candidates per query (nprobe * n / nlist): picks warps per query
+  const int32_t* order; // nq: processing order of the queries (null = 0..nq-1); results stay at q
 };
 void launch_scan(const ScanParams& p, cudaStream_t st);
+// misc.cu: the scan's query order — a counting sort of the queries by their nearest probed list
+// (probes[q][0]), so queries that share lists are scanned close in time (L2 reuse of their
+// tiles). cnt: nlist ints of scratch; order: nq ints.
+void launch_query_order(const int32_t* probes, int nq, int nprobe, int nlist, int* cnt, int32_t* order,
+                        cudaStream_t st);
 // ‖x~‖² of every list-major row of the blocked layout (fp64 sums, stored fp32)
 void launch_row_norms(const float* layout, int64_t n, int D, float* out, cudaStream_t st);
 // estimate.cu (NEXT-2, Exp-7): top-K by the d-dim estimate over the whole layout; xnorm != null

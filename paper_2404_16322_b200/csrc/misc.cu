@@ -44,6 +44,52 @@ __global__ void __launch_bounds__(256) k_merge_topk(const int64_t* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ scan query order
+__global__ void k_order_hist(const int32_t* __restrict__ probes, int nq, int nprobe, int* __restrict__ cnt) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x)
+    atomicAdd(&cnt[probes[(int64_t)q * nprobe]], 1);
+}
+
+// exclusive prefix sum of cnt[0, nlist) in place, one CTA of 1024 threads (contiguous chunks)
+__global__ void __launch_bounds__(1024) k_order_offsets(int* __restrict__ cnt, int nlist) {
+  __shared__ int part[1024];
+  const int per = (nlist + 1023) / 1024;
+  const int b = threadIdx.x * per, e = min(nlist, b + per);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += cnt[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan of the chunk sums
+    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int i = b; i < e; ++i) {
+    const int c = cnt[i];
+    cnt[i] = run;
+    run += c;
+  }
+}
+
+__global__ void k_order_scatter(const int32_t* __restrict__ probes, int nq, int nprobe, int* __restrict__ cur,
+                                int32_t* __restrict__ order) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x)
+    order[atomicAdd(&cur[probes[(int64_t)q * nprobe]], 1)] = q;
+}
+
+void launch_query_order(const int32_t* probes, int nq, int nprobe, int nlist, int* cnt, int32_t* order,
+                        cudaStream_t st) {
+  if (nq <= 0) return;
+  DADE_CK(cudaMemsetAsync(cnt, 0, sizeof(int) * nlist, st));
+  const int g = std::min((nq + 255) / 256, 1184);
+  k_order_hist<<<g, 256, 0, st>>>(probes, nq, nprobe, cnt);
+  k_order_offsets<<<1, 1024, 0, st>>>(cnt, nlist);
+  k_order_scatter<<<g, 256, 0, st>>>(probes, nq, nprobe, cnt, order);
+  DADE_CK(cudaGetLastError());
+}
+
 void launch_merge_topk(const int64_t* ids_in, const float* d_in, int S, int nq, int K,
                        int64_t* ids_out, float* d_out, cudaStream_t st) {
   if (nq <= 0) return;

@@ -311,7 +311,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   const unsigned lt_mask = (1u << lane) - 1;
 
   for (;;) {
-    if (threadIdx.x == 0) *qslot = atomicAdd(p.work_counter, 1);
+    if (threadIdx.x == 0) {
+      const int slot = atomicAdd(p.work_counter, 1);
+      *qslot = slot < p.nq && p.order ? p.order[slot] : slot;
+    }
     __syncthreads();
     const int qi = *qslot;
     if (qi >= p.nq) break;

@@ -188,6 +188,18 @@ def test_search_host_pipeline_chunks(sift_small, chunks, prep, monkeypatch):
     assert np.array_equal(a.cpu().numpy(), ih.numpy()) and np.array_equal(b.cpu().numpy(), dh.numpy())
 
 
+def test_scan_query_order_invariance(sift_small, monkeypatch):
+    """DADE_SCAN_ORDER=1 (queries scanned grouped by nearest probed list) returns exactly the
+    default order's results and counters: each query's scan depends only on its own stream."""
+    cfg, (torch, ix, oidx, X, Xd) = sift_small
+    Q = torch.from_numpy(synth.queries(cfg, n=700)).cuda()
+    a, b, sa = ix.search(Q, 10, 8, 16, 0.005, stats=True)
+    monkeypatch.setenv("DADE_SCAN_ORDER", "1")
+    c, d, sc = ix.search(Q, 10, 8, 16, 0.005, stats=True)
+    assert torch.equal(a, c) and torch.equal(b, d)
+    assert sa["tested"] == sc["tested"] and sa["dims_scanned"] == sc["dims_scanned"]
+
+
 def test_save_load_roundtrip(sift_small, tmp_path):
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     from paper_2404_16322_b200 import Index
