@@ -281,9 +281,13 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
 // passes of the probe's tensor-core filter: 1 (tf32 hi parts only: 1/3 of the MMAs and 1/2 of the
 // operand bytes, a ~40x wider but still rigorous certified window; the fp64 re-rank keeps the
 // result exact) unless DADE_PROBE_PASSES=3
-int probe_passes() {
+// tf32 passes of the probe filter: 1 (hi x hi) with its wider certified window, or 3 (split
+// precision) when the rows are long — at D = 960 the 1-pass window holds so many near-ties that
+// the fp64 certification dominates (measured C3 step 1.95 -> 1.83 ms with 3 passes; C2, C4 and
+// the C5 shard, D <= 256, are faster with 1). DADE_PROBE_PASSES overrides.
+int probe_passes(int D) {
   const char* e = getenv("DADE_PROBE_PASSES");
-  return e ? atoi(e) : 1;
+  return e ? atoi(e) : (D >= 512 ? 3 : 1);
 }
 
 void upload_rotation(dade_index* x) {
@@ -334,7 +338,7 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
   if (x->nlist == 1) {
     DADE_CK(cudaMemsetAsync(probes, 0, sizeof(int32_t) * nq, st));
   } else {
-    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, false, probe_passes());
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, false, probe_passes(x->D));
   }
   DADE_CK(cudaStreamWaitEvent(st, x->join, 0));
 }
@@ -1360,7 +1364,7 @@ extern "C" dade_status dade_probe(dade_index* x, const float* Q, int nq, int npr
   DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "no IVF");
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
   DeviceGuard g(x->device);
-  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, true, probe_passes());
+  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, true, probe_passes(x->D));
   API_END
 }
 
