@@ -245,7 +245,10 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     // the warp-specialised d_hat writer pays off for very wide rows (measured on C5, 65,536
     // columns: 1.42 -> 1.19 ms); up to 16,384 columns the one-tile-per-CTA kernel with 3 CTAs/SM
     // is faster (C2 68 vs 97 us, C4 222 vs 358 us, C3 36 vs 42 us)
-    if (use_gmin && n > 32768)
+    if (use_gmin && n > 32768 && dhat_ares_ok(D, passes))
+      launch_dhat_ares(x->a_tc.hi.p, x->a_tc.norm.p, mm, bop.hi.p, bop.norm.p, n, D, x->dmat.p, n, x->gmin.p,
+                       gshift, x->stream);
+    else if (use_gmin && n > 32768)
       launch_dhat_tc(x->a_tc.hi.p, x->a_tc.lo.p, x->a_tc.norm.p, mm, bop.hi.p, bop.lo.p, bop.norm.p, n, D,
                      x->dmat.p, n, x->gmin.p, gshift, passes, x->stream);
     else

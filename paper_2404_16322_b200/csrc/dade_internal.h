@@ -101,6 +101,9 @@ void launch_dhat_tc(const float* Ahi, const float* Alo, const float* an, int64_t
                     const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo, float* gmin,
                     int gshift, int passes, cudaStream_t st);
 int probe_tc_splits(int64_t m, int64_t n, int sms);
+bool dhat_ares_ok(int D, int passes);
+void launch_dhat_ares(const float* Ahi, const float* an, int64_t m, const float* Bhi, const float* bn, int64_t n,
+                      int D, float* out, int64_t ldo, float* gmin, int gshift, cudaStream_t st);
 void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                      const float* Blo, const float* bn, int64_t n, int D, int k, const float* slack,
                      const float* A, const float* B, int32_t* cand, int32_t* ccount, int nsplit,

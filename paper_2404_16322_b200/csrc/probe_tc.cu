@@ -488,6 +488,161 @@ __global__ void __launch_bounds__(kThreads, 2) k_dhat_tc(
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
+// k_dhat_tc with the row tile's A operand RESIDENT in shared memory (1-pass, nkc * 8 KB <= 168 KB,
+// i.e. D <= 336): the A chunks are fetched once per CTA instead of once per column tile, halving
+// the L2 -> SM operand traffic that bounds the wide-row d_hat writer (C5 shard: 128 KB of A and
+// 128 KB of B per 128 x 128 tile at D = 256). One CTA per SM (A + a four-stage B ring).
+__global__ void __launch_bounds__(kThreads, 1) k_dhat_ares(
+    const float* __restrict__ Ahi, const float* __restrict__ an, const float* __restrict__ Bhi,
+    const float* __restrict__ bn, int nkc, int64_t m, int64_t n, int tiles_per_split, float* __restrict__ out,
+    int64_t ldo, float* __restrict__ gmin, int64_t ldg, int gshift) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  constexpr int S = 4;
+  constexpr int CB = kSub * 4;  // bytes of one (tile, chunk) operand block
+  unsigned char* areg = sm;
+  unsigned char* ring = sm + (size_t)nkc * CB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * CB);
+  uint64_t* empty = full + 4;
+  uint64_t* tfull = empty + 4;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* afull = tempty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(afull + 1);
+  float* stg_all = reinterpret_cast<float*>(ring + S * CB + 128);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tm = blockIdx.x;
+  const int64_t ntiles = (n + kTM - 1) / kTM;
+  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
+  const int64_t rem = ntiles - t0;
+  const int nt = rem <= 0 ? 0 : (int)(rem < tiles_per_split ? rem : tiles_per_split);
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    mbar_init(afull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0 && nt > 0) {  // ---------------- TMA producer: A once, then the B chunks
+      mbar_expect_tx(afull, (uint32_t)nkc * CB);
+      for (int kc = 0; kc < nkc; ++kc) bulk_g2s(areg + (size_t)kc * CB, Ahi + (tm * nkc + kc) * kSub, CB, afull);
+      int it = 0;
+      for (int t = 0; t < nt; ++t) {
+        const int64_t tn = t0 + t;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % S;
+          if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+          mbar_expect_tx(&full[s], CB);
+          bulk_g2s(ring + s * CB, Bhi + (tn * nkc + kc) * kSub, CB, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nt > 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+      mbar_wait(afull, 0);
+      int it = 0;
+      for (int t = 0; t < nt; ++t) {
+        const int b = t & 1;
+        if (t >= 2) mbar_wait(&tempty[b], ((t >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + b * kTM;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < kKC / 8; ++j) {
+            const uint64_t ah = umma_desc(areg + (size_t)kc * CB + j * 256, 128, kSBO);
+            const uint64_t bh = umma_desc(ring + s * CB + j * 256, 128, kSBO);
+            mma_tf32(acc, ah, bh, idesc, (kc | j) != 0);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[b]);
+      }
+    }
+  } else {  // ---------------- epilogue: one thread per row, warp-transposed stores
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int64_t row = tm * kTM + r;
+    const float a2 = row < m ? an[row] : 0.f;
+    float* stg = stg_all + (warp - 2) * 32 * 33;
+    float gmn = INFINITY;
+    for (int t = 0; t < nt; ++t) {
+      const int b = t & 1;
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t cb0 = (t0 + t) * kTM;
+#pragma unroll 1
+      for (int cb = 0; cb < kTM / 32; ++cb) {
+        uint32_t v[32];
+        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + b * kTM + cb * 32, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (cb == kTM / 32 - 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        const int64_t c0 = cb0 + cb * 32;
+        const bool fullc = c0 + 32 <= n;
+        float d[32];
+        const float2* bn2 = reinterpret_cast<const float2*>(bn + c0);  // bn is padded to 128
+        const unsigned long long a2p = pk2(a2, a2), m2 = pk2(-2.f, -2.f);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float2 bb = __ldg(bn2 + jj);
+          const unsigned long long x = fma2(m2, pk2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1])),
+                                            add2(a2p, pk2(bb.x, bb.y)));
+          const float2 xf = *reinterpret_cast<const float2*>(&x);
+          d[2 * jj] = c0 + 2 * jj < n ? fmaxf(0.f, xf.x) : INFINITY;
+          d[2 * jj + 1] = c0 + 2 * jj + 1 < n ? fmaxf(0.f, xf.y) : INFINITY;
+        }
+        if (gmin && row < m && c0 < n) {
+          float mn = d[0];
+#pragma unroll
+          for (int j = 1; j < 32; ++j) mn = fminf(mn, d[j]);
+          if (gshift == 6) {
+            if ((cb & 1) == 0) gmn = mn;
+            mn = fminf(mn, gmn);
+          }
+          if (gshift == 5 || (cb & 1) == 1 || c0 + 32 >= n) gmin[row * ldg + (c0 >> gshift)] = mn;
+        }
+        if (fullc && (ldo & 3) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = d[j];
+          __syncwarp();
+#pragma unroll
+          for (int itr = 0; itr < 8; ++itr) {
+            const int ri = itr * 4 + (lane >> 3), cc = (lane & 7) * 4;
+            const int64_t grow = tm * kTM + q * 32 + ri;
+            if (grow < m) {
+              const float* sp = stg + ri * 33 + cc;
+              *reinterpret_cast<float4*>(out + grow * ldo + c0 + cc) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+            }
+          }
+          __syncwarp();
+        } else if (row < m) {
+          float* o = out + row * ldo + c0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < n) o[j] = d[j];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
 __device__ __forceinline__ bool cless(double d0, int32_t c0, double d1, int32_t c1) {
   return d0 < d1 || (d0 == d1 && c0 < c1);
 }
@@ -687,6 +842,44 @@ void launch_dhat_tc(const float* Ahi, const float* Alo, const float* an, int64_t
   dim3 grid((unsigned)mt, (unsigned)((ntiles + tps - 1) / tps));
   k_dhat_tc<<<grid, kThreads, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), m, n, tps, out, ldo, gmin,
                                          (n + (1 << gshift) - 1) >> gshift, gshift, passes);
+  DADE_CK(cudaGetLastError());
+}
+
+// the A-resident writer applies to the 1-pass filter with nkc * 8 KB of A <= 168 KB (D <= 336).
+// Off by default (DADE_DHAT_ARES=1 enables it): measured on the C5 shard it is SLOWER (search
+// 3.03 -> 3.76 ms) — the writer is bound by its epilogue, not by operand traffic, and one CTA per
+// SM halves the epilogue warps.
+static size_t dhat_ares_smem(int nkc) { return (size_t)nkc * kSub * 4 + 4 * kSub * 4 + 128 + 4 * 32 * 33 * 4; }
+bool dhat_ares_ok(int D, int passes) {
+  const char* e = getenv("DADE_DHAT_ARES");
+  if (!e || atoi(e) == 0) return false;
+  return passes == 1 && dhat_ares_smem(tc_nkc(D)) <= 220 * 1024;
+}
+
+void launch_dhat_ares(const float* Ahi, const float* an, int64_t m, const float* Bhi, const float* bn, int64_t n,
+                      int D, float* out, int64_t ldo, float* gmin, int gshift, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return;
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    DADE_CK(cudaGetDevice(&dev));
+    DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int nkc = tc_nkc(D);
+  const size_t smem = dhat_ares_smem(nkc);
+  static size_t attr = 0;
+  if (smem > attr) {
+    DADE_CK(cudaFuncSetAttribute(k_dhat_ares, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM;
+  // one CTA per SM: about three waves of (row tile, column range) CTAs, >= 4 column tiles each
+  int64_t nsplit = std::max<int64_t>(1, (3 * (int64_t)sms + mt - 1) / mt);
+  nsplit = std::min<int64_t>(nsplit, std::max<int64_t>(1, ntiles / 4));
+  const int tps = (int)((ntiles + nsplit - 1) / nsplit);
+  dim3 grid((unsigned)mt, (unsigned)((ntiles + tps - 1) / tps));
+  k_dhat_ares<<<grid, kThreads, smem, st>>>(Ahi, an, Bhi, bn, nkc, m, n, tps, out, ldo, gmin,
+                                            (n + (1 << gshift) - 1) >> gshift, gshift);
   DADE_CK(cudaGetLastError());
 }
 

@@ -103,3 +103,26 @@ def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe, C, probe_passes):
     pr = ix.probe(torch.from_numpy(Q).cuda(), nprobe).cpu().numpy()
     for q in range(0, 300, 7):
         assert pr[q].tolist() == O.probe(Q[q], cent, nprobe).tolist()
+
+
+@pytest.mark.parametrize("ares", ["0", "1"])
+def test_probe_wide_d256_resident_a(torch_cuda, ares, monkeypatch):
+    # the wide-row d_hat writers at D = 256 (the C5 shape; nkc = 16 chunks of A resident in
+    # shared memory for "1"), 1-pass filter, 64-column groups, ragged last tile: probes must equal
+    # the oracle's exactly with either writer
+    torch = torch_cuda
+    monkeypatch.setenv("DADE_PROBE_PASSES", "1")
+    monkeypatch.setenv("DADE_DHAT_ARES", ares)
+    rng = np.random.default_rng(11)
+    D, C = 256, 33000
+    X = rng.integers(0, 5, size=(2 * C, D)).astype(np.float32)
+    cent = X[rng.choice(2 * C, C, replace=False)].copy()
+    cent[20000] = cent[30]
+    ix = _idx(torch, D)
+    mean, R, lam = O.fit_rotation(X)
+    ix.set_rotation(mean, R, lam)
+    ix.build_ivf(torch.from_numpy(X).cuda(), C, centroids=torch.from_numpy(cent).cuda())
+    Q = rng.integers(0, 5, size=(200, D)).astype(np.float32)
+    pr = ix.probe(torch.from_numpy(Q).cuda(), 8).cpu().numpy()
+    for q in range(0, 200, 9):
+        assert pr[q].tolist() == O.probe(Q[q], cent, 8).tolist()
