@@ -46,14 +46,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+#ifndef DADE_MBAR_HINT
+#define DADE_MBAR_HINT 0
+#endif
+// DADE_MBAR_HINT > 0: try_wait with a suspend-time hint (ns), so a waiting warp yields its issue slots
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "W%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
-      "r"(ph)
-      : "memory");
+  if (DADE_MBAR_HINT > 0) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+        "r"(ph), "r"((uint32_t)DADE_MBAR_HINT)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+        "r"(ph)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

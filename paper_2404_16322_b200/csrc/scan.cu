@@ -63,14 +63,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
+#ifndef DADE_SCAN_MBAR_HINT
+#define DADE_SCAN_MBAR_HINT 0
+#endif
+// DADE_SCAN_MBAR_HINT > 0: try_wait with a suspend-time hint (ns), so a waiting warp yields its issue slots
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "W%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
-      "r"(phase)
-      : "memory");
+  if (DADE_SCAN_MBAR_HINT > 0) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+        "r"(phase), "r"((uint32_t)DADE_SCAN_MBAR_HINT)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+        "r"(phase)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile(
