@@ -319,6 +319,14 @@ __global__ void k_ids_from_idx(const int32_t* idx, const double* d64, int64_t cn
 
 // a4 + a5: q~ = R(q - mu) (side stream) and the exact probes (main stream), joined on the main
 // stream. qrot: device nq x D, probes: device nq x nprobe.
+void ensure_side(dade_index* x) {
+  if (!x->side) {
+    DADE_CK(cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking));
+    DADE_CK(cudaEventCreateWithFlags(&x->fork, cudaEventDisableTiming));
+    DADE_CK(cudaEventCreateWithFlags(&x->join, cudaEventDisableTiming));
+  }
+}
+
 void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int32_t* probes, bool stats) {
   const int D = x->D;
   cudaStream_t st = x->stream;
@@ -327,11 +335,7 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
     x->flag.reserve(1);
     DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), st));
   }
-  if (!x->side) {
-    DADE_CK(cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking));
-    DADE_CK(cudaEventCreateWithFlags(&x->fork, cudaEventDisableTiming));
-    DADE_CK(cudaEventCreateWithFlags(&x->join, cudaEventDisableTiming));
-  }
+  ensure_side(x);
   DADE_CK(cudaEventRecord(x->fork, st));
   DADE_CK(cudaStreamWaitEvent(x->side, x->fork, 0));
   launch_check_finite(Q, (int64_t)nq * D, x->flag.p, x->side, 3);
@@ -356,6 +360,19 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
 // two costs 0.19 ms more on the device (the scan's per-launch tail: 0.36 ms at 5,000 queries vs
 // 0.55 ms at 10,000) while the H2D it could hide is 0.20 ms, so chunking does not pay at these
 // batch sizes. DADE_HOST_CHUNKS=c sets c chunks.
+// DADE_SCAN_TAIL=X: the last X queries of a batch are scanned by a concurrent second launch with
+// DADE_SCAN_TAIL_G (default 4) warps per query (measurement switch; 0 = off). Measured on C2:
+// X = 500 -0.7% (noise), 1,000 +4%, 2,000 +13%; C4 X = 1,000 -0.5% — the one-warp scan is
+// throughput-bound, not tail-bound, so it stays off.
+int scan_tail(int nq) {
+  const char* e = getenv("DADE_SCAN_TAIL");
+  return e ? std::max(0, std::min(atoi(e), nq)) : 0;
+}
+int scan_tail_g() {
+  const char* e = getenv("DADE_SCAN_TAIL_G");
+  return e ? atoi(e) : 4;
+}
+
 // DADE_SCAN_ORDER=1: the scan takes the queries grouped by nearest probed list
 // (launch_query_order). Off by default — measured: C2 scan unchanged (0.546 ms; ~3,500 queries are
 // in flight at once, so the order barely changes which lists are hot together) and +20 us for the
@@ -491,7 +508,34 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   DADE_CK(cudaMemsetAsync(x->work.p, 0, sizeof(int), st));
   p.work_counter = x->work.p;
   p.order = order;
-  launch_scan(p, st);
+  const int tail = scan_tail(nq);
+  if (tail > 0 && tail < nq && !order) {
+    // the last `tail` queries run as a second scan with 4 warps per query on the side stream:
+    // its CTAs take the SM slots the first scan's warps free as they run out of queries, so the
+    // first scan's tail is filled and the second's is 4x shorter
+    x->work.reserve(2);
+    DADE_CK(cudaMemsetAsync(x->work.p, 0, 2 * sizeof(int), st));
+    const int q0 = nq - tail;
+    ScanParams p2 = p;
+    p.nq = q0;
+    p2.nq = tail;
+    p2.qrot += (size_t)q0 * D;
+    p2.probes += (size_t)q0 * nprobe;
+    p2.out_ids += (size_t)q0 * K;
+    p2.out_d += (size_t)q0 * K;
+    if (p2.qconst) p2.qconst += (size_t)q0 * (nsteps - 1);
+    p2.work_counter = x->work.p + 1;
+    p2.g_force = scan_tail_g();
+    ensure_side(x);
+    DADE_CK(cudaEventRecord(x->fork, st));
+    DADE_CK(cudaStreamWaitEvent(x->side, x->fork, 0));
+    launch_scan(p, st);
+    launch_scan(p2, x->side);
+    DADE_CK(cudaEventRecord(x->join, x->side));
+    DADE_CK(cudaStreamWaitEvent(st, x->join, 0));
+  } else {
+    launch_scan(p, st);
+  }
   if (evs && !stats) DADE_CK(cudaEventRecord(x->ev[3], st));
   if (stats) {
     DADE_CK(cudaEventRecord(x->ev[3], st));

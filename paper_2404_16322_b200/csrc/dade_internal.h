@@ -150,6 +150,7 @@ struct ScanParams {
   const float* qconst;  // nq x (nsteps - 1): ‖q_r‖² − m·σ_d per step (residual only)
   int64_t avg_stream;   // expected candidates per query (nprobe * n / nlist): picks warps per query
   const int32_t* order; // nq: processing order of the queries (null = 0..nq-1); results stay at q
+  int g_force;          // warps per query (0 = the scan_group heuristic)
 };
 void launch_scan(const ScanParams& p, cudaStream_t st);
 // misc.cu: the scan's query order — a counting sort of the queries by their nearest probed list

@@ -744,7 +744,7 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
     DADE_CK(cudaGetDevice(&dev));
     DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int G = scan_group(p.nq, sms, p.avg_stream);
+  const int G = p.g_force > 0 ? p.g_force : scan_group(p.nq, sms, p.avg_stream);
   DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
   if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, ASY, RES>(p, st, 1, sms);
   else launch_g<DD, KPL, LA, MAXREG, true, ASY, RES>(p, st, G, sms);
