@@ -200,6 +200,19 @@ def test_scan_query_order_invariance(sift_small, monkeypatch):
     assert sa["tested"] == sc["tested"] and sa["dims_scanned"] == sc["dims_scanned"]
 
 
+@pytest.mark.parametrize("tail", ["1", "300"])
+def test_scan_tail_split_invariance(sift_small, tail, monkeypatch):
+    """DADE_SCAN_TAIL (the last queries scanned by a concurrent 4-warps-per-query launch) returns
+    exactly the single launch's results and counters."""
+    cfg, (torch, ix, oidx, X, Xd) = sift_small
+    Q = torch.from_numpy(synth.queries(cfg, n=700)).cuda()
+    a, b, sa = ix.search(Q, 10, 8, 16, 0.005, stats=True)
+    monkeypatch.setenv("DADE_SCAN_TAIL", tail)
+    c, d, sc = ix.search(Q, 10, 8, 16, 0.005, stats=True)
+    assert torch.equal(a, c) and torch.equal(b, d)
+    assert sa["tested"] == sc["tested"] and sa["dims_scanned"] == sc["dims_scanned"]
+
+
 def test_save_load_roundtrip(sift_small, tmp_path):
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     from paper_2404_16322_b200 import Index
