@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
   __shared__ float sg[kGmWarps][32 * GPL];
   __shared__ double cd[kGmWarps][kGmCap];
   __shared__ int32_t cc[kGmWarps][kGmCap];
-  __shared__ float xstage[kGmWarps][32 * (kXbDim + 1)];
+  __shared__ __align__(16) float xstage[kGmWarps][kXbStage];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * kGmWarps + w;
   if (row >= m) return;
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin_wide(
   __shared__ float sg[1][32 * GPL];
   __shared__ double cd[1][kGmCap];
   __shared__ int32_t cc[1][kGmCap];
-  __shared__ float xstage[kGmWarps][32 * (kXbDim + 1)];
+  __shared__ __align__(16) float xstage[kGmWarps][kXbStage];
   __shared__ int s_cnt;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, w = 0;
   const int64_t row = blockIdx.x;

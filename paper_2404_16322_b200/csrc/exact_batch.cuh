@@ -8,13 +8,17 @@
 
 namespace dade {
 
-constexpr int kXbDim = 32;  // dims staged per pass; stage = 32 x (kXbDim + 1) floats per warp
+constexpr int kXbDim = 32;  // dims staged per pass
+// per-warp stage (floats, 8-byte aligned): 32 candidate rows x (kXbDim + 1), then the query's
+// current slice as kXbDim doubles (read by every lane with one broadcast LDS.64 per dimension)
+constexpr int kXbStage = 32 * (kXbDim + 1) + 2 * kXbDim;
 
 // c: this lane's candidate row index (< 0: none); a: the query row (global, broadcast reads);
 // nc (warp-uniform, <= 32): candidates are in lanes [0, nc) — only those rows are staged
 __device__ __forceinline__ double exact_batch32(const float* __restrict__ a, const float* __restrict__ B, int D,
                                                 int32_t c, float* stage, int lane, int nc = 32) {
   double acc = 0.0;
+  double* qd = reinterpret_cast<double*>(stage + 32 * (kXbDim + 1));
   // the next slice's 32 loads are issued before the current slice is accumulated
   float v[32];
   auto load = [&](int j0) {
@@ -39,12 +43,13 @@ __device__ __forceinline__ double exact_batch32(const float* __restrict__ a, con
 #pragma unroll
         for (int i = i0; i < i0 + 8; ++i) stage[i * (kXbDim + 1) + lane] = v[i];
       }
+    qd[lane] = lane < w ? (double)__ldg(a + j0 + lane) : 0.0;
     __syncwarp();
     if (j0 + kXbDim < D) load(j0 + kXbDim);
     if (c >= 0) {
       const float* sr = stage + lane * (kXbDim + 1);
       for (int jj = 0; jj < w; ++jj) {
-        const double t = __dsub_rn((double)__ldg(a + j0 + jj), (double)sr[jj]);
+        const double t = __dsub_rn(qd[jj], (double)sr[jj]);
         acc = __dadd_rn(acc, __dmul_rn(t, t));
       }
     }
