@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Summarise an ncu launch list (gpu__time_duration.sum per launch) for the LAST dade_search
-step of a bench run: kernel, launches, total and share of the step. Usage: launch_shares.py launches.csv"""
+"""Summarise an ncu launch list (gpu__time_duration.sum per launch) for the last timed device
+dade_search step of a bench run: kernel, duration and share of the step. Usage: launch_shares.py launches.csv"""
 import csv
 import sys
 
@@ -9,9 +9,18 @@ h = next(r for r in rows if "Kernel Name" in r)
 i0 = rows.index(h)
 kn, mv = h.index("Kernel Name"), h.index("Metric Value")
 seq = [(r[kn], float(r[mv].replace(",", ""))) for r in rows[i0 + 1:] if len(r) == len(h)]
-# the last step = everything after the last torch fill kernel (the untimed L2 flush)
-last_fill = max(i for i, (k, _) in enumerate(seq) if "FillFunctor" in k)
-step = [(k, v) for k, v in seq[last_fill + 1:] if "FillFunctor" not in k]
+# steps are separated by the torch fill kernel (the untimed L2 flush); the last timed DEVICE step
+# is the last one with a single k_rotate (the e2e steps after it rotate + probe in two halves)
+steps, cur = [], []
+for k, v in seq:
+    if "FillFunctor" in k:
+        if cur:
+            steps.append(cur)
+        cur = []
+    else:
+        cur.append((k, v))
+steps.append(cur)
+step = [s for s in steps if sum("k_rotate" in k for k, _ in s) == 1 and any("k_scan" in k for k, _ in s)][-1]
 tot = sum(v for _, v in step)
 print(f"| kernel | duration (us) | share of step |")
 print(f"|---|---|---|")
