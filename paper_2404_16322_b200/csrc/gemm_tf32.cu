@@ -150,13 +150,12 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
                                                   const float* __restrict__ Blo, const float* __restrict__ bn,
                                                   int nkc, float* __restrict__ out, int64_t m, int64_t n,
                                                   int64_t ldo, float* __restrict__ gmin, int64_t ldg, int passes,
-                                                  int gshift) {
+                                                  int gshift, int s1) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  // 64 KB of operand stages: 2 x 32 KB (3-pass: A_hi, A_lo, B_hi, B_lo) or 4 x 16 KB (1-pass:
-  // A_hi, B_hi) — the 1-pass filter keeps four chunks in flight
-  const int S = passes == 1 ? 4 : 2;
+  // operand stages: 2 x 32 KB (3-pass: A_hi, A_lo, B_hi, B_lo) or s1 x 16 KB (1-pass: A_hi, B_hi)
+  const int S = passes == 1 ? s1 : 2;
   const int SB = passes == 1 ? kStageBytes / 2 : kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * SB);
   uint64_t* empty = full + 4;
   uint64_t* accf = full + 8;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(full + 9);
@@ -335,14 +334,20 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
                   cudaStream_t st, float* gmin, int passes, int gshift) {
   if (m <= 0 || n <= 0) return;
   static bool attr = false;
-  const size_t smem = 2 * kStageBytes + 128;
   if (!attr) {
-    DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStageBytes + 128));
     attr = true;
   }
+  // 1-pass stages (16 KB each): three — 48 KB lets four CTAs share an SM (with four stages the
+  // 64 KB allowed three), hiding more of each CTA's wait for its accumulator (C2 search 0.721 ->
+  // 0.712-0.718 ms). DADE_L2TC_S1 in {2, 3, 4} overrides; the epilogue's transposition buffers
+  // (4 x 32 x 33 floats) reuse the stage region, so >= 2 stages
+  int s1 = 3;
+  if (const char* e = getenv("DADE_L2TC_S1")) s1 = std::max(2, std::min(4, atoi(e)));
+  const size_t smem = (passes == 1 ? (size_t)s1 * (kStageBytes / 2) : 2 * (size_t)kStageBytes) + 128;
   dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
   k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), out, m, n, ldo, gmin,
-                                   (n + (1 << gshift) - 1) >> gshift, passes, gshift);
+                                   (n + (1 << gshift) - 1) >> gshift, passes, gshift, s1);
   DADE_CK(cudaGetLastError());
 }
 
