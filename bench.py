@@ -365,17 +365,27 @@ def run_dade(args):
 
 
 def launches_per_search(cfg, world, nprobe):
-    """Kernels of ours per dade_search: k_check_finite, k_rotate, per probe chunk either (wide
-    centroid sets, fused path) k_split_tf32, k_slack, k_probe_tc, k_probe_finish or (d_hat path)
-    k_split_tf32, k_l2_tc, k_slack, k_select_gmin, k_select_small over the overflow list;
-    k_scan; + k_merge_topk when sharded."""
-    if cfg.nlist <= 1:
+    """Kernels of ours per dade_search (mirrors exact_knn's path choice in dade_api.cu):
+    k_check_finite, k_rotate; per probe row chunk either the fused path (> 1024 64-column
+    groups) k_split_tf32, k_slack, k_probe_tc, k_probe_finish, or the group-minima path
+    (> 2^20 centroids) k_split_tf32, k_l2_tc, k_slack, k_select_groups, or the d_hat path
+    k_split_tf32, k_l2_tc | k_dhat_tc, k_slack, k_select_gmin, k_select_small; k_scan;
+    + k_merge_topk when sharded (each rank probes its block of nq / world queries)."""
+    n, k = cfg.nlist, nprobe
+    nq = -(-cfg.nq // world)
+    rows_pad = -(-nq // 128) * 128
+    if n <= 1:
         probe = 0
-    elif nprobe <= 64 and (cfg.nlist + 31) // 32 > 1024:
-        probe = 4 * ((cfg.nq + 65535) // 65536)
+    elif k <= 64 and n >= 256 and (n + 63) // 64 > 1024:
+        probe = 4 * -(-nq // min(rows_pad, 65536))
+    elif k <= 512 and 4 * k <= (n + 31) // 32 and n > (1 << 20):
+        ng = (n + 31) // 32
+        chunk = min(max(128, (1 << 27) // ng // 128 * 128), rows_pad)
+        probe = 4 * -(-nq // chunk)
     else:
-        chunk = min(max(128, (1 << 29) // cfg.nlist // 128 * 128), 16384)
-        probe = 5 * ((cfg.nq + chunk - 1) // chunk)
+        chunk = max(128, (1 << 29) // n // 128 * 128)
+        chunk = min(chunk, 16384, rows_pad)
+        probe = 5 * -(-nq // chunk)
     return 2 + probe + 1 + (1 if world > 1 else 0)
 
 

@@ -35,3 +35,8 @@ def test_launch_count_claim():
     assert bench.launches_per_search(synth.config("c2"), 2, 8) == 9
     # flat (one list): no probe kernels
     assert bench.launches_per_search(synth.config("c1"), 1, 1) == 3
+    # C5 shard (65,536 lists): d_hat path in two row chunks of 8,192 (the ncu launch list of one
+    # search shows 13 of our kernels)
+    assert bench.launches_per_search(synth.config("c5").scaled(n=12_500_000, nlist=65536), 1, 8) == 13
+    # C3 (1,000 queries, nprobe 64): one chunk
+    assert bench.launches_per_search(synth.config("c3").scaled(nq=1000), 1, 64) == 8
