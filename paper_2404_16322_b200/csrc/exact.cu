@@ -433,30 +433,30 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin(
 #pragma unroll
   for (int j = 0; j < GPL; ++j) gv[j] = lane + 32 * j < ng ? gm[row * ng + lane + 32 * j] : INFINITY;
   float E;
-  if (k <= 16) {  // k rounds of a warp-wide minimum (keys (value bits, group) are unique)
-    float rem[GPL];
+  if (k <= 16) {  // k rounds of a warp-wide minimum (REDUX on the value bits: minima are >= 0 or
+    // +inf, so unsigned order is float order); each round removes ONE occurrence of the minimum,
+    // so E is the k-th smallest value of the multiset whichever tied group is removed
+    unsigned rem[GPL];
 #pragma unroll
-    for (int j = 0; j < GPL; ++j) rem[j] = gv[j];
-    unsigned long long key = 0;
+    for (int j = 0; j < GPL; ++j) rem[j] = __float_as_uint(gv[j]);
+    unsigned mn = 0;
     for (int r = 0; r < k; ++r) {
-      unsigned long long mine = ~0ull;
+      unsigned lm = rem[0];
 #pragma unroll
-      for (int j = 0; j < GPL; ++j) {
-        const unsigned long long kk = ((unsigned long long)__float_as_uint(rem[j]) << 32) | (unsigned)(lane + 32 * j);
-        mine = kk < mine ? kk : mine;
+      for (int j = 1; j < GPL; ++j) lm = min(lm, rem[j]);
+      mn = __reduce_min_sync(0xffffffffu, lm);
+      const unsigned who = __ballot_sync(0xffffffffu, lm == mn);
+      if (lane == __ffs(who) - 1) {
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < GPL; ++j)
+          if (!done && rem[j] == mn) {
+            rem[j] = 0xffffffffu;  // removed: above every value, +inf included
+            done = true;
+          }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, mine, o);
-        mine = t < mine ? t : mine;
-      }
-      key = mine;
-      const int gsel = (int)(key & 0xffffffffu);
-#pragma unroll
-      for (int j = 0; j < GPL; ++j)
-        if (lane + 32 * j == gsel) rem[j] = __uint_as_float(0x7f800001u);  // removed (NaN: sorts last as bits)
     }
-    E = __uint_as_float((unsigned)(key >> 32));
+    E = __uint_as_float(mn);
   } else {  // bitonic sort of the group minima (GPL per lane)
     float* g = sg[w];
 #pragma unroll
@@ -535,30 +535,30 @@ __global__ void __launch_bounds__(kGmWarps * 32) k_select_gmin_wide(
 #pragma unroll
   for (int j = 0; j < GPL; ++j) gv[j] = lane + 32 * j < ng ? gm[row * ng + lane + 32 * j] : INFINITY;
   float E;
-  if (k <= 16) {  // k rounds of a warp-wide minimum (keys (value bits, group) are unique)
-    float rem[GPL];
+  if (k <= 16) {  // k rounds of a warp-wide minimum (REDUX on the value bits: minima are >= 0 or
+    // +inf, so unsigned order is float order); each round removes ONE occurrence of the minimum,
+    // so E is the k-th smallest value of the multiset whichever tied group is removed
+    unsigned rem[GPL];
 #pragma unroll
-    for (int j = 0; j < GPL; ++j) rem[j] = gv[j];
-    unsigned long long key = 0;
+    for (int j = 0; j < GPL; ++j) rem[j] = __float_as_uint(gv[j]);
+    unsigned mn = 0;
     for (int r = 0; r < k; ++r) {
-      unsigned long long mine = ~0ull;
+      unsigned lm = rem[0];
 #pragma unroll
-      for (int j = 0; j < GPL; ++j) {
-        const unsigned long long kk = ((unsigned long long)__float_as_uint(rem[j]) << 32) | (unsigned)(lane + 32 * j);
-        mine = kk < mine ? kk : mine;
+      for (int j = 1; j < GPL; ++j) lm = min(lm, rem[j]);
+      mn = __reduce_min_sync(0xffffffffu, lm);
+      const unsigned who = __ballot_sync(0xffffffffu, lm == mn);
+      if (lane == __ffs(who) - 1) {
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < GPL; ++j)
+          if (!done && rem[j] == mn) {
+            rem[j] = 0xffffffffu;  // removed: above every value, +inf included
+            done = true;
+          }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, mine, o);
-        mine = t < mine ? t : mine;
-      }
-      key = mine;
-      const int gsel = (int)(key & 0xffffffffu);
-#pragma unroll
-      for (int j = 0; j < GPL; ++j)
-        if (lane + 32 * j == gsel) rem[j] = __uint_as_float(0x7f800001u);  // removed (NaN: sorts last as bits)
     }
-    E = __uint_as_float((unsigned)(key >> 32));
+    E = __uint_as_float(mn);
   } else {  // bitonic sort of the group minima (GPL per lane)
     float* g = sg[w];
 #pragma unroll
