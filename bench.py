@@ -2,14 +2,18 @@
 """bench.py — DADE search throughput on B200 (BASELINE.json metric: QPS at recall@10 = 0.95;
 scanned dim-floats/s as a fraction of the HBM roofline).
 
-Workload (N=1): configs[1], the SIFT-shaped IVF-DADE config: 1M x 128 synthetic integer-valued
-base, 10,000 queries, 4,096 IVF lists, K=10, delta_d=16, significance 0.005 (r = 0.995). One
-"step" = one dade_search call over all 10,000 queries (rotation, exact probe, progressive scan,
-top-K), at the smallest swept nprobe whose recall@10 vs the exact top-10 is >= 0.95.
-N>1 (torchrun): the base is sharded by contiguous id ranges, every rank searches all queries on
-its shard, local top-K lists are combined by an NCCL all-gather + the merge kernel.
+Workload (N=1, default): configs[3], the Deep-shaped IVF-DADE config — the largest config that
+fits one GPU, and the one BASELINE.json runs at 1/2/4/8 GPUs: 10M x 96 unit-norm synthetic base,
+10,000 queries, 16,384 IVF lists, K=10, delta_d=16, significance 0.005 (r = 0.995). One "step" =
+one dade_search call over all 10,000 queries (rotation, exact probe, progressive scan, top-K), at
+the smallest swept nprobe whose recall@10 vs the exact top-10 is >= 0.95.
+N>1: the same workload (strong scaling: total work fixed) sharded by contiguous id ranges, one
+rank per GPU; `--gpus N` launches the N ranks itself (torch.distributed.run, 127.0.0.1) unless it
+already runs under torchrun. Every rank rotates + probes nq/N queries, the prepared queries are
+all-gathered, every rank scans all queries on its shard, and the local top-K lists are combined
+by an all-gather + the merge kernel.
 
---impl reference: the CPU oracle (oracle/), timed on host cores on a bounded sample of the
+--impl reference: the CPU oracle (oracle/), timed on all host cores on a bounded sample of the
 same workload (the paper's method has no public GPU reference).
 """
 from __future__ import annotations
@@ -114,6 +118,7 @@ def run_dade(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     if world > 1:
         # NCCL over NVLink in production; DADE_DIST_BACKEND=gloo runs the same multi-rank code path
         # on a single visible GPU as a functional check (its timings are not a measurement)
@@ -316,11 +321,16 @@ def run_dade(args):
     scan_avg_ms = sum(scan_ms) / len(scan_ms)
     achieved = alg_bytes / (scan_avg_ms / 1e3) / 1e9
     peak, peak_src = peaks()
-    traffic = None
+    # ncu --set full of the same launch (profiles/scan_dram_traffic.json: dram__bytes_read.sum +
+    # dram__bytes_write.sum of k_scan, per config, nprobe and world size; null if not captured)
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "scan_dram_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(f"{cfg.name}_nprobe{chosen}")
+            tj = json.load(open(tf))
+            ent = tj.get("captures", {}).get(f"{cfg.name}_n{cfg.n}_nprobe{chosen}_world{world}")
+            if ent:
+                traffic, traffic_src = int(ent["dram_bytes"]), ent["source"]
         except Exception:
             traffic = None
 
@@ -332,10 +342,9 @@ def run_dade(args):
             "metric": "QPS at recall@10=0.95 (dade_search, all stages)",
             "value": round(value, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": f"synthetic (datagen/synth.py, seed 0; {SHAPE[cfg.name]} stand-in for the paper's datasets)",
-            "config": {"workload": f"{cfg.name}: IVF-DADE {SHAPE[cfg.name]} n={cfg.n} D={cfg.d} nq={cfg.nq} "
-                                   f"nlist={cfg.nlist} K={K} delta_d={dd} significance={ALPHA}",
+            "config": {"workload": workload_name(cfg),
                        "method": args.method, "method_param": METHOD_PARAM[args.method],
                        "nprobe": chosen, "recall@10": next(s["recall"] for s in sweep if s["nprobe"] == chosen),
                        "qps_interp_at_0.95": None if interp is None else round(interp, 1),
@@ -349,7 +358,9 @@ def run_dade(args):
                     "h2d_bytes_per_step": cfg.nq * cfg.d * 4, "d2h_bytes_per_step": cfg.nq * K * 12},
             "gpu_launches": args.steps * launches_per_search(cfg, world, chosen),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                         "dram_frac": None if traffic is None else
+                         round(traffic / (scan_avg_ms / 1e3) / 1e9 / peak, 4),
                          "kernel": "k_scan<DD>", "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": int(alg_bytes),
                          "scan_ms_per_launch": round(scan_avg_ms, 4),
@@ -391,45 +402,94 @@ def launches_per_search(cfg, world, nprobe):
 
 # ============================================================================ CPU oracle legs
 def _oracle_sample(cfg, nprobe, n_sub=50_000, nq=40):
-    """Bounded sample of the workload for the oracle: the C2 recipe on a 50k-row prefix of the
-    same base with nlist scaled to keep the average list size (n/nlist ~ 244), the same nprobe,
-    so each query tests the same number of candidates as the full workload."""
+    """Bounded sample of the workload for the oracle: the config's recipe on a 50k-row prefix of
+    the same base with nlist scaled to keep the average list size (C4: n/nlist ~ 610), the same
+    nprobe, K, Δd and α, so each query tests about as many candidates as in the full workload."""
     from oracle import dade_oracle as O
     nlist = max(1, round(cfg.nlist * n_sub / cfg.n))
     sub = cfg.scaled(n=n_sub, nlist=nlist)
     m = synth.model(cfg)
     X = synth.base(sub, m)
-    Q = synth.queries(cfg, m=m)[:nq]
+    Q = synth.queries(cfg, n=nq, m=m)
     Qc = synth.cal_queries(cfg, m=m)[:200]
     t0 = time.time()
     mean, R, lam = O.fit_rotation(X)
     cent = O.kmeans(X, nlist, iters=3)
     idx = O.build_index(X, cent, mean, R)
-    idx["cal"] = O.calibrate(X, idx, Qc, cfg.k, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
+    idx["cal"] = O.calibrate(X, idx, Qc, cfg.k, n_neg=cfg.n_neg, nprobe_neg=min(cfg.nprobe_neg, nlist), seed=0)
     log(f"[oracle] index n={n_sub} nlist={nlist} built in {time.time() - t0:.1f}s")
     return O, idx, Q, sub, nlist
 
 
-def cpu_baseline(cfg, nprobe, budget_s=20.0):
+# the forked workers share the oracle index (copy-on-write); one BLAS thread each
+_POOL_STATE = {}
+
+
+def _worker_init():
     try:
         from threadpoolctl import threadpool_limits
+        _POOL_STATE["limit"] = threadpool_limits(1)
     except Exception:
-        threadpool_limits = None
-    ctx = threadpool_limits(1) if threadpool_limits else None
+        pass
+
+
+def _worker_search(task):
+    """Search queries [q0, q1) of the sample one by one until `deadline` (wall clock); returns the
+    number done and the seconds spent."""
+    q0, q1, deadline = task
+    O, idx, Q, cfg, nprobe = (_POOL_STATE[k] for k in ("O", "idx", "Q", "cfg", "nprobe"))
+    t0, done = time.perf_counter(), 0
+    for q in range(q0, q1):
+        if deadline and time.time() > deadline:
+            break
+        O.search(idx, Q[q:q + 1], cfg.k, nprobe, cfg.delta_d, ALPHA)
+        done += 1
+    return done, time.perf_counter() - t0
+
+
+def _cpu_info():
+    model = "unknown"
     try:
-        O, idx, Q, sub, nlist = _oracle_sample(cfg, nprobe)
-        done, t0 = 0, time.time()
-        while done < len(Q) and time.time() - t0 < budget_s:
-            O.search(idx, Q[done:done + 1], cfg.k, nprobe, cfg.delta_d, ALPHA)
-            done += 1
-        el = time.time() - t0
-        return {"value": round(done / el, 3), "unit": "queries/s", "cores": 1, "kind": "oracle",
-                "sample": f"{done} queries of {cfg.name}, oracle index on a {sub.n}-row prefix with nlist={nlist} "
-                          f"(same ~{cfg.n // cfg.nlist} rows/list), nprobe={nprobe}, K={cfg.k}, "
-                          f"delta_d={cfg.delta_d}, alpha={ALPHA}; float64 NumPy, 1 BLAS thread"}
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def _oracle_pool(cfg, nprobe, nq):
+    import multiprocessing as mp
+    O, idx, Q, sub, nlist = _oracle_sample(cfg, nprobe, nq=nq)
+    _POOL_STATE.update(O=O, idx=idx, Q=Q, cfg=cfg, nprobe=nprobe)
+    cores, model = _cpu_info()
+    pool = mp.get_context("fork").Pool(cores, initializer=_worker_init)
+    return pool, cores, model, sub, nlist
+
+
+def cpu_baseline(cfg, nprobe, budget_s=15.0):
+    """The oracle as it stands, float64 NumPy, one process per host core (1 BLAS thread each),
+    each worker searching its own queries until the time budget runs out."""
+    cores, _ = _cpu_info()
+    nq = 64 * cores
+    pool, cores, model, sub, nlist = _oracle_pool(cfg, nprobe, nq)
+    try:
+        per = nq // cores
+        deadline = time.time() + budget_s
+        t0 = time.perf_counter()
+        res = pool.map(_worker_search, [(w * per, (w + 1) * per, deadline) for w in range(cores)])
+        el = time.perf_counter() - t0
     finally:
-        if ctx is not None:
-            ctx.__exit__(None, None, None)
+        pool.close()
+        pool.join()
+    done = sum(r[0] for r in res)
+    val = done / el
+    return {"value": round(val, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "per_core": round(val / cores, 3), "cpu_model": model,
+            "sample": f"{done} queries of {cfg.name} in {el:.1f} s on {cores} worker processes (1 BLAS thread "
+                      f"each), oracle index on a {sub.n}-row prefix of the same base with nlist={nlist} (same "
+                      f"~{cfg.n // cfg.nlist} rows/list), nprobe={nprobe}, K={cfg.k}, delta_d={cfg.delta_d}, "
+                      f"alpha={ALPHA}; float64 NumPy"}
 
 
 def run_reference(args):
@@ -440,40 +500,55 @@ def run_reference(args):
     if args.nq:
         cfg = cfg.scaled(nq=args.nq)
     nprobe = args.nprobe or REF_NPROBE.get(cfg.name, 8)
-    try:
-        from threadpoolctl import threadpool_limits
-        ctx = threadpool_limits(1)
-    except Exception:
-        ctx = None
-    O, idx, Q, sub, nlist = _oracle_sample(cfg, nprobe, nq=max(args.steps + args.warmup, 1) * 4)
-    per_step = 4
+    cores, _ = _cpu_info()
+    per_step = 2 * cores                      # two queries per worker per step
+    steps = args.warmup + args.steps
+    pool, cores, model, sub, nlist = _oracle_pool(cfg, nprobe, per_step * steps)
     ts = []
-    for s in range(args.warmup + args.steps):
-        qs = Q[s * per_step:(s + 1) * per_step]
-        t0 = time.perf_counter()
-        O.search(idx, qs, cfg.k, nprobe, cfg.delta_d, ALPHA)
-        if s >= args.warmup:
-            ts.append(time.perf_counter() - t0)
+    try:
+        for s in range(steps):
+            tasks = [(s * per_step + 2 * w, s * per_step + 2 * w + 2, 0) for w in range(cores)]
+            t0 = time.perf_counter()
+            pool.map(_worker_search, tasks)
+            if s >= args.warmup:
+                ts.append(time.perf_counter() - t0)
+    finally:
+        pool.close()
+        pool.join()
     tot = sum(ts)
     val = per_step * len(ts) / tot
+    sample = (f"each step: {per_step} queries ({2} per worker process, {cores} processes, 1 BLAS thread each) on an "
+              f"oracle index over a {sub.n}-row prefix of the same base (nlist={nlist}, same ~{cfg.n // cfg.nlist} "
+              f"rows per list), nprobe={nprobe}")
     out = {"impl": "reference", "metric": "QPS at recall@10=0.95 (dade_search, all stages)",
            "value": round(val, 3), "unit": "queries/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(ts), 3),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (datagen/synth.py, seed 0)",
-           "config": {"workload": f"{cfg.name}: IVF-DADE {SHAPE[cfg.name]} n={cfg.n} D={cfg.d} nq={cfg.nq} "
-                                  f"nlist={cfg.nlist} K={cfg.k} delta_d={cfg.delta_d} significance={ALPHA}",
-                      "nprobe": nprobe, "method": "bsa_p",
-                      "sample": f"each step: {per_step} queries on an oracle index over a {sub.n}-row prefix of the "
-                                f"same base (nlist={nlist}, same ~{cfg.n // cfg.nlist} rows per list)"},
-           "cpu_baseline": {"value": round(val, 3), "unit": "queries/s", "kind": "oracle", "cores": 1,
-                            "sample": f"{per_step} queries per step on a {sub.n}-row prefix index"},
+           "config": {"workload": workload_name(cfg), "nprobe": nprobe, "method": "bsa_p", "sample": sample},
+           "cpu_baseline": {"value": round(val, 3), "unit": "queries/s", "kind": "oracle", "cores": cores,
+                            "per_core": round(val / cores, 3), "cpu_model": model, "sample": sample},
            "e2e": {"value": round(val, 3), "unit": "queries/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    if ctx is not None:
-        ctx.__exit__(None, None, None)
     print(json.dumps(out), flush=True)
     return out
+
+
+def workload_name(cfg):
+    return (f"{cfg.name}: IVF-DADE {SHAPE[cfg.name]} n={cfg.n} D={cfg.d} nq={cfg.nq} nlist={cfg.nlist} "
+            f"K={cfg.k} delta_d={cfg.delta_d} significance={ALPHA}")
+
+
+def relaunch_distributed(args):
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run with N ranks
+    (one per GPU, rendezvous on 127.0.0.1) and pass its exit code through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -482,7 +557,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dade", choices=["dade", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4", help="c1..c5 (default c4: the largest single-GPU config)")
     ap.add_argument("--method", default="bsa_p", choices=["bsa_p", "adsampling", "bsa_res"],
                     help="per-step correction: the paper's data-driven BSA-p (default, the headline), or the "
                          "NEXT-1 comparisons ADSampling (eps0 = 2.1, random rotation) / BSA-res (m = 8)")
@@ -492,12 +567,14 @@ def main():
     ap.add_argument("--nlist", type=int, default=0)
     ap.add_argument("--nq", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "dade":
         log("warning: fewer than 3 warm-up steps")
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     else:
         run_dade(args)
 

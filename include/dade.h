@@ -46,6 +46,7 @@ typedef enum {
   DADE_ERR_NONFINITE = 4,  /* NaN/Inf in an input array */
   DADE_ERR_OOM = 5,        /* device allocation failed */
   DADE_ERR_CUDA = 6,       /* CUDA runtime error */
+  DADE_ERR_NCCL = 7,       /* NCCL error (multi-rank calls after dade_set_comm), or libnccl missing */
   DADE_ERR_UNSUPPORTED = 8 /* valid but outside what the kernels implement (D%16, K>256, ...) */
 } dade_status;
 
@@ -92,7 +93,11 @@ dade_status dade_pca_cov_partial(dade_index* idx, const float* X, int64_t n, int
 dade_status dade_set_rotation_from_cov(dade_index* idx, const double* mean, const double* cov_sum,
                                        int64_t count);
 
-/* Host copies of the rotation: mean[D], R[D*D] (row-major, rows = directions), eigvals[D]. */
+/* Host copies of the rotation: mean[D], R[D*D] (row-major, rows = directions), eigvals[D].
+ * dade_set_rotation installs a rotation (host arrays; eigvals may be NULL: then BSA-res, which
+ * needs them, returns STATE). Installing a rotation — by either setter or by fit — discards the
+ * IVF layout and the calibration built in the previous basis (build_ivf / set_ivf again).
+ * Errors: ARG (NULL), NONFINITE. */
 dade_status dade_get_rotation(const dade_index* idx, double* mean, double* R, double* eigvals);
 dade_status dade_set_rotation(dade_index* idx, const double* mean, const double* R,
                               const double* eigvals);
@@ -117,6 +122,15 @@ dade_status dade_get_ivf(const dade_index* idx, int64_t* off, int64_t* row_id, i
 dade_status dade_get_sizes(const dade_index* idx, int64_t* n, int* nlist);
 /* Host copy of the blocked layout as list-major rows: Xrot[n*D] (row p = x~ of row_id[p]). */
 dade_status dade_get_layout(const dade_index* idx, float* Xrot);
+/* Inject a ready IVF + layout (parity tests, or an index built elsewhere) in the
+ * CURRENT rotation's basis: Xrot device n x D fp32 ROTATED rows x~ = R(x - mu) in list-major order
+ * (row p = x~ of row_id[p]; copied into the blocked layout); row_id host n int64 global ids,
+ * off host nlist+1 int64 list offsets (lists hold ids ascending, ids = a permutation of
+ * [id_base, id_base+n), as dade_get_ivf returns them); centroids device nlist x D fp32 raw-space
+ * (the probe's space). Discards the calibration. Errors: STATE (no rotation), ARG
+ * (inconsistent off / row_id, ids >= 2^31), NONFINITE, OOM, CUDA. */
+dade_status dade_set_ivf(dade_index* idx, const float* Xrot, int64_t n, int64_t id_base, const int64_t* row_id,
+                         const int64_t* off, int nlist, const float* centroids);
 
 /* ---------------------------------------------------------------- a3 calibrate
  * X: device n x D, the raw rows given to dade_build_ivf (the index keeps only the rotated layout).
@@ -137,7 +151,8 @@ dade_status dade_set_calibration(dade_index* idx, int K, int n0, int n_cls, cons
 
 /* ---------------------------------------------------------------- a4..a8 search
  * Q: device nq x D raw queries; ids (int64) / dists (fp32 squared L2) device nq x K, ascending by
- * (dist, id); missing slots -> id -1, dist +inf. delta_d: positive multiple of 16 dividing D.
+ * (dist, id); missing slots -> id -1, dist +inf. delta_d: any positive multiple of 16 dividing D
+ * (D / delta_d <= DADE_MAX_STEPS).
  * significance alpha in [0,1): alpha = 0 disables pruning (exact IVF); alpha > 0 uses
  * beta'_d = v_d[k-1], k = clamp(ceil((1 - alpha*delta_d/D) * n0), 1, n0) (R4, R5).
  * Per query: q~ = R(q-mu) (fp64 accumulation), exact probes (fp64-certified, ties to lower id),
@@ -222,11 +237,11 @@ dade_status dade_search_prepared(dade_index* idx, const float* qrot, const int32
 
 /* Same as dade_search with HOST Q/ids/dists: the H2D copy of Q and the D2H copy of the results
  * are part of the call (synchronous; returns when ids/dists are written). The copies run on two
- * copy streams; with DADE_HOST_CHUNKS=c (default 1) the batch is cut into c chunks pipelined so
+ * copy streams; with DADE_OPT_HOST_CHUNKS = c (default 1) the batch is cut into c chunks pipelined so
  * that chunk c's H2D overlaps the search of chunk c-1 and its D2H the search of chunk c+1 (not
  * the default: measured slower on C2). Each query's result is independent of
  * the chunking. Unchunked batches of >= 4,096 queries copy Q in two halves and rotate + probe
- * each half as it lands (DADE_HOST_PREP_CHUNKS overrides), then scan once. Pinned host memory
+ * each half as it lands (DADE_OPT_HOST_PREP_CHUNKS overrides), then scan once. Pinned host memory
  * gives asynchronous copies;
  * pageable memory works but serialises them. With stats != NULL the batch runs unchunked.
  * Used for the end-to-end (e2e) measurement. Errors: as dade_search. */
@@ -249,6 +264,30 @@ dade_status dade_search_host(dade_index* idx, const float* Q_host, int nq, int K
 #define DADE_EST_RESIDUAL 1
 dade_status dade_estimate_knn(dade_index* idx, const float* Q, int nq, int d, int method, int K, int64_t* ids,
                               float* est);
+
+/* Parity run of the search (SURVEY §8(c) "decisions identical outside R21's tie band"): the same
+ * search (one warp per query; decisions and results do not depend on the warp split), plus a
+ * decision log: for every tested candidate one record of 3 int32 {query, global id, dims read}
+ * (dims = s * delta_d if the classifier at step s pruned it, D if it reached the exact distance),
+ * in no particular order. log: device log_cap x 3 int32; *log_count (host) = records produced
+ * (> log_cap: the rest were dropped). method BSA_P or ADSAMPLING. Synchronous.
+ * Errors: as dade_search_method; UNSUPPORTED for BSA_RES. */
+dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int nprobe, int delta_d, int method,
+                            double param, int64_t* ids, float* dists, int32_t* log, int64_t log_cap,
+                            int64_t* log_count);
+
+/* Tuning options of one index (defaults are the measured best; the alternatives exist for A/B
+ * measurement and for tests proving every path returns identical results). Errors: ARG (unknown
+ * option or value). */
+#define DADE_OPT_KNN_PATH 1        /* exact-KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima */
+#define DADE_OPT_PROBE_PASSES 2    /* tf32 passes of the probe filter: 0 auto (1 if D < 512, else 3), 1, 3 */
+#define DADE_OPT_SCAN_WARPS 3      /* warps per query in the scan: 0 auto, 1, 2, 4, 8 */
+#define DADE_OPT_SCAN_ORDER 4      /* 1: scan queries grouped by their nearest probed list */
+#define DADE_OPT_SCAN_TAIL 5       /* X > 0: last X queries in a concurrent 4-warps-per-query scan */
+#define DADE_OPT_HOST_CHUNKS 6     /* dade_search_host: chunks pipelined with the copies (default 1) */
+#define DADE_OPT_HOST_PREP_CHUNKS 7 /* dade_search_host: rotation+probe chunks ahead of one scan (0 auto) */
+#define DADE_OPT_DHAT_ARES 8       /* 1: A-resident d_hat writer for very wide probe rows */
+dade_status dade_set_option(dade_index* idx, int option, int64_t value);
 
 /* Exact probes (a5 alone): probes[nq*nprobe] int32 device, ordered by (exact fp64 dist, id). */
 dade_status dade_probe(dade_index* idx, const float* Q, int nq, int nprobe, int32_t* probes);

@@ -377,7 +377,7 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
     out_ids = np.full((Q.shape[0], K), -1, dtype=np.int64)
     out_d = np.full((Q.shape[0], K), np.inf)
     st = {"tested": 0, "dims_scanned": 0, "survivors": 0, "pruned_at_step": np.zeros(ns, np.int64),
-          "n_epochs": 0, "decisions": []}
+          "n_epochs": 0, "decisions": [], "candidates": []}
     Qr = rotate(Q, index["mean"], index["R"])
     steps = np.arange(1, ns) * delta_d
     for qn in range(Q.shape[0]):
@@ -395,6 +395,7 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
                 P = np.cumsum((Xr[ids - base] - Qr[qn]) ** 2, axis=1)
                 keep = np.ones(len(ids), dtype=bool)
                 dims = np.full(len(ids), D)
+                margin = np.full(len(ids), np.inf)
                 if np.isfinite(tau) and ns > 1:
                     score = m[None, :] * P[:, steps - 1] + b[None, :]
                     if res:  # P_d + ‖x_r‖² + c_d, ‖x_r‖² = ‖x‖² − N_d
@@ -411,6 +412,16 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
                             s = first[i]
                             st["decisions"].append((qn, int(ids[i]), int(steps[s]),
                                                     float(score[i, s]), float(tau)))
+                        # closest call of each candidate over the tests it went through (up to and
+                        # including the deciding one): |score − τ| / (|m1·P| + |β'| + τ) — a decision
+                        # taken in another rounding (fp32 on the GPU, R21) can only differ where it is tiny
+                        scale = np.abs(m[None, :] * P[:, steps - 1]) + np.abs(b[None, :]) + tau
+                        rel = np.abs(score - tau) / scale
+                        last = np.where(anyp, first, ns - 2)
+                        upto = np.arange(ns - 1)[None, :] <= last[:, None]
+                        margin = np.where(upto, rel, np.inf).min(axis=1)
+                if log:
+                    st["candidates"].append((np.full(len(ids), qn), ids.copy(), dims.copy(), margin))
                 st["dims_scanned"] += int(dims.sum())
                 st["survivors"] += int(keep.sum())
                 cd = np.concatenate([top_d, P[keep, D - 1]])

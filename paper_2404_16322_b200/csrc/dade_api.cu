@@ -23,12 +23,27 @@ struct TcOp {
   void release() { hi.release(); lo.release(); norm.release(); maxn.release(); center.release(); csum.release(); rows = 0; }
 };
 
+// Tuning options (dade_set_option): every default is the measured best; the others exist for
+// A/B measurement and for the tests that prove each path returns identical results.
+struct Options {
+  int knn_path = 0;         // exact KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima
+  int probe_passes = 0;     // tf32 passes of the probe filter: 0 auto (1 if D < 512 else 3), 1, 3
+  int scan_warps = 0;       // warps per query in k_scan: 0 auto, 1, 2, 4, 8
+  int scan_order = 0;       // 1: scan queries grouped by their nearest probed list
+  int scan_tail = 0;        // last X queries scanned by a concurrent 4-warps-per-query launch
+  int host_chunks = 1;      // dade_search_host: searches pipelined with the copies
+  int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
+  int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
+};
+
 struct dade_index {
   int device = 0;
+  Options opt;
   cudaStream_t stream = nullptr;
   int D = 0;
   // rotation (a0)
   bool has_rot = false;
+  bool has_lam = false;  // eigenvalues known (fit_rotation, or given to set_rotation): BSA-res needs them
   std::vector<double> mean, R, lam;
   DBuf<double> R_d, mean_d;
   // IVF + layout (a1, a2)
@@ -50,7 +65,7 @@ struct dade_index {
   DBuf<int32_t> probes, cand, idx32;
   DBuf<double> d64;
   DBuf<int> flag, fflag, work, ovf;
-  DBuf<unsigned long long> counters;
+  DBuf<unsigned long long> counters, dlog_n;
   DBuf<int64_t> ids_tmp;
   DBuf<int> ordcnt;      // scan query order: per-list counts / cursors
   DBuf<int32_t> order;
@@ -174,13 +189,13 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   }
   // fused path only for very wide rows, where the d_hat matrix would not fit the group-minima
   // select (> 1024 groups; measured at 16,384 columns: d_hat path 0.31 ms, fused 0.61 ms);
-  // DADE_FUSED_PROBE=0/1 forces either path (tests cover both)
-  const char* fz = getenv("DADE_FUSED_PROBE");
-  const bool fused = k <= 64 && n >= 256 && (fz ? atoi(fz) != 0 : (n + 63) / 64 > 1024);
+  // DADE_OPT_KNN_PATH forces a path (tests cover each)
+  const int path = x->opt.knn_path;
+  const bool fused = k <= 64 && n >= 256 && (path ? path == 2 : (n + 63) / 64 > 1024);
   if (fused) {
     // fused filter GEMM + candidate tracking (probe_tc.cu): no m x n d_hat matrix
-    static int sms = 0;
-    if (!sms) DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device));
+    int sms = 0;
+    DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device));
     const int64_t chunk = std::min<int64_t>(tc_rows_pad(m), 65536);
     const int nsplit = probe_tc_splits(chunk, n, sms);
     const int C = probe_tc_cap(k);
@@ -200,8 +215,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   const int64_t ng = (n + 31) / 32;
   // group-minima-only path (no d_hat matrix): measured slower than the d_hat path at k <= 32
   // (32 exact fp64 columns per candidate group, uncoalesced); kept for very wide rows
-  const char* fg = getenv("DADE_PROBE_GROUPS");  // 1 forces the group path (measurement)
-  if (k <= 512 && (int64_t)k * 4 <= ng && (fg ? atoi(fg) != 0 : n > (int64_t)1 << 20)) {
+  if (k <= 512 && (int64_t)k * 4 <= ng && (path ? path == 3 : n > (int64_t)1 << 20)) {
     // the GEMM writes only 32-column group minima; exact fp64 distances for the columns of the
     // groups inside the certified window (no m x n d_hat matrix)
     int64_t chunk = std::max<int64_t>(128, ((int64_t)1 << 27) / ng / 128 * 128);
@@ -245,7 +259,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     // the warp-specialised d_hat writer pays off for very wide rows (measured on C5, 65,536
     // columns: 1.42 -> 1.19 ms); up to 16,384 columns the one-tile-per-CTA kernel with 3 CTAs/SM
     // is faster (C2 68 vs 97 us, C4 222 vs 358 us, C3 36 vs 42 us)
-    if (use_gmin && n > 32768 && dhat_ares_ok(D, passes))
+    if (use_gmin && n > 32768 && x->opt.dhat_ares && dhat_ares_ok(D, passes))
       launch_dhat_ares(x->a_tc.hi.p, x->a_tc.norm.p, mm, bop.hi.p, bop.norm.p, n, D, x->dmat.p, n, x->gmin.p,
                        gshift, x->stream);
     else if (use_gmin && n > 32768)
@@ -283,18 +297,22 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
 
 // passes of the probe's tensor-core filter: 1 (tf32 hi parts only: 1/3 of the MMAs and 1/2 of the
 // operand bytes, a ~40x wider but still rigorous certified window; the fp64 re-rank keeps the
-// result exact) unless DADE_PROBE_PASSES=3
+// result exact) unless DADE_OPT_PROBE_PASSES = 3
 // tf32 passes of the probe filter: 1 (hi x hi) with its wider certified window, or 3 (split
 // precision) when the rows are long — at D = 960 the 1-pass window holds so many near-ties that
 // the fp64 certification dominates (measured C3 step 1.95 -> 1.83 ms with 3 passes; C2, C4 and
-// the C5 shard, D <= 256, are faster with 1). DADE_PROBE_PASSES overrides.
-int probe_passes(int D) {
-  const char* e = getenv("DADE_PROBE_PASSES");
-  return e ? atoi(e) : (D >= 512 ? 3 : 1);
+// the C5 shard, D <= 256, are faster with 1). DADE_OPT_PROBE_PASSES overrides.
+int probe_passes(const dade_index* x) {
+  return x->opt.probe_passes ? x->opt.probe_passes : (x->D >= 512 ? 3 : 1);
 }
 
+// Installs x->mean / x->R on the device. A new rotation invalidates everything built in the old
+// basis: the rotated layout (and the IVF that owns it), the calibration table and the row norms.
 void upload_rotation(dade_index* x) {
   const int D = x->D;
+  x->has_ivf = false;
+  x->has_cal = false;
+  x->xnorm_ok = false;
   x->R_d.reserve((size_t)D * D);
   x->mean_d.reserve(D);
   DADE_CK(cudaMemcpyAsync(x->R_d.p, x->R.data(), sizeof(double) * D * D, cudaMemcpyHostToDevice, x->stream));
@@ -345,7 +363,7 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
   if (x->nlist == 1) {
     DADE_CK(cudaMemsetAsync(probes, 0, sizeof(int32_t) * nq, st));
   } else {
-    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, false, probe_passes(x->D));
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, false, probe_passes(x));
   }
   DADE_CK(cudaStreamWaitEvent(st, x->join, 0));
 }
@@ -356,47 +374,37 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
 #define DADE_C0_MULT 4
 #endif
 
-// dade_search_host's pipeline depth. Default 1: on C2 (tools/e2e_breakdown.py) a search cut in
-// two costs 0.19 ms more on the device (the scan's per-launch tail: 0.36 ms at 5,000 queries vs
-// 0.55 ms at 10,000) while the H2D it could hide is 0.20 ms, so chunking does not pay at these
-// batch sizes. DADE_HOST_CHUNKS=c sets c chunks.
-// DADE_SCAN_TAIL=X: the last X queries of a batch are scanned by a concurrent second launch with
-// DADE_SCAN_TAIL_G (default 4) warps per query (measurement switch; 0 = off). Measured on C2:
-// X = 500 -0.7% (noise), 1,000 +4%, 2,000 +13%; C4 X = 1,000 -0.5% — the one-warp scan is
-// throughput-bound, not tail-bound, so it stays off.
-int scan_tail(int nq) {
-  const char* e = getenv("DADE_SCAN_TAIL");
-  return e ? std::max(0, std::min(atoi(e), nq)) : 0;
-}
-int scan_tail_g() {
-  const char* e = getenv("DADE_SCAN_TAIL_G");
-  return e ? atoi(e) : 4;
-}
-
-// DADE_SCAN_ORDER=1: the scan takes the queries grouped by nearest probed list
+// dade_search_host's pipeline depth (DADE_OPT_HOST_CHUNKS, default 1): on C2
+// (tools/e2e_breakdown.py) a search cut in two costs 0.19 ms more on the device (the scan's
+// per-launch tail: 0.36 ms at 5,000 queries vs 0.55 ms at 10,000) while the H2D it could hide is
+// 0.20 ms, so chunking does not pay at these batch sizes.
+// DADE_OPT_SCAN_TAIL = X: the last X queries of a batch are scanned by a concurrent second launch
+// with 4 warps per query. Measured on C2: X = 500 -0.7% (noise), 1,000 +4%, 2,000 +13%; C4 X =
+// 1,000 -0.5% — the one-warp scan is throughput-bound, not tail-bound, so it stays off.
+// DADE_OPT_SCAN_ORDER = 1: the scan takes the queries grouped by nearest probed list
 // (launch_query_order). Off by default — measured: C2 scan unchanged (0.546 ms; ~3,500 queries are
 // in flight at once, so the order barely changes which lists are hot together) and +20 us for the
 // three ordering kernels; C4 scan -3.6% but the step only -1%; C3 no change.
-bool scan_order(int nq) {
-  if (const char* e = getenv("DADE_SCAN_ORDER")) return atoi(e) != 0 && nq > 0;
-  return false;
-}
-
-// dade_search_host's rotation + probe chunks when the search itself is not chunked
-// (DADE_HOST_PREP_CHUNKS overrides; default 2 for batches of >= 4,096 queries)
-int host_prep_chunks(int nq) {
-  if (const char* e = getenv("DADE_HOST_PREP_CHUNKS")) return std::max(1, std::min(atoi(e), std::max(nq, 1)));
+int scan_tail(const dade_index* x, int nq) { return std::max(0, std::min(x->opt.scan_tail, nq)); }
+bool scan_order(const dade_index* x, int nq) { return x->opt.scan_order != 0 && nq > 0; }
+// dade_search_host's rotation + probe chunks when the search itself is not chunked (default 2 for
+// batches of >= 4,096 queries)
+int host_prep_chunks(const dade_index* x, int nq) {
+  if (x->opt.host_prep_chunks > 0) return std::max(1, std::min(x->opt.host_prep_chunks, std::max(nq, 1)));
   return nq >= 4096 ? 2 : 1;
 }
+int host_chunks(const dade_index* x, int nq) { return std::max(1, std::min(x->opt.host_chunks, std::max(nq, 1))); }
 
-int host_chunks(int nq) {
-  if (const char* e = getenv("DADE_HOST_CHUNKS")) return std::max(1, std::min(atoi(e), std::max(nq, 1)));
-  return 1;
-}
+struct DecisionLog {
+  int32_t* buf = nullptr;  // device, cap x 3 int32
+  int64_t cap = 0;
+  int64_t* count = nullptr;  // host out
+};
 
 void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d, double alpha,
                int64_t* ids, float* dists, dade_stats* stats, int method = DADE_METHOD_BSA_P,
-               const float* qrot_in = nullptr, const int32_t* probes_in = nullptr) {
+               const float* qrot_in = nullptr, const int32_t* probes_in = nullptr,
+               const DecisionLog* dlog = nullptr) {
   const int D = x->D;
   DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
   DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
@@ -417,13 +425,11 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   else
     DADE_REQUIRE(alpha > 0.0 && std::isfinite(alpha), DADE_ERR_ARG, "eps0 / m must be positive");
   if (method == DADE_METHOD_BSA_RES)
-    DADE_REQUIRE(!x->lam.empty(), DADE_ERR_STATE, "BSA-res needs the rotation's eigenvalues");
+    DADE_REQUIRE(x->has_lam, DADE_ERR_STATE, "BSA-res needs the rotation's eigenvalues");
   const int nsteps = D / delta_d;
   DADE_REQUIRE(nsteps <= DADE_MAX_STEPS, DADE_ERR_UNSUPPORTED, "D/delta_d > DADE_MAX_STEPS");
   const int dd = delta_d / 16;
   const bool prune = alpha > 0.0 && nsteps > 1;
-  DADE_REQUIRE(!prune || dd == 1 || dd == 2 || dd == 4, DADE_ERR_UNSUPPORTED,
-               "with pruning, delta_d must be 16, 32 or 64");
   if (prune && method == DADE_METHOD_BSA_P) {
     DADE_REQUIRE(x->has_cal, DADE_ERR_STATE, "significance > 0 requires calibration");
     DADE_REQUIRE(x->calK == K, DADE_ERR_STATE, "K differs from the calibrated K");
@@ -449,7 +455,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   }
   // the scan's query order (counted with the probe stage, so the scan's events time k_scan alone)
   const int32_t* order = nullptr;
-  if (scan_order(nq)) {
+  if (scan_order(x, nq)) {
     x->ordcnt.reserve((size_t)x->nlist);
     x->order.reserve((size_t)nq);
     launch_query_order(probes, nq, nprobe, x->nlist, x->ordcnt.p, x->order.p, st);
@@ -504,17 +510,25 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     p.xnorm = x->xnorm.p;
     p.qconst = x->qconst.p;
   }
-  x->work.reserve(1);
-  DADE_CK(cudaMemsetAsync(x->work.p, 0, sizeof(int), st));
+  // work counters: [0] the main scan, [1] the tail scan; reserved (and zeroed) before any pointer
+  // into the buffer is taken
+  x->work.reserve(2);
+  DADE_CK(cudaMemsetAsync(x->work.p, 0, 2 * sizeof(int), st));
   p.work_counter = x->work.p;
   p.order = order;
-  const int tail = scan_tail(nq);
+  p.g_force = x->opt.scan_warps;
+  if (dlog) {
+    x->dlog_n.reserve(1);
+    DADE_CK(cudaMemsetAsync(x->dlog_n.p, 0, sizeof(unsigned long long), st));
+    p.dlog = dlog->buf;
+    p.dlog_cap = dlog->cap;
+    p.dlog_n = x->dlog_n.p;
+  }
+  const int tail = dlog ? 0 : scan_tail(x, nq);
   if (tail > 0 && tail < nq && !order) {
     // the last `tail` queries run as a second scan with 4 warps per query on the side stream:
     // its CTAs take the SM slots the first scan's warps free as they run out of queries, so the
     // first scan's tail is filled and the second's is 4x shorter
-    x->work.reserve(2);
-    DADE_CK(cudaMemsetAsync(x->work.p, 0, 2 * sizeof(int), st));
     const int q0 = nq - tail;
     ScanParams p2 = p;
     p.nq = q0;
@@ -525,7 +539,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     p2.out_d += (size_t)q0 * K;
     if (p2.qconst) p2.qconst += (size_t)q0 * (nsteps - 1);
     p2.work_counter = x->work.p + 1;
-    p2.g_force = scan_tail_g();
+    p2.g_force = 4;
     ensure_side(x);
     DADE_CK(cudaEventRecord(x->fork, st));
     DADE_CK(cudaStreamWaitEvent(x->side, x->fork, 0));
@@ -537,6 +551,12 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     launch_scan(p, st);
   }
   if (evs && !stats) DADE_CK(cudaEventRecord(x->ev[3], st));
+  if (dlog) {
+    unsigned long long cnt = 0;
+    DADE_CK(cudaMemcpyAsync(&cnt, x->dlog_n.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    *dlog->count = (int64_t)cnt;
+  }
   if (stats) {
     DADE_CK(cudaEventRecord(x->ev[3], st));
     unsigned long long c[4 + DADE_MAX_STEPS + 8];
@@ -588,7 +608,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->R_d.release(); x->mean_d.release(); x->cent.release(); x->layout.release();
   x->off_d.release(); x->row_id_d.release(); x->qrot.release(); x->dmat.release();
   x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
-  x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->ids_tmp.release(); x->ordcnt.release(); x->order.release(); x->xnorm.release(); x->qconst.release(); x->lam_d.release();
+  x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->dlog_n.release(); x->ids_tmp.release(); x->ordcnt.release(); x->order.release(); x->xnorm.release(); x->qconst.release(); x->lam_d.release();
   x->dists_tmp.release();
   x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release();
   for (auto& e : x->ev)
@@ -691,6 +711,7 @@ extern "C" dade_status dade_set_rotation_from_cov(dade_index* x, const double* m
   x->mean.assign(mean, mean + D);
   x->R = std::move(R);
   x->lam = std::move(lam);
+  x->has_lam = true;
   upload_rotation(x);
   API_END
 }
@@ -733,9 +754,13 @@ extern "C" dade_status dade_set_rotation(dade_index* x, const double* mean, cons
   const int D = x->D;
   for (int64_t i = 0; i < (int64_t)D * D; ++i)
     DADE_REQUIRE(std::isfinite(R[i]), DADE_ERR_NONFINITE, "non-finite R");
+  for (int i = 0; i < D; ++i) DADE_REQUIRE(std::isfinite(mean[i]), DADE_ERR_NONFINITE, "non-finite mean");
+  if (ev)
+    for (int i = 0; i < D; ++i) DADE_REQUIRE(std::isfinite(ev[i]), DADE_ERR_NONFINITE, "non-finite eigenvalues");
   x->mean.assign(mean, mean + D);
   x->R.assign(R, R + (size_t)D * D);
   if (ev) x->lam.assign(ev, ev + D); else x->lam.assign(D, 0.0);
+  x->has_lam = ev != nullptr;
   upload_rotation(x);
   API_END
 }
@@ -1295,7 +1320,7 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   // Pipeline: the batch is cut into chunks; chunk c's H2D (copy stream) overlaps the search of
   // chunk c-1 (library stream), whose results' D2H (second copy stream) overlaps chunk c's search.
   // Stats need one search over the whole batch, so they run unchunked.
-  int nch = host_chunks(nq);
+  int nch = host_chunks(x, nq);
   if (stats || nq <= 0) nch = 1;
   if (!x->h2d) {
     DADE_CK(cudaStreamCreateWithFlags(&x->h2d, cudaStreamNonBlocking));
@@ -1309,7 +1334,7 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   DADE_CK(cudaEventRecord(x->hev[0], st));  // the copies start after earlier work on the stream
   DADE_CK(cudaStreamWaitEvent(x->h2d, x->hev[0], 0));
   DADE_CK(cudaStreamWaitEvent(x->d2h, x->hev[0], 0));
-  const int npc_copy = nch == 1 && !stats && nq > 0 ? host_prep_chunks(nq) : 1;
+  const int npc_copy = nch == 1 && !stats && nq > 0 ? host_prep_chunks(x, nq) : 1;
   while ((int)x->hev.size() < npc_copy + 3) {
     cudaEvent_t e;
     DADE_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1332,7 +1357,7 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   }
   // one search: its rotation + probe (a4, a5) run per H2D chunk, so the copy of chunk c+1
   // overlaps the probe of chunk c; the scan (a6-a8) then runs once over the whole batch
-  const int npc = nch == 1 && !stats && nq > 0 ? host_prep_chunks(nq) : 1;
+  const int npc = nch == 1 && !stats && nq > 0 ? host_prep_chunks(x, nq) : 1;
   if (npc > 1) {
     DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
     DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
@@ -1411,7 +1436,7 @@ extern "C" dade_status dade_probe(dade_index* x, const float* Q, int nq, int npr
   DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "no IVF");
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
   DeviceGuard g(x->device);
-  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, true, probe_passes(x->D));
+  if (nq > 0) exact_knn(x, Q, nq, x->cent.p, x->nlist, nprobe, probes, nullptr, x->cent_tc, true, probe_passes(x));
   API_END
 }
 
@@ -1484,6 +1509,28 @@ extern "C" dade_status dade_save(const dade_index* x, const char* path) {
   API_END
 }
 
+// IVF/layout consistency shared by dade_load and dade_set_ivf: off monotone from 0 to n, row ids a
+// permutation of [id_base, id_base + n) ascending inside each list (lists hold ids
+// ascending). Fills assign (local id -> list) and pos_of (local id -> list-major position).
+static void check_ivf(int64_t n, int64_t id_base, int nlist, const std::vector<int64_t>& off,
+               const std::vector<int64_t>& rid, std::vector<int32_t>& assign, std::vector<int32_t>& pos_of) {
+  DADE_REQUIRE(n >= 1 && nlist >= 1 && nlist <= n, DADE_ERR_ARG, "ivf: nlist not in [1, n]");
+  DADE_REQUIRE(id_base >= 0 && id_base + n < ((int64_t)1 << 31), DADE_ERR_ARG, "ivf: ids must be < 2^31");
+  DADE_REQUIRE(off[0] == 0 && off[nlist] == n, DADE_ERR_ARG, "ivf: off must run from 0 to n");
+  for (int c = 0; c < nlist; ++c) DADE_REQUIRE(off[c] <= off[c + 1], DADE_ERR_ARG, "ivf: off not monotone");
+  assign.assign(n, -1);
+  pos_of.assign(n, 0);
+  for (int c = 0; c < nlist; ++c)
+    for (int64_t p = off[c]; p < off[c + 1]; ++p) {
+      const int64_t loc = rid[p] - id_base;
+      DADE_REQUIRE(loc >= 0 && loc < n, DADE_ERR_ARG, "ivf: row id outside [id_base, id_base + n)");
+      DADE_REQUIRE(assign[loc] < 0, DADE_ERR_ARG, "ivf: row id listed twice");
+      DADE_REQUIRE(p == off[c] || rid[p] > rid[p - 1], DADE_ERR_ARG, "ivf: ids not ascending inside a list");
+      assign[loc] = c;
+      pos_of[loc] = (int32_t)p;
+    }
+}
+
 extern "C" dade_status dade_load(dade_index* x, const char* path) {
   API_BEGIN
   need(x, "index"); need(path, "path");
@@ -1496,6 +1543,11 @@ extern "C" dade_status dade_load(dade_index* x, const char* path) {
   DADE_REQUIRE(hdr[0] == (int64_t)kMagic, DADE_ERR_ARG, "not a DADE index file");
   DADE_REQUIRE(hdr[1] == x->D, DADE_ERR_SHAPE, "file D differs from the index D");
   const int D = x->D;
+  // header ranges before any allocation sized by them
+  DADE_REQUIRE(hdr[3] >= 1 && hdr[3] < ((int64_t)1 << 31), DADE_ERR_ARG, "file: n out of range");
+  DADE_REQUIRE(hdr[2] >= 1 && hdr[2] <= hdr[3], DADE_ERR_ARG, "file: nlist out of range");
+  DADE_REQUIRE(hdr[4] >= 0 && hdr[4] + hdr[3] < ((int64_t)1 << 31), DADE_ERR_ARG, "file: id_base out of range");
+  DADE_REQUIRE(hdr[5] == 0 || hdr[5] == 1, DADE_ERR_ARG, "file: bad calibration flag");
   const int nlist = (int)hdr[2];
   const int64_t n = hdr[3];
   std::vector<double> mean(D), R((size_t)D * D), lam(D);
@@ -1510,24 +1562,117 @@ extern "C" dade_status dade_load(dade_index* x, const char* path) {
   int64_t c[3] = {0, 0, 0};
   if (hdr[5]) {
     rd(f, c, sizeof(c));
+    DADE_REQUIRE(c[0] >= 1 && c[0] <= DADE_MAX_K && c[1] >= 1 && c[1] <= ((int64_t)1 << 31) && c[2] == D / 16 - 1,
+                 DADE_ERR_ARG, "file: bad calibration header");
     m1.resize(c[2]); v.resize((size_t)c[2] * c[1]);
     rd(f, m1.data(), 8 * m1.size()); rd(f, v.data(), 8 * v.size());
   }
-  x->mean = mean; x->R = R; x->lam = lam;
-  upload_rotation(x);
-  x->cent.reserve(cent.size()); x->layout.reserve(lay.size());
-  x->off_d.reserve(nlist + 1); x->row_id_d.reserve(n);
+  // contents: the same checks as a build, before any state changes
+  std::vector<int32_t> asg_chk, pos_of;
+  check_ivf(n, hdr[4], nlist, off, rid, asg_chk, pos_of);
+  DADE_REQUIRE(asg_chk == asg, DADE_ERR_ARG, "file: assign does not match the lists");
+  for (double t : mean) DADE_REQUIRE(std::isfinite(t), DADE_ERR_NONFINITE, "file: non-finite mean");
+  for (double t : R) DADE_REQUIRE(std::isfinite(t), DADE_ERR_NONFINITE, "file: non-finite R");
+  for (float t : cent) DADE_REQUIRE(std::isfinite(t), DADE_ERR_NONFINITE, "file: non-finite centroids");
+  for (float t : lay) DADE_REQUIRE(std::isfinite(t), DADE_ERR_NONFINITE, "file: non-finite layout");
+  DBuf<float> cent_d, lay_d;
+  DBuf<int32_t> off_d, rid_d;
+  cent_d.reserve(cent.size()); lay_d.reserve(lay.size()); off_d.reserve(nlist + 1); rid_d.reserve(n);
   std::vector<int32_t> off32(off.begin(), off.end()), rid32(rid.begin(), rid.end());
-  DADE_CK(cudaMemcpy(x->cent.p, cent.data(), 4 * cent.size(), cudaMemcpyHostToDevice));
-  DADE_CK(cudaMemcpy(x->layout.p, lay.data(), 4 * lay.size(), cudaMemcpyHostToDevice));
-  DADE_CK(cudaMemcpy(x->off_d.p, off32.data(), 4 * off32.size(), cudaMemcpyHostToDevice));
-  DADE_CK(cudaMemcpy(x->row_id_d.p, rid32.data(), 4 * rid32.size(), cudaMemcpyHostToDevice));
-  x->off_h = off; x->row_id_h = rid; x->assign_h = asg;
-  x->pos_of_h.assign(n, 0);
-  for (int64_t p = 0; p < n; ++p) x->pos_of_h[rid[p] - hdr[4]] = (int32_t)p;
+  DADE_CK(cudaMemcpy(cent_d.p, cent.data(), 4 * cent.size(), cudaMemcpyHostToDevice));
+  DADE_CK(cudaMemcpy(lay_d.p, lay.data(), 4 * lay.size(), cudaMemcpyHostToDevice));
+  DADE_CK(cudaMemcpy(off_d.p, off32.data(), 4 * off32.size(), cudaMemcpyHostToDevice));
+  DADE_CK(cudaMemcpy(rid_d.p, rid32.data(), 4 * rid32.size(), cudaMemcpyHostToDevice));
+  // commit
+  x->mean = mean; x->R = R; x->lam = lam; x->has_lam = true;
+  upload_rotation(x);
+  std::swap(x->cent, cent_d); std::swap(x->layout, lay_d); std::swap(x->off_d, off_d); std::swap(x->row_id_d, rid_d);
+  cent_d.release(); lay_d.release(); off_d.release(); rid_d.release();
+  x->off_h = off; x->row_id_h = rid; x->assign_h = asg; x->pos_of_h = std::move(pos_of);
   x->nlist = nlist; x->n = n; x->id_base = hdr[4]; x->has_ivf = true; x->xnorm_ok = false;
   tc_prepare(x, x->cent.p, nlist, x->cent_tc, true);
   x->has_cal = hdr[5] != 0;
   if (x->has_cal) { x->calK = (int)c[0]; x->n0 = (int)c[1]; x->ncls = (int)c[2]; x->m1 = m1; x->v = v; }
+  API_END
+}
+
+// ================================================================== injection of a ready layout
+extern "C" dade_status dade_set_ivf(dade_index* x, const float* Xrot, int64_t n, int64_t id_base,
+                                    const int64_t* row_id, const int64_t* off, int nlist,
+                                    const float* centroids) {
+  API_BEGIN
+  need(x, "index"); need(Xrot, "Xrot"); need(row_id, "row_id"); need(off, "off"); need(centroids, "centroids");
+  DADE_REQUIRE(x->has_rot, DADE_ERR_STATE, "set_ivf needs the rotation the layout was made with");
+  DADE_REQUIRE(n >= 1 && n < ((int64_t)1 << 31), DADE_ERR_ARG, "n out of range");
+  DADE_REQUIRE(nlist >= 1 && nlist <= n, DADE_ERR_ARG, "nlist not in [1, n]");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  std::vector<int64_t> offv(off, off + nlist + 1), rid(row_id, row_id + n);
+  std::vector<int32_t> asg, pos_of;
+  check_ivf(n, id_base, nlist, offv, rid, asg, pos_of);
+  check_finite(x, Xrot, n * D, "Xrot");
+  check_finite(x, centroids, (int64_t)nlist * D, "centroids");
+  DBuf<float> cent, lay;
+  DBuf<int32_t> off_d, rid_d;
+  cent.reserve((size_t)nlist * D); lay.reserve((size_t)n * D); off_d.reserve(nlist + 1); rid_d.reserve(n);
+  std::vector<int32_t> off32(offv.begin(), offv.end()), rid32(rid.begin(), rid.end());
+  DADE_CK(cudaMemcpyAsync(cent.p, centroids, sizeof(float) * nlist * D, cudaMemcpyDeviceToDevice, st));
+  DADE_CK(cudaMemcpyAsync(off_d.p, off32.data(), 4 * off32.size(), cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(rid_d.p, rid32.data(), 4 * rid32.size(), cudaMemcpyHostToDevice, st));
+  launch_to_blocked(Xrot, n, D, lay.p, st);
+  DADE_CK(cudaStreamSynchronize(st));
+  std::swap(x->cent, cent); std::swap(x->layout, lay); std::swap(x->off_d, off_d); std::swap(x->row_id_d, rid_d);
+  cent.release(); lay.release(); off_d.release(); rid_d.release();
+  x->off_h = std::move(offv); x->row_id_h = std::move(rid); x->assign_h = std::move(asg); x->pos_of_h = std::move(pos_of);
+  x->nlist = nlist; x->n = n; x->id_base = id_base;
+  tc_prepare(x, x->cent.p, nlist, x->cent_tc, true);
+  x->has_ivf = true; x->has_cal = false; x->xnorm_ok = false;
+  API_END
+}
+
+// ================================================================== options
+extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value) {
+  API_BEGIN
+  need(x, "index");
+  Options& o = x->opt;
+  auto in = [&](std::initializer_list<int64_t> ok) {
+    for (int64_t v : ok) if (v == value) return;
+    throw Error(DADE_ERR_ARG, "option value not allowed");
+  };
+  switch (option) {
+    case DADE_OPT_KNN_PATH: in({0, 1, 2, 3}); o.knn_path = (int)value; break;
+    case DADE_OPT_PROBE_PASSES: in({0, 1, 3}); o.probe_passes = (int)value; break;
+    case DADE_OPT_SCAN_WARPS: in({0, 1, 2, 4, 8}); o.scan_warps = (int)value; break;
+    case DADE_OPT_SCAN_ORDER: in({0, 1}); o.scan_order = (int)value; break;
+    case DADE_OPT_SCAN_TAIL:
+      DADE_REQUIRE(value >= 0 && value < ((int64_t)1 << 31), DADE_ERR_ARG, "scan tail out of range");
+      o.scan_tail = (int)value; break;
+    case DADE_OPT_HOST_CHUNKS:
+      DADE_REQUIRE(value >= 1 && value <= 1024, DADE_ERR_ARG, "host chunks not in [1, 1024]");
+      o.host_chunks = (int)value; break;
+    case DADE_OPT_HOST_PREP_CHUNKS:
+      DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "prep chunks not in [0, 64]");
+      o.host_prep_chunks = (int)value; break;
+    case DADE_OPT_DHAT_ARES: in({0, 1}); o.dhat_ares = (int)value; break;
+    default: throw Error(DADE_ERR_ARG, "unknown option");
+  }
+  API_END
+}
+
+// ================================================================== decision log (parity)
+extern "C" dade_status dade_search_log(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d,
+                                       int method, double param, int64_t* ids, float* dists, int32_t* log,
+                                       int64_t log_cap, int64_t* log_count) {
+  API_BEGIN
+  need(x, "index"); need(log_count, "log_count");
+  DADE_REQUIRE(log_cap >= 0, DADE_ERR_ARG, "log_cap < 0");
+  if (log_cap > 0) need(log, "log");
+  DADE_REQUIRE(method != DADE_METHOD_BSA_RES, DADE_ERR_UNSUPPORTED, "decision log: BSA-p and ADSampling only");
+  DeviceGuard g(x->device);
+  DecisionLog dl;
+  dl.buf = log; dl.cap = log_cap; dl.count = log_count;
+  *log_count = 0;
+  do_search(x, Q, nq, K, nprobe, delta_d, param, ids, dists, nullptr, method, nullptr, nullptr, &dl);
   API_END
 }

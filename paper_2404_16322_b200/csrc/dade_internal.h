@@ -136,7 +136,7 @@ struct ScanParams {
   const int32_t* row_id;  // n global ids (list-major)
   const float* layout;    // D/16 blocks of n x 16
   int64_t n;
-  int D, nq, nprobe, K, dd, nsteps, c0;
+  int D, nq, nprobe, K, dd, nsteps, c0;  // dd = classifier spacing in 16-dim blocks (delta_d / 16)
   int prune;              // 0: no classifier can prune (alpha = 0 or one step)
   float m1[DADE_MAX_STEPS];
   float beta[DADE_MAX_STEPS];
@@ -151,6 +151,11 @@ struct ScanParams {
   int64_t avg_stream;   // expected candidates per query (nprobe * n / nlist): picks warps per query
   const int32_t* order; // nq: processing order of the queries (null = 0..nq-1); results stay at q
   int g_force;          // warps per query (0 = the scan_group heuristic)
+  unsigned dd_magic;    // ceil(2^32 / dd), set by launch_scan
+  // decision log (parity runs; null = off): per tested candidate (query, global id, dims read)
+  int32_t* dlog;
+  int64_t dlog_cap;              // records
+  unsigned long long* dlog_n;    // records written (may exceed dlog_cap: the caller sees the overflow)
 };
 void launch_scan(const ScanParams& p, cudaStream_t st);
 // misc.cu: the scan's query order — a counting sort of the queries by their nearest probed list
@@ -172,6 +177,8 @@ void launch_res_consts(const float* qrot, int nq, int D, int delta_d, const doub
 void launch_merge_topk(const int64_t* ids_in, const float* d_in, int S, int nq, int K,
                        int64_t* ids_out, float* d_out, cudaStream_t st);
 void launch_check_finite(const float* X, int64_t n, int* flag, cudaStream_t st, int code = 1);
+// row-major n x D -> dimension-blocked layout (block b = n x 16, rows in the same order)
+void launch_to_blocked(const float* X, int64_t n, int D, float* out, cudaStream_t st);
 void launch_gather_rows(const float* X, const int32_t* rows, int64_t m, int D, float* out,
                         cudaStream_t st);
 

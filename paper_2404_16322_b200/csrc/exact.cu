@@ -738,11 +738,7 @@ void launch_select_groups(const float* gmin, int64_t m, int64_t n, int k, const 
   if (m <= 0) return;
   DADE_REQUIRE(k >= 1 && k <= 512, DADE_ERR_UNSUPPORTED, "group select: k > 512");
   const size_t smem = (size_t)kGsWarps * kGsCap * 12 + (size_t)kGsWarps * 256 * 4;
-  static bool attr = false;
-  if (!attr) {
-    DADE_CK(cudaFuncSetAttribute(k_select_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  DADE_CK(cudaFuncSetAttribute(k_select_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  // per launch: per device
   k_select_groups<<<(unsigned)((m + kGsWarps - 1) / kGsWarps), kGsWarps * 32, smem, st>>>(
       gmin, m, n, k, A, B, D, out_idx, out_d64, slack);
   DADE_CK(cudaGetLastError());
@@ -797,13 +793,9 @@ void launch_select_exact(const float* d_hat, int64_t m, int64_t n, int k, const 
     DADE_CK(cudaGetLastError());
     return;
   }
-  static bool attr = false;
   const size_t smem = kSortCap * sizeof(Cand);
-  if (!attr) {
-    DADE_CK(cudaFuncSetAttribute(k_select_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = true;
-  }
+  DADE_CK(cudaFuncSetAttribute(k_select_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));  // per launch: per device
   k_select_exact<<<(unsigned)m, kSelThreads, smem, st>>>(d_hat, n, k, A, B, D, out_idx, out_d64,
                                                          cand_buf, cand_cap, d_flag, slack);
   DADE_CK(cudaGetLastError());

@@ -333,17 +333,13 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
                   cudaStream_t st, float* gmin, int passes, int gshift) {
   if (m <= 0 || n <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStageBytes + 128));
-    attr = true;
-  }
+  // set on every launch: the attribute is per device
+  DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStageBytes + 128));
   // 1-pass stages (16 KB each): three — 48 KB lets four CTAs share an SM (with four stages the
   // 64 KB allowed three), hiding more of each CTA's wait for its accumulator (C2 search 0.721 ->
-  // 0.712-0.718 ms). DADE_L2TC_S1 in {2, 3, 4} overrides; the epilogue's transposition buffers
+  // 0.712-0.718 ms; 2 and 4 measured no better); the epilogue's transposition buffers
   // (4 x 32 x 33 floats) reuse the stage region, so >= 2 stages
-  int s1 = 3;
-  if (const char* e = getenv("DADE_L2TC_S1")) s1 = std::max(2, std::min(4, atoi(e)));
+  const int s1 = 3;
   const size_t smem = (passes == 1 ? (size_t)s1 * (kStageBytes / 2) : 2 * (size_t)kStageBytes) + 128;
   dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
   k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), out, m, n, ldo, gmin,

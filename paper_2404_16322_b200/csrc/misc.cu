@@ -90,6 +90,24 @@ void launch_query_order(const int32_t* probes, int nq, int nprobe, int nlist, in
   DADE_CK(cudaGetLastError());
 }
 
+// row-major n x D (list-major rows) -> the dimension-blocked layout: block b is an n x 16 matrix
+__global__ void k_to_blocked(const float* __restrict__ X, int64_t n, int D, float* __restrict__ out) {
+  const int nb = D / 16;
+  const int64_t tot = n * nb * 4;  // 16-B chunks
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / (nb * 4);
+    const int r = (int)(i - p * nb * 4), b = r >> 2, c = r & 3;
+    const float4 v = reinterpret_cast<const float4*>(X + p * D + b * 16)[c];
+    reinterpret_cast<float4*>(out + ((int64_t)b * n + p) * 16)[c] = v;
+  }
+}
+
+void launch_to_blocked(const float* X, int64_t n, int D, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_to_blocked<<<1184, 256, 0, st>>>(X, n, D, out);
+  DADE_CK(cudaGetLastError());
+}
+
 void launch_merge_topk(const int64_t* ids_in, const float* d_in, int S, int nq, int K,
                        int64_t* ids_out, float* d_out, cudaStream_t st) {
   if (nq <= 0) return;

@@ -837,18 +837,11 @@ void launch_dhat_tc(const float* Ahi, const float* Alo, const float* an, int64_t
                     const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo, float* gmin,
                     int gshift, int passes, cudaStream_t st) {
   if (m <= 0 || n <= 0) return;
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    DADE_CK(cudaGetDevice(&dev));
-    DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int dev = 0, sms = 0;  // per call: the index may live on any device
+  DADE_CK(cudaGetDevice(&dev));
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const size_t smem = kStages * kStageBytes + 128 + 4 * 32 * 33 * 4;
-  static bool attr = false;
-  if (!attr) {
-    DADE_CK(cudaFuncSetAttribute(k_dhat_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  DADE_CK(cudaFuncSetAttribute(k_dhat_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  // per launch: per device
   const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM;
   int64_t nsplit = 1;
   while (mt * nsplit < 2 * sms && nsplit * 4 <= ntiles) nsplit *= 2;  // >= 4 tiles per CTA
@@ -860,32 +853,21 @@ void launch_dhat_tc(const float* Ahi, const float* Alo, const float* an, int64_t
 }
 
 // the A-resident writer applies to the 1-pass filter with nkc * 8 KB of A <= 168 KB (D <= 336).
-// Off by default (DADE_DHAT_ARES=1 enables it): measured on the C5 shard it is SLOWER (search
-// 3.03 -> 3.76 ms) — the writer is bound by its epilogue, not by operand traffic, and one CTA per
-// SM halves the epilogue warps.
+// Off by default (DADE_OPT_DHAT_ARES = 1 enables it): measured on the C5 shard it is SLOWER
+// (search 3.03 -> 3.76 ms) — the writer is bound by its epilogue, not by operand traffic, and one
+// CTA per SM halves the epilogue warps.
 static size_t dhat_ares_smem(int nkc) { return (size_t)nkc * kSub * 4 + 4 * kSub * 4 + 128 + 4 * 32 * 33 * 4; }
-bool dhat_ares_ok(int D, int passes) {
-  const char* e = getenv("DADE_DHAT_ARES");
-  if (!e || atoi(e) == 0) return false;
-  return passes == 1 && dhat_ares_smem(tc_nkc(D)) <= 220 * 1024;
-}
+bool dhat_ares_ok(int D, int passes) { return passes == 1 && dhat_ares_smem(tc_nkc(D)) <= 220 * 1024; }
 
 void launch_dhat_ares(const float* Ahi, const float* an, int64_t m, const float* Bhi, const float* bn, int64_t n,
                       int D, float* out, int64_t ldo, float* gmin, int gshift, cudaStream_t st) {
   if (m <= 0 || n <= 0) return;
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    DADE_CK(cudaGetDevice(&dev));
-    DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int dev = 0, sms = 0;  // per call: the index may live on any device
+  DADE_CK(cudaGetDevice(&dev));
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int nkc = tc_nkc(D);
   const size_t smem = dhat_ares_smem(nkc);
-  static size_t attr = 0;
-  if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_dhat_ares, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  DADE_CK(cudaFuncSetAttribute(k_dhat_ares, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  // per launch: per device
   const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM;
   // one CTA per SM: about three waves of (row tile, column range) CTAs, >= 4 column tiles each
   int64_t nsplit = std::max<int64_t>(1, (3 * (int64_t)sms + mt - 1) / mt);
@@ -912,11 +894,7 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
   const int C = probe_tc_cap(k);
   const size_t smem = kStages * kStageBytes + 128 + (size_t)kTM * (k * 4 + C * 8);
   DADE_REQUIRE(smem <= 227 * 1024, DADE_ERR_UNSUPPORTED, "probe: k too large for the fused filter");
-  static size_t attr = 0;
-  if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_probe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  DADE_CK(cudaFuncSetAttribute(k_probe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  // per launch: per device
   const int64_t ntiles = (n + kTM - 1) / kTM;
   const int tps = (int)((ntiles + nsplit - 1) / nsplit);
   dim3 grid((unsigned)((m + kTM - 1) / kTM), (unsigned)nsplit);
@@ -924,11 +902,7 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
                                           ccount, passes);
   DADE_CK(cudaGetLastError());
   const size_t fsm = (size_t)kFinWarps * kFinWarpBytes;
-  static bool fattr = false;
-  if (!fattr) {
-    DADE_CK(cudaFuncSetAttribute(k_probe_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-    fattr = true;
-  }
+  DADE_CK(cudaFuncSetAttribute(k_probe_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));  // per launch: per device
   k_probe_finish<<<(unsigned)((m + kFinWarps - 1) / kFinWarps), kFinWarps * 32, fsm, st>>>(
       cand, ccount, nsplit, C, m, n, k, A, B, D, slack, out_idx, out_d64);
   DADE_CK(cudaGetLastError());

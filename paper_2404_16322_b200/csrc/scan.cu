@@ -26,7 +26,11 @@
 //    the distance is the fp32 sum of per-block sums, added in block order (R21) — identical
 //    whichever round a block is processed in, so results never depend on the schedule;
 //  * the top-K is REGISTER-RESIDENT: KPL sorted keys (dist_bits << 32 | id) per lane, position
-//    lane*KPL + i; an accepted key is inserted by a warp-wide shift (no shared memory).
+//    lane*KPL + i; an accepted key is inserted by a warp-wide shift (no shared memory);
+//  * Delta_d is any multiple of 16 dividing D: the template DD (1, 2 or 4 blocks) is the unit the
+//    TMA tiles and gather rounds move, the runtime p.dd (a multiple of DD) the classifier spacing;
+//  * LOG instantiations (parity only) append every tested candidate's decision (query, id, dims
+//    read) to a device log — the per-candidate comparison with the oracle.
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
@@ -251,13 +255,13 @@ __device__ unsigned long long g_scan_prof[16];
   } while (0)
 #endif
 
-// Per-warp shared-memory slice: tiles | mbar | meta | ring | (ASY) staging.
-// Ring capacity: synchronous rounds start at 32 queued and stage 1 runs below 32, so at most 63
-// entries are queued; with an async round in flight stage 1 may run up to 64 queued (+32 + 32).
-template <int DD, bool ASY>
+// Per-warp shared-memory slice: tiles | mbar | meta | ring.
+// Ring capacity: rounds start at 32 queued and stage 1 runs below 32, so at most 63 entries are
+// queued.
+template <int DD>
 struct Slice {
 #ifdef DADE_SCAN_STAGES  // experiment builds (tools/build_variant.py)
-  static constexpr int kStages = ASY ? 2 : DADE_SCAN_STAGES;
+  static constexpr int kStages = DADE_SCAN_STAGES;
 #else
   // two tiles in flight: measured on C2 scan 0.553 -> 0.531 ms against three (C4 equal, C3 and the
   // C5 shard already used two) — fewer TMA bytes in flight leave the latency-critical survivor
@@ -265,11 +269,27 @@ struct Slice {
   static constexpr int kStages = 2;
 #endif
   static constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
-  static constexpr int QCAP = ASY ? 128 : 64;
-  static constexpr size_t stage_bytes = ASY ? 2 * (32 * 64 + 32 * 4) : 0;  // 2 async rounds: rows + ids
-  static constexpr size_t bytes = (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + QCAP * sizeof(QEntry) +
-                                  stage_bytes;
+  static constexpr int QCAP = 64;
+  static constexpr size_t bytes = (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + QCAP * sizeof(QEntry);
 };
+
+// decision log (LOG builds): (query, global id, dims read) of one tested candidate
+__device__ __forceinline__ void log_decision(const ScanParams& p, int64_t q, int32_t id, int dims) {
+  const unsigned long long slot = atomicAdd(p.dlog_n, 1ull);
+  if ((int64_t)slot < p.dlog_cap) {
+    int32_t* r = p.dlog + 3 * slot;
+    r[0] = (int32_t)q;
+    r[1] = id;
+    r[2] = dims;
+  }
+}
+
+// classifier step index of block count blk: ns = blk / dd if blk is a multiple of dd, else 0
+// (dd = p.dd, magic = ceil(2^32 / dd): exact for blk, dd <= 256)
+__device__ __forceinline__ int step_of(int blk, int dd, unsigned magic) {
+  const int ns = (int)__umulhi((unsigned)blk, magic);
+  return ns * dd == blk ? ns : 0;
+}
 
 // CTA = G warps (blockDim.x = 32 G), one query at a time. G = 1: the warp owns the query and its
 // register top-K is the query's top-K. G > 1: the query's candidate tiles are dealt round-robin
@@ -277,10 +297,10 @@ struct Slice {
 // frozen tau (R13), so the split cannot change a decision; at each epoch end the warps' local
 // top-K lists are merged exactly (rank by binary search, smem) into the query's top-K.
 // CTA shared memory: G slices | pruned[64] | lists[nprobe] | qs[D] | qi | (G > 1) W[G][K] + Gk[2][K].
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY, bool RES>
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG>
 __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  using SL = Slice<DD, ASY>;
+  using SL = Slice<DD>;
   constexpr int kQCap = SL::QCAP;
   constexpr int kStages = SL::kStages;
   constexpr int TB = SL::TB;
@@ -292,7 +312,6 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
   TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + 4);
   QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
-  unsigned char* stg = reinterpret_cast<unsigned char*>(ring + kQCap);  // async rounds: 2 x (32 x 64 B rows, ids)
   unsigned* pruned = reinterpret_cast<unsigned*>(smem + G * SL::bytes);
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
@@ -318,6 +337,9 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
 
   const int nsteps = p.nsteps;
   const int nblk = D >> 4;
+  const int sdd = p.dd;                 // classifier spacing in blocks (a multiple of DD)
+  const unsigned smagic = p.dd_magic;
+  const bool test1 = sdd == DD && nsteps > 1;  // stage 1 ends on a classifier step
   const float* lay = p.layout;
   const int64_t n = p.n;
   unsigned long long c_tested = 0, c_surv = 0;  // warp-uniform
@@ -443,12 +465,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
           phi += b;
           if (RES) res -= nq;
           ++blk;
-          if (blk % DD == 0 && blk < nblk) {
-            const int ns = blk / DD;
+          const int ns = blk < nblk ? step_of(blk, sdd, smagic) : 0;
+          if (ns) {
             const bool pr = RES ? phi + res + qcs[ns - 1] > tau : fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau;
             if (pr) {
               alive = false;
               if (stats && sub == 0) atomicAdd(&pruned[ns], 1u);
+              if (LOG && sub == 0) log_decision(p, q, __ldg(p.row_id + e.row), blk * 16);
             }
           }
         }
@@ -464,6 +487,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
                  RES ? __shfl_sync(0xffffffffu, bq[s], (ei << lg) + j) : 0.f);
       }
       const bool fin = alive && blk == nblk && sub == 0;  // d = D: exact distance (no test, R10)
+      if (LOG && fin) log_decision(p, q, (int32_t)gid, D);
       push(alive && blk < nblk && sub == 0, QEntry{e.row, phi, blk, res});
       if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
       const unsigned long long key = fin ? make_key(phi, gid) : kKeyInf;
@@ -509,93 +533,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       tk.init(K);
     };
 
-    // ASY: full rounds (32 queued survivors, one block each) are issued as cp.async copies into
-    // one of two staging buffers and completed later (oldest first), so up to two gather round
-    // trips are in flight per warp while stage 1 works on the tiles the TMA ring already holds
-    QEntry pe0{0, 0.f, nblk, 0.f}, pe1{0, 0.f, nblk, 0.f};
-    int npend = 0, pfirst = 0, since = 0;
-    auto issue_round = [&]() {
-      const int slot = (pfirst + npend) & 1;
-      const QEntry e = ring[(head + lane) & (kQCap - 1)];
-      if (slot) pe1 = e; else pe0 = e;
-      head += 32;
-      unsigned char* sb = stg + slot * (32 * 64 + 32 * 4);
-      const float* src = lay + (((int64_t)e.blk * n + e.row) << 4);
-      const uint32_t dst = smem_u32(sb + lane * 64);
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(src + c * 4) : "memory");
-      if (e.blk + 1 == nblk)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sb + 32 * 64 + lane * 4)),
-                     "l"(p.row_id + e.row)
-                     : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (npend == 0) since = 0;
-      ++npend;
-    };
-    auto complete_round = [&]() {  // the oldest pending round
-      if (npend == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
-      else asm volatile("cp.async.wait_group 0;" ::: "memory");
-      const int slot = pfirst;
-      const QEntry pe = slot ? pe1 : pe0;
-      const unsigned char* sb = stg + slot * (32 * 64 + 32 * 4);
-      const ulonglong2* sr = reinterpret_cast<const ulonglong2*>(sb + lane * 64);
-      unsigned long long x[8];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const ulonglong2 v = sr[c];
-        x[2 * c] = v.x;
-        x[2 * c + 1] = v.y;
-      }
-      const float phi = pe.phi + block_sum(x, qs + pe.blk * 16);
-      const float res = RES ? pe.res - block_sq(x) : 0.f;
-      const int blk = pe.blk + 1;
-      bool alive = true;
-      if (blk % DD == 0 && blk < nblk) {
-        const int ns = blk / DD;
-        if (RES ? phi + res + qcs[ns - 1] > tau : fmaf(p.m1[ns - 1], phi, p.beta[ns - 1]) > tau) {
-          alive = false;
-          if (stats) atomicAdd(&pruned[ns], 1u);
-        }
-      }
-      const bool fin = alive && blk == nblk;
-      push(alive && !fin, QEntry{pe.row, phi, blk, res});
-      if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, fin));
-      const unsigned long long key = fin ? make_key(phi, reinterpret_cast<const uint32_t*>(sb + 32 * 64)[lane]) : kKeyInf;
-      __syncwarp();
-      tk.offer(!MULTI || key < cap ? key : kKeyInf, lane);
-      pfirst ^= 1;
-      --npend;
-      since = 0;
-    };
-
     // ---------------------------------------------------- consumer (one call site per action)
     bool ready = false;  // the tile in `slot` has landed and its meta is read
     TileMeta tm{0, 0, 0, 0};
     for (;;) {
       const int qlen = tail - head;
-      if (ASY) {
-        if (npend < 2 && qlen >= 32) {
-          issue_round();
-          continue;
-        }
-        if (npend > 0) {
-          if (!ready && consumed < issued) {
-            const int slot = consumed % kStages;
-            mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
-            phase_bits ^= 1u << slot;
-            tm = meta[slot];
-            ready = true;
-          }
-          // room: this tile's survivors (32) and every pending round's results (32 each)
-          if (!(ready && tm.ep == cur_ep && since < 4 && qlen + 32 * (npend + 1) <= kQCap)) {
-            complete_round();
-            continue;
-          }
-        }
-      }
-      bool round = !ASY && qlen >= 32, drain = false, ep_end = false;
-      if (!round && !(ASY && npend > 0)) {
+      bool round = qlen >= 32, drain = false, ep_end = false;
+      if (!round) {
         if (!ready && consumed < issued) {
           const int slot = consumed % kStages;
           mbar_wait(&mbar[slot], (phase_bits >> slot) & 1u);
@@ -648,14 +592,14 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       }
       __syncwarp();  // every lane is done reading this slot
       ++consumed;
-      ++since;
       ready = false;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(slot);
       if (stats) c_tested += tm.nr;
       const float res = xn - sq;
-      const bool prune = val && nsteps > 1 &&
+      const bool prune = val && test1 &&
                          (RES ? s + res + qcs[0] > tau : fmaf(p.m1[0], s, p.beta[0]) > tau);
+      if (LOG && prune) log_decision(p, q, __ldg(p.row_id + tm.row0 + lane), DD * 16);
       push(val && !prune, QEntry{tm.row0 + lane, s, DD, res});
       if (stats) {
         const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
@@ -703,9 +647,9 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   }
 }
 
-template <int DD, bool ASY, bool RES>
+template <int DD, bool RES>
 static size_t scan_smem(int D, int K, int nprobe, int G) {
-  return (size_t)G * Slice<DD, ASY>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
+  return (size_t)G * Slice<DD>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
          (size_t)((D + 3) & ~3) * 4 + (RES ? DADE_MAX_STEPS * 4 : 0) + (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
 
@@ -714,80 +658,56 @@ static size_t scan_smem(int D, int K, int nprobe, int G) {
 // C4 (10k queries, ~4,900 candidates each) G = 2 1.19 ms vs 1 1.26; C2 (~2,000) G = 1 0.57 vs
 // 2 0.67; C5 shard (~1,500) G = 1 1.66 vs 2 1.90 — larger groups pay epoch barriers
 static int scan_group(int nq, int sms, int64_t avg_stream) {
-  const char* e = getenv("DADE_SCAN_G");
-  if (e) return atoi(e);
   int G = avg_stream >= 4000 ? 2 : 1;
   while (G < 8 && (int64_t)nq * G < (int64_t)sms * 16) G *= 2;
   return G;
 }
 
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool ASY, bool RES>
+// The attribute and the SM count are set / read on every launch (cheap host calls): they apply
+// per device, and an index may live on any device of the process.
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG>
 static void launch_g(const ScanParams& p, cudaStream_t st, int G, int sms) {
-  const size_t smem = scan_smem<DD, ASY, RES>(p.D, p.K, p.nprobe, G);
+  auto kern = k_scan<DD, KPL, LA, MAXREG, MULTI, RES, LOG>;
+  const size_t smem = scan_smem<DD, RES>(p.D, p.K, p.nprobe, G);
   DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
-  static size_t attr = 0;
-  if (smem > attr) {
-    DADE_CK(cudaFuncSetAttribute(k_scan<DD, KPL, LA, MAXREG, MULTI, ASY, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  DADE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<DD, KPL, LA, MAXREG, MULTI, ASY, RES>, 32 * G, smem));
+  DADE_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * G, smem));
   const int max_blocks = (occ > 0 ? occ : 1) * sms;
-  k_scan<DD, KPL, LA, MAXREG, MULTI, ASY, RES><<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
+  kern<<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
 }
 
-template <int DD, int KPL, int LA, int MAXREG, bool ASY = false, bool RES = false>
+template <int DD, int KPL, int LA, int MAXREG, bool RES = false>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    DADE_CK(cudaGetDevice(&dev));
-    DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int dev = 0, sms = 0;
+  DADE_CK(cudaGetDevice(&dev));
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (p.dlog) {  // decision log (parity runs): one warp per query; decisions do not depend on G
+    if constexpr (!RES) launch_g<DD, KPL, LA, MAXREG, false, false, true>(p, st, 1, sms);
+    return;
   }
   const int G = p.g_force > 0 ? p.g_force : scan_group(p.nq, sms, p.avg_stream);
   DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
-  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, ASY, RES>(p, st, 1, sms);
-  else launch_g<DD, KPL, LA, MAXREG, true, ASY, RES>(p, st, G, sms);
-}
-
-// tuning variants (DADE_SCAN_VARIANT, read per launch) for the Delta_d = 16, K <= 32 kernel
-static int scan_variant() {
-  const char* e = getenv("DADE_SCAN_VARIANT");
-  return e ? atoi(e) : 0;
+  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, RES, false>(p, st, 1, sms);
+  else launch_g<DD, KPL, LA, MAXREG, true, RES, false>(p, st, G, sms);
 }
 
 template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
-  constexpr int kReg = (KPL >= 4 || DD >= 4) ? 96 : 80;
   if (p.residual) {  // BSA-res (NEXT-1): residual-norm test
-    launch_v<DD, KPL, 1, 96, false, true>(p, st);
+    DADE_REQUIRE(!p.dlog, DADE_ERR_UNSUPPORTED, "scan: decision log is for BSA-p / ADSampling only");
+    launch_v<DD, KPL, 1, 96, true>(p, st);
     return;
   }
-  if constexpr (DD == 1 && KPL == 1) {
-    switch (scan_variant()) {
-      case 1: launch_v<DD, KPL, 1, 80, true>(p, st); return;
-      case 2: launch_v<DD, KPL, 1, 72, true>(p, st); return;
-      case 3: launch_v<DD, KPL, 1, 72>(p, st); return;
-      case 4: launch_v<DD, KPL, 1, 64>(p, st); return;
-      case 5: launch_v<DD, KPL, 1, 96>(p, st); return;
-      case 6: launch_v<DD, KPL, 1, 88>(p, st); return;
-      case 10: launch_v<DD, KPL, 2, 80>(p, st); return;   // 2 blocks per lane in draining rounds
-      case 11: launch_v<DD, KPL, 2, 88>(p, st); return;
-      case 12: launch_v<DD, KPL, 2, 96>(p, st); return;
-      default: break;
-    }
+  if constexpr (DD >= 2) {
+    // a step spans DD blocks: gather a whole step per round trip; register cap 128 (16 warps/SM,
+    // no spills): measured C5 shard 1.99 -> 1.66 ms, C3 1.50 -> 1.40 against 96
+    launch_v<DD, KPL, 2, 128>(p, st);
+  } else {
+    // 80 registers (24 one-warp CTAs per SM) measured best on C2 and C4 against 64, 72 and 96
+    // (C4 scan 1.200 ms vs 1.454 / 1.264 / 1.284, profiles/r02_scan_variants.jsonl)
+    launch_v<DD, KPL, 1, (KPL >= 4 ? 96 : 80)>(p, st);
   }
-  if constexpr (DD >= 2) {  // a step spans DD blocks: gather a whole step per round trip
-    // register cap 128 (16 warps/SM, no spills): measured C5 shard 1.99 -> 1.66 ms, C3 1.50 -> 1.40
-    const int v = scan_variant();
-    if (v == 8) { launch_v<DD, KPL, 2, 96>(p, st); return; }
-    if (v == 9) { launch_v<DD, KPL, 2, 112>(p, st); return; }
-    if (v != 7) {
-      launch_v<DD, KPL, 2, 128>(p, st);
-      return;
-    }
-  }
-  launch_v<DD, KPL, 1, kReg>(p, st);
 }
 
 template <int DD>
@@ -812,11 +732,14 @@ extern "C" int dade_scan_prof_read(unsigned long long* out16, int reset) {
 void launch_scan(const ScanParams& p, cudaStream_t st) {
   if (p.nq <= 0) return;
   DADE_REQUIRE(p.K <= 256, DADE_ERR_UNSUPPORTED, "scan: K > 256");
-  switch (p.dd) {
-    case 1: launch_dd<1>(p, st); break;
-    case 2: launch_dd<2>(p, st); break;
-    case 4: launch_dd<4>(p, st); break;
-    default: throw Error(DADE_ERR_UNSUPPORTED, "delta_d must be 16, 32 or 64");
+  DADE_REQUIRE(p.dd >= 1 && p.dd * 16 <= p.D && p.D % (p.dd * 16) == 0, DADE_ERR_ARG, "scan: bad delta_d");
+  ScanParams q = p;
+  q.dd_magic = (unsigned)((((uint64_t)1 << 32) + (uint64_t)p.dd - 1) / (uint64_t)p.dd);
+  // staging unit: the largest of 4, 2, 1 blocks dividing the classifier spacing
+  switch (p.dd % 4 == 0 ? 4 : p.dd % 2 == 0 ? 2 : 1) {
+    case 4: launch_dd<4>(q, st); break;
+    case 2: launch_dd<2>(q, st); break;
+    default: launch_dd<1>(q, st); break;
   }
   DADE_CK(cudaGetLastError());
 }

@@ -17,7 +17,10 @@ MAX_STEPS = 64
 MAX_K = 256
 
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_STATE", 4: "ERR_NONFINITE", 5: "ERR_OOM",
-          6: "ERR_CUDA", 8: "ERR_UNSUPPORTED"}
+          6: "ERR_CUDA", 7: "ERR_NCCL", 8: "ERR_UNSUPPORTED"}
+# dade_set_option (include/dade.h DADE_OPT_*)
+OPTIONS = {"knn_path": 1, "probe_passes": 2, "scan_warps": 3, "scan_order": 4, "scan_tail": 5,
+           "host_chunks": 6, "host_prep_chunks": 7, "dhat_ares": 8}
 
 
 class DadeError(RuntimeError):
@@ -74,6 +77,9 @@ _SIGS = {
     "dade_estimate_knn": [P, P, I32, I32, I32, I32, P, P],
     "dade_bruteforce_knn": [P, P, I64, I64, P, I32, I32, P, P],
     "dade_merge_topk": [P, P, P, I32, I32, I32, P, P],
+    "dade_set_ivf": [P, P, I64, I64, P, P, I32, P],
+    "dade_set_option": [P, I32, I64],
+    "dade_search_log": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P, I64, P],
     "dade_save": [P, C.c_char_p],
     "dade_load": [P, C.c_char_p],
 }
@@ -196,6 +202,21 @@ class Index:
         _ck(lib().dade_get_ivf(self.h, _ptr(off), _ptr(row_id), _ptr(assign), _ptr(cent)))
         return off, row_id, assign, cent
 
+    def set_ivf(self, Xrot, row_id, off, centroids, id_base: int = 0):
+        """Inject a ready layout in the current rotation's basis: Xrot CUDA [n, D] fp32 rotated
+        rows in list-major order, row_id / off host int64 (as get_ivf returns them), centroids
+        CUDA [nlist, D] fp32 raw-space."""
+        import torch
+        Xrot = _dev(Xrot, torch.float32); centroids = _dev(centroids, torch.float32)
+        rid = np.ascontiguousarray(row_id, np.int64); off = np.ascontiguousarray(off, np.int64)
+        _ck(lib().dade_set_ivf(self.h, _ptr(Xrot), Xrot.shape[0], id_base, _ptr(rid), _ptr(off),
+                               len(off) - 1, _ptr(centroids)))
+
+    def set_option(self, name: str, value: int):
+        """Tuning option of this index (dade_set_option): knn_path, probe_passes, scan_warps,
+        scan_order, scan_tail, host_chunks, host_prep_chunks, dhat_ares."""
+        _ck(lib().dade_set_option(self.h, OPTIONS[name], int(value)))
+
     def get_layout(self):
         n, _ = self.sizes()
         out = np.zeros((n, self.D), np.float32)
@@ -252,6 +273,25 @@ class Index:
         _ck(lib().dade_search_method(self.h, _ptr(Q), nq, K, nprobe, delta_d, self.METHODS[method], float(param),
                                      _ptr(ids), _ptr(dists), C.byref(st) if st is not None else None))
         return (ids, dists, st.as_dict()) if stats else (ids, dists)
+
+    def search_log(self, Q, K: int, nprobe: int, delta_d: int, param: float, method: str = "bsa_p",
+                   cap: int = 0):
+        """Parity run: the search plus its decision log — per tested candidate (query, global id,
+        dims read) as an int32 [count, 3] CUDA tensor (unordered). Returns (ids, dists, log)."""
+        import torch
+        Q = _dev(Q, torch.float32)
+        nq = Q.shape[0]
+        ids = torch.empty((nq, K), dtype=torch.int64, device=Q.device)
+        dists = torch.empty((nq, K), dtype=torch.float32, device=Q.device)
+        cap = cap or max(1, nq * 4096)
+        log = torch.empty((cap, 3), dtype=torch.int32, device=Q.device)
+        cnt = np.zeros(1, np.int64)
+        _ck(lib().dade_search_log(self.h, _ptr(Q), nq, K, nprobe, delta_d, self.METHODS[method], float(param),
+                                  _ptr(ids), _ptr(dists), _ptr(log), cap, _ptr(cnt)))
+        n = int(cnt[0])
+        if n > cap:
+            return self.search_log(Q, K, nprobe, delta_d, param, method, cap=n)
+        return ids, dists, log[:n]
 
     def kmeans_partial(self, X, id_base: int, n_total: int, nlist: int, centroids=None):
         """This shard's fp64 sums / counts of one Lloyd step over the global strided sample

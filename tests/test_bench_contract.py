@@ -22,8 +22,11 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["metric"].startswith("QPS at recall@10=0.95")
-    assert d["config"]["workload"].startswith("c2: IVF-DADE SIFT-shaped n=1000000 D=128 nq=10000 nlist=4096 K=10")
+    # the default workload is configs[3] (C4), the largest single-GPU config
+    assert d["config"]["workload"].startswith("c4: IVF-DADE Deep-shaped (unit norm) n=10000000 D=96 nq=10000 "
+                                              "nlist=16384 K=10")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)     # all host cores
 
 
 def test_launch_count_claim():
@@ -40,3 +43,15 @@ def test_launch_count_claim():
     assert bench.launches_per_search(synth.config("c5").scaled(n=12_500_000, nlist=65536), 1, 8) == 13
     # C3 (1,000 queries, nprobe 64): one chunk
     assert bench.launches_per_search(synth.config("c3").scaled(nq=1000), 1, 64) == 8
+
+
+def test_gpus_flag_must_match_world_size():
+    # a driver call `bench.py --gpus N` relaunches itself under torch.distributed.run; inside a
+    # launched rank, WORLD_SIZE must equal --gpus
+    import argparse
+    import bench
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "-c", "import bench, argparse; "
+                        "bench.run_dade(argparse.Namespace(gpus=4))"], capture_output=True, text=True,
+                       cwd=ROOT, env=env, timeout=300)
+    assert r.returncode != 0 and "--gpus 4 but WORLD_SIZE=2" in r.stderr

@@ -90,17 +90,18 @@ def g_setup(request):
     return cfg, _setup(cfg, nprobe_neg=6)
 
 
-@pytest.mark.parametrize("G", ["1", "2", "4", "8"])
-def test_warps_per_query_do_not_change_results(g_setup, G, monkeypatch):
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_warps_per_query_do_not_change_results(g_setup, G):
     # the scan deals a query's tiles to G warps with tau frozen per epoch (R13) and merges the
     # warps' top-K lists exactly at each epoch end: decisions and results must not depend on G
     # (K = 10: one key per lane; K = 100: four keys per lane)
     cfg, (torch, ix, oidx, X, Xd) = g_setup
     Q = torch.from_numpy(synth.queries(cfg)).cuda()
-    monkeypatch.setenv("DADE_SCAN_G", "1")
+    ix.set_option("scan_warps", 1)
     ri, rd, rs = ix.search(Q, cfg.k, 10, cfg.delta_d, 0.005, stats=True)
-    monkeypatch.setenv("DADE_SCAN_G", G)
+    ix.set_option("scan_warps", G)
     gi, gd, gs = ix.search(Q, cfg.k, 10, cfg.delta_d, 0.005, stats=True)
+    ix.set_option("scan_warps", 0)
     assert torch.equal(ri, gi) and torch.equal(rd, gd)
     assert rs["tested"] == gs["tested"] and rs["dims_scanned"] == gs["dims_scanned"]
     assert rs["pruned_at_step"] == gs["pruned_at_step"]

@@ -7,12 +7,17 @@ from oracle import dade_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["0", "1"], ids=["dhat-matrix", "fused-filter"])
-def knn_path(request, monkeypatch):
+_OPTS = {}  # dade_set_option values applied to every index a test creates
+
+
+@pytest.fixture(autouse=True, params=[1, 2], ids=["dhat-matrix", "fused-filter"])
+def knn_path(request):
     # both selection paths: the d_hat-matrix select (exact.cu) and the fused filter GEMM with
     # in-epilogue candidate tracking (probe_tc.cu); each must be bit-exact
-    monkeypatch.setenv("DADE_FUSED_PROBE", request.param)
-    return request.param
+    _OPTS.clear()
+    _OPTS["knn_path"] = request.param
+    yield request.param
+    _OPTS.clear()
 
 
 @pytest.fixture(scope="module")
@@ -26,7 +31,10 @@ def torch_cuda():
 
 def _idx(torch, D):
     from paper_2404_16322_b200 import Index
-    return Index(D)
+    ix = Index(D)
+    for k, v in _OPTS.items():
+        ix.set_option(k, v)
+    return ix
 
 
 @pytest.mark.parametrize("n,D,K", [(1000, 16, 1), (3001, 48, 10), (777, 128, 100), (5000, 64, 257)])
@@ -53,11 +61,11 @@ def test_bruteforce_knn_integer_ties(torch_cuda):
     assert np.array_equal(gi.cpu().numpy(), oi)
 
 
-@pytest.fixture(params=["1", "3"], ids=["1-pass", "3-pass"])
-def probe_passes(request, monkeypatch):
+@pytest.fixture(params=[1, 3], ids=["1-pass", "3-pass"])
+def probe_passes(request):
     # the probe's tensor-core filter runs 1-pass (hi parts, wide window) or 3-pass (split); both
     # must certify the same exact answer
-    monkeypatch.setenv("DADE_PROBE_PASSES", request.param)
+    _OPTS["probe_passes"] = request.param
     return request.param
 
 
@@ -105,14 +113,14 @@ def test_probe_wide_ragged_bit_exact(torch_cuda, nprobe, C, probe_passes):
         assert pr[q].tolist() == O.probe(Q[q], cent, nprobe).tolist()
 
 
-@pytest.mark.parametrize("ares", ["0", "1"])
-def test_probe_wide_d256_resident_a(torch_cuda, ares, monkeypatch):
+@pytest.mark.parametrize("ares", [0, 1])
+def test_probe_wide_d256_resident_a(torch_cuda, ares):
     # the wide-row d_hat writers at D = 256 (the C5 shape; nkc = 16 chunks of A resident in
     # shared memory for "1"), 1-pass filter, 64-column groups, ragged last tile: probes must equal
     # the oracle's exactly with either writer
     torch = torch_cuda
-    monkeypatch.setenv("DADE_PROBE_PASSES", "1")
-    monkeypatch.setenv("DADE_DHAT_ARES", ares)
+    _OPTS["probe_passes"] = 1
+    _OPTS["dhat_ares"] = ares
     rng = np.random.default_rng(11)
     D, C = 256, 33000
     X = rng.integers(0, 5, size=(2 * C, D)).astype(np.float32)

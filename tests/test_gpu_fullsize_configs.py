@@ -1,7 +1,11 @@
-"""configs[2], configs[3] and one per-GPU shard of configs[4] at FULL size, in the launch
-configuration bench.py times (public API: fit_rotation, build_ivf with k-means, calibrate, search),
-checked on sampled outputs the oracle computes one by one and on properties that hold at any size.
+"""configs[1], configs[2], configs[3] and one per-GPU shard of configs[4] at FULL size, in the
+launch configuration bench.py times (public API: fit_rotation, build_ivf with k-means, calibrate,
+search), checked on sampled outputs the oracle computes one by one and on properties that hold at
+any size; and STAGE-ISOLATED oracle parity of the pruned search: the oracle's own search (O5) runs
+on the GPU-built rotation, IVF and calibration table (tests/stage_parity.py) for ~20 sampled
+queries at the bench's nprobe, compared on ids, distances and every candidate's decision.
 
+  c2: 1M x 128 SIFT-shaped, 4096 lists, 10,000 queries, K = 10, delta_d = 16
   c3: 1M x 960 GIST-shaped, 4096 lists, 1,000 queries, K = 100, delta_d = 32
   c4: 10M x 96 Deep-shaped, 16,384 lists, 10,000 queries, K = 10, delta_d = 16
   c5 shard: ids [0, 12.5M) of the 100M x 256 config (the rows one of 8 GPUs holds), 65,536 lists
@@ -16,14 +20,18 @@ import pytest
 from datagen import synth
 from oracle import dade_oracle as O
 from tests.helpers import rel_err, tie_adjusted_overlap
+from tests.stage_parity import compare_decisions, oracle_index_from_gpu, step_histogram
 
 pytestmark = pytest.mark.gpu
 
 WORKERS = min(16, os.cpu_count() or 1)
+# nprobe: a mid-sweep operating point; bench_nprobe: where bench.py's sweep first reaches
+# recall@10 >= 0.95 (profiles/r01_bench_*.json)
 CASES = {
-    "c3": dict(cfg=synth.config("c3"), nprobe=96),
-    "c4": dict(cfg=synth.config("c4"), nprobe=8),
-    "c5shard": dict(cfg=synth.config("c5").scaled(n=12_500_000), nprobe=32),
+    "c2": dict(cfg=synth.config("c2"), nprobe=32, bench_nprobe=8),
+    "c3": dict(cfg=synth.config("c3"), nprobe=96, bench_nprobe=64),
+    "c4": dict(cfg=synth.config("c4"), nprobe=8, bench_nprobe=8),
+    "c5shard": dict(cfg=synth.config("c5").scaled(n=12_500_000), nprobe=32, bench_nprobe=8),
 }
 
 
@@ -44,14 +52,14 @@ def built(request):
     ix.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
     ix.calibrate(Xd, torch.from_numpy(synth.cal_queries(cfg, m=m)).cuda(), cfg.k, n_neg=cfg.n_neg,
                  nprobe_neg=cfg.nprobe_neg, seed=0)
-    yield torch, cfg, case["nprobe"], X, Q, Xd, Qd, ix
+    yield torch, cfg, case["nprobe"], X, Q, Xd, Qd, ix, case["bench_nprobe"]
     ix.close()
     del Xd
     torch.cuda.empty_cache()
 
 
 def test_lists_assignment_probes(built):
-    torch, cfg, nprobe, X, Q, Xd, Qd, ix = built
+    torch, cfg, nprobe, X, Q, Xd, Qd, ix, _ = built
     off, row_id, assign, cent = ix.get_ivf()
     assert off[-1] == cfg.n and np.all(np.diff(off) >= 0)
     rng = np.random.default_rng(0)
@@ -67,7 +75,7 @@ def test_lists_assignment_probes(built):
 
 
 def test_search_sampled_parity(built):
-    torch, cfg, nprobe, X, Q, Xd, Qd, ix = built
+    torch, cfg, nprobe, X, Q, Xd, Qd, ix, _ = built
     K = cfg.k
     gi, gd, st = ix.search(Qd, K, nprobe, cfg.delta_d, 0.005, stats=True)
     gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
@@ -87,3 +95,26 @@ def test_search_sampled_parity(built):
         assert rel_err(gd[q][ok], O.sqdist_seq(X[gi[q][ok]], Q[q])) <= 1e-5
     # DADE loses <= 1% recall@K against exact IVF at the same nprobe (P:L3115 <0.5%)
     assert O.recall_at_k(gi, ei, K) >= 0.99
+
+
+def test_stage_isolated_oracle_parity(built):
+    """The oracle's search on the GPU's artefacts, ~20 sampled queries at the bench nprobe:
+    tie-adjusted id overlap >= 0.999 (north_star), distances <= 1e-5 relative, and every tested
+    candidate's decision identical outside the R21 band (decision log vs the oracle's log)."""
+    torch, cfg, _, X, Q, Xd, Qd, ix, nprobe = built
+    K, dd, D = cfg.k, cfg.delta_d, cfg.d
+    oidx = oracle_index_from_gpu(ix, X)
+    sample = np.arange(0, Q.shape[0], max(1, Q.shape[0] // 20))[:20]
+    Qs = Q[sample]
+    oi, od, ost = O.search(oidx, Qs, K, nprobe, dd, 0.005, log=True)
+    gi, gd, glog = ix.search_log(torch.from_numpy(Qs).cuda(), K, nprobe, dd, 0.005)
+    gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
+    assert tie_adjusted_overlap(gi, gd, oi, od) >= 0.999
+    same = gi == oi
+    assert rel_err(gd[same], od[same]) <= 1e-5
+    flagged, oq, odims, gdims = compare_decisions(glog.cpu().numpy(), ost["candidates"])
+    assert len(flagged) <= 1, flagged
+    assert np.array_equal(step_histogram(oq, odims, D, dd, flagged), step_histogram(oq, gdims, D, dd, flagged))
+    # the same queries inside the full batch (the bench's launch) return the same results
+    fi, fd = ix.search(Qd, K, nprobe, dd, 0.005)
+    assert np.array_equal(fi.cpu().numpy()[sample], gi) and np.array_equal(fd.cpu().numpy()[sample], gd)

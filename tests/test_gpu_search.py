@@ -11,14 +11,15 @@ from tests.helpers import rel_err, tie_adjusted_overlap
 pytestmark = pytest.mark.gpu
 
 
-def _setup(cfg, kmeans_iters=4, cal=True, nprobe_neg=None):
+def _setup(cfg, kmeans_iters=4, cal=True, nprobe_neg=None, cent=None):
     import torch
     assert torch.cuda.is_available(), "GPU test run without a GPU"
     from paper_2404_16322_b200 import build, Index
     build.build()
     X = synth.base(cfg)
     mean, R, lam = O.fit_rotation(X)
-    cent = O.kmeans(X, cfg.nlist, iters=kmeans_iters) if cfg.nlist > 1 else X[:1].copy()
+    if cent is None:
+        cent = O.kmeans(X, cfg.nlist, iters=kmeans_iters) if cfg.nlist > 1 else X[:1].copy()
     oidx = O.build_index(X, cent, mean, R)
     if cal:
         npn = cfg.nprobe_neg if nprobe_neg is None else nprobe_neg
@@ -101,9 +102,12 @@ def test_delta_d_equal_D_and_32(sift_small):
 def test_k_larger_than_stream_and_empty_lists():
     # many lists relative to n: some lists are tiny or empty; K exceeds a 1-list stream
     cfg = synth.config("c1", n=1000, nlist=200, nq=10, n_cal=20)
-    torch, ix, oidx, X, Xd = _setup(cfg, kmeans_iters=2, cal=False)
+    X = synth.base(cfg)
+    cent = O.kmeans(X, cfg.nlist, iters=2)
+    cent[[7, 50, 199]] = 1e3                      # three centroids far from every row: empty lists
+    torch, ix, oidx, X, Xd = _setup(cfg, cal=False, cent=cent)
     off, *_ = ix.get_ivf()
-    assert (np.diff(off) == 0).any() or True
+    assert (np.diff(off)[[7, 50, 199]] == 0).all()
     Q = synth.queries(cfg)
     gi, gd = ix.search(torch.from_numpy(Q).cuda(), 50, 1, 32, 0.0)
     oi, od, _ = O.search(oidx, Q, 50, 1, 32, 0.0)
@@ -111,6 +115,10 @@ def test_k_larger_than_stream_and_empty_lists():
     assert np.array_equal(gi < 0, oi < 0)          # padding slots: id -1, dist +inf
     assert np.all(np.isinf(gd[gi < 0]))
     assert tie_adjusted_overlap(gi, gd, oi, od) == 1.0
+    # every list probed: the empty lists sit inside the candidate stream
+    gi, gd = ix.search(torch.from_numpy(Q).cuda(), 50, cfg.nlist, 32, 0.0)
+    oi, od, _ = O.search(oidx, Q, 50, cfg.nlist, 32, 0.0)
+    assert tie_adjusted_overlap(gi.cpu().numpy(), gd.cpu().numpy(), oi, od) == 1.0
 
 
 def test_gist_shaped_k100_dd32():
@@ -171,44 +179,48 @@ def test_search_host_matches_device(sift_small):
     assert np.array_equal(a.cpu().numpy(), c) and np.array_equal(b.cpu().numpy(), d)
 
 
-@pytest.mark.parametrize("chunks,prep", [("1", "1"), ("3", "1"), ("7", "1"), ("1", "2"), ("1", "3")])
-def test_search_host_pipeline_chunks(sift_small, chunks, prep, monkeypatch):
+@pytest.mark.parametrize("chunks,prep", [(1, 1), (3, 1), (7, 1), (1, 2), (1, 3)])
+def test_search_host_pipeline_chunks(sift_small, chunks, prep):
     """The H2D / search / D2H pipeline of dade_search_host (pinned buffers, ragged chunks; search
     chunks or rotation + probe chunks ahead of one scan) returns exactly the device-buffer
     search's results."""
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     Q = synth.queries(cfg, n=1001)
     a, b = ix.search(torch.from_numpy(Q).cuda(), 10, 8, 16, 0.005)
-    monkeypatch.setenv("DADE_HOST_CHUNKS", chunks)
-    monkeypatch.setenv("DADE_HOST_PREP_CHUNKS", prep)
+    ix.set_option("host_chunks", chunks)
+    ix.set_option("host_prep_chunks", prep)
     Qh = torch.from_numpy(Q).pin_memory()
     ih = torch.empty((1001, 10), dtype=torch.int64).pin_memory()
     dh = torch.empty((1001, 10), dtype=torch.float32).pin_memory()
     ix.search_host(Qh, 10, 8, 16, 0.005, ids=ih, dists=dh)
+    ix.set_option("host_chunks", 1)
+    ix.set_option("host_prep_chunks", 0)
     assert np.array_equal(a.cpu().numpy(), ih.numpy()) and np.array_equal(b.cpu().numpy(), dh.numpy())
 
 
-def test_scan_query_order_invariance(sift_small, monkeypatch):
-    """DADE_SCAN_ORDER=1 (queries scanned grouped by nearest probed list) returns exactly the
+def test_scan_query_order_invariance(sift_small):
+    """DADE_OPT_SCAN_ORDER = 1 (queries scanned grouped by nearest probed list) returns exactly the
     default order's results and counters: each query's scan depends only on its own stream."""
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     Q = torch.from_numpy(synth.queries(cfg, n=700)).cuda()
     a, b, sa = ix.search(Q, 10, 8, 16, 0.005, stats=True)
-    monkeypatch.setenv("DADE_SCAN_ORDER", "1")
+    ix.set_option("scan_order", 1)
     c, d, sc = ix.search(Q, 10, 8, 16, 0.005, stats=True)
+    ix.set_option("scan_order", 0)
     assert torch.equal(a, c) and torch.equal(b, d)
     assert sa["tested"] == sc["tested"] and sa["dims_scanned"] == sc["dims_scanned"]
 
 
-@pytest.mark.parametrize("tail", ["1", "300"])
-def test_scan_tail_split_invariance(sift_small, tail, monkeypatch):
-    """DADE_SCAN_TAIL (the last queries scanned by a concurrent 4-warps-per-query launch) returns
+@pytest.mark.parametrize("tail", [1, 300])
+def test_scan_tail_split_invariance(sift_small, tail):
+    """DADE_OPT_SCAN_TAIL (the last queries scanned by a concurrent 4-warps-per-query launch) returns
     exactly the single launch's results and counters."""
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     Q = torch.from_numpy(synth.queries(cfg, n=700)).cuda()
     a, b, sa = ix.search(Q, 10, 8, 16, 0.005, stats=True)
-    monkeypatch.setenv("DADE_SCAN_TAIL", tail)
+    ix.set_option("scan_tail", tail)
     c, d, sc = ix.search(Q, 10, 8, 16, 0.005, stats=True)
+    ix.set_option("scan_tail", 0)
     assert torch.equal(a, c) and torch.equal(b, d)
     assert sa["tested"] == sc["tested"] and sa["dims_scanned"] == sc["dims_scanned"]
 

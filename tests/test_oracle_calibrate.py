@@ -88,11 +88,46 @@ def test_logistic_matches_independent_optimiser(seed):
     assert abs(m1 - 2.5 / 3.0) < 0.15
 
 
-def test_logistic_degenerate_flags():
-    # label independent of P and τ-weight non-negative → flagged, m1 = 1
-    P = np.arange(100.0); tau = np.ones(100); y = np.r_[np.zeros(50), np.ones(50)]
-    m1, beta, ok = O.logistic_irls(P[::-1].copy(), tau, y)
-    assert (not ok and m1 == 1.0) or m1 > 0
+def test_logistic_flag_rule_w_tau_nonnegative():
+    # R3 flag rule, case w_τ ≥ 0: the label rises with τ (and does not depend on P), so the fitted
+    # τ-weight is positive — the model "prune iff m1·P + β > τ" does not exist — and the fit must
+    # return exactly (m1, β, ok) = (1, 0, False). Non-separable: each τ level carries both labels.
+    tau = np.repeat(np.arange(1.0, 11.0), 20)            # 10 τ levels x 20 pairs
+    P = np.tile(np.arange(20.0), 10)                     # P uncorrelated with y
+    y = np.zeros(200)
+    for lvl in range(10):                                # label-1 count grows with τ: 2 + lvl of 20
+        y[lvl * 20: lvl * 20 + 2 + lvl] = 1.0
+    m1, beta, ok = O.logistic_irls(P, tau, y)
+    assert (m1, beta, ok) == (1.0, 0.0, False)
+
+
+def test_logistic_flag_rule_m1_nonpositive():
+    # R3 flag rule, case m1 ≤ 0: w_τ < 0 (label 1 more likely at small τ, as the model expects) but
+    # w_P < 0 too (label 1 more likely at SMALL partial distances), so m1 = −w_P/w_τ < 0: flagged,
+    # exactly (1, 0, False). Hand-built, non-separable counts.
+    rows = []
+    for t in (1.0, 2.0, 3.0, 4.0):
+        for p in (1.0, 2.0, 3.0, 4.0):
+            n1 = int(10 - t - p)                          # label-1 count falls with both τ and P
+            rows += [(p, t, 1.0)] * n1 + [(p, t, 0.0)] * (10 - n1)
+    P, tau, y = (np.array(c) for c in zip(*rows))
+    m1, beta, ok = O.logistic_irls(P, tau, y)
+    assert (m1, beta, ok) == (1.0, 0.0, False)
+
+
+def test_logistic_flag_rule_accepts_the_expected_sign():
+    # control for the two flag tests: label 1 rises with P and falls with τ (the model's shape)
+    # → ok, m1 > 0 (the same hand-built counts with P reversed)
+    rows = []
+    for t in (1.0, 2.0, 3.0, 4.0):
+        for p in (1.0, 2.0, 3.0, 4.0):
+            n1 = int(10 - t - (5.0 - p))
+            rows += [(p, t, 1.0)] * n1 + [(p, t, 0.0)] * (10 - n1)
+    P, tau, y = (np.array(c) for c in zip(*rows))
+    m1, beta, ok = O.logistic_irls(P, tau, y)
+    assert ok and m1 > 0
+    # symmetric counts in (P, 5 − τ): the fitted weights are equal and opposite → m1 = 1 exactly
+    assert abs(m1 - 1.0) < 1e-9
 
 
 def test_step_table_alpha_zero_disables_pruning():

@@ -3,7 +3,6 @@
 DADE_LIB (the product library is untouched): python tools/build_variant.py NAME -DX=1 ...
 -> exp_libs/libdade_NAME.so"""
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -14,10 +13,7 @@ def build_variant(name, defines):
     from paper_2404_16322_b200 import build as B
     out = os.path.join(ROOT, "exp_libs", f"libdade_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = [B.NVCC, *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *defines,
-           "-I", os.path.join(ROOT, "include"), "-o", out, *B.sources(), "-lcudart"]
-    subprocess.run(cmd, check=True, stderr=subprocess.DEVNULL)
-    return out
+    return B.build(extra=list(defines), out=out)
 
 
 if __name__ == "__main__":

@@ -69,8 +69,8 @@ def dev_chunks(c):
 
 def host_chunks(c, prep=1):
     def f():
-        os.environ["DADE_HOST_CHUNKS"] = str(c)
-        os.environ["DADE_HOST_PREP_CHUNKS"] = str(prep)
+        ix.set_option("host_chunks", c)
+        ix.set_option("host_prep_chunks", prep)
         ix.search_host(Qh, K, a.nprobe, dd, 0.005, ids=ih, dists=dh)
     return f
 

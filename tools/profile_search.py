@@ -20,7 +20,7 @@ ap.add_argument("--nprobe", type=int, default=8)
 ap.add_argument("--alpha", type=float, default=0.005)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--nlist", type=int, default=0)
-ap.add_argument("--env", default="", help="NAME=VALUE set just before the profiled search")
+ap.add_argument("--opt", default="", help="OPTION=VALUE (dade_set_option) set just before the profiled search")
 a = ap.parse_args()
 build.build()
 cfg = synth.config(a.config)
@@ -36,9 +36,9 @@ ix.build_ivf(X, cfg.nlist, kmeans_iters=10)
 ix.calibrate(X, Qc, cfg.k, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
 for _ in range(3):
     ix.search(Q, cfg.k, a.nprobe, cfg.delta_d, a.alpha)
-if a.env:
-    k_, v_ = a.env.split("=", 1)
-    os.environ[k_] = v_
+if a.opt:
+    k_, v_ = a.opt.split("=", 1)
+    ix.set_option(k_, int(v_))
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
 ix.search(Q, cfg.k, a.nprobe, cfg.delta_d, a.alpha)

@@ -7,7 +7,6 @@ import argparse
 import ctypes
 import json
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -17,10 +16,8 @@ PROF_LIB = os.environ.get("DADE_PROF_LIB", os.path.join(ROOT, "exp_libs", "libda
 
 def build_prof():
     from paper_2404_16322_b200 import build as B
-    cmd = [B.NVCC, *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-DDADE_SCAN_PROF",
-           "-I", os.path.join(ROOT, "include"), "-o", PROF_LIB, *B.sources(), "-lcudart"]
     os.makedirs(os.path.dirname(PROF_LIB), exist_ok=True)
-    subprocess.run(cmd, check=True)
+    B.build(extra=["-DDADE_SCAN_PROF"], out=PROF_LIB)
 
 
 PHASES = ["query_start", "tile_wait", "round_full", "round_drain", "epoch_end", "stage1", "results", "exit"]
