@@ -120,10 +120,10 @@ def run_dade(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     if world > 1:
-        # NCCL over NVLink in production; DADE_DIST_BACKEND=gloo runs the same multi-rank code path
-        # on a single visible GPU as a functional check (its timings are not a measurement)
-        dist.init_process_group(os.environ.get("DADE_DIST_BACKEND", "nccl"))
-    local = local % max(1, torch.cuda.device_count())
+        # the process group carries the NCCL unique id, barriers and the max-over-ranks timing;
+        # the data path's collectives run on the library's own NCCL communicator
+        dist.init_process_group("nccl")
+    assert world <= torch.cuda.device_count(), "one GPU per rank"
     torch.cuda.set_device(local)
     from paper_2404_16322_b200 import Index, build, sharded
     if rank == 0:
@@ -157,8 +157,9 @@ def run_dade(args):
     # identical on every rank and equal to the single-GPU build's.
     t0 = time.time()
     ix = Index(cfg.d, local, stream)
-    if world > 1:  # a0: fp64 partial moments + all-reduce
-        sharded.fit_rotation_sharded(ix, Xd, lo, cfg.n)
+    if world > 1:  # the library joins its own NCCL group; a0: fp64 partial moments all-reduced inside
+        sharded.attach_comm(ix)
+        ix.fit_rotation_dist(Xd, lo, cfg.n)
     else:
         ix.fit_rotation(Xd)
     if args.method == "adsampling":  # ADSampling's projection: a Haar-random orthogonal matrix
@@ -166,16 +167,15 @@ def run_dade(args):
         ix.set_rotation(mean, synth.haar_basis(cfg.d, np.random.default_rng(12345)).T.copy(), lam)
     torch.cuda.synchronize()
     t_rot = time.time() - t0
-    if world > 1:  # k-means: fp64 per-centroid sums / counts all-reduced; then the local IVF
-        cent = sharded.kmeans_sharded(ix, Xd, lo, cfg.n, cfg.nlist, iters=10)
-        ix.build_ivf(Xd, cfg.nlist, centroids=torch.from_numpy(cent).to(dev), id_base=lo)
+    if world > 1:  # k-means: fp64 per-centroid sums / counts all-reduced inside; then the local IVF
+        ix.build_ivf_dist(Xd, lo, cfg.n, cfg.nlist, kmeans_iters=10)
     else:
         ix.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
     torch.cuda.synchronize()
     t_ivf = time.time() - t0 - t_rot
     if args.method == "bsa_p":
-        if world > 1:  # R14-R16 over the shards: merged K-NN, merged negatives, summed P_d
-            sharded.calibrate_sharded(ix, Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
+        if world > 1:  # R14-R16 over the shards: merged K-NN, merged negatives, summed P_d (inside)
+            ix.calibrate_dist(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
         else:
             ix.calibrate(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
     torch.cuda.synchronize()
@@ -193,20 +193,10 @@ def run_dade(args):
     dists = torch.empty((cfg.nq, K), dtype=torch.float32, device=dev)
 
 
-    qpart = sharded.QueryPartitionedSearch(ix) if world > 1 else None
-
-    def shard_stats(nprobe):
-        """N > 1: counters and stage times of this rank's scan of all queries (a separate prepared
-        search; never inside a timed region)."""
-        qr, pr = ix.prepare(Qd, nprobe)
-        return ix.search_prepared(qr, pr, K, dd, args.method, METHOD_PARAM[args.method], stats=True)[2]
-
     def step(nprobe, stats=False):
-        if world > 1:
-            # N > 1: each rank rotates + probes nq/N queries, NCCL all-gather of q~ and probes,
-            # every rank scans all queries on its shard, NCCL all-gather of the local top-K + merge
-            out = qpart.search(Qd, K, nprobe, dd, args.method, METHOD_PARAM[args.method])
-            return out, (shard_stats(nprobe) if stats else None)
+        # N > 1 the call is collective inside the library: each rank rotates + probes nq/N queries,
+        # NCCL all-gather of q~ and probes, every rank scans all queries on its shard, NCCL
+        # all-gather of the local top-K + merge kernel (stats = this rank's shard counters)
         if args.method == "bsa_p":
             r = ix.search(Qd, K, nprobe, dd, ALPHA, ids=ids, dists=dists, stats=stats)
         else:
@@ -256,7 +246,7 @@ def run_dade(args):
     # the roofline is read from those events after each step; the counters (deterministic) come
     # from one untimed stats call
     ix.set_timing(True)
-    stats_acc = step(chosen, stats=True)[1] if world == 1 else shard_stats(chosen)
+    stats_acc = step(chosen, stats=True)[1]
     with Clocks(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)
@@ -292,13 +282,8 @@ def run_dade(args):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if args.method == "bsa_p" and world == 1:
+        if args.method == "bsa_p":  # N > 1: H2D, the collective search (NCCL inside), D2H
             ix.search_host(Qh, K, chosen, dd, ALPHA, ids=ih, dists=dh)
-        elif world > 1:  # H2D, the query-partitioned multi-GPU search (NCCL inside), D2H
-            Qtmp.copy_(Qh, non_blocking=True)
-            oi, od = qpart.search(Qtmp, K, chosen, dd, args.method, METHOD_PARAM[args.method])
-            ih.copy_(oi, non_blocking=True)
-            dh.copy_(od, non_blocking=True)
         else:  # H2D of the queries, search, D2H of the results, all on the library's stream
             Qtmp.copy_(Qh, non_blocking=True)
             ix.search_method(Qtmp, K, chosen, dd, args.method, METHOD_PARAM[args.method], ids=ids, dists=dists)
@@ -471,7 +456,7 @@ def cpu_baseline(cfg, nprobe, budget_s=15.0):
     """The oracle as it stands, float64 NumPy, one process per host core (1 BLAS thread each),
     each worker searching its own queries until the time budget runs out."""
     cores, _ = _cpu_info()
-    nq = 64 * cores
+    nq = 2000 * cores           # more than any worker finishes in the budget: the deadline stops them
     pool, cores, model, sub, nlist = _oracle_pool(cfg, nprobe, nq)
     try:
         per = nq // cores

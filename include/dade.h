@@ -304,6 +304,50 @@ dade_status dade_bruteforce_knn(dade_index* idx, const float* X, int64_t n, int6
 dade_status dade_merge_topk(dade_index* idx, const int64_t* ids_in, const float* dists_in, int S,
                             int nq, int K, int64_t* ids_out, float* dists_out);
 
+/* ---------------------------------------------------------------- multi-rank
+ * The database is sharded by contiguous global-id ranges, one index (one process, one GPU) per
+ * shard; mu, R, the centroids and the calibration table are replicated. The library owns the NCCL
+ * communicator (libnccl.so.2 is loaded at run time; absent -> DADE_ERR_NCCL).
+ *   dade_comm_unique_id  one rank creates the 128-byte NCCL unique id (host); the caller
+ *                        distributes it to the other ranks (any out-of-band channel).
+ *   dade_set_comm        every rank joins the group (collective; blocks until all have joined).
+ *                        id may be NULL when nranks == 1. Replaces a previous communicator.
+ * With a communicator (any nranks), dade_search / dade_search_method / dade_search_host are
+ * COLLECTIVE: every rank passes the same queries; rank r rotates and probes its block of
+ * ceil(nq/S) queries, the q~ and probe blocks are all-gathered (ncclAllGather), every rank scans all
+ * queries over its shard, and the local top-K lists are all-gathered and merged by (dist, id); every
+ * rank receives the full result. Each shard prunes against its own tau (its local K-th distance,
+ * >= the global one): never unsafe; alpha = 0 gives exactly the unsharded exact IVF.
+ * The sharded build (collective; X = this rank's rows, global ids [id_base, id_base+n) of n_total):
+ *   dade_fit_rotation_dist  a0 on the GLOBAL strided sample (fp64 moments all-reduced);
+ *   dade_build_ivf_dist     k-means on the global strided sample (R19; per-iteration fp64 sums and
+ *                           counts all-reduced), then this shard's lists for all nlist centroids;
+ *   dade_calibrate_dist     a3: shard K-NN lists merged, negatives merged, pair features summed —
+ *                           the same table as an unsharded dade_calibrate on the whole base.
+ * Errors: NCCL, STATE (no communicator for the _dist calls), and as the single-GPU calls. */
+dade_status dade_comm_unique_id(void* id128);
+dade_status dade_set_comm(dade_index* idx, const void* id128, int nranks, int rank);
+dade_status dade_fit_rotation_dist(dade_index* idx, const float* X, int64_t n, int64_t id_base, int64_t n_total,
+                                   int64_t sample_size);
+dade_status dade_build_ivf_dist(dade_index* idx, const float* X, int64_t n, int64_t id_base, int64_t n_total,
+                                int nlist, int kmeans_iters);
+dade_status dade_calibrate_dist(dade_index* idx, const float* X, const float* Qc, int nq, int K, int n_neg,
+                                int nprobe_neg, uint64_t seed);
+/* Host combination steps of the sharded build (HOST arrays, no index, no GPU; the steps
+ * dade_*_dist run between collectives, exported for drivers that move the buffers themselves):
+ *   dade_kmeans_update      centroid[c] = fp32(sums[c] / counts[c]) where counts[c] > 0 (R19);
+ *   dade_merge_knn          ids/dists S x nq x K (rank-major) -> the first K by (fp64 dist, id) (R14);
+ *   dade_calibration_pairs  per query: its K nearest (Label 0) then the n_neg smallest (hash, id)
+ *                           over the S shards' negative candidates keys/neg_ids S x nq x n_neg,
+ *                           counts S x nq (Label 1), tau = the K-th distance (R15/R16); outputs
+ *                           sized nq*(K+n_neg), *npairs = pairs written. */
+dade_status dade_kmeans_update(int nlist, int D, const double* sums, const int64_t* counts, float* centroids);
+dade_status dade_merge_knn(int S, int nq, int K, const int64_t* ids, const double* dists, int64_t* out_ids,
+                           double* out_dists);
+dade_status dade_calibration_pairs(int S, int nq, int K, int n_neg, const int64_t* knn_ids, const double* knn_dists,
+                                   const uint64_t* keys, const int64_t* neg_ids, const int32_t* counts,
+                                   int32_t* pair_q, int64_t* pair_id, double* tau, double* y, int64_t* npairs);
+
 /* Persistence of {rotation, IVF, layout, calibration} (little-endian binary). */
 dade_status dade_save(const dade_index* idx, const char* path);
 dade_status dade_load(dade_index* idx, const char* path);

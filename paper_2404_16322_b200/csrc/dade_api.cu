@@ -7,6 +7,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "dade_internal.h"
@@ -82,6 +83,11 @@ struct dade_index {
   // dade_search_host: copy streams and per-chunk events of the H2D / search / D2H pipeline
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> hev;
+  // multi-rank (dade_set_comm): the NCCL communicator of this shard's group
+  Comm* comm = nullptr;
+  DBuf<int64_t> gids;    // collective search: all-gathered local top-K ids / dists
+  DBuf<float> gdists;
+  DBuf<double> red;      // device staging of host partials for all-reduce
 };
 
 // ------------------------------------------------------------------ error plumbing
@@ -580,6 +586,78 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   }
 }
 
+// Collective search (dade_set_comm with nranks > 1): every rank passes the same
+// queries. Rank r rotates and probes its block of ceil(nq / S) queries (a4 + a5), the blocks of
+// q~ and probe lists are all-gathered in place, every rank scans ALL queries over its own shard
+// (a6-a8), and the local top-K lists are all-gathered and merged by (dist, id) (a9, k_merge_topk).
+// mu, R and the centroids are replicated, so a query's q~ and probes are the same whichever rank
+// prepared them; with alpha = 0 the result equals the unsharded search.
+void do_search_collective(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d, double alpha,
+                          int64_t* ids, float* dists, dade_stats* stats, int method) {
+  const int S = comm_size(x->comm), r = comm_rank(x->comm);
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
+  DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
+  DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
+  DADE_REQUIRE(K >= 1 && K <= DADE_MAX_K, DADE_ERR_ARG, "K not in [1, DADE_MAX_K]");
+  if (nq == 0) return;
+  need(Q, "Q"); need(ids, "ids"); need(dists, "dists");
+  const int per = (nq + S - 1) / S;
+  const int lo = std::min(r * per, nq), hi = std::min(lo + per, nq);
+  x->qrot.reserve((size_t)S * per * D);
+  x->probes.reserve((size_t)S * per * nprobe);
+  float* qr = x->qrot.p + (size_t)r * per * D;
+  int32_t* pr = x->probes.p + (size_t)r * per * nprobe;
+  if (hi > lo) prepare(x, Q + (size_t)lo * D, hi - lo, nprobe, qr, pr, false);
+  comm_allgather(x->comm, qr, x->qrot.p, sizeof(float) * per * D, st);
+  comm_allgather(x->comm, pr, x->probes.p, sizeof(int32_t) * per * nprobe, st);
+  x->gids.reserve((size_t)S * nq * K);
+  x->gdists.reserve((size_t)S * nq * K);
+  int64_t* li = x->gids.p + (size_t)r * nq * K;
+  float* ld = x->gdists.p + (size_t)r * nq * K;
+  // the local scan over this shard (scratch q~ / probes are the gathered buffers: the scan reads
+  // them in place; do_search does not touch x->qrot / x->probes when they are passed in)
+  do_search(x, nullptr, nq, K, nprobe, delta_d, alpha, li, ld, stats, method, x->qrot.p, x->probes.p);
+  comm_allgather(x->comm, li, x->gids.p, sizeof(int64_t) * nq * K, st);
+  comm_allgather(x->comm, ld, x->gdists.p, sizeof(float) * nq * K, st);
+  launch_merge_topk(x->gids.p, x->gdists.p, S, nq, K, ids, dists, st);
+  if (stats) DADE_CK(cudaStreamSynchronize(st));
+}
+
+// any communicator makes the searches collective (a group of one runs the same schedule: the
+// all-gathers are copies and the merge sorts one list — the single-GPU test of this path)
+bool collective(const dade_index* x) { return x->comm != nullptr; }
+
+// all-reduce (sum) of a HOST array over the index's communicator, staged through the device
+template <typename T>
+void allreduce_host(dade_index* x, T* a, size_t count) {
+  if (!x->comm || count == 0) return;
+  static_assert(sizeof(T) == 8, "fp64 / int64 only");
+  x->red.reserve(count);
+  DADE_CK(cudaMemcpyAsync(x->red.p, a, 8 * count, cudaMemcpyHostToDevice, x->stream));
+  comm_allreduce_sum(x->comm, x->red.p, count, std::is_same<T, double>::value ? CommType::F64 : CommType::I64,
+                     x->stream);
+  DADE_CK(cudaMemcpyAsync(a, x->red.p, 8 * count, cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+}
+
+// all-gather of a HOST array (same size on every rank) -> out[S * count]
+template <typename T>
+void allgather_host(dade_index* x, const T* a, size_t count, T* out) {
+  const int S = comm_size(x->comm), r = comm_rank(x->comm);
+  if (count == 0) return;
+  const size_t words = (count * sizeof(T) + 7) / 8;
+  x->red.reserve((size_t)S * words);
+  char* base = reinterpret_cast<char*>(x->red.p);
+  DADE_CK(cudaMemcpyAsync(base + (size_t)r * words * 8, a, sizeof(T) * count, cudaMemcpyHostToDevice, x->stream));
+  comm_allgather(x->comm, base + (size_t)r * words * 8, base, words * 8, x->stream);
+  for (int s = 0; s < S; ++s)
+    DADE_CK(cudaMemcpyAsync(out + (size_t)s * count, base + (size_t)s * words * 8, sizeof(T) * count,
+                            cudaMemcpyDeviceToHost, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+}
+
 }  // namespace
 
 // ================================================================== lifecycle
@@ -625,6 +703,8 @@ extern "C" dade_status dade_destroy(dade_index* x) {
       cudaStreamDestroy(s2);
     }
   for (auto e : x->hev) cudaEventDestroy(e);
+  x->gids.release(); x->gdists.release(); x->red.release();
+  comm_destroy(x->comm);
   delete x;
   API_END
 }
@@ -1248,7 +1328,8 @@ extern "C" dade_status dade_search(dade_index* x, const float* Q, int nq, int K,
   API_BEGIN
   need(x, "index");
   DeviceGuard g(x->device);
-  do_search(x, Q, nq, K, nprobe, delta_d, significance, ids, dists, stats);
+  if (collective(x)) do_search_collective(x, Q, nq, K, nprobe, delta_d, significance, ids, dists, stats, DADE_METHOD_BSA_P);
+  else do_search(x, Q, nq, K, nprobe, delta_d, significance, ids, dists, stats);
   API_END
 }
 
@@ -1258,7 +1339,8 @@ extern "C" dade_status dade_search_method(dade_index* x, const float* Q, int nq,
   API_BEGIN
   need(x, "index");
   DeviceGuard g(x->device);
-  do_search(x, Q, nq, K, nprobe, delta_d, param, ids, dists, stats, method);
+  if (collective(x)) do_search_collective(x, Q, nq, K, nprobe, delta_d, param, ids, dists, stats, method);
+  else do_search(x, Q, nq, K, nprobe, delta_d, param, ids, dists, stats, method);
   API_END
 }
 
@@ -1320,6 +1402,19 @@ extern "C" dade_status dade_search_host(dade_index* x, const float* Qh, int nq, 
   // Pipeline: the batch is cut into chunks; chunk c's H2D (copy stream) overlaps the search of
   // chunk c-1 (library stream), whose results' D2H (second copy stream) overlaps chunk c's search.
   // Stats need one search over the whole batch, so they run unchunked.
+  if (collective(x)) {  // H2D, the collective search (NCCL inside), D2H
+    if (nq > 0) {
+      DADE_CK(cudaMemcpyAsync(x->qbuf.p, Qh, sizeof(float) * nq * D, cudaMemcpyHostToDevice, st));
+      do_search_collective(x, x->qbuf.p, nq, K, nprobe, delta_d, significance, x->ids_tmp.p, x->dists_tmp.p, stats,
+                           DADE_METHOD_BSA_P);
+      DADE_CK(cudaMemcpyAsync(ids_h, x->ids_tmp.p, sizeof(int64_t) * nq * K, cudaMemcpyDeviceToHost, st));
+      DADE_CK(cudaMemcpyAsync(dists_h, x->dists_tmp.p, sizeof(float) * nq * K, cudaMemcpyDeviceToHost, st));
+    }
+    DADE_CK(cudaStreamSynchronize(st));
+    check_knn_flag(x);
+    g_err.clear();
+    return DADE_OK;
+  }
   int nch = host_chunks(x, nq);
   if (stats || nq <= 0) nch = 1;
   if (!x->h2d) {
@@ -1674,5 +1769,167 @@ extern "C" dade_status dade_search_log(dade_index* x, const float* Q, int nq, in
   dl.buf = log; dl.cap = log_cap; dl.count = log_count;
   *log_count = 0;
   do_search(x, Q, nq, K, nprobe, delta_d, param, ids, dists, nullptr, method, nullptr, nullptr, &dl);
+  API_END
+}
+
+// ================================================================== multi-rank
+extern "C" dade_status dade_comm_unique_id(void* id128) {
+  API_BEGIN
+  need(id128, "id");
+  comm_unique_id(id128);
+  API_END
+}
+
+extern "C" dade_status dade_set_comm(dade_index* x, const void* id128, int nranks, int rank) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, DADE_ERR_ARG, "bad nranks / rank");
+  DeviceGuard g(x->device);
+  unsigned char own[128];
+  if (!id128) {
+    DADE_REQUIRE(nranks == 1, DADE_ERR_ARG, "a group of more than one rank needs the shared unique id");
+    comm_unique_id(own);
+    id128 = own;
+  }
+  Comm* c = comm_create(id128, nranks, rank);
+  comm_destroy(x->comm);
+  x->comm = c;
+  API_END
+}
+
+// a0 over a sharded base: fp64 partial moments of the owned strided-sample rows, all-reduced
+extern "C" dade_status dade_fit_rotation_dist(dade_index* x, const float* X, int64_t n, int64_t id_base,
+                                              int64_t n_total, int64_t sample_size) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->comm, DADE_ERR_STATE, "dade_fit_rotation_dist needs dade_set_comm");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  std::vector<double> sum(D + 1), cov((size_t)D * D);
+  int64_t cnt = 0;
+  dade_status s = dade_pca_mean_partial(x, X, n, id_base, n_total, sample_size, sum.data(), &cnt);
+  if (s != DADE_OK) throw Error(s, g_err);
+  sum[D] = (double)cnt;                                   // exact: counts < 2^53
+  allreduce_host(x, sum.data(), sum.size());
+  const int64_t tot = (int64_t)sum[D];
+  DADE_REQUIRE(tot > 0, DADE_ERR_ARG, "empty PCA sample");
+  std::vector<double> mean(D);
+  for (int j = 0; j < D; ++j) mean[j] = sum[j] / (double)tot;
+  s = dade_pca_cov_partial(x, X, n, id_base, n_total, sample_size, mean.data(), cov.data());
+  if (s != DADE_OK) throw Error(s, g_err);
+  allreduce_host(x, cov.data(), cov.size());
+  s = dade_set_rotation_from_cov(x, mean.data(), cov.data(), tot);
+  if (s != DADE_OK) throw Error(s, g_err);
+  API_END
+}
+
+// a2 over a sharded base: k-means (R19) on the GLOBAL strided sample — the init rows and every
+// Lloyd step's fp64 per-cluster sums / counts all-reduced, the update on every rank — then this
+// rank's sub-lists for all nlist global centroids (a1 + a2 on the shard)
+extern "C" dade_status dade_build_ivf_dist(dade_index* x, const float* X, int64_t n, int64_t id_base,
+                                           int64_t n_total, int nlist, int kmeans_iters) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->comm, DADE_ERR_STATE, "dade_build_ivf_dist needs dade_set_comm");
+  DADE_REQUIRE(kmeans_iters >= 0, DADE_ERR_ARG, "kmeans_iters < 0");
+  DeviceGuard g(x->device);
+  const int D = x->D;
+  std::vector<double> sums((size_t)nlist * D);
+  std::vector<int64_t> counts(nlist);
+  std::vector<float> cent((size_t)nlist * D);
+  dade_status s = dade_kmeans_partial(x, X, n, id_base, n_total, nlist, nullptr, sums.data(), counts.data());
+  if (s != DADE_OK) throw Error(s, g_err);
+  allreduce_host(x, sums.data(), sums.size());
+  for (size_t i = 0; i < cent.size(); ++i) cent[i] = (float)sums[i];   // the first nlist sampled rows
+  for (int it = 0; it < kmeans_iters; ++it) {
+    s = dade_kmeans_partial(x, X, n, id_base, n_total, nlist, cent.data(), sums.data(), counts.data());
+    if (s != DADE_OK) throw Error(s, g_err);
+    allreduce_host(x, sums.data(), sums.size());
+    allreduce_host(x, counts.data(), counts.size());
+    kmeans_update(nlist, D, sums.data(), counts.data(), cent.data());
+  }
+  DBuf<float> cd;
+  cd.reserve(cent.size());
+  DADE_CK(cudaMemcpyAsync(cd.p, cent.data(), 4 * cent.size(), cudaMemcpyHostToDevice, x->stream));
+  s = dade_build_ivf(x, X, n, id_base, nlist, cd.p, 0);
+  cd.release();
+  if (s != DADE_OK) throw Error(s, g_err);
+  API_END
+}
+
+// a3 over a sharded base (R14-R16): merged K-NN, merged negatives, summed pair features, then the
+// same fit on every rank — the table equals an unsharded dade_calibrate on the whole base
+extern "C" dade_status dade_calibrate_dist(dade_index* x, const float* X, const float* Qc, int nq, int K,
+                                           int n_neg, int nprobe_neg, uint64_t seed) {
+  API_BEGIN
+  need(x, "index"); need(X, "X"); need(Qc, "Qc");
+  DADE_REQUIRE(x->comm, DADE_ERR_STATE, "dade_calibrate_dist needs dade_set_comm");
+  DeviceGuard g(x->device);
+  calib_checks(x, Qc, nq, K, n_neg, nprobe_neg);
+  DADE_REQUIRE(K <= x->n, DADE_ERR_ARG, "K > shard size");
+  const int S = comm_size(x->comm);
+  std::vector<int64_t> ki;
+  std::vector<double> kd;
+  calib_knn(x, X, Qc, nq, K, ki, kd);
+  std::vector<int64_t> gi((size_t)S * nq * K), mi((size_t)nq * K);
+  std::vector<double> gd((size_t)S * nq * K), md((size_t)nq * K);
+  allgather_host(x, ki.data(), ki.size(), gi.data());
+  allgather_host(x, kd.data(), kd.size(), gd.data());
+  merge_knn(S, nq, K, gi.data(), gd.data(), mi.data(), md.data());
+  std::vector<std::vector<std::pair<uint64_t, int64_t>>> neg;
+  calib_negatives(x, Qc, nq, K, mi.data(), n_neg, nprobe_neg, seed, neg);
+  const size_t w = std::max(n_neg, 1);
+  std::vector<uint64_t> keys((size_t)nq * w, 0), gk((size_t)S * nq * w);
+  std::vector<int64_t> nid((size_t)nq * w, 0), gn((size_t)S * nq * w);
+  std::vector<int32_t> cnt(nq), gc((size_t)S * nq);
+  for (int q = 0; q < nq; ++q) {
+    cnt[q] = (int32_t)neg[q].size();
+    for (size_t j = 0; j < neg[q].size(); ++j) { keys[q * w + j] = neg[q][j].first; nid[q * w + j] = neg[q][j].second; }
+  }
+  allgather_host(x, keys.data(), keys.size(), gk.data());
+  allgather_host(x, nid.data(), nid.size(), gn.data());
+  allgather_host(x, cnt.data(), cnt.size(), gc.data());
+  const size_t cap = (size_t)nq * (K + n_neg);
+  std::vector<int32_t> pq(cap);
+  std::vector<int64_t> pid(cap);
+  std::vector<double> tau(cap), y(cap);
+  const int64_t np = calibration_pairs(S, nq, K, (int)w, mi.data(), md.data(), gk.data(), gn.data(), gc.data(),
+                                       pq.data(), pid.data(), tau.data(), y.data());
+  std::vector<double> F;
+  pair_features(x, Qc, nq, (int)np, pq.data(), pid.data(), F);
+  allreduce_host(x, F.data(), F.size());
+  fit_calibration(x, K, (int)np, F.data(), tau.data(), y.data());
+  API_END
+}
+
+// host combination steps of the sharded build (no index, no GPU): the process-group driver
+// (sharded.py) moves the buffers and calls these
+extern "C" dade_status dade_kmeans_update(int nlist, int D, const double* sums, const int64_t* counts,
+                                          float* centroids) {
+  API_BEGIN
+  need(sums, "sums"); need(counts, "counts"); need(centroids, "centroids");
+  DADE_REQUIRE(nlist >= 1 && D >= 1, DADE_ERR_ARG, "bad nlist / D");
+  kmeans_update(nlist, D, sums, counts, centroids);
+  API_END
+}
+
+extern "C" dade_status dade_merge_knn(int S, int nq, int K, const int64_t* ids, const double* dists,
+                                      int64_t* out_ids, double* out_dists) {
+  API_BEGIN
+  need(ids, "ids"); need(dists, "dists"); need(out_ids, "out_ids"); need(out_dists, "out_dists");
+  DADE_REQUIRE(S >= 1 && nq >= 0 && K >= 1, DADE_ERR_ARG, "bad S / nq / K");
+  merge_knn(S, nq, K, ids, dists, out_ids, out_dists);
+  API_END
+}
+
+extern "C" dade_status dade_calibration_pairs(int S, int nq, int K, int n_neg, const int64_t* knn_ids,
+                                              const double* knn_dists, const uint64_t* keys, const int64_t* neg_ids,
+                                              const int32_t* counts, int32_t* pair_q, int64_t* pair_id,
+                                              double* tau, double* y, int64_t* npairs) {
+  API_BEGIN
+  need(knn_ids, "knn_ids"); need(knn_dists, "knn_dists"); need(counts, "counts"); need(npairs, "npairs");
+  need(pair_q, "pair_q"); need(pair_id, "pair_id"); need(tau, "tau"); need(y, "y");
+  DADE_REQUIRE(S >= 1 && nq >= 0 && K >= 1 && n_neg >= 1, DADE_ERR_ARG, "bad S / nq / K / n_neg");
+  *npairs = calibration_pairs(S, nq, K, n_neg, knn_ids, knn_dists, keys, neg_ids, counts, pair_q, pair_id, tau, y);
   API_END
 }

@@ -182,6 +182,24 @@ void launch_to_blocked(const float* X, int64_t n, int D, float* out, cudaStream_
 void launch_gather_rows(const float* X, const int32_t* rows, int64_t m, int D, float* out,
                         cudaStream_t st);
 
+// comm.cpp : the index's NCCL communicator (dlopen'd libnccl) and the sharded build's host steps
+struct Comm;
+enum class CommType { F64, I64 };
+void comm_unique_id(void* out128);
+Comm* comm_create(const void* id128, int nranks, int rank);
+void comm_destroy(Comm* c);
+int comm_size(const Comm* c);
+int comm_rank(const Comm* c);
+// in-place sum over ranks of a DEVICE buffer, on `st`
+void comm_allreduce_sum(Comm* c, void* buf, size_t count, CommType t, cudaStream_t st);
+// DEVICE all-gather: recv = rank 0's bytes, rank 1's, ... (in place when send == recv + rank * bytes)
+void comm_allgather(Comm* c, const void* send, void* recv, size_t bytes_per_rank, cudaStream_t st);
+void kmeans_update(int nlist, int D, const double* sums, const int64_t* counts, float* cent);
+void merge_knn(int S, int nq, int K, const int64_t* ids, const double* d, int64_t* out_ids, double* out_d);
+int64_t calibration_pairs(int S, int nq, int K, int n_neg, const int64_t* knn_ids, const double* knn_d,
+                          const uint64_t* keys, const int64_t* nids, const int32_t* cnt, int32_t* pq,
+                          int64_t* pid, double* tau, double* y);
+
 // host_eig.cpp : symmetric eigendecomposition (Householder tridiagonalisation + implicit QL)
 void sym_eig(int n, const double* A, double* eigval, double* eigvec_colmajor);
 // host_calib.cpp

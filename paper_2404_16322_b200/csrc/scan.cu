@@ -41,6 +41,9 @@ namespace dade {
 
 namespace {
 constexpr int TR = 32;            // rows per tile: one row per lane
+#ifndef DADE_SCAN_REG1  // register cap of the Delta_d = 16, K <= 64 kernels (experiment builds may change it)
+#define DADE_SCAN_REG1 80
+#endif
 #ifndef DADE_EPOCH_GROWTH  // R13: epoch boundaries c0, 2 c0, 4 c0, ... (experiment builds may change it)
 #define DADE_EPOCH_GROWTH 2
 #endif
@@ -287,6 +290,7 @@ __device__ __forceinline__ void log_decision(const ScanParams& p, int64_t q, int
 // classifier step index of block count blk: ns = blk / dd if blk is a multiple of dd, else 0
 // (dd = p.dd, magic = ceil(2^32 / dd): exact for blk, dd <= 256)
 __device__ __forceinline__ int step_of(int blk, int dd, unsigned magic) {
+  if (dd == 1) return blk;
   const int ns = (int)__umulhi((unsigned)blk, magic);
   return ns * dd == blk ? ns : 0;
 }
@@ -706,7 +710,7 @@ static void launch_k(const ScanParams& p, cudaStream_t st) {
   } else {
     // 80 registers (24 one-warp CTAs per SM) measured best on C2 and C4 against 64, 72 and 96
     // (C4 scan 1.200 ms vs 1.454 / 1.264 / 1.284, profiles/r02_scan_variants.jsonl)
-    launch_v<DD, KPL, 1, (KPL >= 4 ? 96 : 80)>(p, st);
+    launch_v<DD, KPL, 1, (KPL >= 4 ? 96 : DADE_SCAN_REG1)>(p, st);
   }
 }
 
@@ -734,7 +738,7 @@ void launch_scan(const ScanParams& p, cudaStream_t st) {
   DADE_REQUIRE(p.K <= 256, DADE_ERR_UNSUPPORTED, "scan: K > 256");
   DADE_REQUIRE(p.dd >= 1 && p.dd * 16 <= p.D && p.D % (p.dd * 16) == 0, DADE_ERR_ARG, "scan: bad delta_d");
   ScanParams q = p;
-  q.dd_magic = (unsigned)((((uint64_t)1 << 32) + (uint64_t)p.dd - 1) / (uint64_t)p.dd);
+  q.dd_magic = p.dd == 1 ? 0u : (unsigned)((((uint64_t)1 << 32) + (uint64_t)p.dd - 1) / (uint64_t)p.dd);
   // staging unit: the largest of 4, 2, 1 blocks dividing the classifier spacing
   switch (p.dd % 4 == 0 ? 4 : p.dd % 2 == 0 ? 2 : 1) {
     case 4: launch_dd<4>(q, st); break;

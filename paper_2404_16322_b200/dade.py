@@ -80,6 +80,14 @@ _SIGS = {
     "dade_set_ivf": [P, P, I64, I64, P, P, I32, P],
     "dade_set_option": [P, I32, I64],
     "dade_search_log": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P, I64, P],
+    "dade_comm_unique_id": [P],
+    "dade_set_comm": [P, P, I32, I32],
+    "dade_fit_rotation_dist": [P, P, I64, I64, I64, I64],
+    "dade_build_ivf_dist": [P, P, I64, I64, I64, I32, I32],
+    "dade_calibrate_dist": [P, P, P, I32, I32, I32, I32, C.c_uint64],
+    "dade_kmeans_update": [I32, I32, P, P, P],
+    "dade_merge_knn": [I32, I32, I32, P, P, P, P],
+    "dade_calibration_pairs": [I32, I32, I32, I32, P, P, P, P, P, P, P, P, P, P],
     "dade_save": [P, C.c_char_p],
     "dade_load": [P, C.c_char_p],
 }
@@ -123,6 +131,47 @@ def _dev(t, dtype):
     assert isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.is_contiguous(), \
         f"expected a contiguous CUDA {dtype} tensor"
     return t
+
+
+# ---------------------------------------------------------------- host steps of the sharded build
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id for dade_set_comm (created on one rank, shared with the others)."""
+    buf = C.create_string_buffer(128)
+    _ck(lib().dade_comm_unique_id(C.cast(buf, P)))
+    return buf.raw
+
+
+def kmeans_update(sums, counts, centroids):
+    """dade_kmeans_update: centroid = fp32(sum / count) where count > 0 (in place on `centroids`)."""
+    sums = np.ascontiguousarray(sums, np.float64); counts = np.ascontiguousarray(counts, np.int64)
+    assert centroids.dtype == np.float32 and centroids.flags["C_CONTIGUOUS"]
+    _ck(lib().dade_kmeans_update(centroids.shape[0], centroids.shape[1], _ptr(sums), _ptr(counts), _ptr(centroids)))
+    return centroids
+
+
+def merge_knn(ids_g, d_g, K: int):
+    """dade_merge_knn: [S, nq, K] shard K-NN lists (global ids, fp64) -> the global K-NN by (dist, id)."""
+    ids_g = np.ascontiguousarray(ids_g, np.int64); d_g = np.ascontiguousarray(d_g, np.float64)
+    S, nq, _ = ids_g.shape
+    oi = np.zeros((nq, K), np.int64); od = np.zeros((nq, K))
+    _ck(lib().dade_merge_knn(S, nq, K, _ptr(ids_g), _ptr(d_g), _ptr(oi), _ptr(od)))
+    return oi, od
+
+
+def calibration_pairs(knn_ids, knn_d, keys_g, nids_g, cnt_g, n_neg: int):
+    """dade_calibration_pairs: (pair_q, pair_id, tau, y) in dade_calibrate's order."""
+    knn_ids = np.ascontiguousarray(knn_ids, np.int64); knn_d = np.ascontiguousarray(knn_d, np.float64)
+    keys_g = np.ascontiguousarray(keys_g, np.uint64); nids_g = np.ascontiguousarray(nids_g, np.int64)
+    cnt_g = np.ascontiguousarray(cnt_g, np.int32)
+    S, nq, w = keys_g.shape
+    K = knn_ids.shape[1]
+    cap = nq * (K + w)
+    pq = np.zeros(cap, np.int32); pid = np.zeros(cap, np.int64); tau = np.zeros(cap); y = np.zeros(cap)
+    npairs = np.zeros(1, np.int64)
+    _ck(lib().dade_calibration_pairs(S, nq, K, w, _ptr(knn_ids), _ptr(knn_d), _ptr(keys_g), _ptr(nids_g),
+                                     _ptr(cnt_g), _ptr(pq), _ptr(pid), _ptr(tau), _ptr(y), _ptr(npairs)))
+    n = int(npairs[0])
+    return pq[:n], pid[:n], tau[:n], y[:n]
 
 
 class Index:
@@ -425,6 +474,28 @@ class Index:
         d = torch.empty((nq, K), dtype=torch.float32, device=ids_in.device)
         _ck(lib().dade_merge_topk(self.h, _ptr(ids_in), _ptr(dists_in), S, nq, K, _ptr(ids), _ptr(d)))
         return ids, d
+
+    # -------------------------------------------------- multi-rank (the library owns NCCL)
+    def set_comm(self, uid, nranks: int, rank: int):
+        """Join the NCCL group (collective). uid: the 128-byte id from comm_unique_id() (None for a
+        group of one). Afterwards search / search_method / search_host are collective."""
+        buf = None if uid is None else C.create_string_buffer(bytes(uid), 128)
+        _ck(lib().dade_set_comm(self.h, None if buf is None else C.cast(buf, P), nranks, rank))
+
+    def fit_rotation_dist(self, X, id_base: int, n_total: int, sample_size: int = 0):
+        import torch
+        X = _dev(X, torch.float32)
+        _ck(lib().dade_fit_rotation_dist(self.h, _ptr(X), X.shape[0], id_base, n_total, sample_size))
+
+    def build_ivf_dist(self, X, id_base: int, n_total: int, nlist: int, kmeans_iters: int = 10):
+        import torch
+        X = _dev(X, torch.float32)
+        _ck(lib().dade_build_ivf_dist(self.h, _ptr(X), X.shape[0], id_base, n_total, nlist, kmeans_iters))
+
+    def calibrate_dist(self, X, Qc, K: int, n_neg: int = 50, nprobe_neg: int = 0, seed: int = 0):
+        import torch
+        X = _dev(X, torch.float32); Qc = _dev(Qc, torch.float32)
+        _ck(lib().dade_calibrate_dist(self.h, _ptr(X), _ptr(Qc), Qc.shape[0], K, n_neg, nprobe_neg, seed))
 
     def save(self, path: str):
         _ck(lib().dade_save(self.h, path.encode()))
