@@ -524,3 +524,226 @@ def estimate_knn(index, Q: np.ndarray, d: int, K: int, estimator: str = "partial
         o = order_by_dist_id(e, gid)[:K]
         ids[i], est[i] = gid[o], e[o]
     return ids, est
+
+
+# ----------------------------------------------------------------------------- NEXT-3 BSA-q (§V-B)
+# The data-driven correction on a QUANTIZATION distance: dis' = the asymmetric
+# distance (ADC) from the query to the product-quantized candidate, OPQ rotation, one
+# extra feature = the candidate's distance to its own quantized reconstruction.
+# Readings R28-R30: OPQ trained on a strided sample of 65,536 rows,
+# PCA-initialised, alternating per-subspace k-means and orthogonal Procrustes; m = D/4 subspaces
+# (D/8 for GIST-like data), 8-bit codes; one classifier (PQ has no incremental
+# refinement: survivors get the exact distance), target recall r (α_s = α).
+PQ_K = 256  # 2^nbits codewords per subspace, nbits = 8
+
+
+def pq_subspaces(D: int, gist_like: bool = False) -> int:
+    """m = D/8 for GIST, D/4 for the other datasets."""
+    return D // 8 if gist_like else D // 4
+
+
+def pq_kmeans(Z: np.ndarray, iters: int, init: np.ndarray | None = None) -> np.ndarray:
+    """One subspace's codebook: k-means with 256 centroids on the rows of Z (R28): init = the first
+    256 rows (the sample is strided, so they are spread over the base) unless `init` is given,
+    `iters` Lloyd iterations with exact assignment (`assign`: fp64 sequential sums, lower code on
+    ties), centroid = fp64 mean rounded to fp32, an empty cell keeps its centroid."""
+    C = (np.asarray(Z[:PQ_K], np.float64) if init is None else np.asarray(init, np.float64)).astype(np.float32)
+    for _ in range(iters):
+        a = assign(Z, C)
+        sums = np.zeros((PQ_K, Z.shape[1]))
+        np.add.at(sums, a, np.asarray(Z, np.float64))
+        cnt = np.bincount(a, minlength=PQ_K)
+        nz = cnt > 0
+        C[nz] = (sums[nz] / cnt[nz, None]).astype(np.float32)
+    return C
+
+
+def pq_encode(Xr: np.ndarray, C: np.ndarray):
+    """PQ code of each rotated row: per subspace j the nearest codeword of C[j]
+    (256 x D/m), exact fp64 sequential sums, ties to the lower code (R30); and the row's distance
+    to its reconstruction e = ||x − x̂||² (the extra feature), fp64.
+    Returns codes (n x m uint8), e (n fp64)."""
+    Xr = np.asarray(Xr)
+    m, _, ds = C.shape
+    codes = np.zeros((Xr.shape[0], m), np.uint8)
+    e = np.zeros(Xr.shape[0])
+    for j in range(m):
+        Z = Xr[:, j * ds:(j + 1) * ds]
+        a = assign(Z, C[j])
+        codes[:, j] = a
+        diff = np.asarray(Z, np.float64) - C[j][a].astype(np.float64)
+        e += np.sum(diff * diff, axis=1)
+    return codes, e
+
+
+def procrustes(X: np.ndarray, Y: np.ndarray) -> np.ndarray:
+    """Orthogonal R minimising Σ_rows ||R x − y||² (OPQ's rotation step): with
+    M = Σ x yᵀ = U S Vᵀ, R = V Uᵀ."""
+    M = np.asarray(X, np.float64).T @ np.asarray(Y, np.float64)
+    U, _, Vt = np.linalg.svd(M)
+    return Vt.T @ U.T
+
+
+def opq_train(X: np.ndarray, m: int, n_train: int = 65536, iters: int = 8, km_iters: int = 4,
+              final_iters: int = 10):
+    """OPQ on a strided sample of min(N, 65,536) rows, R28: centred on the
+    sample mean; R initialised to the sample's PCA rotation (fit_rotation); `iters` rounds of
+    {per-subspace k-means (`km_iters` Lloyd iterations, warm-started), R ← procrustes(x − μ,
+    reconstruction)}; then `final_iters` Lloyd iterations of the codebooks on the final rotation.
+    Returns (mean[D], R[D,D] rows = directions, C[m, 256, D/m] fp32)."""
+    X = np.asarray(X)
+    n, D = X.shape
+    ds = D // m
+    S = X[strided_ids(n, min(n, n_train))]
+    mean, R, _ = fit_rotation(S, sample_size=S.shape[0])
+    Xc = S.astype(np.float64) - mean
+    C = None
+    for _ in range(iters):
+        Z = Xc @ R.T
+        C = np.stack([pq_kmeans(Z[:, j * ds:(j + 1) * ds], km_iters, None if C is None else C[j])
+                      for j in range(m)])
+        codes, _ = pq_encode(Z, C)
+        Y = np.concatenate([C[j][codes[:, j]].astype(np.float64) for j in range(m)], axis=1)
+        R = procrustes(Xc, Y)
+    Z = Xc @ R.T
+    C = np.stack([pq_kmeans(Z[:, j * ds:(j + 1) * ds], final_iters, None if C is None else C[j])
+                  for j in range(m)])
+    return mean, R, C
+
+
+def adc_lut(q_rot: np.ndarray, C: np.ndarray) -> np.ndarray:
+    """Asymmetric distance look-up table: lut[j, c] = ||q_j − C[j, c]||², fp64."""
+    m, _, ds = C.shape
+    q = np.asarray(q_rot, np.float64)
+    lut = np.zeros((m, PQ_K))
+    for j in range(m):
+        d = C[j].astype(np.float64) - q[j * ds:(j + 1) * ds]
+        lut[j] = np.sum(d * d, axis=1)
+    return lut
+
+
+def adc(lut: np.ndarray, codes: np.ndarray) -> np.ndarray:
+    """ADC distance of coded rows: Σ_j lut[j, code_j] (m table look-ups)."""
+    return lut[np.arange(lut.shape[0])[None, :], np.asarray(codes, np.int64)].sum(axis=1)
+
+
+def logistic_irls_multi(F: np.ndarray, tau: np.ndarray, y: np.ndarray, ridge: float = 1e-8,
+                        max_iter: int = 100, tol: float = 1e-12):
+    """logistic_irls with several approximate-distance features (ADC distance and the
+    distance to the quantized centroid, plus τ): the BCE minimiser by damped Newton/IRLS on
+    standardised features (R3). Returns (m[k], β, ok): the model m·f + β > τ, m_i = −w_i/w_τ.
+    Flag (R29): w_τ ≥ 0, a non-finite weight, or m_0 (the ADC slope) ≤ 0 → (e_0, 0, False)."""
+    F = np.atleast_2d(np.asarray(F, F64).T).T
+    n, k = F.shape
+    tau = np.asarray(tau, F64); y = np.asarray(y, F64)
+    mf, sf = F.mean(axis=0), F.std(axis=0)
+    sf = np.where(sf > 0, sf, 1.0)
+    mt, st = tau.mean(), tau.std()
+    st = st if st > 0 else 1.0
+    A = np.concatenate([np.ones((n, 1)), (F - mf) / sf, ((tau - mt) / st)[:, None]], axis=1)
+    reg = np.r_[0.0, np.full(k + 1, ridge)]
+
+    def loss(w):
+        z = A @ w
+        return float(np.sum(np.logaddexp(0.0, z) - y * z) + 0.5 * np.sum(reg * w * w))
+
+    w = np.zeros(k + 2)
+    cur = loss(w)
+    for _ in range(max_iter):
+        z = A @ w
+        p = 0.5 * (1.0 + np.tanh(0.5 * z))
+        g = A.T @ (y - p) - reg * w
+        H = (A * (p * (1 - p))[:, None]).T @ A + np.diag(reg)
+        step = np.linalg.solve(H, g)
+        t = 1.0
+        for _h in range(30):
+            nw = w + t * step
+            nl = loss(nw)
+            if nl <= cur:
+                break
+            t *= 0.5
+        w, cur = nw, nl
+        if np.max(np.abs(t * step)) < tol:
+            break
+    wf, wt = w[1:k + 1] / sf, w[k + 1] / st
+    b = w[0] - np.sum(w[1:k + 1] * mf / sf) - w[k + 1] * mt / st
+    unit = np.r_[1.0, np.zeros(k - 1)]
+    if not (wt < 0) or not np.all(np.isfinite(wf)) or not np.isfinite(wt):
+        return unit, 0.0, False
+    mv = -wf / wt
+    if not (mv[0] > 0) or not np.all(np.isfinite(mv)):
+        return unit, 0.0, False
+    return mv, float(-b / wt), True
+
+
+def build_index_q(X, centroids, mean, R, C, id_base=0):
+    """build_index plus the PQ encoding of the rotated base (codes, reconstruction errors)."""
+    idx = build_index(X, centroids, mean, R, id_base=id_base)
+    idx["pq"] = np.asarray(C, np.float32)
+    idx["codes"], idx["pq_err"] = pq_encode(idx["Xr"], idx["pq"])
+    return idx
+
+
+def calibrate_q(X, index, Qc, K, n_neg=50, nprobe_neg=0, seed=0):
+    """§V-A correction on the ADC distance (BSA-q): the calibration pairs of
+    `calibration_pairs` (R14-R16), features (ADC dis', e) and τ, the logistic fit (R3/R29), and
+    v = sort_desc(τ − m_1·dis' − m_2·e) over the Label-0 pairs, from which search derives β'."""
+    qi, ids, lab, tau = calibration_pairs(X, index, Qc, K, n_neg, nprobe_neg, seed)
+    Qr = rotate(Qc, index["mean"], index["R"])
+    rows = ids - index["id_base"]
+    dis = np.array([adc(adc_lut(Qr[q], index["pq"]), index["codes"][r:r + 1])[0] for q, r in zip(qi, rows)])
+    e = index["pq_err"][rows]
+    mv, _, ok = logistic_irls_multi(np.stack([dis, e], axis=1), tau, lab)
+    v = np.sort(tau[lab == 0] - mv[0] * dis[lab == 0] - mv[1] * e[lab == 0])[::-1]
+    return {"m": mv, "v": v, "ok": ok, "n0": int(np.sum(lab == 0)), "K": K}
+
+
+def search_q(index, Q, K, nprobe, alpha, c0=None, log=False):
+    """IVF search with the quantization-distance correction (BSA-q, O5 with one classifier):
+    per candidate of the probed lists (probe order), dis' = ADC(q̃, code), prune iff τ_e < ∞ and
+    m_1·dis' + m_2·e + β' > τ_e with β' = v[k−1], k = clamp(⌈(1−α)·n0⌉, 1, n0) (R4; one classifier,
+    α_s = α, R29); survivors get the exact distance P_D over the rotated vectors and enter
+    the top-K; τ frozen per epoch (R13). α = 0 disables pruning. Logged dims: 0 for an ADC prune
+    (only the code was read), D for a survivor."""
+    Q = np.atleast_2d(Q)
+    D = Q.shape[1]
+    cal = index["calq"]
+    beta = -np.inf if alpha == 0 else beta_from_v(cal["v"], alpha)
+    m1, m2 = cal["m"]
+    off, row_id, Xr, base = index["off"], index["row_id"], index["Xr"], index["id_base"]
+    codes, err = index["codes"], index["pq_err"]
+    out_ids = np.full((Q.shape[0], K), -1, dtype=np.int64)
+    out_d = np.full((Q.shape[0], K), np.inf)
+    st = {"tested": 0, "survivors": 0, "pruned": 0, "n_epochs": 0, "candidates": []}
+    Qr = rotate(Q, index["mean"], index["R"])
+    for qn in range(Q.shape[0]):
+        pr = probe(Q[qn], index["centroids"], nprobe)
+        cand = np.concatenate([row_id[off[l]:off[l + 1]] for l in pr])
+        lut = adc_lut(Qr[qn], index["pq"])
+        top_d = np.zeros(0); top_i = np.zeros(0, dtype=np.int64)
+        st["tested"] += len(cand)
+        bounds = epoch_bounds(len(cand), K, c0)
+        st["n_epochs"] = max(st["n_epochs"], len(bounds) - 1)
+        for e in range(len(bounds) - 1):
+            tau = top_d[K - 1] if len(top_d) >= K else np.inf
+            ids = cand[bounds[e]:bounds[e + 1]]
+            rows = ids - base
+            keep = np.ones(len(ids), dtype=bool)
+            margin = np.full(len(ids), np.inf)
+            if np.isfinite(tau) and np.isfinite(beta):
+                score = m1 * adc(lut, codes[rows]) + m2 * err[rows] + beta
+                keep = ~(score > tau)
+                scale = np.abs(score - beta) + abs(beta) + tau
+                margin = np.abs(score - tau) / scale
+            st["pruned"] += int((~keep).sum())
+            st["survivors"] += int(keep.sum())
+            dis = np.sum((Xr[rows[keep]] - Qr[qn]) ** 2, axis=1)
+            if log:
+                st["candidates"].append((np.full(len(ids), qn), ids.copy(), np.where(keep, D, 0), margin))
+            cd = np.concatenate([top_d, dis])
+            ci = np.concatenate([top_i, ids[keep]])
+            o = order_by_dist_id(cd, ci)[:K]
+            top_d, top_i = cd[o], ci[o]
+        out_ids[qn, :len(top_i)] = top_i
+        out_d[qn, :len(top_d)] = top_d
+    return out_ids, out_d, st
