@@ -177,6 +177,7 @@ dade_status dade_search(dade_index* idx, const float* Q, int nq, int K, int npro
 #define DADE_METHOD_BSA_P 0
 #define DADE_METHOD_ADSAMPLING 1
 #define DADE_METHOD_BSA_RES 2
+#define DADE_METHOD_BSA_Q 3   /* NEXT-3, see the BSA-q section below; param = significance alpha */
 dade_status dade_search_method(dade_index* idx, const float* Q, int nq, int K, int nprobe, int delta_d,
                                int method, double param, int64_t* ids, float* dists, dade_stats* stats);
 
@@ -303,6 +304,41 @@ dade_status dade_bruteforce_knn(dade_index* idx, const float* X, int64_t n, int6
  * are ignored. */
 dade_status dade_merge_topk(dade_index* idx, const int64_t* ids_in, const float* dists_in, int S,
                             int nq, int K, int64_t* ids_out, float* dists_out);
+
+/* ---------------------------------------------------------------- NEXT-3: BSA-q (§V-B)
+ * The data-driven correction on a QUANTIZATION distance: dis' = the asymmetric distance (ADC) of
+ * the query to the candidate's product-quantization code (m subspaces of D/m dims, 256 codewords
+ * each: nbits = 8; m = D/4, D/8 for GIST-like data), OPQ rotation, and the
+ * candidate's distance to its own reconstruction e = ||x~ - x^||^2 as a second feature.
+ * One classifier (R29): prune iff m1 * dis' + m2 * e + beta' > tau; survivors get the exact
+ * distance and enter the top-K; tau frozen per epoch (R13) as in dade_search.
+ *   dade_train_pq   OPQ on a strided sample of min(n, n_train ? n_train : 65,536) rows (P:L3105,
+ *                   R28): PCA init, `iters` rounds of per-subspace k-means (km_iters Lloyd
+ *                   iterations) + orthogonal Procrustes, then final_iters Lloyd iterations.
+ *                   X: device n x D raw rows. INSTALLS the OPQ rotation as the index rotation
+ *                   (discarding a built IVF: build_ivf afterwards) and the codebooks.
+ *   dade_set_pq     install codebooks (host m x 256 x D/m fp32, row-major) in the CURRENT rotation's
+ *                   basis; the layout (if built) is encoded at once.
+ *   dade_get_pq     *m, codebooks (host, may be NULL), codes (host n x m, list-major rows) and err
+ *                   (host n fp32 reconstruction errors) of the layout (may be NULL).
+ *   Codes (R30): per subspace the argmin over the 256 codewords of the fp64 sequential sum of
+ *   (x~_i - c_i)^2 over the subspace's dims of the STORED fp32 x~, ties to the lower code.
+ *   dade_calibrate_pq  as dade_calibrate (same Label 0/1 pairs, R14-R16) with features (ADC dis', e):
+ *                   two-feature logistic fit (R3, R29) -> m1, m2; v = sort_desc(tau - m1 dis' - m2 e)
+ *                   over Label-0 pairs; a search with significance alpha uses beta' = v[k-1],
+ *                   k = clamp(ceil((1 - alpha) n0), 1, n0).
+ *   dade_get/set_calibration_q  K, n0, m[2] = {m1, m2}, v[n0] (host).
+ * Search: dade_search_method(..., DADE_METHOD_BSA_Q, alpha, ...); stats->pruned_at_step[0] counts
+ * the ADC prunes (0 dims read), n_steps = 1. PQ state is not saved by dade_save.
+ * Errors: ARG (m does not divide D, D/m > 32, < 256 training rows), STATE (order), NONFINITE, CUDA. */
+dade_status dade_train_pq(dade_index* idx, const float* X, int64_t n, int m, int64_t n_train, int iters,
+                          int km_iters, int final_iters);
+dade_status dade_set_pq(dade_index* idx, int m, const float* codebooks);
+dade_status dade_get_pq(const dade_index* idx, int* m, float* codebooks, uint8_t* codes, float* err);
+dade_status dade_calibrate_pq(dade_index* idx, const float* X, const float* Qc, int nq, int K, int n_neg,
+                              int nprobe_neg, uint64_t seed);
+dade_status dade_get_calibration_q(const dade_index* idx, int* K, int* n0, double* m, double* v);
+dade_status dade_set_calibration_q(dade_index* idx, int K, int n0, const double* m, const double* v);
 
 /* ---------------------------------------------------------------- multi-rank
  * The database is sharded by contiguous global-id ranges, one index (one process, one GPU) per

@@ -83,6 +83,18 @@ struct dade_index {
   // dade_search_host: copy streams and per-chunk events of the H2D / search / D2H pipeline
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> hev;
+  // NEXT-3 BSA-q: PQ codebooks (m x 256 x D/m, in the current rotation's basis), the code rows of
+  // the layout (list-major; codes | fp32 reconstruction error | pad, pq_stride bytes), calibration
+  bool has_pq = false;
+  int pq_m = 0, pq_stride = 0, pq_eo = 0;
+  std::vector<float> pq_C;
+  DBuf<float> pq_Cd;
+  DBuf<uint8_t> pq_codes;
+  bool pq_codes_ok = false;
+  bool has_calq = false;
+  int calqK = 0, n0q = 0;
+  double mq[2] = {1.0, 0.0};
+  std::vector<double> vq;
   // multi-rank (dade_set_comm): the NCCL communicator of this shard's group
   Comm* comm = nullptr;
   DBuf<int64_t> gids;    // collective search: all-gathered local top-K ids / dists
@@ -319,12 +331,66 @@ void upload_rotation(dade_index* x) {
   x->has_ivf = false;
   x->has_cal = false;
   x->xnorm_ok = false;
+  x->has_pq = false;  // codebooks live in the old basis
+  x->pq_codes_ok = false;
+  x->has_calq = false;
   x->R_d.reserve((size_t)D * D);
   x->mean_d.reserve(D);
   DADE_CK(cudaMemcpyAsync(x->R_d.p, x->R.data(), sizeof(double) * D * D, cudaMemcpyHostToDevice, x->stream));
   DADE_CK(cudaMemcpyAsync(x->mean_d.p, x->mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice, x->stream));
   DADE_CK(cudaStreamSynchronize(x->stream));
   x->has_rot = true;
+}
+
+// PQ code rows of the current layout (R30): codes | fp32 reconstruction error, stride bytes
+void pq_encode_layout(dade_index* x) {
+  x->pq_codes_ok = false;
+  x->has_calq = false;
+  if (!x->has_pq || !x->has_ivf) return;
+  x->pq_codes.reserve((size_t)x->n * x->pq_stride);
+  DADE_CK(cudaMemsetAsync(x->pq_codes.p, 0, (size_t)x->n * x->pq_stride, x->stream));
+  launch_pq_assign(x->layout.p, true, x->n, x->D, x->pq_m, x->pq_Cd.p, x->pq_codes.p, x->pq_stride, x->stream);
+  launch_pq_err(x->layout.p, x->n, x->D, x->pq_m, x->pq_Cd.p, x->pq_codes.p, x->pq_stride, x->pq_eo, x->stream);
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  x->pq_codes_ok = true;
+}
+
+void install_pq(dade_index* x, int m, const float* C) {
+  const int D = x->D;
+  DADE_REQUIRE(m >= 1 && D % m == 0 && D / m <= 32, DADE_ERR_ARG, "pq: m must divide D with D/m <= 32");
+  for (size_t i = 0; i < (size_t)D * 256; ++i) DADE_REQUIRE(std::isfinite(C[i]), DADE_ERR_NONFINITE, "pq: non-finite codebook");
+  x->pq_m = m;
+  x->pq_eo = (m + 3) & ~3;
+  x->pq_stride = (x->pq_eo + 4 + 15) & ~15;
+  DADE_REQUIRE(x->pq_stride <= 256, DADE_ERR_UNSUPPORTED, "pq: more than 248 subspaces");
+  x->pq_C.assign(C, C + (size_t)D * 256);
+  x->pq_Cd.reserve((size_t)D * 256);
+  DADE_CK(cudaMemcpyAsync(x->pq_Cd.p, x->pq_C.data(), sizeof(float) * D * 256, cudaMemcpyHostToDevice, x->stream));
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  x->has_pq = true;
+  pq_encode_layout(x);
+}
+
+// R from a covariance (eigenvectors by descending eigenvalue, sign rule R18)
+void rotation_from_cov(int D, std::vector<double> cov, std::vector<double>& R, std::vector<double>& lam) {
+  std::vector<double> ev(D), V((size_t)D * D);
+  for (int a = 0; a < D; ++a)
+    for (int b = a + 1; b < D; ++b) cov[(size_t)b * D + a] = cov[(size_t)a * D + b];
+  sym_eig(D, cov.data(), ev.data(), V.data());
+  std::vector<int> order(D);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ev[a] > ev[b]; });
+  R.assign((size_t)D * D, 0.0);
+  lam.assign(D, 0.0);
+  for (int i = 0; i < D; ++i) {
+    const double* col = &V[(size_t)order[i] * D];
+    int jm = 0;
+    for (int j = 1; j < D; ++j)
+      if (std::fabs(col[j]) > std::fabs(col[jm])) jm = j;
+    const double sg = col[jm] < 0 ? -1.0 : 1.0;
+    for (int j = 0; j < D; ++j) R[(size_t)i * D + j] = sg * col[j];
+    lam[i] = ev[order[i]];
+  }
 }
 
 int64_t sample_count(int64_t n_total, int64_t sample_size) {
@@ -424,9 +490,10 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   DADE_REQUIRE(nprobe >= 1 && nprobe <= x->nlist, DADE_ERR_ARG, "nprobe not in [1, nlist]");
   DADE_REQUIRE(delta_d >= 16 && delta_d % 16 == 0 && D % delta_d == 0, DADE_ERR_ARG,
                "delta_d must be a positive multiple of 16 dividing D");
-  DADE_REQUIRE(method == DADE_METHOD_BSA_P || method == DADE_METHOD_ADSAMPLING || method == DADE_METHOD_BSA_RES,
-               DADE_ERR_ARG, "unknown method");
-  if (method == DADE_METHOD_BSA_P)
+  DADE_REQUIRE(method == DADE_METHOD_BSA_P || method == DADE_METHOD_ADSAMPLING || method == DADE_METHOD_BSA_RES ||
+               method == DADE_METHOD_BSA_Q, DADE_ERR_ARG, "unknown method");
+  const bool pqm = method == DADE_METHOD_BSA_Q;
+  if (method == DADE_METHOD_BSA_P || pqm)
     DADE_REQUIRE(alpha >= 0.0 && alpha < 1.0, DADE_ERR_ARG, "significance not in [0,1)");
   else
     DADE_REQUIRE(alpha > 0.0 && std::isfinite(alpha), DADE_ERR_ARG, "eps0 / m must be positive");
@@ -435,7 +502,14 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   const int nsteps = D / delta_d;
   DADE_REQUIRE(nsteps <= DADE_MAX_STEPS, DADE_ERR_UNSUPPORTED, "D/delta_d > DADE_MAX_STEPS");
   const int dd = delta_d / 16;
-  const bool prune = alpha > 0.0 && nsteps > 1;
+  const bool prune = alpha > 0.0 && (pqm || nsteps > 1);
+  if (pqm) {
+    DADE_REQUIRE(x->has_pq && x->pq_codes_ok, DADE_ERR_STATE, "BSA-q needs PQ codebooks (dade_train_pq / dade_set_pq)");
+    if (prune) {
+      DADE_REQUIRE(x->has_calq, DADE_ERR_STATE, "BSA-q with significance > 0 requires dade_calibrate_pq");
+      DADE_REQUIRE(x->calqK == K, DADE_ERR_STATE, "K differs from the PQ-calibrated K");
+    }
+  }
   if (prune && method == DADE_METHOD_BSA_P) {
     DADE_REQUIRE(x->has_cal, DADE_ERR_STATE, "significance > 0 requires calibration");
     DADE_REQUIRE(x->calK == K, DADE_ERR_STATE, "K differs from the calibrated K");
@@ -475,6 +549,33 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   // alpha = 0 (or a single step): nothing can be pruned; the kernel then runs with 16-dim
   // steps (no classifier fires: m1 = 1, beta' = -inf), which serves every delta_d | D.
   p.dd = prune ? dd : 1; p.nsteps = prune ? nsteps : D / 16; p.c0 = DADE_C0_MULT * K; p.prune = prune ? 1 : 0;
+  if (pqm) {
+    // BSA-q: one classifier on the ADC distance in stage 1 (R29), then exact distances — no
+    // classifier in the gather rounds (spacing = all blocks, one step)
+    p.dd = D / 16;
+    p.nsteps = 1;
+    p.pq = 1;
+    p.pq_codes = x->pq_codes.p;
+    p.pq_stride = x->pq_stride;
+    p.pq_eo = x->pq_eo;
+    p.pq_m = x->pq_m;
+    p.pq_ds = D / x->pq_m;
+    p.pq_C = x->pq_Cd.p;
+    p.pq_m1 = (float)x->mq[0];
+    p.pq_m2 = (float)x->mq[1];
+    if (prune) {  // beta' = v[k-1], k = clamp(ceil((1 - alpha) n0), 1, n0): one classifier, alpha_s = alpha
+      long k = (long)std::ceil((1.0 - alpha) * (double)x->n0q);
+      k = std::min<long>(std::max<long>(k, 1), x->n0q);
+      p.pq_beta = (float)x->vq[(size_t)(k - 1)];
+    } else {
+      p.pq_beta = -INFINITY;
+    }
+    // gather rounds: enough lanes per survivor to load all of its blocks in one round trip
+    const int la = x->pq_stride <= 64 ? 1 : 2;
+    int lanes = 1;
+    while (lanes < 32 && lanes * la < D / 16) lanes *= 2;
+    p.pq_lg = __builtin_ctz(lanes);
+  }
   p.avg_stream = (int64_t)nprobe * x->n / std::max(1, x->nlist);
   for (int s = 1; s < p.nsteps; ++s) {
     if (prune && method == DADE_METHOD_ADSAMPLING) {  // m1_d = (D/d)/(1 + eps0/sqrt(d))^2, beta = 0
@@ -578,7 +679,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     stats->dims_scanned = dims;
     stats->n_epochs = (int32_t)c[3];
     for (int s = 0; s < DADE_MAX_STEPS; ++s) stats->pruned_at_step[s] = (int64_t)c[4 + s];
-    stats->n_steps = nsteps;
+    stats->n_steps = pqm ? 1 : nsteps;
     cudaEventElapsedTime(&stats->ms_rotate, x->ev[0], x->ev[1]);  // concurrent with the probe
     cudaEventElapsedTime(&stats->ms_probe, x->ev[0], x->ev[2]);
     cudaEventElapsedTime(&stats->ms_scan, x->ev[2], x->ev[3]);
@@ -703,7 +804,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
       cudaStreamDestroy(s2);
     }
   for (auto e : x->hev) cudaEventDestroy(e);
-  x->gids.release(); x->gdists.release(); x->red.release();
+  x->gids.release(); x->gdists.release(); x->red.release(); x->pq_Cd.release(); x->pq_codes.release();
   comm_destroy(x->comm);
   delete x;
   API_END
@@ -963,6 +1064,7 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
   x->has_ivf = true;
   x->xnorm_ok = false;
   x->has_cal = false;
+  pq_encode_layout(x);  // BSA-q: codes of the new layout (if codebooks are installed)
   API_END
 }
 
@@ -1723,6 +1825,7 @@ extern "C" dade_status dade_set_ivf(dade_index* x, const float* Xrot, int64_t n,
   x->nlist = nlist; x->n = n; x->id_base = id_base;
   tc_prepare(x, x->cent.p, nlist, x->cent_tc, true);
   x->has_ivf = true; x->has_cal = false; x->xnorm_ok = false;
+  pq_encode_layout(x);
   API_END
 }
 
@@ -1931,5 +2034,251 @@ extern "C" dade_status dade_calibration_pairs(int S, int nq, int K, int n_neg, c
   need(pair_q, "pair_q"); need(pair_id, "pair_id"); need(tau, "tau"); need(y, "y");
   DADE_REQUIRE(S >= 1 && nq >= 0 && K >= 1 && n_neg >= 1, DADE_ERR_ARG, "bad S / nq / K / n_neg");
   *npairs = calibration_pairs(S, nq, K, n_neg, knn_ids, knn_dists, keys, neg_ids, counts, pair_q, pair_id, tau, y);
+  API_END
+}
+
+// ================================================================== NEXT-3 BSA-q (§V-B)
+// OPQ on a strided sample of min(n, n_train) rows (R28): PCA-initialised,
+// `iters` rounds of {per-subspace k-means (km_iters Lloyd iterations, warm-started), orthogonal
+// Procrustes R = V U^T of M = sum (x - mu) y^T = U S V^T (computed as (M^T M)^(-1/2) M^T)}, then
+// final_iters Lloyd iterations on the final rotation. Installs (mu, R) as the index rotation
+// (discarding a built IVF) and the codebooks.
+extern "C" dade_status dade_train_pq(dade_index* x, const float* X, int64_t n, int m, int64_t n_train, int iters,
+                                     int km_iters, int final_iters) {
+  API_BEGIN
+  need(x, "index"); need(X, "X");
+  const int D = x->D;
+  DADE_REQUIRE(m >= 1 && D % m == 0 && D / m <= 32, DADE_ERR_ARG, "m must divide D with D/m <= 32");
+  DADE_REQUIRE(iters >= 0 && km_iters >= 0 && final_iters >= 0, DADE_ERR_ARG, "negative iteration count");
+  const int64_t ns = std::min<int64_t>(n, n_train > 0 ? n_train : 65536);
+  DADE_REQUIRE(ns >= 256, DADE_ERR_ARG, "OPQ needs at least 256 training rows");
+  DeviceGuard g(x->device);
+  cudaStream_t st = x->stream;
+  check_finite(x, X, n * D, "X");
+  const int ds = D / m;
+  // the strided sample (row-major ns x D)
+  std::vector<int32_t> sid(ns);
+  for (int64_t k = 0; k < ns; ++k) sid[k] = (int32_t)(((__int128)k * n) / ns);
+  DBuf<int32_t> sid_d;
+  DBuf<float> Xs, Z, Cd;
+  DBuf<double> mu_d, R_d, M_d;
+  DBuf<uint8_t> codes;
+  sid_d.reserve(ns); Xs.reserve((size_t)ns * D); Z.reserve((size_t)ns * D); Cd.reserve((size_t)D * 256);
+  mu_d.reserve(D); R_d.reserve((size_t)D * D); M_d.reserve((size_t)D * D); codes.reserve((size_t)ns * m);
+  DADE_CK(cudaMemcpyAsync(sid_d.p, sid.data(), 4 * ns, cudaMemcpyHostToDevice, st));
+  launch_gather_rows(X, sid_d.p, ns, D, Xs.p, st);
+  // PCA of the sample (its mean centres everything)
+  std::vector<double> sum(D), cov((size_t)D * D), mean(D), R, lam;
+  int64_t cnt = 0;
+  dade_status s = dade_pca_mean_partial(x, Xs.p, ns, 0, ns, ns, sum.data(), &cnt);
+  if (s != DADE_OK) throw Error(s, g_err);
+  for (int j = 0; j < D; ++j) mean[j] = sum[j] / (double)cnt;
+  s = dade_pca_cov_partial(x, Xs.p, ns, 0, ns, ns, mean.data(), cov.data());
+  if (s != DADE_OK) throw Error(s, g_err);
+  for (auto& c : cov) c /= (double)cnt;
+  rotation_from_cov(D, cov, R, lam);
+  DADE_CK(cudaMemcpyAsync(mu_d.p, mean.data(), 8 * D, cudaMemcpyHostToDevice, st));
+  std::vector<float> C((size_t)D * 256), Zh((size_t)ns * D);
+  std::vector<uint8_t> ch((size_t)ns * m);
+  bool have_C = false;
+  auto rotate_sample = [&]() {
+    DADE_CK(cudaMemcpyAsync(R_d.p, R.data(), 8 * R.size(), cudaMemcpyHostToDevice, st));
+    launch_rotate(Xs.p, nullptr, ns, D, R_d.p, mu_d.p, Z.p, nullptr, st);
+    DADE_CK(cudaMemcpyAsync(Zh.data(), Z.p, 4 * Zh.size(), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    if (!have_C) {  // init: the first 256 sampled rows' sub-vectors (R28)
+      for (int j = 0; j < m; ++j)
+        for (int c = 0; c < 256; ++c)
+          for (int i = 0; i < ds; ++i) C[((size_t)j * 256 + c) * ds + i] = Zh[(size_t)c * D + j * ds + i];
+      have_C = true;
+    }
+  };
+  auto assign_all = [&]() {
+    DADE_CK(cudaMemcpyAsync(Cd.p, C.data(), 4 * C.size(), cudaMemcpyHostToDevice, st));
+    launch_pq_assign(Z.p, false, ns, D, m, Cd.p, codes.p, m, st);
+    DADE_CK(cudaMemcpyAsync(ch.data(), codes.p, ch.size(), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+  };
+  std::vector<double> sums((size_t)D * 256);
+  std::vector<int64_t> cnts((size_t)m * 256);
+  auto lloyd = [&](int its) {  // centroid = fp64 mean (sample order) rounded to fp32; empty keeps
+    for (int it = 0; it < its; ++it) {
+      assign_all();
+      std::fill(sums.begin(), sums.end(), 0.0);
+      std::fill(cnts.begin(), cnts.end(), (int64_t)0);
+      for (int64_t r = 0; r < ns; ++r)
+        for (int j = 0; j < m; ++j) {
+          const int c = ch[(size_t)r * m + j];
+          ++cnts[(size_t)j * 256 + c];
+          double* sr = &sums[((size_t)j * 256 + c) * ds];
+          const float* zr = &Zh[(size_t)r * D + j * ds];
+          for (int i = 0; i < ds; ++i) sr[i] += (double)zr[i];
+        }
+      for (int j = 0; j < m; ++j)
+        for (int c = 0; c < 256; ++c) {
+          const int64_t k = cnts[(size_t)j * 256 + c];
+          if (k > 0)
+            for (int i = 0; i < ds; ++i)
+              C[((size_t)j * 256 + c) * ds + i] = (float)(sums[((size_t)j * 256 + c) * ds + i] / (double)k);
+        }
+    }
+  };
+  std::vector<double> M((size_t)D * D), MtM((size_t)D * D), ev(D), V((size_t)D * D), T((size_t)D * D);
+  for (int t = 0; t < iters; ++t) {
+    rotate_sample();
+    lloyd(km_iters);
+    assign_all();  // codes of the updated codebooks -> reconstructions y
+    DADE_CK(cudaMemcpyAsync(Cd.p, C.data(), 4 * C.size(), cudaMemcpyHostToDevice, st));
+    launch_pq_cross(Xs.p, mu_d.p, ns, D, m, Cd.p, codes.p, M_d.p, st);
+    DADE_CK(cudaMemcpyAsync(M.data(), M_d.p, 8 * M.size(), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    // R = V S^-1 V^T M^T with M^T M = V S^2 V^T (the polar factor: R = V U^T for M = U S V^T)
+    for (int a = 0; a < D; ++a)
+      for (int b = a; b < D; ++b) {
+        double acc = 0;
+        for (int k = 0; k < D; ++k) acc += M[(size_t)k * D + a] * M[(size_t)k * D + b];
+        MtM[(size_t)a * D + b] = MtM[(size_t)b * D + a] = acc;
+      }
+    sym_eig(D, MtM.data(), ev.data(), V.data());  // V column-major: V[k * D + a] = V_a,k
+    for (int k = 0; k < D; ++k) {
+      DADE_REQUIRE(ev[k] > 0, DADE_ERR_ARG, "OPQ: singular cross-product (degenerate training data)");
+      const double inv = 1.0 / std::sqrt(ev[k]);
+      for (int b = 0; b < D; ++b) {  // T[k][b] = (V^T M^T)[k][b] / s_k = sum_c V_c,k M[b][c] / s_k
+        double acc = 0;
+        for (int c = 0; c < D; ++c) acc += V[(size_t)k * D + c] * M[(size_t)b * D + c];
+        T[(size_t)k * D + b] = acc * inv;
+      }
+    }
+    for (int a = 0; a < D; ++a)
+      for (int b = 0; b < D; ++b) {
+        double acc = 0;
+        for (int k = 0; k < D; ++k) acc += V[(size_t)k * D + a] * T[(size_t)k * D + b];
+        R[(size_t)a * D + b] = acc;
+      }
+  }
+  rotate_sample();
+  lloyd(final_iters);
+  // install: the OPQ rotation becomes the index rotation (invalidates a built IVF), then codebooks
+  x->mean = mean;
+  x->R = R;
+  x->lam.assign(D, 0.0);
+  x->has_lam = false;
+  upload_rotation(x);
+  install_pq(x, m, C.data());
+  API_END
+}
+
+extern "C" dade_status dade_set_pq(dade_index* x, int m, const float* codebooks) {
+  API_BEGIN
+  need(x, "index"); need(codebooks, "codebooks");
+  DADE_REQUIRE(x->has_rot, DADE_ERR_STATE, "set_pq needs the rotation the codebooks live in");
+  DeviceGuard g(x->device);
+  install_pq(x, m, codebooks);
+  API_END
+}
+
+extern "C" dade_status dade_get_pq(const dade_index* x, int* m, float* codebooks, uint8_t* codes, float* err) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_pq, DADE_ERR_STATE, "no PQ codebooks");
+  if (m) *m = x->pq_m;
+  if (codebooks) memcpy(codebooks, x->pq_C.data(), sizeof(float) * x->pq_C.size());
+  if (codes || err) {
+    DADE_REQUIRE(x->pq_codes_ok, DADE_ERR_STATE, "no PQ codes (build the IVF)");
+    DeviceGuard g(x->device);
+    std::vector<uint8_t> rows((size_t)x->n * x->pq_stride);
+    DADE_CK(cudaMemcpyAsync(rows.data(), x->pq_codes.p, rows.size(), cudaMemcpyDeviceToHost, x->stream));
+    DADE_CK(cudaStreamSynchronize(x->stream));
+    for (int64_t p = 0; p < x->n; ++p) {
+      const uint8_t* r = &rows[(size_t)p * x->pq_stride];
+      if (codes) memcpy(codes + (size_t)p * x->pq_m, r, x->pq_m);
+      if (err) memcpy(err + p, r + x->pq_eo, 4);
+    }
+  }
+  API_END
+}
+
+// §V-A correction on the ADC distance (BSA-q; R29): the calibration pairs of
+// dade_calibrate (R14-R16), features (ADC dis', reconstruction error e) in fp64 from the stored
+// codes and the GPU-rotated queries, the two-feature logistic fit, v = sort_desc(tau - m1 dis' - m2 e)
+// over the Label-0 pairs
+extern "C" dade_status dade_calibrate_pq(dade_index* x, const float* X, const float* Qc, int nq, int K, int n_neg,
+                                         int nprobe_neg, uint64_t seed) {
+  API_BEGIN
+  need(x, "index"); need(X, "X"); need(Qc, "Qc");
+  DeviceGuard g(x->device);
+  calib_checks(x, Qc, nq, K, n_neg, nprobe_neg);
+  DADE_REQUIRE(x->has_pq && x->pq_codes_ok, DADE_ERR_STATE, "calibrate_pq needs PQ codes");
+  DADE_REQUIRE(K <= x->n, DADE_ERR_ARG, "K not in [1, n]");
+  const int D = x->D;
+  cudaStream_t st = x->stream;
+  std::vector<int64_t> ki;
+  std::vector<double> kd;
+  calib_knn(x, X, Qc, nq, K, ki, kd);
+  std::vector<std::vector<std::pair<uint64_t, int64_t>>> neg;
+  calib_negatives(x, Qc, nq, K, ki.data(), n_neg, nprobe_neg, seed, neg);
+  std::vector<int32_t> pq, prow;
+  std::vector<double> ptau, py;
+  for (int qi = 0; qi < nq; ++qi) {
+    const double tau = kd[(size_t)qi * K + K - 1];
+    for (int j = 0; j < K; ++j) {
+      pq.push_back(qi); prow.push_back(x->pos_of_h[ki[(size_t)qi * K + j] - x->id_base]);
+      ptau.push_back(tau); py.push_back(0.0);
+    }
+    for (const auto& c : neg[qi]) {
+      pq.push_back(qi); prow.push_back(x->pos_of_h[c.second - x->id_base]); ptau.push_back(tau); py.push_back(1.0);
+    }
+  }
+  const int np = (int)pq.size();
+  DBuf<float> qr;
+  DBuf<int32_t> pq_d, pr_d;
+  DBuf<double> feat;
+  qr.reserve((size_t)nq * D); pq_d.reserve(np); pr_d.reserve(np); feat.reserve((size_t)2 * np);
+  launch_rotate(Qc, nullptr, nq, D, x->R_d.p, x->mean_d.p, qr.p, nullptr, st);
+  DADE_CK(cudaMemcpyAsync(pq_d.p, pq.data(), 4 * np, cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(pr_d.p, prow.data(), 4 * np, cudaMemcpyHostToDevice, st));
+  launch_pq_pair_feat(x->pq_codes.p, x->pq_stride, x->pq_eo, x->pq_m, D, x->pq_Cd.p, qr.p, pq_d.p, pr_d.p, np,
+                      feat.p, st);
+  std::vector<double> F((size_t)2 * np);
+  DADE_CK(cudaMemcpyAsync(F.data(), feat.p, 8 * F.size(), cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaStreamSynchronize(st));
+  std::vector<double> mv;
+  double beta;
+  logistic_irls_multi(F, 2, ptau, py, 1e-8, 100, 1e-12, mv, &beta);
+  std::vector<double> v;
+  for (int i = 0; i < np; ++i)
+    if (py[i] == 0.0) v.push_back(ptau[i] - mv[0] * F[2 * (size_t)i] - mv[1] * F[2 * (size_t)i + 1]);
+  std::sort(v.begin(), v.end(), std::greater<double>());
+  x->mq[0] = mv[0];
+  x->mq[1] = mv[1];
+  x->vq = std::move(v);
+  x->n0q = (int)x->vq.size();
+  x->calqK = K;
+  x->has_calq = true;
+  API_END
+}
+
+extern "C" dade_status dade_get_calibration_q(const dade_index* x, int* K, int* n0, double* m2, double* v) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_calq, DADE_ERR_STATE, "no PQ calibration");
+  if (K) *K = x->calqK;
+  if (n0) *n0 = x->n0q;
+  if (m2) { m2[0] = x->mq[0]; m2[1] = x->mq[1]; }
+  if (v) memcpy(v, x->vq.data(), sizeof(double) * x->vq.size());
+  API_END
+}
+
+extern "C" dade_status dade_set_calibration_q(dade_index* x, int K, int n0, const double* m2, const double* v) {
+  API_BEGIN
+  need(x, "index"); need(m2, "m"); need(v, "v");
+  DADE_REQUIRE(K >= 1 && K <= DADE_MAX_K && n0 >= 1, DADE_ERR_ARG, "bad K / n0");
+  DADE_REQUIRE(x->has_pq, DADE_ERR_STATE, "set_calibration_q needs PQ codebooks");
+  x->mq[0] = m2[0];
+  x->mq[1] = m2[1];
+  x->vq.assign(v, v + n0);
+  x->n0q = n0;
+  x->calqK = K;
+  x->has_calq = true;
   API_END
 }

@@ -152,6 +152,15 @@ struct ScanParams {
   const int32_t* order; // nq: processing order of the queries (null = 0..nq-1); results stay at q
   int g_force;          // warps per query (0 = the scan_group heuristic)
   unsigned dd_magic;    // ceil(2^32 / dd), set by launch_scan
+  // BSA-q (NEXT-3): stage 1 reads the candidates' PQ code rows (codes | fp32
+  // reconstruction error, pq_stride bytes per list-major row) and prunes iff
+  // pq_m1 * ADC + pq_m2 * err + pq_beta > tau; survivors get the exact distance over all blocks
+  int pq;
+  const uint8_t* pq_codes;
+  int pq_stride, pq_eo, pq_m, pq_ds;
+  const float* pq_C;       // m x 256 x ds codebooks
+  float pq_m1, pq_m2, pq_beta;
+  int pq_lg;               // log2 lanes per survivor in the exact-distance gather rounds
   // decision log (parity runs; null = off): per tested candidate (query, global id, dims read)
   int32_t* dlog;
   int64_t dlog_cap;              // records
@@ -200,12 +209,25 @@ int64_t calibration_pairs(int S, int nq, int K, int n_neg, const int64_t* knn_id
                           const uint64_t* keys, const int64_t* nids, const int32_t* cnt, int32_t* pq,
                           int64_t* pid, double* tau, double* y);
 
+// pq.cu (NEXT-3 BSA-q)
+void launch_pq_assign(const float* X, bool blocked, int64_t n, int D, int m, const float* C, uint8_t* codes,
+                      int stride, cudaStream_t st);
+void launch_pq_err(const float* layout, int64_t n, int D, int m, const float* C, uint8_t* codes, int stride, int eo,
+                   cudaStream_t st);
+void launch_pq_pair_feat(const uint8_t* codes, int stride, int eo, int m, int D, const float* C, const float* qrot,
+                         const int32_t* pq, const int32_t* pr, int npairs, double* out, cudaStream_t st);
+void launch_pq_cross(const float* X, const double* mu, int64_t n, int D, int m, const float* C, const uint8_t* codes,
+                     double* M, cudaStream_t st);
+
 // host_eig.cpp : symmetric eigendecomposition (Householder tridiagonalisation + implicit QL)
 void sym_eig(int n, const double* A, double* eigval, double* eigvec_colmajor);
 // host_calib.cpp
 bool logistic_irls(const std::vector<double>& P, const std::vector<double>& tau,
                    const std::vector<double>& y, double ridge, int max_iter, double tol,
                    double* m1, double* beta);
+bool logistic_irls_multi(const std::vector<double>& F, int k, const std::vector<double>& tau,
+                         const std::vector<double>& y, double ridge, int max_iter, double tol,
+                         std::vector<double>& m_out, double* beta_out);
 uint64_t splitmix64(uint64_t x);
 
 }  // namespace dade

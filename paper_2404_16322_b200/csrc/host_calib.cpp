@@ -111,4 +111,116 @@ bool logistic_irls(const std::vector<double>& P, const std::vector<double>& tau,
   return true;
 }
 
+// Several features (BSA-q: the ADC distance and the distance to the quantized
+// centroid) — the same damped Newton / IRLS on standardised features (R3), k features + tau.
+// F: n x k row-major. Returns the model m . f + beta > tau (m_i = -w_i / w_tau); flag (R29):
+// w_tau >= 0, a non-finite weight or m_0 <= 0 -> m = e_0, beta = 0, false.
+static bool solve_n(std::vector<double>& M, int n, std::vector<double>& x) {  // M: n x (n+1)
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(M[(size_t)r * (n + 1) + c]) > std::fabs(M[(size_t)piv * (n + 1) + c])) piv = r;
+    if (M[(size_t)piv * (n + 1) + c] == 0.0) return false;
+    if (piv != c)
+      for (int j = 0; j <= n; ++j) std::swap(M[(size_t)c * (n + 1) + j], M[(size_t)piv * (n + 1) + j]);
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const double f = M[(size_t)r * (n + 1) + c] / M[(size_t)c * (n + 1) + c];
+      for (int j = c; j <= n; ++j) M[(size_t)r * (n + 1) + j] -= f * M[(size_t)c * (n + 1) + j];
+    }
+  }
+  x.resize(n);
+  for (int i = 0; i < n; ++i) x[i] = M[(size_t)i * (n + 1) + n] / M[(size_t)i * (n + 1) + i];
+  return true;
+}
+
+bool logistic_irls_multi(const std::vector<double>& F, int k, const std::vector<double>& tau,
+                         const std::vector<double>& y, double ridge, int max_iter, double tol,
+                         std::vector<double>& m_out, double* beta_out) {
+  const size_t n = tau.size();
+  const int nw = k + 2;  // intercept, k features, tau
+  std::vector<double> mean(k + 1, 0.0), sd(k + 1, 0.0);
+  for (size_t i = 0; i < n; ++i) {
+    for (int j = 0; j < k; ++j) mean[j] += F[i * k + j];
+    mean[k] += tau[i];
+  }
+  for (auto& v : mean) v /= (double)n;
+  for (size_t i = 0; i < n; ++i) {
+    for (int j = 0; j < k; ++j) sd[j] += (F[i * k + j] - mean[j]) * (F[i * k + j] - mean[j]);
+    sd[k] += (tau[i] - mean[k]) * (tau[i] - mean[k]);
+  }
+  for (auto& v : sd) { v = std::sqrt(v / (double)n); if (!(v > 0)) v = 1.0; }
+  std::vector<double> A(n * nw);
+  for (size_t i = 0; i < n; ++i) {
+    A[i * nw] = 1.0;
+    for (int j = 0; j < k; ++j) A[i * nw + 1 + j] = (F[i * k + j] - mean[j]) / sd[j];
+    A[i * nw + 1 + k] = (tau[i] - mean[k]) / sd[k];
+  }
+  std::vector<double> reg(nw, ridge);
+  reg[0] = 0.0;
+  auto loss = [&](const std::vector<double>& w) {
+    double L = 0;
+    for (size_t i = 0; i < n; ++i) {
+      double z = 0;
+      for (int j = 0; j < nw; ++j) z += A[i * nw + j] * w[j];
+      L += log1pexp(z) - y[i] * z;
+    }
+    for (int j = 0; j < nw; ++j) L += 0.5 * reg[j] * w[j] * w[j];
+    return L;
+  };
+  std::vector<double> w(nw, 0.0), nwv(nw), step;
+  double cur = loss(w);
+  std::vector<double> M((size_t)nw * (nw + 1));
+  for (int it = 0; it < max_iter; ++it) {
+    std::fill(M.begin(), M.end(), 0.0);
+    for (size_t i = 0; i < n; ++i) {
+      double z = 0;
+      for (int j = 0; j < nw; ++j) z += A[i * nw + j] * w[j];
+      const double p = 0.5 * (1.0 + std::tanh(0.5 * z));
+      const double r = y[i] - p, ww = p * (1.0 - p);
+      for (int a = 0; a < nw; ++a) {
+        M[(size_t)a * (nw + 1) + nw] += A[i * nw + a] * r;
+        for (int b = 0; b < nw; ++b) M[(size_t)a * (nw + 1) + b] += A[i * nw + a] * A[i * nw + b] * ww;
+      }
+    }
+    for (int j = 0; j < nw; ++j) {
+      M[(size_t)j * (nw + 1) + nw] -= reg[j] * w[j];
+      M[(size_t)j * (nw + 1) + j] += reg[j];
+    }
+    if (!solve_n(M, nw, step)) break;
+    double t = 1.0, nl = cur;
+    for (int h = 0; h < 30; ++h) {
+      for (int j = 0; j < nw; ++j) nwv[j] = w[j] + t * step[j];
+      nl = loss(nwv);
+      if (nl <= cur) break;
+      t *= 0.5;
+    }
+    double mx = 0;
+    for (int j = 0; j < nw; ++j) { w[j] = nwv[j]; mx = std::fmax(mx, std::fabs(t * step[j])); }
+    cur = nl;
+    if (mx < tol) break;
+  }
+  const double wt = w[1 + k] / sd[k];
+  double b = w[0] - w[1 + k] * mean[k] / sd[k];
+  std::vector<double> wf(k);
+  bool finite = std::isfinite(wt);
+  for (int j = 0; j < k; ++j) {
+    wf[j] = w[1 + j] / sd[j];
+    b -= w[1 + j] * mean[j] / sd[j];
+    finite = finite && std::isfinite(wf[j]);
+  }
+  m_out.assign(k, 0.0);
+  m_out[0] = 1.0;
+  *beta_out = 0.0;
+  if (!(wt < 0) || !finite) return false;
+  std::vector<double> mv(k);
+  for (int j = 0; j < k; ++j) mv[j] = -wf[j] / wt;
+  if (!(mv[0] > 0)) return false;
+  for (double v : mv)
+    if (!std::isfinite(v)) return false;
+  m_out = mv;
+  *beta_out = -b / wt;
+  return true;
+}
+
 }  // namespace dade

@@ -301,7 +301,7 @@ __device__ __forceinline__ int step_of(int blk, int dd, unsigned magic) {
 // frozen tau (R13), so the split cannot change a decision; at each epoch end the warps' local
 // top-K lists are merged exactly (rank by binary search, smem) into the query's top-K.
 // CTA shared memory: G slices | pruned[64] | lists[nprobe] | qs[D] | qi | (G > 1) W[G][K] + Gk[2][K].
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG>
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG, bool PQ>
 __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   using SL = Slice<DD>;
@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
   float* qcs = qs + ((D + 3) & ~3);                       // residual: per-step query constants
-  int* qslot = reinterpret_cast<int*>(qcs + (RES ? DADE_MAX_STEPS : 0));
+  float* lut = qcs + (RES ? DADE_MAX_STEPS : 0);                // PQ: m x 256 ADC table of the query
+  int* qslot = reinterpret_cast<int*>(lut + (PQ ? p.pq_m * 256 : 0));
   unsigned long long* W = reinterpret_cast<unsigned long long*>(qslot + 4);  // G x K (G > 1)
   unsigned long long* Gk = W + (size_t)G * K;                               // 2 x K (G > 1)
 
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   const int sdd = p.dd;                 // classifier spacing in blocks (a multiple of DD)
   const unsigned smagic = p.dd_magic;
   const bool test1 = sdd == DD && nsteps > 1;  // stage 1 ends on a classifier step
+  const int kRoundQ = PQ ? (32 >> p.pq_lg) : 32;  // queued survivors that make a full gather round
   const float* lay = p.layout;
   const int64_t n = p.n;
   unsigned long long c_tested = 0, c_surv = 0;  // warp-uniform
@@ -370,6 +372,20 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     if (MULTI)
       for (int j = threadIdx.x; j < K; j += blockDim.x) Gk[j] = kKeyInf;
     __syncthreads();
+    if (PQ) {  // ADC look-up table: lut[j][c] = ||q~_j - C_j[c]||^2, fp32, dims in order
+      const int ds = p.pq_ds;
+      for (int idx = threadIdx.x; idx < p.pq_m * 256; idx += blockDim.x) {
+        const int j = idx >> 8;
+        const float* c = p.pq_C + (int64_t)idx * ds;
+        float acc = 0.f;
+        for (int t = 0; t < ds; ++t) {
+          const float d = qs[j * ds + t] - __ldg(c + t);
+          acc = fmaf(d, d, acc);
+        }
+        lut[idx] = acc;
+      }
+      __syncthreads();
+    }
     int L = 0;
     for (int j = lane; j < p.nprobe; j += 32) L += lists[j].y;
 #pragma unroll
@@ -405,11 +421,17 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       }
       if (lane == 0) {
         meta[slot] = TileMeta{row0, nr, pep, 0};
-        const uint32_t bytes = (uint32_t)nr * 64u;
-        mbar_expect_tx(&mbar[slot], bytes * DD);
+        if (PQ) {  // the tile's code rows: one contiguous range of list-major rows
+          const uint32_t bytes = (uint32_t)nr * (uint32_t)p.pq_stride;
+          mbar_expect_tx(&mbar[slot], bytes);
+          bulk_g2s(tiles + slot * TB, p.pq_codes + (int64_t)row0 * p.pq_stride, bytes, &mbar[slot]);
+        } else {
+          const uint32_t bytes = (uint32_t)nr * 64u;
+          mbar_expect_tx(&mbar[slot], bytes * DD);
 #pragma unroll
-        for (int bb = 0; bb < DD; ++bb)
-          bulk_g2s(tiles + slot * TB + bb * TR * 64, lay + (((int64_t)bb * n + row0) << 4), bytes, &mbar[slot]);
+          for (int bb = 0; bb < DD; ++bb)
+            bulk_g2s(tiles + slot * TB + bb * TR * 64, lay + (((int64_t)bb * n + row0) << 4), bytes, &mbar[slot]);
+        }
       }
       ++issued;
       return true;
@@ -435,14 +457,15 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     // blocks, so one round trip advances it by up to 32/qn*LA blocks; the group's block sums are then accumulated in block order by every
     // lane of the group (shuffles), so phi is bit-identical to the one-lane path.
     auto queue_round = [&](bool drain) {
-      const int qn = min(tail - head, 32);
-      // log2 lanes per survivor: a draining round spreads its survivors over all 32 lanes
-      const int lg = !drain ? 0 : drain_lanes_log2(qn);
+      const int qn = min(tail - head, kRoundQ);
+      // log2 lanes per survivor: a draining round spreads its survivors over all 32 lanes (PQ:
+      // every round — a survivor of the ADC test needs all of its blocks)
+      const int lg = !(drain || PQ) ? 0 : drain_lanes_log2(qn);
       const int ei = lane >> lg, sub = lane & ((1 << lg) - 1);
       const bool val = ei < qn;
       QEntry e = val ? ring[(head + ei) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0.f};
       // full rounds: one step (DD blocks, LA >= DD) or LA blocks; draining rounds: LA per lane
-      int wtot = drain ? (LA << lg) : (DD < LA ? DD : LA);
+      int wtot = (drain || PQ) ? (LA << lg) : (DD < LA ? DD : LA);
       wtot = min(wtot, nblk - e.blk);
       const int b0 = e.blk + sub * LA;  // this lane's first block
       const int want = max(0, min(LA, e.blk + wtot - b0));
@@ -542,7 +565,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     TileMeta tm{0, 0, 0, 0};
     for (;;) {
       const int qlen = tail - head;
-      bool round = qlen >= 32, drain = false, ep_end = false;
+      bool round = qlen >= kRoundQ, drain = false, ep_end = false;
       if (!round) {
         if (!ready && consumed < issued) {
           const int slot = consumed % kStages;
@@ -573,9 +596,41 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         PROF_MARK(4);
         continue;
       }
-      // stage 1 (qlen < 32: the ring has room for 32 more): one row per lane, DD blocks
       const int slot = consumed % kStages;
       const bool val = lane < tm.nr;
+      if constexpr (PQ) {
+        // stage 1 of BSA-q: dis' = ADC of the row's code (m table look-ups), the
+        // test m1 * dis' + m2 * err + beta' > tau; survivors are queued at block 0 (phi = 0) and
+        // get the exact distance from the gather rounds
+        const unsigned char* crow = tiles + slot * TB + lane * p.pq_stride;
+        float adc = 0.f, err = 0.f;
+        if (val) {
+          for (int c0 = 0; c0 < p.pq_m; c0 += 16) {
+            const uint4 w = *reinterpret_cast<const uint4*>(crow + c0);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b)
+              if (c0 + b < p.pq_m) adc += lut[((c0 + b) << 8) + ((ws[b >> 2] >> ((b & 3) * 8)) & 255u)];
+          }
+          err = *reinterpret_cast<const float*>(crow + p.pq_eo);
+        }
+        __syncwarp();
+        ++consumed;
+        ready = false;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(slot);
+        if (stats) c_tested += tm.nr;
+        const bool prune = val && fmaf(p.pq_m1, adc, fmaf(p.pq_m2, err, p.pq_beta)) > tau;
+        if (LOG && prune) log_decision(p, q, __ldg(p.row_id + tm.row0 + lane), 0);
+        push(val && !prune, QEntry{tm.row0 + lane, 0.f, 0, 0.f});
+        if (stats) {
+          const int np_ = __popc(__ballot_sync(0xffffffffu, prune));
+          if (lane == 0 && np_) atomicAdd(&pruned[0], (unsigned)np_);
+        }
+        PROF_MARK(5);
+        continue;
+      }
+      // stage 1 (qlen < 32: the ring has room for 32 more): one row per lane, DD blocks
       const unsigned char* trow = tiles + slot * TB + lane * 64;
       float s = 0.f, sq = 0.f;
       const float xn = RES && val ? __ldg(p.xnorm + tm.row0 + lane) : 0.f;
@@ -652,9 +707,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
 }
 
 template <int DD, bool RES>
-static size_t scan_smem(int D, int K, int nprobe, int G) {
+static size_t scan_smem(int D, int K, int nprobe, int G, int pq_m) {
   return (size_t)G * Slice<DD>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
-         (size_t)((D + 3) & ~3) * 4 + (RES ? DADE_MAX_STEPS * 4 : 0) + (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
+         (size_t)((D + 3) & ~3) * 4 + (RES ? DADE_MAX_STEPS * 4 : 0) + (size_t)pq_m * 256 * 4 +
+         (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
 
 // warps per query: the smallest G giving >= 16 query-warps per SM, and G >= 2 for long candidate
@@ -669,10 +725,10 @@ static int scan_group(int nq, int sms, int64_t avg_stream) {
 
 // The attribute and the SM count are set / read on every launch (cheap host calls): they apply
 // per device, and an index may live on any device of the process.
-template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG>
+template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG, bool PQ>
 static void launch_g(const ScanParams& p, cudaStream_t st, int G, int sms) {
-  auto kern = k_scan<DD, KPL, LA, MAXREG, MULTI, RES, LOG>;
-  const size_t smem = scan_smem<DD, RES>(p.D, p.K, p.nprobe, G);
+  auto kern = k_scan<DD, KPL, LA, MAXREG, MULTI, RES, LOG, PQ>;
+  const size_t smem = scan_smem<DD, RES>(p.D, p.K, p.nprobe, G, PQ ? p.pq_m : 0);
   DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
   DADE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
@@ -681,23 +737,28 @@ static void launch_g(const ScanParams& p, cudaStream_t st, int G, int sms) {
   kern<<<p.nq < max_blocks ? p.nq : max_blocks, 32 * G, smem, st>>>(p);
 }
 
-template <int DD, int KPL, int LA, int MAXREG, bool RES = false>
+template <int DD, int KPL, int LA, int MAXREG, bool RES = false, bool PQ = false>
 static void launch_v(const ScanParams& p, cudaStream_t st) {
   int dev = 0, sms = 0;
   DADE_CK(cudaGetDevice(&dev));
   DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (p.dlog) {  // decision log (parity runs): one warp per query; decisions do not depend on G
-    if constexpr (!RES) launch_g<DD, KPL, LA, MAXREG, false, false, true>(p, st, 1, sms);
+    if constexpr (!RES) launch_g<DD, KPL, LA, MAXREG, false, false, true, PQ>(p, st, 1, sms);
     return;
   }
-  const int G = p.g_force > 0 ? p.g_force : scan_group(p.nq, sms, p.avg_stream);
+  // BSA-q: the CTA's ADC table (m x 256 floats) is shared by 8 warps per query
+  const int G = p.g_force > 0 ? p.g_force : PQ ? 8 : scan_group(p.nq, sms, p.avg_stream);
   DADE_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, DADE_ERR_ARG, "scan: warps per query must be 1, 2, 4 or 8");
-  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, RES, false>(p, st, 1, sms);
-  else launch_g<DD, KPL, LA, MAXREG, true, RES, false>(p, st, G, sms);
+  if (G == 1) launch_g<DD, KPL, LA, MAXREG, false, RES, false, PQ>(p, st, 1, sms);
+  else launch_g<DD, KPL, LA, MAXREG, true, RES, false, PQ>(p, st, G, sms);
 }
 
 template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
+  if (p.pq) {  // BSA-q (NEXT-3): ADC test in stage 1, exact distance of the survivors
+    launch_v<DD, KPL, DD >= 2 ? 2 : 1, DD >= 2 ? 128 : 96, false, true>(p, st);
+    return;
+  }
   if (p.residual) {  // BSA-res (NEXT-1): residual-norm test
     DADE_REQUIRE(!p.dlog, DADE_ERR_UNSUPPORTED, "scan: decision log is for BSA-p / ADSampling only");
     launch_v<DD, KPL, 1, 96, true>(p, st);
@@ -739,8 +800,13 @@ void launch_scan(const ScanParams& p, cudaStream_t st) {
   DADE_REQUIRE(p.dd >= 1 && p.dd * 16 <= p.D && p.D % (p.dd * 16) == 0, DADE_ERR_ARG, "scan: bad delta_d");
   ScanParams q = p;
   q.dd_magic = p.dd == 1 ? 0u : (unsigned)((((uint64_t)1 << 32) + (uint64_t)p.dd - 1) / (uint64_t)p.dd);
-  // staging unit: the largest of 4, 2, 1 blocks dividing the classifier spacing
-  switch (p.dd % 4 == 0 ? 4 : p.dd % 2 == 0 ? 2 : 1) {
+  // staging unit: the largest of 4, 2, 1 blocks dividing the classifier spacing; BSA-q: the
+  // smallest tile holding 32 code rows (64 * DD bytes per row)
+  const int unit = p.pq ? (p.pq_stride <= 64 ? 1 : p.pq_stride <= 128 ? 2 : 4)
+                        : (p.dd % 4 == 0 ? 4 : p.dd % 2 == 0 ? 2 : 1);
+  DADE_REQUIRE(!p.pq || (p.pq_stride <= 256 && p.pq_stride % 16 == 0), DADE_ERR_UNSUPPORTED,
+               "scan: PQ code rows wider than 256 bytes");
+  switch (unit) {
     case 4: launch_dd<4>(q, st); break;
     case 2: launch_dd<2>(q, st); break;
     default: launch_dd<1>(q, st); break;

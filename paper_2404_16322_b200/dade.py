@@ -80,6 +80,12 @@ _SIGS = {
     "dade_set_ivf": [P, P, I64, I64, P, P, I32, P],
     "dade_set_option": [P, I32, I64],
     "dade_search_log": [P, P, I32, I32, I32, I32, I32, DBL, P, P, P, I64, P],
+    "dade_train_pq": [P, P, I64, I32, I64, I32, I32, I32],
+    "dade_set_pq": [P, I32, P],
+    "dade_get_pq": [P, P, P, P, P],
+    "dade_calibrate_pq": [P, P, P, I32, I32, I32, I32, C.c_uint64],
+    "dade_get_calibration_q": [P, P, P, P, P],
+    "dade_set_calibration_q": [P, I32, I32, P, P],
     "dade_comm_unique_id": [P],
     "dade_set_comm": [P, P, I32, I32],
     "dade_fit_rotation_dist": [P, P, I64, I64, I64, I64],
@@ -304,7 +310,7 @@ class Index:
                               _ptr(dists), C.byref(st) if st is not None else None))
         return (ids, dists, st.as_dict()) if stats else (ids, dists)
 
-    METHODS = {"bsa_p": 0, "adsampling": 1, "bsa_res": 2}
+    METHODS = {"bsa_p": 0, "adsampling": 1, "bsa_res": 2, "bsa_q": 3}
 
     def search_method(self, Q, K: int, nprobe: int, delta_d: int, method: str, param: float, ids=None,
                       dists=None, stats: bool = False):
@@ -474,6 +480,45 @@ class Index:
         d = torch.empty((nq, K), dtype=torch.float32, device=ids_in.device)
         _ck(lib().dade_merge_topk(self.h, _ptr(ids_in), _ptr(dists_in), S, nq, K, _ptr(ids), _ptr(d)))
         return ids, d
+
+    # -------------------------------------------------- NEXT-3 BSA-q (OPQ + PQ codes + ADC test)
+    def train_pq(self, X, m: int, n_train: int = 0, iters: int = 8, km_iters: int = 4, final_iters: int = 10):
+        """OPQ training (installs the OPQ rotation and the codebooks; build_ivf afterwards)."""
+        import torch
+        X = _dev(X, torch.float32)
+        _ck(lib().dade_train_pq(self.h, _ptr(X), X.shape[0], m, n_train, iters, km_iters, final_iters))
+
+    def set_pq(self, codebooks):
+        C = np.ascontiguousarray(codebooks, np.float32)
+        _ck(lib().dade_set_pq(self.h, C.shape[0], _ptr(C)))
+
+    def get_pq(self, with_codes: bool = True):
+        """(codebooks [m, 256, D/m] fp32, codes [n, m] uint8 list-major, err [n] fp32)."""
+        mm = np.zeros(1, np.int32)
+        _ck(lib().dade_get_pq(self.h, _ptr(mm), None, None, None))
+        m = int(mm[0])
+        C = np.zeros((m, 256, self.D // m), np.float32)
+        n, _ = self.sizes()
+        codes = np.zeros((n, m), np.uint8) if with_codes else None
+        err = np.zeros(n, np.float32) if with_codes else None
+        _ck(lib().dade_get_pq(self.h, None, _ptr(C), _ptr(codes), _ptr(err)))
+        return C, codes, err
+
+    def calibrate_pq(self, X, Qc, K: int, n_neg: int = 50, nprobe_neg: int = 0, seed: int = 0):
+        import torch
+        X = _dev(X, torch.float32); Qc = _dev(Qc, torch.float32)
+        _ck(lib().dade_calibrate_pq(self.h, _ptr(X), _ptr(Qc), Qc.shape[0], K, n_neg, nprobe_neg, seed))
+
+    def get_calibration_q(self):
+        K, n0 = np.zeros(1, np.int32), np.zeros(1, np.int32)
+        _ck(lib().dade_get_calibration_q(self.h, _ptr(K), _ptr(n0), None, None))
+        m = np.zeros(2); v = np.zeros(int(n0[0]))
+        _ck(lib().dade_get_calibration_q(self.h, None, None, _ptr(m), _ptr(v)))
+        return {"K": int(K[0]), "n0": int(n0[0]), "m": m, "v": v}
+
+    def set_calibration_q(self, K: int, m, v):
+        m = np.ascontiguousarray(m, np.float64); v = np.ascontiguousarray(v, np.float64)
+        _ck(lib().dade_set_calibration_q(self.h, K, len(v), _ptr(m), _ptr(v)))
 
     # -------------------------------------------------- multi-rank (the library owns NCCL)
     def set_comm(self, uid, nranks: int, rank: int):

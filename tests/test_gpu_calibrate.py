@@ -40,7 +40,7 @@ def test_sharded_calibration_equals_single():
     # merged and summed as the all-gathers and all-reduce would) installs exactly the table an
     # unsharded dade_calibrate computes on the same base, centroids and rotation
     import torch
-    from paper_2404_16322_b200 import Index, build, sharded
+    from paper_2404_16322_b200 import Index, build, dade
     build.build()
     cfg = synth.config("c2", n=24000, nlist=64, nq=10, n_cal=40)
     X = synth.base(cfg)
@@ -62,9 +62,9 @@ def test_sharded_calibration_equals_single():
         ix.build_ivf(Xd[lo:hi].contiguous(), cfg.nlist, centroids=cent, id_base=lo)
         shards.append((ix, Xd[lo:hi].contiguous()))
     kl = [ix.calib_knn(Xs, Qc, cfg.k) for ix, Xs in shards]
-    knn_ids, knn_d = sharded.merge_knn_lists(np.stack([k[0] for k in kl]), np.stack([k[1] for k in kl]), cfg.k)
+    knn_ids, knn_d = dade.merge_knn(np.stack([k[0] for k in kl]), np.stack([k[1] for k in kl]), cfg.k)
     ng = [ix.calib_negatives(Qc, cfg.k, knn_ids, cfg.n_neg, 6, 3) for ix, _ in shards]
-    pq, pid, tau, y = sharded.calibration_pairs(knn_ids, knn_d, np.stack([g[0] for g in ng]),
+    pq, pid, tau, y = dade.calibration_pairs(knn_ids, knn_d, np.stack([g[0] for g in ng]),
                                                 np.stack([g[1] for g in ng]), np.stack([g[2] for g in ng]), cfg.n_neg)
     F = sum(ix.pair_features(Qc, pq, pid) for ix, _ in shards)
     shards[0][0].fit_calibration(cfg.k, F, tau, y)
