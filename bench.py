@@ -44,7 +44,7 @@ SHAPE = {"c1": "flat, 20-component Gaussian mixture", "c2": "SIFT-shaped", "c3":
 # reference arm (the CPU oracle) is timed on the same operating point
 REF_NPROBE = {"c1": 1, "c2": 8, "c3": 64, "c4": 8, "c5": 8}
 # NEXT-1 comparison (--method): the paper's defaults ε₀ = 2.1 (ADSampling), m = 8 (BSA-res)
-METHOD_PARAM = {"bsa_p": ALPHA, "adsampling": 2.1, "bsa_res": 8.0}
+METHOD_PARAM = {"bsa_p": ALPHA, "adsampling": 2.1, "bsa_res": 8.0, "bsa_q": ALPHA}
 
 
 def log(*a):
@@ -165,6 +165,9 @@ def run_dade(args):
     if args.method == "adsampling":  # ADSampling's projection: a Haar-random orthogonal matrix
         mean, _, lam = ix.get_rotation()
         ix.set_rotation(mean, synth.haar_basis(cfg.d, np.random.default_rng(12345)).T.copy(), lam)
+    if args.method == "bsa_q":  # OPQ rotation + codebooks (m = D/4, D/8 for GIST-like data)
+        assert world == 1, "BSA-q is single-GPU here"
+        ix.train_pq(Xd, cfg.d // 8 if cfg.kind == "gist" else cfg.d // 4)
     torch.cuda.synchronize()
     t_rot = time.time() - t0
     if world > 1:  # k-means: fp64 per-centroid sums / counts all-reduced inside; then the local IVF
@@ -173,6 +176,8 @@ def run_dade(args):
         ix.build_ivf(Xd, cfg.nlist, kmeans_iters=10)
     torch.cuda.synchronize()
     t_ivf = time.time() - t0 - t_rot
+    if args.method == "bsa_q":
+        ix.calibrate_pq(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
     if args.method == "bsa_p":
         if world > 1:  # R14-R16 over the shards: merged K-NN, merged negatives, summed P_d (inside)
             ix.calibrate_dist(Xd, Qcd, K, n_neg=cfg.n_neg, nprobe_neg=cfg.nprobe_neg, seed=0)
@@ -303,6 +308,8 @@ def run_dade(args):
     # ---- roofline of the dominant kernel (k_scan): algorithmic bytes / launch time
     st = stats_acc
     alg_bytes = 4 * st["dims_scanned"] + 4 * st["survivors"] + 4 * cfg.d * cfg.nq
+    if args.method == "bsa_q":  # + every tested candidate's code row (m codes + fp32 reconstruction error)
+        alg_bytes += st["tested"] * ((cfg.d // 8 if cfg.kind == "gist" else cfg.d // 4) + 4)
     scan_avg_ms = sum(scan_ms) / len(scan_ms)
     achieved = alg_bytes / (scan_avg_ms / 1e3) / 1e9
     peak, peak_src = peaks()
@@ -543,9 +550,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dade", choices=["dade", "reference"])
     ap.add_argument("--config", default="c4", help="c1..c5 (default c4: the largest single-GPU config)")
-    ap.add_argument("--method", default="bsa_p", choices=["bsa_p", "adsampling", "bsa_res"],
-                    help="per-step correction: the paper's data-driven BSA-p (default, the headline), or the "
-                         "NEXT-1 comparisons ADSampling (eps0 = 2.1, random rotation) / BSA-res (m = 8)")
+    ap.add_argument("--method", default="bsa_p", choices=["bsa_p", "adsampling", "bsa_res", "bsa_q"],
+                    help="per-step correction: the paper's data-driven BSA-p (default, the headline), the NEXT-1 "
+                         "comparisons ADSampling (eps0 = 2.1, random rotation) / BSA-res (m = 8), or NEXT-3 BSA-q "
+                         "(OPQ + 8-bit PQ codes, ADC test, significance 0.005)")
     ap.add_argument("--nprobe", type=int, default=0, help="fix nprobe instead of sweeping to recall 0.95")
     ap.add_argument("--n", "--base-n", dest="n", type=int, default=0,
                     help="override base size (testing only; use --base-n under torchrun)")

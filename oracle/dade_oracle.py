@@ -346,7 +346,7 @@ def bsa_res_consts(q_rot: np.ndarray, lam: np.ndarray, delta_d: int, m: float) -
 
 
 def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False, method="bsa_p",
-           eps0=2.1, m_res=8.0):
+           eps0=2.1, m_res=8.0, epochs=None, init_top=None, tau_cap=None):
     """IVF search with the per-step data-driven correction (O5).
     Refinement: result queue of size K, τ = its K-th distance (R11: +∞ until full).
     Candidates = the probed lists in probe order. For each candidate, the partial
@@ -357,7 +357,11 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
     target); mode="sequential": τ refreshed after every survivor (P:L42-43 literal).
     method (NEXT-1, the paper's other corrections on the same loop): "bsa_p" (above, α =
     significance), "adsampling" (adsampling_table(ε₀); use a random orthogonal R), "bsa_res"
-    (bsa_res_consts(m_res); needs index["lam"]). α = 0 disables pruning for every method."""
+    (bsa_res_consts(m_res); needs index["lam"]). α = 0 disables pruning for every method.
+    Cross-shard τ seed (R32, epoch mode, used by search_sharded): `epochs` = (first, end) runs only
+    those epochs of the stream; `init_top` = (ids, dists) per query starts the result queue (the
+    shard's own epoch-0 results); `tau_cap` per query bounds τ_e from above (τ_e = min(K-th of the
+    queue, tau_cap[q]))."""
     Q = np.atleast_2d(Q)
     D = Q.shape[1]
     ns = D // delta_d
@@ -385,12 +389,19 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
         qc = bsa_res_consts(Qr[qn], index["lam"], delta_d, m_res) if res else None
         cand = np.concatenate([row_id[off[l]:off[l + 1]] for l in pr]) if len(pr) else np.zeros(0, np.int64)
         top_d = np.zeros(0); top_i = np.zeros(0, dtype=np.int64)
-        st["tested"] += len(cand)
+        if init_top is not None:
+            ok = init_top[0][qn] >= 0
+            top_d, top_i = np.asarray(init_top[1][qn], F64)[ok], np.asarray(init_top[0][qn], np.int64)[ok]
         if mode == "epoch":
             bounds = epoch_bounds(len(cand), K, c0)
+            e_first, e_end = (0, len(bounds) - 1) if epochs is None else (epochs[0], min(epochs[1], len(bounds) - 1))
+            last = len(bounds) - 1
+            st["tested"] += bounds[min(max(e_end, e_first), last)] - bounds[min(e_first, last)]
             st["n_epochs"] = max(st["n_epochs"], len(bounds) - 1)
-            for e in range(len(bounds) - 1):
+            for e in range(e_first, e_end):
                 tau = top_d[K - 1] if len(top_d) >= K else np.inf
+                if tau_cap is not None:
+                    tau = min(tau, float(tau_cap[qn]))
                 ids = cand[bounds[e]:bounds[e + 1]]
                 P = np.cumsum((Xr[ids - base] - Qr[qn]) ** 2, axis=1)
                 keep = np.ones(len(ids), dtype=bool)
@@ -429,6 +440,7 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
                 o = order_by_dist_id(cd, ci)[:K]
                 top_d, top_i = cd[o], ci[o]
         else:
+            st["tested"] += len(cand)
             for idn in cand:
                 tau = top_d[K - 1] if len(top_d) >= K else np.inf
                 P = np.cumsum((Xr[idn - base] - Qr[qn]) ** 2)
@@ -453,6 +465,44 @@ def search(index, Q, K, nprobe, delta_d, alpha, c0=None, mode="epoch", log=False
         out_ids[qn, :len(top_i)] = top_i
         out_d[qn, :len(top_d)] = top_d
     return out_ids, out_d, st
+
+
+def search_sharded(shards, Q, K, nprobe, delta_d, alpha, seed=True, exchanges=2, method="bsa_p", **kw):
+    """The database split over S shards: every shard searches its own sub-lists of
+    the same probed lists with the same calibration, and the local top-K lists are merged by
+    (dist, id). seed=True is R32's schedule: per-shard c0 = ⌈4K/S⌉ (the shards' epoch-0 prefixes
+    together are as long as the single index's); the shards run epoch 0, then epoch 1, …, epoch
+    `exchanges`−1 as separate phases and, after each, exchange their top-K lists (all-gather +
+    merge): from epoch 1 on every shard tests against τ_e = min(its own K-th, the merged K-th of
+    the last exchange); the remaining epochs run as one last phase. The merged K-th is the K-th
+    distance of a subset of the candidates the search has seen, so it bounds the global queue's
+    τ from above. seed=False: independent shards (each τ is its own K-th, c0 = 4K). S = 1 with
+    seed reduces to `search`. Returns (ids, dists, per-shard stats)."""
+    S = len(shards)
+    if not seed:
+        parts, sts = [], []
+        for sh in shards:
+            i, d, st = search(sh, Q, K, nprobe, delta_d, alpha, method=method, **kw)
+            parts.append((i, d)); sts.append(st)
+        return (*merge_shards(parts, K), sts)
+    c0 = -(-4 * K // S)
+    edges = list(range(exchanges + 1)) + [1 << 30]
+    tops, cap, sts = [None] * S, None, [None] * S
+    for a, b in zip(edges[:-1], edges[1:]):
+        for s, sh in enumerate(shards):
+            i, d, st = search(sh, Q, K, nprobe, delta_d, alpha, c0=c0, method=method, epochs=(a, b),
+                              init_top=tops[s], tau_cap=cap, **kw)
+            tops[s] = (i, d)
+            if sts[s] is None:
+                sts[s] = st
+            else:
+                for k in ("tested", "dims_scanned", "survivors"):
+                    sts[s][k] += st[k]
+                sts[s]["pruned_at_step"] = sts[s]["pruned_at_step"] + st["pruned_at_step"]
+        if b < (1 << 30):  # exchange: merged K-th of the shards' queues
+            mi, md = merge_shards(tops, K)
+            cap = np.where(mi[:, K - 1] >= 0, md[:, K - 1], np.inf)
+    return (*merge_shards(tops, K), sts)
 
 
 def exact_ivf(index, X, Q, K, nprobe):

@@ -571,7 +571,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
       p.pq_beta = -INFINITY;
     }
     // gather rounds: enough lanes per survivor to load all of its blocks in one round trip
-    const int la = x->pq_stride <= 64 ? 1 : 2;
+    const int la = 2;  // the PQ scan loads two blocks per lane (scan.cu launch_k)
     int lanes = 1;
     while (lanes < 32 && lanes * la < D / 16) lanes *= 2;
     p.pq_lg = __builtin_ctz(lanes);

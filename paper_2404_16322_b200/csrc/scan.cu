@@ -189,6 +189,20 @@ __device__ __forceinline__ int drain_lanes_log2(int qn) {
   return lg < DADE_DRAIN_LG ? lg : DADE_DRAIN_LG;
 }
 
+// DADE_DEBUG_CHECKS builds (tools/build_variant.py; compute-sanitizer is not available on the
+// GPU pool): device-side invariants of the rings and index ranges — a violation traps, and the
+// next synchronising call reports a CUDA error
+#ifdef DADE_DEBUG_CHECKS
+#define DADE_DCHECK(c) \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define DADE_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
+
 __device__ __forceinline__ unsigned long long make_key(float d, uint32_t id) {
   return ((unsigned long long)__float_as_uint(d) << 32) | id;
 }
@@ -413,10 +427,12 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         while (ppos + pl.y <= pr) {  // skip exhausted (and empty) lists; pr < L keeps pj < nprobe
           ppos += pl.y;
           pl = lists[++pj];
+          DADE_DCHECK(pj < p.nprobe);
         }
         nr = min(min(pe_hi, ppos + pl.y) - pr, TR);
         row0 = pl.x + (pr - ppos);
         pr += nr;
+        DADE_DCHECK(nr >= 1 && nr <= TR && row0 >= 0 && (int64_t)row0 + nr <= n);
         if (!MULTI || (tix++ & (G - 1)) == warp) break;
       }
       if (lane == 0) {
@@ -449,6 +465,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const unsigned km = __ballot_sync(0xffffffffu, keep);
       if (keep) ring[(tail + __popc(km & lt_mask)) & (kQCap - 1)] = e;
       tail += __popc(km);
+      DADE_DCHECK(tail - head <= kQCap);
     };
 
     // One gather round over up to 32 queued survivors. Normally one lane per survivor, up to LA
@@ -464,6 +481,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const int ei = lane >> lg, sub = lane & ((1 << lg) - 1);
       const bool val = ei < qn;
       QEntry e = val ? ring[(head + ei) & (kQCap - 1)] : QEntry{0, 0.f, nblk, 0.f};
+      // blk == nblk: stage 1 already covered every block (D = 16 * DD); the round only finishes it
+      DADE_DCHECK(!val || (e.row >= 0 && (int64_t)e.row < n && e.blk >= 0 && e.blk <= nblk));
       // full rounds: one step (DD blocks, LA >= DD) or LA blocks; draining rounds: LA per lane
       int wtot = (drain || PQ) ? (LA << lg) : (DD < LA ? DD : LA);
       wtot = min(wtot, nblk - e.blk);
@@ -756,7 +775,8 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
 template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
   if (p.pq) {  // BSA-q (NEXT-3): ADC test in stage 1, exact distance of the survivors
-    launch_v<DD, KPL, DD >= 2 ? 2 : 1, DD >= 2 ? 128 : 96, false, true>(p, st);
+    // two blocks per lane: a survivor's exact distance takes nblk / 2 lanes, one round trip
+    launch_v<DD, KPL, 2, 128, false, true>(p, st);
     return;
   }
   if (p.residual) {  // BSA-res (NEXT-1): residual-norm test

@@ -25,20 +25,20 @@ def _lib():
 def test_hand_worked_bsaq_on_gpu():
     torch, Index = _lib()
     X, idx = _hand_q()
-    ix = Index(8)
-    ix.set_rotation(np.zeros(8), np.eye(8))
-    ix.build_ivf(torch.from_numpy(X).cuda(), 1, centroids=torch.zeros((1, 8), device="cuda"))
+    ix = Index(16)
+    ix.set_rotation(np.zeros(16), np.eye(16))
+    ix.build_ivf(torch.from_numpy(X).cuda(), 1, centroids=torch.zeros((1, 16), device="cuda"))
     ix.set_pq(idx["pq"])
     C, codes, err = ix.get_pq()
     assert np.array_equal(codes, idx["codes"]) and np.array_equal(err, idx["pq_err"].astype(np.float32))
     ix.set_calibration_q(1, idx["calq"]["m"], idx["calq"]["v"])
-    Q = torch.zeros((1, 8), device="cuda")
+    Q = torch.zeros((1, 16), device="cuda")
     gi, gd, log = ix.search_log(Q, 1, 1, 16, 0.3, method="bsa_q")
     assert gi.tolist() == [[8]] and gd.tolist() == [[0.0]]
     assert sorted(map(tuple, log.cpu().numpy().tolist())) == \
-        [(0, i, d) for i, d in enumerate([8, 8, 8, 8, 0, 8, 8, 0, 8, 0])]
+        [(0, i, d) for i, d in enumerate([16, 16, 16, 16, 0, 16, 16, 0, 16, 0])]
     _, _, st = ix.search_method(Q, 1, 1, 16, "bsa_q", 0.3, stats=True)
-    assert st["pruned_at_step"] == [3] and st["survivors"] == 7 and st["dims_scanned"] == 7 * 8
+    assert st["pruned_at_step"] == [3] and st["survivors"] == 7 and st["dims_scanned"] == 7 * 16
 
 
 @pytest.fixture(scope="module")

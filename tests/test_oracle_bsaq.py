@@ -120,12 +120,12 @@ def test_logistic_multi_flags_wrong_slope():
     assert not ok and mv.tolist() == [1.0, 0.0] and beta == 0.0
 
 
-# ---------------------------------------------------------------- hand-worked search (D = 8, m = 2)
+# ---------------------------------------------------------------- hand-worked search (D = 16, m = 2)
 def _hand_q():
-    D, ds = 8, 4
+    D, ds = 16, 8
     C = np.zeros((2, O.PQ_K, ds), np.float32)
-    C[:, :, 0] = np.arange(O.PQ_K)                       # codeword c = (c, 0, 0, 0): lut[j, c] = c² at q̃ = 0
-    rows = [  # (a, b): x̃ = (a, 0, 0, 0, b, 0, 0, 0)
+    C[:, :, 0] = np.arange(O.PQ_K)                       # codeword c = (c, 0, ..., 0): lut[j, c] = c² at q̃ = 0
+    rows = [  # (a, b): x̃ = (a, 0 x 7, b, 0 x 7)
         (3.0, 0.0), (2.0, 1.0), (1.0, 1.0), (0.0, 2.0),   # epoch 0 (c0 = 4K = 4): τ = ∞; dists 9 5 2 4 → τ_1 = 2
         (1.25, 0.0),   # id 4: code (1, 0), ADC 1, e 1/16: 1 + 4/16 + 1 = 2.25 > 2 → pruned (exact dist 1.5625)
         (0.0, 1.0),    # id 5: ADC 1, e 0: 2 > 2? no → exact 1
@@ -136,7 +136,7 @@ def _hand_q():
     ]
     X = np.zeros((len(rows), D), np.float32)
     for i, (a, b) in enumerate(rows):
-        X[i, 0], X[i, 4] = a, b
+        X[i, 0], X[i, 8] = a, b
     idx = O.build_index_q(X, np.zeros((1, D), np.float32), np.zeros(D), np.eye(D), C)
     # m = (1, 4); v sorted descending (n0 = 4): α = 0.3 → k = ⌈0.7·4⌉ = 3 → β' = v[2] = 1
     idx["calq"] = {"m": np.array([1.0, 4.0]), "v": np.array([5.0, 3.0, 1.0, -1.0]), "n0": 4, "K": 1}
@@ -147,14 +147,14 @@ def test_hand_worked_bsaq_search():
     X, idx = _hand_q()
     assert idx["codes"].tolist()[4] == [1, 0] and idx["codes"].tolist()[7] == [0, 1]
     assert idx["pq_err"].tolist()[4] == 0.0625 and idx["pq_err"].tolist()[7] == 0.25
-    ids, d, st = O.search_q(idx, np.zeros((1, 8), np.float32), 1, 1, 0.3, log=True)
+    ids, d, st = O.search_q(idx, np.zeros((1, 16), np.float32), 1, 1, 0.3, log=True)
     assert ids.tolist() == [[8]] and d.tolist() == [[0.0]]
     assert st["tested"] == 10 and st["survivors"] == 7 and st["pruned"] == 3     # ids 4, 7, 9 pruned
     q_, i_, dims, margin = (np.concatenate(c) for c in zip(*st["candidates"]))
-    assert dims.tolist() == [8, 8, 8, 8, 0, 8, 8, 0, 8, 0]
+    assert dims.tolist() == [16, 16, 16, 16, 0, 16, 16, 0, 16, 0]
     # id 5: |2 − 2| = 0; id 4: |2.25 − 2| / (1.25 + 1 + 2) = 1/17
     assert margin[5] == 0.0 and abs(margin[4] - 1 / 17) < 1e-15
-    ids, d, st = O.search_q(idx, np.zeros((1, 8), np.float32), 2, 1, 0.0)       # α = 0: exact
+    ids, d, st = O.search_q(idx, np.zeros((1, 16), np.float32), 2, 1, 0.0)      # α = 0: exact
     assert ids.tolist() == [[8, 5]] and st["pruned"] == 0
 
 
