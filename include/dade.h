@@ -288,6 +288,7 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 #define DADE_OPT_HOST_CHUNKS 6     /* dade_search_host: chunks pipelined with the copies (default 1) */
 #define DADE_OPT_HOST_PREP_CHUNKS 7 /* dade_search_host: rotation+probe chunks ahead of one scan (0 auto) */
 #define DADE_OPT_DHAT_ARES 8       /* 1: A-resident d_hat writer for very wide probe rows */
+#define DADE_OPT_SHARD_EXCHANGES 9 /* collective search: top-K exchanges after epochs 0..E-1 (R32; default 2, 0 = none) */
 dade_status dade_set_option(dade_index* idx, int option, int64_t value);
 
 /* Exact probes (a5 alone): probes[nq*nprobe] int32 device, ordered by (exact fp64 dist, id). */
@@ -352,8 +353,13 @@ dade_status dade_set_calibration_q(dade_index* idx, int K, int n0, const double*
  * COLLECTIVE: every rank passes the same queries; rank r rotates and probes its block of
  * ceil(nq/S) queries, the q~ and probe blocks are all-gathered (ncclAllGather), every rank scans all
  * queries over its shard, and the local top-K lists are all-gathered and merged by (dist, id); every
- * rank receives the full result. Each shard prunes against its own tau (its local K-th distance,
- * >= the global one): never unsafe; alpha = 0 gives exactly the unsharded exact IVF.
+ * rank receives the full result. Pruning across shards (R32): per-shard c0 = ceil(4K/S); the scan
+ * runs in E + 1 phases (epochs 0, ..., E-1 one by one, then the rest; E = DADE_OPT_SHARD_EXCHANGES,
+ * default 2) and after each of the first E phases the shards' queues are all-gathered and merged:
+ * from then on every shard prunes against tau_e = min(its own K-th, the merged K-th) — the merged
+ * K-th bounds the global queue's tau from above, so a shard prunes no more aggressively than the
+ * single-index search does at the same stream position. alpha = 0 gives exactly the unsharded
+ * exact IVF. A group of one rank runs the same schedule and equals dade_search.
  * The sharded build (collective; X = this rank's rows, global ids [id_base, id_base+n) of n_total):
  *   dade_fit_rotation_dist  a0 on the GLOBAL strided sample (fp64 moments all-reduced);
  *   dade_build_ivf_dist     k-means on the global strided sample (R19; per-iteration fp64 sums and

@@ -35,6 +35,7 @@ struct Options {
   int host_chunks = 1;      // dade_search_host: searches pipelined with the copies
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
   int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
+  int shard_exchanges = 2;  // collective search: top-K exchanges after epochs 0 .. E-1 (R32)
 };
 
 struct dade_index {
@@ -97,8 +98,8 @@ struct dade_index {
   std::vector<double> vq;
   // multi-rank (dade_set_comm): the NCCL communicator of this shard's group
   Comm* comm = nullptr;
-  DBuf<int64_t> gids;    // collective search: all-gathered local top-K ids / dists
-  DBuf<float> gdists;
+  DBuf<int64_t> gids, cap_ids;    // collective search: all-gathered local top-K ids / dists, the
+  DBuf<float> gdists, cap_d;      // merged queue of the last exchange (R32)
   DBuf<double> red;      // device staging of host partials for all-reduce
 };
 
@@ -467,6 +468,18 @@ int host_prep_chunks(const dade_index* x, int nq) {
 }
 int host_chunks(const dade_index* x, int nq) { return std::max(1, std::min(x->opt.host_chunks, std::max(nq, 1))); }
 
+// One phase of a sharded search (R32): the epochs it runs, the queue it starts from, the exchanged
+// queue bounding tau, the per-shard c0; counters are zeroed by the first phase and read by the last.
+struct Phase {
+  int ep_first = 0, ep_end = 1 << 30;
+  const int64_t* init_ids = nullptr;
+  const float* init_d = nullptr;
+  const int64_t* cap_ids = nullptr;
+  const float* cap_d = nullptr;
+  int c0 = 0;
+  bool first = true, last = true;
+};
+
 struct DecisionLog {
   int32_t* buf = nullptr;  // device, cap x 3 int32
   int64_t cap = 0;
@@ -476,7 +489,9 @@ struct DecisionLog {
 void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int delta_d, double alpha,
                int64_t* ids, float* dists, dade_stats* stats, int method = DADE_METHOD_BSA_P,
                const float* qrot_in = nullptr, const int32_t* probes_in = nullptr,
-               const DecisionLog* dlog = nullptr) {
+               const DecisionLog* dlog = nullptr, const Phase* phase = nullptr) {
+  const Phase ph0;
+  const Phase& ph = phase ? *phase : ph0;
   const int D = x->D;
   DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "search before build_ivf");
   DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
@@ -549,6 +564,13 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   // alpha = 0 (or a single step): nothing can be pruned; the kernel then runs with 16-dim
   // steps (no classifier fires: m1 = 1, beta' = -inf), which serves every delta_d | D.
   p.dd = prune ? dd : 1; p.nsteps = prune ? nsteps : D / 16; p.c0 = DADE_C0_MULT * K; p.prune = prune ? 1 : 0;
+  if (ph.c0 > 0) p.c0 = ph.c0;
+  p.ep_first = ph.ep_first;
+  p.ep_end = ph.ep_end;
+  p.init_ids = ph.init_ids;
+  p.init_d = ph.init_d;
+  p.cap_ids = ph.cap_ids;
+  p.cap_d = ph.cap_d;
   if (pqm) {
     // BSA-q: one classifier on the ADC distance in stage 1 (R29), then exact distances — no
     // classifier in the gather rounds (spacing = all blocks, one step)
@@ -600,7 +622,8 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   p.out_ids = ids; p.out_d = dists;
   if (stats) {
     x->counters.reserve(4 + DADE_MAX_STEPS + 8);
-    DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS + 8), st));
+    if (ph.first)
+      DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS + 8), st));
     p.counters = x->counters.p;
   }
   if (prune && method == DADE_METHOD_BSA_RES) {
@@ -664,7 +687,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     DADE_CK(cudaStreamSynchronize(st));
     *dlog->count = (int64_t)cnt;
   }
-  if (stats) {
+  if (stats && ph.last) {
     DADE_CK(cudaEventRecord(x->ev[3], st));
     unsigned long long c[4 + DADE_MAX_STEPS + 8];
     DADE_CK(cudaMemcpyAsync(c, x->counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
@@ -717,11 +740,31 @@ void do_search_collective(dade_index* x, const float* Q, int nq, int K, int npro
   x->gdists.reserve((size_t)S * nq * K);
   int64_t* li = x->gids.p + (size_t)r * nq * K;
   float* ld = x->gdists.p + (size_t)r * nq * K;
-  // the local scan over this shard (scratch q~ / probes are the gathered buffers: the scan reads
-  // them in place; do_search does not touch x->qrot / x->probes when they are passed in)
-  do_search(x, nullptr, nq, K, nprobe, delta_d, alpha, li, ld, stats, method, x->qrot.p, x->probes.p);
-  comm_allgather(x->comm, li, x->gids.p, sizeof(int64_t) * nq * K, st);
-  comm_allgather(x->comm, ld, x->gdists.p, sizeof(float) * nq * K, st);
+  // the local scan over this shard in E + 1 phases (R32): epochs 0, 1, ..., E-1 one by one, then
+  // the rest; after each of the first E phases the shards' queues are all-gathered and merged and
+  // the merged K-th distance bounds every shard's tau from then on. Per-shard c0 = ceil(4K / S).
+  // Each phase starts from this shard's own queue (init = its previous output, in place: a
+  // query's queue is read at its start and written at its end by the same CTA).
+  const int E = x->opt.shard_exchanges;
+  Phase P;
+  P.c0 = E > 0 ? (DADE_C0_MULT * K + S - 1) / S : DADE_C0_MULT * K;
+  x->cap_ids.reserve((size_t)nq * K);
+  x->cap_d.reserve((size_t)nq * K);
+  for (int e = 0; e <= E; ++e) {
+    P.ep_first = e;
+    P.ep_end = e < E ? e + 1 : (1 << 30);
+    P.first = e == 0;
+    P.last = e == E;
+    P.init_ids = e > 0 ? li : nullptr;
+    P.init_d = e > 0 ? ld : nullptr;
+    P.cap_ids = e > 0 ? x->cap_ids.p : nullptr;
+    P.cap_d = e > 0 ? x->cap_d.p : nullptr;
+    // scratch q~ / probes are the gathered buffers: the scan reads them in place
+    do_search(x, nullptr, nq, K, nprobe, delta_d, alpha, li, ld, stats, method, x->qrot.p, x->probes.p, nullptr, &P);
+    comm_allgather(x->comm, li, x->gids.p, sizeof(int64_t) * nq * K, st);
+    comm_allgather(x->comm, ld, x->gdists.p, sizeof(float) * nq * K, st);
+    if (e < E) launch_merge_topk(x->gids.p, x->gdists.p, S, nq, K, x->cap_ids.p, x->cap_d.p, st);
+  }
   launch_merge_topk(x->gids.p, x->gdists.p, S, nq, K, ids, dists, st);
   if (stats) DADE_CK(cudaStreamSynchronize(st));
 }
@@ -804,7 +847,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
       cudaStreamDestroy(s2);
     }
   for (auto e : x->hev) cudaEventDestroy(e);
-  x->gids.release(); x->gdists.release(); x->red.release(); x->pq_Cd.release(); x->pq_codes.release();
+  x->gids.release(); x->gdists.release(); x->cap_ids.release(); x->cap_d.release(); x->red.release(); x->pq_Cd.release(); x->pq_codes.release();
   comm_destroy(x->comm);
   delete x;
   API_END
@@ -1853,6 +1896,9 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
       DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "prep chunks not in [0, 64]");
       o.host_prep_chunks = (int)value; break;
     case DADE_OPT_DHAT_ARES: in({0, 1}); o.dhat_ares = (int)value; break;
+    case DADE_OPT_SHARD_EXCHANGES:
+      DADE_REQUIRE(value >= 0 && value <= 16, DADE_ERR_ARG, "shard exchanges not in [0, 16]");
+      o.shard_exchanges = (int)value; break;
     default: throw Error(DADE_ERR_ARG, "unknown option");
   }
   API_END

@@ -161,6 +161,14 @@ struct ScanParams {
   const float* pq_C;       // m x 256 x ds codebooks
   float pq_m1, pq_m2, pq_beta;
   int pq_lg;               // log2 lanes per survivor in the exact-distance gather rounds
+  // phases of a sharded search (R32): epochs [ep_first, ep_end) of each query's stream; the
+  // previous phase's queue (init_*: nq x K, null = empty) and the exchanged merged queue whose
+  // K-th distance bounds tau from above (cap_*: nq x K, null = no bound)
+  int ep_first, ep_end;
+  const int64_t* init_ids;
+  const float* init_d;
+  const int64_t* cap_ids;
+  const float* cap_d;
   // decision log (parity runs; null = off): per tested candidate (query, global id, dims read)
   int32_t* dlog;
   int64_t dlog_cap;              // records

@@ -404,16 +404,58 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     for (int j = lane; j < p.nprobe; j += 32) L += lists[j].y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    // this launch's epochs [ep_first, ep_end) (R32 phases of a sharded search; default: all):
+    // stream positions [e_lo0, L) with L capped at the end of epoch ep_end - 1
+    int e_lo0 = 0, e_hi0 = p.c0;
+    for (int e = 0; e < p.ep_first; ++e) {
+      e_lo0 = e_hi0;
+      e_hi0 = e_hi0 > (1 << 29) / DADE_EPOCH_GROWTH ? (1 << 30) : e_hi0 * DADE_EPOCH_GROWTH;
+    }
+    {
+      int64_t b = 0, h = p.c0;
+      for (int e = 0; e < p.ep_end && b < L; ++e, b = h, h *= DADE_EPOCH_GROWTH) {}
+      if (b < L) L = (int)b;
+    }
     int n_ep = 0;  // epochs the stream touches: [0,c0), [c0,2c0), [2c0,4c0), ...
     for (int64_t e_lo = 0, e_hi = p.c0; e_lo < L; e_lo = e_hi, e_hi *= DADE_EPOCH_GROWTH) ++n_ep;
 
     RegTopK<KPL> tk;
     tk.init(K);
     unsigned long long cap = kKeyInf;  // G > 1: the query's K-th key at the start of the epoch
+    // a previous phase's result queue (R32) and the exchanged K-th distance bounding tau
+    float* qtcap = reinterpret_cast<float*>(qslot + 1);
+    if (p.init_ids) {
+      if (!MULTI) {
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) {
+          const int pos = lane * KPL + i;
+          if (pos < K) {
+            const int64_t id = p.init_ids[q * K + pos];
+            tk.k[i] = id < 0 ? kKeyInf : make_key(p.init_d[q * K + pos], (uint32_t)id);
+          }
+        }
+        tk.refresh_kth();
+      } else {
+        unsigned long long* G0 = Gk + (p.ep_first & 1) * K;
+        __syncthreads();
+        for (int j = threadIdx.x; j < K; j += blockDim.x) {
+          const int64_t id = p.init_ids[q * K + j];
+          G0[j] = id < 0 ? kKeyInf : make_key(p.init_d[q * K + j], (uint32_t)id);
+        }
+        __syncthreads();
+        cap = G0[K - 1];
+      }
+    }
+    if (threadIdx.x == 0) {
+      float tc = INFINITY;
+      if (p.cap_ids && p.cap_ids[q * K + K - 1] >= 0) tc = p.cap_d[q * K + K - 1];
+      *qtcap = tc;
+    }
+    __syncthreads();
 
     // ---------------------------------------------------- producer state (warp-uniform)
     // tiles never cross a list or an epoch boundary (R13); tile t belongs to warp t mod G
-    int pj = 0, ppos = 0, pr = 0, pep = 0, pe_hi = p.c0, tix = 0;
+    int pj = 0, ppos = 0, pr = e_lo0, pep = p.ep_first, pe_hi = e_hi0, tix = 0;
     int2 pl = p.nprobe > 0 ? lists[0] : make_int2(0, 0);
     int issued = 0;
     auto issue = [&](int slot) -> bool {
@@ -458,8 +500,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     PROF_MARK(0);  // query start: work item, q~, list table, first tile issues
 
     int head = 0, tail = 0;  // survivor ring (monotonic indices), warp-uniform
-    float tau = INFINITY;
-    int cur_ep = 0, consumed = 0;
+    float tau = MULTI ? (cap == kKeyInf ? INFINITY : __uint_as_float((unsigned)(cap >> 32)))
+                      : (tk.kth == kKeyInf ? INFINITY : __uint_as_float((unsigned)(tk.kth >> 32)));
+    tau = fminf(tau, *qtcap);
+    int cur_ep = p.ep_first, consumed = 0;
 
     auto push = [&](bool keep, const QEntry& e) {
       const unsigned km = __ballot_sync(0xffffffffu, keep);
@@ -546,6 +590,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     auto epoch_end = [&]() {
       if (!MULTI) {
         tau = tk.kth == kKeyInf ? INFINITY : __uint_as_float((unsigned)(tk.kth >> 32));
+        tau = fminf(tau, *qtcap);
         return;
       }
       unsigned long long* Gcur = Gk + (cur_ep & 1) * K;
@@ -576,6 +621,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       __syncthreads();
       cap = Gnew[K - 1];
       tau = cap == kKeyInf ? INFINITY : __uint_as_float((unsigned)(cap >> 32));
+      tau = fminf(tau, *qtcap);
       tk.init(K);
     };
 

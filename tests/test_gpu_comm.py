@@ -61,6 +61,28 @@ def test_collective_search_equals_search(pair):
     assert z[0].shape == (0, cfg.k)
 
 
+@pytest.mark.parametrize("E", [0, 1, 3])
+def test_collective_phases_equal_search(pair, E):
+    # R32's phased schedule (epochs 0..E-1 one launch each, queue carried over, exchanged K-th as a
+    # tau bound) in a group of one: every phase boundary must be invisible — results and counters
+    # equal the single-launch search, for one warp per query and for several (G > 1 epoch merges)
+    torch, cfg, a, b = pair
+    Q = torch.from_numpy(synth.queries(cfg)).cuda()
+    b.set_option("shard_exchanges", E)
+    for G in (1, 4):
+        a.set_option("scan_warps", G); b.set_option("scan_warps", G)
+        i1, d1, s1 = a.search(Q, cfg.k, 8, 16, 0.005, stats=True)
+        i2, d2, s2 = b.search(Q, cfg.k, 8, 16, 0.005, stats=True)
+        assert torch.equal(i1, i2) and torch.equal(d1, d2)
+        assert s1["tested"] == s2["tested"] and s1["dims_scanned"] == s2["dims_scanned"]
+        assert s1["pruned_at_step"] == s2["pruned_at_step"]
+        i1, d1 = a.search(Q, 100, 8, 32, 0.0)                 # K = 100: four keys per lane
+        i2, d2 = b.search(Q, 100, 8, 32, 0.0)
+        assert torch.equal(i1, i2) and torch.equal(d1, d2)
+    a.set_option("scan_warps", 0); b.set_option("scan_warps", 0)
+    b.set_option("shard_exchanges", 2)
+
+
 def test_comm_errors(pair):
     torch, cfg, a, b = pair
     from paper_2404_16322_b200 import DadeError
