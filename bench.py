@@ -398,6 +398,7 @@ def _oracle_sample(cfg, nprobe, n_sub=50_000, nq=40):
     the same base with nlist scaled to keep the average list size (C4: n/nlist ~ 610), the same
     nprobe, K, Δd and α, so each query tests about as many candidates as in the full workload."""
     from oracle import dade_oracle as O
+    n_sub = min(n_sub, cfg.n)                       # C1 (10k rows): the whole base
     nlist = max(1, round(cfg.nlist * n_sub / cfg.n))
     sub = cfg.scaled(n=n_sub, nlist=nlist)
     m = synth.model(cfg)

@@ -41,6 +41,9 @@ namespace dade {
 
 namespace {
 constexpr int TR = 32;            // rows per tile: one row per lane
+#ifndef DADE_SCAN_TMAG  // 1: survivor gathers staged by TMA bulk copies instead of LDG.256 (experiment builds)
+#define DADE_SCAN_TMAG 0
+#endif
 #ifndef DADE_SCAN_REG1  // register cap of the Delta_d = 16, K <= 64 kernels (experiment builds may change it)
 #define DADE_SCAN_REG1 80
 #endif
@@ -275,7 +278,7 @@ __device__ unsigned long long g_scan_prof[16];
 // Per-warp shared-memory slice: tiles | mbar | meta | ring.
 // Ring capacity: rounds start at 32 queued and stage 1 runs below 32, so at most 63 entries are
 // queued.
-template <int DD>
+template <int DD, int LA = 1>
 struct Slice {
 #ifdef DADE_SCAN_STAGES  // experiment builds (tools/build_variant.py)
   static constexpr int kStages = DADE_SCAN_STAGES;
@@ -287,7 +290,9 @@ struct Slice {
 #endif
   static constexpr int TB = TR * 64 * DD;  // tile bytes (DD blocks of 32 rows)
   static constexpr int QCAP = 64;
-  static constexpr size_t bytes = (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + QCAP * sizeof(QEntry);
+  static constexpr size_t GB = DADE_SCAN_TMAG ? (size_t)32 * LA * 64 : 0;  // TMA gather staging
+  static constexpr size_t bytes =
+      (size_t)kStages * TB + 4 * 8 + kStages * sizeof(TileMeta) + QCAP * sizeof(QEntry) + GB;
 };
 
 // decision log (LOG builds): (query, global id, dims read) of one tested candidate
@@ -318,7 +323,7 @@ __device__ __forceinline__ int step_of(int blk, int dd, unsigned magic) {
 template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG, bool PQ>
 __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  using SL = Slice<DD>;
+  using SL = Slice<DD, LA>;
   constexpr int kQCap = SL::QCAP;
   constexpr int kStages = SL::kStages;
   constexpr int TB = SL::TB;
@@ -330,6 +335,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   uint64_t* mbar = reinterpret_cast<uint64_t*>(base + kStages * TB);
   TileMeta* meta = reinterpret_cast<TileMeta*>(mbar + 4);
   QEntry* ring = reinterpret_cast<QEntry*>(meta + kStages);
+  unsigned char* gstg = reinterpret_cast<unsigned char*>(ring + kQCap);  // TMAG: gather staging
+  uint64_t* gbar = &mbar[3];
   unsigned* pruned = reinterpret_cast<unsigned*>(smem + G * SL::bytes);
   int2* lists = reinterpret_cast<int2*>(pruned + DADE_MAX_STEPS);
   float* qs = reinterpret_cast<float*>(lists + ((p.nprobe + 1) & ~1));
@@ -348,8 +355,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   if (lane < 16) sprof[lane] = 0;
   long long prof_last = clock64();
 #endif
+  uint32_t gphase = 0;
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&mbar[s], 1);
+    if (DADE_SCAN_TMAG) mbar_init(gbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -533,13 +542,42 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const int b0 = e.blk + sub * LA;  // this lane's first block
       const int want = max(0, min(LA, e.blk + wtot - b0));
       unsigned long long v[LA][8];
+#if DADE_SCAN_TMAG
+      {  // the rows come through shared memory: one 64-B bulk copy per lane per block
+        const unsigned bytes = __reduce_add_sync(0xffffffffu, (unsigned)want * 64u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of the staging
+        if (lane == 0) mbar_expect_tx(gbar, bytes);
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < LA; ++s)
+          if (s < want)
+            bulk_g2s(gstg + (lane * LA + s) * 64, lay + (((int64_t)(b0 + s) * n + e.row) << 4), 64u, gbar);
+      }
+#else
 #pragma unroll
       for (int s = 0; s < LA; ++s)
         if (s < want) ld_block(v[s], lay + (((int64_t)(b0 + s) * n + e.row) << 4));
+#endif
       uint32_t gid = 0;
       if (e.blk + wtot == nblk && val && sub == 0) gid = (uint32_t)__ldg(p.row_id + e.row);
       head += qn;
       __syncwarp();
+#if DADE_SCAN_TMAG
+      mbar_wait(gbar, gphase);
+      gphase ^= 1u;
+#pragma unroll
+      for (int s = 0; s < LA; ++s)
+        if (s < want) {
+          const ulonglong2* src = reinterpret_cast<const ulonglong2*>(gstg + (lane * LA + s) * 64);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const ulonglong2 t = src[c];
+            v[s][2 * c] = t.x;
+            v[s][2 * c + 1] = t.y;
+          }
+        }
+      __syncwarp();
+#endif
       float bs[LA], bq[LA];
 #pragma unroll
       for (int s = 0; s < LA; ++s) {
@@ -771,9 +809,9 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   }
 }
 
-template <int DD, bool RES>
+template <int DD, int LA, bool RES>
 static size_t scan_smem(int D, int K, int nprobe, int G, int pq_m) {
-  return (size_t)G * Slice<DD>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
+  return (size_t)G * Slice<DD, LA>::bytes + DADE_MAX_STEPS * 4 + (size_t)((nprobe + 1) & ~1) * 8 +
          (size_t)((D + 3) & ~3) * 4 + (RES ? DADE_MAX_STEPS * 4 : 0) + (size_t)pq_m * 256 * 4 +
          (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
@@ -793,7 +831,7 @@ static int scan_group(int nq, int sms, int64_t avg_stream) {
 template <int DD, int KPL, int LA, int MAXREG, bool MULTI, bool RES, bool LOG, bool PQ>
 static void launch_g(const ScanParams& p, cudaStream_t st, int G, int sms) {
   auto kern = k_scan<DD, KPL, LA, MAXREG, MULTI, RES, LOG, PQ>;
-  const size_t smem = scan_smem<DD, RES>(p.D, p.K, p.nprobe, G, PQ ? p.pq_m : 0);
+  const size_t smem = scan_smem<DD, LA, RES>(p.D, p.K, p.nprobe, G, PQ ? p.pq_m : 0);
   DADE_REQUIRE(smem <= 220 * 1024, DADE_ERR_UNSUPPORTED, "scan: shared memory too large (D, K, nprobe)");
   DADE_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
