@@ -797,3 +797,124 @@ def search_q(index, Q, K, nprobe, alpha, c0=None, log=False):
         out_ids[qn, :len(top_i)] = top_i
         out_d[qn, :len(top_d)] = top_d
     return out_ids, out_d, st
+
+
+# ----------------------------------------------------------------------------- NEXT-4 graph refinement
+# HNSW (M = 16, efConstruction = 500) with the DCO in its base-layer
+# refinement. Readings R33-R35: the base layer is a fixed-degree graph of M0 = 2M =
+# 32 neighbours per node chosen from the node's nearest candidates by HNSW's neighbour-selection
+# heuristic; the upper layers only supply the entry point, read as the node nearest to the mean;
+# the search is HNSW's best-first base-layer search with a result queue of size ef (N^{ef}), the
+# DCO tests a neighbour against τ = the queue's max, frozen while one node is expanded.
+def graph_neighbors(X: np.ndarray, pool: np.ndarray, pool_d: np.ndarray, M0: int = 32) -> np.ndarray:
+    """HNSW's neighbour-selection heuristic (R33): walk each node's candidate pool in (dist, id)
+    order and keep a candidate e iff it is closer to the node than to every kept neighbour r
+    (dist(e, node) < dist(e, r)); then fill up to M0 with the nearest discarded candidates (HNSW's
+    keepPrunedConnections). pool / pool_d: n x P candidate ids (exact nearest first, the node
+    itself excluded) and their distances to the node. Returns n x M0 int64 (−1 padded)."""
+    n = pool.shape[0]
+    out = np.full((n, M0), -1, dtype=np.int64)
+    for i in range(n):
+        kept, dropped = [], []
+        for e, de in zip(pool[i], pool_d[i]):
+            if e < 0:
+                continue
+            if len(kept) < M0 and all(de < float(sqdist_seq(X[r:r + 1], X[e])[0]) for r in kept):
+                kept.append(int(e))
+            else:
+                dropped.append(int(e))
+        sel = (kept + dropped)[:M0]
+        out[i, :len(sel)] = sel
+    return out
+
+
+def build_graph(X: np.ndarray, M0: int = 32, P: int = 64):
+    """The base-layer graph (R33) from EXACT candidate pools: each node's P nearest other nodes
+    (fp64, (dist, id) order), the heuristic, and the entry point = the node nearest to the mean
+    of the base (ties → lower id). Returns (nbrs n x M0, entry)."""
+    n = X.shape[0]
+    P = min(P, n - 1)
+    ids, d = brute_force_knn(X, X, P + 1)
+    pool = np.zeros((n, P), np.int64); pool_d = np.zeros((n, P))
+    for i in range(n):
+        keep = ids[i] != i
+        pool[i], pool_d[i] = ids[i][keep][:P], d[i][keep][:P]
+    mu = np.asarray(X, F64).mean(axis=0)
+    entry = int(order_by_dist_id(sqdist_seq(X, mu), np.arange(n))[0])
+    return graph_neighbors(X, pool, pool_d, M0), entry
+
+
+def graph_search(index, Q, K, ef, delta_d, alpha, log=False):
+    """HNSW base-layer refinement with the DCO (R34): result queue W of size ef, candidate queue C;
+    start at the entry point (exact distance); repeatedly take the nearest unexpanded c of C, stop
+    once W holds ef entries and dist(c) > max W; expand c: every unvisited neighbour u is tested
+    with the BSA-p cascade against τ = max W (∞ while |W| < ef), FROZEN during this expansion
+    (prune iff m1_d·P_d + β'_d > τ at d = Δd, 2Δd, …); a survivor's exact
+    distance P_D enters C and W (in (dist, id) order) if |W| < ef or it is below max W; W keeps its
+    ef best. Returns the first K of W (ids, dists) and counters. α = 0: no pruning (plain HNSW
+    refinement). index: build_index(...) over the rows in id order plus "nbrs", "entry"."""
+    Q = np.atleast_2d(Q)
+    D = Q.shape[1]
+    ns = D // delta_d
+    if alpha == 0:
+        m, b = np.ones(ns - 1), np.full(ns - 1, -np.inf)
+    else:
+        m, b = step_table(index["cal"], D, delta_d, alpha)
+    steps = np.arange(1, ns) * delta_d
+    Xr, nbrs, base = index["Xr"], index["nbrs"], index["id_base"]
+    Qr = rotate(Q, index["mean"], index["R"])
+    out_i = np.full((Q.shape[0], K), -1, np.int64); out_d = np.full((Q.shape[0], K), np.inf)
+    st = {"tested": 0, "dims_scanned": 0, "survivors": 0, "expansions": 0,
+          "pruned_at_step": np.zeros(ns, np.int64), "candidates": []}
+    for qn in range(Q.shape[0]):
+        q = Qr[qn]
+        e0 = index["entry"]
+        d0 = float(np.sum((Xr[e0 - base] - q) ** 2))
+        visited = {e0}
+        W = [(d0, e0)]
+        C = [(d0, e0)]
+        st["tested"] += 1; st["dims_scanned"] += D; st["survivors"] += 1
+        while C:
+            c = min(C)
+            C.remove(c)
+            if len(W) >= ef and c[0] > max(W)[0]:
+                break
+            st["expansions"] += 1
+            tau = max(W)[0] if len(W) >= ef else np.inf
+            us = [int(u) for u in nbrs[c[1] - base] if u >= 0 and int(u) not in visited]
+            for u in us:
+                visited.add(u)
+            if not us:
+                continue
+            U = np.array(us, np.int64)
+            P = np.cumsum((Xr[U - base] - q) ** 2, axis=1)
+            dims = np.full(len(U), D)
+            keep = np.ones(len(U), bool)
+            margin = np.full(len(U), np.inf)
+            if np.isfinite(tau) and ns > 1:
+                score = m[None, :] * P[:, steps - 1] + b[None, :]
+                test = score > tau
+                anyp = test.any(axis=1)
+                first = np.argmax(test, axis=1)
+                keep = ~anyp
+                dims[anyp] = steps[first[anyp]]
+                np.add.at(st["pruned_at_step"], first[anyp] + 1, 1)
+                if log:
+                    scale = np.abs(m[None, :] * P[:, steps - 1]) + np.abs(b[None, :]) + tau
+                    rel = np.abs(score - tau) / scale
+                    last = np.where(anyp, first, ns - 2)
+                    upto = np.arange(ns - 1)[None, :] <= last[:, None]
+                    margin = np.where(upto, rel, np.inf).min(axis=1)
+            st["tested"] += len(U); st["dims_scanned"] += int(dims.sum()); st["survivors"] += int(keep.sum())
+            if log:
+                st["candidates"].append((np.full(len(U), qn), U.copy(), dims.copy(), margin))
+            for du, u in sorted(zip(P[keep, D - 1].tolist(), U[keep].tolist())):
+                if len(W) < ef or (du, u) < max(W):
+                    C.append((du, u))
+                    W.append((du, u))
+                    if len(W) > ef:
+                        W.remove(max(W))
+        W.sort()
+        for j, (dd, u) in enumerate(W[:K]):
+            out_i[qn, j], out_d[qn, j] = u, dd
+    return out_i, out_d, st
