@@ -341,6 +341,36 @@ dade_status dade_calibrate_pq(dade_index* idx, const float* X, const float* Qc, 
 dade_status dade_get_calibration_q(const dade_index* idx, int* K, int* n0, double* m, double* v);
 dade_status dade_set_calibration_q(dade_index* idx, int K, int n0, const double* m, const double* v);
 
+/* ---------------------------------------------------------------- NEXT-4: graph refinement with the DCO
+ * HNSW (M = 16 -> base-layer degree M0 = 32) searched with the same
+ * classifier-pruned progressive distances. Readings R33-R35:
+ *   graph       a base-layer graph over this index's rows: each row's M0 neighbours chosen from its
+ *               P nearest other rows by HNSW's neighbour-selection heuristic (keep e iff e is closer
+ *               to the row than to every kept neighbour; fill from the dropped ones); the upper
+ *               layers only supply the entry point, read as the row nearest to the rotation's mean.
+ *   search      HNSW's best-first base-layer search: result queue W of size ef (N^{ef}), candidate
+ *               queue C; pop the nearest c, stop when |W| = ef and dist(c) > max W; every unvisited
+ *               neighbour is tested against tau = max W (inf while |W| < ef), FROZEN for the
+ *               expansion; survivors' exact distances enter C and W in (dist, id) order; the first
+ *               K of W are returned. The BSA-p step table comes from dade_calibrate with K = ef.
+ *   dade_build_graph   pools from exact IVF searches of the rows themselves at nprobe_pool lists
+ *                      (nprobe_pool = nlist: the exact P nearest), X = the raw rows (device);
+ *                      1 <= M0 <= 32, M0 <= P <= 128.
+ *   dade_set_graph / dade_get_graph   host n x M0 global ids (row i = id id_base + i, -1 pads), entry id.
+ *   dade_graph_search  Q device nq x D raw; ids / dists device nq x K; K <= ef <= DADE_MAX_K; alpha
+ *                      = 0: no pruning. stats (may be NULL): tested = nodes whose distance was
+ *                      started, survivors = exact distances, dims_scanned, pruned_at_step,
+ *                      n_epochs = node expansions. log (device log_cap x 3 int32, may be NULL): one
+ *                      record {query, id, dims read} per tested node; *log_count = records produced.
+ * A new IVF / rotation discards the graph. Errors: ARG, STATE (no IVF / graph / calibration with
+ * K = ef), NONFINITE, UNSUPPORTED (D, ef too large for shared memory), CUDA. */
+dade_status dade_build_graph(dade_index* idx, const float* X, int M0, int P, int nprobe_pool);
+dade_status dade_set_graph(dade_index* idx, const int64_t* nbrs, int M0, int64_t entry);
+dade_status dade_get_graph(const dade_index* idx, int* M0, int64_t* nbrs, int64_t* entry);
+dade_status dade_graph_search(dade_index* idx, const float* Q, int nq, int K, int ef, int delta_d, double alpha,
+                              int64_t* ids, float* dists, dade_stats* stats, int32_t* log, int64_t log_cap,
+                              int64_t* log_count);
+
 /* ---------------------------------------------------------------- multi-rank
  * The database is sharded by contiguous global-id ranges, one index (one process, one GPU) per
  * shard; mu, R, the centroids and the calibration table are replicated. The library owns the NCCL

@@ -815,15 +815,23 @@ def graph_neighbors(X: np.ndarray, pool: np.ndarray, pool_d: np.ndarray, M0: int
     n = pool.shape[0]
     out = np.full((n, M0), -1, dtype=np.int64)
     for i in range(n):
+        cand = [(int(e), float(de)) for e, de in zip(pool[i], pool_d[i]) if e >= 0]
+        if not cand:
+            continue
+        ce = np.array([e for e, _ in cand])
+        # distances among the pool members: sequential fp64 sums over the dims (R20's rule)
+        A = np.asarray(X[ce], F64)
+        pair = np.zeros((len(ce), len(ce)))
+        for j in range(A.shape[1]):
+            t = A[:, j][:, None] - A[:, j][None, :]
+            pair += t * t
         kept, dropped = [], []
-        for e, de in zip(pool[i], pool_d[i]):
-            if e < 0:
-                continue
-            if len(kept) < M0 and all(de < float(sqdist_seq(X[r:r + 1], X[e])[0]) for r in kept):
-                kept.append(int(e))
+        for a, (e, de) in enumerate(cand):
+            if len(kept) < M0 and all(de < pair[a, r] for r in kept):
+                kept.append(a)
             else:
-                dropped.append(int(e))
-        sel = (kept + dropped)[:M0]
+                dropped.append(a)
+        sel = [int(ce[a]) for a in (kept + dropped)[:M0]]
         out[i, :len(sel)] = sel
     return out
 
@@ -874,6 +882,8 @@ def graph_search(index, Q, K, ef, delta_d, alpha, log=False):
         W = [(d0, e0)]
         C = [(d0, e0)]
         st["tested"] += 1; st["dims_scanned"] += D; st["survivors"] += 1
+        if log:
+            st["candidates"].append((np.array([qn]), np.array([e0]), np.array([D]), np.array([np.inf])))
         while C:
             c = min(C)
             C.remove(c)

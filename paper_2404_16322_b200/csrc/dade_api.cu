@@ -96,6 +96,13 @@ struct dade_index {
   int calqK = 0, n0q = 0;
   double mq[2] = {1.0, 0.0};
   std::vector<double> vq;
+  // NEXT-4 graph refinement: base-layer adjacency (n x M0 layout positions), entry position,
+  // per-warp-slot visited bitmaps and lists
+  bool has_graph = false;
+  int g_M0 = 0, g_entry = 0;
+  DBuf<int32_t> g_adj, g_vlist;
+  DBuf<unsigned> g_vis;
+  int64_t g_slots = 0;
   // multi-rank (dade_set_comm): the NCCL communicator of this shard's group
   Comm* comm = nullptr;
   DBuf<int64_t> gids, cap_ids;    // collective search: all-gathered local top-K ids / dists, the
@@ -333,6 +340,7 @@ void upload_rotation(dade_index* x) {
   x->has_cal = false;
   x->xnorm_ok = false;
   x->has_pq = false;  // codebooks live in the old basis
+  x->has_graph = false;
   x->pq_codes_ok = false;
   x->has_calq = false;
   x->R_d.reserve((size_t)D * D);
@@ -848,6 +856,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
     }
   for (auto e : x->hev) cudaEventDestroy(e);
   x->gids.release(); x->gdists.release(); x->cap_ids.release(); x->cap_d.release(); x->red.release(); x->pq_Cd.release(); x->pq_codes.release();
+  x->g_adj.release(); x->g_vlist.release(); x->g_vis.release();
   comm_destroy(x->comm);
   delete x;
   API_END
@@ -1108,6 +1117,7 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
   x->xnorm_ok = false;
   x->has_cal = false;
   pq_encode_layout(x);  // BSA-q: codes of the new layout (if codebooks are installed)
+  x->has_graph = false;
   API_END
 }
 
@@ -1867,7 +1877,7 @@ extern "C" dade_status dade_set_ivf(dade_index* x, const float* Xrot, int64_t n,
   x->off_h = std::move(offv); x->row_id_h = std::move(rid); x->assign_h = std::move(asg); x->pos_of_h = std::move(pos_of);
   x->nlist = nlist; x->n = n; x->id_base = id_base;
   tc_prepare(x, x->cent.p, nlist, x->cent_tc, true);
-  x->has_ivf = true; x->has_cal = false; x->xnorm_ok = false;
+  x->has_ivf = true; x->has_cal = false; x->xnorm_ok = false; x->has_graph = false;
   pq_encode_layout(x);
   API_END
 }
@@ -2326,5 +2336,226 @@ extern "C" dade_status dade_set_calibration_q(dade_index* x, int K, int n0, cons
   x->n0q = n0;
   x->calqK = K;
   x->has_calq = true;
+  API_END
+}
+
+// ================================================================== NEXT-4 graph refinement
+namespace {
+void install_graph(dade_index* x, const std::vector<int32_t>& adj_pos, int M0, int entry_pos) {
+  x->g_adj.reserve(adj_pos.size());
+  DADE_CK(cudaMemcpyAsync(x->g_adj.p, adj_pos.data(), 4 * adj_pos.size(), cudaMemcpyHostToDevice, x->stream));
+  int sms = 0;
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device));
+  x->g_slots = graph_slots(sms);
+  const size_t words = (size_t)((x->n + 31) / 32);
+  x->g_vis.reserve((size_t)x->g_slots * words);
+  DADE_CK(cudaMemsetAsync(x->g_vis.p, 0, 4 * (size_t)x->g_slots * words, x->stream));
+  x->g_vlist.reserve((size_t)x->g_slots * 8192);
+  DADE_CK(cudaStreamSynchronize(x->stream));
+  x->g_M0 = M0;
+  x->g_entry = entry_pos;
+  x->has_graph = true;
+}
+}  // namespace
+
+// Inject a base-layer graph (R33): nbrs host n x M0 global ids (row i = global id id_base + i; -1
+// pads), entry = global id of the entry point. The graph lives over this index's rows.
+extern "C" dade_status dade_set_graph(dade_index* x, const int64_t* nbrs, int M0, int64_t entry) {
+  API_BEGIN
+  need(x, "index"); need(nbrs, "nbrs");
+  DADE_REQUIRE(x->has_ivf, DADE_ERR_STATE, "set_graph needs the index's rows (build_ivf)");
+  DADE_REQUIRE(M0 >= 1 && M0 <= 32, DADE_ERR_ARG, "M0 not in [1, 32]");
+  DADE_REQUIRE(entry >= x->id_base && entry < x->id_base + x->n, DADE_ERR_ARG, "entry outside the index");
+  DeviceGuard g(x->device);
+  std::vector<int32_t> adj((size_t)x->n * M0, -1);
+  for (int64_t i = 0; i < x->n; ++i)
+    for (int j = 0; j < M0; ++j) {
+      const int64_t u = nbrs[(size_t)i * M0 + j];
+      if (u < 0) continue;
+      DADE_REQUIRE(u >= x->id_base && u < x->id_base + x->n, DADE_ERR_ARG, "neighbour id outside the index");
+      adj[(size_t)x->pos_of_h[i] * M0 + j] = x->pos_of_h[u - x->id_base];
+    }
+  install_graph(x, adj, M0, x->pos_of_h[entry - x->id_base]);
+  API_END
+}
+
+extern "C" dade_status dade_get_graph(const dade_index* x, int* M0, int64_t* nbrs, int64_t* entry) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_graph, DADE_ERR_STATE, "no graph");
+  if (M0) *M0 = x->g_M0;
+  if (entry) *entry = x->row_id_h[x->g_entry];
+  if (nbrs) {
+    DeviceGuard g(x->device);
+    std::vector<int32_t> adj((size_t)x->n * x->g_M0);
+    DADE_CK(cudaMemcpyAsync(adj.data(), x->g_adj.p, 4 * adj.size(), cudaMemcpyDeviceToHost, x->stream));
+    DADE_CK(cudaStreamSynchronize(x->stream));
+    for (int64_t i = 0; i < x->n; ++i)
+      for (int j = 0; j < x->g_M0; ++j) {
+        const int32_t pv = adj[(size_t)x->pos_of_h[i] * x->g_M0 + j];
+        nbrs[(size_t)i * x->g_M0 + j] = pv < 0 ? -1 : x->row_id_h[pv];
+      }
+  }
+  API_END
+}
+
+// Build the base-layer graph (R33): each row's P nearest other rows from an exact IVF search of
+// the row itself at nprobe_pool lists (nprobe_pool = nlist: the exact P nearest), HNSW's heuristic
+// down to M0 on the GPU, entry = the row nearest to the rotation's mean (min ||x~||^2, lower id on
+// ties). X: device n x D raw rows of this index (the IVF's input).
+extern "C" dade_status dade_build_graph(dade_index* x, const float* X, int M0, int P, int nprobe_pool) {
+  API_BEGIN
+  need(x, "index"); need(X, "X");
+  DADE_REQUIRE(x->has_ivf && x->has_rot, DADE_ERR_STATE, "build_graph needs build_ivf");
+  DADE_REQUIRE(M0 >= 1 && M0 <= 32 && P >= M0 && P <= 128 && P < x->n, DADE_ERR_ARG, "need 1 <= M0 <= 32, M0 <= P <= 128, P < n");
+  DADE_REQUIRE(nprobe_pool >= 1 && nprobe_pool <= x->nlist, DADE_ERR_ARG, "nprobe_pool not in [1, nlist]");
+  DeviceGuard g(x->device);
+  const int64_t n = x->n;
+  const int K = P + 1;
+  cudaStream_t st = x->stream;
+  std::vector<int32_t> pool((size_t)n * P, -1);
+  std::vector<float> pool_d((size_t)n * P, INFINITY);
+  const int64_t chunk = 65536;
+  DBuf<int64_t> ids;
+  DBuf<float> ds;
+  ids.reserve((size_t)chunk * K);
+  ds.reserve((size_t)chunk * K);
+  std::vector<int64_t> hi((size_t)chunk * K);
+  std::vector<float> hd((size_t)chunk * K);
+  for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+    const int m = (int)std::min(chunk, n - r0);
+    do_search(x, X + r0 * x->D, m, K, nprobe_pool, 16, 0.0, ids.p, ds.p, nullptr);
+    DADE_CK(cudaMemcpyAsync(hi.data(), ids.p, 8 * (size_t)m * K, cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaMemcpyAsync(hd.data(), ds.p, 4 * (size_t)m * K, cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < m; ++i) {
+      const int64_t gid = x->id_base + r0 + i;
+      const size_t row = (size_t)x->pos_of_h[r0 + i] * P;
+      int c = 0;
+      for (int j = 0; j < K && c < P; ++j) {
+        const int64_t u = hi[(size_t)i * K + j];
+        if (u < 0 || u == gid) continue;
+        pool[row + c] = x->pos_of_h[u - x->id_base];
+        pool_d[row + c] = hd[(size_t)i * K + j];
+        ++c;
+      }
+    }
+  }
+  ids.release(); ds.release();
+  DBuf<int32_t> pool_dev, adj_dev;
+  DBuf<float> pd_dev;
+  pool_dev.reserve(pool.size()); pd_dev.reserve(pool_d.size()); adj_dev.reserve((size_t)n * M0);
+  DADE_CK(cudaMemcpyAsync(pool_dev.p, pool.data(), 4 * pool.size(), cudaMemcpyHostToDevice, st));
+  DADE_CK(cudaMemcpyAsync(pd_dev.p, pool_d.data(), 4 * pool_d.size(), cudaMemcpyHostToDevice, st));
+  launch_graph_prune(x->layout.p, n, x->D, pool_dev.p, pd_dev.p, P, M0, adj_dev.p, st);
+  std::vector<int32_t> adj((size_t)n * M0);
+  DADE_CK(cudaMemcpyAsync(adj.data(), adj_dev.p, 4 * adj.size(), cudaMemcpyDeviceToHost, st));
+  // entry: min ||x~||^2 (the row nearest to mu), ties to the lower id
+  if (!x->xnorm_ok) {
+    x->xnorm.reserve((size_t)std::max<int64_t>(n, 1));
+    launch_row_norms(x->layout.p, n, x->D, x->xnorm.p, st);
+    x->xnorm_ok = true;
+  }
+  std::vector<float> nrm(n);
+  DADE_CK(cudaMemcpyAsync(nrm.data(), x->xnorm.p, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  DADE_CK(cudaStreamSynchronize(st));
+  int entry = 0;
+  for (int64_t p = 1; p < n; ++p)
+    if (nrm[p] < nrm[entry] || (nrm[p] == nrm[entry] && x->row_id_h[p] < x->row_id_h[entry])) entry = (int)p;
+  install_graph(x, adj, M0, entry);
+  API_END
+}
+
+// HNSW base-layer refinement with the DCO (R34): Q device nq x D raw; result queue of size ef,
+// tau = its max frozen per expansion; BSA-p step table from the calibration (calibrated with K =
+// ef; alpha = 0: no pruning); the first K of the queue -> ids / dists (device nq x K). stats may be
+// NULL; log (device, log_cap x 3 int32: query, id, dims read per tested node) may be NULL.
+extern "C" dade_status dade_graph_search(dade_index* x, const float* Q, int nq, int K, int ef, int delta_d,
+                                         double alpha, int64_t* ids, float* dists, dade_stats* stats, int32_t* log,
+                                         int64_t log_cap, int64_t* log_count) {
+  API_BEGIN
+  need(x, "index");
+  DADE_REQUIRE(x->has_graph, DADE_ERR_STATE, "graph search needs a graph (dade_build_graph / dade_set_graph)");
+  DADE_REQUIRE(nq >= 0, DADE_ERR_ARG, "nq < 0");
+  DADE_REQUIRE(K >= 1 && ef >= K && ef <= DADE_MAX_K, DADE_ERR_ARG, "need 1 <= K <= ef <= DADE_MAX_K");
+  const int D = x->D;
+  DADE_REQUIRE(delta_d >= 16 && delta_d % 16 == 0 && D % delta_d == 0, DADE_ERR_ARG,
+               "delta_d must be a positive multiple of 16 dividing D");
+  DADE_REQUIRE(alpha >= 0.0 && alpha < 1.0, DADE_ERR_ARG, "significance not in [0,1)");
+  const int nsteps = D / delta_d;
+  const bool prune = alpha > 0.0 && nsteps > 1;
+  if (prune) {
+    DADE_REQUIRE(x->has_cal, DADE_ERR_STATE, "significance > 0 requires calibration (with K = ef)");
+    DADE_REQUIRE(x->calK == ef, DADE_ERR_STATE, "the calibration's K differs from ef");
+  }
+  if (log) DADE_REQUIRE(log_count != nullptr && log_cap >= 0, DADE_ERR_ARG, "log needs log_count");
+  if (nq == 0) { if (log_count) *log_count = 0; g_err.clear(); return DADE_OK; }
+  need(Q, "Q"); need(ids, "ids"); need(dists, "dists");
+  DeviceGuard g(x->device);
+  cudaStream_t st = x->stream;
+  check_finite(x, Q, (int64_t)nq * D, "Q");
+  x->qrot.reserve((size_t)nq * D);
+  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
+  GraphParams p{};
+  p.qrot = x->qrot.p; p.layout = x->layout.p; p.row_id = x->row_id_d.p; p.adj = x->g_adj.p; p.n = x->n;
+  p.D = D; p.nq = nq; p.K = K; p.ef = ef; p.M0 = x->g_M0; p.entry = x->g_entry;
+  p.dd = prune ? delta_d / 16 : 1;
+  p.nsteps = prune ? nsteps : D / 16;
+  for (int s2 = 1; s2 < p.nsteps; ++s2) {
+    if (prune) {  // the scan's step table (R4, R5)
+      const int idx = (s2 * delta_d) / 16 - 1;
+      const double alpha_s = (alpha * delta_d) / D;
+      long k = (long)std::ceil((1.0 - alpha_s) * (double)x->n0);
+      k = std::min<long>(std::max<long>(k, 1), x->n0);
+      p.m1[s2 - 1] = (float)x->m1[idx];
+      p.beta[s2 - 1] = (float)x->v[(size_t)idx * x->n0 + (k - 1)];
+    } else {
+      p.m1[s2 - 1] = 1.f;
+      p.beta[s2 - 1] = -INFINITY;
+    }
+  }
+  p.out_ids = ids; p.out_d = dists;
+  p.visited = x->g_vis.p; p.vlist = x->g_vlist.p; p.vcap = 8192;
+  x->work.reserve(2);
+  DADE_CK(cudaMemsetAsync(x->work.p, 0, sizeof(int), st));
+  p.work = x->work.p;
+  if (stats) {
+    x->counters.reserve(4 + DADE_MAX_STEPS + 8);
+    DADE_CK(cudaMemsetAsync(x->counters.p, 0, sizeof(unsigned long long) * (4 + DADE_MAX_STEPS + 8), st));
+    p.counters = x->counters.p;
+  }
+  if (log) {
+    x->dlog_n.reserve(1);
+    DADE_CK(cudaMemsetAsync(x->dlog_n.p, 0, sizeof(unsigned long long), st));
+    p.dlog = log; p.dlog_cap = log_cap; p.dlog_n = x->dlog_n.p;
+  }
+  int sms = 0;
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device));
+  if (stats) DADE_CK(cudaEventRecord(x->ev[0] ? x->ev[0] : (cudaEventCreate(&x->ev[0]), x->ev[0]), st));
+  launch_graph_search(p, sms, st);
+  if (log) {
+    unsigned long long c = 0;
+    DADE_CK(cudaMemcpyAsync(&c, x->dlog_n.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    *log_count = (int64_t)c;
+  }
+  if (stats) {
+    if (!x->ev[3]) DADE_CK(cudaEventCreate(&x->ev[3]));
+    DADE_CK(cudaEventRecord(x->ev[3], st));
+    unsigned long long c[4 + DADE_MAX_STEPS + 8];
+    DADE_CK(cudaMemcpyAsync(c, x->counters.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+    DADE_CK(cudaStreamSynchronize(st));
+    memset(stats, 0, sizeof(*stats));
+    stats->tested = (int64_t)c[0];
+    stats->survivors = (int64_t)c[1];
+    int64_t dims = (int64_t)c[1] * D;
+    for (int s2 = 1; s2 < DADE_MAX_STEPS; ++s2) dims += (int64_t)c[4 + s2] * s2 * (p.dd * 16);
+    stats->dims_scanned = dims;
+    stats->n_epochs = (int32_t)std::min<unsigned long long>(c[2], 0x7fffffffull);  // expansions
+    for (int s2 = 0; s2 < DADE_MAX_STEPS; ++s2) stats->pruned_at_step[s2] = (int64_t)c[4 + s2];
+    stats->n_steps = p.nsteps;
+    cudaEventElapsedTime(&stats->ms_total, x->ev[0], x->ev[3]);
+    stats->ms_scan = stats->ms_total;
+  }
   API_END
 }

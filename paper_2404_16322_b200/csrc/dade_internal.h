@@ -227,6 +227,36 @@ void launch_pq_pair_feat(const uint8_t* codes, int stride, int eo, int m, int D,
 void launch_pq_cross(const float* X, const double* mu, int64_t n, int D, int m, const float* C, const uint8_t* codes,
                      double* M, cudaStream_t st);
 
+// graph.cu (NEXT-4): HNSW base-layer refinement with the DCO
+struct GraphParams {  // one graph search launch (graph.cu)
+  const float* qrot;        // nq x D
+  const float* layout;      // blocked
+  const int32_t* row_id;    // list-major position -> global id
+  const int32_t* adj;       // n x M0 positions (-1 pad)
+  int64_t n;
+  int D, nq, K, ef, M0, entry, dd, nsteps;
+  float m1[DADE_MAX_STEPS], beta[DADE_MAX_STEPS];
+  int64_t* out_ids;
+  float* out_d;
+  unsigned* visited;        // per warp slot: ceil(n / 32) words, zero between queries
+  int32_t* vlist;           // per warp slot: vcap positions set in the bitmap
+  int vcap;
+  int* work;
+  unsigned long long* counters;  // [0] tested [1] survivors [2] expansions [3] unused [4 + s] pruned at step s
+  int32_t* dlog;
+  int64_t dlog_cap;
+  unsigned long long* dlog_n;
+};
+
+
+size_t graph_smem(int D, int ef);
+int graph_slots(int sms);
+void launch_graph_search(const GraphParams& p, int sms, cudaStream_t st);
+// HNSW's neighbour-selection heuristic per node over its candidate pool (positions, ascending by
+// (dist, id)); out: n x M0 positions (-1 pad)
+void launch_graph_prune(const float* layout, int64_t n, int D, const int32_t* pool, const float* pool_d, int P,
+                        int M0, int32_t* out, cudaStream_t st);
+
 // host_eig.cpp : symmetric eigendecomposition (Householder tridiagonalisation + implicit QL)
 void sym_eig(int n, const double* A, double* eigval, double* eigvec_colmajor);
 // host_calib.cpp

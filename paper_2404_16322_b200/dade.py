@@ -86,6 +86,10 @@ _SIGS = {
     "dade_calibrate_pq": [P, P, P, I32, I32, I32, I32, C.c_uint64],
     "dade_get_calibration_q": [P, P, P, P, P],
     "dade_set_calibration_q": [P, I32, I32, P, P],
+    "dade_build_graph": [P, P, I32, I32, I32],
+    "dade_set_graph": [P, P, I32, I64],
+    "dade_get_graph": [P, P, P, P],
+    "dade_graph_search": [P, P, I32, I32, I32, I32, DBL, P, P, P, P, I64, P],
     "dade_comm_unique_id": [P],
     "dade_set_comm": [P, P, I32, I32],
     "dade_fit_rotation_dist": [P, P, I64, I64, I64, I64],
@@ -519,6 +523,53 @@ class Index:
     def set_calibration_q(self, K: int, m, v):
         m = np.ascontiguousarray(m, np.float64); v = np.ascontiguousarray(v, np.float64)
         _ck(lib().dade_set_calibration_q(self.h, K, len(v), _ptr(m), _ptr(v)))
+
+    # -------------------------------------------------- NEXT-4 graph refinement with the DCO
+    def build_graph(self, X, M0: int = 32, P: int = 64, nprobe_pool: int = 0):
+        """Base-layer graph over this index's rows (X = the raw rows given to build_ivf);
+        nprobe_pool = 0: every list (exact pools)."""
+        import torch
+        X = _dev(X, torch.float32)
+        _, nlist = self.sizes()
+        _ck(lib().dade_build_graph(self.h, _ptr(X), M0, P, nprobe_pool or nlist))
+
+    def set_graph(self, nbrs, entry: int):
+        nb = np.ascontiguousarray(nbrs, np.int64)
+        _ck(lib().dade_set_graph(self.h, _ptr(nb), nb.shape[1], int(entry)))
+
+    def get_graph(self):
+        m0 = np.zeros(1, np.int32); e = np.zeros(1, np.int64)
+        _ck(lib().dade_get_graph(self.h, _ptr(m0), None, _ptr(e)))
+        n, _ = self.sizes()
+        nb = np.zeros((n, int(m0[0])), np.int64)
+        _ck(lib().dade_get_graph(self.h, None, _ptr(nb), None))
+        return nb, int(e[0])
+
+    def graph_search(self, Q, K: int, ef: int, delta_d: int, significance: float, stats: bool = False,
+                     log: bool = False, cap: int = 0):
+        """HNSW base-layer refinement with the DCO. Returns (ids, dists[, stats][, log])."""
+        import torch
+        Q = _dev(Q, torch.float32)
+        nq = Q.shape[0]
+        ids = torch.empty((nq, K), dtype=torch.int64, device=Q.device)
+        dists = torch.empty((nq, K), dtype=torch.float32, device=Q.device)
+        st = Stats() if stats else None
+        lg, cnt = None, np.zeros(1, np.int64)
+        if log:
+            cap = cap or max(1, nq * 4 * ef * 32)
+            lg = torch.empty((cap, 3), dtype=torch.int32, device=Q.device)
+        _ck(lib().dade_graph_search(self.h, _ptr(Q), nq, K, ef, delta_d, float(significance), _ptr(ids), _ptr(dists),
+                                    C.byref(st) if st is not None else None, _ptr(lg) if log else None,
+                                    cap if log else 0, _ptr(cnt) if log else None))
+        out = [ids, dists]
+        if stats:
+            out.append(st.as_dict())
+        if log:
+            n = int(cnt[0])
+            if n > cap:
+                return self.graph_search(Q, K, ef, delta_d, significance, stats, log, cap=n)
+            out.append(lg[:n])
+        return tuple(out)
 
     # -------------------------------------------------- multi-rank (the library owns NCCL)
     def set_comm(self, uid, nranks: int, rank: int):

@@ -70,6 +70,6 @@ def test_hand_worked_graph_search():
     assert st["pruned_at_step"].tolist() == [0, 0, 1]
     assert st["dims_scanned"] == 4 * 48 + 32
     q_, u_, dims, _ = (np.concatenate(c) for c in zip(*st["candidates"]))
-    assert list(zip(u_.tolist(), dims.tolist())) == [(1, 48), (2, 48), (3, 48), (4, 32)]
+    assert list(zip(u_.tolist(), dims.tolist())) == [(0, 48), (1, 48), (2, 48), (3, 48), (4, 32)]
     ids, d, st = O.graph_search(idx, np.zeros((1, D), np.float32), 2, 2, 16, 0.0)   # no DCO
     assert ids.tolist() == [[3, 1]] and st["pruned_at_step"].sum() == 0
