@@ -347,7 +347,9 @@ dade_status dade_set_calibration_q(dade_index* idx, int K, int n0, const double*
  *   graph       a base-layer graph over this index's rows: each row's M0 neighbours chosen from its
  *               P nearest other rows by HNSW's neighbour-selection heuristic (keep e iff e is closer
  *               to the row than to every kept neighbour; fill from the dropped ones); the upper
- *               layers only supply the entry point, read as the row nearest to the rotation's mean.
+ *               layers only supply the entry point: with an IVF (nlist > 1) the lowest-id row of
+ *               the query's nearest non-empty list (the coarse quantizer stands in for them), in a
+ *               flat index the row nearest to the rotation's mean.
  *   search      HNSW's best-first base-layer search: result queue W of size ef (N^{ef}), candidate
  *               queue C; pop the nearest c, stop when |W| = ef and dist(c) > max W; every unvisited
  *               neighbour is tested against tau = max W (inf while |W| < ef), FROZEN for the

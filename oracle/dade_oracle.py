@@ -860,7 +860,9 @@ def graph_search(index, Q, K, ef, delta_d, alpha, log=False):
     (prune iff m1_d·P_d + β'_d > τ at d = Δd, 2Δd, …); a survivor's exact
     distance P_D enters C and W (in (dist, id) order) if |W| < ef or it is below max W; W keeps its
     ef best. Returns the first K of W (ids, dists) and counters. α = 0: no pruning (plain HNSW
-    refinement). index: build_index(...) over the rows in id order plus "nbrs", "entry"."""
+    refinement). index: build_index(...) over the rows in id order plus "nbrs", "entry". The
+    entry point (R33): with an IVF (nlist > 1) the lowest-id node of the query's nearest non-empty
+    list — the coarse quantizer stands in for HNSW's upper layers — else index["entry"]."""
     Q = np.atleast_2d(Q)
     D = Q.shape[1]
     ns = D // delta_d
@@ -874,9 +876,15 @@ def graph_search(index, Q, K, ef, delta_d, alpha, log=False):
     out_i = np.full((Q.shape[0], K), -1, np.int64); out_d = np.full((Q.shape[0], K), np.inf)
     st = {"tested": 0, "dims_scanned": 0, "survivors": 0, "expansions": 0,
           "pruned_at_step": np.zeros(ns, np.int64), "candidates": []}
+    nlist = len(index["off"]) - 1
     for qn in range(Q.shape[0]):
         q = Qr[qn]
         e0 = index["entry"]
+        if nlist > 1:  # R33: the entry is the lowest-id node of the query's nearest non-empty IVF list
+            for l in probe(Q[qn], index["centroids"], min(nlist, 8)):
+                if index["off"][l + 1] > index["off"][l]:
+                    e0 = int(index["row_id"][index["off"][l]])
+                    break
         d0 = float(np.sum((Xr[e0 - base] - q) ** 2))
         visited = {e0}
         W = [(d0, e0)]

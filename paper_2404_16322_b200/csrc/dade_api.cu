@@ -2497,6 +2497,13 @@ extern "C" dade_status dade_graph_search(dade_index* x, const float* Q, int nq, 
   x->qrot.reserve((size_t)nq * D);
   launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
   GraphParams p{};
+  if (x->nlist > 1) {  // R33: entry = first row of the query's nearest non-empty list (exact probes)
+    p.eprobe = std::min(x->nlist, 8);
+    x->probes.reserve((size_t)nq * p.eprobe);
+    exact_knn(x, Q, nq, x->cent.p, x->nlist, p.eprobe, x->probes.p, nullptr, x->cent_tc, false, probe_passes(x));
+    p.eprobes = x->probes.p;
+    p.off = x->off_d.p;
+  }
   p.qrot = x->qrot.p; p.layout = x->layout.p; p.row_id = x->row_id_d.p; p.adj = x->g_adj.p; p.n = x->n;
   p.D = D; p.nq = nq; p.K = K; p.ef = ef; p.M0 = x->g_M0; p.entry = x->g_entry;
   p.dd = prune ? delta_d / 16 : 1;

@@ -235,6 +235,11 @@ struct GraphParams {  // one graph search launch (graph.cu)
   const int32_t* adj;       // n x M0 positions (-1 pad)
   int64_t n;
   int D, nq, K, ef, M0, entry, dd, nsteps;
+  // per-query entry (R33): the first row of the query's nearest non-empty list among `eprobe`
+  // probes (null: the index-wide entry)
+  const int32_t* eprobes;
+  int eprobe;
+  const int32_t* off;
   float m1[DADE_MAX_STEPS], beta[DADE_MAX_STEPS];
   int64_t* out_ids;
   float* out_d;

@@ -85,7 +85,13 @@ __global__ void __launch_bounds__(kGW * 32) k_graph_search(const __grid_constant
     int nvis = 1;  // visited positions recorded in vl (beyond vcap the whole bitmap is wiped)
     int wn = 1, ch = 0, cn = 1;  // W holds wn keys; C holds cn entries at [ch, ch + cn)
     if (lane == 0) {  // entry point: exact distance (dims = D)
-      const int e = p.entry;
+      int e = p.entry;
+      if (p.eprobes)
+        for (int j = 0; j < p.eprobe; ++j) {
+          const int l = p.eprobes[q * p.eprobe + j];
+          const int o0 = __ldg(p.off + l), o1 = __ldg(p.off + l + 1);
+          if (o1 > o0) { e = o0; break; }
+        }
       float phi = 0.f;
       for (int b = 0; b < nblk; ++b) phi += block_sq_diff(p.layout + (((int64_t)b * p.n + e) << 4), qs + b * 16);
       const unsigned long long k = gkey(phi, (uint32_t)__ldg(p.row_id + e));

@@ -131,3 +131,26 @@ def test_library_graph_builder_matches_oracle(graph_case):
     gi, gd = iy.graph_search(torch.from_numpy(Q).cuda(), 10, 64, 16, 0.0)[:2]
     bi, _ = O.brute_force_knn(X, Q, 10)
     assert O.recall_at_k(gi.cpu().numpy(), bi, 10) >= 0.95
+
+
+def test_graph_decisions_with_ivf_entry(graph_case):
+    # nlist > 1: the entry point of each query is the lowest-id node of its nearest non-empty list
+    # (R33); the same decisions as the oracle's on the same graph and calibration
+    torch, cfg, X, Xd, ix, oidx, ef = graph_case
+    from paper_2404_16322_b200 import Index
+    cent = O.kmeans(X, 16, iters=2)
+    mean, R, lam = ix.get_rotation()
+    iz = Index(cfg.d)
+    iz.set_rotation(mean, R, lam)
+    iz.build_ivf(Xd, 16, centroids=torch.from_numpy(cent).cuda())
+    iz.set_graph(oidx["nbrs"], oidx["entry"])
+    iz.set_calibration(ef, oidx["cal"]["m1"], oidx["cal"]["v"])
+    o16 = O.build_index(X, cent, mean, R, oidx["cal"])
+    o16["nbrs"], o16["entry"] = oidx["nbrs"], oidx["entry"]
+    Q = synth.queries(cfg)
+    gi, gd, log = iz.graph_search(torch.from_numpy(Q).cuda(), 10, ef, 16, 0.005, log=True)
+    oi, od, ost = O.graph_search(o16, Q, 10, ef, 16, 0.005, log=True)
+    flagged, n_cmp = _graph_decisions(log.cpu().numpy(), ost["candidates"])
+    assert len(flagged) <= 1
+    keep = [q for q in range(Q.shape[0]) if q not in flagged]
+    assert tie_adjusted_overlap(gi.cpu().numpy()[keep], gd.cpu().numpy()[keep], oi[keep], od[keep]) == 1.0
