@@ -372,7 +372,8 @@ def launches_per_search(cfg, world, nprobe):
     k_check_finite, k_rotate; per probe row chunk either the fused path (> 1024 64-column
     groups) k_split_tf32, k_slack, k_probe_tc, k_probe_finish, or the group-minima path
     (> 2^20 centroids) k_split_tf32, k_l2_tc, k_slack, k_select_groups, or the d_hat path
-    k_split_tf32, k_l2_tc | k_dhat_tc, k_slack, k_select_gmin, k_select_small; k_scan;
+    k_split_tf32, k_l2_tc | k_dhat_tc, k_slack, k_select_gmin, k_select_small; the query order
+    (k_lpt_key, k_order_offsets, k_key_scatter); k_scan;
     + k_merge_topk when sharded (each rank probes its block of nq / world queries)."""
     n, k = cfg.nlist, nprobe
     nq = -(-cfg.nq // world)
@@ -389,7 +390,8 @@ def launches_per_search(cfg, world, nprobe):
         chunk = max(128, (1 << 29) // n // 128 * 128)
         chunk = min(chunk, 16384, rows_pad)
         probe = 5 * -(-nq // chunk)
-    return 2 + probe + 1 + (1 if world > 1 else 0)
+    # + 3 kernels of the scan's query order (longest stream first: key, offsets, scatter)
+    return 2 + probe + 3 + 1 + (1 if world > 1 else 0)
 
 
 # ============================================================================ CPU oracle legs

@@ -283,7 +283,7 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 #define DADE_OPT_KNN_PATH 1        /* exact-KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima */
 #define DADE_OPT_PROBE_PASSES 2    /* tf32 passes of the probe filter: 0 auto (1 if D < 512, else 3), 1, 3 */
 #define DADE_OPT_SCAN_WARPS 3      /* warps per query in the scan: 0 auto, 1, 2, 4, 8 */
-#define DADE_OPT_SCAN_ORDER 4      /* 1: scan queries grouped by their nearest probed list */
+#define DADE_OPT_SCAN_ORDER 4      /* scan order: 2 (default) longest candidate stream first, 1 grouped by nearest list, 0 as given */
 #define DADE_OPT_SCAN_TAIL 5       /* X > 0: last X queries in a concurrent 4-warps-per-query scan */
 #define DADE_OPT_HOST_CHUNKS 6     /* dade_search_host: chunks pipelined with the copies (default 1) */
 #define DADE_OPT_HOST_PREP_CHUNKS 7 /* dade_search_host: rotation+probe chunks ahead of one scan (0 auto) */

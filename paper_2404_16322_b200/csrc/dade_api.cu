@@ -30,7 +30,7 @@ struct Options {
   int knn_path = 0;         // exact KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima
   int probe_passes = 0;     // tf32 passes of the probe filter: 0 auto (1 if D < 512 else 3), 1, 3
   int scan_warps = 0;       // warps per query in k_scan: 0 auto, 1, 2, 4, 8
-  int scan_order = 0;       // 1: scan queries grouped by their nearest probed list
+  int scan_order = 2;       // 0: as given, 1: grouped by nearest probed list, 2: longest stream first
   int scan_tail = 0;        // last X queries scanned by a concurrent 4-warps-per-query launch
   int host_chunks = 1;      // dade_search_host: searches pipelined with the copies
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
@@ -462,10 +462,12 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
 // DADE_OPT_SCAN_TAIL = X: the last X queries of a batch are scanned by a concurrent second launch
 // with 4 warps per query. Measured on C2: X = 500 -0.7% (noise), 1,000 +4%, 2,000 +13%; C4 X =
 // 1,000 -0.5% — the one-warp scan is throughput-bound, not tail-bound, so it stays off.
-// DADE_OPT_SCAN_ORDER = 1: the scan takes the queries grouped by nearest probed list
-// (launch_query_order). Off by default — measured: C2 scan unchanged (0.546 ms; ~3,500 queries are
-// in flight at once, so the order barely changes which lists are hot together) and +20 us for the
-// three ordering kernels; C4 scan -3.6% but the step only -1%; C3 no change.
+// DADE_OPT_SCAN_ORDER: the order in which the persistent scan takes the queries (results do not
+// depend on it). 2 (default): longest candidate stream first (a counting sort on the stream length,
+// launch_query_order_lpt) — the last wave of the persistent grid then holds the shortest queries;
+// measured (profiles/r02_scan_order_c{2,4}.jsonl): C4 scan 1.196 -> 1.103 ms, step 1.460 -> 1.384;
+// C2 scan 0.553 -> 0.500, step 0.700 -> 0.664. 1: grouped by nearest probed list (C2 scan unchanged,
+// C4 -3.6%, +20 us of ordering kernels). 0: as given.
 int scan_tail(const dade_index* x, int nq) { return std::max(0, std::min(x->opt.scan_tail, nq)); }
 bool scan_order(const dade_index* x, int nq) { return x->opt.scan_order != 0 && nq > 0; }
 // dade_search_host's rotation + probe chunks when the search itself is not chunked (default 2 for
@@ -559,9 +561,15 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   // the scan's query order (counted with the probe stage, so the scan's events time k_scan alone)
   const int32_t* order = nullptr;
   if (scan_order(x, nq)) {
-    x->ordcnt.reserve((size_t)x->nlist);
     x->order.reserve((size_t)nq);
-    launch_query_order(probes, nq, nprobe, x->nlist, x->ordcnt.p, x->order.p, st);
+    if (x->opt.scan_order == 2) {  // longest candidate stream first
+      x->ordcnt.reserve((size_t)1024 + nq);
+      launch_query_order_lpt(probes, nq, nprobe, x->off_d.p, (int64_t)nprobe * x->n / std::max(1, x->nlist),
+                             x->ordcnt.p, x->order.p, st);
+    } else {
+      x->ordcnt.reserve((size_t)x->nlist);
+      launch_query_order(probes, nq, nprobe, x->nlist, x->ordcnt.p, x->order.p, st);
+    }
     order = x->order.p;
   }
   if (evs) DADE_CK(cudaEventRecord(x->ev[2], st));
@@ -1895,7 +1903,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_KNN_PATH: in({0, 1, 2, 3}); o.knn_path = (int)value; break;
     case DADE_OPT_PROBE_PASSES: in({0, 1, 3}); o.probe_passes = (int)value; break;
     case DADE_OPT_SCAN_WARPS: in({0, 1, 2, 4, 8}); o.scan_warps = (int)value; break;
-    case DADE_OPT_SCAN_ORDER: in({0, 1}); o.scan_order = (int)value; break;
+    case DADE_OPT_SCAN_ORDER: in({0, 1, 2}); o.scan_order = (int)value; break;
     case DADE_OPT_SCAN_TAIL:
       DADE_REQUIRE(value >= 0 && value < ((int64_t)1 << 31), DADE_ERR_ARG, "scan tail out of range");
       o.scan_tail = (int)value; break;

@@ -180,6 +180,9 @@ void launch_scan(const ScanParams& p, cudaStream_t st);
 // tiles). cnt: nlist ints of scratch; order: nq ints.
 void launch_query_order(const int32_t* probes, int nq, int nprobe, int nlist, int* cnt, int32_t* order,
                         cudaStream_t st);
+// the scan's query order, longest candidate stream first (scratch: 1024 + nq ints)
+void launch_query_order_lpt(const int32_t* probes, int nq, int nprobe, const int32_t* off, int64_t avg_stream,
+                            int* scratch, int32_t* order, cudaStream_t st);
 // ‖x~‖² of every list-major row of the blocked layout (fp64 sums, stored fp32)
 void launch_row_norms(const float* layout, int64_t n, int D, float* out, cudaStream_t st);
 // estimate.cu (NEXT-2, Exp-7): top-K by the d-dim estimate over the whole layout; xnorm != null

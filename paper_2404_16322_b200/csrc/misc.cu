@@ -79,6 +79,45 @@ __global__ void k_order_scatter(const int32_t* __restrict__ probes, int nq, int 
     order[atomicAdd(&cur[probes[(int64_t)q * nprobe]], 1)] = q;
 }
 
+// longest candidate stream first (DADE_OPT_SCAN_ORDER = 2): bucket of query q = the length of its
+// stream (sum of its probed lists' sizes) >> shift, buckets in DESCENDING order
+constexpr int kLptBuckets = 1024;
+__global__ void k_lpt_key(const int32_t* __restrict__ probes, int nq, int nprobe, const int32_t* __restrict__ off,
+                          int shift, int* __restrict__ key, int* __restrict__ cnt) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    int64_t L = 0;
+    for (int j = 0; j < nprobe; ++j) {
+      const int l = probes[(int64_t)q * nprobe + j];
+      L += off[l + 1] - off[l];
+    }
+    const int64_t bl = L >> shift;
+    const int b = bl < kLptBuckets - 1 ? (int)bl : kLptBuckets - 1;
+    const int k = kLptBuckets - 1 - b;
+    key[q] = k;
+    atomicAdd(&cnt[k], 1);
+  }
+}
+
+__global__ void k_key_scatter(const int* __restrict__ key, int nq, int* __restrict__ cur, int32_t* __restrict__ order) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x)
+    order[atomicAdd(&cur[key[q]], 1)] = q;
+}
+
+void launch_query_order_lpt(const int32_t* probes, int nq, int nprobe, const int32_t* off, int64_t avg_stream,
+                            int* scratch, int32_t* order, cudaStream_t st) {
+  if (nq <= 0) return;
+  int shift = 0;
+  while ((4 * std::max<int64_t>(avg_stream, 1) >> shift) >= kLptBuckets) ++shift;
+  int* cnt = scratch;               // kLptBuckets
+  int* key = scratch + kLptBuckets; // nq
+  DADE_CK(cudaMemsetAsync(cnt, 0, sizeof(int) * kLptBuckets, st));
+  const int g = std::min((nq + 255) / 256, 1184);
+  k_lpt_key<<<g, 256, 0, st>>>(probes, nq, nprobe, off, shift, key, cnt);
+  k_order_offsets<<<1, 1024, 0, st>>>(cnt, kLptBuckets);
+  k_key_scatter<<<g, 256, 0, st>>>(key, nq, cnt, order);
+  DADE_CK(cudaGetLastError());
+}
+
 void launch_query_order(const int32_t* probes, int nq, int nprobe, int nlist, int* cnt, int32_t* order,
                         cudaStream_t st) {
   if (nq <= 0) return;

@@ -198,15 +198,17 @@ def test_search_host_pipeline_chunks(sift_small, chunks, prep):
     assert np.array_equal(a.cpu().numpy(), ih.numpy()) and np.array_equal(b.cpu().numpy(), dh.numpy())
 
 
-def test_scan_query_order_invariance(sift_small):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_scan_query_order_invariance(sift_small, mode):
     """DADE_OPT_SCAN_ORDER = 1 (queries scanned grouped by nearest probed list) returns exactly the
     default order's results and counters: each query's scan depends only on its own stream."""
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     Q = torch.from_numpy(synth.queries(cfg, n=700)).cuda()
+    ix.set_option("scan_order", 0)      # as given
     a, b, sa = ix.search(Q, 10, 8, 16, 0.005, stats=True)
-    ix.set_option("scan_order", 1)
+    ix.set_option("scan_order", mode)   # 1: grouped by nearest list, 2: longest stream first
     c, d, sc = ix.search(Q, 10, 8, 16, 0.005, stats=True)
-    ix.set_option("scan_order", 0)
+    ix.set_option("scan_order", 2)
     assert torch.equal(a, c) and torch.equal(b, d)
     assert sa["tested"] == sc["tested"] and sa["dims_scanned"] == sc["dims_scanned"]
 
@@ -217,10 +219,12 @@ def test_scan_tail_split_invariance(sift_small, tail):
     exactly the single launch's results and counters."""
     cfg, (torch, ix, oidx, X, Xd) = sift_small
     Q = torch.from_numpy(synth.queries(cfg, n=700)).cuda()
+    ix.set_option("scan_order", 0)      # the tail split applies to the as-given order
     a, b, sa = ix.search(Q, 10, 8, 16, 0.005, stats=True)
     ix.set_option("scan_tail", tail)
     c, d, sc = ix.search(Q, 10, 8, 16, 0.005, stats=True)
     ix.set_option("scan_tail", 0)
+    ix.set_option("scan_order", 2)
     assert torch.equal(a, c) and torch.equal(b, d)
     assert sa["tested"] == sc["tested"] and sa["dims_scanned"] == sc["dims_scanned"]
 

@@ -4,7 +4,8 @@ product library) on one workload. The index is built once with the product libra
 (/tmp/dade_exp_<cfg>.idx); every library then loads it in its own subprocess, so all variants
 search the identical layout and calibration.
 
-Usage: python tools/exp_scan.py --config c4 --nprobe 8 LIB[=ENV=V,ENV2=V] ...
+Usage: python tools/exp_scan.py --config c4 --nprobe 8 LIB[=ENV:V,ENV2:V] ...
+(DADE_EXP_OPTS:scan_order:2 sets dade_set_option values in the child)
 Prints one JSON line per library: scan ms (median / min of --reps, L2 flushed), total ms, scan
 rate, recall@10 vs exact IVF at the same nprobe."""
 import argparse
@@ -51,6 +52,9 @@ def child(a, path):
     Q = torch.from_numpy(np.load(path + ".q.npy")).cuda()
     ix = Index(cfg.d)
     ix.load(path)
+    for kv in filter(None, os.environ.get("DADE_EXP_OPTS", "").split(",")):
+        k_, v_ = kv.split(":")
+        ix.set_option(k_, int(v_))
     K, dd = cfg.k, cfg.delta_d
     ei, _ = ix.search(Q, K, a.nprobe, dd, 0.0)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
