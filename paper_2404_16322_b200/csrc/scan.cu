@@ -816,12 +816,15 @@ static size_t scan_smem(int D, int K, int nprobe, int G, int pq_m) {
          (G > 1 ? (size_t)(G + 2) * K * 8 : 0) + 16;
 }
 
-// warps per query: the smallest G giving >= 16 query-warps per SM, and G >= 2 for long candidate
-// streams (>= 4,000 per query) — measured: C3 (1,000 queries) G = 4 1.35 ms, 2 1.41, 1 1.87;
-// C4 (10k queries, ~4,900 candidates each) G = 2 1.19 ms vs 1 1.26; C2 (~2,000) G = 1 0.57 vs
-// 2 0.67; C5 shard (~1,500) G = 1 1.66 vs 2 1.90 — larger groups pay epoch barriers
+// warps per query: the smallest G giving >= 16 query-warps per SM. With the longest-stream-first
+// query order (dade_api.cu) one warp per query is best whenever the batch fills the machine —
+// measured (profiles/r02_scan_warps_c{2,3,4}.jsonl): C4 (10k queries, ~5,400 candidates each)
+// G = 1 0.990 ms vs 2 1.100 vs 4 1.459; C2 G = 1 0.500 vs 2 0.639; C3 (1,000 queries) G = 4 1.338
+// vs 2 1.449, 8 1.728, 1 1.903. (Round 1, without the order, G = 2 won on C4: the second warp
+// mostly shortened the grid's tail, which the order now removes.)
 static int scan_group(int nq, int sms, int64_t avg_stream) {
-  int G = avg_stream >= 4000 ? 2 : 1;
+  (void)avg_stream;
+  int G = 1;
   while (G < 8 && (int64_t)nq * G < (int64_t)sms * 16) G *= 2;
   return G;
 }
