@@ -608,11 +608,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     } else {
       p.pq_beta = -INFINITY;
     }
-    // gather rounds: enough lanes per survivor to load all of its blocks in one round trip
-    const int la = 2;  // the PQ scan loads two blocks per lane (scan.cu launch_k)
-    int lanes = 1;
-    while (lanes < 32 && lanes * la < D / 16) lanes *= 2;
-    p.pq_lg = __builtin_ctz(lanes);
+    p.pq_lg = 0;  // lanes per survivor of the gather rounds: set with the kernel's LA (scan.cu launch_k)
   }
   p.avg_stream = (int64_t)nprobe * x->n / std::max(1, x->nlist);
   for (int s = 1; s < p.nsteps; ++s) {

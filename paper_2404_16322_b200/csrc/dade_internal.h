@@ -51,6 +51,16 @@ struct DBuf {
 };
 
 constexpr int kBlk = 16;  // layout block width B_L (dims per 64-B row)
+#ifndef DADE_SCAN_PQ_LA  // BSA-q gather rounds: blocks per lane; 0 = chosen per D (scan.cu launch_k)
+#define DADE_SCAN_PQ_LA 0
+#endif
+// lanes per survivor in a BSA-q gather round of LA blocks per lane: the fewest (a power of two,
+// at most 32) that cover all nblk blocks in one round trip
+inline int pq_gather_lanes(int nblk, int la) {
+  int lanes = 1;
+  while (lanes < 32 && lanes * la < nblk) lanes *= 2;
+  return lanes;
+}
 
 // --------------------------------------------------------------------- kernel launchers
 // exact.cu : fp32 tile distances + fp64-certified selection (assign / probe / KNN)

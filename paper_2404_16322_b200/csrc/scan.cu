@@ -862,8 +862,23 @@ static void launch_v(const ScanParams& p, cudaStream_t st) {
 template <int DD, int KPL>
 static void launch_k(const ScanParams& p, cudaStream_t st) {
   if (p.pq) {  // BSA-q (NEXT-3): ADC test in stage 1, exact distance of the survivors
-    // two blocks per lane: a survivor's exact distance takes nblk / 2 lanes, one round trip
-    launch_v<DD, KPL, 2, 128, false, true>(p, st);
+    // LA blocks per lane, 2^pq_lg lanes per survivor: the fewest lanes that load a survivor's
+    // nblk blocks in one round trip, LA = 4 only where that saves lanes over LA = 3 and the
+    // top-K leaves the registers for it (KPL >= 4 spills at LA = 4). Measured C4 (D = 96, 6
+    // blocks) scan 5.07 / 4.15 / 4.67 ms at LA 2 / 3 / 4, C2 (D = 128, 8 blocks) 5.10 / 5.10 /
+    // 3.98 ms (profiles/r02_pq_la.jsonl)
+    ScanParams q = p;
+    const int nblk = p.D / kBlk, l3 = pq_gather_lanes(nblk, 3), l4 = pq_gather_lanes(nblk, 4);
+    if constexpr (KPL <= 2 && DADE_SCAN_PQ_LA == 0) {
+      if (l4 < l3) {
+        q.pq_lg = __builtin_ctz(l4);
+        launch_v<DD, KPL, 4, 128, false, true>(q, st);
+        return;
+      }
+    }
+    constexpr int kLA = DADE_SCAN_PQ_LA > 0 ? DADE_SCAN_PQ_LA : 3;
+    q.pq_lg = __builtin_ctz(pq_gather_lanes(nblk, kLA));
+    launch_v<DD, KPL, kLA, 128, false, true>(q, st);
     return;
   }
   if (p.residual) {  // BSA-res (NEXT-1): residual-norm test
