@@ -48,6 +48,8 @@ struct dade_index {
   bool has_lam = false;  // eigenvalues known (fit_rotation, or given to set_rotation): BSA-res needs them
   std::vector<double> mean, R, lam;
   DBuf<double> R_d, mean_d;
+  RotOp rot_op;              // R split for the tensor-core rotation (rotate.cu)
+  RotWs rot_ws, rot_ws_side;  // slice scratch: main stream / side stream (query rotation ∥ probe)
   // IVF + layout (a1, a2)
   bool has_ivf = false;
   int nlist = 0;
@@ -347,6 +349,7 @@ void upload_rotation(dade_index* x) {
   x->mean_d.reserve(D);
   DADE_CK(cudaMemcpyAsync(x->R_d.p, x->R.data(), sizeof(double) * D * D, cudaMemcpyHostToDevice, x->stream));
   DADE_CK(cudaMemcpyAsync(x->mean_d.p, x->mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice, x->stream));
+  rot_prepare(x->rot_op, x->R_d.p, D, x->stream);  // R's slices for the tensor-core rotation
   DADE_CK(cudaStreamSynchronize(x->stream));
   x->has_rot = true;
 }
@@ -438,7 +441,7 @@ void prepare(dade_index* x, const float* Q, int nq, int nprobe, float* qrot, int
   DADE_CK(cudaEventRecord(x->fork, st));
   DADE_CK(cudaStreamWaitEvent(x->side, x->fork, 0));
   launch_check_finite(Q, (int64_t)nq * D, x->flag.p, x->side, 3);
-  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, qrot, nullptr, x->side);
+  launch_rotate(x->rot_op, x->rot_ws_side, Q, nullptr, nq, x->mean_d.p, qrot, nullptr, x->side);
   if (stats) DADE_CK(cudaEventRecord(x->ev[1], x->side));
   DADE_CK(cudaEventRecord(x->join, x->side));
   if (x->nlist == 1) {
@@ -840,6 +843,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   DeviceGuard g(x->device);
   cudaStreamSynchronize(x->stream);
   x->R_d.release(); x->mean_d.release(); x->cent.release(); x->layout.release();
+  x->rot_op.release(); x->rot_ws.release(); x->rot_ws_side.release();
   x->off_d.release(); x->row_id_d.release(); x->qrot.release(); x->dmat.release();
   x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
   x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->dlog_n.release(); x->ids_tmp.release(); x->ordcnt.release(); x->order.release(); x->xnorm.release(); x->qconst.release(); x->lam_d.release();
@@ -1101,7 +1105,7 @@ extern "C" dade_status dade_build_ivf(dade_index* x, const float* X, int64_t n, 
   DADE_CK(cudaMemcpyAsync(off_d.p, off32.data(), sizeof(int32_t) * (nlist + 1), cudaMemcpyHostToDevice, st));
   DADE_CK(cudaMemcpyAsync(rid_d.p, rid32.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
   DADE_CK(cudaMemcpyAsync(src_d.p, src.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-  launch_rotate(X, src_d.p, n, D, x->R_d.p, x->mean_d.p, nullptr, layout.p, st);
+  launch_rotate(x->rot_op, x->rot_ws, X, src_d.p, n, x->mean_d.p, nullptr, layout.p, st);
   DADE_CK(cudaStreamSynchronize(st));
   src_d.release();
   // commit (state unchanged on any earlier error)
@@ -1314,7 +1318,7 @@ void pair_features(dade_index* x, const float* Qc, int nq, int npairs, const int
   cudaStream_t st = x->stream;
   DBuf<float> qr;
   qr.reserve((size_t)nq * D);
-  launch_rotate(Qc, nullptr, nq, D, x->R_d.p, x->mean_d.p, qr.p, nullptr, st);
+  launch_rotate(x->rot_op, x->rot_ws, Qc, nullptr, nq, x->mean_d.p, qr.p, nullptr, st);
   DBuf<int32_t> pq_d, pr_d;
   DBuf<double> feat;
   pq_d.reserve(m); pr_d.reserve(m); feat.reserve((size_t)m * nblk);
@@ -1673,7 +1677,7 @@ extern "C" dade_status dade_estimate_knn(dade_index* x, const float* Q, int nq, 
   cudaStream_t st = x->stream;
   check_finite(x, Q, (int64_t)nq * D, "Q");
   x->qrot.reserve((size_t)nq * D);
-  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
+  launch_rotate(x->rot_op, x->rot_ws, Q, nullptr, nq, x->mean_d.p, x->qrot.p, nullptr, st);
   if (method == DADE_EST_RESIDUAL && !x->xnorm_ok) {
     x->xnorm.reserve((size_t)std::max<int64_t>(x->n, 1));
     launch_row_norms(x->layout.p, x->n, D, x->xnorm.p, st);
@@ -2123,6 +2127,8 @@ extern "C" dade_status dade_train_pq(dade_index* x, const float* X, int64_t n, i
   DBuf<float> Xs, Z, Cd;
   DBuf<double> mu_d, R_d, M_d;
   DBuf<uint8_t> codes;
+  RotOp rop;
+  RotWs rws;
   sid_d.reserve(ns); Xs.reserve((size_t)ns * D); Z.reserve((size_t)ns * D); Cd.reserve((size_t)D * 256);
   mu_d.reserve(D); R_d.reserve((size_t)D * D); M_d.reserve((size_t)D * D); codes.reserve((size_t)ns * m);
   DADE_CK(cudaMemcpyAsync(sid_d.p, sid.data(), 4 * ns, cudaMemcpyHostToDevice, st));
@@ -2143,7 +2149,8 @@ extern "C" dade_status dade_train_pq(dade_index* x, const float* X, int64_t n, i
   bool have_C = false;
   auto rotate_sample = [&]() {
     DADE_CK(cudaMemcpyAsync(R_d.p, R.data(), 8 * R.size(), cudaMemcpyHostToDevice, st));
-    launch_rotate(Xs.p, nullptr, ns, D, R_d.p, mu_d.p, Z.p, nullptr, st);
+    rot_prepare(rop, R_d.p, D, st);
+    launch_rotate(rop, rws, Xs.p, nullptr, ns, mu_d.p, Z.p, nullptr, st);
     DADE_CK(cudaMemcpyAsync(Zh.data(), Z.p, 4 * Zh.size(), cudaMemcpyDeviceToHost, st));
     DADE_CK(cudaStreamSynchronize(st));
     if (!have_C) {  // init: the first 256 sampled rows' sub-vectors (R28)
@@ -2294,7 +2301,7 @@ extern "C" dade_status dade_calibrate_pq(dade_index* x, const float* X, const fl
   DBuf<int32_t> pq_d, pr_d;
   DBuf<double> feat;
   qr.reserve((size_t)nq * D); pq_d.reserve(np); pr_d.reserve(np); feat.reserve((size_t)2 * np);
-  launch_rotate(Qc, nullptr, nq, D, x->R_d.p, x->mean_d.p, qr.p, nullptr, st);
+  launch_rotate(x->rot_op, x->rot_ws, Qc, nullptr, nq, x->mean_d.p, qr.p, nullptr, st);
   DADE_CK(cudaMemcpyAsync(pq_d.p, pq.data(), 4 * np, cudaMemcpyHostToDevice, st));
   DADE_CK(cudaMemcpyAsync(pr_d.p, prow.data(), 4 * np, cudaMemcpyHostToDevice, st));
   launch_pq_pair_feat(x->pq_codes.p, x->pq_stride, x->pq_eo, x->pq_m, D, x->pq_Cd.p, qr.p, pq_d.p, pr_d.p, np,
@@ -2499,7 +2506,7 @@ extern "C" dade_status dade_graph_search(dade_index* x, const float* Q, int nq, 
   cudaStream_t st = x->stream;
   check_finite(x, Q, (int64_t)nq * D, "Q");
   x->qrot.reserve((size_t)nq * D);
-  launch_rotate(Q, nullptr, nq, D, x->R_d.p, x->mean_d.p, x->qrot.p, nullptr, st);
+  launch_rotate(x->rot_op, x->rot_ws, Q, nullptr, nq, x->mean_d.p, x->qrot.p, nullptr, st);
   GraphParams p{};
   if (x->nlist > 1) {  // R33: entry = first row of the query's nearest non-empty list (exact probes)
     p.eprobe = std::min(x->nlist, 8);

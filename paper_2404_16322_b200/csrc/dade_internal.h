@@ -34,6 +34,19 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr; o.cap = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; cap = o.cap;
+      o.p = nullptr; o.cap = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }  // scoped scratch (e.g. inside dade_train_pq) is freed on every exit path
   void reserve(size_t n) {
     if (n <= cap) return;
     if (p) cudaFree(p);
@@ -120,10 +133,25 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
                      int32_t* out_idx, double* out_d64, cudaStream_t st, int passes = 3);
 void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st);
 
-// rotate.cu : x~ = R (x - mu) with fp64 accumulation, stored fp32.
-//  rowmajor_out != null: out[p*D + i]; else blocked layout out[(b*n_out + p)*16 + i%16].
+// rotate.cu : x~ = R (x - mu) on the tensor cores (tcgen05 kind::i8, kRotSlices-way split with
+// exact int32 levels combined in fp64), stored fp32.
+//  rowmajor_out != null: out[p*D + i]; blocked_out != null: out[(b*n_out + p)*16 + i%16].
 //  src_rows != null: input row of output p is X[src_rows[p]] (gather) else X[p].
-void launch_rotate(const float* X, const int32_t* src_rows, int64_t n_out, int D, const double* R,
+constexpr int kRotSlices = 6;
+constexpr int kRotMaxD = 16384;
+struct RotOp {  // R's rows, split (rot_prepare; once per rotation)
+  DBuf<int8_t> bs;
+  DBuf<int32_t> be;
+  int D = 0;
+  void release() { bs.release(); be.release(); D = 0; }
+};
+struct RotWs {  // slice scratch of the rotated rows (one per stream that rotates)
+  DBuf<int8_t> as;
+  DBuf<int32_t> ae;
+  void release() { as.release(); ae.release(); }
+};
+void rot_prepare(RotOp& op, const double* R, int D, cudaStream_t st);
+void launch_rotate(const RotOp& op, RotWs& ws, const float* X, const int32_t* src_rows, int64_t n_out,
                    const double* mu, float* rowmajor_out, float* blocked_out, cudaStream_t st);
 
 // pca.cu : strided-sample moments in fp64

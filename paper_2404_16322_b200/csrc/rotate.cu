@@ -1,156 +1,379 @@
-// Rotation x~ = R(x - mu) (centring P:L305) with fp64 accumulation, stored fp32.
-// Database rows are written straight into the dimension-blocked, list-major layout (a1):
-// block b = dims [16b, 16b+16) is an n x 16 fp32 matrix, row p = list-major position p, so one
-// Delta_d = 16 step of one IVF list is one contiguous, 64-B-per-row, 128-bit-vectorisable stream.
+// Rotation x~ = R(x - mu) (centring P:L305) on the 5th-generation tensor cores,
+// stored fp32. Database rows are written straight into the dimension-blocked, list-major layout
+// (a1): block b = dims [16b, 16b+16) is an n x 16 fp32 matrix, row p = list-major position p, so
+// one Delta_d = 16 step of one IVF list is one contiguous, 64-B-per-row, 128-bit stream.
+//
+// The contraction (N x D by D x D) runs as tcgen05.mma kind::i8 in split precision, exact in its
+// integer part (the Ozaki splitting): each row v of the left operand (v = x - mu, formed in fp64)
+// and each row r_i of R is scaled by its own power of two 2^e (max |v| < 2^e) and cut into kS
+// signed 7-bit slices, the base-128 digits of T = trunc(v 2^(7 kS - e)) (|T| < 2^(7 kS)):
+//   v 2^-e = sum_{s=1..kS} A_s 2^(-7s) + w,   A_s in [-127, 127],   |w| < 2^(-7 kS).
+// Then
+//   <v, r_i> ~ 2^(e_v + e_i) sum_{L=2..kS+1} 2^(-7L) P_L,   P_L = sum_{s+t=L} A_s . B_t,
+// where every P_L is an EXACT int32 sum on the tensor cores (|P_L| <= kS D 127^2 < 2^31 for
+// D <= 16,384) in its own TMEM accumulator, and the kS levels are combined in fp64 in the
+// epilogue. The dropped cross terms (s + t > kS + 1) and the remainders bound the error of each
+// output by 9 D 2^(-7 kS) 2^(e_v + e_i) (kS = 6: ~2^-27 max|v| at D = 960 in the worst case; the
+// typical error is ~sqrt(D) times smaller) — below the final fp32 rounding of x~, so the stored
+// layout carries the same ~2^-24 relative error as an fp64 rotation (tests/test_gpu_rotate.py).
+//
+// Level accumulation with one MMA per A slice: R's slices of a 32-dim output tile are stacked
+// as one 192-row B operand (row 32 (t-1) + j = slice t of dim j), and the MMA of A_s with the
+// first 32 (kS + 1 - s) rows of it is issued at TMEM column offset 32 (s - 1): column block
+// L - 2 then receives exactly the pairs s + t = L. kS MMAs per 32-wide K step (N = 192, 160, ...,
+// 32) instead of kS (kS + 1) / 2 small ones.
+//
+// k_rot_slice: 8 rows x 4 16-dim groups per warp pass, so each slice is written as 512
+// contiguous bytes of the UMMA canonical K-major layout (one block per (row tile, 64-B K chunk)).
+// k_rot_i8: persistent, warp-specialised: warp 0 issues the TMA bulk copies (3 stages of 6 x 8 KB
+// of A + 12 KB of B), warp 1 the MMAs, warps 2-9 drain a double-buffered accumulator (2 x 192
+// TMEM columns; 16 columns x 6 levels per warp, one tcgen05.ld wait) while the MMAs fill the
+// other buffer; int32 -> fp64 by the 2^52 + 2^31 bias and one DADD, scaling by one multiply.
+#include <algorithm>
+#include <cstdint>
+
 #include "dade_internal.h"
 
 namespace dade {
 
-// 64 rows x 64 output dims per CTA, 256 threads, 4 x 4 fp64 accumulators per thread.
-__global__ void __launch_bounds__(256) k_rotate(const float* __restrict__ X,
-                                                const int32_t* __restrict__ src_rows,
-                                                int64_t n_out, int D, const double* __restrict__ R,
-                                                const double* __restrict__ mu,
-                                                float* __restrict__ rm_out,
-                                                float* __restrict__ blk_out) {
-  __shared__ double Xs[16][64 + 1];
-  __shared__ double Rs[16][64 + 1];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t p0 = (int64_t)blockIdx.x * 64;
-  const int i0 = blockIdx.y * 64;
-  double acc[4][4] = {};
-  const int lr = threadIdx.x >> 2, lc = (threadIdx.x & 3) * 4;  // 64 rows x 16 cols loader
-  const int64_t p = p0 + lr;
-  const int64_t src = (p < n_out) ? (src_rows ? (int64_t)src_rows[p] : p) : -1;
-  for (int k0 = 0; k0 < D; k0 += 16) {
-    if (src >= 0) {
-      const float4 v = *reinterpret_cast<const float4*>(X + src * D + k0 + lc);
-      Xs[lc + 0][lr] = (double)v.x - mu[k0 + lc + 0];
-      Xs[lc + 1][lr] = (double)v.y - mu[k0 + lc + 1];
-      Xs[lc + 2][lr] = (double)v.z - mu[k0 + lc + 2];
-      Xs[lc + 3][lr] = (double)v.w - mu[k0 + lc + 3];
-    } else {
-      Xs[lc + 0][lr] = Xs[lc + 1][lr] = Xs[lc + 2][lr] = Xs[lc + 3][lr] = 0.0;
-    }
-    const int ri = i0 + lr;  // output dim (row of R)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) Rs[lc + c][lr] = (ri < D) ? R[(int64_t)ri * D + k0 + lc + c] : 0.0;
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      double xv[4], rv[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) { xv[a] = Xs[k][ty * 4 + a]; rv[a] = Rs[k][tx * 4 + a]; }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(xv[a], rv[b], acc[a][b]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int64_t pp = p0 + ty * 4 + a;
-    if (pp >= n_out) continue;
-    const int i = i0 + tx * 4;
-    if (i >= D) continue;
-    const float4 v = make_float4((float)acc[a][0], (float)acc[a][1], (float)acc[a][2],
-                                 (float)acc[a][3]);
-    if (rm_out) *reinterpret_cast<float4*>(rm_out + pp * D + i) = v;
-    if (blk_out)
-      *reinterpret_cast<float4*>(blk_out + (((int64_t)(i >> 4) * n_out + pp) << 4) + (i & 15)) = v;
-  }
-}
+namespace {
+constexpr int kS = kRotSlices;            // slices per operand
+constexpr int kTM = 128;                  // rows per tile (UMMA M)
+constexpr int kTN = 32;                   // output dims per tile
+constexpr int kBN = kS * kTN;             // stacked B rows (192)
+constexpr int kKB = 64;                   // K bytes (int8 elements) per chunk
+constexpr int kABlk = kTM * kKB;          // 8 KB: one slice of one (row tile, chunk)
+constexpr int kBBlk = kBN * kKB;          // 12 KB: all slices of one (dim tile, chunk)
+constexpr int kStage = kS * kABlk + kBBlk;  // 60 KB
+constexpr int kStages = 3;
+constexpr int kAccCols = kS * kTN;        // 192 TMEM columns per accumulator buffer
+constexpr int kRowChunk = 1 << 20;        // rows sliced per pass (bounds the slice scratch)
 
-// 128 rows x 64 output dims per CTA, 128 threads, 8 x 8 fp64 accumulators per thread: each k
-// step reads 8 + 8 doubles with 128-bit shared loads for 64 DFMA (4x the FMA:load ratio of the
-// 4 x 4 tile above). D is a multiple of 16, so output dims never straddle a 16-dim block.
-__global__ void __launch_bounds__(128) k_rotate8(const float* __restrict__ X, const int32_t* __restrict__ src_rows,
-                                                 int64_t n_out, int D, const double* __restrict__ R,
-                                                 const double* __restrict__ mu, float* __restrict__ rm_out,
-                                                 float* __restrict__ blk_out) {
-  __shared__ __align__(16) double Xs[16][128];
-  __shared__ __align__(16) double Rs[16][64];
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;  // 8 column groups x 16 row groups
-  const int64_t p0 = (int64_t)blockIdx.x * 128;
-  const int i0 = blockIdx.y * 64;
-  double acc[8][8];
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// canonical K-major no-swizzle offset of byte kb of row rr inside a (rows x 64 B) block:
+// core matrix = 8 rows x 16 B (128 B contiguous), LBO (K direction) = 128 B, SBO (8-row groups) = 512 B
+__device__ __forceinline__ int canon_off(int rr, int kb) { return (rr >> 3) * 512 + (kb >> 4) * 128 + (rr & 7) * 16; }
+
+// Slices of rows [0, rows_pad) of one pass. A mode (B = false): row r is input row
+// src_rows ? src_rows[p0 + r] : p0 + r of the fp32 X, centred by the fp64 mu; slice s goes to
+// block ((r / 128) nkc + kc) kS + s, row r % 128. B mode: row r is R's row r (fp64); slice s goes
+// to block (r / 32) nkc + kc, row 32 s + r % 32. Rows >= rows and dims >= D are 0.
+// Lane = (row % 8) + 8 (16-dim group % 4): 8 rows x 64 dims per warp pass.
+template <typename T, bool B>
+__global__ void __launch_bounds__(256) k_rot_slice(const T* __restrict__ X, const int32_t* __restrict__ src_rows,
+                                                   int64_t p0, int64_t rows, int64_t rows_pad, int D, int nkc,
+                                                   const double* __restrict__ mu, int8_t* __restrict__ out,
+                                                   int32_t* __restrict__ expo) {
+  const int lane = threadIdx.x & 31, r8 = lane & 7, g4 = lane >> 3;
+  const int64_t r = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8 + r8;
+  if (r - r8 >= rows_pad) return;  // whole warp out of range
+  const bool live = r < rows;
+  const int64_t src = live ? (src_rows ? (int64_t)src_rows[p0 + r] : p0 + r) : 0;
+  const T* xr = X + src * D;
+  auto load16 = [&](int k0, double* v) {  // dims [k0, k0 + 16) of the row, centred, 0 outside
+    if (!live || k0 >= D) {
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-  for (int k0 = 0; k0 < D; k0 += 16) {
-    // X tile: 128 rows x 16 dims (one row per thread, four float4 loads), centred in fp64
-    {
-      const int64_t p = p0 + threadIdx.x;
-      const int64_t src = (p < n_out) ? (src_rows ? (int64_t)src_rows[p] : p) : -1;
+      for (int j = 0; j < 16; ++j) v[j] = 0.0;
+      return;
+    }
+    if constexpr (sizeof(T) == 4) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (src >= 0) v = *reinterpret_cast<const float4*>(X + src * D + k0 + c * 4);
-        const int kk = c * 4;
-        Xs[kk + 0][threadIdx.x] = src >= 0 ? (double)v.x - mu[k0 + kk + 0] : 0.0;
-        Xs[kk + 1][threadIdx.x] = src >= 0 ? (double)v.y - mu[k0 + kk + 1] : 0.0;
-        Xs[kk + 2][threadIdx.x] = src >= 0 ? (double)v.z - mu[k0 + kk + 2] : 0.0;
-        Xs[kk + 3][threadIdx.x] = src >= 0 ? (double)v.w - mu[k0 + kk + 3] : 0.0;
+        const float4 f = *reinterpret_cast<const float4*>(xr + k0 + 4 * c);
+        v[4 * c] = f.x; v[4 * c + 1] = f.y; v[4 * c + 2] = f.z; v[4 * c + 3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 f = *reinterpret_cast<const double2*>(xr + k0 + 2 * c);
+        v[2 * c] = f.x; v[2 * c + 1] = f.y;
       }
     }
-    // R tile: 64 output dims x 16 input dims (8 doubles per thread)
+    if (mu) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int idx = threadIdx.x * 8 + e;  // 0..1023
-      const int r = idx >> 4, kk = idx & 15;
-      Rs[kk][r] = (i0 + r < D) ? R[(int64_t)(i0 + r) * D + k0 + kk] : 0.0;
+      for (int j = 0; j < 16; ++j) v[j] -= __ldg(mu + k0 + j);
     }
-    __syncthreads();
+  };
+  // pass 1: max |v| over the row (the 4 lanes of a row split its groups)
+  double mx = 0.0;
+  for (int kc = 0; kc < nkc; ++kc) {
+    double v[16];
+    load16(kc * kKB + g4 * 16, v);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      double xv[8], rv[8];
-#pragma unroll
-      for (int a = 0; a < 8; a += 2) {
-        const double2 t = *reinterpret_cast<const double2*>(&Xs[k][ty * 8 + a]);
-        xv[a] = t.x; xv[a + 1] = t.y;
-        const double2 u = *reinterpret_cast<const double2*>(&Rs[k][tx * 8 + a]);
-        rv[a] = u.x; rv[a + 1] = u.y;
-      }
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = fma(xv[a], rv[b], acc[a][b]);
-    }
-    __syncthreads();
+    for (int j = 0; j < 16; ++j) mx = fmax(mx, fabs(v[j]));
   }
-  const int i = i0 + tx * 8;
-  if (i >= D) return;
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): max |v| < 2^e
+  if (g4 == 0 && r < rows_pad) expo[r] = live ? e : 0;
+  // pass 2: digits of T = trunc(v 2^(7 kS - e)), 16 B per (lane, slice)
+  const int64_t tile = B ? r / kTN : r / kTM;
+  const int rr = (int)(B ? r % kTN : r % kTM);
+  for (int kc = 0; kc < nkc; ++kc) {
+    double v[16];
+    load16(kc * kKB + g4 * 16, v);
+    uint32_t pk[kS][4];
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int64_t pp = p0 + ty * 8 + a;
-    if (pp >= n_out) continue;
-    const float4 v0 = make_float4((float)acc[a][0], (float)acc[a][1], (float)acc[a][2], (float)acc[a][3]);
-    const float4 v1 = make_float4((float)acc[a][4], (float)acc[a][5], (float)acc[a][6], (float)acc[a][7]);
-    if (rm_out) {
-      *reinterpret_cast<float4*>(rm_out + pp * D + i) = v0;
-      *reinterpret_cast<float4*>(rm_out + pp * D + i + 4) = v1;
+    for (int s = 0; s < kS; ++s) pk[s][0] = pk[s][1] = pk[s][2] = pk[s][3] = 0u;
+    // 2^(7 kS - e) as a bit pattern (|v| 2^(7 kS - e) < 2^(7 kS): the product is exact)
+    const int se = min(max(7 * kS - e, -1022), 1023);
+    const double sc = __longlong_as_double((long long)(se + 1023) << 52);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const long long t = __double2ll_rz(v[j] * sc);
+      const unsigned long long m = (unsigned long long)(t < 0 ? -t : t);
+#pragma unroll
+      for (int s = 0; s < kS; ++s) {
+        int d = (int)((m >> (7 * (kS - 1 - s))) & 127u);
+        if (t < 0) d = -d;
+        pk[s][j >> 2] |= ((uint32_t)(uint8_t)(int8_t)d) << ((j & 3) * 8);
+      }
     }
-    if (blk_out) {
-      float* o = blk_out + (((int64_t)(i >> 4) * n_out + pp) << 4) + (i & 15);
-      *reinterpret_cast<float4*>(o) = v0;
-      *reinterpret_cast<float4*>(o + 4) = v1;
+    if (r >= rows_pad) continue;
+#pragma unroll
+    for (int s = 0; s < kS; ++s) {
+      int8_t* dst = B ? out + (tile * nkc + kc) * (int64_t)kBBlk + canon_off(s * kTN + rr, g4 * 16)
+                      : out + ((tile * nkc + kc) * kS + s) * (int64_t)kABlk + canon_off(rr, g4 * 16);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
     }
   }
 }
 
-void launch_rotate(const float* X, const int32_t* src_rows, int64_t n_out, int D, const double* R,
+__device__ __forceinline__ void mbar_init(uint64_t* b, int c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n}" ::"r"(smem_u32(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ uint64_t umma_desc(const void* smem) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(smem) >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128u >> 4) << 16;  // LBO: next core matrix along K
+  d |= (uint64_t)(512u >> 4) << 32;  // SBO: next 8-row group
+  d |= (uint64_t)1 << 46;            // descriptor version (Blackwell); no swizzle
+  return d;
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+
+#define ROT_TMEM_LD16(taddr, r)                                                                         \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),        \
+                 "=r"(r[15])                                                                                   \
+               : "r"(taddr))
+
+// Tiles t = m * ntn + n (rows [128 m, +128) of the pass x dims [32 n, +32)), CTA c takes
+// t = c, c + grid, ... (consecutive CTAs share an A tile in L2).
+__global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As, const int32_t* __restrict__ ea,
+                                                   const int8_t* __restrict__ Bs, const int32_t* __restrict__ eb,
+                                                   int nkc, int64_t rows, int64_t p0, int64_t n_out, int D,
+                                                   float* __restrict__ rm_out, float* __restrict__ blk_out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStage);
+  uint64_t* empty = full + kStages;
+  uint64_t* accf = empty + kStages;  // [2] accumulator buffer b ready (MMA commit)
+  uint64_t* acce = accf + 2;         // [2] accumulator buffer b drained (256 epilogue threads)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acce + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntn = (D + kTN - 1) / kTN;
+  const int64_t ntm = (rows + kTM - 1) / kTM, ntiles = ntm * ntn;
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&accf[b], 1); mbar_init(&acce[b], 256); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // 2 x 192 accumulator columns -> 512
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer: TMA bulk copies of each tile's K chunks
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t m = t / ntn, n = t % ntn;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % kStages, u = it / kStages;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          unsigned char* st = sm + s * kStage;
+          mbar_expect_tx(&full[s], kStage);
+          bulk_g2s(st, As + (m * nkc + kc) * (int64_t)(kS * kABlk), kS * kABlk, &full[s]);
+          bulk_g2s(st + kS * kABlk, Bs + (n * nkc + kc) * (int64_t)kBBlk, kBBlk, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int it = 0, tl = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        const int b = tl & 1, ub = tl >> 1;
+        if (ub > 0) mbar_wait(&acce[b], (ub - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc0 = tmem + (uint32_t)(b * kAccCols);
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % kStages, u = it / kStages;
+          mbar_wait(&full[s], u & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const unsigned char* st = sm + s * kStage;
+#pragma unroll
+          for (int j = 0; j < kKB / 32; ++j) {  // UMMA_K = 32 for 8-bit operands (32 B of K)
+            const uint64_t bd = umma_desc(st + kS * kABlk + j * 256);
+#pragma unroll
+            for (int sa = 0; sa < kS; ++sa) {
+              // A slice sa+1 against B slices 1 .. kS - sa (N = 32 (kS - sa)) at column 32 sa:
+              // column block L - 2 accumulates the pairs of level L; the sa = 0 MMA of the first
+              // K step covers every block and overwrites
+              const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((kTN * (kS - sa)) >> 3) << 17) |
+                                     ((uint32_t)(kTM >> 4) << 24);
+              mma_i8(acc0 + (uint32_t)(sa * kTN), umma_desc(st + sa * kABlk + j * 256), bd, idesc,
+                     (kc | j) != 0 || sa != 0);
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accf[b]);
+      }
+    }
+  } else {  // epilogue: warps 2..9; TMEM lane quarter warp % 4, columns 16 h .. 16 h + 15
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    int tl = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+      const int b = tl & 1, ub = tl >> 1;
+      const int64_t m = t / ntn;
+      const int n = (int)(t % ntn);
+      const int64_t r = m * kTM + q * 32 + lane;
+      const int e_row = r < rows ? __ldg(ea + r) : 0;
+      const int i0 = n * kTN + h * 16;
+      const int e_col = i0 + (lane & 15) < D ? __ldg(eb + i0 + (lane & 15)) : 0;
+      mbar_wait(&accf[b], ub & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t v[kS][16];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * kAccCols + h * 16);
+#pragma unroll
+      for (int L = 0; L < kS; ++L) ROT_TMEM_LD16(ta + (uint32_t)(L * kTN), v[L]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acce[b]);  // the MMAs may refill this buffer
+      float o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        // sum_L P_L 2^(-7 (L + 2)), smallest terms first; int32 -> double exactly as
+        // (2^52 + 2^31 + P) - (2^52 + 2^31) (one integer op and one DADD)
+        double acc = 0.0;
+#pragma unroll
+        for (int L = kS - 1; L >= 0; --L) {
+          const double d = __hiloint2double(0x43300000, (int)(v[L][j] ^ 0x80000000u)) - 4503601774854144.0;
+          acc = fma(d, 1.0 / (double)(1ull << (7 * (L + 2))), acc);
+        }
+        // times 2^(e_row + e_col): one multiply by the power of two (clamped to the normal
+        // range: beyond it the fp32 result is 0 or inf either way)
+        int E = e_row + __shfl_sync(0xffffffffu, e_col, j);
+        E = E < -1022 ? -1022 : (E > 1023 ? 1023 : E);
+        o[j] = (float)(acc * __longlong_as_double((long long)(E + 1023) << 52));
+      }
+      if (r < rows) {
+        const int64_t p = p0 + r;
+        if (i0 < D) {
+          if (rm_out) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+              *reinterpret_cast<float4*>(rm_out + p * D + i0 + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+          }
+          if (blk_out) {
+            float* dst = blk_out + (((int64_t)(i0 >> 4) * n_out + p) << 4);
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+              *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+int rot_nkc(int D) { return (D + kKB - 1) / kKB; }
+}  // namespace
+
+void rot_prepare(RotOp& op, const double* R, int D, cudaStream_t st) {
+  DADE_REQUIRE(D % 16 == 0 && D >= 16 && D <= kRotMaxD, DADE_ERR_UNSUPPORTED,
+               "rotation: D must be a multiple of 16, <= 16384");
+  const int nkc = rot_nkc(D);
+  const int64_t ntn = (D + kTN - 1) / kTN, rp = ntn * kTN;
+  op.bs.reserve((size_t)ntn * nkc * kBBlk);
+  op.be.reserve((size_t)rp);
+  k_rot_slice<double, true><<<(unsigned)((rp + 63) / 64), 256, 0, st>>>(R, nullptr, 0, D, rp, D, nkc, nullptr, op.bs.p,
+                                                                         op.be.p);
+  DADE_CK(cudaGetLastError());
+  op.D = D;
+}
+
+void launch_rotate(const RotOp& op, RotWs& ws, const float* X, const int32_t* src_rows, int64_t n_out,
                    const double* mu, float* rowmajor_out, float* blocked_out, cudaStream_t st) {
   if (n_out <= 0) return;
-  if (n_out >= 65536) {  // database rotation: enough 128-row tiles to fill the machine
-    dim3 grid((unsigned)((n_out + 127) / 128), (unsigned)((D + 63) / 64));
-    k_rotate8<<<grid, 128, 0, st>>>(X, src_rows, n_out, D, R, mu, rowmajor_out, blocked_out);
-  } else {  // query batches: smaller tiles, more CTAs (measured faster at 10k x 128)
-    dim3 grid((unsigned)((n_out + 63) / 64), (unsigned)((D + 63) / 64));
-    k_rotate<<<grid, 256, 0, st>>>(X, src_rows, n_out, D, R, mu, rowmajor_out, blocked_out);
+  const int D = op.D;
+  DADE_REQUIRE(D > 0, DADE_ERR_STATE, "rotation operand not prepared");
+  const int nkc = rot_nkc(D);
+  const int64_t chunk = std::min<int64_t>(n_out, kRowChunk);
+  const int64_t cpad = (chunk + kTM - 1) / kTM * kTM;
+  ws.as.reserve((size_t)cpad * nkc * kKB * kS);
+  ws.ae.reserve((size_t)cpad);
+  const size_t smem = (size_t)kStages * kStage + 128;
+  int dev = 0, sms = 0;
+  DADE_CK(cudaGetDevice(&dev));
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // set on every launch: the attribute is per device
+  DADE_CK(cudaFuncSetAttribute(k_rot_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t ntn = (D + kTN - 1) / kTN;
+  for (int64_t p0 = 0; p0 < n_out; p0 += chunk) {
+    const int64_t rows = std::min<int64_t>(chunk, n_out - p0);
+    const int64_t rp = (rows + kTM - 1) / kTM * kTM;
+    k_rot_slice<float, false><<<(unsigned)((rp + 63) / 64), 256, 0, st>>>(X, src_rows, p0, rows, rp, D, nkc, mu,
+                                                                          ws.as.p, ws.ae.p);
+    DADE_CK(cudaGetLastError());
+    const int64_t ntiles = rp / kTM * ntn;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
+    k_rot_i8<<<grid, 320, smem, st>>>(ws.as.p, ws.ae.p, op.bs.p, op.be.p, nkc, rows, p0, n_out, D, rowmajor_out,
+                                      blocked_out);
+    DADE_CK(cudaGetLastError());
   }
-  DADE_CK(cudaGetLastError());
 }
 
 }  // namespace dade
