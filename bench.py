@@ -369,7 +369,7 @@ def run_dade(args):
 
 def launches_per_search(cfg, world, nprobe):
     """Kernels of ours per dade_search (mirrors exact_knn's path choice in dade_api.cu):
-    k_check_finite, k_rotate; per probe row chunk either the fused path (> 1024 64-column
+    k_check_finite; k_rot_slice + k_rot_i8 per 2^20 queries (rotate.cu); per probe row chunk either the fused path (> 1024 64-column
     groups) k_split_tf32, k_slack, k_probe_tc, k_probe_finish, or the group-minima path
     (> 2^20 centroids) k_split_tf32, k_l2_tc, k_slack, k_select_groups, or the d_hat path
     k_split_tf32, k_l2_tc | k_dhat_tc, k_slack, k_select_gmin, k_select_small; the query order
@@ -390,8 +390,9 @@ def launches_per_search(cfg, world, nprobe):
         chunk = max(128, (1 << 29) // n // 128 * 128)
         chunk = min(chunk, 16384, rows_pad)
         probe = 5 * -(-nq // chunk)
+    rot = 2 * -(-nq // (1 << 20))
     # + 3 kernels of the scan's query order (longest stream first: key, offsets, scatter)
-    return 2 + probe + 3 + 1 + (1 if world > 1 else 0)
+    return 1 + rot + probe + 3 + 1 + (1 if world > 1 else 0)
 
 
 # ============================================================================ CPU oracle legs

@@ -32,17 +32,17 @@ def test_reference_arm_json_line():
 def test_launch_count_claim():
     import bench
     from datagen import synth
-    # C2 (4,096 lists): check_finite, rotate, split, l2_tc, slack, select_gmin, select_small, the
+    # C2 (4,096 lists): check_finite, rotate (slice + i8 GEMM), split, l2_tc, slack, select_gmin, select_small, the
     # query order (3), scan
-    assert bench.launches_per_search(synth.config("c2"), 1, 8) == 11
+    assert bench.launches_per_search(synth.config("c2"), 1, 8) == 12
     # sharded: + the merge kernel
-    assert bench.launches_per_search(synth.config("c2"), 2, 8) == 12
+    assert bench.launches_per_search(synth.config("c2"), 2, 8) == 13
     # flat (one list): no probe kernels
-    assert bench.launches_per_search(synth.config("c1"), 1, 1) == 6
+    assert bench.launches_per_search(synth.config("c1"), 1, 1) == 7
     # C5 shard (65,536 lists): d_hat path in two row chunks of 8,192
-    assert bench.launches_per_search(synth.config("c5").scaled(n=12_500_000, nlist=65536), 1, 8) == 16
+    assert bench.launches_per_search(synth.config("c5").scaled(n=12_500_000, nlist=65536), 1, 8) == 17
     # C3 (1,000 queries, nprobe 64): one chunk
-    assert bench.launches_per_search(synth.config("c3").scaled(nq=1000), 1, 64) == 11
+    assert bench.launches_per_search(synth.config("c3").scaled(nq=1000), 1, 64) == 12
 
 
 def test_gpus_flag_must_match_world_size():
