@@ -280,7 +280,8 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 /* Tuning options of one index (defaults are the measured best; the alternatives exist for A/B
  * measurement and for tests proving every path returns identical results). Errors: ARG (unknown
  * option or value). */
-#define DADE_OPT_KNN_PATH 1        /* exact-KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima */
+#define DADE_OPT_KNN_PATH 1        /* exact-KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima,
+                                      4 throughput fused filter on fp16 operands, 5 the same on tf32 (probe_fz.cu) */
 #define DADE_OPT_PROBE_PASSES 2    /* tf32 passes of the probe filter: 0 auto (1 if D < 512, else 3), 1, 3 */
 #define DADE_OPT_SCAN_WARPS 3      /* warps per query in the scan: 0 auto, 1, 2, 4, 8 */
 #define DADE_OPT_SCAN_ORDER 4      /* scan order: 2 (default) longest candidate stream first, 1 grouped by nearest list, 0 as given */
@@ -289,6 +290,11 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 #define DADE_OPT_HOST_PREP_CHUNKS 7 /* dade_search_host: rotation+probe chunks ahead of one scan (0 auto) */
 #define DADE_OPT_DHAT_ARES 8       /* 1: A-resident d_hat writer for very wide probe rows */
 #define DADE_OPT_SHARD_EXCHANGES 9 /* collective search: top-K exchanges after epochs 0..E-1 (R32; default 2, 0 = none) */
+#define DADE_OPT_FZ_STAGES 10      /* fused probe filter (knn_path 4/5): B ring stages (0 auto) */
+#define DADE_OPT_FZ_GROUPS 11      /* fused probe filter: epilogue groups of 4 warps (0 auto, 1, 2) */
+#define DADE_OPT_FZ_DEBUG 13       /* measurement only: 1/2 add a pipeline-only launch of the fused filter */
+#define DADE_OPT_FZ_CPC 14         /* fused probe filter: 8 KB operand chunks per TMA copy (0 auto) */
+#define DADE_OPT_FZ_CPS 12         /* fused probe filter: persistent CTAs per SM (0 auto = 1, 2 with 1 group) */
 dade_status dade_set_option(dade_index* idx, int option, int64_t value);
 
 /* Exact probes (a5 alone): probes[nq*nprobe] int32 device, ordered by (exact fp64 dist, id). */

@@ -12,6 +12,7 @@
 
 #include "dade_internal.h"
 
+namespace dade { extern int g_fz_debug; }
 using namespace dade;
 
 // A matrix pre-split for the tensor-core distance filter (gemm_tf32.cu): tf32 hi/lo parts in the
@@ -19,15 +20,25 @@ using namespace dade;
 struct TcOp {
   DBuf<float> hi, lo, norm, maxn, center;
   DBuf<double> csum;
+  DBuf<uint16_t> h16;  // fp16 operand (probe_fz.cu), K-major tiles of 32 halves per row per chunk
+  DBuf<float> hinv;    // per-row 1 / scale of the fp16 operand (A side)
   int64_t rows = 0;
   float maxnorm = 0.f;
-  void release() { hi.release(); lo.release(); norm.release(); maxn.release(); center.release(); csum.release(); rows = 0; }
+  float hinv_b = 0.f;  // 1 / matrix scale of the fp16 operand (B side)
+  bool h16_ok = false;
+  void release() {
+    hi.release(); lo.release(); norm.release(); maxn.release(); center.release(); csum.release();
+    h16.release(); hinv.release();
+    rows = 0;
+    h16_ok = false;
+  }
 };
 
 // Tuning options (dade_set_option): every default is the measured best; the others exist for
 // A/B measurement and for the tests that prove each path returns identical results.
 struct Options {
-  int knn_path = 0;         // exact KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima
+  int knn_path = 0;         // exact KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima,
+                            // 4 throughput fused filter on fp16 operands, 5 the same on tf32 hi parts
   int probe_passes = 0;     // tf32 passes of the probe filter: 0 auto (1 if D < 512 else 3), 1, 3
   int scan_warps = 0;       // warps per query in k_scan: 0 auto, 1, 2, 4, 8
   int scan_order = 2;       // 0: as given, 1: grouped by nearest probed list, 2: longest stream first
@@ -36,6 +47,10 @@ struct Options {
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
   int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
   int shard_exchanges = 2;  // collective search: top-K exchanges after epochs 0 .. E-1 (R32)
+  int fz_stages = 0;        // probe_fz.cu: B ring stages (0 auto)
+  int fz_groups = 0;        // probe_fz.cu: epilogue groups of 4 warps (0 auto, 1, 2)
+  int fz_cps = 0;           // probe_fz.cu: persistent CTAs per SM (0 auto = 1; 2 needs 1 group and smem <= 113 KB)
+  int fz_cpc = 0;           // probe_fz.cu: 8 KB operand chunks per TMA copy (0 auto = 1)
 };
 
 struct dade_index {
@@ -64,7 +79,7 @@ struct dade_index {
   int calK = 0, n0 = 0, ncls = 0;
   std::vector<double> m1, v;
   // scratch
-  DBuf<float> qrot, dmat, qbuf, slack, gmin;
+  DBuf<float> qrot, dmat, qbuf, slack, gmin, fzseed;
   TcOp a_tc;  // scratch: query-side operand of the filter GEMM
   DBuf<int32_t> probes, cand, idx32;
   DBuf<double> d64;
@@ -198,6 +213,22 @@ void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_ma
     launch_max_nonneg(op.norm.p, n, op.maxn.p, x->stream);
     DADE_CK(cudaMemcpyAsync(&op.maxnorm, op.maxn.p, sizeof(float), cudaMemcpyDeviceToHost, x->stream));
     DADE_CK(cudaStreamSynchronize(x->stream));
+    // fp16 copy for the throughput probe filter (probe_fz.cu): one power-of-two scale from the
+    // largest centred norm, ||b'||_inf <= sqrt(maxnorm (1 + 2^-20)) < 2^E, s = 2^(14 - E)
+    op.h16_ok = false;
+    if (fz_nkc(D, 1) * 8192 <= 64 * 1024) {
+      int E = 0;
+      const double bnd = std::sqrt((double)op.maxnorm * (1.0 + 9.5367431640625e-07));
+      if (bnd > 0.0) std::frexp(bnd, &E);
+      const int e = std::min(60, 14 - E);
+      if (e >= -60) {
+        const float sc = std::ldexp(1.f, e);
+        op.h16.reserve((size_t)rp * fz_nkc(D, 1) * 4096);
+        launch_split_h16(B, n, D, center, op.h16.p, nullptr, nullptr, sc, x->stream);
+        op.hinv_b = 1.f / sc;
+        op.h16_ok = true;
+      }
+    }
   }
 }
 
@@ -219,6 +250,70 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   // select (> 1024 groups; measured at 16,384 columns: d_hat path 0.31 ms, fused 0.61 ms);
   // DADE_OPT_KNN_PATH forces a path (tests cover each)
   const int path = x->opt.knn_path;
+  // throughput fused filter (probe_fz.cu): the 1-pass probe filter on fp16 (4) or tf32 (5)
+  // operands with the A tile resident in shared memory; where it does not apply (3-pass filters,
+  // k > 64, n < 256, A tiles wider than shared memory) paths 4/5 fall back to the d_hat matrix
+  {
+    const int kind = path == 5 ? 0 : 1;
+    int G = 0, S = 0;
+    // auto: only for very wide rows (> 32,768 columns, the C5 shard's 65,536 lists) — measured
+    // (tools/exp_probe_fz.py): C5 shard 1.42 -> 0.95 ms, but slower than the d_hat path at 4,096
+    // and 16,384 columns (C2, C4), where the d_hat matrix is small
+    int cps = 1;
+    bool fz = passes == 1 && k <= 32 && n >= 256 && (path ? (path == 4 || path == 5) : n > 32768) &&
+              (kind == 0 || bop.h16_ok) && fz_config(D, kind, k, &G, &S, &cps);
+    int cpc = 1;
+    if (fz && (x->opt.fz_groups || x->opt.fz_stages || x->opt.fz_cps || x->opt.fz_cpc)) {  // measurement overrides
+      if (x->opt.fz_groups) G = x->opt.fz_groups;
+      if (x->opt.fz_stages) S = x->opt.fz_stages;
+      if (x->opt.fz_cps) cps = x->opt.fz_cps;
+      if (x->opt.fz_cpc) cpc = x->opt.fz_cpc;
+      DADE_REQUIRE(fz_smem(D, kind, k, G, S, cpc) * cps <= 226 * 1024 && (cps == 1 || G == 1), DADE_ERR_UNSUPPORTED,
+                   "fz options: shared memory or TMEM does not fit");
+    }
+    if (fz) {
+      int sms = 0;
+      DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device));
+      const int64_t chunk = std::min<int64_t>(tc_rows_pad(m), 65536);
+      // persistent: one CTA per SM (at most one per (row tile, column tile) pair)
+      auto ctas = [&](int64_t rows) {
+        return (int)std::min<int64_t>((int64_t)sms * cps, ((rows + 127) / 128) * ((n + 127) / 128));
+      };
+      const int64_t last = m - (m - 1) / chunk * chunk;  // rows of the last chunk
+      const size_t nl = (size_t)G * std::max((size_t)chunk * fz_lists_per_row(chunk, n, ctas(chunk)),
+                                             (size_t)last * fz_lists_per_row(last, n, ctas(last)));
+      const int C = fz_cap(k);
+      x->slack.reserve((size_t)chunk);
+      x->cand.reserve(nl * C * 2 + nl);
+      x->fzseed.reserve(nl * k);
+      for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+        const int64_t mm = std::min(chunk, m - r0);
+        const void* Aop;
+        const float* ainv = nullptr;
+        if (kind == 1) {
+          const int64_t rp = tc_rows_pad(mm);
+          x->a_tc.h16.reserve((size_t)rp * fz_nkc(D, 1) * 4096);
+          x->a_tc.hinv.reserve((size_t)rp);
+          x->a_tc.norm.reserve((size_t)rp);
+          launch_split_h16(A + r0 * D, mm, D, bop.center.p, x->a_tc.h16.p, x->a_tc.norm.p, x->a_tc.hinv.p, 0.f,
+                           x->stream);
+          launch_slack_h16(x->a_tc.norm.p, x->a_tc.hinv.p, mm, bop.maxnorm, bop.hinv_b, D, x->slack.p, x->stream);
+          Aop = x->a_tc.h16.p;
+          ainv = x->a_tc.hinv.p;
+        } else {
+          tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
+          launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream, 1);
+          Aop = x->a_tc.hi.p;
+        }
+        launch_probe_fz(kind, Aop, x->a_tc.norm.p, ainv, mm, kind == 1 ? (const void*)bop.h16.p : (const void*)bop.hi.p,
+                        bop.norm.p, bop.hinv_b, bop.maxnorm, n, D, k, x->slack.p, A + r0 * D, B, x->fzseed.p, x->cand.p,
+                        x->cand.p + nl * C * 2, ctas(mm), fz_lists_per_row(mm, n, ctas(mm)), G, S, cpc, out_idx + r0 * k,
+                        out_d64 ? out_d64 + r0 * k : nullptr, x->stream);
+      }
+      if (sync) check_knn_flag(x);
+      return;
+    }
+  }
   const bool fused = k <= 64 && n >= 256 && (path ? path == 2 : (n + 63) / 64 > 1024);
   if (fused) {
     // fused filter GEMM + candidate tracking (probe_tc.cu): no m x n d_hat matrix
@@ -848,7 +943,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->qbuf.release(); x->probes.release(); x->cand.release(); x->idx32.release();
   x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->dlog_n.release(); x->ids_tmp.release(); x->ordcnt.release(); x->order.release(); x->xnorm.release(); x->qconst.release(); x->lam_d.release();
   x->dists_tmp.release();
-  x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release();
+  x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release(); x->fzseed.release();
   for (auto& e : x->ev)
     if (e) cudaEventDestroy(e);
   if (x->side) {
@@ -1900,7 +1995,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     throw Error(DADE_ERR_ARG, "option value not allowed");
   };
   switch (option) {
-    case DADE_OPT_KNN_PATH: in({0, 1, 2, 3}); o.knn_path = (int)value; break;
+    case DADE_OPT_KNN_PATH: in({0, 1, 2, 3, 4, 5}); o.knn_path = (int)value; break;
     case DADE_OPT_PROBE_PASSES: in({0, 1, 3}); o.probe_passes = (int)value; break;
     case DADE_OPT_SCAN_WARPS: in({0, 1, 2, 4, 8}); o.scan_warps = (int)value; break;
     case DADE_OPT_SCAN_ORDER: in({0, 1, 2}); o.scan_order = (int)value; break;
@@ -1917,6 +2012,13 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_SHARD_EXCHANGES:
       DADE_REQUIRE(value >= 0 && value <= 16, DADE_ERR_ARG, "shard exchanges not in [0, 16]");
       o.shard_exchanges = (int)value; break;
+    case DADE_OPT_FZ_STAGES: DADE_REQUIRE(value >= 0 && value <= 16, DADE_ERR_ARG, "fz stages not in [0, 16]");
+      o.fz_stages = (int)value; break;
+    case DADE_OPT_FZ_GROUPS: in({0, 1, 2}); o.fz_groups = (int)value; break;
+    case DADE_OPT_FZ_CPS: in({0, 1, 2}); o.fz_cps = (int)value; break;
+    case DADE_OPT_FZ_DEBUG: in({0, 1, 2}); g_fz_debug = (int)value; break;
+    case DADE_OPT_FZ_CPC: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz cpc not in [0, 64]");
+      o.fz_cpc = (int)value; break;
     default: throw Error(DADE_ERR_ARG, "unknown option");
   }
   API_END

@@ -132,6 +132,26 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
                      const float* A, const float* B, int32_t* cand, int32_t* ccount, int nsplit,
                      int32_t* out_idx, double* out_d64, cudaStream_t st, int passes = 3);
 void launch_max_nonneg(const float* v, int64_t n, float* out_dev, cudaStream_t st);
+// exact finish of the fused filters: union of nlists candidate lists per row, fp64 re-rank
+void launch_probe_finish(const int32_t* cand, const int32_t* ccount, int nlists, int C, int64_t m, int64_t n, int k,
+                         const float* A, const float* B, int D, const float* slack, int32_t* out_idx, double* out_d64,
+                         cudaStream_t st);
+// probe_fz.cu: throughput fused filter (A tile resident, B ring, 2G TMEM accumulators, skip test)
+// kind 1 = fp16 operands (kind::f16, power-of-two scales), 0 = tf32 hi parts (kind::tf32)
+int fz_nkc(int D, int kind);
+int fz_cap(int k);
+size_t fz_smem(int D, int kind, int k, int G, int S, int cpc);
+bool fz_config(int D, int kind, int k, int* G, int* S, int* cps);
+int fz_lists_per_row(int64_t m, int64_t n, int P);
+// gscale > 0: one matrix scale; else per-row power-of-two scales (inv_scale[r] = 1/s_r, +inf if unbounded)
+void launch_split_h16(const float* X, int64_t rows, int D, const float* center, uint16_t* h, float* norm,
+                      float* inv_scale, float gscale, cudaStream_t st);
+void launch_slack_h16(const float* an, const float* ainv, int64_t m, float bmax, float binv, int D, float* slack,
+                      cudaStream_t st);
+void launch_probe_fz(int kind, const void* Aop, const float* an, const float* ainv, int64_t m, const void* Bop,
+                     const float* bn, float binv, float bmax, int64_t n, int D, int k, const float* slack,
+                     const float* A, const float* B, float* seeds, int32_t* cand, int32_t* ccount, int P, int maxL,
+                     int G, int S, int cpc, int32_t* out_idx, double* out_d64, cudaStream_t st);
 
 // rotate.cu : x~ = R (x - mu) on the tensor cores (tcgen05 kind::i8, kRotSlices-way split with
 // exact int32 levels combined in fp64), stored fp32.

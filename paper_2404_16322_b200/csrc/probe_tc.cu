@@ -15,8 +15,8 @@
 // list of every column with d_hat <= thr(current k-th); a column above the threshold costs one
 // compare. Since t_split >= t (the split sees a subset), thr(t_split) >= thr(t): the union of
 // the splits' lists contains every exact k-nearest column.
-// k_probe_finish: warp per row, exact fp64 distances of the union (candidate rows staged in
-// shared memory so global loads stay coalesced), bitonic sort by (dist, column), first k out.
+// k_probe_finish: warp per row, exact fp64 distances of the union (one candidate per lane, its row
+// streamed with 16-B loads), bitonic sort by (dist, column), first k out.
 // A row whose list overflowed is finished by an exact scan of all n columns (correct, slow).
 #include <cfloat>
 #include <cstdint>
@@ -663,30 +663,36 @@ __device__ __forceinline__ bool cless(double d0, int32_t c0, double d1, int32_t 
 
 constexpr int kFinWarps = 4;
 constexpr int kFinCap = 512;   // candidates per row held at once (running top-k beyond that)
-constexpr int kFinDim = 32;    // dims staged per pass
-constexpr size_t kFinWarpBytes = (size_t)kFinCap * (8 + 4 * 4) + 256 * 4 + 32 * (kFinDim + 1) * 4;
+constexpr size_t kFinWarpBytes = (size_t)kFinCap * (8 + 4 * 4) + 256 * 4;
 
-// exact distances of up to 32 candidate columns (one per lane; c < 0 = none), accumulated
-// sequentially over j = 0..D-1 in fp64 (R20); rows staged through shared memory in 64-dim slices
+// exact distance of one candidate column per lane (c < 0 = none), accumulated sequentially over
+// j = 0..D-1 in fp64 (R20). Each lane streams its own candidate row with 16-B loads (the row is
+// contiguous), so a lane keeps several loads in flight instead of a chain of dependent gathers.
 __device__ __forceinline__ double exact_batch(const float* __restrict__ a, const float* __restrict__ B, int D,
-                                              int32_t c, float* stage, int lane) {
+                                              int32_t c, float* /*stage*/, int /*lane*/) {
   double acc = 0.0;
-  for (int j0 = 0; j0 < D; j0 += kFinDim) {
-    const int w = min(kFinDim, D - j0);
-    for (int i = 0; i < 32; ++i) {  // candidate i's slice, coalesced
-      const int32_t ci = __shfl_sync(0xffffffffu, c, i);
-      if (ci >= 0)
-        for (int jj = lane; jj < w; jj += 32) stage[i * (kFinDim + 1) + jj] = __ldg(B + (int64_t)ci * D + j0 + jj);
+  if (c < 0) return acc;
+  const float* b = B + (int64_t)c * D;
+  if ((D & 3) == 0) {
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll 4
+    for (int j = 0; j < D / 4; ++j) {
+      const float4 y = __ldg(b4 + j), x = __ldg(a4 + j);
+      double t = __dsub_rn((double)x.x, (double)y.x);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)x.y, (double)y.y);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)x.z, (double)y.z);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)x.w, (double)y.w);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
     }
-    __syncwarp();
-    if (c >= 0) {
-      const float* sr = stage + lane * (kFinDim + 1);
-      for (int jj = 0; jj < w; ++jj) {
-        const double t = __dsub_rn((double)a[j0 + jj], (double)sr[jj]);
-        acc = __dadd_rn(acc, __dmul_rn(t, t));
-      }
+  } else {
+    for (int j = 0; j < D; ++j) {
+      const double t = __dsub_rn((double)__ldg(a + j), (double)__ldg(b + j));
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
     }
-    __syncwarp();
   }
   return acc;
 }
@@ -697,7 +703,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
     const float* __restrict__ slack, int32_t* __restrict__ out_idx, double* __restrict__ out_d) {
   extern __shared__ __align__(16) unsigned char fs[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // per-warp region: cd | cc | sel | ucol | udh | hist[256] | stage[32][kFinDim + 1]
+  // per-warp region: cd | cc | sel | ucol | udh | hist[256]
   unsigned char* base = fs + (size_t)w * kFinWarpBytes;
   double* cd = reinterpret_cast<double*>(base);
   int32_t* cc = reinterpret_cast<int32_t*>(cd + kFinCap);
@@ -705,7 +711,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
   int32_t* ucol = sel + kFinCap;
   unsigned* udh = reinterpret_cast<unsigned*>(ucol + kFinCap);
   unsigned* hist = udh + kFinCap;
-  float* stage = reinterpret_cast<float*>(hist + 256);
+  float* stage = nullptr;  // (exact_batch reads candidate rows directly)
   const int64_t row = (int64_t)blockIdx.x * kFinWarps + w;
   if (row >= m) return;
   const float* a = A + row * (int64_t)D;
@@ -901,10 +907,16 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
   k_probe_tc<<<grid, kThreads, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), m, n, tps, k, C, slack, cand,
                                           ccount, passes);
   DADE_CK(cudaGetLastError());
+  launch_probe_finish(cand, ccount, nsplit, C, m, n, k, A, B, D, slack, out_idx, out_d64, st);
+}
+
+void launch_probe_finish(const int32_t* cand, const int32_t* ccount, int nlists, int C, int64_t m, int64_t n, int k,
+                         const float* A, const float* B, int D, const float* slack, int32_t* out_idx, double* out_d64,
+                         cudaStream_t st) {
   const size_t fsm = (size_t)kFinWarps * kFinWarpBytes;
   DADE_CK(cudaFuncSetAttribute(k_probe_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));  // per launch: per device
   k_probe_finish<<<(unsigned)((m + kFinWarps - 1) / kFinWarps), kFinWarps * 32, fsm, st>>>(
-      cand, ccount, nsplit, C, m, n, k, A, B, D, slack, out_idx, out_d64);
+      cand, ccount, nlists, C, m, n, k, A, B, D, slack, out_idx, out_d64);
   DADE_CK(cudaGetLastError());
 }
 

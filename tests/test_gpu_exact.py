@@ -10,10 +10,11 @@ pytestmark = pytest.mark.gpu
 _OPTS = {}  # dade_set_option values applied to every index a test creates
 
 
-@pytest.fixture(autouse=True, params=[1, 2], ids=["dhat-matrix", "fused-filter"])
+@pytest.fixture(autouse=True, params=[1, 2, 4, 5], ids=["dhat-matrix", "fused-filter", "fz-fp16", "fz-tf32"])
 def knn_path(request):
-    # both selection paths: the d_hat-matrix select (exact.cu) and the fused filter GEMM with
-    # in-epilogue candidate tracking (probe_tc.cu); each must be bit-exact
+    # every selection path: the d_hat-matrix select (exact.cu), the fused filter GEMM with
+    # in-epilogue candidate tracking (probe_tc.cu) and the throughput fused filter on fp16 / tf32
+    # operands (probe_fz.cu; 1-pass filters only, the others fall back); each must be bit-exact
     _OPTS.clear()
     _OPTS["knn_path"] = request.param
     yield request.param
