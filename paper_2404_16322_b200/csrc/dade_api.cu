@@ -213,23 +213,28 @@ void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_ma
     launch_max_nonneg(op.norm.p, n, op.maxn.p, x->stream);
     DADE_CK(cudaMemcpyAsync(&op.maxnorm, op.maxn.p, sizeof(float), cudaMemcpyDeviceToHost, x->stream));
     DADE_CK(cudaStreamSynchronize(x->stream));
-    // fp16 copy for the throughput probe filter (probe_fz.cu): one power-of-two scale from the
-    // largest centred norm, ||b'||_inf <= sqrt(maxnorm (1 + 2^-20)) < 2^E, s = 2^(14 - E)
-    op.h16_ok = false;
-    if (fz_nkc(D, 1) * 8192 <= 64 * 1024) {
-      int E = 0;
-      const double bnd = std::sqrt((double)op.maxnorm * (1.0 + 9.5367431640625e-07));
-      if (bnd > 0.0) std::frexp(bnd, &E);
-      const int e = std::min(60, 14 - E);
-      if (e >= -60) {
-        const float sc = std::ldexp(1.f, e);
-        op.h16.reserve((size_t)rp * fz_nkc(D, 1) * 4096);
-        launch_split_h16(B, n, D, center, op.h16.p, nullptr, nullptr, sc, x->stream);
-        op.hinv_b = 1.f / sc;
-        op.h16_ok = true;
-      }
-    }
   }
+  op.h16_ok = false;  // the fp16 copy (probe_fz.cu) is made on first use: tc_prepare_h16
+}
+
+// fp16 copy of a prepared B operand for the fused probe filter (probe_fz.cu), made once per
+// preparation: one power-of-two scale from the largest centred norm, ||b'||_inf <=
+// sqrt(maxnorm (1 + 2^-20)) < 2^E, s = 2^(14 - E). Leaves h16_ok false when the operand is too
+// wide for the kernel or the scale would clamp.
+void tc_prepare_h16(dade_index* x, const float* B, TcOp& op) {
+  if (op.h16_ok) return;
+  const int D = x->D;
+  if (fz_nkc(D, 1) * 8192 > 64 * 1024) return;
+  int E = 0;
+  const double bnd = std::sqrt((double)op.maxnorm * (1.0 + 9.5367431640625e-07));
+  if (bnd > 0.0) std::frexp(bnd, &E);
+  const int e = std::min(60, 14 - E);
+  if (e < -60) return;
+  const float sc = std::ldexp(1.f, e);
+  op.h16.reserve((size_t)tc_rows_pad(op.rows) * fz_nkc(D, 1) * 32);  // 32 halves per row per chunk
+  launch_split_h16(B, op.rows, D, op.center.p, op.h16.p, nullptr, nullptr, sc, x->stream);
+  op.hinv_b = 1.f / sc;
+  op.h16_ok = true;
 }
 
 // Exact k nearest rows of B for every row of A: tensor-core distance filter (tcgen05 kind::tf32,
@@ -256,6 +261,8 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   {
     const int kind = path == 5 ? 0 : 1;
     int G = 0, S = 0;
+    if (kind == 1 && passes == 1 && k <= 32 && n >= 256 && (path ? path == 4 : n > 32768))
+      tc_prepare_h16(x, B, const_cast<TcOp&>(bop));  // the operand cache (cent_tc) gains its fp16 copy
     // auto: only for very wide rows (> 32,768 columns, the C5 shard's 65,536 lists) — measured
     // (tools/exp_probe_fz.py): C5 shard 1.42 -> 0.95 ms, but slower than the d_hat path at 4,096
     // and 16,384 columns (C2, C4), where the d_hat matrix is small
@@ -292,7 +299,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
         const float* ainv = nullptr;
         if (kind == 1) {
           const int64_t rp = tc_rows_pad(mm);
-          x->a_tc.h16.reserve((size_t)rp * fz_nkc(D, 1) * 4096);
+          x->a_tc.h16.reserve((size_t)rp * fz_nkc(D, 1) * 32);  // 32 halves per row per chunk
           x->a_tc.hinv.reserve((size_t)rp);
           x->a_tc.norm.reserve((size_t)rp);
           launch_split_h16(A + r0 * D, mm, D, bop.center.p, x->a_tc.h16.p, x->a_tc.norm.p, x->a_tc.hinv.p, 0.f,
