@@ -2024,6 +2024,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_FZ_GROUPS: in({0, 1, 2}); o.fz_groups = (int)value; break;
     case DADE_OPT_FZ_CPS: in({0, 1, 2}); o.fz_cps = (int)value; break;
     case DADE_OPT_FZ_DEBUG: in({0, 1, 2}); g_fz_debug = (int)value; break;
+    case DADE_OPT_PCA_TC: in({0, 1}); g_pca_tc = (int)value; break;
     case DADE_OPT_FZ_CPC: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz cpc not in [0, 64]");
       o.fz_cpc = (int)value; break;
     default: throw Error(DADE_ERR_ARG, "unknown option");

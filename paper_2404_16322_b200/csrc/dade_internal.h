@@ -181,6 +181,8 @@ void launch_pca_cov(const float* X, int64_t n, int64_t id_base, int64_t n_total,
                     const double* mean_dev, double* cov_dev, double* scratch, int64_t scratch_elems,
                     cudaStream_t st);
 int64_t pca_cov_scratch_elems(int64_t n_owned, int D);
+extern int g_pca_tc;  // 1 (default): covariance on the int8 tensor cores; 0: fp64 CUDA cores
+// rotate.cu: acc[a][b] += sum_k Y[a][k] Y[b][k] (rows x K fp64 Y, K % 64 == 0, K <= 16384, rmax = row max bits)
 
 // calib.cu : per-pair prefix partial distances in fp64 from the fp32 layout
 void launch_pair_prefix(const float* layout, int64_t n_rows, int D, const float* qrot,
@@ -334,4 +336,6 @@ bool logistic_irls_multi(const std::vector<double>& F, int k, const std::vector<
                          std::vector<double>& m_out, double* beta_out);
 uint64_t splitmix64(uint64_t x);
 
+void launch_gram_i8(const double* Y, int rows, int64_t K, const unsigned long long* rmax, RotWs& wa, RotOp& wb,
+                    double* acc, cudaStream_t st);
 }  // namespace dade

@@ -1,5 +1,7 @@
 // fp64 moments of the strided PCA sample (Theorem 1; sample P:L3105 / R17;
 // covariance divisor P:L4074). Deterministic: fixed-order partial sums, no atomics.
+#include <algorithm>
+
 #include "dade_internal.h"
 
 namespace dade {
@@ -18,7 +20,7 @@ __device__ __forceinline__ int64_t sample_row(int64_t k, int64_t n_total, int64_
   return (int64_t)(((__int128)k * n_total) / ns) - id_base;
 }
 
-constexpr int kSumRows = 4096;
+constexpr int kSumRows = 256;  // sample rows per partial (a CTA each; partials added in chunk order)
 
 // partial[c][j] = sum over sample chunk c (kSumRows consecutive k) of x_j, sequential in k
 __global__ void k_pca_sum(const float* __restrict__ X, int64_t klo, int64_t khi, int64_t n_total,
@@ -120,13 +122,75 @@ __global__ void k_mirror(double* __restrict__ cov, int D) {
   }
 }
 
+int g_pca_tc = 1;  // covariance on the int8 tensor cores (Gram mode of rotate.cu); 0: fp64 CUDA cores
+constexpr int64_t kGramK = 16384;  // sample rows per Gram launch (exact int32 levels up to 16,384)
+
+static bool pca_tc(int D) { return g_pca_tc && D % 16 == 0 && D <= kRotMaxD; }
+
 int64_t pca_cov_scratch_elems(int64_t n_owned, int D) {
+  if (pca_tc(D)) return (int64_t)D * std::min<int64_t>(kGramK, (n_owned + 63) / 64 * 64);
   return ((n_owned + kCovRows - 1) / kCovRows) * (int64_t)D * D;
 }
 
+// Yt[a][kk] = x_a - mu_a (fp64) of sampled row kc0 + kk, kk < cnt; 0 for kk in [cnt, K):
+// the transposed, centred sample chunk, 32 x 32 tiles through shared memory
+__global__ void k_cov_gather_t(const float* __restrict__ X, int64_t kc0, int64_t cnt, int64_t K, int64_t n_total,
+                               int64_t ns, int64_t id_base, int D, const double* __restrict__ mu,
+                               double* __restrict__ Yt, unsigned long long* __restrict__ rmax) {
+  __shared__ double t[32][33];
+  const int64_t kb = (int64_t)blockIdx.x * 32;
+  const int ab = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t kk = kb + i;
+    const int a = ab + threadIdx.x;
+    double v = 0.0;
+    if (kk < cnt && a < D) v = (double)X[sample_row(kc0 + kk, n_total, ns, id_base) * D + a] - mu[a];
+    t[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {  // one warp per dim: row maxima for the slices
+    const int a = ab + i;
+    const int64_t kk = kb + threadIdx.x;
+    const double v = t[threadIdx.x][i];
+    if (a < D && kk < K) Yt[(int64_t)a * K + kk] = v;
+    double m = fabs(v);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0 && a < D && m > 0.0) atomicMax(rmax + a, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// Sigma_sum = sum over the rank's sampled rows of (x - mu)(x - mu)^T in fp64. Tensor-core path:
+// chunks of <= 16,384 sampled rows, each transposed and centred in fp64, then one Gram launch on
+// the int8 tensor cores (rotate.cu, exact int32 levels, error bound of R36) accumulating into the
+// fp64 result; the chunk sums are added in chunk order. CUDA-core path (g_pca_tc = 0): fp64 FMA
+// tiles with split-K partials.
 void launch_pca_cov(const float* X, int64_t n, int64_t id_base, int64_t n_total, int64_t ns, int D,
                     const double* mean_dev, double* cov_dev, double* scratch,
                     int64_t scratch_elems, cudaStream_t st) {
+  if (pca_tc(D)) {
+    int64_t klo, khi;
+    owned_k_range(n, id_base, n_total, ns, &klo, &khi);
+    const int64_t cnt = khi > klo ? khi - klo : 0;
+    DADE_CK(cudaMemsetAsync(cov_dev, 0, sizeof(double) * D * D, st));
+    if (cnt == 0) return;
+    RotWs wa;
+    RotOp wb;
+    DBuf<unsigned long long> rmax;
+    rmax.reserve((size_t)D);
+    for (int64_t c0 = 0; c0 < cnt; c0 += kGramK) {
+      const int64_t c = std::min(kGramK, cnt - c0), K = (c + 63) / 64 * 64;
+      DADE_REQUIRE((int64_t)D * K <= scratch_elems, DADE_ERR_OOM, "pca scratch too small");
+      DADE_CK(cudaMemsetAsync(rmax.p, 0, sizeof(unsigned long long) * D, st));
+      dim3 grid((unsigned)(K / 32), (unsigned)((D + 31) / 32));
+      k_cov_gather_t<<<grid, dim3(32, 8), 0, st>>>(X, klo + c0, c, K, n_total, ns, id_base, D, mean_dev, scratch,
+                                                    rmax.p);
+      DADE_CK(cudaGetLastError());
+      launch_gram_i8(scratch, D, K, rmax.p, wa, wb, cov_dev, st);
+    }
+    DADE_CK(cudaStreamSynchronize(st));  // the slice scratch (wa, wb) is freed on return
+    return;
+  }
   int64_t klo, khi;
   owned_k_range(n, id_base, n_total, ns, &klo, &khi);
   const int64_t cnt = khi > klo ? khi - klo : 0;

@@ -64,7 +64,9 @@ template <typename T, bool B>
 __global__ void __launch_bounds__(256) k_rot_slice(const T* __restrict__ X, const int32_t* __restrict__ src_rows,
                                                    int64_t p0, int64_t rows, int64_t rows_pad, int D, int nkc,
                                                    const double* __restrict__ mu, int8_t* __restrict__ out,
-                                                   int32_t* __restrict__ expo) {
+                                                   int32_t* __restrict__ expo,
+                                                   const unsigned long long* __restrict__ rmax = nullptr,
+                                                   int kcpb = 1 << 30) {
   const int lane = threadIdx.x & 31, r8 = lane & 7, g4 = lane >> 3;
   const int64_t r = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8 + r8;
   if (r - r8 >= rows_pad) return;  // whole warp out of range
@@ -95,23 +97,30 @@ __global__ void __launch_bounds__(256) k_rot_slice(const T* __restrict__ X, cons
       for (int j = 0; j < 16; ++j) v[j] -= __ldg(mu + k0 + j);
     }
   };
-  // pass 1: max |v| over the row (the 4 lanes of a row split its groups)
+  // pass 1: max |v| over the row (the 4 lanes of a row split its groups), or the row maxima
+  // given (rmax: bit patterns of non-negative doubles; then blockIdx.y picks chunks
+  // [kcpb y, kcpb (y + 1)) of a long row, so many CTAs share one row)
   double mx = 0.0;
-  for (int kc = 0; kc < nkc; ++kc) {
-    double v[16];
-    load16(kc * kKB + g4 * 16, v);
+  if (rmax) {
+    mx = live ? __longlong_as_double((long long)rmax[r]) : 0.0;
+  } else {
+    for (int kc = 0; kc < nkc; ++kc) {
+      double v[16];
+      load16(kc * kKB + g4 * 16, v);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) mx = fmax(mx, fabs(v[j]));
+      for (int j = 0; j < 16; ++j) mx = fmax(mx, fabs(v[j]));
+    }
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   }
-  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
   int e = 0;
   if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): max |v| < 2^e
-  if (g4 == 0 && r < rows_pad) expo[r] = live ? e : 0;
+  if (blockIdx.y == 0 && g4 == 0 && r < rows_pad) expo[r] = live ? e : 0;
+  const int kcb = (int)min((int64_t)blockIdx.y * kcpb, (int64_t)nkc), kce = (int)min((int64_t)kcb + kcpb, (int64_t)nkc);
   // pass 2: digits of T = trunc(v 2^(7 kS - e)), 16 B per (lane, slice)
   const int64_t tile = B ? r / kTN : r / kTM;
   const int rr = (int)(B ? r % kTN : r % kTM);
-  for (int kc = 0; kc < nkc; ++kc) {
+  for (int kc = kcb; kc < kce; ++kc) {
     double v[16];
     load16(kc * kKB + g4 * 16, v);
     uint32_t pk[kS][4];
@@ -198,7 +207,8 @@ __device__ __forceinline__ void mma_commit(uint64_t* b) {
 __global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As, const int32_t* __restrict__ ea,
                                                    const int8_t* __restrict__ Bs, const int32_t* __restrict__ eb,
                                                    int nkc, int64_t rows, int64_t p0, int64_t n_out, int D,
-                                                   float* __restrict__ rm_out, float* __restrict__ blk_out) {
+                                                   float* __restrict__ rm_out, float* __restrict__ blk_out,
+                                                   double* __restrict__ acc64) {
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStage);
   uint64_t* empty = full + kStages;
@@ -290,6 +300,7 @@ __global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acce[b]);  // the MMAs may refill this buffer
       float o[16];
+      double o64[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         // sum_L P_L 2^(-7 (L + 2)), smallest terms first; int32 -> double exactly as
@@ -304,7 +315,8 @@ __global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As
         // range: beyond it the fp32 result is 0 or inf either way)
         int E = e_row + __shfl_sync(0xffffffffu, e_col, j);
         E = E < -1022 ? -1022 : (E > 1023 ? 1023 : E);
-        o[j] = (float)(acc * __longlong_as_double((long long)(E + 1023) << 52));
+        o64[j] = acc * __longlong_as_double((long long)(E + 1023) << 52);
+        o[j] = (float)o64[j];
       }
       if (r < rows) {
         const int64_t p = p0 + r;
@@ -313,6 +325,11 @@ __global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As
 #pragma unroll
             for (int j = 0; j < 16; j += 4)
               *reinterpret_cast<float4*>(rm_out + p * D + i0 + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+          }
+          if (acc64) {  // Gram mode (pca.cu): fp64 sums over the K chunks of successive launches
+            double* dst = acc64 + p * D + i0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) dst[j] += o64[j];
           }
           if (blk_out) {
             float* dst = blk_out + (((int64_t)(i0 >> 4) * n_out + p) << 4);
@@ -371,9 +388,46 @@ void launch_rotate(const RotOp& op, RotWs& ws, const float* X, const int32_t* sr
     const int64_t ntiles = rp / kTM * ntn;
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
     k_rot_i8<<<grid, 320, smem, st>>>(ws.as.p, ws.ae.p, op.bs.p, op.be.p, nkc, rows, p0, n_out, D, rowmajor_out,
-                                      blocked_out);
+                                      blocked_out, nullptr);
     DADE_CK(cudaGetLastError());
   }
+}
+
+// Gram matrix on the int8 tensor cores (the PCA covariance, pca.cu): acc[a][b] += sum_k Y[a][k]
+// Y[b][k] for the rows x K fp64 matrix Y (K a multiple of 64, <= 16,384 so every level sum stays
+// an exact int32; rmax[a] = bits of max_k |Y[a][k]|). Y's rows are both operands: the A slices (per-row scale, 128-row tiles) and the
+// B slices (32-row tiles) of the same digits, so the result is exactly symmetric; the error of each
+// entry is bounded like the rotation's (R36): 9 K 2^-42 2^(e_a + e_b) with max_k |Y[a][k]| < 2^e_a.
+void launch_gram_i8(const double* Y, int rows, int64_t K, const unsigned long long* rmax, RotWs& wa, RotOp& wb,
+                    double* acc, cudaStream_t st) {
+  DADE_REQUIRE(K % kKB == 0 && K > 0 && K <= kRotMaxD && rows % 16 == 0, DADE_ERR_UNSUPPORTED,
+               "gram: K must be a positive multiple of 64, <= 16384, rows a multiple of 16");
+  const int nkc = (int)(K / kKB);
+  const int64_t rpa = (rows + kTM - 1) / kTM * kTM, ntn = (rows + kTN - 1) / kTN, rpb = ntn * kTN;
+  wa.as.reserve((size_t)rpa * nkc * kKB * kS);
+  wa.ae.reserve((size_t)rpa);
+  wb.bs.reserve((size_t)ntn * nkc * kBBlk);
+  wb.be.reserve((size_t)rpb);
+  // long rows, few of them: CTAs split each row into 8-chunk (512-K) pieces; the row maxima come
+  // from the gather (rmax), so the A and B digits use the same exponents
+  constexpr int kcpb = 8;
+  const unsigned gy = (unsigned)((nkc + kcpb - 1) / kcpb);
+  k_rot_slice<double, false><<<dim3((unsigned)((rpa + 63) / 64), gy), 256, 0, st>>>(
+      Y, nullptr, 0, rows, rpa, (int)K, nkc, nullptr, wa.as.p, wa.ae.p, rmax, kcpb);
+  DADE_CK(cudaGetLastError());
+  k_rot_slice<double, true><<<dim3((unsigned)((rpb + 63) / 64), gy), 256, 0, st>>>(
+      Y, nullptr, 0, rows, rpb, (int)K, nkc, nullptr, wb.bs.p, wb.be.p, rmax, kcpb);
+  DADE_CK(cudaGetLastError());
+  const size_t smem = (size_t)kStages * kStage + 128;
+  int dev = 0, sms = 0;
+  DADE_CK(cudaGetDevice(&dev));
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DADE_CK(cudaFuncSetAttribute(k_rot_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t ntiles = rpa / kTM * ntn;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
+  k_rot_i8<<<grid, 320, smem, st>>>(wa.as.p, wa.ae.p, wb.bs.p, wb.be.p, nkc, rows, 0, rows, rows, nullptr, nullptr,
+                                    acc);
+  DADE_CK(cudaGetLastError());
 }
 
 }  // namespace dade
