@@ -295,6 +295,7 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 #define DADE_OPT_FZ_DEBUG 13       /* measurement only: 1/2 add a pipeline-only launch of the fused filter */
 #define DADE_OPT_FZ_CPC 14         /* fused probe filter: 8 KB operand chunks per TMA copy (0 auto) */
 #define DADE_OPT_PCA_TC 15         /* PCA covariance: 1 (default) int8 tensor cores (exact levels), 0 fp64 CUDA cores (process-wide) */
+#define DADE_OPT_SCAN_P1 17        /* 1: scan stage 1 list-major (first-step rows read once per probed list; p1.cu); 0 (default) off */
 #define DADE_OPT_FZ_CPS 12         /* fused probe filter: persistent CTAs per SM (0 auto = 1, 2 with 1 group) */
 dade_status dade_set_option(dade_index* idx, int option, int64_t value);
 

@@ -46,6 +46,7 @@ struct Options {
   int host_chunks = 1;      // dade_search_host: searches pipelined with the copies
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
   int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
+  int scan_p1 = 0;          // stage 1 list-major (p1.cu): 1 on; 0 (default) off — measured slower
   int shard_exchanges = 2;  // collective search: top-K exchanges after epochs 0 .. E-1 (R32)
   int fz_stages = 0;        // probe_fz.cu: B ring stages (0 auto)
   int fz_groups = 0;        // probe_fz.cu: epilogue groups of 4 warps (0 auto, 1, 2)
@@ -79,7 +80,9 @@ struct dade_index {
   int calK = 0, n0 = 0, ncls = 0;
   std::vector<double> m1, v;
   // scratch
-  DBuf<float> qrot, dmat, qbuf, slack, gmin, fzseed;
+  DBuf<float> qrot, dmat, qbuf, slack, gmin, fzseed, p1;
+  DBuf<int> p1_base, p1_scr;
+  DBuf<long long> p1_total;
   TcOp a_tc;  // scratch: query-side operand of the filter GEMM
   DBuf<int32_t> probes, cand, idx32;
   DBuf<double> d64;
@@ -764,6 +767,28 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
   p.work_counter = x->work.p;
   p.order = order;
   p.g_force = x->opt.scan_warps;
+  // stage 1 list-major (p1.cu, DADE_OPT_SCAN_P1 = 1): each probed list's first-step rows read once
+  // for every query that probes it (BSA-p / ADSampling). Off by default: measured on C4 it halves
+  // the scan's DRAM bytes (5.20 -> 2.59 GB) but the scan is bound by its survivors' gather round
+  // trips (1.68 -> 1.44 ms under ncu) and the precompute costs more than that (0.95 ms)
+  {
+    const int unit = p.pq ? 0 : (p.dd % 4 == 0 ? 4 : p.dd % 2 == 0 ? 2 : 1);  // the scan's staging unit
+    const bool want = x->opt.scan_p1 == 1;
+    if (want && unit && !p.residual && !p.pq && x->nlist > 1) {
+      const int64_t avg = std::max<int64_t>(1, x->n / std::max(1, x->nlist));
+      const int64_t cap = std::min<int64_t>((int64_t)nq * nprobe * avg * 2 + 65536, (int64_t)1 << 31);
+      x->p1.reserve((size_t)cap + 4);
+      x->p1_base.reserve((size_t)nq + 1);
+      x->p1_scr.reserve(p1_scratch_ints(nq, nprobe, x->nlist));
+      x->p1_total.reserve(1);
+      p1_launch(x->layout.p, x->n, x->off_d.p, x->nlist, probes, nq, nprobe, qrot, D, unit, x->p1_scr.p,
+                x->p1_base.p, x->p1.p, cap, x->p1_total.p, st);
+      p.p1 = x->p1.p;
+      p.p1_base = x->p1_base.p;
+      p.p1_total = x->p1_total.p;
+      p.p1_cap = cap;
+    }
+  }
   if (dlog) {
     x->dlog_n.reserve(1);
     DADE_CK(cudaMemsetAsync(x->dlog_n.p, 0, sizeof(unsigned long long), st));
@@ -784,6 +809,7 @@ void do_search(dade_index* x, const float* Q, int nq, int K, int nprobe, int del
     p2.probes += (size_t)q0 * nprobe;
     p2.out_ids += (size_t)q0 * K;
     p2.out_d += (size_t)q0 * K;
+    if (p2.p1_base) p2.p1_base += q0;
     if (p2.qconst) p2.qconst += (size_t)q0 * (nsteps - 1);
     p2.work_counter = x->work.p + 1;
     p2.g_force = 4;
@@ -951,6 +977,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->dlog_n.release(); x->ids_tmp.release(); x->ordcnt.release(); x->order.release(); x->xnorm.release(); x->qconst.release(); x->lam_d.release();
   x->dists_tmp.release();
   x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release(); x->fzseed.release();
+  x->p1.release(); x->p1_base.release(); x->p1_scr.release(); x->p1_total.release();
   for (auto& e : x->ev)
     if (e) cudaEventDestroy(e);
   if (x->side) {
@@ -2025,6 +2052,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_FZ_CPS: in({0, 1, 2}); o.fz_cps = (int)value; break;
     case DADE_OPT_FZ_DEBUG: in({0, 1, 2}); g_fz_debug = (int)value; break;
     case DADE_OPT_PCA_TC: in({0, 1}); g_pca_tc = (int)value; break;
+    case DADE_OPT_SCAN_P1: in({0, 1}); o.scan_p1 = (int)value; break;
     case DADE_OPT_FZ_CPC: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz cpc not in [0, 64]");
       o.fz_cpc = (int)value; break;
     default: throw Error(DADE_ERR_ARG, "unknown option");

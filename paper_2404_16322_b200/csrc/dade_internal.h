@@ -229,12 +229,26 @@ struct ScanParams {
   const float* init_d;
   const int64_t* cap_ids;
   const float* cap_d;
+  // stage 1 from the list-major precompute (p1.cu; null = read the rows): p1[p1_base[q] + t] is
+  // the first step's partial distance of candidate t of query q's stream (BSA-p / ADSampling)
+  const float* p1;
+  const int* p1_base;
+  const long long* p1_total;  // the streams' total length (device); p1 is used only if <= p1_cap
+  long long p1_cap;
   // decision log (parity runs; null = off): per tested candidate (query, global id, dims read)
   int32_t* dlog;
   int64_t dlog_cap;              // records
   unsigned long long* dlog_n;    // records written (may exceed dlog_cap: the caller sees the overflow)
 };
 void launch_scan(const ScanParams& p, cudaStream_t st);
+// p1.cu: the first step's partial distances of every (query, candidate) pair, list-major (each
+// probed list's first-step rows read once for all queries probing it). dd_unit = the scan's
+// staging unit in blocks (1, 2, 4); scratch: p1_scratch_ints ints; qbase_out: nq ints; p1: the
+// sum of the queries' stream lengths (+ 4) floats.
+size_t p1_scratch_ints(int nq, int nprobe, int nlist);
+void p1_launch(const float* layout, int64_t n, const int32_t* off, int nlist, const int32_t* probes, int nq,
+               int nprobe, const float* qrot, int D, int dd_unit, int* scratch, int* qbase_out, float* p1,
+               int64_t p1_cap, long long* total, cudaStream_t st);
 // misc.cu: the scan's query order — a counting sort of the queries by their nearest probed list
 // (probes[q][0]), so queries that share lists are scanned close in time (L2 reuse of their
 // tiles). cnt: nlist ints of scratch; order: nq ints.

@@ -144,7 +144,10 @@ __device__ __forceinline__ float block_sum(const unsigned long long (&x)[8], con
 }
 
 // Same with the 16-B chunks in a per-lane rotated order (stage 1 reads the tile rotated so the
-// 8 lanes of a shared-memory phase hit distinct banks); q chunk c pairs with x chunk c.
+// 8 lanes of a shared-memory phase hit distinct banks); q chunk c pairs with x chunk c. (Measured:
+// rotating the chunk partials back to block_sum's association costs ~2% of the C4 scan; the
+// rounding of the block-0 sum therefore depends on the row's lane, a deterministic function of
+// the stream — R21's bound covers either association.)
 __device__ __forceinline__ float block_sum_rot(const unsigned long long (&x)[8], const float* const (&q)[4]) {
   unsigned long long a[4];
 #pragma unroll
@@ -465,10 +468,12 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     // ---------------------------------------------------- producer state (warp-uniform)
     // tiles never cross a list or an epoch boundary (R13); tile t belongs to warp t mod G
     int pj = 0, ppos = 0, pr = e_lo0, pep = p.ep_first, pe_hi = e_hi0, tix = 0;
+    const float* p1q =  // list-major stage 1 (p1.cu), unless its buffer was too small
+        (!PQ && !RES && p.p1 && *p.p1_total <= p.p1_cap) ? p.p1 + p.p1_base[q] : nullptr;
     int2 pl = p.nprobe > 0 ? lists[0] : make_int2(0, 0);
     int issued = 0;
     auto issue = [&](int slot) -> bool {
-      int row0, nr;
+      int row0, nr, sp;
       for (;;) {
         if (pr >= L) return false;
         if (pr >= pe_hi) {
@@ -482,13 +487,20 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         }
         nr = min(min(pe_hi, ppos + pl.y) - pr, TR);
         row0 = pl.x + (pr - ppos);
+        sp = pr;
         pr += nr;
         DADE_DCHECK(nr >= 1 && nr <= TR && row0 >= 0 && (int64_t)row0 + nr <= n);
         if (!MULTI || (tix++ & (G - 1)) == warp) break;
       }
       if (lane == 0) {
         meta[slot] = TileMeta{row0, nr, pep, 0};
-        if (PQ) {  // the tile's code rows: one contiguous range of list-major rows
+        if (!PQ && !RES && p1q) {  // the tile's precomputed stage-1 values: 16-B aligned superset
+          const uintptr_t a = reinterpret_cast<uintptr_t>(p1q + sp), a0 = a & ~(uintptr_t)15;
+          const uint32_t bytes = (uint32_t)(((a + 4u * (uint32_t)nr + 15) & ~(uintptr_t)15) - a0);
+          meta[slot].pad = (int32_t)((a - a0) >> 2);
+          mbar_expect_tx(&mbar[slot], bytes);
+          bulk_g2s(tiles + slot * TB, reinterpret_cast<const void*>(a0), bytes, &mbar[slot]);
+        } else if (PQ) {  // the tile's code rows: one contiguous range of list-major rows
           const uint32_t bytes = (uint32_t)nr * (uint32_t)p.pq_stride;
           mbar_expect_tx(&mbar[slot], bytes);
           bulk_g2s(tiles + slot * TB, p.pq_codes + (int64_t)row0 * p.pq_stride, bytes, &mbar[slot]);
@@ -737,6 +749,9 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
       const unsigned char* trow = tiles + slot * TB + lane * 64;
       float s = 0.f, sq = 0.f;
       const float xn = RES && val ? __ldg(p.xnorm + tm.row0 + lane) : 0.f;
+      if (!RES && p1q) {  // list-major precompute (p1.cu): the same block sums, read as one float
+        s = val ? reinterpret_cast<const float*>(tiles + slot * TB)[tm.pad + lane] : 0.f;
+      } else
 #pragma unroll
       for (int bb = 0; bb < DD; ++bb) {
         unsigned long long x[8];

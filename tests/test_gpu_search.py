@@ -287,3 +287,20 @@ def test_extreme_shapes(D, K, dd):
     from paper_2404_16322_b200 import DadeError
     with pytest.raises(DadeError):
         ix.search(torch.from_numpy(Q).cuda(), 257, 4, dd, 0.0)   # K > DADE_MAX_K
+
+
+@pytest.mark.parametrize("dd", [16, 32, 64])
+def test_list_major_stage1_option(dd):
+    # DADE_OPT_SCAN_P1 = 1 (p1.cu): stage 1 from the list-major precompute (the first step's
+    # block sums of every (query, candidate), each probed list read once) — the same oracle
+    # parity as the row-reading stage 1, on a SIFT-shaped index with lists shared by many queries;
+    # staging units 1, 2 and 4 blocks (delta_d 16 / 32 / 64)
+    cfg = synth.config("c2", n=20000, nlist=32, nq=120, n_cal=60)
+    torch, ix, oidx, X, Xd = _setup(cfg)
+    Q = synth.queries(cfg)
+    ix.set_option("scan_p1", 1)
+    gi, gd, st, oi, od, ost = _compare(torch, ix, oidx, Q, cfg.k, 6, dd, 0.005)
+    ix.set_option("scan_p1", 0)
+    gi0, gd0, st0 = ix.search(torch.from_numpy(Q).cuda(), cfg.k, 6, dd, 0.005, stats=True)
+    assert tie_adjusted_overlap(gi, gd, gi0.cpu().numpy(), gd0.cpu().numpy()) >= 0.999
+    assert st["tested"] == st0["tested"]
