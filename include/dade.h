@@ -296,6 +296,7 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 #define DADE_OPT_FZ_CPC 14         /* fused probe filter: 8 KB operand chunks per TMA copy (0 auto) */
 #define DADE_OPT_PCA_TC 15         /* PCA covariance: 1 (default) int8 tensor cores (exact levels), 0 fp64 CUDA cores (process-wide) */
 #define DADE_OPT_SCAN_P1 17        /* 1: scan stage 1 list-major (first-step rows read once per probed list; p1.cu); 0 (default) off */
+#define DADE_OPT_DHAT_CHUNK_MB 18  /* probe d_hat matrix chunk size in MB (0 = 2 GiB) */
 #define DADE_OPT_FZ_CPS 12         /* fused probe filter: persistent CTAs per SM (0 auto = 1, 2 with 1 group) */
 dade_status dade_set_option(dade_index* idx, int option, int64_t value);
 

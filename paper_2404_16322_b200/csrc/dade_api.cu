@@ -46,6 +46,7 @@ struct Options {
   int host_chunks = 1;      // dade_search_host: searches pipelined with the copies
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
   int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
+  int dhat_chunk_mb = 0;    // d_hat matrix chunk in MB (0: 2 GiB); measurement option
   int scan_p1 = 0;          // stage 1 list-major (p1.cu): 1 on; 0 (default) off — measured slower
   int shard_exchanges = 2;  // collective search: top-K exchanges after epochs 0 .. E-1 (R32)
   int fz_stages = 0;        // probe_fz.cu: B ring stages (0 auto)
@@ -367,7 +368,8 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     if (sync) check_knn_flag(x);
     return;
   }
-  const int64_t budget = (int64_t)1 << 29;  // floats of d_hat per chunk (2 GiB)
+  // floats of d_hat per chunk (2 GiB; DADE_OPT_DHAT_CHUNK_MB overrides, e.g. an L2-sized chunk)
+  const int64_t budget = x->opt.dhat_chunk_mb ? (int64_t)x->opt.dhat_chunk_mb << 18 : (int64_t)1 << 29;
   int64_t chunk = std::max<int64_t>(128, budget / std::max<int64_t>(n, 1) / 128 * 128);
   const int cand_cap = 4096;
   if (k > 1 || out_d64) {
@@ -2053,6 +2055,8 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_FZ_DEBUG: in({0, 1, 2}); g_fz_debug = (int)value; break;
     case DADE_OPT_PCA_TC: in({0, 1}); g_pca_tc = (int)value; break;
     case DADE_OPT_SCAN_P1: in({0, 1}); o.scan_p1 = (int)value; break;
+    case DADE_OPT_DHAT_CHUNK_MB: DADE_REQUIRE(value >= 0 && value <= 8192, DADE_ERR_ARG, "dhat chunk not in [0, 8192] MB");
+      o.dhat_chunk_mb = (int)value; break;
     case DADE_OPT_FZ_CPC: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz cpc not in [0, 64]");
       o.fz_cpc = (int)value; break;
     default: throw Error(DADE_ERR_ARG, "unknown option");
