@@ -281,7 +281,8 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
  * measurement and for tests proving every path returns identical results). Errors: ARG (unknown
  * option or value). */
 #define DADE_OPT_KNN_PATH 1        /* exact-KNN filter: 0 auto, 1 d_hat matrix, 2 fused (no d_hat), 3 group minima,
-                                      4 throughput fused filter on fp16 operands, 5 the same on tf32 (probe_fz.cu) */
+                                      4 throughput fused filter on fp16 operands, 5 the same on tf32 (probe_fz.cu),
+                                      6 int8 exact-split filter + group-minima select (rotate.cu distance mode) */
 #define DADE_OPT_PROBE_PASSES 2    /* tf32 passes of the probe filter: 0 auto (1 if D < 512, else 3), 1, 3 */
 #define DADE_OPT_SCAN_WARPS 3      /* warps per query in the scan: 0 auto, 1, 2, 4, 8 */
 #define DADE_OPT_SCAN_ORDER 4      /* scan order: 2 (default) longest candidate stream first, 1 grouped by nearest list, 0 as given */
@@ -297,6 +298,7 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 #define DADE_OPT_PCA_TC 15         /* PCA covariance: 1 (default) int8 tensor cores (exact levels), 0 fp64 CUDA cores (process-wide) */
 #define DADE_OPT_SCAN_P1 17        /* 1: scan stage 1 list-major (first-step rows read once per probed list; p1.cu); 0 (default) off */
 #define DADE_OPT_DHAT_CHUNK_MB 18  /* probe d_hat matrix chunk size in MB (0 = 2 GiB) */
+#define DADE_OPT_KNN_I8 19         /* exact KNN for D >= 512: 1 int8 exact-split filter, 0 (default) the 3-pass tf32 filter */
 #define DADE_OPT_FZ_CPS 12         /* fused probe filter: persistent CTAs per SM (0 auto = 1, 2 with 1 group) */
 dade_status dade_set_option(dade_index* idx, int option, int64_t value);
 

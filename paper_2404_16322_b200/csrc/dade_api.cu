@@ -26,11 +26,20 @@ struct TcOp {
   float maxnorm = 0.f;
   float hinv_b = 0.f;  // 1 / matrix scale of the fp16 operand (B side)
   bool h16_ok = false;
+  // int8 exact-split filter (rotate.cu distance mode), B side: slices, fp64 centre and norms,
+  // largest slice exponent and norm (device)
+  RotOp i8b;
+  DBuf<double> mu64, bn64;
+  DBuf<int> i8e;
+  DBuf<unsigned long long> i8bmax;
+  bool i8_ok = false;
   void release() {
     hi.release(); lo.release(); norm.release(); maxn.release(); center.release(); csum.release();
     h16.release(); hinv.release();
+    i8b.release(); mu64.release(); bn64.release(); i8e.release(); i8bmax.release();
     rows = 0;
     h16_ok = false;
+    i8_ok = false;
   }
 };
 
@@ -47,6 +56,7 @@ struct Options {
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
   int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
   int dhat_chunk_mb = 0;    // d_hat matrix chunk in MB (0: 2 GiB); measurement option
+  int knn_i8 = 0;           // exact_knn: 1 = int8 exact-split filter for D >= 512; 0 (default) the 3-pass tf32 one
   int scan_p1 = 0;          // stage 1 list-major (p1.cu): 1 on; 0 (default) off — measured slower
   int shard_exchanges = 2;  // collective search: top-K exchanges after epochs 0 .. E-1 (R32)
   int fz_stages = 0;        // probe_fz.cu: B ring stages (0 auto)
@@ -82,6 +92,7 @@ struct dade_index {
   std::vector<double> m1, v;
   // scratch
   DBuf<float> qrot, dmat, qbuf, slack, gmin, fzseed, p1;
+  DBuf<double> an64;  // int8 filter: fp64 centred query norms
   DBuf<int> p1_base, p1_scr;
   DBuf<long long> p1_total;
   TcOp a_tc;  // scratch: query-side operand of the filter GEMM
@@ -219,6 +230,20 @@ void tc_prepare(dade_index* x, const float* B, int64_t n, TcOp& op, bool need_ma
     DADE_CK(cudaStreamSynchronize(x->stream));
   }
   op.h16_ok = false;  // the fp16 copy (probe_fz.cu) is made on first use: tc_prepare_h16
+  op.i8_ok = false;   // so is the int8 split (tc_prepare_i8)
+}
+
+// int8 exact-split copy of a prepared B operand (the wide-row filter of exact_knn), on first use
+void tc_prepare_i8(dade_index* x, const float* B, TcOp& op) {
+  if (op.i8_ok) return;
+  const int D = x->D;
+  const int64_t rp = (op.rows + 31) / 32 * 32;
+  op.mu64.reserve((size_t)D);
+  op.bn64.reserve((size_t)rp);
+  op.i8e.reserve(1);
+  op.i8bmax.reserve(1);
+  launch_i8_bprep(B, op.rows, D, op.center.p, op.mu64.p, op.i8b, op.bn64.p, op.i8e.p, op.i8bmax.p, x->stream);
+  op.i8_ok = true;
 }
 
 // fp16 copy of a prepared B operand for the fused probe filter (probe_fz.cu), made once per
@@ -367,6 +392,47 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     }
     if (sync) check_knn_flag(x);
     return;
+  }
+  // int8 exact-split filter (rotate.cu distance mode) for long rows, where the 3-pass tf32 window
+  // (gamma_3 ~ 6 Dp 2^-23 of the norms) holds hundreds of near-ties: the exact split bounds the
+  // dot product to 9 D 2^-42 of the slice scales, so the window is the fp32 rounding of d_hat and
+  // the fp64 certification sees ~k columns (knn_path 6 forces it; DADE_OPT_KNN_I8 = 1 uses it for
+  // D >= 512 with the group-minima select). Off by default: measured on C3 (1,000 x 4,096 x 960,
+  // k = 64) the probe takes 0.334 ms against the 3-pass tf32 filter's 0.285 — the group-minima
+  // select (0.27 ms) does not shrink with the window, and the int8 split + GEMM (0.23 ms) costs
+  // more than the tf32 split + 3-pass GEMM (0.14 ms)
+  {
+    const int64_t ngr = (n + 31) / 32;
+    const bool i8 = k > 1 && k <= ngr && ngr <= 1024 && D % 16 == 0 && D <= kRotMaxD &&
+                    (path ? path == 6 : (passes == 3 && D >= 512 && x->opt.knn_i8));
+    if (i8) {
+      tc_prepare_i8(x, B, const_cast<TcOp&>(bop));
+      const int64_t budget = (int64_t)1 << 29;
+      int64_t chunk = std::max<int64_t>(128, budget / std::max<int64_t>(n, 1) / 128 * 128);
+      chunk = std::min<int64_t>(std::min<int64_t>(chunk, 16384), tc_rows_pad(m));
+      x->dmat.reserve((size_t)chunk * n);
+      x->gmin.reserve((size_t)chunk * ngr);
+      x->slack.reserve((size_t)chunk);
+      x->an64.reserve((size_t)chunk);
+      x->ovf.reserve((size_t)chunk + 1);
+      if (!x->flag.p) {
+        x->flag.reserve(1);
+        DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
+      }
+      for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+        const int64_t mm = std::min(chunk, m - r0);
+        launch_cnorm64(A + r0 * D, mm, mm, D, bop.mu64.p, x->an64.p, x->stream);
+        DADE_CK(cudaMemsetAsync(x->gmin.p, 0x7f, sizeof(float) * (size_t)mm * ngr, x->stream));
+        launch_dist_i8(A + r0 * D, mm, D, bop.mu64.p, x->an64.p, x->rot_ws, bop.i8b, bop.bn64.p, n, x->dmat.p,
+                       reinterpret_cast<unsigned*>(x->gmin.p), ngr, x->stream);
+        launch_slack_i8(x->an64.p, x->rot_ws.ae.p, mm, bop.i8e.p, bop.i8bmax.p, D, x->slack.p, x->stream);
+        launch_select_gmin(x->dmat.p, x->gmin.p, 5, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
+                           out_d64 ? out_d64 + r0 * k : nullptr, x->flag.p, x->slack.p, x->ovf.p, x->ovf.p + 1,
+                           x->stream);
+      }
+      if (sync) check_knn_flag(x);
+      return;
+    }
   }
   // floats of d_hat per chunk (2 GiB; DADE_OPT_DHAT_CHUNK_MB overrides, e.g. an L2-sized chunk)
   const int64_t budget = x->opt.dhat_chunk_mb ? (int64_t)x->opt.dhat_chunk_mb << 18 : (int64_t)1 << 29;
@@ -979,7 +1045,7 @@ extern "C" dade_status dade_destroy(dade_index* x) {
   x->d64.release(); x->flag.release(); x->fflag.release(); x->work.release(); x->ovf.release(); x->counters.release(); x->dlog_n.release(); x->ids_tmp.release(); x->ordcnt.release(); x->order.release(); x->xnorm.release(); x->qconst.release(); x->lam_d.release();
   x->dists_tmp.release();
   x->cent_tc.release(); x->a_tc.release(); x->slack.release(); x->gmin.release(); x->fzseed.release();
-  x->p1.release(); x->p1_base.release(); x->p1_scr.release(); x->p1_total.release();
+  x->p1.release(); x->p1_base.release(); x->p1_scr.release(); x->p1_total.release(); x->an64.release();
   for (auto& e : x->ev)
     if (e) cudaEventDestroy(e);
   if (x->side) {
@@ -2031,7 +2097,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     throw Error(DADE_ERR_ARG, "option value not allowed");
   };
   switch (option) {
-    case DADE_OPT_KNN_PATH: in({0, 1, 2, 3, 4, 5}); o.knn_path = (int)value; break;
+    case DADE_OPT_KNN_PATH: in({0, 1, 2, 3, 4, 5, 6}); o.knn_path = (int)value; break;
     case DADE_OPT_PROBE_PASSES: in({0, 1, 3}); o.probe_passes = (int)value; break;
     case DADE_OPT_SCAN_WARPS: in({0, 1, 2, 4, 8}); o.scan_warps = (int)value; break;
     case DADE_OPT_SCAN_ORDER: in({0, 1, 2}); o.scan_order = (int)value; break;
@@ -2055,6 +2121,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_FZ_DEBUG: in({0, 1, 2}); g_fz_debug = (int)value; break;
     case DADE_OPT_PCA_TC: in({0, 1}); g_pca_tc = (int)value; break;
     case DADE_OPT_SCAN_P1: in({0, 1}); o.scan_p1 = (int)value; break;
+    case DADE_OPT_KNN_I8: in({0, 1}); o.knn_i8 = (int)value; break;
     case DADE_OPT_DHAT_CHUNK_MB: DADE_REQUIRE(value >= 0 && value <= 8192, DADE_ERR_ARG, "dhat chunk not in [0, 8192] MB");
       o.dhat_chunk_mb = (int)value; break;
     case DADE_OPT_FZ_CPC: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz cpc not in [0, 64]");

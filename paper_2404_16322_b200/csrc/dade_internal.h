@@ -350,6 +350,20 @@ bool logistic_irls_multi(const std::vector<double>& F, int k, const std::vector<
                          std::vector<double>& m_out, double* beta_out);
 uint64_t splitmix64(uint64_t x);
 
+// rotate.cu, the int8 filter of exact_knn (distance mode): B slices (centred on mu, fp64),
+// fp64 centred norms, per-row slack, and the d_hat matrix + 32-column group minima (float bits)
+void prepare_i8_b(const float* B, int64_t n, int D, const double* mu, RotOp& ob, cudaStream_t st);
+void launch_cnorm64(const float* X, int64_t n, int64_t rows_pad, int D, const double* mu, double* out,
+                    cudaStream_t st);
+void launch_slack_i8(const double* an, const int32_t* ea, int64_t m, const int* e_bmax,
+                     const unsigned long long* bmax_bits, int D, float* slack, cudaStream_t st);
+// B side of the int8 filter, all on the device: mu64 = the fp32 centre, the slices, fp64 norms
+// (bn64: n rounded up to 32 entries), the largest slice exponent and the largest norm
+void launch_i8_bprep(const float* B, int64_t n, int D, const float* center, double* mu64, RotOp& ob, double* bn64,
+                     int* emax, unsigned long long* bmax_bits, cudaStream_t st);
+void launch_dist_i8(const float* A, int64_t m, int D, const double* mu, const double* an64, RotWs& wa,
+                    const RotOp& ob, const double* bn64, int64_t n, float* dist, unsigned* gmin, int64_t ldg,
+                    cudaStream_t st);
 void launch_gram_i8(const double* Y, int rows, int64_t K, const unsigned long long* rmax, RotWs& wa, RotOp& wb,
                     double* acc, cudaStream_t st);
 }  // namespace dade

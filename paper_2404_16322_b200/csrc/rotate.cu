@@ -208,7 +208,10 @@ __global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As
                                                    const int8_t* __restrict__ Bs, const int32_t* __restrict__ eb,
                                                    int nkc, int64_t rows, int64_t p0, int64_t n_out, int D,
                                                    float* __restrict__ rm_out, float* __restrict__ blk_out,
-                                                   double* __restrict__ acc64) {
+                                                   double* __restrict__ acc64, const double* __restrict__ an64 = nullptr,
+                                                   const double* __restrict__ bn64 = nullptr,
+                                                   float* __restrict__ dist_out = nullptr,
+                                                   unsigned* __restrict__ gmin_out = nullptr, int64_t ldg = 0) {
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStage);
   uint64_t* empty = full + kStages;
@@ -326,6 +329,29 @@ __global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As
             for (int j = 0; j < 16; j += 4)
               *reinterpret_cast<float4*>(rm_out + p * D + i0 + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
           }
+          if (dist_out) {  // distance mode (exact_knn's int8 filter): an + bn - 2 <a, b> in fp64 -> fp32
+            const double a2 = an64[r];
+            float mn = INFINITY;
+            float dv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const double dd = a2 + bn64[i0 + j] - 2.0 * o64[j];
+              dv[j] = i0 + j < D ? fmaxf(0.f, (float)dd) : INFINITY;
+              mn = fminf(mn, dv[j]);
+            }
+            float* dst = dist_out + p * D + i0;
+            if ((D & 3) == 0 && i0 + 16 <= D) {  // (the last tile of a ragged row: scalar stores)
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(dv[j], dv[j + 1], dv[j + 2], dv[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (i0 + j < D) dst[j] = dv[j];
+            }
+            // 32-column group minimum (the other 16 columns are another warp's): values >= 0, so
+            // the float bits order as unsigned
+            atomicMin(gmin_out + p * ldg + (i0 >> 5), __float_as_uint(mn));
+          }
           if (acc64) {  // Gram mode (pca.cu): fp64 sums over the K chunks of successive launches
             double* dst = acc64 + p * D + i0;
 #pragma unroll
@@ -391,6 +417,132 @@ void launch_rotate(const RotOp& op, RotWs& ws, const float* X, const int32_t* sr
                                       blocked_out, nullptr);
     DADE_CK(cudaGetLastError());
   }
+}
+
+// fp64 squared norms of the centred rows, sum_j (x_j - mu_j)^2 (warp per row; rows >= n and the
+// padding up to rows_pad are 0)
+__global__ void k_cnorm64(const float* __restrict__ X, int64_t n, int64_t rows_pad, int D, const double* __restrict__ mu,
+                          double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows_pad) return;
+  double s = 0.0;
+  if (r < n)
+    for (int j = lane; j < D; j += 32) {
+      const double v = (double)X[r * D + j] - mu[j];
+      s += v * v;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[r] = s;
+}
+
+// the int8 filter's error bound per row (rounded up to fp32): |d_hat - d| <= slack + 2^-20 d with
+// slack = 2 * 9 D 2^-42 2^(e_a + e_bmax) (the exact split, R36, doubled for -2 <a, b>) plus the
+// fp64 arithmetic ((D + 16) 2^-51 (an + bmax): the D-term norm sums and the final combination);
+// the fp32 rounding of d_hat is inside the 2^-20 d term
+__global__ void k_slack_i8(const double* __restrict__ an, const int32_t* __restrict__ ea, int64_t m,
+                           const int* __restrict__ e_bmax, const unsigned long long* __restrict__ bmax_bits, int D,
+                           float* __restrict__ slack) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double bmax = __longlong_as_double((long long)*bmax_bits);
+  // fp64 part: the sequential norm sums (D terms each) and the final an + bn - 2 o, generously
+  const double s = 18.0 * D * ldexp(1.0, ea[i] + *e_bmax - 42) + (D + 16) * 4.440892098500626e-16 * (an[i] + bmax);
+  slack[i] = __double2float_ru(s);
+}
+
+// the B operand's largest slice exponent and largest centred norm (for the slack), and the fp64
+// centre from the fp32 one
+__global__ void k_i8_bstats(const int32_t* __restrict__ be, const double* __restrict__ bn, int64_t n,
+                            int* __restrict__ emax, unsigned long long* __restrict__ bmax_bits) {
+  int e = -1 << 30;
+  double b = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    e = max(e, be[i]);
+    b = fmax(b, bn[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(emax, e);
+    atomicMax(bmax_bits, (unsigned long long)__double_as_longlong(b));
+  }
+}
+__global__ void k_f2d(const float* __restrict__ a, double* __restrict__ b, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (double)a[i];
+}
+
+void launch_cnorm64(const float* X, int64_t n, int64_t rows_pad, int D, const double* mu, double* out,
+                    cudaStream_t st) {
+  if (rows_pad <= 0) return;
+  k_cnorm64<<<(unsigned)((rows_pad + 7) / 8), 256, 0, st>>>(X, n, rows_pad, D, mu, out);
+  DADE_CK(cudaGetLastError());
+}
+
+void launch_slack_i8(const double* an, const int32_t* ea, int64_t m, const int* e_bmax,
+                     const unsigned long long* bmax_bits, int D, float* slack, cudaStream_t st) {
+  if (m <= 0) return;
+  k_slack_i8<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(an, ea, m, e_bmax, bmax_bits, D, slack);
+  DADE_CK(cudaGetLastError());
+}
+
+void launch_i8_bprep(const float* B, int64_t n, int D, const float* center, double* mu64, RotOp& ob, double* bn64,
+                     int* emax, unsigned long long* bmax_bits, cudaStream_t st) {
+  k_f2d<<<(D + 255) / 256, 256, 0, st>>>(center, mu64, D);
+  DADE_CK(cudaGetLastError());
+  prepare_i8_b(B, n, D, mu64, ob, st);
+  const int64_t rp = (n + kTN - 1) / kTN * kTN;
+  launch_cnorm64(B, n, rp, D, mu64, bn64, st);
+  DADE_CK(cudaMemsetAsync(emax, 0x80, sizeof(int), st));  // 0x80808080: a very negative int
+  DADE_CK(cudaMemsetAsync(bmax_bits, 0, sizeof(unsigned long long), st));
+  k_i8_bstats<<<(unsigned)std::min<int64_t>((n + 255) / 256, 592), 256, 0, st>>>(ob.be.p, bn64, n, emax, bmax_bits);
+  DADE_CK(cudaGetLastError());
+}
+
+// Filter distances on the int8 tensor cores (exact_knn, wide rows): d[p][i] = fp32(an[p] + bn[i] -
+// 2 <a_p, b_i>) for centred A (rows p, the queries) and B (rows i, the centroids), both sliced by
+// k_rot_slice with the same fp64 centre; the dot product carries the exact-split error bound
+// 9 D 2^-42 2^(e_a + e_b) (R36), the rest is fp64 arithmetic and one fp32 rounding, so the
+// certified window of the selection is ~k wide. gmin[p][g] = the minimum of columns [32 g, 32 g +
+// 32) (as float bits; the caller fills it with 0x7f7f7f7f first).
+void prepare_i8_b(const float* B, int64_t n, int D, const double* mu, RotOp& ob, cudaStream_t st) {
+  const int nkc = rot_nkc(D);
+  const int64_t ntn = (n + kTN - 1) / kTN, rp = ntn * kTN;
+  ob.bs.reserve((size_t)ntn * nkc * kBBlk);
+  ob.be.reserve((size_t)rp);
+  k_rot_slice<float, true><<<(unsigned)((rp + 63) / 64), 256, 0, st>>>(B, nullptr, 0, n, rp, D, nkc, mu, ob.bs.p,
+                                                                        ob.be.p);
+  DADE_CK(cudaGetLastError());
+  ob.D = D;
+}
+
+void launch_dist_i8(const float* A, int64_t m, int D, const double* mu, const double* an64, RotWs& wa,
+                    const RotOp& ob, const double* bn64, int64_t n, float* dist, unsigned* gmin, int64_t ldg,
+                    cudaStream_t st) {
+  if (m <= 0) return;
+  const int nkc = rot_nkc(D);
+  const int64_t rp = (m + kTM - 1) / kTM * kTM;
+  wa.as.reserve((size_t)rp * nkc * kKB * kS);
+  wa.ae.reserve((size_t)rp);
+  k_rot_slice<float, false><<<(unsigned)((rp + 63) / 64), 256, 0, st>>>(A, nullptr, 0, m, rp, D, nkc, mu, wa.as.p,
+                                                                         wa.ae.p);
+  DADE_CK(cudaGetLastError());
+  const size_t smem = (size_t)kStages * kStage + 128;
+  int dev = 0, sms = 0;
+  DADE_CK(cudaGetDevice(&dev));
+  DADE_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DADE_CK(cudaFuncSetAttribute(k_rot_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t ntn = (n + kTN - 1) / kTN, ntiles = rp / kTM * ntn;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms);
+  // "D" of the kernel = output width (n columns); K = nkc chunks of the D dims
+  k_rot_i8<<<grid, 320, smem, st>>>(wa.as.p, wa.ae.p, ob.bs.p, ob.be.p, nkc, m, 0, m, (int)n, nullptr, nullptr,
+                                    nullptr, an64, bn64, dist, gmin, ldg);
+  DADE_CK(cudaGetLastError());
 }
 
 // Gram matrix on the int8 tensor cores (the PCA covariance, pca.cu): acc[a][b] += sum_k Y[a][k]

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 _OPTS = {}  # dade_set_option values applied to every index a test creates
 
 
-@pytest.fixture(autouse=True, params=[1, 2, 4, 5], ids=["dhat-matrix", "fused-filter", "fz-fp16", "fz-tf32"])
+@pytest.fixture(autouse=True, params=[1, 2, 4, 5, 6], ids=["dhat-matrix", "fused-filter", "fz-fp16", "fz-tf32", "int8-split"])
 def knn_path(request):
     # every selection path: the d_hat-matrix select (exact.cu), the fused filter GEMM with
     # in-epilogue candidate tracking (probe_tc.cu) and the throughput fused filter on fp16 / tf32

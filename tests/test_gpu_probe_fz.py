@@ -130,3 +130,33 @@ def test_fz_many_rows_chunks(torch_cuda):
     ix.set_option("knn_path", 1)
     pr1 = ix.probe(torch.from_numpy(Q).cuda(), 8).cpu().numpy()
     assert np.array_equal(pr4, pr1)
+
+
+@pytest.mark.parametrize("D,C,nprobe", [(960, 4096, 64), (512, 3000, 16), (960, 777, 8)])
+def test_int8_split_filter_gist_like(torch_cuda, D, C, nprobe):
+    # the int8 exact-split filter (knn_path 6; DADE_OPT_KNN_I8 for D >= 512): GIST-like
+    # data in [0, 1] with a decaying spectrum (dense near-ties at D = 960), ragged column tiles;
+    # probes bit-exact against the oracle and equal to the 3-pass tf32 path's
+    torch = torch_cuda
+    from paper_2404_16322_b200 import Index
+    rng = np.random.default_rng(D + C)
+    lam = np.arange(1, D + 1, dtype=np.float64) ** -1.5
+    basis = np.linalg.qr(rng.standard_normal((D, D)))[0]
+    X = ((rng.standard_normal((2 * C, D)) * np.sqrt(lam)) @ basis.T)
+    X = ((X - X.min()) / (X.max() - X.min())).astype(np.float32)
+    cent = X[rng.choice(2 * C, C, replace=False)].copy()
+    cent[C - 1] = cent[3]
+    ix = Index(D)
+    mean, R, lam_ = O.fit_rotation(X)
+    ix.set_rotation(mean, R, lam_)
+    ix.build_ivf(torch.from_numpy(X).cuda(), C, centroids=torch.from_numpy(cent).cuda())
+    Q = np.clip(((rng.standard_normal((200, D)) * np.sqrt(lam)) @ basis.T - X.min()) / (X.max() - X.min()), 0, 1)
+    Q = Q.astype(np.float32)
+    Q[5] = cent[3]
+    ix.set_option("probe_passes", 3)
+    ix.set_option("knn_path", 6)
+    pr = _check(torch, ix, Q, cent, nprobe, step=4)
+    ix.set_option("knn_path", 1)
+    ix.set_option("knn_i8", 0)
+    pr3 = ix.probe(torch.from_numpy(Q).cuda(), nprobe).cpu().numpy()
+    assert np.array_equal(pr, pr3)
