@@ -56,6 +56,7 @@ struct Options {
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
   int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
   int dhat_chunk_mb = 0;    // d_hat matrix chunk in MB (0: 2 GiB); measurement option
+  int gmin_ratio = 1;       // exact_knn: group-minima select only when k * ratio <= number of 32-column groups
   int knn_i8 = 0;           // exact_knn: 1 = int8 exact-split filter for D >= 512; 0 (default) the 3-pass tf32 one
   int scan_p1 = 0;          // stage 1 list-major (p1.cu): 1 on; 0 (default) off — measured slower
   int shard_exchanges = 2;  // collective search: top-K exchanges after epochs 0 .. E-1 (R32)
@@ -456,7 +457,11 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t mm = std::min(chunk, m - r0);
     tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
-    const bool use_gmin = k > 1 && k <= ngrp && ngrp <= 1024;
+    // the group-minima select bounds the k-th smallest d_hat by the k-th smallest GROUP minimum,
+    // loose when k nears the number of groups (C3: k = 64 of 128); the histogram select
+    // (k_select_small, DADE_OPT_GMIN_RATIO > 1 moves rows to it) measured slower even there
+    // (C3 probe 0.28 -> 0.45 ms, C2 at nprobe 64 0.555 -> 0.61 ms)
+    const bool use_gmin = k > 1 && (int64_t)k * x->opt.gmin_ratio <= ngrp && ngrp <= 1024;
     // the warp-specialised d_hat writer pays off for very wide rows (measured on C5, 65,536
     // columns: 1.42 -> 1.19 ms); up to 16,384 columns the one-tile-per-CTA kernel with 3 CTAs/SM
     // is faster (C2 68 vs 97 us, C4 222 vs 358 us, C3 36 vs 42 us)
@@ -2122,6 +2127,8 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_PCA_TC: in({0, 1}); g_pca_tc = (int)value; break;
     case DADE_OPT_SCAN_P1: in({0, 1}); o.scan_p1 = (int)value; break;
     case DADE_OPT_KNN_I8: in({0, 1}); o.knn_i8 = (int)value; break;
+    case DADE_OPT_GMIN_RATIO: DADE_REQUIRE(value >= 1 && value <= 1024, DADE_ERR_ARG, "gmin ratio not in [1, 1024]");
+      o.gmin_ratio = (int)value; break;
     case DADE_OPT_DHAT_CHUNK_MB: DADE_REQUIRE(value >= 0 && value <= 8192, DADE_ERR_ARG, "dhat chunk not in [0, 8192] MB");
       o.dhat_chunk_mb = (int)value; break;
     case DADE_OPT_FZ_CPC: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz cpc not in [0, 64]");
