@@ -63,6 +63,7 @@ struct Options {
   int fz_stages = 0;        // probe_fz.cu: B ring stages (0 auto)
   int fz_groups = 0;        // probe_fz.cu: epilogue groups of 4 warps (0 auto, 1, 2)
   int fz_cps = 0;           // probe_fz.cu: persistent CTAs per SM (0 auto = 1; 2 needs 1 group and smem <= 113 KB)
+  int fz_seed_stride = 0;   // probe_fz.cu: seed pass column-tile stride (0 auto: >= 16 k group minima, <= 16)
   int fz_cpc = 0;           // probe_fz.cu: 8 KB operand chunks per TMA copy (0 auto = 1)
 };
 
@@ -322,7 +323,16 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
       const int C = fz_cap(k);
       x->slack.reserve((size_t)chunk);
       x->cand.reserve(nl * C * 2 + nl);
-      x->fzseed.reserve(nl * k);
+      auto seed_plan = [&](int64_t rows, int* cs, int* P1, int* L1) {
+        fz_seed_plan(rows, n, k, ctas(rows), x->opt.fz_seed_stride, cs, P1, L1);
+      };
+      size_t nseed = 0;
+      for (int64_t rows : {chunk, last}) {
+        int cs, P1, L1;
+        seed_plan(rows, &cs, &P1, &L1);
+        nseed = std::max(nseed, (size_t)rows * L1 * G);
+      }
+      x->fzseed.reserve(std::max(nl, nseed) * k);
       for (int64_t r0 = 0; r0 < m; r0 += chunk) {
         const int64_t mm = std::min(chunk, m - r0);
         const void* Aop;
@@ -342,10 +352,12 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
           launch_slack(x->a_tc.norm.p, mm, bop.maxnorm, D, x->slack.p, x->stream, 1);
           Aop = x->a_tc.hi.p;
         }
+        int cs1, P1, L1;
+        seed_plan(mm, &cs1, &P1, &L1);
         launch_probe_fz(kind, Aop, x->a_tc.norm.p, ainv, mm, kind == 1 ? (const void*)bop.h16.p : (const void*)bop.hi.p,
                         bop.norm.p, bop.hinv_b, bop.maxnorm, n, D, k, x->slack.p, A + r0 * D, B, x->fzseed.p, x->cand.p,
-                        x->cand.p + nl * C * 2, ctas(mm), fz_lists_per_row(mm, n, ctas(mm)), G, S, cpc, out_idx + r0 * k,
-                        out_d64 ? out_d64 + r0 * k : nullptr, x->stream);
+                        x->cand.p + nl * C * 2, ctas(mm), fz_lists_per_row(mm, n, ctas(mm)), G, S, cpc, cs1, P1,
+                        L1, out_idx + r0 * k, out_d64 ? out_d64 + r0 * k : nullptr, x->stream);
       }
       if (sync) check_knn_flag(x);
       return;
@@ -2127,6 +2139,8 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_PCA_TC: in({0, 1}); g_pca_tc = (int)value; break;
     case DADE_OPT_SCAN_P1: in({0, 1}); o.scan_p1 = (int)value; break;
     case DADE_OPT_KNN_I8: in({0, 1}); o.knn_i8 = (int)value; break;
+    case DADE_OPT_FZ_SEED_STRIDE: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz seed stride not in [0, 64]");
+      o.fz_seed_stride = (int)value; break;
     case DADE_OPT_GMIN_RATIO: DADE_REQUIRE(value >= 1 && value <= 1024, DADE_ERR_ARG, "gmin ratio not in [1, 1024]");
       o.gmin_ratio = (int)value; break;
     case DADE_OPT_DHAT_CHUNK_MB: DADE_REQUIRE(value >= 0 && value <= 8192, DADE_ERR_ARG, "dhat chunk not in [0, 8192] MB");

@@ -142,7 +142,8 @@ int fz_nkc(int D, int kind);
 int fz_cap(int k);
 size_t fz_smem(int D, int kind, int k, int G, int S, int cpc);
 bool fz_config(int D, int kind, int k, int* G, int* S, int* cps);
-int fz_lists_per_row(int64_t m, int64_t n, int P);
+int fz_lists_per_row(int64_t m, int64_t n, int P, int cstride = 1);
+void fz_seed_plan(int64_t m, int64_t n, int k, int P, int force, int* cstride, int* P1, int* maxL1);
 // gscale > 0: one matrix scale; else per-row power-of-two scales (inv_scale[r] = 1/s_r, +inf if unbounded)
 void launch_split_h16(const float* X, int64_t rows, int D, const float* center, uint16_t* h, float* norm,
                       float* inv_scale, float gscale, cudaStream_t st);
@@ -151,7 +152,8 @@ void launch_slack_h16(const float* an, const float* ainv, int64_t m, float bmax,
 void launch_probe_fz(int kind, const void* Aop, const float* an, const float* ainv, int64_t m, const void* Bop,
                      const float* bn, float binv, float bmax, int64_t n, int D, int k, const float* slack,
                      const float* A, const float* B, float* seeds, int32_t* cand, int32_t* ccount, int P, int maxL,
-                     int G, int S, int cpc, int32_t* out_idx, double* out_d64, cudaStream_t st);
+                     int G, int S, int cpc, int cstride, int P1, int maxL1, int32_t* out_idx, double* out_d64,
+                     cudaStream_t st);
 
 // rotate.cu : x~ = R (x - mu) on the tensor cores (tcgen05 kind::i8, kRotSlices-way split with
 // exact int32 levels combined in fp64), stored fp32.

@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
     const unsigned char* __restrict__ Aop, const float* __restrict__ an, const float* __restrict__ ahs,
     const unsigned char* __restrict__ Bop, const float* __restrict__ bn, float bhs, float bmax, int nkc,
     int64_t m, int64_t n, int maxL, int k, int C, int G, int S, int cpc, const float* __restrict__ slack,
-    float* __restrict__ seeds, int32_t* __restrict__ cand, int32_t* __restrict__ ccount) {
+    float* __restrict__ seeds, int32_t* __restrict__ cand, int32_t* __restrict__ ccount, int cstride,
+    int nlists_seed) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* areg = sm;
   unsigned char* ring = sm + (size_t)nkc * kChunkBytes;
@@ -196,7 +197,9 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
   float* lists = bnbuf + 8 * kTM;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NB = 2 * G;
-  const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM;
+  // this launch's column tiles: every cstride-th of the row (MODE 1 may sample a subset: its
+  // seeds stay valid upper bounds), ntiles of them per row tile
+  const int64_t mt = (m + kTM - 1) / kTM, ntiles = ((n + kTM - 1) / kTM + cstride - 1) / cstride;
   const int64_t I = mt * ntiles, P = gridDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * I / P, i1 = ((int64_t)blockIdx.x + 1) * I / P;
   if (tid == 0) {
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
         for (int kc = 0; kc < nkc; ++kc)
           bulk_g2s(areg + (size_t)kc * kChunkBytes, Aop + (size_t)(rt * nkc + kc) * kChunkBytes, kChunkBytes, afull);
         for (; i < iend; ++i) {
-          const int64_t tn = i - rt * ntiles;
+          const int64_t tn = (i - rt * ntiles) * cstride;
           for (int kc = 0; kc < nkc; kc += cpc, ++it) {  // one copy per stage of cpc chunks
             const int s = it % S;
             if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
           // the tile's column norms into bnbuf[T mod 2NB] (last read for tile T - 2NB, finished before
           // the epilogue released tile T - NB's buffer), completing on tfull[b] with the accumulator
           mbar_expect_tx(&tfull[b], kTM * 4);
-          bulk_g2s(bnbuf + (T % (2 * NB)) * kTM, bn + (i - rt * ntiles) * kTM, kTM * 4, &tfull[b]);
+          bulk_g2s(bnbuf + (T % (2 * NB)) * kTM, bn + (i - rt * ntiles) * cstride * kTM, kTM * 4, &tfull[b]);
           if (MODE == 3 && blockIdx.x == 0 && T < 256) dbg[1024 + T] = clock64();
           const uint32_t acc = tmem + b * kTM;
           for (int kc = 0; kc < nkc; kc += cpc, ++it) {
@@ -308,9 +311,9 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
       int nl = 0;
       if (MODE == 2) {
         if (live && !ovf) {  // U = the k-th smallest of the union of the row's seeds
-          for (int l = 0; l < nlists; ++l)
+          for (int l = 0; l < nlists_seed; ++l)
             for (int e = 0; e < k; ++e) {
-              float x = seeds[((size_t)row * nlists + l) * k + e];
+              float x = seeds[((size_t)row * nlists_seed + l) * k + e];
 #pragma unroll
               for (int j = 0; j < KS; ++j) {
                 const float lo = fminf(kb[j], x);
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
         mbar_wait(&tfull[b], (uint32_t)(T / NB) & 1);
         if (MODE == 3 && blockIdx.x == 0 && T < 256 && lane == 0 && q == 2) reinterpret_cast<unsigned long long*>(seeds)[1536 + T] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int64_t cb0 = (i - rt * ntiles) * kTM;
+        const int64_t cb0 = (i - rt * ntiles) * cstride * kTM;
         const float* bns = bnbuf + (size_t)(T % (2 * NB)) * kTM;  // this tile's column norms
         // per 32-column chunk (v: the chunk's accumulators of this thread's row)
         auto chunk = [&](const uint32_t* v, int cb) {
@@ -674,8 +677,8 @@ bool fz_config(int D, int kind, int k, int* G, int* S, int* cps) {
 }
 
 // lists per row of the persistent split: CTAs covering one row tile (host mirror of fz_cta_of)
-int fz_lists_per_row(int64_t m, int64_t n, int P) {
-  const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM, I = mt * ntiles;
+int fz_lists_per_row(int64_t m, int64_t n, int P, int cstride) {
+  const int64_t mt = (m + kTM - 1) / kTM, ntiles = ((n + kTM - 1) / kTM + cstride - 1) / cstride, I = mt * ntiles;
   int mx = 1;
   for (int64_t rt = 0; rt < mt; ++rt) {
     const int64_t c0 = ((rt * ntiles + 1) * P - 1) / I, c1 = (((rt + 1) * ntiles) * P - 1) / I;
@@ -705,11 +708,12 @@ template <int KIND, int MODE, int KS>
 static void fz_launch(int P, unsigned threads, size_t smem, cudaStream_t st, const void* Aop, const float* an,
                       const float* ainv, const void* Bop, const float* bn, float binv, float bmax, int nkc, int64_t m,
                       int64_t n, int maxL, int k, int C, int G, int S, int cpc, const float* slack, float* seeds,
-                      int32_t* cand, int32_t* ccount) {
+                      int32_t* cand, int32_t* ccount, int cstride = 1, int nlists_seed = 0) {
   DADE_CK(cudaFuncSetAttribute(k_probe_fz<KIND, MODE, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_probe_fz<KIND, MODE, KS><<<P, threads, smem, st>>>(static_cast<const unsigned char*>(Aop), an, ainv,
                                                        static_cast<const unsigned char*>(Bop), bn, binv, bmax, nkc, m,
-                                                       n, maxL, k, C, G, S, cpc, slack, seeds, cand, ccount);
+                                                       n, maxL, k, C, G, S, cpc, slack, seeds, cand, ccount, cstride,
+                                                       nlists_seed);
   DADE_CK(cudaGetLastError());
 }
 
@@ -719,25 +723,43 @@ template <int KIND, int KS>
 static void fz_two_pass(int P, unsigned threads, size_t smem, cudaStream_t st, const void* Aop, const float* an,
                         const float* ainv, const void* Bop, const float* bn, float binv, float bmax, int nkc,
                         int64_t m, int64_t n, int maxL, int k, int C, int G, int S, int cpc, const float* slack,
-                        float* seeds, int32_t* cand, int32_t* ccount) {
+                        float* seeds, int32_t* cand, int32_t* ccount, int cstride, int maxL1, int P1) {
   if (g_fz_debug) {
     if (g_fz_debug == 1)
       fz_launch<KIND, 0, KS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S,
-                             cpc, slack, seeds, cand, ccount);
+                             cpc, slack, seeds, cand, ccount, 1, 0);
     else
       fz_launch<KIND, 3, KS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S,
-                             cpc, slack, seeds, cand, ccount);
+                             cpc, slack, seeds, cand, ccount, 1, 0);
   }
-  fz_launch<KIND, 1, KS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S, cpc,
-                         slack, seeds, cand, ccount);
+  // seed pass over every cstride-th column tile (its own persistent split: P1 CTAs, maxL1 lists
+  // per row), then the select pass over all columns, reading maxL1 G seed lists per row
+  fz_launch<KIND, 1, KS>(P1, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL1, k, C, G, S, cpc,
+                         slack, seeds, cand, ccount, cstride, 0);
   fz_launch<KIND, 2, KS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S, cpc,
-                         slack, seeds, cand, ccount);
+                         slack, seeds, cand, ccount, 1, maxL1 * G);
+}
+
+// The seed pass samples every cstride-th column tile so that >= 64 k group minima remain (their
+// k-th smallest is still an upper bound of the row's k-th smallest d_hat; the select pass then
+// starts from a somewhat wider window): on the C5 shard (512 column tiles, k = 8) one tile in 4.
+// Measured there (tools/exp_probe_fz.py): probe 1.207 / 1.006 / 1.154 / 1.353 ms at strides
+// 1 / 4 / 8 / 16 — sparser seeds cost the select pass more than they save. Its persistent split
+// has P1 CTAs and maxL1 seed lists per row.
+void fz_seed_plan(int64_t m, int64_t n, int k, int P, int force, int* cstride, int* P1, int* maxL1) {
+  const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM;
+  int64_t cs = force > 0 ? force : std::max<int64_t>(1, std::min<int64_t>(16, ntiles / (16 * (int64_t)k)));
+  *cstride = (int)cs;
+  const int64_t nts = (ntiles + cs - 1) / cs;
+  *P1 = (int)std::min<int64_t>(P, mt * nts);
+  *maxL1 = fz_lists_per_row(m, n, *P1, (int)cs);
 }
 
 void launch_probe_fz(int kind, const void* Aop, const float* an, const float* ainv, int64_t m, const void* Bop,
                      const float* bn, float binv, float bmax, int64_t n, int D, int k, const float* slack,
                      const float* A, const float* B, float* seeds, int32_t* cand, int32_t* ccount, int P, int maxL,
-                     int G, int S, int cpc, int32_t* out_idx, double* out_d64, cudaStream_t st) {
+                     int G, int S, int cpc, int cstride, int P1, int maxL1, int32_t* out_idx, double* out_d64,
+                     cudaStream_t st) {
   if (m <= 0) return;
   DADE_REQUIRE(k >= 1 && k <= 32, DADE_ERR_UNSUPPORTED, "probe: fused filter needs k <= 32");
   const int C = fz_cap(k);
@@ -745,12 +767,13 @@ void launch_probe_fz(int kind, const void* Aop, const float* an, const float* ai
   DADE_REQUIRE(cpc >= 1 && fz_nkc(D, kind) % cpc == 0, DADE_ERR_ARG, "fz: chunks per copy must divide the chunks per tile");
   DADE_REQUIRE(smem <= 227 * 1024, DADE_ERR_UNSUPPORTED, "probe: operands too wide for the fused filter");
   // seeds of rows / segments a CTA never covers stay huge (0x7f7f7f7f = 3.4e38: never below U)
-  DADE_CK(cudaMemsetAsync(seeds, 0x7f, sizeof(float) * (size_t)m * maxL * G * k, st));
+  DADE_CK(cudaMemsetAsync(seeds, 0x7f, sizeof(float) * (size_t)m * maxL1 * G * k, st));
   DADE_CK(cudaMemsetAsync(ccount, 0, sizeof(int32_t) * (size_t)m * maxL * G, st));
   const unsigned threads = 64 + 128 * G;
   const int nkc = fz_nkc(D, kind);
   const float bi = kind == 1 ? binv : 1.f;
-#define FZ_ARGS P, threads, smem, st, Aop, an, ainv, Bop, bn, bi, bmax, nkc, m, n, maxL, k, C, G, S, cpc, slack, seeds, cand, ccount
+#define FZ_ARGS P, threads, smem, st, Aop, an, ainv, Bop, bn, bi, bmax, nkc, m, n, maxL, k, C, G, S, cpc, slack, seeds, cand, ccount, \
+                cstride, maxL1, P1
   if (kind == 1) {
     if (k <= 8) fz_two_pass<1, 8>(FZ_ARGS);
     else if (k <= 16) fz_two_pass<1, 16>(FZ_ARGS);

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--paths", default="1,2,4,5")
     ap.add_argument("--nq", type=int, default=0)
+    ap.add_argument("--seed-stride", default="", help="comma list of DADE_OPT_FZ_SEED_STRIDE values (path 4)")
     ap.add_argument("--gmin-ratio", default="", help="comma list of DADE_OPT_GMIN_RATIO values (path 0)")
     ap.add_argument("--chunk-mb", default="", help="comma list of DADE_OPT_DHAT_CHUNK_MB values (path 1)")
     ap.add_argument("--debug", type=int, default=0, help="fz_debug option (1/2: pipeline-only launch first)")
@@ -51,12 +52,14 @@ def main():
     runs += [(4, tuple(int(v) for v in f.split(":"))) for f in a.fz.split(",") if f]
     runs += [(1, ("chunk_mb", int(v))) for v in a.chunk_mb.split(",") if v]
     runs += [(0, ("gmin_ratio", int(v))) for v in a.gmin_ratio.split(",") if v]
+    runs += [(4, ("seed_stride", int(v))) for v in a.seed_stride.split(",") if v]
     for path, fz in runs:
         ix.set_option("knn_path", path)
-        ix.set_option("gmin_ratio", fz[1] if fz and fz[0] == "gmin_ratio" else 8)
+        ix.set_option("gmin_ratio", fz[1] if fz and fz[0] == "gmin_ratio" else 1)
+        ix.set_option("fz_seed_stride", fz[1] if fz and fz[0] == "seed_stride" else 0)
         if fz and fz[0] == "chunk_mb":
             ix.set_option("dhat_chunk_mb", fz[1])
-        elif fz and fz[0] == "gmin_ratio":
+        elif fz and fz[0] in ("gmin_ratio", "seed_stride"):
             pass
         else:
             ix.set_option("dhat_chunk_mb", 0)
