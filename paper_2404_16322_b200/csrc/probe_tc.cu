@@ -662,8 +662,9 @@ __device__ __forceinline__ bool cless(double d0, int32_t c0, double d1, int32_t 
 }
 
 constexpr int kFinWarps = 4;
-constexpr int kFinCap = 512;   // candidates per row held at once (running top-k beyond that)
-constexpr size_t kFinWarpBytes = (size_t)kFinCap * (8 + 4 * 4) + 256 * 4;
+constexpr int kFinCapMax = 512;  // candidates per row held at once (running top-k beyond that)
+// per-warp shared memory for a capacity: cd | cc | sel | ucol | udh | hist[256]
+__host__ __device__ constexpr size_t fin_warp_bytes(int cap) { return (size_t)cap * (8 + 4 * 4) + 256 * 4; }
 
 // exact distance of one candidate column per lane (c < 0 = none), accumulated sequentially over
 // j = 0..D-1 in fp64 (R20). Each lane streams its own candidate row with 16-B loads (the row is
@@ -676,7 +677,7 @@ __device__ __forceinline__ double exact_batch(const float* __restrict__ a, const
   if ((D & 3) == 0) {
     const float4* a4 = reinterpret_cast<const float4*>(a);
     const float4* b4 = reinterpret_cast<const float4*>(b);
-#pragma unroll 4
+#pragma unroll 8
     for (int j = 0; j < D / 4; ++j) {
       const float4 y = __ldg(b4 + j), x = __ldg(a4 + j);
       double t = __dsub_rn((double)x.x, (double)y.x);
@@ -700,11 +701,11 @@ __device__ __forceinline__ double exact_batch(const float* __restrict__ a, const
 __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
     const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount, int nsplit, int C, int64_t m,
     int64_t n, int k, const float* __restrict__ A, const float* __restrict__ B, int D,
-    const float* __restrict__ slack, int32_t* __restrict__ out_idx, double* __restrict__ out_d) {
+    const float* __restrict__ slack, int32_t* __restrict__ out_idx, double* __restrict__ out_d, int kFinCap) {
   extern __shared__ __align__(16) unsigned char fs[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // per-warp region: cd | cc | sel | ucol | udh | hist[256]
-  unsigned char* base = fs + (size_t)w * kFinWarpBytes;
+  unsigned char* base = fs + (size_t)w * fin_warp_bytes(kFinCap);
   double* cd = reinterpret_cast<double*>(base);
   int32_t* cc = reinterpret_cast<int32_t*>(cd + kFinCap);
   int32_t* sel = cc + kFinCap;
@@ -715,12 +716,28 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
   const int64_t row = (int64_t)blockIdx.x * kFinWarps + w;
   if (row >= m) return;
   const float* a = A + row * (int64_t)D;
+  // list counts: lane s holds list s's (nsplit <= 32: one load per lane, all in flight at once),
+  // their exclusive prefix places each list in the union
   bool full_scan = false;
-  int total = 0;
-  for (int s = 0; s < nsplit; ++s) {
-    const int c = ccount[row * nsplit + s];
-    full_scan |= c < 0;
-    total += c < 0 ? 0 : c;
+  int total = 0, my_c = 0, my_off = 0;
+  if (nsplit <= 32) {
+    my_c = lane < nsplit ? ccount[row * nsplit + lane] : 0;
+    full_scan = __any_sync(0xffffffffu, my_c < 0);
+    const int c = my_c < 0 ? 0 : my_c;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    my_off = inc - c;
+    total = __shfl_sync(0xffffffffu, inc, 31);
+  } else {
+    for (int s = 0; s < nsplit; ++s) {
+      const int c = ccount[row * nsplit + s];
+      full_scan |= c < 0;
+      total += c < 0 ? 0 : c;
+    }
   }
   for (int i = lane; i < k; i += 32) { cd[i] = DBL_MAX; cc[i] = 0x7fffffff; }
   int cnt = k;
@@ -751,21 +768,34 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
     __syncwarp();
   };
   if (!full_scan && total >= k) {
-    // stage the union (column, d_hat bits) in shared memory once
-    int nu = 0;
-    for (int s = 0; s < nsplit; ++s) {
-      const int nc = ccount[row * nsplit + s];
-      const int32_t* cl = cand + (row * nsplit + s) * (int64_t)C * 2;
-      for (int i = lane; i < nc; i += 32) {
-        if (nu + i < kFinCap) {
+    // stage the union (column, d_hat bits) in shared memory once; with the counts and offsets in
+    // registers the lists' loads do not wait on one another
+    if (total > kFinCap) {
+      full_scan = true;
+    } else if (nsplit <= 32) {
+#pragma unroll 4
+      for (int s = 0; s < nsplit; ++s) {
+        const int nc = __shfl_sync(0xffffffffu, my_c, s), o = __shfl_sync(0xffffffffu, my_off, s);
+        const int2* cl = reinterpret_cast<const int2*>(cand + (row * nsplit + s) * (int64_t)C * 2);
+        for (int i = lane; i < nc; i += 32) {
+          const int2 e = __ldg(cl + i);
+          ucol[o + i] = e.x;
+          udh[o + i] = (unsigned)e.y;
+        }
+      }
+    } else {
+      int nu = 0;
+      for (int s = 0; s < nsplit; ++s) {
+        const int nc = ccount[row * nsplit + s];
+        const int32_t* cl = cand + (row * nsplit + s) * (int64_t)C * 2;
+        for (int i = lane; i < nc; i += 32) {
           ucol[nu + i] = cl[2 * i];
           udh[nu + i] = (unsigned)cl[2 * i + 1];
         }
+        nu += nc;
       }
-      nu += nc;
     }
     __syncwarp();
-    if (nu > kFinCap) full_scan = true;
   }
   if (full_scan || total < k) {
     for (int64_t c0 = 0; c0 < n; c0 += 32) add32(c0 + lane < n ? (int32_t)(c0 + lane) : -1);
@@ -913,10 +943,15 @@ void launch_probe_tc(const float* Ahi, const float* Alo, const float* an, int64_
 void launch_probe_finish(const int32_t* cand, const int32_t* ccount, int nlists, int C, int64_t m, int64_t n, int k,
                          const float* A, const float* B, int D, const float* slack, int32_t* out_idx, double* out_d64,
                          cudaStream_t st) {
-  const size_t fsm = (size_t)kFinWarps * kFinWarpBytes;
+  // capacity: the union of the lists (nlists x C) rounded up, so small unions leave room for more
+  // resident CTAs (C5 shard: 256 instead of 512 -> 7 CTAs per SM instead of 4 on the gathers)
+  // (a power of two: the bitonic compaction sorts up to the next power of two of its count)
+  int cap = 64;
+  while (cap < kFinCapMax && cap < (int64_t)nlists * C + 32) cap <<= 1;
+  const size_t fsm = (size_t)kFinWarps * fin_warp_bytes(cap);
   DADE_CK(cudaFuncSetAttribute(k_probe_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));  // per launch: per device
   k_probe_finish<<<(unsigned)((m + kFinWarps - 1) / kFinWarps), kFinWarps * 32, fsm, st>>>(
-      cand, ccount, nlists, C, m, n, k, A, B, D, slack, out_idx, out_d64);
+      cand, ccount, nlists, C, m, n, k, A, B, D, slack, out_idx, out_d64, cap);
   DADE_CK(cudaGetLastError());
 }
 
