@@ -369,8 +369,9 @@ def run_dade(args):
 
 def launches_per_search(cfg, world, nprobe):
     """Kernels of ours per dade_search (mirrors exact_knn's path choice in dade_api.cu):
-    k_check_finite; k_rot_slice + k_rot_i8 per 2^20 queries (rotate.cu); per probe row chunk either the fused path (> 1024 64-column
-    groups) k_split_tf32, k_slack, k_probe_tc, k_probe_finish, or the group-minima path
+    k_check_finite; k_rot_slice + k_rot_i8 per 2^20 queries (rotate.cu); per probe row chunk either the fused fp16 path
+    (> 32,768 centroids, k <= 32, D <= 256) k_split_h16, k_slack_h16, k_probe_fz x 2, k_probe_finish, the fused
+    tf32 path (> 1024 64-column groups) k_split_tf32, k_slack, k_probe_tc, k_probe_finish, or the group-minima path
     (> 2^20 centroids) k_split_tf32, k_l2_tc, k_slack, k_select_groups, or the d_hat path
     k_split_tf32, k_l2_tc | k_dhat_tc, k_slack, k_select_gmin, k_select_small; the query order
     (k_lpt_key, k_order_offsets, k_key_scatter); k_scan;
@@ -380,6 +381,10 @@ def launches_per_search(cfg, world, nprobe):
     rows_pad = -(-nq // 128) * 128
     if n <= 1:
         probe = 0
+    elif k <= 32 and n > 32768 and cfg.d <= 256:
+        # the fused fp16 filter (probe_fz.cu): k_split_h16, k_slack_h16, the seed and select
+        # passes of k_probe_fz, k_probe_finish per row chunk
+        probe = 5 * -(-nq // min(rows_pad, 65536))
     elif k <= 64 and n >= 256 and (n + 63) // 64 > 1024:
         probe = 4 * -(-nq // min(rows_pad, 65536))
     elif k <= 512 and 4 * k <= (n + 31) // 32 and n > (1 << 20):

@@ -39,8 +39,8 @@ def test_launch_count_claim():
     assert bench.launches_per_search(synth.config("c2"), 2, 8) == 13
     # flat (one list): no probe kernels
     assert bench.launches_per_search(synth.config("c1"), 1, 1) == 7
-    # C5 shard (65,536 lists): d_hat path in two row chunks of 8,192
-    assert bench.launches_per_search(synth.config("c5").scaled(n=12_500_000, nlist=65536), 1, 8) == 17
+    # C5 shard (65,536 lists): the fused fp16 filter (split, slack, seed pass, select pass, finish)
+    assert bench.launches_per_search(synth.config("c5").scaled(n=12_500_000, nlist=65536), 1, 8) == 12
     # C3 (1,000 queries, nprobe 64): one chunk
     assert bench.launches_per_search(synth.config("c3").scaled(nq=1000), 1, 64) == 12
 
