@@ -332,7 +332,8 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
         seed_plan(rows, &cs, &P1, &L1);
         nseed = std::max(nseed, (size_t)rows * L1 * G);
       }
-      x->fzseed.reserve(std::max(nl, nseed) * k);
+      // (>= 4,096 floats: the pipeline-only measurement build records its timeline there)
+      x->fzseed.reserve(std::max<size_t>(std::max(nl, nseed) * k, 4096));
       for (int64_t r0 = 0; r0 < m; r0 += chunk) {
         const int64_t mm = std::min(chunk, m - r0);
         const void* Aop;
