@@ -19,6 +19,19 @@
 
 #include "dade_internal.h"
 
+// DADE_DEBUG_CHECKS builds (tools/build_variant.py; compute-sanitizer is closed on the GPU pool):
+// device-side invariants — a violation traps and the next synchronising call reports it
+#ifdef DADE_DEBUG_CHECKS
+#define DADE_DCHECK(c) \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define DADE_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace dade {
 
 namespace {
@@ -164,6 +177,7 @@ __global__ void __launch_bounds__(kP1Rows) k_p1_fill(const float* __restrict__ l
           float s = 0.f;
 #pragma unroll
           for (int bb = 0; bb < DD; ++bb) s += block_sum(x[bb], &qsh[j][bb * 16]);
+          DADE_DCHECK((int64_t)osh[j] + r0 + t < *total);
           p1[(int64_t)osh[j] + r0 + t] = s;
         }
       }

@@ -41,6 +41,19 @@
 
 #include "dade_internal.h"
 
+// DADE_DEBUG_CHECKS builds (tools/build_variant.py; compute-sanitizer is closed on the GPU pool):
+// device-side invariants — a violation traps and the next synchronising call reports it
+#ifdef DADE_DEBUG_CHECKS
+#define DADE_DCHECK(c) \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define DADE_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace dade {
 
 namespace {
@@ -474,6 +487,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
               over = nlr + ni > C;  // > C near-ties inside the window: k_probe_finish rescans the row
             }
             if (!over) {
+              DADE_DCHECK(nlr + ni <= C && jseg >= 0 && jseg < maxL && c0 + lane < ((n + kTM - 1) / kTM) * kTM);
               if (in) L[nlr + __popc(im & lt)] = make_int2((int32_t)(c0 + lane), (int32_t)__float_as_uint(dc));
               nlr += ni;
             }
@@ -518,6 +532,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
       const int64_t slot = ((int64_t)row * maxL + jseg) * G + g;
       if (MODE == 1) {
         if (live) {
+          DADE_DCHECK(jseg >= 0 && jseg < maxL);
 #pragma unroll
           for (int j = 0; j < KS; ++j)
             if (j < k) seeds[slot * k + j] = kb[j];

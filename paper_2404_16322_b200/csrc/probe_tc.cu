@@ -25,6 +25,19 @@
 #include "dade_internal.h"
 #include "exact_batch.cuh"
 
+// DADE_DEBUG_CHECKS builds (tools/build_variant.py; compute-sanitizer is closed on the GPU pool):
+// device-side invariants — a violation traps and the next synchronising call reports it
+#ifdef DADE_DEBUG_CHECKS
+#define DADE_DCHECK(c) \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define DADE_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace dade {
 
 namespace {
@@ -778,6 +791,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) k_probe_finish(
         const int nc = __shfl_sync(0xffffffffu, my_c, s), o = __shfl_sync(0xffffffffu, my_off, s);
         const int2* cl = reinterpret_cast<const int2*>(cand + (row * nsplit + s) * (int64_t)C * 2);
         for (int i = lane; i < nc; i += 32) {
+          DADE_DCHECK(o + i < kFinCap && nc <= C);
           const int2 e = __ldg(cl + i);
           ucol[o + i] = e.x;
           udh[o + i] = (unsigned)e.y;

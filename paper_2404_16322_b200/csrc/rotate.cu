@@ -34,6 +34,19 @@
 
 #include "dade_internal.h"
 
+// DADE_DEBUG_CHECKS builds (tools/build_variant.py; compute-sanitizer is closed on the GPU pool):
+// device-side invariants — a violation traps and the next synchronising call reports it
+#ifdef DADE_DEBUG_CHECKS
+#define DADE_DCHECK(c) \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define DADE_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace dade {
 
 namespace {
@@ -330,6 +343,7 @@ __global__ void __launch_bounds__(320, 1) k_rot_i8(const int8_t* __restrict__ As
               *reinterpret_cast<float4*>(rm_out + p * D + i0 + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
           }
           if (dist_out) {  // distance mode (exact_knn's int8 filter): an + bn - 2 <a, b> in fp64 -> fp32
+            DADE_DCHECK(r < rows && (i0 & 15) == 0);
             const double a2 = an64[r];
             float mn = INFINITY;
             float dv[16];
