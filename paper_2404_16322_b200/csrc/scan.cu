@@ -50,6 +50,9 @@ constexpr int TR = 32;            // rows per tile: one row per lane
 #ifndef DADE_EPOCH_GROWTH  // R13: epoch boundaries c0, 2 c0, 4 c0, ... (experiment builds may change it)
 #define DADE_EPOCH_GROWTH 2
 #endif
+#ifndef DADE_SCAN_STREAM0  // 0: epoch 0 through stage 1 + gather rounds like later epochs (experiment builds)
+#define DADE_SCAN_STREAM0 1
+#endif
 constexpr unsigned long long kKeyInf = ~0ull;
 
 struct __align__(16) QEntry {
@@ -330,6 +333,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   constexpr int kQCap = SL::QCAP;
   constexpr int kStages = SL::kStages;
   constexpr int TB = SL::TB;
+  constexpr bool kStream0 = DADE_SCAN_STREAM0 && !PQ && !RES && DD >= 2;  // epoch-0 streaming (below)
   const int D = p.D, K = p.K;
   const int G = MULTI ? (blockDim.x >> 5) : 1;  // warps per query (power of two)
   const int lane = threadIdx.x & 31, warp = MULTI ? threadIdx.x >> 5 : 0;
@@ -472,8 +476,34 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         (!PQ && !RES && p.p1 && *p.p1_total <= p.p1_cap) ? p.p1 + p.p1_base[q] : nullptr;
     int2 pl = p.nprobe > 0 ? lists[0] : make_int2(0, 0);
     int issued = 0;
+    // Epoch-0 streaming: while tau is +inf (epoch 0 of a search that starts from an empty queue
+    // and no exchanged bound) nothing can be pruned, so every candidate of epoch 0 is read in
+    // full. Instead of stage 1 + gather rounds, its 32-row group is streamed by TMA as nblk / DD
+    // sub-tiles of DD blocks each (contiguous in the blocked layout) and the exact distance is
+    // accumulated in a register, block by block in block order (R21). Warp-uniform.
+    const bool stream0 = kStream0 && !p1q && nblk > DD && p.ep_first == 0 && !p.init_ids &&
+                         *qtcap == INFINITY;
+    // (DD = 1 kernels: C2 / C4 run 80-register warps whose epoch 0 is <= 9% of the dims read;
+    // the extra state would spill there)
+    int sb = 0, srow0 = 0, snr = 0;  // stream0: next sub-tile block of the current row group
     auto issue = [&](int slot) -> bool {
-      int row0, nr, sp;
+      int row0, nr, sp, b0 = -1;
+      if (kStream0 && sb > 0) {  // the next sub-tile of an epoch-0 row group (same warp, same rows)
+        row0 = srow0;
+        nr = snr;
+        b0 = sb;
+        sb = b0 + DD < nblk ? b0 + DD : 0;
+        if (lane == 0) {
+          meta[slot] = TileMeta{row0, nr, 0, b0 + 1};
+          mbar_expect_tx(&mbar[slot], (uint32_t)nr * 64u * DD);
+#pragma unroll
+          for (int bb = 0; bb < DD; ++bb)
+            bulk_g2s(tiles + slot * TB + bb * TR * 64, lay + (((int64_t)(b0 + bb) * n + row0) << 4),
+                     (uint32_t)nr * 64u, &mbar[slot]);
+        }
+        ++issued;
+        return true;
+      }
       for (;;) {
         if (pr >= L) return false;
         if (pr >= pe_hi) {
@@ -492,8 +522,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         DADE_DCHECK(nr >= 1 && nr <= TR && row0 >= 0 && (int64_t)row0 + nr <= n);
         if (!MULTI || (tix++ & (G - 1)) == warp) break;
       }
+      if (stream0 && pep == 0) {  // first sub-tile of an epoch-0 row group
+        srow0 = row0;
+        snr = nr;
+        sb = DD;
+      }
       if (lane == 0) {
-        meta[slot] = TileMeta{row0, nr, pep, 0};
+        meta[slot] = TileMeta{row0, nr, pep, stream0 && pep == 0 ? 1 : 0};
         if (!PQ && !RES && p1q) {  // the tile's precomputed stage-1 values: 16-B aligned superset
           const uintptr_t a = reinterpret_cast<uintptr_t>(p1q + sp), a0 = a & ~(uintptr_t)15;
           const uint32_t bytes = (uint32_t)(((a + 4u * (uint32_t)nr + 15) & ~(uintptr_t)15) - a0);
@@ -678,6 +713,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
     // ---------------------------------------------------- consumer (one call site per action)
     bool ready = false;  // the tile in `slot` has landed and its meta is read
     TileMeta tm{0, 0, 0, 0};
+    float sacc = 0.f;     // stream0: the lane's row distance over the sub-tiles consumed so far
+    uint32_t sgid = 0u;   // stream0: the lane's row id
     for (;;) {
       const int qlen = tail - head;
       bool round = qlen >= kRoundQ, drain = false, ep_end = false;
@@ -745,8 +782,44 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
         PROF_MARK(5);
         continue;
       }
-      // stage 1 (qlen < 32: the ring has room for 32 more): one row per lane, DD blocks
       const unsigned char* trow = tiles + slot * TB + lane * 64;
+      if (kStream0 && stream0 && tm.pad > 0) {  // epoch-0 sub-tile: DD more blocks of every row's distance
+        const int b0 = tm.pad - 1;
+        const bool val0 = lane < tm.nr;
+        if (b0 == 0) {
+          sacc = 0.f;
+          sgid = val0 ? (uint32_t)__ldg(p.row_id + tm.row0 + lane) : 0u;
+        }
+#pragma unroll
+        for (int bb = 0; bb < DD; ++bb) {
+          unsigned long long x[8];
+          const float* qc[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int ch = (c + lane) & 3;
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(trow + bb * TR * 64 + ch * 16);
+            x[2 * c] = v.x;
+            x[2 * c + 1] = v.y;
+            qc[c] = qs + (b0 + bb) * 16 + ch * 4;
+          }
+          sacc += block_sum_rot(x, qc);
+        }
+        __syncwarp();
+        ++consumed;
+        ready = false;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(slot);
+        if (stats && b0 == 0) c_tested += tm.nr;
+        if (b0 + DD >= nblk) {  // d = D: exact distance, no test (R10)
+          if (LOG && val0) log_decision(p, q, (int32_t)sgid, D);
+          if (stats) c_surv += __popc(__ballot_sync(0xffffffffu, val0));
+          const unsigned long long key = val0 ? make_key(sacc, sgid) : kKeyInf;
+          tk.offer(!MULTI || key < cap ? key : kKeyInf, lane);
+        }
+        PROF_MARK(5);
+        continue;
+      }
+      // stage 1 (qlen < 32: the ring has room for 32 more): one row per lane, DD blocks
       float s = 0.f, sq = 0.f;
       const float xn = RES && val ? __ldg(p.xnorm + tm.row0 + lane) : 0.f;
       if (!RES && p1q) {  // list-major precompute (p1.cu): the same block sums, read as one float
