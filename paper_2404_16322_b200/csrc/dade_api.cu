@@ -65,6 +65,8 @@ struct Options {
   int fz_cps = 0;           // probe_fz.cu: persistent CTAs per SM (0 auto = 1; 2 needs 1 group and smem <= 113 KB)
   int fz_seed_stride = 0;   // probe_fz.cu: seed pass column-tile stride (0 auto: >= 16 k group minima, <= 16)
   int fz_cpc = 0;           // probe_fz.cu: 8 KB operand chunks per TMA copy (0 auto = 1)
+  int fz_rows = 0;          // probe_fz.cu: 128-row A tiles per CTA sharing the B stream (0 auto, 1, 2)
+  int fz_cols = 0;          // probe_fz.cu: epilogue groups per accumulator, column shares (0 auto, 1, 2)
 };
 
 struct dade_index {
@@ -262,7 +264,7 @@ void tc_prepare_h16(dade_index* x, const float* B, TcOp& op) {
   const int e = std::min(60, 14 - E);
   if (e < -60) return;
   const float sc = std::ldexp(1.f, e);
-  op.h16.reserve((size_t)tc_rows_pad(op.rows) * fz_nkc(D, 1) * 32);  // 32 halves per row per chunk
+  op.h16.reserve((size_t)fz_rows_pad(op.rows) * fz_nkc(D, 1) * 32);  // 32 halves per row per chunk
   launch_split_h16(B, op.rows, D, op.center.p, op.h16.p, nullptr, nullptr, sc, x->stream);
   op.hinv_b = 1.f / sc;
   op.h16_ok = true;
@@ -297,17 +299,28 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     // auto: only for very wide rows (> 32,768 columns, the C5 shard's 65,536 lists) — measured
     // (tools/exp_probe_fz.py): C5 shard 1.42 -> 0.95 ms, but slower than the d_hat path at 4,096
     // and 16,384 columns (C2, C4), where the d_hat matrix is small
-    int cps = 1;
+    int cps = 1, RP = 1, CS = 1;
     bool fz = passes == 1 && k <= 32 && n >= 256 && (path ? (path == 4 || path == 5) : n > 32768) &&
-              (kind == 0 || bop.h16_ok) && fz_config(D, kind, k, &G, &S, &cps);
+              (kind == 0 || bop.h16_ok) && fz_config(D, kind, k, &G, &S, &cps, &RP);
     int cpc = 1;
-    if (fz && (x->opt.fz_groups || x->opt.fz_stages || x->opt.fz_cps || x->opt.fz_cpc)) {  // measurement overrides
+    if (fz && (x->opt.fz_groups || x->opt.fz_stages || x->opt.fz_cps || x->opt.fz_cpc || x->opt.fz_rows ||
+               x->opt.fz_cols)) {
+      // measurement overrides
       if (x->opt.fz_groups) G = x->opt.fz_groups;
       if (x->opt.fz_stages) S = x->opt.fz_stages;
       if (x->opt.fz_cps) cps = x->opt.fz_cps;
       if (x->opt.fz_cpc) cpc = x->opt.fz_cpc;
-      DADE_REQUIRE(fz_smem(D, kind, k, G, S, cpc) * cps <= 226 * 1024 && (cps == 1 || G == 1), DADE_ERR_UNSUPPORTED,
-                   "fz options: shared memory or TMEM does not fit");
+      if (x->opt.fz_rows) RP = x->opt.fz_rows;
+      if (x->opt.fz_cols) CS = x->opt.fz_cols;
+      if (RP == 2 || CS == 2) {  // row-tile pairs: one group, one CTA per SM, the deepest ring that fits
+        if (!x->opt.fz_groups) G = 1;
+        if (!x->opt.fz_cps) cps = 1;
+        if (!x->opt.fz_stages)
+          for (S = 12; S > 3 && fz_smem(D, kind, k, G, S, cpc, RP, CS) * cps > 226 * 1024; --S) {}
+      }
+      DADE_REQUIRE(fz_smem(D, kind, k, G, S, cpc, RP, CS) * cps <= 226 * 1024 && (cps == 1 || G == 1) &&
+                       (RP == 1 || (kind == 1 && G == 1)) && (CS == 1 || kind == 1) && G * RP * CS * cps <= 4,
+                   DADE_ERR_UNSUPPORTED, "fz options: shared memory or TMEM does not fit");
     }
     if (fz) {
       int sms = 0;
@@ -315,22 +328,22 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
       const int64_t chunk = std::min<int64_t>(tc_rows_pad(m), 65536);
       // persistent: one CTA per SM (at most one per (row tile, column tile) pair)
       auto ctas = [&](int64_t rows) {
-        return (int)std::min<int64_t>((int64_t)sms * cps, ((rows + 127) / 128) * ((n + 127) / 128));
+        return (int)std::min<int64_t>((int64_t)sms * cps, ((rows + 128 * RP - 1) / (128 * RP)) * ((n + 127) / 128));
       };
       const int64_t last = m - (m - 1) / chunk * chunk;  // rows of the last chunk
-      const size_t nl = (size_t)G * std::max((size_t)chunk * fz_lists_per_row(chunk, n, ctas(chunk)),
-                                             (size_t)last * fz_lists_per_row(last, n, ctas(last)));
+      const size_t nl = (size_t)G * CS * std::max((size_t)chunk * fz_lists_per_row(chunk, n, ctas(chunk), 1, RP),
+                                             (size_t)last * fz_lists_per_row(last, n, ctas(last), 1, RP));
       const int C = fz_cap(k);
       x->slack.reserve((size_t)chunk);
       x->cand.reserve(nl * C * 2 + nl);
       auto seed_plan = [&](int64_t rows, int* cs, int* P1, int* L1) {
-        fz_seed_plan(rows, n, k, ctas(rows), x->opt.fz_seed_stride, cs, P1, L1);
+        fz_seed_plan(rows, n, k, ctas(rows), x->opt.fz_seed_stride, cs, P1, L1, RP);
       };
       size_t nseed = 0;
       for (int64_t rows : {chunk, last}) {
         int cs, P1, L1;
         seed_plan(rows, &cs, &P1, &L1);
-        nseed = std::max(nseed, (size_t)rows * L1 * G);
+        nseed = std::max(nseed, (size_t)rows * L1 * G * CS);
       }
       // (>= 4,096 floats: the pipeline-only measurement build records its timeline there)
       x->fzseed.reserve(std::max<size_t>(std::max(nl, nseed) * k, 4096));
@@ -339,7 +352,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
         const void* Aop;
         const float* ainv = nullptr;
         if (kind == 1) {
-          const int64_t rp = tc_rows_pad(mm);
+          const int64_t rp = fz_rows_pad(mm);
           x->a_tc.h16.reserve((size_t)rp * fz_nkc(D, 1) * 32);  // 32 halves per row per chunk
           x->a_tc.hinv.reserve((size_t)rp);
           x->a_tc.norm.reserve((size_t)rp);
@@ -357,8 +370,8 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
         seed_plan(mm, &cs1, &P1, &L1);
         launch_probe_fz(kind, Aop, x->a_tc.norm.p, ainv, mm, kind == 1 ? (const void*)bop.h16.p : (const void*)bop.hi.p,
                         bop.norm.p, bop.hinv_b, bop.maxnorm, n, D, k, x->slack.p, A + r0 * D, B, x->fzseed.p, x->cand.p,
-                        x->cand.p + nl * C * 2, ctas(mm), fz_lists_per_row(mm, n, ctas(mm)), G, S, cpc, cs1, P1,
-                        L1, out_idx + r0 * k, out_d64 ? out_d64 + r0 * k : nullptr, x->stream);
+                        x->cand.p + nl * C * 2, ctas(mm), fz_lists_per_row(mm, n, ctas(mm), 1, RP), G, S, cpc, cs1,
+                        P1, L1, out_idx + r0 * k, out_d64 ? out_d64 + r0 * k : nullptr, x->stream, RP, CS);
       }
       if (sync) check_knn_flag(x);
       return;
@@ -2142,6 +2155,8 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
     case DADE_OPT_KNN_I8: in({0, 1}); o.knn_i8 = (int)value; break;
     case DADE_OPT_FZ_SEED_STRIDE: DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "fz seed stride not in [0, 64]");
       o.fz_seed_stride = (int)value; break;
+    case DADE_OPT_FZ_ROWS: in({0, 1, 2}); o.fz_rows = (int)value; break;
+    case DADE_OPT_FZ_COLS: in({0, 1, 2}); o.fz_cols = (int)value; break;
     case DADE_OPT_GMIN_RATIO: DADE_REQUIRE(value >= 1 && value <= 1024, DADE_ERR_ARG, "gmin ratio not in [1, 1024]");
       o.gmin_ratio = (int)value; break;
     case DADE_OPT_DHAT_CHUNK_MB: DADE_REQUIRE(value >= 0 && value <= 8192, DADE_ERR_ARG, "dhat chunk not in [0, 8192] MB");

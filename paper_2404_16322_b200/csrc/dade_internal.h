@@ -140,10 +140,11 @@ void launch_probe_finish(const int32_t* cand, const int32_t* ccount, int nlists,
 // kind 1 = fp16 operands (kind::f16, power-of-two scales), 0 = tf32 hi parts (kind::tf32)
 int fz_nkc(int D, int kind);
 int fz_cap(int k);
-size_t fz_smem(int D, int kind, int k, int G, int S, int cpc);
-bool fz_config(int D, int kind, int k, int* G, int* S, int* cps);
-int fz_lists_per_row(int64_t m, int64_t n, int P, int cstride = 1);
-void fz_seed_plan(int64_t m, int64_t n, int k, int P, int force, int* cstride, int* P1, int* maxL1);
+size_t fz_smem(int D, int kind, int k, int G, int S, int cpc, int RP = 1, int CS = 1);
+int64_t fz_rows_pad(int64_t rows);
+bool fz_config(int D, int kind, int k, int* G, int* S, int* cps, int* RP);
+int fz_lists_per_row(int64_t m, int64_t n, int P, int cstride = 1, int RP = 1);
+void fz_seed_plan(int64_t m, int64_t n, int k, int P, int force, int* cstride, int* P1, int* maxL1, int RP = 1);
 // gscale > 0: one matrix scale; else per-row power-of-two scales (inv_scale[r] = 1/s_r, +inf if unbounded)
 void launch_split_h16(const float* X, int64_t rows, int D, const float* center, uint16_t* h, float* norm,
                       float* inv_scale, float gscale, cudaStream_t st);
@@ -153,7 +154,7 @@ void launch_probe_fz(int kind, const void* Aop, const float* an, const float* ai
                      const float* bn, float binv, float bmax, int64_t n, int D, int k, const float* slack,
                      const float* A, const float* B, float* seeds, int32_t* cand, int32_t* ccount, int P, int maxL,
                      int G, int S, int cpc, int cstride, int P1, int maxL1, int32_t* out_idx, double* out_d64,
-                     cudaStream_t st);
+                     cudaStream_t st, int RP = 1, int CS = 1);
 
 // rotate.cu : x~ = R (x - mu) on the tensor cores (tcgen05 kind::i8, kRotSlices-way split with
 // exact int32 levels combined in fp64), stored fp32.

@@ -187,8 +187,8 @@ __device__ __forceinline__ int64_t fz_cta_of(int64_t i, int64_t I, int64_t P) { 
 //    window thr(U) instead of an open window. The lists then see only the few columns inside the
 //    window (no warm-up of a running threshold per list).
 // smem: A region | B ring | barriers | Sk[G][128][k] | stage[4G][32 x 33]
-template <int KIND, int MODE, int KS>
-__global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
+template <int KIND, int MODE, int KS, int RP, int CS>
+__global__ void __launch_bounds__(64 + 128 * (CS == 2 ? 4 : 2), 1) k_probe_fz(
     const unsigned char* __restrict__ Aop, const float* __restrict__ an, const float* __restrict__ ahs,
     const unsigned char* __restrict__ Bop, const float* __restrict__ bn, float bhs, float bmax, int nkc,
     int64_t m, int64_t n, int maxL, int k, int C, int G, int S, int cpc, const float* __restrict__ slack,
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
     int nlists_seed) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* areg = sm;
-  unsigned char* ring = sm + (size_t)nkc * kChunkBytes;
+  unsigned char* ring = sm + (size_t)RP * nkc * kChunkBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * cpc * kChunkBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
@@ -212,19 +212,22 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
   const int NB = 2 * G;
   // this launch's column tiles: every cstride-th of the row (MODE 1 may sample a subset: its
   // seeds stay valid upper bounds), ntiles of them per row tile
-  const int64_t mt = (m + kTM - 1) / kTM, ntiles = ((n + kTM - 1) / kTM + cstride - 1) / cstride;
+  // RP = 2: a row tile is a pair of 128-row A tiles (both resident) sharing every B chunk — two
+  // MMAs per chunk into two accumulators, one epilogue group per half — so each B byte brought
+  // into the SM feeds twice the tensor work (the B stream is the pipeline's bound)
+  const int64_t mt = (m + kTM * RP - 1) / (kTM * RP), ntiles = ((n + kTM - 1) / kTM + cstride - 1) / cstride;
   const int64_t I = mt * ntiles, P = gridDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * I / P, i1 = ((int64_t)blockIdx.x + 1) * I / P;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     // tfull: the accumulator's commit + the MMA thread's expect_tx for the tile's column norms
-    for (int b = 0; b < NB; ++b) { mbar_init(&tfull[b], 2); mbar_init(&tempty[b], 4); }
+    for (int b = 0; b < NB; ++b) { mbar_init(&tfull[b], 2); mbar_init(&tempty[b], 4 * RP * CS); }
     mbar_init(afull, 1);
     mbar_init(afree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    const uint32_t ncols = 128u * NB;
+    const uint32_t ncols = 128u * NB * RP;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(ncols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -240,9 +243,9 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
       for (int64_t i = i0; i < i1; ++seg) {
         const int64_t rt = i / ntiles, iend = min(i1, (rt + 1) * ntiles);
         if (seg > 0) mbar_wait(afree, (seg - 1) & 1);  // every MMA of the last segment completed
-        mbar_expect_tx(afull, (uint32_t)nkc * kChunkBytes);
-        for (int kc = 0; kc < nkc; ++kc)
-          bulk_g2s(areg + (size_t)kc * kChunkBytes, Aop + (size_t)(rt * nkc + kc) * kChunkBytes, kChunkBytes, afull);
+        mbar_expect_tx(afull, (uint32_t)(RP * nkc) * kChunkBytes);
+        for (int kc = 0; kc < RP * nkc; ++kc)  // RP consecutive 128-row tiles (padded to RP * 128 rows)
+          bulk_g2s(areg + (size_t)kc * kChunkBytes, Aop + (size_t)(rt * RP * nkc + kc) * kChunkBytes, kChunkBytes, afull);
         for (; i < iend; ++i) {
           const int64_t tn = (i - rt * ntiles) * cstride;
           for (int kc = 0; kc < nkc; kc += cpc, ++it) {  // one copy per stage of cpc chunks
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
           mbar_expect_tx(&tfull[b], kTM * 4);
           bulk_g2s(bnbuf + (T % (2 * NB)) * kTM, bn + (i - rt * ntiles) * cstride * kTM, kTM * 4, &tfull[b]);
           if (MODE == 3 && blockIdx.x == 0 && T < 256) dbg[1024 + T] = clock64();
-          const uint32_t acc = tmem + b * kTM;
+          const uint32_t acc = tmem + b * RP * kTM;
           for (int kc = 0; kc < nkc; kc += cpc, ++it) {
             const int s = it % S;
             mbar_wait(&full[s], (it / S) & 1);
@@ -286,10 +289,12 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
             for (int c = 0; c < cpc; ++c)
 #pragma unroll
               for (int j = 0; j < 2; ++j)  // two MMAs of K = 32 B per row (16 halves / 8 floats)
-                if (MODE != 3)  // (MODE 3: pipeline measurement without the MMAs)
-                  mma<KIND>(acc, umma_desc(areg + (size_t)(kc + c) * kChunkBytes + j * 256),
-                            umma_desc(ring + ((size_t)s * cpc + c) * kChunkBytes + j * 256), idesc,
-                            ((kc + c) | j) != 0);
+#pragma unroll
+                for (int h = 0; h < RP; ++h)  // one per resident A tile, the same B chunk
+                  if (MODE != 3)  // (MODE 3: pipeline measurement without the MMAs)
+                    mma<KIND>(acc + h * kTM, umma_desc(areg + (size_t)(h * nkc + kc + c) * kChunkBytes + j * 256),
+                              umma_desc(ring + ((size_t)s * cpc + c) * kChunkBytes + j * 256), idesc,
+                              ((kc + c) | j) != 0);
             mma_commit(&empty[s]);
           }
           mma_commit(&tfull[b]);
@@ -298,17 +303,23 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
       }
     }
   } else {  // ---------------- epilogue
-    const int g = (warp - 2) >> 2;
+    // epilogue group eg = (g RP + h) CS + cs: tile group g (tiles T = g mod G), A half h, column
+    // share cs (CS = 2: two groups drain each accumulator, 64 columns each, with their own
+    // per-row windows and lists — every list / seed set is a valid partial, the finish and the
+    // select pass take their union over Gt = G CS slots per (row, segment))
+    const int eg = (warp - 2) >> 2;
+    const int cs = eg % CS, h = (eg / CS) % RP, g = eg / (CS * RP);
+    const int Gt = G * CS, gt = g * CS + cs;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int r = q * 32 + lane;
-    float* Sk = lists + (size_t)g * kTM * k;  // [128][k] sorted k smallest d_hat seen (MODE 2)
-    float* stage = lists + (size_t)G * kTM * k + (size_t)(warp - 2) * 32 * 33;
+    float* Sk = lists + (size_t)eg * kTM * k;  // [128][k] sorted k smallest d_hat seen (MODE 2)
+    float* stage = lists + (size_t)G * RP * CS * kTM * k + (size_t)(warp - 2) * 32 * 33;
     const unsigned lt = (1u << lane) - 1u;
-    const int nlists = maxL * G;
     int64_t T = 0;
     for (int64_t i = i0; i < i1;) {
       const int64_t rt = i / ntiles, iend = min(i1, (rt + 1) * ntiles);
-      const int64_t row = rt * kTM + r;
+      const int64_t rbase = (rt * RP + h) * kTM;  // first row of this group's A tile
+      const int64_t row = rbase + r;
       const bool live = row < m;
       const int jseg = (int)(blockIdx.x - fz_cta_of(rt * ntiles, I, P));
       const float a2 = live ? an[row] : 0.f;
@@ -469,7 +480,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
             const bool in = hit && (int)__float_as_uint(d) <= (int)thr2;
             const unsigned im = __ballot_sync(0xffffffffu, in);
             const int ni = __popc(im);
-            int2* L = reinterpret_cast<int2*>(cand) + ((((int64_t)rt * kTM + R) * maxL + jseg) * G + g) * C;
+            int2* L = reinterpret_cast<int2*>(cand) + (((rbase + R) * maxL + jseg) * Gt + gt) * C;
             int nlr = __shfl_sync(0xffffffffu, nl, rr);
             bool over = false;
             if (nlr + ni > C) {
@@ -502,7 +513,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
           }
           __syncwarp();  // the stage is rewritten by the next chunk
         };
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + b * kTM;
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (b * RP + h) * kTM;
         if (MODE == 0 || MODE == 3) {  // pipeline measurement: drain the accumulator only
           uint32_t v0[32];
           FZ_TMEM_LD32(tbase, v0);
@@ -516,11 +527,11 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
         // one chunk at a time (measured faster than batching the TMEM loads: fewer live registers);
         // the buffer is released after the last chunk's load, its column norms stay in bnbuf
 #pragma unroll 1
-        for (int cb = 0; cb < kTM / 32; ++cb) {
+        for (int cb = cs * (4 / CS); cb < (cs + 1) * (4 / CS); ++cb) {
           uint32_t v[32];
           FZ_TMEM_LD32(tbase + cb * 32, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (cb == kTM / 32 - 1) {
+          if (cb == (cs + 1) * (4 / CS) - 1) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[b]);
@@ -529,7 +540,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
         }
       }
       // ---- segment end
-      const int64_t slot = ((int64_t)row * maxL + jseg) * G + g;
+      const int64_t slot = ((int64_t)row * maxL + jseg) * Gt + gt;
       if (MODE == 1) {
         if (live) {
           DADE_DCHECK(jseg >= 0 && jseg < maxL);
@@ -543,9 +554,9 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
         for (int rr = 0; rr < 32; ++rr) {
           const int nlr = __shfl_sync(0xffffffffu, nl, rr);
           const unsigned thrr = __shfl_sync(0xffffffffu, thr, rr);
-          const int64_t rowr = rt * kTM + q * 32 + rr;
+          const int64_t rowr = rbase + q * 32 + rr;
           if (rowr >= m || nlr == 0) continue;
-          int2* L = reinterpret_cast<int2*>(cand) + ((rowr * maxL + jseg) * G + g) * C;
+          int2* L = reinterpret_cast<int2*>(cand) + ((rowr * maxL + jseg) * Gt + gt) * C;
           int nn = 0;
           for (int e0 = 0; e0 < nlr; e0 += 32) {
             const int e = e0 + lane;
@@ -585,7 +596,7 @@ __global__ void __launch_bounds__(64 + 256, 1) k_probe_fz(
            cpc, S, nkc, nch, lat / (nch - S), gap / (nch - S), reuse / (nch - S), nti, tl / (nti - 1), tg / (nti - 1));
   }
   if (warp == 1) {
-    const uint32_t ncols = 128u * NB;
+    const uint32_t ncols = 128u * NB * RP;
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
   }
 }
@@ -667,33 +678,37 @@ int fz_cap(int k) { return k + 48; }
 
 int fz_nkc(int D, int kind) { return kind == 1 ? (D + kKH - 1) / kKH : tc_nkc(D); }
 
-size_t fz_smem(int D, int kind, int k, int G, int S, int cpc) {
-  return (size_t)fz_nkc(D, kind) * kChunkBytes + (size_t)S * cpc * kChunkBytes + 16 * S + 256 + 8 * kTM * 4 +
-         (size_t)G * kTM * k * 4 +
-         (size_t)G * 4 * 32 * 33 * 4;
+size_t fz_smem(int D, int kind, int k, int G, int S, int cpc, int RP, int CS) {
+  return (size_t)RP * fz_nkc(D, kind) * kChunkBytes + (size_t)S * cpc * kChunkBytes + 16 * S + 256 + 8 * kTM * 4 +
+         (size_t)G * RP * CS * kTM * k * 4 +
+         (size_t)G * RP * CS * 4 * 32 * 33 * 4;
 }
+
+// fp16 operand rows are padded to 256 (a whole row-tile pair for RP = 2)
+int64_t fz_rows_pad(int64_t rows) { return (rows + 2 * kTM - 1) / (2 * kTM) * (2 * kTM); }
 
 // Launch shape: two persistent CTAs per SM with one epilogue group each (TMEM 2 x 256 columns,
 // <= 113 KB of shared memory each, >= 3 ring stages) when they fit — the pipeline is latency-
 // bound per CTA and two independent CTAs measured 1.5x faster on the C5 shard probe — else one
 // CTA with two groups (>= 6 stages), else one group (>= 4). k <= 32 (the seed pass keeps the k
 // smallest group minima in registers).
-bool fz_config(int D, int kind, int k, int* G, int* S, int* cps) {
+bool fz_config(int D, int kind, int k, int* G, int* S, int* cps, int* RP) {
   if (k > 32) return false;
+  *RP = 1;
   for (int s = 8; s >= 3; --s)
-    if (2 * fz_smem(D, kind, k, 1, s, 1) <= 226 * 1024) { *G = 1; *S = s; *cps = 2; return true; }
+    if (2 * fz_smem(D, kind, k, 1, s, 1, 1) <= 226 * 1024) { *G = 1; *S = s; *cps = 2; return true; }
   const size_t cap = 225 * 1024;
   for (int g = 2; g >= 1; --g) {
     int s = 12;
-    while (s >= (g == 2 ? 6 : 4) && fz_smem(D, kind, k, g, s, 1) > cap) --s;
+    while (s >= (g == 2 ? 6 : 4) && fz_smem(D, kind, k, g, s, 1, 1) > cap) --s;
     if (s >= (g == 2 ? 6 : 4)) { *G = g; *S = s; *cps = 1; return true; }
   }
   return false;
 }
 
 // lists per row of the persistent split: CTAs covering one row tile (host mirror of fz_cta_of)
-int fz_lists_per_row(int64_t m, int64_t n, int P, int cstride) {
-  const int64_t mt = (m + kTM - 1) / kTM, ntiles = ((n + kTM - 1) / kTM + cstride - 1) / cstride, I = mt * ntiles;
+int fz_lists_per_row(int64_t m, int64_t n, int P, int cstride, int RP) {
+  const int64_t mt = (m + kTM * RP - 1) / (kTM * RP), ntiles = ((n + kTM - 1) / kTM + cstride - 1) / cstride, I = mt * ntiles;
   int mx = 1;
   for (int64_t rt = 0; rt < mt; ++rt) {
     const int64_t c0 = ((rt * ntiles + 1) * P - 1) / I, c1 = (((rt + 1) * ntiles) * P - 1) / I;
@@ -704,7 +719,7 @@ int fz_lists_per_row(int64_t m, int64_t n, int P, int cstride) {
 
 void launch_split_h16(const float* X, int64_t rows, int D, const float* center, uint16_t* h, float* norm,
                       float* inv_scale, float gscale, cudaStream_t st) {
-  const int64_t rp = tc_rows_pad(rows);
+  const int64_t rp = fz_rows_pad(rows);
   if (rp == 0) return;
   k_split_h16<<<(unsigned)((rp + 7) / 8), 256, 0, st>>>(X, rows, D, fz_nkc(D, 1), center,
                                                         reinterpret_cast<__half*>(h), norm, inv_scale, rp, gscale);
@@ -719,13 +734,13 @@ void launch_slack_h16(const float* an, const float* ainv, int64_t m, float bmax,
   DADE_CK(cudaGetLastError());
 }
 
-template <int KIND, int MODE, int KS>
+template <int KIND, int MODE, int KS, int RP, int CS>
 static void fz_launch(int P, unsigned threads, size_t smem, cudaStream_t st, const void* Aop, const float* an,
                       const float* ainv, const void* Bop, const float* bn, float binv, float bmax, int nkc, int64_t m,
                       int64_t n, int maxL, int k, int C, int G, int S, int cpc, const float* slack, float* seeds,
                       int32_t* cand, int32_t* ccount, int cstride = 1, int nlists_seed = 0) {
-  DADE_CK(cudaFuncSetAttribute(k_probe_fz<KIND, MODE, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_probe_fz<KIND, MODE, KS><<<P, threads, smem, st>>>(static_cast<const unsigned char*>(Aop), an, ainv,
+  DADE_CK(cudaFuncSetAttribute(k_probe_fz<KIND, MODE, KS, RP, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_probe_fz<KIND, MODE, KS, RP, CS><<<P, threads, smem, st>>>(static_cast<const unsigned char*>(Aop), an, ainv,
                                                        static_cast<const unsigned char*>(Bop), bn, binv, bmax, nkc, m,
                                                        n, maxL, k, C, G, S, cpc, slack, seeds, cand, ccount, cstride,
                                                        nlists_seed);
@@ -734,25 +749,25 @@ static void fz_launch(int P, unsigned threads, size_t smem, cudaStream_t st, con
 
 int g_fz_debug = 0;  // measurement: 1 = pipeline without epilogue math, 2 = pipeline without MMAs
 
-template <int KIND, int KS>
+template <int KIND, int KS, int RP, int CS>
 static void fz_two_pass(int P, unsigned threads, size_t smem, cudaStream_t st, const void* Aop, const float* an,
                         const float* ainv, const void* Bop, const float* bn, float binv, float bmax, int nkc,
                         int64_t m, int64_t n, int maxL, int k, int C, int G, int S, int cpc, const float* slack,
                         float* seeds, int32_t* cand, int32_t* ccount, int cstride, int maxL1, int P1) {
   if (g_fz_debug) {
     if (g_fz_debug == 1)
-      fz_launch<KIND, 0, KS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S,
+      fz_launch<KIND, 0, KS, RP, CS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S,
                              cpc, slack, seeds, cand, ccount, 1, 0);
     else
-      fz_launch<KIND, 3, KS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S,
+      fz_launch<KIND, 3, KS, RP, CS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S,
                              cpc, slack, seeds, cand, ccount, 1, 0);
   }
   // seed pass over every cstride-th column tile (its own persistent split: P1 CTAs, maxL1 lists
   // per row), then the select pass over all columns, reading maxL1 G seed lists per row
-  fz_launch<KIND, 1, KS>(P1, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL1, k, C, G, S, cpc,
+  fz_launch<KIND, 1, KS, RP, CS>(P1, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL1, k, C, G, S, cpc,
                          slack, seeds, cand, ccount, cstride, 0);
-  fz_launch<KIND, 2, KS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S, cpc,
-                         slack, seeds, cand, ccount, 1, maxL1 * G);
+  fz_launch<KIND, 2, KS, RP, CS>(P, threads, smem, st, Aop, an, ainv, Bop, bn, binv, bmax, nkc, m, n, maxL, k, C, G, S, cpc,
+                         slack, seeds, cand, ccount, 1, maxL1 * G * CS);
 }
 
 // The seed pass samples every cstride-th column tile so that >= 64 k group minima remain (their
@@ -761,45 +776,59 @@ static void fz_two_pass(int P, unsigned threads, size_t smem, cudaStream_t st, c
 // Measured there (tools/exp_probe_fz.py): probe 1.207 / 1.006 / 1.154 / 1.353 ms at strides
 // 1 / 4 / 8 / 16 — sparser seeds cost the select pass more than they save. Its persistent split
 // has P1 CTAs and maxL1 seed lists per row.
-void fz_seed_plan(int64_t m, int64_t n, int k, int P, int force, int* cstride, int* P1, int* maxL1) {
-  const int64_t mt = (m + kTM - 1) / kTM, ntiles = (n + kTM - 1) / kTM;
+void fz_seed_plan(int64_t m, int64_t n, int k, int P, int force, int* cstride, int* P1, int* maxL1, int RP) {
+  const int64_t mt = (m + kTM * RP - 1) / (kTM * RP), ntiles = (n + kTM - 1) / kTM;
   int64_t cs = force > 0 ? force : std::max<int64_t>(1, std::min<int64_t>(16, ntiles / (16 * (int64_t)k)));
   *cstride = (int)cs;
   const int64_t nts = (ntiles + cs - 1) / cs;
   *P1 = (int)std::min<int64_t>(P, mt * nts);
-  *maxL1 = fz_lists_per_row(m, n, *P1, (int)cs);
+  *maxL1 = fz_lists_per_row(m, n, *P1, (int)cs, RP);
 }
 
 void launch_probe_fz(int kind, const void* Aop, const float* an, const float* ainv, int64_t m, const void* Bop,
                      const float* bn, float binv, float bmax, int64_t n, int D, int k, const float* slack,
                      const float* A, const float* B, float* seeds, int32_t* cand, int32_t* ccount, int P, int maxL,
                      int G, int S, int cpc, int cstride, int P1, int maxL1, int32_t* out_idx, double* out_d64,
-                     cudaStream_t st) {
+                     cudaStream_t st, int RP, int CS) {
   if (m <= 0) return;
   DADE_REQUIRE(k >= 1 && k <= 32, DADE_ERR_UNSUPPORTED, "probe: fused filter needs k <= 32");
   const int C = fz_cap(k);
-  const size_t smem = fz_smem(D, kind, k, G, S, cpc);
+  DADE_REQUIRE(RP == 1 || (RP == 2 && kind == 1 && G == 1), DADE_ERR_ARG, "fz: row-tile pairs need fp16 operands and one group");
+  DADE_REQUIRE((CS == 1 || (CS == 2 && kind == 1)) && G * RP * CS <= 4, DADE_ERR_ARG, "fz: column shares need fp16 operands, <= 4 groups");
+  const size_t smem = fz_smem(D, kind, k, G, S, cpc, RP, CS);
   DADE_REQUIRE(cpc >= 1 && fz_nkc(D, kind) % cpc == 0, DADE_ERR_ARG, "fz: chunks per copy must divide the chunks per tile");
   DADE_REQUIRE(smem <= 227 * 1024, DADE_ERR_UNSUPPORTED, "probe: operands too wide for the fused filter");
   // seeds of rows / segments a CTA never covers stay huge (0x7f7f7f7f = 3.4e38: never below U)
-  DADE_CK(cudaMemsetAsync(seeds, 0x7f, sizeof(float) * (size_t)m * maxL1 * G * k, st));
-  DADE_CK(cudaMemsetAsync(ccount, 0, sizeof(int32_t) * (size_t)m * maxL * G, st));
-  const unsigned threads = 64 + 128 * G;
+  DADE_CK(cudaMemsetAsync(seeds, 0x7f, sizeof(float) * (size_t)m * maxL1 * G * CS * k, st));
+  DADE_CK(cudaMemsetAsync(ccount, 0, sizeof(int32_t) * (size_t)m * maxL * G * CS, st));
+  const unsigned threads = 64 + 128 * G * RP * CS;
   const int nkc = fz_nkc(D, kind);
   const float bi = kind == 1 ? binv : 1.f;
 #define FZ_ARGS P, threads, smem, st, Aop, an, ainv, Bop, bn, bi, bmax, nkc, m, n, maxL, k, C, G, S, cpc, slack, seeds, cand, ccount, \
                 cstride, maxL1, P1
-  if (kind == 1) {
-    if (k <= 8) fz_two_pass<1, 8>(FZ_ARGS);
-    else if (k <= 16) fz_two_pass<1, 16>(FZ_ARGS);
-    else fz_two_pass<1, 32>(FZ_ARGS);
+  if (kind == 1 && RP == 2 && CS == 2) {
+    if (k <= 8) fz_two_pass<1, 8, 2, 2>(FZ_ARGS);
+    else if (k <= 16) fz_two_pass<1, 16, 2, 2>(FZ_ARGS);
+    else fz_two_pass<1, 32, 2, 2>(FZ_ARGS);
+  } else if (kind == 1 && RP == 2) {
+    if (k <= 8) fz_two_pass<1, 8, 2, 1>(FZ_ARGS);
+    else if (k <= 16) fz_two_pass<1, 16, 2, 1>(FZ_ARGS);
+    else fz_two_pass<1, 32, 2, 1>(FZ_ARGS);
+  } else if (kind == 1 && CS == 2) {
+    if (k <= 8) fz_two_pass<1, 8, 1, 2>(FZ_ARGS);
+    else if (k <= 16) fz_two_pass<1, 16, 1, 2>(FZ_ARGS);
+    else fz_two_pass<1, 32, 1, 2>(FZ_ARGS);
+  } else if (kind == 1) {
+    if (k <= 8) fz_two_pass<1, 8, 1, 1>(FZ_ARGS);
+    else if (k <= 16) fz_two_pass<1, 16, 1, 1>(FZ_ARGS);
+    else fz_two_pass<1, 32, 1, 1>(FZ_ARGS);
   } else {
-    if (k <= 8) fz_two_pass<0, 8>(FZ_ARGS);
-    else if (k <= 16) fz_two_pass<0, 16>(FZ_ARGS);
-    else fz_two_pass<0, 32>(FZ_ARGS);
+    if (k <= 8) fz_two_pass<0, 8, 1, 1>(FZ_ARGS);
+    else if (k <= 16) fz_two_pass<0, 16, 1, 1>(FZ_ARGS);
+    else fz_two_pass<0, 32, 1, 1>(FZ_ARGS);
   }
 #undef FZ_ARGS
-  launch_probe_finish(cand, ccount, maxL * G, C, m, n, k, A, B, D, slack, out_idx, out_d64, st);
+  launch_probe_finish(cand, ccount, maxL * G * CS, C, m, n, k, A, B, D, slack, out_idx, out_d64, st);
 }
 
 }  // namespace dade

@@ -132,6 +132,38 @@ def test_fz_many_rows_chunks(torch_cuda):
     assert np.array_equal(pr4, pr1)
 
 
+@pytest.mark.parametrize("D,C,nprobe,nq", [(256, 20000, 8, 300), (96, 16384, 8, 1000), (128, 4096, 8, 257),
+                                           (64, 5000, 16, 129), (32, 777, 1, 40), (256, 1000, 33, 513)])
+@pytest.mark.parametrize("rows,cols", [(2, 1), (1, 2), (2, 2)])
+def test_fz_row_tile_pairs(torch_cuda, D, C, nprobe, nq, rows, cols):
+    # DADE_OPT_FZ_ROWS = 2: two resident 128-row A tiles share every B chunk (two accumulators, one
+    # epilogue group per half); ragged pairs (nq = 300, 257, 129, 40, 513: the second tile of the
+    # last pair partly or wholly past the rows). DADE_OPT_FZ_COLS = 2: two epilogue groups drain
+    # each accumulator (64 columns each, separate per-row windows and lists, united by the select
+    # pass and the finish). Bit-exact vs the oracle and equal to the default kernel on every row;
+    # integer data adds exact ties.
+    if rows * cols == 4 and D > 128:
+        pytest.skip("two A tiles + four epilogue groups exceed shared memory at D > 128")
+    torch = torch_cuda
+    rng = np.random.default_rng(D + C + nq)
+    if D == 64:
+        X = rng.integers(0, 4, size=(2 * C, D)).astype(np.float32)
+        Q = rng.integers(0, 4, size=(nq, D)).astype(np.float32)
+    else:
+        centers = rng.standard_normal((64, D)).astype(np.float32) * 2
+        X = (centers[rng.integers(0, 64, 2 * C)] + rng.standard_normal((2 * C, D)).astype(np.float32)).astype(np.float32)
+        Q = (centers[rng.integers(0, 64, nq)] + rng.standard_normal((nq, D)).astype(np.float32)).astype(np.float32)
+    cent = X[rng.choice(2 * C, C, replace=False)].copy()
+    ix = _index(torch, X, cent, 4)
+    ix.set_option("fz_rows", rows)
+    ix.set_option("fz_cols", cols)
+    pr2 = _check(torch, ix, Q, cent, nprobe, step=3)
+    ix.set_option("fz_rows", 0)
+    ix.set_option("fz_cols", 0)
+    pr1 = ix.probe(torch.from_numpy(Q).cuda(), nprobe).cpu().numpy()
+    assert np.array_equal(pr2, pr1)
+
+
 @pytest.mark.parametrize("D,C,nprobe", [(960, 4096, 64), (512, 3000, 16), (960, 777, 8)])
 def test_int8_split_filter_gist_like(torch_cuda, D, C, nprobe):
     # the int8 exact-split filter (knn_path 6; DADE_OPT_KNN_I8 for D >= 512): GIST-like

@@ -30,7 +30,7 @@ def main():
     ap.add_argument("--gmin-ratio", default="", help="comma list of DADE_OPT_GMIN_RATIO values (path 0)")
     ap.add_argument("--chunk-mb", default="", help="comma list of DADE_OPT_DHAT_CHUNK_MB values (path 1)")
     ap.add_argument("--debug", type=int, default=0, help="fz_debug option (1/2: pipeline-only launch first)")
-    ap.add_argument("--fz", default="", help="comma list of S:G:cps[:cpc] overrides for paths 4/5, e.g. 4:1:1,12:2:1")
+    ap.add_argument("--fz", default="", help="comma list of S:G:cps[:cpc[:rows[:cols]]] overrides for paths 4/5, e.g. 4:1:1,12:2:1")
     a = ap.parse_args()
     build.build()
     cfg = synth.config(a.config)
@@ -63,7 +63,8 @@ def main():
             pass
         else:
             ix.set_option("dhat_chunk_mb", 0)
-            for nm, val in zip(("fz_stages", "fz_groups", "fz_cps", "fz_cpc"), (tuple(fz) + (0,) * 4)[:4] if fz else (0,) * 4):
+            for nm, val in zip(("fz_stages", "fz_groups", "fz_cps", "fz_cpc", "fz_rows", "fz_cols"),
+                               (tuple(fz) + (0,) * 6)[:6] if fz else (0,) * 6):
                 ix.set_option(nm, val)
         pr = ix.probe(Qd, a.nprobe)
         same = None
