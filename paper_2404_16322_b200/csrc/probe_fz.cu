@@ -54,6 +54,10 @@
   } while (0)
 #endif
 
+#ifndef DADE_FZ_BN_TMA
+#define DADE_FZ_BN_TMA 0
+#endif
+
 namespace dade {
 
 namespace {
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(64 + 128 * (CS == 2 ? 4 : 2), 1) k_probe_fz(
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     // tfull: the accumulator's commit + the MMA thread's expect_tx for the tile's column norms
-    for (int b = 0; b < NB; ++b) { mbar_init(&tfull[b], 2); mbar_init(&tempty[b], 4 * RP * CS); }
+    for (int b = 0; b < NB; ++b) { mbar_init(&tfull[b], DADE_FZ_BN_TMA ? 2 : 1); mbar_init(&tempty[b], 4 * RP * CS); }
     mbar_init(afull, 1);
     mbar_init(afree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -277,8 +281,10 @@ __global__ void __launch_bounds__(64 + 128 * (CS == 2 ? 4 : 2), 1) k_probe_fz(
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           // the tile's column norms into bnbuf[T mod 2NB] (last read for tile T - 2NB, finished before
           // the epilogue released tile T - NB's buffer), completing on tfull[b] with the accumulator
-          mbar_expect_tx(&tfull[b], kTM * 4);
-          bulk_g2s(bnbuf + (T % (2 * NB)) * kTM, bn + (i - rt * ntiles) * cstride * kTM, kTM * 4, &tfull[b]);
+          if (DADE_FZ_BN_TMA) {
+            mbar_expect_tx(&tfull[b], kTM * 4);
+            bulk_g2s(bnbuf + (T % (2 * NB)) * kTM, bn + (i - rt * ntiles) * cstride * kTM, kTM * 4, &tfull[b]);
+          }
           if (MODE == 3 && blockIdx.x == 0 && T < 256) dbg[1024 + T] = clock64();
           const uint32_t acc = tmem + b * RP * kTM;
           for (int kc = 0; kc < nkc; kc += cpc, ++it) {
@@ -363,7 +369,10 @@ __global__ void __launch_bounds__(64 + 128 * (CS == 2 ? 4 : 2), 1) k_probe_fz(
         if (MODE == 3 && blockIdx.x == 0 && T < 256 && lane == 0 && q == 2) reinterpret_cast<unsigned long long*>(seeds)[1536 + T] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int64_t cb0 = (i - rt * ntiles) * cstride * kTM;
-        const float* bns = bnbuf + (size_t)(T % (2 * NB)) * kTM;  // this tile's column norms
+        // this tile's column norms: read by the epilogue straight from global memory (L2/L1-resident,
+        // broadcast loads). DADE_FZ_BN_TMA = 1 (measurement builds): staged by a TMA copy the MMA
+        // thread issues when it starts the tile — its latency then sits on every tile's critical path
+        const float* bns = DADE_FZ_BN_TMA ? bnbuf + (size_t)(T % (2 * NB)) * kTM : bn + cb0;
         // per 32-column chunk (v: the chunk's accumulators of this thread's row)
         auto chunk = [&](const uint32_t* v, int cb) {
           float4 bq[8];  // the chunk's column norms (broadcast shared-memory loads)
