@@ -53,6 +53,9 @@ constexpr int TR = 32;            // rows per tile: one row per lane
 #ifndef DADE_SCAN_STREAM0  // 0: epoch 0 through stage 1 + gather rounds like later epochs (experiment builds)
 #define DADE_SCAN_STREAM0 1
 #endif
+#ifndef DADE_SCAN_STREAM0_MINDD  // smallest staging unit (blocks) whose kernels stream epoch 0
+#define DADE_SCAN_STREAM0_MINDD 2
+#endif
 constexpr unsigned long long kKeyInf = ~0ull;
 
 struct __align__(16) QEntry {
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MAXREG) k_scan(const __grid_c
   constexpr int kQCap = SL::QCAP;
   constexpr int kStages = SL::kStages;
   constexpr int TB = SL::TB;
-  constexpr bool kStream0 = DADE_SCAN_STREAM0 && !PQ && !RES && DD >= 2;  // epoch-0 streaming (below)
+  constexpr bool kStream0 = DADE_SCAN_STREAM0 && !PQ && !RES && DD >= DADE_SCAN_STREAM0_MINDD;  // epoch-0 streaming (below)
   const int D = p.D, K = p.K;
   const int G = MULTI ? (blockDim.x >> 5) : 1;  // warps per query (power of two)
   const int lane = threadIdx.x & 31, warp = MULTI ? threadIdx.x >> 5 : 0;
