@@ -66,7 +66,11 @@ def main():
             for nm, val in zip(("fz_stages", "fz_groups", "fz_cps", "fz_cpc", "fz_rows", "fz_cols"),
                                (tuple(fz) + (0,) * 6)[:6] if fz else (0,) * 6):
                 ix.set_option(nm, val)
-        pr = ix.probe(Qd, a.nprobe)
+        try:
+            pr = ix.probe(Qd, a.nprobe)
+        except Exception as e:  # an override that does not fit shared memory / TMEM: report, go on
+            print(json.dumps({"config": cfg.name, "knn_path": path, "fz": fz, "error": str(e)[:120]}), flush=True)
+            continue
         same = None
         if ref is None:
             ref = pr.clone()
