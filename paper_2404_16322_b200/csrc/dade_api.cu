@@ -55,6 +55,7 @@ struct Options {
   int host_chunks = 1;      // dade_search_host: searches pipelined with the copies
   int host_prep_chunks = 0; // dade_search_host: rotation + probe chunks ahead of one scan (0 auto)
   int dhat_ares = 0;        // 1: A-resident d_hat writer for very wide rows (1-pass filter)
+  int dhat_h16 = 1;         // 1 (default): the d_hat writer's 1-pass filter on fp16 operands (kind::f16), 0: tf32 hi parts
   int dhat_chunk_mb = 0;    // d_hat matrix chunk in MB (0: 2 GiB); measurement option
   int gmin_ratio = 1;       // exact_knn: group-minima select only when k * ratio <= number of 32-column groups
   int knn_i8 = 0;           // exact_knn: 1 = int8 exact-split filter for D >= 512; 0 (default) the 3-pass tf32 one
@@ -480,8 +481,32 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
     x->flag.reserve(1);
     DADE_CK(cudaMemsetAsync(x->flag.p, 0, sizeof(int), x->stream));
   }
+  // fp16 operands for the d_hat writer (DADE_OPT_DHAT_H16; 1-pass filter + group-minima select):
+  // the same power-of-two scaled operands, d_hat formula and slack as the fused fp16 filter
+  // (probe_fz.cu MODE 1), half the operand bytes and half the MMAs of the tf32 hi x hi filter
+  const bool h16_want = x->opt.dhat_h16 && passes == 1 && k > 1 && n <= 32768 &&
+                        (int64_t)k * x->opt.gmin_ratio <= ngrp && ngrp <= 1024;
+  if (h16_want) tc_prepare_h16(x, B, const_cast<TcOp&>(bop));
+  const bool h16 = h16_want && bop.h16_ok;
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t mm = std::min(chunk, m - r0);
+    if (h16) {
+      const int64_t rp = fz_rows_pad(mm);
+      x->a_tc.h16.reserve((size_t)rp * fz_nkc(D, 1) * 32);
+      x->a_tc.hinv.reserve((size_t)rp);
+      x->a_tc.norm.reserve((size_t)rp);
+      launch_split_h16(A + r0 * D, mm, D, bop.center.p, x->a_tc.h16.p, x->a_tc.norm.p, x->a_tc.hinv.p, 0.f,
+                       x->stream);
+      launch_l2_tc(reinterpret_cast<const float*>(x->a_tc.h16.p), nullptr, x->a_tc.norm.p, mm,
+                   reinterpret_cast<const float*>(bop.h16.p), nullptr, bop.norm.p, n, D, x->dmat.p, n, x->stream,
+                   x->gmin.p, 1, gshift, x->a_tc.hinv.p, bop.hinv_b);
+      launch_slack_h16(x->a_tc.norm.p, x->a_tc.hinv.p, mm, bop.maxnorm, bop.hinv_b, D, x->slack.p, x->stream);
+      x->ovf.reserve((size_t)chunk + 1);
+      launch_select_gmin(x->dmat.p, x->gmin.p, gshift, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
+                         out_d64 ? out_d64 + r0 * k : nullptr, x->flag.p, x->slack.p, x->ovf.p,
+                         x->ovf.p + 1, x->stream);
+      continue;
+    }
     tc_prepare(x, A + r0 * D, mm, x->a_tc, false, bop.center.p);
     // the group-minima select bounds the k-th smallest d_hat by the k-th smallest GROUP minimum,
     // loose when k nears the number of groups (C3: k = 64 of 128); the histogram select
@@ -2142,6 +2167,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
       DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "prep chunks not in [0, 64]");
       o.host_prep_chunks = (int)value; break;
     case DADE_OPT_DHAT_ARES: in({0, 1}); o.dhat_ares = (int)value; break;
+    case DADE_OPT_DHAT_H16: in({0, 1}); o.dhat_h16 = (int)value; break;
     case DADE_OPT_SHARD_EXCHANGES:
       DADE_REQUIRE(value >= 0 && value <= 16, DADE_ERR_ARG, "shard exchanges not in [0, 16]");
       o.shard_exchanges = (int)value; break;

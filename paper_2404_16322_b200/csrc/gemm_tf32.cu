@@ -128,6 +128,14 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
                : "memory");
@@ -150,7 +158,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
                                                   const float* __restrict__ Blo, const float* __restrict__ bn,
                                                   int nkc, float* __restrict__ out, int64_t m, int64_t n,
                                                   int64_t ldo, float* __restrict__ gmin, int64_t ldg, int passes,
-                                                  int gshift, int s1) {
+                                                  int gshift, int s1, const float* __restrict__ ahs, float bhs) {
   extern __shared__ __align__(1024) unsigned char sm[];
   // operand stages: 2 x 32 KB (3-pass: A_hi, A_lo, B_hi, B_lo) or s1 x 16 KB (1-pass: A_hi, B_hi)
   const int S = passes == 1 ? s1 : 2;
@@ -177,7 +185,10 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
 
   if (tid == 0) {
     // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+    // (ahs != null: fp16 operands — the same 8-KB blocks hold 32 halves per row, kind::f16,
+    // A/B format F16 (0); 1-pass only)
+    const uint32_t fmt = ahs ? 0u : 2u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
     // stage layout: A_hi | B_hi (1-pass) or A_hi | A_lo | B_hi | B_lo (3-pass)
     const int offB = passes == 1 ? kSub * 4 : 2 * kSub * 4;
     auto load = [&](int kc) {
@@ -202,7 +213,8 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
       for (int j = 0; j < kKC / 8; ++j) {  // UMMA_K = 8 for tf32 (32 B of K)
         const uint64_t ah = umma_desc(st + j * 256, 128, kSBO);
         const uint64_t bh = umma_desc(st + offB + j * 256, 128, kSBO);
-        mma_tf32(tmem, ah, bh, idesc, (kc | j) != 0);
+        if (ahs) mma_f16(tmem, ah, bh, idesc, (kc | j) != 0);
+        else mma_tf32(tmem, ah, bh, idesc, (kc | j) != 0);
         if (passes != 1) {
           const uint64_t al = umma_desc(st + kSub * 4 + j * 256, 128, kSBO);
           const uint64_t bl = umma_desc(st + 3 * kSub * 4 + j * 256, 128, kSBO);
@@ -223,6 +235,8 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   __shared__ float sbn[kTM];
   const int64_t row = tm * kTM + warp * 32 + lane;
   const float a2 = row < m ? an[row] : 0.f;
+  // fp16 operands were scaled by powers of two (per row of A, one scale for B): m2 undoes both, exactly
+  const float m2 = ahs ? (row < m ? -2.f * ahs[row] * bhs : -2.f) : -2.f;
   sbn[tid] = tn * kTM + tid < n ? bn[tn * kTM + tid] : 0.f;
   __syncthreads();
   mbar_wait(accf, 0);
@@ -243,15 +257,15 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
         const float4 b4 = *reinterpret_cast<const float4*>(sbn + cb * 32 + j);
-        d[j + 0] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 0]), a2 + b4.x));
-        d[j + 1] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 1]), a2 + b4.y));
-        d[j + 2] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 2]), a2 + b4.z));
-        d[j + 3] = fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j + 3]), a2 + b4.w));
+        d[j + 0] = fmaxf(0.f, fmaf(m2, __uint_as_float(r[j + 0]), a2 + b4.x));
+        d[j + 1] = fmaxf(0.f, fmaf(m2, __uint_as_float(r[j + 1]), a2 + b4.y));
+        d[j + 2] = fmaxf(0.f, fmaf(m2, __uint_as_float(r[j + 2]), a2 + b4.z));
+        d[j + 3] = fmaxf(0.f, fmaf(m2, __uint_as_float(r[j + 3]), a2 + b4.w));
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        d[j] = c0 + j < n ? fmaxf(0.f, fmaf(-2.f, __uint_as_float(r[j]), a2 + sbn[cb * 32 + j])) : INFINITY;
+        d[j] = c0 + j < n ? fmaxf(0.f, fmaf(m2, __uint_as_float(r[j]), a2 + sbn[cb * 32 + j])) : INFINITY;
     }
     if (gmin && row < m && c0 < n) {  // per-row minimum of this 2^gshift-column group (select hint)
       float mn = d[0];
@@ -331,8 +345,9 @@ void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, c
 
 void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
-                  cudaStream_t st, float* gmin, int passes, int gshift) {
+                  cudaStream_t st, float* gmin, int passes, int gshift, const float* ahs, float bhs) {
   if (m <= 0 || n <= 0) return;
+  DADE_REQUIRE(!ahs || passes == 1, DADE_ERR_ARG, "l2_tc: fp16 operands are 1-pass only");
   // set on every launch: the attribute is per device
   DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStageBytes + 128));
   // 1-pass stages (16 KB each): three — 48 KB lets four CTAs share an SM (with four stages the
@@ -342,8 +357,9 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
   const int s1 = 3;
   const size_t smem = (passes == 1 ? (size_t)s1 * (kStageBytes / 2) : 2 * (size_t)kStageBytes) + 128;
   dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
-  k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, tc_nkc(D), out, m, n, ldo, gmin,
-                                   (n + (1 << gshift) - 1) >> gshift, passes, gshift, s1);
+  // fp16 operands (Ahi / Bhi point at launch_split_h16's blocks): 32 halves per row per chunk
+  k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, ahs ? fz_nkc(D, 1) : tc_nkc(D), out, m, n, ldo, gmin,
+                                   (n + (1 << gshift) - 1) >> gshift, passes, gshift, s1, ahs, bhs);
   DADE_CK(cudaGetLastError());
 }
 

@@ -21,7 +21,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_STATE", 4: "ERR_NONFINI
 # dade_set_option (include/dade.h DADE_OPT_*)
 OPTIONS = {"knn_path": 1, "probe_passes": 2, "scan_warps": 3, "scan_order": 4, "scan_tail": 5,
            "host_chunks": 6, "host_prep_chunks": 7, "dhat_ares": 8, "shard_exchanges": 9,
-           "fz_stages": 10, "fz_groups": 11, "fz_cps": 12, "fz_debug": 13, "fz_cpc": 14, "pca_tc": 15, "scan_p1": 17, "dhat_chunk_mb": 18, "knn_i8": 19, "gmin_ratio": 20, "fz_seed_stride": 21, "fz_rows": 22, "fz_cols": 23}
+           "fz_stages": 10, "fz_groups": 11, "fz_cps": 12, "fz_debug": 13, "fz_cpc": 14, "pca_tc": 15, "scan_p1": 17, "dhat_chunk_mb": 18, "knn_i8": 19, "gmin_ratio": 20, "fz_seed_stride": 21, "fz_rows": 22, "fz_cols": 23, "dhat_h16": 24}
 
 
 class DadeError(RuntimeError):

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--seed-stride", default="", help="comma list of DADE_OPT_FZ_SEED_STRIDE values (path 4)")
     ap.add_argument("--gmin-ratio", default="", help="comma list of DADE_OPT_GMIN_RATIO values (path 0)")
     ap.add_argument("--chunk-mb", default="", help="comma list of DADE_OPT_DHAT_CHUNK_MB values (path 1)")
+    ap.add_argument("--h16", action="store_true", help="also time path 1 with the fp16-operand d_hat writer (DADE_OPT_DHAT_H16)")
     ap.add_argument("--debug", type=int, default=0, help="fz_debug option (1/2: pipeline-only launch first)")
     ap.add_argument("--fz", default="", help="comma list of S:G:cps[:cpc[:rows[:cols]]] overrides for paths 4/5, e.g. 4:1:1,12:2:1")
     a = ap.parse_args()
@@ -50,6 +51,7 @@ def main():
         ix.set_option("fz_debug", a.debug)
     runs = [(int(p), None) for p in a.paths.split(",")]
     runs += [(4, tuple(int(v) for v in f.split(":"))) for f in a.fz.split(",") if f]
+    runs += [(1, ("dhat_h16", 1))] if a.h16 else []
     runs += [(1, ("chunk_mb", int(v))) for v in a.chunk_mb.split(",") if v]
     runs += [(0, ("gmin_ratio", int(v))) for v in a.gmin_ratio.split(",") if v]
     runs += [(4, ("seed_stride", int(v))) for v in a.seed_stride.split(",") if v]
@@ -57,9 +59,10 @@ def main():
         ix.set_option("knn_path", path)
         ix.set_option("gmin_ratio", fz[1] if fz and fz[0] == "gmin_ratio" else 1)
         ix.set_option("fz_seed_stride", fz[1] if fz and fz[0] == "seed_stride" else 0)
+        ix.set_option("dhat_h16", 1 if fz and fz[0] == "dhat_h16" else 0)
         if fz and fz[0] == "chunk_mb":
             ix.set_option("dhat_chunk_mb", fz[1])
-        elif fz and fz[0] in ("gmin_ratio", "seed_stride"):
+        elif fz and fz[0] in ("gmin_ratio", "seed_stride", "dhat_h16"):
             pass
         else:
             ix.set_option("dhat_chunk_mb", 0)
