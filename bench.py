@@ -373,7 +373,8 @@ def launches_per_search(cfg, world, nprobe):
     (> 32,768 centroids, k <= 32, D <= 256) k_split_h16, k_slack_h16, k_probe_fz x 2, k_probe_finish, the fused
     tf32 path (> 1024 64-column groups) k_split_tf32, k_slack, k_probe_tc, k_probe_finish, or the group-minima path
     (> 2^20 centroids) k_split_tf32, k_l2_tc, k_slack, k_select_groups, or the d_hat path
-    k_split_tf32, k_l2_tc | k_dhat_tc, k_slack, k_select_gmin, k_select_small; the query order
+    k_split_tf32 | k_split_h16, k_l2_tc | k_dhat_tc, k_slack | k_slack_h16, k_select_gmin, k_select_small (fp16
+    operands for the 1-pass filter, D <= 256: the same five launches); the query order
     (k_lpt_key, k_order_offsets, k_key_scatter); k_scan;
     + k_merge_topk when sharded (each rank probes its block of nq / world queries)."""
     n, k = cfg.nlist, nprobe
