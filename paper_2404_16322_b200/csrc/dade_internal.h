@@ -106,7 +106,8 @@ void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, c
 void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
                   cudaStream_t st, float* gmin = nullptr, int passes = 3, int gshift = 5,
-                  const float* ahs = nullptr, float bhs = 1.f);  // ahs: fp16 operands (per-row 1/scale of A, bhs = B's)
+                  const float* ahs = nullptr, float bhs = 1.f,  // ahs: fp16 operands (per-row 1/scale of A, bhs = B's)
+                  int nt = 1);  // nt = 2: 128 x 256 tiles (1-pass)
 // warp-per-row exact select using the GEMM's 32-column group minima (k <= ceil(n/32) <= 256)
 void launch_select_gmin(const float* d_hat, const float* gmin, int gshift, int64_t m, int64_t n, int k,
                         const float* A, const float* B, int D, int32_t* out_idx, double* out_d64,

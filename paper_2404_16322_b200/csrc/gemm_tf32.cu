@@ -152,8 +152,12 @@ __device__ __forceinline__ void mma_commit(uint64_t* b) {
         "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                         \
       : "r"(taddr))
 
-// One CTA = one 128 x 128 output tile; K = nkc chunks of 32, 2-stage TMA -> MMA pipeline.
-__global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi, const float* __restrict__ Alo,
+// One CTA = one 128 x (128 NT) output tile; K = nkc chunks of 32, 2-stage TMA -> MMA pipeline.
+// NT = 2 (1-pass filters): the A tile feeds an N = 256 MMA over two adjacent column tiles (their
+// B blocks are contiguous 8-row groups in the stage), eight epilogue warps — a quarter less
+// operand traffic per output and half the CTAs (their barrier / TMEM set-up and operand wait).
+template <int NT>
+__global__ void __launch_bounds__(128 * NT, NT == 1 ? 3 : 2) k_l2_tc(const float* __restrict__ Ahi, const float* __restrict__ Alo,
                                                   const float* __restrict__ an, const float* __restrict__ Bhi,
                                                   const float* __restrict__ Blo, const float* __restrict__ bn,
                                                   int nkc, float* __restrict__ out, int64_t m, int64_t n,
@@ -162,20 +166,22 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   extern __shared__ __align__(1024) unsigned char sm[];
   // operand stages: 2 x 32 KB (3-pass: A_hi, A_lo, B_hi, B_lo) or s1 x 16 KB (1-pass: A_hi, B_hi)
   const int S = passes == 1 ? s1 : 2;
-  const int SB = passes == 1 ? kStageBytes / 2 : kStageBytes;
+  const int SB = passes == 1 ? (1 + NT) * kSub * 4 : kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * SB);
   uint64_t* empty = full + 4;
   uint64_t* accf = full + 8;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(full + 9);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t tm = blockIdx.y, tn = blockIdx.x;
+  const int64_t tm = blockIdx.y, tn = (int64_t)blockIdx.x * NT;  // tn: first 128-column tile
+  const int64_t ntn = (n + kTM - 1) / kTM;
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)) : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(128u * NT)
+                 : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
     // (ahs != null: fp16 operands — the same 8-KB blocks hold 32 halves per row, kind::f16,
     // A/B format F16 (0); 1-pass only)
     const uint32_t fmt = ahs ? 0u : 2u;
-    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)((kTM * NT) >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
     // stage layout: A_hi | B_hi (1-pass) or A_hi | A_lo | B_hi | B_lo (3-pass)
     const int offB = passes == 1 ? kSub * 4 : 2 * kSub * 4;
     auto load = [&](int kc) {
@@ -198,6 +204,8 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
       const int64_t ao = (tm * nkc + kc) * kSub, bo = (tn * nkc + kc) * kSub;
       bulk_g2s(st, Ahi + ao, kSub * 4, &full[s]);
       bulk_g2s(st + offB, Bhi + bo, kSub * 4, &full[s]);
+      if (NT == 2)  // the second column tile (past the last one: the last tile again, masked in the epilogue)
+        bulk_g2s(st + offB + kSub * 4, Bhi + ((tn + 1 < ntn ? tn + 1 : ntn - 1) * nkc + kc) * kSub, kSub * 4, &full[s]);
       if (passes != 1) {
         bulk_g2s(st + kSub * 4, Alo + ao, kSub * 4, &full[s]);
         bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
@@ -232,8 +240,9 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   }
   // the epilogue's norms are fetched while the MMAs run: ||a||^2 of this thread's row and the
   // tile's 128 column norms (smem), so their latency is not exposed after the accumulator wait
-  __shared__ float sbn[kTM];
-  const int64_t row = tm * kTM + warp * 32 + lane;
+  __shared__ float sbn[kTM * NT];
+  const int q = warp & 3, hh = warp >> 2;  // TMEM lane quarter, column tile of this warp
+  const int64_t row = tm * kTM + q * 32 + lane;
   const float a2 = row < m ? an[row] : 0.f;
   // fp16 operands were scaled by powers of two (per row of A, one scale for B): m2 undoes both, exactly
   const float m2 = ahs ? (row < m ? -2.f * ahs[row] * bhs : -2.f) : -2.f;
@@ -248,15 +257,16 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
 #pragma unroll 1
   for (int cb = 0; cb < kTM / 32; ++cb) {
     uint32_t r[32];
-    TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + cb * 32, r);
+    TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + hh * kTM + cb * 32, r);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int64_t c0 = tn * kTM + cb * 32;
+    const int64_t c0 = (tn + hh) * kTM + cb * 32;
+    const float* sb = sbn + hh * kTM + cb * 32;
     const bool full = c0 + 32 <= n;
     float d[32];
     if (full) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
-        const float4 b4 = *reinterpret_cast<const float4*>(sbn + cb * 32 + j);
+        const float4 b4 = *reinterpret_cast<const float4*>(sb + j);
         d[j + 0] = fmaxf(0.f, fmaf(m2, __uint_as_float(r[j + 0]), a2 + b4.x));
         d[j + 1] = fmaxf(0.f, fmaf(m2, __uint_as_float(r[j + 1]), a2 + b4.y));
         d[j + 2] = fmaxf(0.f, fmaf(m2, __uint_as_float(r[j + 2]), a2 + b4.z));
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        d[j] = c0 + j < n ? fmaxf(0.f, fmaf(m2, __uint_as_float(r[j]), a2 + sbn[cb * 32 + j])) : INFINITY;
+        d[j] = c0 + j < n ? fmaxf(0.f, fmaf(m2, __uint_as_float(r[j]), a2 + sb[j])) : INFINITY;
     }
     if (gmin && row < m && c0 < n) {  // per-row minimum of this 2^gshift-column group (select hint)
       float mn = d[0];
@@ -285,7 +295,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
 #pragma unroll
       for (int it = 0; it < 8; ++it) {  // 4 rows x 32 columns per instruction, 128 B per row
         const int ri = it * 4 + (lane >> 3), cc = (lane & 7) * 4;
-        const int64_t grow = tm * kTM + warp * 32 + ri;
+        const int64_t grow = tm * kTM + q * 32 + ri;
         if (grow < m) {
           const float* sp = stg + ri * 33 + cc;
           *reinterpret_cast<float4*>(out + grow * ldo + c0 + cc) = make_float4(sp[0], sp[1], sp[2], sp[3]);
@@ -301,7 +311,7 @@ __global__ void __launch_bounds__(128, 3) k_l2_tc(const float* __restrict__ Ahi,
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u * NT) : "memory");
 }
 
 __global__ void k_slack(const float* __restrict__ an, int64_t m, float bmax, float gamma, float* __restrict__ slack) {
@@ -345,11 +355,22 @@ void launch_slack(const float* an, int64_t m, float bmax, int D, float* slack, c
 
 void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m, const float* Bhi,
                   const float* Blo, const float* bn, int64_t n, int D, float* out, int64_t ldo,
-                  cudaStream_t st, float* gmin, int passes, int gshift, const float* ahs, float bhs) {
+                  cudaStream_t st, float* gmin, int passes, int gshift, const float* ahs, float bhs, int nt) {
   if (m <= 0 || n <= 0) return;
   DADE_REQUIRE(!ahs || passes == 1, DADE_ERR_ARG, "l2_tc: fp16 operands are 1-pass only");
   // set on every launch: the attribute is per device
-  DADE_CK(cudaFuncSetAttribute(k_l2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStageBytes + 128));
+  DADE_REQUIRE(nt == 1 || (nt == 2 && passes == 1), DADE_ERR_ARG, "l2_tc: 256-column tiles are 1-pass only");
+  if (nt == 2) {  // N = 256 tiles: three 24-KB stages (two CTAs of eight warps per SM: TMEM 2 x 256 columns)
+    const int s2 = 3;
+    const size_t smem2 = (size_t)s2 * 3 * kSub * 4 + 128;
+    DADE_CK(cudaFuncSetAttribute(k_l2_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    dim3 grid2((unsigned)(((n + kTM - 1) / kTM + 1) / 2), (unsigned)((m + kTM - 1) / kTM));
+    k_l2_tc<2><<<grid2, 256, smem2, st>>>(Ahi, Alo, an, Bhi, Blo, bn, ahs ? fz_nkc(D, 1) : tc_nkc(D), out, m, n, ldo, gmin,
+                                          (n + (1 << gshift) - 1) >> gshift, passes, gshift, s2, ahs, bhs);
+    DADE_CK(cudaGetLastError());
+    return;
+  }
+  DADE_CK(cudaFuncSetAttribute(k_l2_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kStageBytes + 128));
   // 1-pass stages (16 KB each): three — 48 KB lets four CTAs share an SM (with four stages the
   // 64 KB allowed three), hiding more of each CTA's wait for its accumulator (C2 search 0.721 ->
   // 0.712-0.718 ms; 2 and 4 measured no better); the epilogue's transposition buffers
@@ -358,7 +379,7 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
   const size_t smem = (passes == 1 ? (size_t)s1 * (kStageBytes / 2) : 2 * (size_t)kStageBytes) + 128;
   dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
   // fp16 operands (Ahi / Bhi point at launch_split_h16's blocks): 32 halves per row per chunk
-  k_l2_tc<<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, ahs ? fz_nkc(D, 1) : tc_nkc(D), out, m, n, ldo, gmin,
+  k_l2_tc<1><<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, ahs ? fz_nkc(D, 1) : tc_nkc(D), out, m, n, ldo, gmin,
                                    (n + (1 << gshift) - 1) >> gshift, passes, gshift, s1, ahs, bhs);
   DADE_CK(cudaGetLastError());
 }

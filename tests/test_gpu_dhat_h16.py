@@ -21,12 +21,22 @@ def torch_cuda():
     return torch
 
 
+H16 = 1   # 1: 128 x 128 tiles, 2: 128 x 256 tiles (set per test by the fixture below)
+
+
+@pytest.fixture(autouse=True, params=[1, 2])
+def _tiles(request):
+    global H16
+    H16 = request.param
+    yield
+
+
 def _index(torch, X, cent):
     from paper_2404_16322_b200 import Index
     ix = Index(X.shape[1])
     ix.set_option("knn_path", 1)
     ix.set_option("probe_passes", 1)
-    ix.set_option("dhat_h16", 1)
+    ix.set_option("dhat_h16", H16)
     mean, R, lam = O.fit_rotation(X)
     ix.set_rotation(mean, R, lam)
     ix.build_ivf(torch.from_numpy(X).cuda(), cent.shape[0], centroids=torch.from_numpy(cent).cuda())
@@ -40,7 +50,7 @@ def _check(torch, ix, Q, cent, nprobe, step=1):
         assert pr[q].tolist() == O.probe(Q[q], cent, nprobe).tolist(), f"query {q}"
     ix.set_option("dhat_h16", 0)          # the tf32 writer returns the same probes on every row
     pt = ix.probe(Qd, nprobe).cpu().numpy()
-    ix.set_option("dhat_h16", 1)
+    ix.set_option("dhat_h16", H16)
     assert np.array_equal(pr, pt)
 
 

@@ -51,7 +51,7 @@ def main():
         ix.set_option("fz_debug", a.debug)
     runs = [(int(p), None) for p in a.paths.split(",")]
     runs += [(4, tuple(int(v) for v in f.split(":"))) for f in a.fz.split(",") if f]
-    runs += [(1, ("dhat_h16", 1))] if a.h16 else []
+    runs += [(1, ("dhat_h16", 1)), (1, ("dhat_h16", 2))] if a.h16 else []  # 2: 128 x 256 tiles
     runs += [(1, ("chunk_mb", int(v))) for v in a.chunk_mb.split(",") if v]
     runs += [(0, ("gmin_ratio", int(v))) for v in a.gmin_ratio.split(",") if v]
     runs += [(4, ("seed_stride", int(v))) for v in a.seed_stride.split(",") if v]
@@ -59,7 +59,7 @@ def main():
         ix.set_option("knn_path", path)
         ix.set_option("gmin_ratio", fz[1] if fz and fz[0] == "gmin_ratio" else 1)
         ix.set_option("fz_seed_stride", fz[1] if fz and fz[0] == "seed_stride" else 0)
-        ix.set_option("dhat_h16", 1 if fz and fz[0] == "dhat_h16" else 0)
+        ix.set_option("dhat_h16", fz[1] if fz and fz[0] == "dhat_h16" else 0)
         if fz and fz[0] == "chunk_mb":
             ix.set_option("dhat_chunk_mb", fz[1])
         elif fz and fz[0] in ("gmin_ratio", "seed_stride", "dhat_h16"):
