@@ -303,7 +303,7 @@ dade_status dade_search_log(dade_index* idx, const float* Q, int nq, int K, int 
 #define DADE_OPT_FZ_SEED_STRIDE 21 /* fused probe filter: seed pass column-tile stride (0 auto) */
 #define DADE_OPT_FZ_ROWS 22        /* fused probe filter: 128-row A tiles per CTA sharing the B stream (0 auto, 1, 2) */
 #define DADE_OPT_FZ_COLS 23        /* fused probe filter: epilogue groups per accumulator (column shares; 0 auto, 1, 2) */
-#define DADE_OPT_DHAT_H16 24       /* probe d_hat writer (1-pass filter): 1 (default) fp16 operands (kind::f16), 2 the same with 128 x 256 tiles, 0 tf32 hi parts */
+#define DADE_OPT_DHAT_H16 24       /* probe d_hat writer (1-pass filter): 1 (default) fp16 operands (kind::f16), 2 the same with 128 x 256 tiles, 3 with cooperative cp.async operand loads (measurement), 0 tf32 hi parts */
 #define DADE_OPT_FZ_CPS 12         /* fused probe filter: persistent CTAs per SM (0 auto = 1, 2 with 1 group) */
 dade_status dade_set_option(dade_index* idx, int option, int64_t value);
 

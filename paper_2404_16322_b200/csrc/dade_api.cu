@@ -499,7 +499,7 @@ void exact_knn(dade_index* x, const float* A, int64_t m, const float* B, int64_t
                        x->stream);
       launch_l2_tc(reinterpret_cast<const float*>(x->a_tc.h16.p), nullptr, x->a_tc.norm.p, mm,
                    reinterpret_cast<const float*>(bop.h16.p), nullptr, bop.norm.p, n, D, x->dmat.p, n, x->stream,
-                   x->gmin.p, 1, gshift, x->a_tc.hinv.p, bop.hinv_b, x->opt.dhat_h16 == 2 ? 2 : 1);
+                   x->gmin.p, 1, gshift, x->a_tc.hinv.p, bop.hinv_b, x->opt.dhat_h16 >= 2 ? x->opt.dhat_h16 : 1);
       launch_slack_h16(x->a_tc.norm.p, x->a_tc.hinv.p, mm, bop.maxnorm, bop.hinv_b, D, x->slack.p, x->stream);
       x->ovf.reserve((size_t)chunk + 1);
       launch_select_gmin(x->dmat.p, x->gmin.p, gshift, mm, n, k, A + r0 * D, B, D, out_idx + r0 * k,
@@ -2167,7 +2167,7 @@ extern "C" dade_status dade_set_option(dade_index* x, int option, int64_t value)
       DADE_REQUIRE(value >= 0 && value <= 64, DADE_ERR_ARG, "prep chunks not in [0, 64]");
       o.host_prep_chunks = (int)value; break;
     case DADE_OPT_DHAT_ARES: in({0, 1}); o.dhat_ares = (int)value; break;
-    case DADE_OPT_DHAT_H16: in({0, 1, 2}); o.dhat_h16 = (int)value; break;
+    case DADE_OPT_DHAT_H16: in({0, 1, 2, 3}); o.dhat_h16 = (int)value; break;
     case DADE_OPT_SHARD_EXCHANGES:
       DADE_REQUIRE(value >= 0 && value <= 16, DADE_ERR_ARG, "shard exchanges not in [0, 16]");
       o.shard_exchanges = (int)value; break;

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(128 * NT, NT == 1 ? 3 : 2) k_l2_tc(const float
                                                   const float* __restrict__ Blo, const float* __restrict__ bn,
                                                   int nkc, float* __restrict__ out, int64_t m, int64_t n,
                                                   int64_t ldo, float* __restrict__ gmin, int64_t ldg, int passes,
-                                                  int gshift, int s1, const float* __restrict__ ahs, float bhs) {
+                                                  int gshift, int s1, const float* __restrict__ ahs, float bhs, int coop) {
   extern __shared__ __align__(1024) unsigned char sm[];
   // operand stages: 2 x 32 KB (3-pass: A_hi, A_lo, B_hi, B_lo) or s1 x 16 KB (1-pass: A_hi, B_hi)
   const int S = passes == 1 ? s1 : 2;
@@ -179,10 +179,30 @@ __global__ void __launch_bounds__(128 * NT, NT == 1 ? 3 : 2) k_l2_tc(const float
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (coop) {
+    // cooperative operand load (1-pass, every K chunk resident: S = nkc stages): all threads copy
+    // the tile's A and B blocks (already in the UMMA layout) with 16-byte cp.async — the LSU path
+    // instead of cp.async.bulk; the generic-proxy writes are fenced for the tensor core's reads
+    for (int kc = 0; kc < nkc; ++kc) {
+      unsigned char* st = sm + kc * SB;
+      const char* ga = reinterpret_cast<const char*>(Ahi + (tm * nkc + kc) * kSub);
+      const char* gb = reinterpret_cast<const char*>(Bhi + (tn * nkc + kc) * kSub);
+      for (int i = tid; i < kSub * 4 / 16; i += 128 * NT) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(st + i * 16)), "l"(ga + i * 16) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(st + kSub * 4 + i * 16)), "l"(gb + i * 16)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(128u * NT)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (coop) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -211,10 +231,11 @@ __global__ void __launch_bounds__(128 * NT, NT == 1 ? 3 : 2) k_l2_tc(const float
         bulk_g2s(st + 3 * kSub * 4, Blo + bo, kSub * 4, &full[s]);
       }
     };
-    for (int kc = 0; kc < S && kc < nkc; ++kc) load(kc);
+    if (!coop)
+      for (int kc = 0; kc < S && kc < nkc; ++kc) load(kc);
     for (int kc = 0; kc < nkc; ++kc) {
       const int s = kc % S;
-      mbar_wait(&full[s], (kc / S) & 1);
+      if (!coop) mbar_wait(&full[s], (kc / S) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       unsigned char* st = sm + s * SB;
 #pragma unroll
@@ -231,7 +252,7 @@ __global__ void __launch_bounds__(128 * NT, NT == 1 ? 3 : 2) k_l2_tc(const float
         }
       }
       mma_commit(&empty[s]);
-      if (kc + S < nkc) {
+      if (!coop && kc + S < nkc) {
         mbar_wait(&empty[s], (kc / S) & 1);  // MMAs reading this stage are done
         load(kc + S);
       }
@@ -359,14 +380,14 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
   if (m <= 0 || n <= 0) return;
   DADE_REQUIRE(!ahs || passes == 1, DADE_ERR_ARG, "l2_tc: fp16 operands are 1-pass only");
   // set on every launch: the attribute is per device
-  DADE_REQUIRE(nt == 1 || (nt == 2 && passes == 1), DADE_ERR_ARG, "l2_tc: 256-column tiles are 1-pass only");
+  DADE_REQUIRE(nt == 1 || nt == 3 || (nt == 2 && passes == 1), DADE_ERR_ARG, "l2_tc: 256-column tiles are 1-pass only");
   if (nt == 2) {  // N = 256 tiles: three 24-KB stages (two CTAs of eight warps per SM: TMEM 2 x 256 columns)
     const int s2 = 3;
     const size_t smem2 = (size_t)s2 * 3 * kSub * 4 + 128;
     DADE_CK(cudaFuncSetAttribute(k_l2_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     dim3 grid2((unsigned)(((n + kTM - 1) / kTM + 1) / 2), (unsigned)((m + kTM - 1) / kTM));
     k_l2_tc<2><<<grid2, 256, smem2, st>>>(Ahi, Alo, an, Bhi, Blo, bn, ahs ? fz_nkc(D, 1) : tc_nkc(D), out, m, n, ldo, gmin,
-                                          (n + (1 << gshift) - 1) >> gshift, passes, gshift, s2, ahs, bhs);
+                                          (n + (1 << gshift) - 1) >> gshift, passes, gshift, s2, ahs, bhs, 0);
     DADE_CK(cudaGetLastError());
     return;
   }
@@ -375,12 +396,14 @@ void launch_l2_tc(const float* Ahi, const float* Alo, const float* an, int64_t m
   // 64 KB allowed three), hiding more of each CTA's wait for its accumulator (C2 search 0.721 ->
   // 0.712-0.718 ms; 2 and 4 measured no better); the epilogue's transposition buffers
   // (4 x 32 x 33 floats) reuse the stage region, so >= 2 stages
-  const int s1 = 3;
+  const int nkc_ = ahs ? fz_nkc(D, 1) : tc_nkc(D);
+  const int coop = nt == 3 && passes == 1 && nkc_ <= 4;  // nt = 3: cooperative cp.async operand load (measurement)
+  const int s1 = coop ? nkc_ : 3;
   const size_t smem = (passes == 1 ? (size_t)s1 * (kStageBytes / 2) : 2 * (size_t)kStageBytes) + 128;
   dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)((m + kTM - 1) / kTM));
   // fp16 operands (Ahi / Bhi point at launch_split_h16's blocks): 32 halves per row per chunk
   k_l2_tc<1><<<grid, 128, smem, st>>>(Ahi, Alo, an, Bhi, Blo, bn, ahs ? fz_nkc(D, 1) : tc_nkc(D), out, m, n, ldo, gmin,
-                                   (n + (1 << gshift) - 1) >> gshift, passes, gshift, s1, ahs, bhs);
+                                   (n + (1 << gshift) - 1) >> gshift, passes, gshift, s1, ahs, bhs, coop);
   DADE_CK(cudaGetLastError());
 }
 

@@ -1,5 +1,5 @@
 """GPU parity of the d_hat writer on fp16 operands (gemm_tf32.cu k_l2_tc with kind::f16,
-DADE_OPT_DHAT_H16 = 1 on the d_hat path, DADE_OPT_KNN_PATH 1): probes bit-exact against the
+DADE_OPT_DHAT_H16 = 1 / 2 / 3 on the d_hat path, DADE_OPT_KNN_PATH 1): probes bit-exact against the
 oracle's fp64 definition (R20) on the bench's centroid-set shapes (C2 / C4 widths),
 ragged tiles, integer ties, k up to 64 and the fp16 edge cases (power-of-two scales far outside
 fp16's range, rows spanning its subnormal range, a zero operand row), and equal to the tf32
@@ -21,10 +21,10 @@ def torch_cuda():
     return torch
 
 
-H16 = 1   # 1: 128 x 128 tiles, 2: 128 x 256 tiles (set per test by the fixture below)
+H16 = 1   # 1: 128 x 128 tiles (default), 2: 128 x 256 tiles, 3: cooperative cp.async operand loads
 
 
-@pytest.fixture(autouse=True, params=[1, 2])
+@pytest.fixture(autouse=True, params=[1, 2, 3])
 def _tiles(request):
     global H16
     H16 = request.param

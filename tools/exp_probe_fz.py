@@ -51,7 +51,7 @@ def main():
         ix.set_option("fz_debug", a.debug)
     runs = [(int(p), None) for p in a.paths.split(",")]
     runs += [(4, tuple(int(v) for v in f.split(":"))) for f in a.fz.split(",") if f]
-    runs += [(1, ("dhat_h16", 1)), (1, ("dhat_h16", 2))] if a.h16 else []  # 2: 128 x 256 tiles
+    runs += [(1, ("dhat_h16", 1)), (1, ("dhat_h16", 2)), (1, ("dhat_h16", 3))] if a.h16 else []  # 2: 128 x 256 tiles
     runs += [(1, ("chunk_mb", int(v))) for v in a.chunk_mb.split(",") if v]
     runs += [(0, ("gmin_ratio", int(v))) for v in a.gmin_ratio.split(",") if v]
     runs += [(4, ("seed_stride", int(v))) for v in a.seed_stride.split(",") if v]
